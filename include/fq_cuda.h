@@ -1,0 +1,212 @@
+/*
+ * fq_cuda.h — the C-ABI boundary of the B200 FlexQuant decode engine.
+ *
+ * Everything the reference's hot path computes on the CPU is reachable through
+ * these entry points: plain pointers, sizes and opaque handles, no C++ or torch
+ * types, no exceptions.  Every function returns an fq_status; on failure the
+ * message is available from fq_last_error() (thread-local).  Status codes map
+ * one-to-one onto the reference's exception hierarchy
+ * (/root/reference/proj/include/flexquant/error.hpp:10-49) so the C++ wrapper
+ * (include/flexquant/*.hpp) can rethrow the matching flexquant::Error subclass.
+ *
+ * Pointer convention: arguments named *_host are host memory, *_dev are device
+ * (cudaMalloc / torch CUDA) memory.  All device work is ordered on the stream
+ * bound to the fq_ctx (fq_ctx_set_stream).
+ *
+ * Which reference interface each entry point replaces is cited next to it as
+ * file:line under /root/reference/proj.
+ */
+#ifndef FQ_CUDA_H
+#define FQ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FQ_ABI_VERSION 1
+
+typedef int32_t fq_status;
+enum {
+  FQ_OK = 0,
+  FQ_E_DIMENSION = 1, /* flexquant::DimensionError */
+  FQ_E_CONFIG = 2,    /* flexquant::ConfigError    */
+  FQ_E_INPUT = 3,     /* flexquant::InputError     */
+  FQ_E_STATE = 4,     /* flexquant::StateError     */
+  FQ_E_FORMAT = 5,    /* flexquant::FormatError    */
+  FQ_E_CAPACITY = 6,  /* flexquant::CapacityError  */
+  FQ_E_CUDA = 7       /* device / driver failure (no reference analogue) */
+};
+
+/* Precision rungs: include/flexquant/rung.hpp:13 (Rung{Fp,Int8,Int4}). */
+enum { FQ_RUNG_FP = 0, FQ_RUNG_INT8 = 1, FQ_RUNG_INT4 = 2 };
+/* Quantization modes: include/flexquant/quantizer.hpp:12 (QuantMode). */
+enum { FQ_MODE_ASYM = 0, FQ_MODE_SYM = 1 };
+/* Element types of activations / logits. */
+enum { FQ_DT_F32 = 0, FQ_DT_F16 = 1, FQ_DT_BF16 = 2 };
+/* Decoder block families. */
+enum {
+  FQ_ARCH_REFERENCE = 0, /* LayerNorm+bias, GELU w1/w2, learned positions, fp32 activations,
+                            double accumulation: the reference's own model (src/model.cpp:193-266) */
+  FQ_ARCH_LLAMA = 1      /* RMSNorm, SwiGLU gate/up/down, RoPE, no biases, bf16/fp16 activations,
+                            fp16 KV cache (BASELINE configs) */
+};
+/* GEMV numerics. */
+enum {
+  FQ_NUMERICS_FAST = 0, /* fp32 accumulation, per-group Σx zero-point folding (decode hot path) */
+  FQ_NUMERICS_EXACT = 1 /* dequantize-on-use in fp32 then double accumulation, as
+                           MultiPrecisionLayer::forward (src/model.cpp:77-98) + linear (src/tensor.cpp:83-101) */
+};
+
+typedef struct fq_ctx fq_ctx;
+typedef struct fq_layer fq_layer;
+typedef struct fq_model fq_model;
+
+/* Per-logits-row statistics, all in double (src/scheduler.cpp:13-49, src/engine.cpp:144-155). */
+typedef struct fq_row_stats {
+  double ppl_entropy;     /* exp(H), ppl_entropy()            scheduler.cpp:29-35 */
+  double entropy;         /* H = -sum p ln p                                      */
+  double p1;              /* largest softmax probability                          */
+  double p2;              /* second largest (duplicates count)                    */
+  double fault_tolerance; /* p1 - p2, fault_tolerance()       scheduler.cpp:37-49 */
+  float max_logit;        /* max over the float logits                            */
+  int32_t argmax;         /* argmax_token(): strict >, lowest index  engine.cpp:144-155 */
+} fq_row_stats;
+
+/* ---------------------------------------------------------------- context */
+const char* fq_last_error(void);
+int32_t fq_abi_version(void);
+fq_status fq_ctx_create(int32_t device, fq_ctx** out);
+fq_status fq_ctx_destroy(fq_ctx* ctx);
+/* Binds a cudaStream_t (passed as void*); NULL selects the context's own stream. */
+fq_status fq_ctx_set_stream(fq_ctx* ctx, void* stream);
+fq_status fq_ctx_get_stream(fq_ctx* ctx, void** stream_out);
+fq_status fq_ctx_synchronize(fq_ctx* ctx);
+/* Number of kernels this context has launched (evidence counter for the bench). */
+fq_status fq_ctx_launch_count(fq_ctx* ctx, int64_t* out);
+
+/* ------------------------------------------------------ weight store (a1-a4, a6) */
+/* One linear layer [out_features x in_features] with resident per-precision copies.
+ * group_size: quantization group along in_features (0 or >= in_features = per row,
+ * the reference's granularity, src/quantizer.cpp:128-185).  Replaces
+ * MultiPrecisionLayer (include/flexquant/model.hpp:45-92). */
+fq_status fq_layer_create(fq_ctx* ctx, int64_t out_features, int64_t in_features,
+                          int64_t group_size, fq_layer** out);
+fq_status fq_layer_destroy(fq_layer* layer);
+/* Uploads one quantized rung from the canonical QuantizedTensor layout
+ * (include/flexquant/quantizer.hpp:24-44 applied to the [N*ceil(K/G), G] group view):
+ * payload = packed codes of the row-major stream (4-bit: low nibble = even index),
+ * scale/zero_point = one per group in (row, group) order. */
+fq_status fq_layer_upload_quantized(fq_layer* layer, int32_t rung, int32_t mode,
+                                    const uint8_t* payload_host, int64_t payload_bytes,
+                                    const float* scale_host, const int32_t* zero_point_host,
+                                    int64_t n_groups);
+/* Reads a rung back in the canonical layout (round trip of the device layout). */
+fq_status fq_layer_download_quantized(const fq_layer* layer, int32_t rung, uint8_t* payload_host,
+                                      float* scale_host, int32_t* zero_point_host);
+/* Full-precision rung (fp32 [N,K]) and optional bias [N]. */
+fq_status fq_layer_upload_fp(fq_layer* layer, const float* weight_host);
+fq_status fq_layer_upload_bias(fq_layer* layer, const float* bias_host);
+/* Device-side RTN quantizer (K9): quantizes fp32 weights already on the device with the
+ * reference rules (src/quantizer.cpp:111-189, round-half-even in double). */
+fq_status fq_layer_quantize_device(fq_layer* layer, int32_t rung, int32_t mode, const float* weight_dev);
+fq_status fq_layer_has(const fq_layer* layer, int32_t rung, int32_t* out);
+fq_status fq_layer_shape(const fq_layer* layer, int64_t* out_features, int64_t* in_features,
+                         int64_t* group_size);
+/* Algorithmic bytes one B-row GEMV over `rung` touches (payload + 5 B/group + activations). */
+fq_status fq_layer_bytes(const fq_layer* layer, int32_t rung, int64_t batch, int64_t* out);
+
+/* y[B,N] = x[B,K] * dequant(W_rung)^T (+ bias).  Replaces MultiPrecisionLayer::forward
+ * (src/model.cpp:77-98): dequantize (src/quantizer.cpp:205-219) + linear (src/tensor.cpp:83-101).
+ * x_dev / y_dev are device buffers of the given dtypes. */
+fq_status fq_gemv(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int64_t batch,
+                  const void* x_dev, int32_t x_dtype, void* y_dev, int32_t y_dtype,
+                  int32_t numerics);
+
+/* ------------------------------------------------------- statistics (a10, a11, a18) */
+/* One fq_row_stats per logits row (fp32 [rows, vocab] on device); stats_dev on device. */
+fq_status fq_softmax_stats(fq_ctx* ctx, const float* logits_dev, int64_t rows, int64_t vocab,
+                           fq_row_stats* stats_dev);
+/* Per row r: kl[r] = KL(softmax(lq_r) || softmax(lp_r)) = sum p_q ln(p_q/p_p),
+ * entropy[r] = H(softmax(lq_r)).  Logit-mode calibration (BASELINE config 4); the
+ * divergence follows kl_divergence (src/analyzer.cpp:65-79). Logits fp32 or bf16. */
+fq_status fq_kl_rows(fq_ctx* ctx, const void* logits_q_dev, const void* logits_p_dev, int32_t dtype,
+                     int64_t rows, int64_t vocab, double* kl_dev, double* entropy_dev);
+/* Weight-histogram KL of one layer's rung against its fp weights (src/analyzer.cpp:83-94:
+ * uniform_edges over [min,max], weight_histogram with +1e-10 smoothing, kl_divergence). */
+fq_status fq_hist_kl(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int32_t bins, double* kl_host);
+
+/* Deterministic N(0, std) generator keyed by (seed, stream_id, element index); the same
+ * values are produced by the host generator in the C++ library and the oracle. */
+fq_status fq_fill_normal(fq_ctx* ctx, float* dst_dev, int64_t n, uint64_t seed, uint64_t stream_id,
+                         float std);
+
+/* ------------------------------------------------------------ device decoder (a7-a9, a14) */
+typedef struct fq_model_config {
+  int32_t arch;          /* FQ_ARCH_*                                   */
+  int32_t act_dtype;     /* llama: FQ_DT_BF16 / FQ_DT_F16; reference: FQ_DT_F32 */
+  int64_t vocab_size;
+  int64_t d_model;
+  int64_t n_heads;
+  int64_t head_dim;
+  int64_t n_layers;
+  int64_t ffn_dim;
+  int64_t max_seq_len;
+  int32_t tie_embeddings; /* reference arch only */
+  int32_t max_batch;      /* resident sequence slots (KV caches, precision-table rows) */
+  int64_t group_size;     /* quantization group (0 = per row) */
+  float norm_eps;         /* LayerNorm / RMSNorm epsilon */
+  float rope_theta;       /* llama only */
+} fq_model_config;
+
+fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** out);
+fq_status fq_model_destroy(fq_model* model);
+/* Switchable linears in the reference's accounting order (src/model.cpp:304-330):
+ * reference arch: blocks.i.attn.{wq,wk,wv,wo}, blocks.i.ffn.{w1,w2}, head;
+ * llama arch:     blocks.i.attn.{wq,wk,wv,wo}, blocks.i.ffn.{w_gate,w_up,w_down}, head. */
+fq_status fq_model_num_linears(const fq_model* model, int32_t* out);
+fq_status fq_model_linear_id(const fq_model* model, int32_t index, char* buf, int32_t buflen);
+fq_status fq_model_linear_index(const fq_model* model, const char* layer_id, int32_t* out);
+fq_status fq_model_linear(fq_model* model, int32_t index, fq_layer** out); /* borrowed */
+/* Non-switchable parameters by name: tok_emb, pos_emb, blocks.i.ln1.gamma/beta,
+ * blocks.i.ln2.gamma/beta (reference), blocks.i.attn_norm / blocks.i.ffn_norm (llama),
+ * final_norm(.gamma/.beta).  fp32 host data. */
+fq_status fq_model_set_param(fq_model* model, const char* name, const float* host, int64_t numel);
+/* Fills every parameter / rung from the deterministic generator on the device (bench). */
+fq_status fq_model_init_random(fq_model* model, uint64_t seed, float std);
+/* Precision table: rung of (sequence slot, linear).  A pointer-of-record write, no payload
+ * touched (Model::set_precision, src/model.cpp:268-278).  Takes effect at the next step. */
+fq_status fq_model_set_rung(fq_model* model, int32_t slot, int32_t linear_index, int32_t rung);
+fq_status fq_model_get_rung(const fq_model* model, int32_t slot, int32_t linear_index, int32_t* out);
+fq_status fq_model_set_all_rungs(fq_model* model, int32_t slot, int32_t rung);
+/* KV cache of a slot (KvCache, src/model.cpp:142-171). */
+fq_status fq_model_reset_slot(fq_model* model, int32_t slot);
+fq_status fq_model_slot_length(const fq_model* model, int32_t slot, int64_t* out);
+/* Prefill n prompt tokens into an empty slot (Model::forward_prefill, src/model.cpp:239-255).
+ * logits_dev: optional device buffer [n, V] fp32 receiving every row; stats_host: n rows. */
+fq_status fq_model_prefill(fq_model* model, int32_t slot, const int32_t* tokens_host, int64_t n,
+                           float* logits_dev, fq_row_stats* stats_host);
+/* One decode step for `batch` slots (Model::forward_decode, src/model.cpp:257-266, batched):
+ * appends one position per slot and writes per-row stats to stats_host.  The step is
+ * replayed from a captured CUDA graph. logits_dev optional [batch, V] copy-out. */
+fq_status fq_model_decode(fq_model* model, int32_t batch, const int32_t* slots_host,
+                          const int32_t* tokens_host, float* logits_dev, fq_row_stats* stats_host);
+/* Device pointer of the model's internal logits buffer [max_batch, V] (valid after a step). */
+fq_status fq_model_logits(fq_model* model, float** logits_dev);
+/* Algorithmic bytes of one decode step for `batch` slots at their current rungs/lengths. */
+fq_status fq_model_step_bytes(const fq_model* model, int32_t batch, const int32_t* slots_host,
+                              int64_t* weight_bytes, int64_t* kv_bytes);
+/* Logit-mode calibration (BASELINE config 4): teacher-forced prefill of `n_seqs` token rows
+ * of length `len`, all linears at `base_rung`, then for every block b the block's linears at
+ * `flip_rung`; kl_host[b] = mean KL(softmax(l_flip) || softmax(l_base)), entropy_host[b] =
+ * mean entropy of the flipped distribution. */
+fq_status fq_model_calibrate_logit_kl(fq_model* model, const int32_t* tokens_host, int64_t n_seqs,
+                                      int64_t len, int32_t base_rung, int32_t flip_rung,
+                                      double* kl_host, double* entropy_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FQ_CUDA_H */

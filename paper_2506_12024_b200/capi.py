@@ -1,0 +1,299 @@
+"""ctypes binding of the C-ABI boundary (include/fq_cuda.h).
+
+This is how Python (tests, bench) reaches the CUDA engine; it exercises exactly the entry
+points a reference maintainer would bind.  There is no CPU fallback: if the
+extension is missing or no B200 is visible, ``load()`` / ``Context()`` raise.
+
+Status codes are mapped onto the reference's exception hierarchy
+(/root/reference/proj/include/flexquant/error.hpp:10-49).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libfq_cuda.so")
+
+RUNG_FP, RUNG_INT8, RUNG_INT4 = 0, 1, 2
+MODE_ASYM, MODE_SYM = 0, 1
+DT_F32, DT_F16, DT_BF16 = 0, 1, 2
+ARCH_REFERENCE, ARCH_LLAMA = 0, 1
+NUMERICS_FAST, NUMERICS_EXACT = 0, 1
+
+ABI_FUNCTIONS = [
+    "fq_last_error", "fq_abi_version", "fq_ctx_create", "fq_ctx_destroy", "fq_ctx_set_stream", "fq_ctx_get_stream",
+    "fq_ctx_synchronize", "fq_ctx_launch_count", "fq_layer_create", "fq_layer_destroy", "fq_layer_upload_quantized",
+    "fq_layer_download_quantized", "fq_layer_upload_fp", "fq_layer_upload_bias", "fq_layer_quantize_device",
+    "fq_layer_has", "fq_layer_shape", "fq_layer_bytes", "fq_gemv", "fq_softmax_stats", "fq_kl_rows", "fq_hist_kl",
+    "fq_fill_normal", "fq_model_create", "fq_model_destroy", "fq_model_num_linears", "fq_model_linear_id",
+    "fq_model_linear_index", "fq_model_linear", "fq_model_set_param", "fq_model_init_random", "fq_model_set_rung",
+    "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
+    "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
+]
+
+
+class Error(RuntimeError):
+    """flexquant::Error"""
+
+
+class DimensionError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class InputError(Error):
+    pass
+
+
+class StateError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class CapacityError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+_ERRORS = {1: DimensionError, 2: ConfigError, 3: InputError, 4: StateError, 5: FormatError, 6: CapacityError,
+           7: CudaError}
+
+
+class RowStats(C.Structure):
+    _fields_ = [("ppl_entropy", C.c_double), ("entropy", C.c_double), ("p1", C.c_double), ("p2", C.c_double),
+                ("fault_tolerance", C.c_double), ("max_logit", C.c_float), ("argmax", C.c_int32)]
+
+
+ROW_STATS_DTYPE = np.dtype([("ppl_entropy", np.float64), ("entropy", np.float64), ("p1", np.float64),
+                            ("p2", np.float64), ("fault_tolerance", np.float64), ("max_logit", np.float32),
+                            ("argmax", np.int32)])
+assert ROW_STATS_DTYPE.itemsize == C.sizeof(RowStats)
+
+
+class ModelConfig(C.Structure):
+    _fields_ = [("arch", C.c_int32), ("act_dtype", C.c_int32), ("vocab_size", C.c_int64), ("d_model", C.c_int64),
+                ("n_heads", C.c_int64), ("head_dim", C.c_int64), ("n_layers", C.c_int64), ("ffn_dim", C.c_int64),
+                ("max_seq_len", C.c_int64), ("tie_embeddings", C.c_int32), ("max_batch", C.c_int32),
+                ("group_size", C.c_int64), ("norm_eps", C.c_float), ("rope_theta", C.c_float)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Loads libfq_cuda.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"CUDA extension {path} is not built; run `make` or __graft_entry__.build()")
+    L = C.CDLL(path)
+    v = C.c_void_p
+    i32, i64, u64 = C.c_int32, C.c_int64, C.c_uint64
+    L.fq_last_error.restype = C.c_char_p
+    L.fq_abi_version.restype = i32
+    sig = {
+        "fq_ctx_create": [i32, C.POINTER(v)],
+        "fq_ctx_destroy": [v],
+        "fq_ctx_set_stream": [v, v],
+        "fq_ctx_get_stream": [v, C.POINTER(v)],
+        "fq_ctx_synchronize": [v],
+        "fq_ctx_launch_count": [v, C.POINTER(i64)],
+        "fq_layer_create": [v, i64, i64, i64, C.POINTER(v)],
+        "fq_layer_destroy": [v],
+        "fq_layer_upload_quantized": [v, i32, i32, v, i64, v, v, i64],
+        "fq_layer_download_quantized": [v, i32, v, v, v],
+        "fq_layer_upload_fp": [v, v],
+        "fq_layer_upload_bias": [v, v],
+        "fq_layer_quantize_device": [v, i32, i32, v],
+        "fq_layer_has": [v, i32, C.POINTER(i32)],
+        "fq_layer_shape": [v, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],
+        "fq_layer_bytes": [v, i32, i64, C.POINTER(i64)],
+        "fq_gemv": [v, v, i32, i64, v, i32, v, i32, i32],
+        "fq_softmax_stats": [v, v, i64, i64, v],
+        "fq_kl_rows": [v, v, v, i32, i64, i64, v, v],
+        "fq_hist_kl": [v, v, i32, i32, C.POINTER(C.c_double)],
+        "fq_fill_normal": [v, v, i64, u64, u64, C.c_float],
+        "fq_model_create": [v, C.POINTER(ModelConfig), C.POINTER(v)],
+        "fq_model_destroy": [v],
+        "fq_model_num_linears": [v, C.POINTER(i32)],
+        "fq_model_linear_id": [v, i32, C.c_char_p, i32],
+        "fq_model_linear_index": [v, C.c_char_p, C.POINTER(i32)],
+        "fq_model_linear": [v, i32, C.POINTER(v)],
+        "fq_model_set_param": [v, C.c_char_p, v, i64],
+        "fq_model_init_random": [v, u64, C.c_float],
+        "fq_model_set_rung": [v, i32, i32, i32],
+        "fq_model_get_rung": [v, i32, i32, C.POINTER(i32)],
+        "fq_model_set_all_rungs": [v, i32, i32],
+        "fq_model_reset_slot": [v, i32],
+        "fq_model_slot_length": [v, i32, C.POINTER(i64)],
+        "fq_model_prefill": [v, i32, v, i64, v, v],
+        "fq_model_decode": [v, i32, v, v, v, v],
+        "fq_model_logits": [v, C.POINTER(v)],
+        "fq_model_step_bytes": [v, i32, v, C.POINTER(i64), C.POINTER(i64)],
+        "fq_model_calibrate_logit_kl": [v, v, i64, i64, i32, i32, v, v],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = i32
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = load().fq_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, Error)(msg)
+
+
+def _ptr(a) -> int | None:
+    """Raw pointer of a numpy array or a torch tensor (host or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if isinstance(a, int):
+        return a
+    raise TypeError(f"cannot take a pointer of {type(a)}")
+
+
+class Context:
+    """fq_ctx: one device + one stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        L = load()
+        h = C.c_void_p()
+        check(L.fq_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.L = L
+        if stream is not None:
+            self.set_stream(stream)
+
+    def set_stream(self, stream) -> None:
+        raw = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        check(self.L.fq_ctx_set_stream(self.h, C.c_void_p(raw)))
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        check(self.L.fq_ctx_get_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self) -> None:
+        check(self.L.fq_ctx_synchronize(self.h))
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        check(self.L.fq_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def close(self) -> None:
+        if self.h:
+            check(self.L.fq_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # stateless kernels -------------------------------------------------------
+    def gemv(self, layer: "Layer", rung: int, batch: int, x, x_dtype: int, y, y_dtype: int,
+             numerics: int = NUMERICS_FAST) -> None:
+        check(self.L.fq_gemv(self.h, layer.h, rung, batch, _ptr(x), x_dtype, _ptr(y), y_dtype, numerics))
+
+    def softmax_stats(self, logits, rows: int, vocab: int, stats_dev) -> None:
+        check(self.L.fq_softmax_stats(self.h, _ptr(logits), rows, vocab, _ptr(stats_dev)))
+
+    def kl_rows(self, lq, lp, dtype: int, rows: int, vocab: int, kl_dev, ent_dev=None) -> None:
+        check(self.L.fq_kl_rows(self.h, _ptr(lq), _ptr(lp), dtype, rows, vocab, _ptr(kl_dev), _ptr(ent_dev)))
+
+    def fill_normal(self, dst_dev, n: int, seed: int, stream_id: int, std: float) -> None:
+        check(self.L.fq_fill_normal(self.h, _ptr(dst_dev), n, seed, stream_id, std))
+
+
+class Layer:
+    """fq_layer: resident per-precision copies of one linear."""
+
+    def __init__(self, ctx: Context, out_features: int, in_features: int, group_size: int = 128, handle=None):
+        self.ctx = ctx
+        self.L = ctx.L
+        self.borrowed = handle is not None
+        if handle is None:
+            h = C.c_void_p()
+            check(self.L.fq_layer_create(ctx.h, out_features, in_features, group_size, C.byref(h)))
+            self.h = h
+        else:
+            self.h = handle
+        n, k, g = C.c_int64(), C.c_int64(), C.c_int64()
+        check(self.L.fq_layer_shape(self.h, C.byref(n), C.byref(k), C.byref(g)))
+        self.N, self.K, self.G = n.value, k.value, g.value
+        self.ng = (self.K + self.G - 1) // self.G
+
+    def upload_quantized(self, rung: int, payload: np.ndarray, scale: np.ndarray, zp: np.ndarray,
+                         mode: int = MODE_ASYM) -> None:
+        payload = np.ascontiguousarray(payload, np.uint8)
+        scale = np.ascontiguousarray(scale, np.float32).ravel()
+        zp = np.ascontiguousarray(zp, np.int32).ravel()
+        check(self.L.fq_layer_upload_quantized(self.h, rung, mode, _ptr(payload), payload.size, _ptr(scale),
+                                               _ptr(zp), scale.size))
+
+    def download_quantized(self, rung: int):
+        bits = 8 if rung == RUNG_INT8 else 4
+        payload = np.zeros((self.N * self.K * bits + 7) // 8, np.uint8)
+        scale = np.zeros(self.N * self.ng, np.float32)
+        zp = np.zeros(self.N * self.ng, np.int32)
+        check(self.L.fq_layer_download_quantized(self.h, rung, _ptr(payload), _ptr(scale), _ptr(zp)))
+        return payload, scale.reshape(self.N, self.ng), zp.reshape(self.N, self.ng)
+
+    def upload_fp(self, w: np.ndarray) -> None:
+        w = np.ascontiguousarray(w, np.float32)
+        check(self.L.fq_layer_upload_fp(self.h, _ptr(w)))
+
+    def upload_bias(self, b: np.ndarray) -> None:
+        b = np.ascontiguousarray(b, np.float32)
+        check(self.L.fq_layer_upload_bias(self.h, _ptr(b)))
+
+    def quantize_device(self, rung: int, w_dev, mode: int = MODE_ASYM) -> None:
+        check(self.L.fq_layer_quantize_device(self.h, rung, mode, _ptr(w_dev)))
+
+    def has(self, rung: int) -> bool:
+        o = C.c_int32()
+        check(self.L.fq_layer_has(self.h, rung, C.byref(o)))
+        return bool(o.value)
+
+    def algorithmic_bytes(self, rung: int, batch: int) -> int:
+        o = C.c_int64()
+        check(self.L.fq_layer_bytes(self.h, rung, batch, C.byref(o)))
+        return o.value
+
+    def hist_kl(self, rung: int, bins: int) -> float:
+        o = C.c_double()
+        check(self.L.fq_hist_kl(self.ctx.h, self.h, rung, bins, C.byref(o)))
+        return o.value
+
+    def close(self) -> None:
+        if self.h and not self.borrowed:
+            check(self.L.fq_layer_destroy(self.h))
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,162 @@
+// Internal declarations shared by the CUDA translation units of libfq_cuda.so.
+// Nothing here crosses the C-ABI; see include/fq_cuda.h for the boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "fq_cuda.h"
+
+namespace fqc {
+
+// Error carried from the implementation to the ABI wrapper (status + message).
+struct Failure {
+  fq_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(fq_status code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+void set_last_error(const std::string& msg);
+
+#define FQ_CUDA(call) ::fqc::check_cuda((call), #call)
+
+// Runs `body` and converts a Failure (or any exception) into a status + fq_last_error().
+template <class F>
+fq_status guarded(F&& body) {
+  try {
+    body();
+    return FQ_OK;
+  } catch (const Failure& f) {
+    set_last_error(f.msg);
+    return f.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return FQ_E_CUDA;
+  }
+}
+
+}  // namespace fqc
+
+// ------------------------------------------------------------------ context
+struct fq_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  // scratch: grows on demand, never shrinks
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* ensure_scratch(size_t bytes);
+};
+
+// One resident precision copy of a linear layer.
+struct fq_rung_store {
+  bool present = false;
+  int bits = 8;            // 8 or 4
+  int mode = FQ_MODE_ASYM;
+  uint8_t* payload = nullptr;   // canonical row-major packed codes (device)
+  int64_t payload_bytes = 0;
+  float* scale = nullptr;       // [N, ng]
+  uint8_t* zp8 = nullptr;       // [N, ng] effective zero point - zp_base (fast path)
+  int32_t* zp32 = nullptr;      // [N, ng] effective zero point (z + stored offset), always kept
+  int32_t zp_base = 0;
+  bool zp_fits_u8 = false;      // fast kernel usable
+};
+
+struct fq_layer {
+  fq_ctx* ctx = nullptr;
+  int64_t N = 0, K = 0, G = 0;  // out, in, group (G == K for per-row)
+  int64_t ng = 0;               // groups per row = ceil(K / G)
+  float* fp = nullptr;          // fp32 [N, K] (optional)
+  float* bias = nullptr;        // fp32 [N] (optional)
+  fq_rung_store r8, r4;
+  bool borrowed = false;        // owned by a model
+
+  const fq_rung_store& store(int rung) const { return rung == FQ_RUNG_INT4 ? r4 : r8; }
+  fq_rung_store& store(int rung) { return rung == FQ_RUNG_INT4 ? r4 : r8; }
+  bool has(int rung) const {
+    if (rung == FQ_RUNG_FP) return fp != nullptr;
+    if (rung == FQ_RUNG_INT8) return r8.present;
+    if (rung == FQ_RUNG_INT4) return r4.present;
+    return false;
+  }
+};
+
+namespace fqc {
+
+// ---------------------------------------------------------------- GEMV launch API
+// A multi-matrix GEMV: up to 3 matrices with identical [N, K] shapes sharing one input
+// (QKV, gate/up).  Each CTA owns the same row range of every matrix.
+enum Epilogue : int {
+  EPI_STORE = 0,     // y[b][m*N + row] = acc (+bias), dtype y_dtype
+  EPI_RESIDUAL = 1,  // resid[b][row] += acc (fp32), per-CTA sum of squares -> partials
+  EPI_SWIGLU = 2,    // y[b][row] = silu(acc_gate) * acc_up   (2 matrices)
+  EPI_SPLIT3 = 3     // y_m[b][row] = acc_m for 3 matrices (q, k, v outputs)
+};
+
+struct GemvMatrix {
+  const fq_layer* layer = nullptr;
+  const uint8_t* rung_table = nullptr;  // device: rung per batch row (stride below) or null
+  int64_t rung_stride = 0;              // bytes between batch rows in rung_table
+  int rung = FQ_RUNG_INT8;              // used when rung_table == null
+  void* y = nullptr;                    // per-matrix output (EPI_SPLIT3)
+};
+
+struct GemvLaunch {
+  GemvMatrix mat[3];
+  int nmat = 1;
+  int64_t batch = 1;
+  // input activations [batch, K]
+  const void* x = nullptr;
+  int x_dtype = FQ_DT_F32;
+  int64_t x_stride = 0;  // elements
+  // optional fused RMSNorm prologue: x is the fp32 residual; h = round_act(x*rstd*gain)
+  const float* norm_gain = nullptr;
+  const float* norm_partials = nullptr;  // [batch, n_partials] sums of squares
+  int n_partials = 0;
+  float norm_eps = 1e-5f;
+  int act_dtype = FQ_DT_BF16;  // rounding applied to the normalized activations
+  // output
+  int epi = EPI_STORE;
+  void* y = nullptr;
+  int y_dtype = FQ_DT_F32;
+  int64_t y_stride = 0;        // elements between batch rows of y
+  float* resid = nullptr;      // EPI_RESIDUAL
+  int64_t resid_stride = 0;
+  float* out_partials = nullptr;  // EPI_RESIDUAL: [batch, out_n_partials]
+  int out_n_partials = 0;
+  bool pdl = false;            // launch with programmatic stream serialization
+};
+
+bool gemv_fast_supported(const fq_layer* L, int rung);
+// Returns the grid size used (the residual epilogue writes one sum-of-squares partial per CTA;
+// out_n_partials must be >= #SM x 4).
+int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);
+void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
+                       int x_dtype, void* y, int y_dtype);
+
+// statistics
+void launch_softmax_stats(fq_ctx* ctx, const float* logits, int64_t rows, int64_t vocab,
+                          int64_t row_stride, fq_row_stats* out);
+void launch_kl_rows(fq_ctx* ctx, const void* lq, const void* lp, int dtype, int64_t rows,
+                    int64_t vocab, double* kl, double* ent);
+double hist_kl(fq_ctx* ctx, const fq_layer* L, int rung, int bins);
+
+// quantization / generation
+void quantize_device(fq_ctx* ctx, fq_layer* L, int rung, int mode, const float* w_dev);
+void fill_normal(fq_ctx* ctx, float* dst, int64_t n, uint64_t seed, uint64_t stream, float std);
+void finalize_rung_meta(fq_ctx* ctx, fq_layer* L, int rung);  // zp32 -> zp8/zp_base
+
+// allocation helpers
+void* dmalloc(size_t bytes);
+void dfree(void* p);
+
+inline int ceil_div_i(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace fqc
