@@ -24,6 +24,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 namespace fqc {
 namespace {
@@ -465,9 +467,22 @@ int pick_warps(int nsteps, int* sw_out) {
 template <int SW, int BB>
 int launch_fast_t(fq_ctx* ctx, const DevArgs& d, int W, size_t smem, bool pdl) {
   auto kern = gemv_fast_kernel<SW, BB>;
-  if (smem > 48 * 1024) FQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  // occupancy is a pure function of (kernel, block, smem): cache it, host queries cost microseconds
+  static std::map<std::pair<int, size_t>, int> occ_cache;
+  static std::mutex occ_mu;
   int per_sm = 0;
-  FQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem));
+  {
+    std::lock_guard<std::mutex> lk(occ_mu);
+    auto it = occ_cache.find({W, smem});
+    if (it == occ_cache.end()) {
+      if (smem > 48 * 1024)
+        FQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      FQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem));
+      occ_cache[{W, smem}] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
   per_sm = std::max(1, std::min(per_sm, 4));
   const int grid = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(ctx->num_sms) * per_sm, d.N));
   if (d.epi == EPI_RESIDUAL && d.out_n_partials < grid) fail(FQ_E_STATE, "gemv: residual partial buffer too small");

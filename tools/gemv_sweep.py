@@ -1,9 +1,15 @@
 """BASELINE config 2: quantized-GEMV sweep at Llama-7B linear shapes.
 
 For every (K x N) shape, bit-width and batch: device-generated N(0,0.02) weights quantized
-per-group-128 on the device (K9), fp16 N(0,1) activations, one GEMV timed with CUDA events
-on the launching stream; L2 is flushed (256 MiB write) before every timed launch.  Prints one
-JSON line per case with algorithmic bytes / time and the fraction of measured HBM peak.
+per-group-128 on the device (K9), fp16 N(0,1) activations.  Two timings, both with CUDA events
+on the launching stream:
+
+* ``cold``  — one launch after a 256 MiB L2 flush (median of --iters);
+* ``chain`` — R distinct copies of the layer (> 2x L2 in total, so every launch streams from
+  HBM) launched back to back inside one CUDA graph, as the decode step issues them; per-launch
+  time = graph time / R.
+
+Prints one JSON line per case: algorithmic bytes / time and the fraction of measured HBM peak.
 """
 import argparse
 import json
@@ -31,45 +37,73 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--batches", default="1,4,16")
     ap.add_argument("--bits", default="8,4")
+    ap.add_argument("--shapes", default="all")
     args = ap.parse_args()
     hbm, kind = peak()
     ctx = capi.Context(0)
     stream = torch.cuda.Stream()
     ctx.set_stream(stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for K, N in SHAPES:
+    shapes = SHAPES if args.shapes == "all" else [SHAPES[int(i)] for i in args.shapes.split(",")]
+    for K, N in shapes:
         w = torch.empty(N * K, dtype=torch.float32, device="cuda")
         ctx.fill_normal(w, N * K, 0, K * 100000 + N, 0.02)
-        L = capi.Layer(ctx, N, K, 128)
-        L.quantize_device(capi.RUNG_INT8, w)
-        L.quantize_device(capi.RUNG_INT4, w)
+        per = N * K * 1.5
+        R = max(4, int(400e6 // per) + 1)
+        layers = []
+        for r in range(R):
+            L = capi.Layer(ctx, N, K, 128)
+            L.quantize_device(capi.RUNG_INT8, w)
+            L.quantize_device(capi.RUNG_INT4, w)
+            layers.append(L)
         del w
         for bits in [int(b) for b in args.bits.split(",")]:
             rung = capi.RUNG_INT8 if bits == 8 else capi.RUNG_INT4
             for B in [int(b) for b in args.batches.split(",")]:
                 x = torch.randn(B, K, device="cuda").half()
                 y = torch.empty(B, N, device="cuda", dtype=torch.float32)
+                L0 = layers[0]
                 with torch.cuda.stream(stream):
                     for _ in range(3):
-                        ctx.gemv(L, rung, B, x, capi.DT_F16, y, capi.DT_F32)
+                        ctx.gemv(L0, rung, B, x, capi.DT_F16, y, capi.DT_F32)
                     times = []
                     for _ in range(args.iters):
                         flush.fill_(1)
                         e0 = torch.cuda.Event(enable_timing=True)
                         e1 = torch.cuda.Event(enable_timing=True)
                         e0.record(stream)
-                        ctx.gemv(L, rung, B, x, capi.DT_F16, y, capi.DT_F32)
+                        ctx.gemv(L0, rung, B, x, capi.DT_F16, y, capi.DT_F32)
                         e1.record(stream)
                         e1.synchronize()
                         times.append(e0.elapsed_time(e1) * 1e-3)
-                times.sort()
-                t = times[len(times) // 2]
-                byts = L.algorithmic_bytes(rung, B)
-                gbs = byts / t / 1e9
-                print(json.dumps({"K": K, "N": N, "bits": bits, "B": B, "us": round(t * 1e6, 2),
-                                  "bytes": byts, "GBps": round(gbs, 1), "frac": round(gbs / hbm, 3),
-                                  "peak": hbm, "peak_kind": kind}), flush=True)
-        L.close()
+                    times.sort()
+                    t_cold = times[len(times) // 2]
+                    # chain of distinct layers inside one graph
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        for L in layers:
+                            ctx.gemv(L, rung, B, x, capi.DT_F16, y, capi.DT_F32)
+                    for _ in range(3):
+                        g.replay()
+                    ch = []
+                    for _ in range(max(3, args.iters // 4)):
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e0.record(stream)
+                        g.replay()
+                        e1.record(stream)
+                        e1.synchronize()
+                        ch.append(e0.elapsed_time(e1) * 1e-3 / len(layers))
+                    ch.sort()
+                    t_chain = ch[len(ch) // 2]
+                byts = L0.algorithmic_bytes(rung, B)
+                print(json.dumps({"K": K, "N": N, "bits": bits, "B": B, "bytes": byts,
+                                  "cold_us": round(t_cold * 1e6, 2), "cold_GBps": round(byts / t_cold / 1e9, 1),
+                                  "chain_us": round(t_chain * 1e6, 2), "chain_GBps": round(byts / t_chain / 1e9, 1),
+                                  "chain_frac": round(byts / t_chain / 1e9 / hbm, 3), "peak": hbm,
+                                  "peak_kind": kind}), flush=True)
+        for L in layers:
+            L.close()
 
 
 if __name__ == "__main__":
