@@ -136,6 +136,8 @@ fq_status fq_layer_create(fq_ctx* ctx, int64_t out_features, int64_t in_features
     L->K = in_features;
     L->G = (group_size == 0 || group_size >= in_features) ? in_features : group_size;
     L->ng = (L->K + L->G - 1) / L->G;
+    L->ng_pad = (L->ng + 3) / 4 * 4;
+    L->zp_pad = (L->ng + 15) / 16 * 16;
     *out = L;
   });
 }
@@ -172,7 +174,7 @@ fq_status fq_layer_upload_quantized(fq_layer* L, int32_t rung, int32_t mode, con
     if (st.present && st.bits != bits) free_store(st);
     if (!st.present) {
       st.payload = static_cast<uint8_t*>(dmalloc(payload_bytes));
-      st.scale = static_cast<float*>(dmalloc(sizeof(float) * n_groups));
+      st.scale = static_cast<float*>(dmalloc(sizeof(float) * L->N * L->ng_pad));
       st.zp32 = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * n_groups));
     }
     st.bits = bits;
@@ -180,7 +182,11 @@ fq_status fq_layer_upload_quantized(fq_layer* L, int32_t rung, int32_t mode, con
     st.payload_bytes = payload_bytes;
     cudaStream_t s = L->ctx->stream;
     FQ_CUDA(cudaMemcpyAsync(st.payload, payload_host, payload_bytes, cudaMemcpyHostToDevice, s));
-    FQ_CUDA(cudaMemcpyAsync(st.scale, scale_host, sizeof(float) * n_groups, cudaMemcpyHostToDevice, s));
+    // device layout: scale rows padded to ng_pad (a fixed, invertible re-layout)
+    std::vector<float> spad(static_cast<size_t>(L->N * L->ng_pad), 0.0f);
+    for (int64_t r = 0; r < L->N; ++r)
+      std::memcpy(&spad[r * L->ng_pad], scale_host + r * L->ng, sizeof(float) * L->ng);
+    FQ_CUDA(cudaMemcpyAsync(st.scale, spad.data(), sizeof(float) * spad.size(), cudaMemcpyHostToDevice, s));
     // effective zero point = z + stored offset (symmetric codes are stored offset by 2^(n-1)-1)
     std::vector<int32_t> zeff(zero_point_host, zero_point_host + n_groups);
     const int32_t off = mode == FQ_MODE_SYM ? (1 << (bits - 1)) - 1 : 0;
@@ -202,11 +208,14 @@ fq_status fq_layer_download_quantized(const fq_layer* L, int32_t rung, uint8_t* 
     const int64_t ngr = L->N * L->ng;
     cudaStream_t s = L->ctx->stream;
     if (payload_host) FQ_CUDA(cudaMemcpyAsync(payload_host, st.payload, st.payload_bytes, cudaMemcpyDeviceToHost, s));
-    if (scale_host) FQ_CUDA(cudaMemcpyAsync(scale_host, st.scale, sizeof(float) * ngr, cudaMemcpyDeviceToHost, s));
+    std::vector<float> spad(static_cast<size_t>(L->N * L->ng_pad));
+    if (scale_host) FQ_CUDA(cudaMemcpyAsync(spad.data(), st.scale, sizeof(float) * spad.size(), cudaMemcpyDeviceToHost, s));
     if (zero_point_host) {
       FQ_CUDA(cudaMemcpyAsync(zero_point_host, st.zp32, sizeof(int32_t) * ngr, cudaMemcpyDeviceToHost, s));
     }
     FQ_CUDA(cudaStreamSynchronize(s));
+    if (scale_host)
+      for (int64_t r = 0; r < L->N; ++r) std::memcpy(scale_host + r * L->ng, &spad[r * L->ng_pad], sizeof(float) * L->ng);
     if (zero_point_host && st.mode == FQ_MODE_SYM) {
       const int32_t off = (1 << (st.bits - 1)) - 1;
       for (int64_t i = 0; i < ngr; ++i) zero_point_host[i] -= off;

@@ -62,8 +62,8 @@ struct fq_rung_store {
   int mode = FQ_MODE_ASYM;
   uint8_t* payload = nullptr;   // canonical row-major packed codes (device)
   int64_t payload_bytes = 0;
-  float* scale = nullptr;       // [N, ng]
-  uint8_t* zp8 = nullptr;       // [N, ng] effective zero point - zp_base (fast path)
+  float* scale = nullptr;       // [N, ng_pad] (rows padded to 16 B for bulk copies)
+  uint8_t* zp8 = nullptr;       // [N, zp_pad] effective zero point - zp_base (fast path)
   int32_t* zp32 = nullptr;      // [N, ng] effective zero point (z + stored offset), always kept
   int32_t zp_base = 0;
   bool zp_fits_u8 = false;      // fast kernel usable
@@ -73,6 +73,8 @@ struct fq_layer {
   fq_ctx* ctx = nullptr;
   int64_t N = 0, K = 0, G = 0;  // out, in, group (G == K for per-row)
   int64_t ng = 0;               // groups per row = ceil(K / G)
+  int64_t ng_pad = 0;           // scale row stride (multiple of 4 floats = 16 B)
+  int64_t zp_pad = 0;           // u8 zero-point row stride (multiple of 16 B)
   float* fp = nullptr;          // fp32 [N, K] (optional)
   float* bias = nullptr;        // fp32 [N] (optional)
   fq_rung_store r8, r4;
@@ -135,6 +137,7 @@ struct GemvLaunch {
 };
 
 bool gemv_fast_supported(const fq_layer* L, int rung);
+int gemv_fast_grid(const fq_ctx* ctx, int64_t N);
 // Returns the grid size used (the residual epilogue writes one sum-of-squares partial per CTA;
 // out_n_partials must be >= #SM x 4).
 int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);

@@ -4,22 +4,24 @@
 // dequantizes the active rung (src/quantizer.cpp:205-219) and runs a double-accumulated
 // linear (src/tensor.cpp:83-101).  Two numerics:
 //
-//  * fast  — the decode hot path.  Each lane streams 16 codes per row per step with one
-//    coalesced 128-bit (W8) or 64-bit (W4) load, unpacks them in registers and accumulates
-//    sum_j q_j x_j with packed FFMA2.  Unpacking is a single LOP/SHF per code: the masked
-//    code bits (q << s), s < 24, reinterpreted as an fp32 bit pattern are exactly
-//    q * 2^(s-149) (subnormal / first binade), so multiplying by x * 2^(109-s) yields
-//    q*x*2^-40 with no int->float conversion.  The zero point is folded per group:
-//    sum_j (q_j - z) x_j = sum_j q_j x_j - z * sum_j x_j, with sum_j x_j precomputed per lane.
-//    fp32 accumulation; deterministic (fixed reduction order, no atomics).
-//  * exact — golden/parity mode: w = float(code - z) * s in fp32 exactly as dequantize()
-//    does, then double accumulation as linear() does.  Any group size, fp rung, bias.
-//
-// Work split (fast): a persistent-style grid of (#SM x CTAs/SM) CTAs; CTA c owns a balanced
-// contiguous row range of every matrix of the launch; the CTA's W warps split the K-steps
-// (512 codes each) so each warp keeps its activations in registers for the whole kernel and
-// reuses them across all of the CTA's rows; per-row partials are reduced across warps through
-// shared memory in warp order.
+//  * fast  — the decode hot path, a TMA-fed streaming kernel:
+//      - one CTA per SM owns a balanced, contiguous row range of every matrix of the launch;
+//        that range is one contiguous byte range of the row-major payload (plus its padded
+//        scale / zero-point rows), so a producer warp streams it through a shared-memory ring
+//        with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  Bytes in flight per
+//        SM are set by the ring size, not by registers.  The producer never depends on the
+//        previous kernel, so under programmatic dependent launch it starts pulling weights
+//        while the previous kernel is still finishing.
+//      - consumer warps split the K-steps of a row (512 codes per step, 16 per lane) and keep
+//        their activations in registers for the whole kernel.  Unpacking is one LOP/SHF per
+//        code: the masked code bits (q << s), s < 24, reinterpreted as fp32 are exactly
+//        q * 2^(s-149) (subnormal / first binade), so an FFMA2 with x * 2^(109-s) accumulates
+//        q*x*2^-40 without any int->float conversion.  The zero point is folded per group:
+//        sum_j (q_j - z) x_j = sum_j q_j x_j - z * sum_j x_j.
+//      - fp32 accumulation; deterministic (fixed reduction order, no atomics).
+//  * exact — golden/parity mode: one thread per output, w = float(code - z) * s in fp32 as
+//    dequantize() does, then a sequential double accumulation in k order as linear() does:
+//    bit-identical to the reference.  Any group size, fp rung, bias.
 #include "fq_internal.cuh"
 
 #include <algorithm>
@@ -33,10 +35,13 @@ namespace {
 constexpr int kStepCodes = 512;  // codes per row per warp step (32 lanes x 16)
 constexpr int kSegCodes = 16;    // codes per lane per step
 constexpr int kMaxB = 4;         // batch rows per fast launch
+constexpr int kMaxStages = 8;
+constexpr int kConsumerWarps = 8;
 constexpr float kTwo109 = 649037107316853453566312041152512.0f;  // 2^109
 constexpr float kTwo40 = 1099511627776.0f;                        // 2^40
 constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;     // 2^-40
 
+// ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void ffma2(float2& acc, float a0, float a1, float b0, float b1) {
   asm("{\n\t.reg .b64 pa, pb, pc;\n\t"
       "mov.b64 pa, {%2, %3};\n\t"
@@ -48,38 +53,45 @@ __device__ __forceinline__ void ffma2(float2& acc, float a0, float a1, float b0,
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 
-__device__ __forceinline__ uint4 ldg_stream16(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint2 ldg_stream8(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
-  return r;
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 
-__device__ __forceinline__ void pdl_wait() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ float f32(uint32_t u) { return __uint_as_float(u); }
 
 // Bit shift (s) of code j of a 16-code segment after extraction, per bit-width.
-__device__ __forceinline__ int seg_shift(int bits, int j) {
-  if (bits == 8) {
-    const int p = j & 3;
-    return p == 3 ? 0 : 8 * p;
-  }
-  const int p = j & 7;
-  return p < 6 ? 4 * p : 4 * (p - 6);
+__host__ __device__ constexpr int seg_shift(int bits, int j) {
+  return bits == 8 ? ((j & 3) == 3 ? 0 : 8 * (j & 3)) : ((j & 7) < 6 ? 4 * (j & 7) : 4 * ((j & 7) - 6));
 }
 
 // sum_j q_j * xs_j for one 16-code W8 segment (4 words); xs pre-scaled by 2^(109-s_j).
@@ -92,7 +104,9 @@ __device__ __forceinline__ float dot_seg8(const uint4 w, const float* xs) {
     ffma2(i & 1 ? b : a, f32(v & 0xFFu), f32(v & 0xFF00u), xs[4 * i + 0], xs[4 * i + 1]);
     ffma2(i & 1 ? a : b, f32(v & 0xFF0000u), f32(v >> 24), xs[4 * i + 2], xs[4 * i + 3]);
   }
-  return (a.x + a.y) + (b.x + b.y);
+  a.x += b.x;
+  a.y += b.y;
+  return a.x + a.y;
 }
 
 // sum_j q_j * xs_j for one 16-code W4 segment (2 words, low nibble = even element).
@@ -108,7 +122,9 @@ __device__ __forceinline__ float dot_seg4(const uint2 w, const float* xs) {
     ffma2(a, f32(v & 0xF0000u), f32(v & 0xF00000u), xs[8 * i + 4], xs[8 * i + 5]);
     ffma2(b, f32(t & 0xFu), f32(t & 0xF0u), xs[8 * i + 6], xs[8 * i + 7]);
   }
-  return (a.x + a.y) + (b.x + b.y);
+  a.x += b.x;
+  a.y += b.y;
+  return a.x + a.y;
 }
 
 __device__ __forceinline__ float load_act(const void* x, int dtype, int64_t i) {
@@ -129,14 +145,12 @@ __device__ __forceinline__ void store_out(void* y, int dtype, int64_t i, float v
   else static_cast<__half*>(y)[i] = __float2half_rn(v);
 }
 
+// ---------------------------------------------------------------- launch descriptor
 struct DevMat {
-  const uint8_t* payload8;
-  const uint8_t* payload4;
-  const float* scale8;
-  const float* scale4;
-  const uint8_t* zp8_8;
-  const uint8_t* zp8_4;
-  int32_t zpbase8, zpbase4;
+  const uint8_t* payload[2];  // [0] = W8, [1] = W4
+  const float* scale[2];
+  const uint8_t* zp[2];
+  int32_t zpbase[2];
   const uint8_t* rung_table;  // per batch row, or null
   int64_t rung_stride;
   int rung;                   // when no table
@@ -147,8 +161,11 @@ struct DevArgs {
   DevMat mat[3];
   int nmat;
   int B;
-  int64_t N, K, G, ng;
+  int64_t N, K, G, ng_pad, zp_pad;
   int nsteps;
+  int rows_per_stage[2];  // [0] = W8, [1] = W4
+  int stage_bytes;        // ring slot size (bytes, multiple of 128)
+  int nstages;
   const void* x;
   int x_dtype;
   int64_t x_stride;
@@ -171,98 +188,34 @@ __device__ __forceinline__ int mat_rung(const DevMat& m, int b) {
   return m.rung_table ? static_cast<int>(m.rung_table[b * m.rung_stride]) : m.rung;
 }
 
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// Batch-row mask (bit b) of matrix m wanting bit-width slot w (0 = W8, 1 = W4).
+__device__ __forceinline__ int pass_mask(const DevArgs& a, int m, int w) {
+  int mask = 0;
+  const int want = w == 0 ? FQ_RUNG_INT8 : FQ_RUNG_INT4;
+  for (int b = 0; b < a.B; ++b) mask |= (mat_rung(a.mat[m], b) == want) << b;
+  return mask;
 }
 
-// Streams rows [0, rows) of one matrix at one bit-width through this warp's K-steps and
-// deposits the warp's per-row partial sums in shared memory.
-template <int BITS, int SW, int BB>
-__device__ __forceinline__ void stream_rows(const DevArgs& a, const DevMat& M, int m, int rows,
-                                            int64_t r0, int bmask, const bool (&step_ok)[SW],
-                                            const int64_t (&seg_k)[SW], const int (&gidx)[SW],
-                                            const float (&xs)[SW][BB][kSegCodes],
-                                            const float (&sig)[SW][BB], float* red) {
-  constexpr int U = (SW >= 3 ? 2 : (SW == 2 ? 4 : 8));
-  constexpr int NW = BITS == 8 ? 4 : 2;
-  constexpr int kPrefetchBatches = 2;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int W = blockDim.x >> 5;
-  const uint8_t* payload = BITS == 8 ? M.payload8 : M.payload4;
-  const float* scale = BITS == 8 ? M.scale8 : M.scale4;
-  const uint8_t* zp = BITS == 8 ? M.zp8_8 : M.zp8_4;
-  const float zbase = static_cast<float>(BITS == 8 ? M.zpbase8 : M.zpbase4);
-  const int64_t row_bytes = BITS == 8 ? a.K : a.K / 2;
-
-  for (int rb = 0; rb < rows; rb += U) {
-    if (threadIdx.x == 0) {
-      const int ahead = rb + U * (kPrefetchBatches + 1);
-      if (ahead < rows) {
-        const int cnt = min(U, rows - ahead);
-        prefetch_l2_bulk(payload + (r0 + ahead) * row_bytes,
-                         static_cast<uint32_t>((cnt * row_bytes) & ~int64_t(15)));
-      }
-    }
-    uint32_t wv[U][SW][NW];
-    float sc[U][SW];
-    float zf[U][SW];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t row = r0 + rb + u;
-      const bool rok = rb + u < rows;
-#pragma unroll
-      for (int s = 0; s < SW; ++s) {
-        const bool ok = rok && step_ok[s];
-        const int64_t meta = row * a.ng + gidx[s];
-        if constexpr (BITS == 8) {
-          const uint4 v = ok ? ldg_stream16(payload + row * row_bytes + seg_k[s]) : make_uint4(0, 0, 0, 0);
-          wv[u][s][0] = v.x; wv[u][s][1] = v.y; wv[u][s][2] = v.z; wv[u][s][3] = v.w;
-        } else {
-          const uint2 v = ok ? ldg_stream8(payload + row * row_bytes + seg_k[s] / 2) : make_uint2(0, 0);
-          wv[u][s][0] = v.x; wv[u][s][1] = v.y;
-        }
-        sc[u][s] = ok ? __ldg(scale + meta) : 0.f;
-        zf[u][s] = ok ? static_cast<float>(__ldg(zp + meta)) + zbase : 0.f;
-      }
-    }
-    float acc[U][BB];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int b = 0; b < BB; ++b) acc[u][b] = 0.f;
-#pragma unroll
-    for (int s = 0; s < SW; ++s) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-#pragma unroll
-        for (int b = 0; b < BB; ++b) {
-          if (!((bmask >> b) & 1)) continue;
-          float p;
-          if constexpr (BITS == 8) p = dot_seg8(make_uint4(wv[u][s][0], wv[u][s][1], wv[u][s][2], wv[u][s][3]), xs[s][b]);
-          else p = dot_seg4(make_uint2(wv[u][s][0], wv[u][s][1]), xs[s][b]);
-          acc[u][b] = fmaf(sc[u][s], fmaf(-zf[u][s], sig[s][b], p), acc[u][b]);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int b = 0; b < BB; ++b) {
-        float v = acc[u][b];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && rb + u < rows && ((bmask >> b) & 1))
-          red[((m * rows + rb + u) * W + warp) * BB + b] = v;
-      }
-    }
-  }
+// One ring slot: [payload rows][scale rows (ng_pad f32)][zero-point rows (zp_pad u8)]
+struct StageLayout {
+  int rows;
+  int row_bytes;
+  uint32_t pay_bytes, sc_bytes, zp_bytes;
+};
+__device__ __forceinline__ StageLayout stage_layout(const DevArgs& a, int w, int rows) {
+  StageLayout L;
+  L.rows = rows;
+  L.row_bytes = static_cast<int>(w == 0 ? a.K : a.K / 2);
+  L.pay_bytes = static_cast<uint32_t>(rows * L.row_bytes);
+  L.sc_bytes = static_cast<uint32_t>(rows * a.ng_pad * 4);
+  L.zp_bytes = static_cast<uint32_t>(rows * a.zp_pad);
+  return L;
 }
 
-template <int BITS, int SW, int BB>
-__device__ __forceinline__ void load_acts(const DevArgs& a, const bool (&step_ok)[SW],
-                                          const int64_t (&seg_k)[SW], const float (&rstd)[BB],
-                                          float (&xs)[SW][BB][kSegCodes], float (&sig)[SW][BB]) {
+template <int SW, int BB>
+__device__ __forceinline__ void load_acts(const DevArgs& a, int bits, const bool (&step_ok)[SW], const int (&seg_k)[SW],
+                                          const float (&rstd)[BB], float (&xs)[SW][BB][kSegCodes],
+                                          float (&sig)[SW][BB]) {
 #pragma unroll
   for (int s = 0; s < SW; ++s) {
 #pragma unroll
@@ -277,94 +230,191 @@ __device__ __forceinline__ void load_acts(const DevArgs& a, const bool (&step_ok
           if (a.norm_gain != nullptr) v = round_act(v * rstd[b] * a.norm_gain[k], a.act_dtype);
         }
         acc += v;
-        xs[s][b][j] = v * (kTwo109 / static_cast<float>(1u << seg_shift(BITS, j)));
+        const float sc8 = kTwo109 / static_cast<float>(1u << seg_shift(8, j));
+        const float sc4 = kTwo109 / static_cast<float>(1u << seg_shift(4, j));
+        xs[s][b][j] = v * (bits == 8 ? sc8 : sc4);
       }
       sig[s][b] = acc * kTwoM40;
     }
   }
 }
 
-// Fast kernel.  SW = K-steps per warp (compile time), BB = batch rows (compile time bound).
+// Reduces v[0..3] (four rows) across the 32 lanes with 6 shuffles; afterwards lane l holds the
+// warp sum of row ((l >> 3) & 3).
+__device__ __forceinline__ float reduce4(const float (&v)[4], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8;
+  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
+  const float t0 = b4 ? v[0] : v[2], t1 = b4 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, t0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, t1, 16);
+  float k = b3 ? k1 : k0;
+  const float t = b3 ? k0 : k1;
+  k += __shfl_xor_sync(0xffffffffu, t, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;
+}
+
+// Consumes one ring slot: rows [row0, row0 + L.rows) of matrix m at bit-width BITS.
+template <int BITS, int SW, int BB>
+__device__ __forceinline__ void consume_stage(const DevArgs& a, const uint8_t* slot, const StageLayout& L, int m,
+                                              int row0, int rows_cta, int bmask, float zbase,
+                                              const bool (&step_ok)[SW], const int (&seg_k)[SW], const int (&gidx)[SW],
+                                              const float (&xs)[SW][BB][kSegCodes], const float (&sig)[SW][BB],
+                                              float* red, int warp, int lane) {
+  const uint8_t* pay = slot;
+  const float* scl = reinterpret_cast<const float*>(slot + L.pay_bytes);
+  const uint8_t* zps = slot + L.pay_bytes + L.sc_bytes;
+  const int ngp = static_cast<int>(a.ng_pad), zpp = static_cast<int>(a.zp_pad);
+  for (int r0 = 0; r0 < L.rows; r0 += 4) {
+    float acc[BB][4];
+#pragma unroll
+    for (int b = 0; b < BB; ++b)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[b][u] = 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = min(r0 + u, L.rows - 1);
+#pragma unroll
+      for (int s = 0; s < SW; ++s) {
+        const float sc = step_ok[s] ? scl[r * ngp + gidx[s]] : 0.f;
+        const float zf = static_cast<float>(zps[r * zpp + gidx[s]]) + zbase;
+        float p[BB];
+        if constexpr (BITS == 8) {
+          const uint4 w = *reinterpret_cast<const uint4*>(pay + r * L.row_bytes + seg_k[s]);
+#pragma unroll
+          for (int b = 0; b < BB; ++b) p[b] = dot_seg8(w, xs[s][b]);
+        } else {
+          const uint2 w = *reinterpret_cast<const uint2*>(pay + r * L.row_bytes + seg_k[s] / 2);
+#pragma unroll
+          for (int b = 0; b < BB; ++b) p[b] = dot_seg4(w, xs[s][b]);
+        }
+#pragma unroll
+        for (int b = 0; b < BB; ++b) acc[b][u] = fmaf(sc, fmaf(-zf, sig[s][b], p[b]), acc[b][u]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+      const float v = reduce4(acc[b], lane);
+      const int u = (lane >> 3) & 3;
+      if ((lane & 7) == 0 && r0 + u < L.rows && ((bmask >> b) & 1))
+        red[((m * rows_cta + row0 + r0 + u) * kConsumerWarps + warp) * BB + b] = v;
+    }
+  }
+}
+
+// Fast kernel.  SW = K-steps per consumer warp, BB = batch rows (compile-time bounds).
 template <int SW, int BB>
-__global__ void __launch_bounds__(512) gemv_fast_kernel(const DevArgs a) {
-  constexpr int U0 = (SW >= 3 ? 2 : (SW == 2 ? 4 : 8));
-  extern __shared__ float red[];  // [nmat][rows_cta][W][BB]
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(const DevArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(a.nstages) * a.stage_bytes);
+  uint64_t* empty = full + kMaxStages;
+  float* red = reinterpret_cast<float*>(empty + kMaxStages);
+  __shared__ float sq_red[kMaxB][kConsumerWarps + 1];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int W = blockDim.x >> 5;
   const int cta = blockIdx.x;
   const int ncta = gridDim.x;
   const int64_t r0 = (a.N * cta) / ncta;
   const int64_t r1 = (a.N * (cta + 1)) / ncta;
   const int rows = static_cast<int>(r1 - r0);
 
-  bool step_ok[SW];
-  int64_t seg_k[SW];
-  int gidx[SW];
-#pragma unroll
-  for (int s = 0; s < SW; ++s) {
-    const int step = warp + s * W;
-    seg_k[s] = static_cast<int64_t>(step) * kStepCodes + lane * kSegCodes;
-    step_ok[s] = step < a.nsteps && seg_k[s] < a.K;
-    gidx[s] = step_ok[s] ? static_cast<int>(seg_k[s] / a.G) : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
 
-  // Weight streams do not depend on the previous kernel: pull the first row batches of every
-  // matrix into L2 with TMA bulk prefetches before waiting on the dependency.
-  if (threadIdx.x == 0 && rows > 0) {
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: stream this CTA's rows of every matrix through the ring
+    if (lane == 0 && rows > 0) {
+      int t = 0;
+      for (int m = 0; m < a.nmat; ++m) {
+        for (int w = 0; w < 2; ++w) {
+          if (pass_mask(a, m, w) == 0) continue;
+          const int rps = a.rows_per_stage[w];
+          const DevMat& M = a.mat[m];
+          for (int rb = 0; rb < rows; rb += rps, ++t) {
+            const int s = t % a.nstages;
+            const uint32_t ph = (t / a.nstages) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            const StageLayout L = stage_layout(a, w, min(rps, rows - rb));
+            uint8_t* dst = ring + static_cast<size_t>(s) * a.stage_bytes;
+            const int64_t row = r0 + rb;
+            mbar_expect_tx(&full[s], L.pay_bytes + L.sc_bytes + L.zp_bytes);
+            bulk_g2s(dst, M.payload[w] + row * L.row_bytes, L.pay_bytes, &full[s]);
+            bulk_g2s(dst + L.pay_bytes, M.scale[w] + row * a.ng_pad, L.sc_bytes, &full[s]);
+            bulk_g2s(dst + L.pay_bytes + L.sc_bytes, M.zp[w] + row * a.zp_pad, L.zp_bytes, &full[s]);
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers
+    bool step_ok[SW];
+    int seg_k[SW];
+    int gidx[SW];
+#pragma unroll
+    for (int s = 0; s < SW; ++s) {
+      const int step = warp + s * kConsumerWarps;
+      seg_k[s] = step * kStepCodes + lane * kSegCodes;
+      step_ok[s] = step < a.nsteps && seg_k[s] < a.K;
+      gidx[s] = step_ok[s] ? static_cast<int>(seg_k[s] / a.G) : 0;
+      if (!step_ok[s]) seg_k[s] = 0;
+    }
+    pdl_wait();  // activations come from the previous kernel
+    float rstd[BB];
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+      rstd[b] = 1.f;
+      if (a.norm_gain != nullptr && b < a.B) {
+        float s = 0.f;
+        for (int i = lane; i < a.n_partials; i += 32) s += a.norm_partials[b * a.n_partials + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        rstd[b] = 1.0f / sqrtf(s / static_cast<float>(a.K) + a.norm_eps);
+      }
+    }
+    float xs[SW][BB][kSegCodes];
+    float sig[SW][BB];
+    int xs_bits = 0;
+    int t = 0;
     for (int m = 0; m < a.nmat; ++m) {
-      for (int b = 0; b < a.B; ++b) {
-        const int rr = mat_rung(a.mat[m], b);
-        if (rr != FQ_RUNG_INT8 && rr != FQ_RUNG_INT4) continue;
-        const uint8_t* base = rr == FQ_RUNG_INT8 ? a.mat[m].payload8 : a.mat[m].payload4;
-        const int64_t rbytes = rr == FQ_RUNG_INT8 ? a.K : a.K / 2;
-        const int cnt = min(rows, U0 * 3);
-        prefetch_l2_bulk(base + r0 * rbytes, static_cast<uint32_t>((cnt * rbytes) & ~int64_t(15)));
-        break;
+      for (int w = 0; w < 2; ++w) {
+        const int bmask = pass_mask(a, m, w);
+        if (bmask == 0 || rows == 0) continue;
+        const int bits = w == 0 ? 8 : 4;
+        if (xs_bits != bits) {
+          load_acts<SW, BB>(a, bits, step_ok, seg_k, rstd, xs, sig);
+          xs_bits = bits;
+        }
+        const float zb = static_cast<float>(a.mat[m].zpbase[w]);
+        const int rps = a.rows_per_stage[w];
+        for (int rb = 0; rb < rows; rb += rps, ++t) {
+          const int s = t % a.nstages;
+          const uint32_t ph = (t / a.nstages) & 1;
+          mbar_wait(&full[s], ph);
+          const StageLayout L = stage_layout(a, w, min(rps, rows - rb));
+          const uint8_t* slot = ring + static_cast<size_t>(s) * a.stage_bytes;
+          if (bits == 8)
+            consume_stage<8, SW, BB>(a, slot, L, m, rb, rows, bmask, zb, step_ok, seg_k, gidx, xs, sig, red, warp, lane);
+          else
+            consume_stage<4, SW, BB>(a, slot, L, m, rb, rows, bmask, zb, step_ok, seg_k, gidx, xs, sig, red, warp, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
       }
     }
   }
-
-  pdl_wait();
-
-  float rstd[BB];
-#pragma unroll
-  for (int b = 0; b < BB; ++b) {
-    rstd[b] = 1.f;
-    if (a.norm_gain != nullptr && b < a.B) {
-      float s = 0.f;
-      for (int i = lane; i < a.n_partials; i += 32) s += a.norm_partials[b * a.n_partials + i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      rstd[b] = 1.0f / sqrtf(s / static_cast<float>(a.K) + a.norm_eps);
-    }
-  }
-
-  float xs[SW][BB][kSegCodes];
-  float sig[SW][BB];
-  int xs_bits = 0;
-  for (int m = 0; m < a.nmat; ++m) {
-    const DevMat& M = a.mat[m];
-    int want8 = 0, want4 = 0;
-    for (int b = 0; b < a.B; ++b) {
-      const int r = mat_rung(M, b);
-      want8 |= (r == FQ_RUNG_INT8) << b;
-      want4 |= (r == FQ_RUNG_INT4) << b;
-    }
-    if (want8) {
-      if (xs_bits != 8) { load_acts<8, SW, BB>(a, step_ok, seg_k, rstd, xs, sig); xs_bits = 8; }
-      stream_rows<8, SW, BB>(a, M, m, rows, r0, want8, step_ok, seg_k, gidx, xs, sig, red);
-    }
-    if (want4) {
-      if (xs_bits != 4) { load_acts<4, SW, BB>(a, step_ok, seg_k, rstd, xs, sig); xs_bits = 4; }
-      stream_rows<4, SW, BB>(a, M, m, rows, r0, want4, step_ok, seg_k, gidx, xs, sig, red);
-    }
-  }
-  // the next kernel in the stream may start its prologue (weight prefetch) now
   pdl_launch_dependents();
   __syncthreads();
 
-  // cross-warp reduction in warp order + epilogue
+  // ---------------- cross-warp reduction in warp order + epilogue
   const int items = rows * BB;
   float local_sq[BB];
 #pragma unroll
@@ -377,7 +427,7 @@ __global__ void __launch_bounds__(512) gemv_fast_kernel(const DevArgs a) {
     float v[3] = {0.f, 0.f, 0.f};
     for (int m = 0; m < a.nmat; ++m) {
       float s = 0.f;
-      for (int w = 0; w < W; ++w) s += red[((m * rows + r) * W + w) * BB + b];
+      for (int w = 0; w < kConsumerWarps; ++w) s += red[((m * rows + r) * kConsumerWarps + w) * BB + b];
       v[m] = s * kTwo40;
     }
     if (a.epi == EPI_STORE) {
@@ -396,7 +446,6 @@ __global__ void __launch_bounds__(512) gemv_fast_kernel(const DevArgs a) {
     }
   }
   if (a.epi == EPI_RESIDUAL) {
-    __shared__ float sq_red[kMaxB][16];
 #pragma unroll
     for (int b = 0; b < BB; ++b) {
       float v = local_sq[b];
@@ -407,24 +456,23 @@ __global__ void __launch_bounds__(512) gemv_fast_kernel(const DevArgs a) {
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < a.B) {
       float s = 0.f;
-      for (int w = 0; w < W; ++w) s += sq_red[threadIdx.x][w];
+      for (int w = 0; w <= kConsumerWarps; ++w) s += sq_red[threadIdx.x][w];
       a.out_partials[threadIdx.x * a.out_n_partials + cta] = s;
     }
   }
 }
 
-// Exact kernel: one warp per (row, batch row), lanes stride K, double accumulation.
+// Exact kernel: one thread per (row, batch row); sequential k, double accumulation.
 __global__ void gemv_exact_kernel(const int64_t N, const int64_t K, const int64_t G, const int64_t ng,
-                                  const int bits, const uint8_t* payload, const float* scale,
-                                  const int32_t* zp, const float* fpw, const float* bias, const int B,
-                                  const void* x, const int x_dtype, void* y, const int y_dtype) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= N * B) return;
-  const int64_t row = gw / B;
-  const int b = static_cast<int>(gw % B);
-  double acc = 0.0;
-  for (int64_t k = lane; k < K; k += 32) {
+                                  const int64_t ng_pad, const int bits, const uint8_t* payload, const float* scale,
+                                  const int32_t* zp, const float* fpw, const float* bias, const int B, const void* x,
+                                  const int x_dtype, void* y, const int y_dtype) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= N * B) return;
+  const int64_t row = t % N;
+  const int b = static_cast<int>(t / N);
+  double acc = bias ? static_cast<double>(bias[row]) : 0.0;
+  for (int64_t k = 0; k < K; ++k) {
     float w;
     if (bits == 0) {
       w = fpw[row * K + k];
@@ -433,87 +481,86 @@ __global__ void gemv_exact_kernel(const int64_t N, const int64_t K, const int64_
       uint32_t code;
       if (bits == 8) code = payload[idx];
       else code = (idx & 1) ? (payload[idx >> 1] >> 4) : (payload[idx >> 1] & 0xFu);
-      const int64_t g = row * ng + k / G;
-      w = static_cast<float>(static_cast<int32_t>(code) - zp[g]) * scale[g];
+      const int64_t g = k / G;
+      w = static_cast<float>(static_cast<int32_t>(code) - zp[row * ng + g]) * scale[row * ng_pad + g];
     }
     acc += static_cast<double>(load_act(x, x_dtype, b * K + k)) * static_cast<double>(w);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) {
-    if (bias) acc += static_cast<double>(bias[row]);
-    store_out(y, y_dtype, b * N + row, static_cast<float>(acc));
-  }
+  store_out(y, y_dtype, b * N + row, static_cast<float>(acc));
 }
 
-int pick_warps(int nsteps, int* sw_out) {
-  // warps per CTA (4..8) dividing the step count as evenly as possible, <= 4 steps per warp
-  int best_w = 8, best_sw = (nsteps + 7) / 8;
-  double best_eff = -1.0;
-  for (int w = 4; w <= 8; ++w) {
-    const int sw = (nsteps + w - 1) / w;
-    if (sw > 4) continue;
-    const double eff = static_cast<double>(nsteps) / (static_cast<double>(sw) * w);
-    if (eff > best_eff + 1e-9 || (eff > best_eff - 1e-9 && w > best_w)) {
-      best_eff = eff;
-      best_w = w;
-      best_sw = sw;
-    }
+struct Plan {
+  int sw;
+  int grid;
+  int rps[2];
+  int stage_bytes;
+  int nstages;
+  size_t smem;
+};
+
+Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
+  Plan p{};
+  const int nsteps = ceil_div_i(L->K, kStepCodes);
+  p.sw = (nsteps + kConsumerWarps - 1) / kConsumerWarps;
+  p.grid = static_cast<int>(std::min<int64_t>(ctx->num_sms, L->N));
+  const int64_t rows_max = (L->N + p.grid - 1) / p.grid;
+  const int64_t target = 24 * 1024;
+  int64_t slot = 0;
+  for (int w = 0; w < 2; ++w) {
+    const int64_t row_bytes = w == 0 ? L->K : L->K / 2;
+    const int64_t per_row = row_bytes + L->ng_pad * 4 + L->zp_pad;
+    int rps = static_cast<int>(std::max<int64_t>(1, target / per_row));
+    rps = std::min(rps, 16);
+    if (rps > 4) rps = rps / 4 * 4;
+    p.rps[w] = rps;
+    slot = std::max<int64_t>(slot, rps * per_row);
   }
-  *sw_out = best_sw;
-  return best_w;
+  p.stage_bytes = static_cast<int>((slot + 127) / 128 * 128);
+  const size_t red_bytes = static_cast<size_t>(nmat) * rows_max * kConsumerWarps * bb * sizeof(float);
+  const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes) - 2 * kMaxStages * 8 - 256;
+  p.nstages = static_cast<int>(std::min<int64_t>(kMaxStages, budget / p.stage_bytes));
+  if (p.nstages < 2) fail(FQ_E_CONFIG, "gemv: layer rows too large for the shared-memory ring");
+  p.smem = static_cast<size_t>(p.nstages) * p.stage_bytes + 2 * kMaxStages * 8 + red_bytes;
+  return p;
 }
 
 template <int SW, int BB>
-int launch_fast_t(fq_ctx* ctx, const DevArgs& d, int W, size_t smem, bool pdl) {
-  auto kern = gemv_fast_kernel<SW, BB>;
-  // occupancy is a pure function of (kernel, block, smem): cache it, host queries cost microseconds
-  static std::map<std::pair<int, size_t>, int> occ_cache;
-  static std::mutex occ_mu;
-  int per_sm = 0;
+void launch_fast_t(fq_ctx* ctx, const DevArgs& d, const Plan& p, bool pdl) {
+  auto kern = gemv_tma_kernel<SW, BB>;
+  static std::mutex mu;
+  static bool configured = false;
   {
-    std::lock_guard<std::mutex> lk(occ_mu);
-    auto it = occ_cache.find({W, smem});
-    if (it == occ_cache.end()) {
-      if (smem > 48 * 1024)
-        FQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      FQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem));
-      occ_cache[{W, smem}] = per_sm;
-    } else {
-      per_sm = it->second;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!configured) {
+      FQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+      configured = true;
     }
   }
-  per_sm = std::max(1, std::min(per_sm, 4));
-  const int grid = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(ctx->num_sms) * per_sm, d.N));
-  if (d.epi == EPI_RESIDUAL && d.out_n_partials < grid) fail(FQ_E_STATE, "gemv: residual partial buffer too small");
-  DevArgs dd = d;
-  dd.out_n_partials = d.epi == EPI_RESIDUAL ? grid : d.out_n_partials;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(W * 32);
-  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3((kConsumerWarps + 1) * 32);
+  cfg.dynamicSmemBytes = p.smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  FQ_CUDA(cudaLaunchKernelEx(&cfg, kern, dd));
+  FQ_CUDA(cudaLaunchKernelEx(&cfg, kern, d));
   ctx->launches += 1;
-  return grid;
 }
 
 template <int SW>
-int launch_fast_sw(fq_ctx* ctx, const DevArgs& d, int W, size_t smem_per_b, bool pdl) {
+void launch_fast_sw(fq_ctx* ctx, const DevArgs& d, const Plan& p, bool pdl) {
   if constexpr (SW == 1) {
-    if (d.B == 1) return launch_fast_t<SW, 1>(ctx, d, W, smem_per_b, pdl);
-    if (d.B == 2) return launch_fast_t<SW, 2>(ctx, d, W, smem_per_b * 2, pdl);
-    return launch_fast_t<SW, 4>(ctx, d, W, smem_per_b * 4, pdl);
+    if (d.B == 1) launch_fast_t<SW, 1>(ctx, d, p, pdl);
+    else if (d.B == 2) launch_fast_t<SW, 2>(ctx, d, p, pdl);
+    else launch_fast_t<SW, 4>(ctx, d, p, pdl);
   } else if constexpr (SW == 2) {
-    if (d.B == 1) return launch_fast_t<SW, 1>(ctx, d, W, smem_per_b, pdl);
-    return launch_fast_t<SW, 2>(ctx, d, W, smem_per_b * 2, pdl);
+    if (d.B == 1) launch_fast_t<SW, 1>(ctx, d, p, pdl);
+    else launch_fast_t<SW, 2>(ctx, d, p, pdl);
   } else {
-    return launch_fast_t<SW, 1>(ctx, d, W, smem_per_b, pdl);
+    launch_fast_t<SW, 1>(ctx, d, p, pdl);
   }
 }
 
@@ -522,7 +569,13 @@ int launch_fast_sw(fq_ctx* ctx, const DevArgs& d, int W, size_t smem_per_b, bool
 bool gemv_fast_supported(const fq_layer* L, int rung) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) return false;
   const fq_rung_store& s = L->store(rung);
-  return s.present && s.zp_fits_u8 && L->K % 32 == 0 && L->G % kSegCodes == 0 && L->G >= kSegCodes;
+  const int nsteps = ceil_div_i(L->K, kStepCodes);
+  return s.present && s.zp_fits_u8 && L->K % 32 == 0 && L->G % kSegCodes == 0 && L->G >= kSegCodes &&
+         nsteps <= 4 * kConsumerWarps;
+}
+
+int gemv_fast_grid(const fq_ctx* ctx, int64_t N) {
+  return static_cast<int>(std::min<int64_t>(ctx->num_sms, N));
 }
 
 int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
@@ -532,7 +585,8 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
   d.N = L0->N;
   d.K = L0->K;
   d.G = L0->G;
-  d.ng = L0->ng;
+  d.ng_pad = L0->ng_pad;
+  d.zp_pad = L0->zp_pad;
   d.nsteps = ceil_div_i(L0->K, kStepCodes);
   d.x = g.x;
   d.x_dtype = g.x_dtype;
@@ -554,27 +608,28 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
     const fq_layer* L = g.mat[m].layer;
     if (L->N != d.N || L->K != d.K || L->G != d.G) fail(FQ_E_DIMENSION, "multi-gemv: matrices differ in shape");
     DevMat& M = d.mat[m];
-    M.payload8 = L->r8.payload;
-    M.payload4 = L->r4.payload;
-    M.scale8 = L->r8.scale;
-    M.scale4 = L->r4.scale;
-    M.zp8_8 = L->r8.zp8;
-    M.zp8_4 = L->r4.zp8;
-    M.zpbase8 = L->r8.zp_base;
-    M.zpbase4 = L->r4.zp_base;
+    const fq_rung_store* st[2] = {&L->r8, &L->r4};
+    for (int w = 0; w < 2; ++w) {
+      M.payload[w] = st[w]->payload;
+      M.scale[w] = st[w]->scale;
+      M.zp[w] = st[w]->zp8;
+      M.zpbase[w] = st[w]->zp_base;
+    }
     M.rung_table = g.mat[m].rung_table;
     M.rung_stride = g.mat[m].rung_stride;
     M.rung = g.mat[m].rung;
     M.y = g.mat[m].y;
   }
-  int sw = 1;
-  const int W = pick_warps(d.nsteps, &sw);
-  // rows per CTA is bounded by ceil(N / #SM) (at least one CTA per SM)
-  const int64_t rows_max = (d.N + ctx->num_sms - 1) / ctx->num_sms;
-  const size_t smem_per_b = static_cast<size_t>(g.nmat) * rows_max * W * sizeof(float);
-  // registers hold SW x B x 16 activations: keep SW*B <= 4 by chunking the batch
-  const int64_t bchunk = sw == 1 ? kMaxB : (sw == 2 ? 2 : 1);
-  int grid = 0;
+  const int sw0 = (d.nsteps + kConsumerWarps - 1) / kConsumerWarps;
+  const int64_t bchunk = sw0 == 1 ? kMaxB : (sw0 == 2 ? 2 : 1);
+  const int64_t bb = std::min<int64_t>(bchunk, g.batch);
+  const Plan p = plan_fast(ctx, L0, g.nmat, static_cast<int>(bb == 3 ? 4 : bb));
+  d.rows_per_stage[0] = p.rps[0];
+  d.rows_per_stage[1] = p.rps[1];
+  d.stage_bytes = p.stage_bytes;
+  d.nstages = p.nstages;
+  if (g.epi == EPI_RESIDUAL && g.out_n_partials < p.grid) fail(FQ_E_STATE, "gemv: residual partial buffer too small");
+  d.out_n_partials = g.out_n_partials;
   for (int64_t b0 = 0; b0 < g.batch; b0 += bchunk) {
     DevArgs c = d;
     c.B = static_cast<int>(std::min<int64_t>(bchunk, g.batch - b0));
@@ -588,25 +643,24 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
     if (g.resid) c.resid = g.resid + b0 * g.resid_stride;
     if (g.out_partials) c.out_partials = g.out_partials + b0 * g.out_n_partials;
     if (g.norm_partials) c.norm_partials = g.norm_partials + b0 * g.n_partials;
-    switch (sw) {
-      case 1: grid = launch_fast_sw<1>(ctx, c, W, smem_per_b, g.pdl); break;
-      case 2: grid = launch_fast_sw<2>(ctx, c, W, smem_per_b, g.pdl); break;
-      case 3: grid = launch_fast_sw<3>(ctx, c, W, smem_per_b, g.pdl); break;
-      default: grid = launch_fast_sw<4>(ctx, c, W, smem_per_b, g.pdl); break;
+    switch (p.sw) {
+      case 1: launch_fast_sw<1>(ctx, c, p, g.pdl); break;
+      case 2: launch_fast_sw<2>(ctx, c, p, g.pdl); break;
+      case 3: launch_fast_sw<3>(ctx, c, p, g.pdl); break;
+      default: launch_fast_sw<4>(ctx, c, p, g.pdl); break;
     }
   }
-  return grid;
+  return p.grid;
 }
 
-void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
-                       int x_dtype, void* y, int y_dtype) {
+void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x, int x_dtype, void* y,
+                       int y_dtype) {
   if (!L->has(rung)) fail(FQ_E_STATE, "gemv: rung not resident on the device");
-  const int threads = 256;
-  const int64_t warps = L->N * batch;
-  const int blocks = ceil_div_i(warps * 32, threads);
+  const int threads = 128;
+  const int64_t n = L->N * batch;
   const fq_rung_store* s = rung == FQ_RUNG_FP ? nullptr : &L->store(rung);
-  gemv_exact_kernel<<<blocks, threads, 0, ctx->stream>>>(
-      L->N, L->K, L->G, L->ng, s ? s->bits : 0, s ? s->payload : nullptr, s ? s->scale : nullptr,
+  gemv_exact_kernel<<<ceil_div_i(n, threads), threads, 0, ctx->stream>>>(
+      L->N, L->K, L->G, L->ng, L->ng_pad, s ? s->bits : 0, s ? s->payload : nullptr, s ? s->scale : nullptr,
       s ? s->zp32 : nullptr, L->fp, L->bias, static_cast<int>(batch), x, x_dtype, y, y_dtype);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;

@@ -17,7 +17,7 @@
 namespace fqc {
 namespace {
 
-__global__ void quantize_group_kernel(const float* __restrict__ w, int64_t N, int64_t K, int64_t G, int64_t ng,
+__global__ void quantize_group_kernel(const float* __restrict__ w, int64_t N, int64_t K, int64_t G, int64_t ng, int64_t ng_pad,
                                       int bits, int mode, uint8_t* __restrict__ payload, float* __restrict__ scale,
                                       int32_t* __restrict__ zp_eff, int* __restrict__ bad) {
   const int lane = threadIdx.x & 31;
@@ -97,7 +97,7 @@ __global__ void quantize_group_kernel(const float* __restrict__ w, int64_t N, in
       put(i, code_of(x[i]), i + 1 < len ? code_of(x[i + 1]) : 0u, i + 1 < len);
   }
   if (lane == 0) {
-    scale[gid] = s;
+    scale[row * ng_pad + g] = s;
     zp_eff[gid] = z + (mode == FQ_MODE_SYM ? static_cast<int32_t>(m) : 0);
   }
 }
@@ -141,10 +141,14 @@ __global__ void zp_range_kernel(const int32_t* __restrict__ zp, int64_t n, int* 
   }
 }
 
-__global__ void zp_pack_kernel(const int32_t* __restrict__ zp, int64_t n, int32_t base, uint8_t* __restrict__ out) {
+__global__ void zp_pack_kernel(const int32_t* __restrict__ zp, int64_t N, int64_t ng, int64_t zp_pad, int32_t base,
+                               uint8_t* __restrict__ out) {
+  const int64_t n = N * zp_pad;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[i] = static_cast<uint8_t>(zp[i] - base);
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / zp_pad, g = i % zp_pad;
+    out[i] = g < ng ? static_cast<uint8_t>(zp[r * ng + g] - base) : 0;
+  }
 }
 
 }  // namespace
@@ -164,8 +168,9 @@ void finalize_rung_meta(fq_ctx* ctx, fq_layer* L, int rung) {
   st.zp_fits_u8 = (static_cast<int64_t>(h[1]) - h[0]) <= 255;
   st.zp_base = st.zp_fits_u8 ? h[0] : 0;
   if (st.zp_fits_u8) {
-    if (st.zp8 == nullptr) st.zp8 = static_cast<uint8_t*>(dmalloc(static_cast<size_t>(n)));
-    zp_pack_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(st.zp32, n, st.zp_base, st.zp8);
+    if (st.zp8 == nullptr) st.zp8 = static_cast<uint8_t*>(dmalloc(static_cast<size_t>(L->N * L->zp_pad)));
+    const int pblocks = static_cast<int>(std::min<int64_t>(1024, (L->N * L->zp_pad + 255) / 256));
+    zp_pack_kernel<<<std::max(pblocks, 1), 256, 0, ctx->stream>>>(st.zp32, L->N, L->ng, L->zp_pad, st.zp_base, st.zp8);
     FQ_CUDA(cudaGetLastError());
     ctx->launches += 1;
   }
@@ -185,7 +190,8 @@ void quantize_device(fq_ctx* ctx, fq_layer* L, int rung, int mode, const float* 
   const int64_t groups = L->N * L->ng;
   if (!st.present) {
     st.payload = static_cast<uint8_t*>(dmalloc(bytes));
-    st.scale = static_cast<float*>(dmalloc(sizeof(float) * groups));
+    st.scale = static_cast<float*>(dmalloc(sizeof(float) * L->N * L->ng_pad));
+    FQ_CUDA(cudaMemsetAsync(st.scale, 0, sizeof(float) * L->N * L->ng_pad, ctx->stream));
     st.zp32 = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * groups));
   }
   st.bits = bits;
@@ -194,7 +200,7 @@ void quantize_device(fq_ctx* ctx, fq_layer* L, int rung, int mode, const float* 
   int* bad = static_cast<int*>(ctx->ensure_scratch(64));
   FQ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
   const int64_t threads = groups * 32;
-  quantize_group_kernel<<<ceil_div_i(threads, 256), 256, 0, ctx->stream>>>(w_dev, L->N, L->K, L->G, L->ng, bits, mode,
+  quantize_group_kernel<<<ceil_div_i(threads, 256), 256, 0, ctx->stream>>>(w_dev, L->N, L->K, L->G, L->ng, L->ng_pad, bits, mode,
                                                                           st.payload, st.scale, st.zp32, bad);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;

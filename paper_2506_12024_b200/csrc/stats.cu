@@ -204,7 +204,7 @@ __global__ void minmax_kernel(const float* __restrict__ w, int64_t n, float* out
 // counts[0..bins) for the fp weights, counts[bins..2bins) for the dequantized rung
 __global__ void hist_kernel(const float* __restrict__ fpw, const uint8_t* __restrict__ payload, int bits,
                             const float* __restrict__ scale, const int32_t* __restrict__ zp, int64_t N,
-                            int64_t K, int64_t G, int64_t ng, const double* __restrict__ edges_g, int bins,
+                            int64_t K, int64_t G, int64_t ng, int64_t ng_pad, const double* __restrict__ edges_g, int bins,
                             unsigned long long* counts) {
   extern __shared__ unsigned char smem_raw[];
   double* edges = reinterpret_cast<double*>(smem_raw);
@@ -232,8 +232,8 @@ __global__ void hist_kernel(const float* __restrict__ fpw, const uint8_t* __rest
     uint32_t code;
     if (bits == 8) code = payload[i];
     else code = (i & 1) ? (payload[i >> 1] >> 4) : (payload[i >> 1] & 0xFu);
-    const int64_t g = row * ng + k / G;
-    const float dq = static_cast<float>(static_cast<int32_t>(code) - zp[g]) * scale[g];
+    const int64_t g = k / G;
+    const float dq = static_cast<float>(static_cast<int32_t>(code) - zp[row * ng + g]) * scale[row * ng_pad + g];
     atomicAdd(&c[bins + bin_of(static_cast<double>(dq))], 1u);
   }
   __syncthreads();
@@ -307,7 +307,7 @@ double hist_kl(fq_ctx* ctx, const fq_layer* L, int rung, int bins) {
   if (smem > 48 * 1024) FQ_CUDA(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int blocks = static_cast<int>(std::min<int64_t>(ctx->num_sms * 2, (n + 1023) / 1024));
   hist_kernel<<<std::max(blocks, 1), 512, smem, ctx->stream>>>(L->fp, st.payload, st.bits, st.scale, st.zp32, L->N, L->K,
-                                                              L->G, L->ng, d_edges, bins, d_counts);
+                                                              L->G, L->ng, L->ng_pad, d_edges, bins, d_counts);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 3;
   std::vector<unsigned long long> counts(2 * bins);
