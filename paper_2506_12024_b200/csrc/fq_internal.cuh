@@ -120,8 +120,9 @@ struct GemvLaunch {
   int64_t x_stride = 0;  // elements
   // optional fused RMSNorm prologue: x is the fp32 residual; h = round_act(x*rstd*gain)
   const float* norm_gain = nullptr;
-  const float* norm_partials = nullptr;  // [batch, n_partials] sums of squares
+  const float* norm_partials = nullptr;  // [batch][partials_stride] sums of squares
   int n_partials = 0;
+  int partials_stride = 0;               // 0 = n_partials
   float norm_eps = 1e-5f;
   int act_dtype = FQ_DT_BF16;  // rounding applied to the normalized activations
   // output

@@ -164,6 +164,8 @@ struct DevArgs {
   int64_t N, K, G, ng_pad, zp_pad;
   int nsteps;
   int rows_per_stage[2];  // [0] = W8, [1] = W4
+  int sc_off[2], zp_off[2];  // byte offsets of the scale / zero-point blocks in a slot
+  int sc_row, zp_row;        // bytes per row of the scale / zero-point blocks
   int stage_bytes;        // ring slot size (bytes, multiple of 128)
   int nstages;
   const void* x;
@@ -172,6 +174,7 @@ struct DevArgs {
   const float* norm_gain;
   const float* norm_partials;
   int n_partials;
+  int partials_stride;
   float norm_eps;
   int act_dtype;
   int epi;
@@ -196,11 +199,13 @@ __device__ __forceinline__ int pass_mask(const DevArgs& a, int m, int w) {
   return mask;
 }
 
-// One ring slot: [payload rows][scale rows (ng_pad f32)][zero-point rows (zp_pad u8)]
+// One ring slot (per bit-width w): [payload: rows_pad rows][scales: rows_pad x ng_pad f32]
+// [zero points: rows_pad x zp_pad u8]; rows_pad = rows per stage rounded up to 4.  A partial
+// stage copies fewer rows; the trailing rows are stale and their results are discarded.
 struct StageLayout {
   int rows;
   int row_bytes;
-  uint32_t pay_bytes, sc_bytes, zp_bytes;
+  uint32_t pay_bytes, sc_bytes, zp_bytes;  // bytes actually copied
 };
 __device__ __forceinline__ StageLayout stage_layout(const DevArgs& a, int w, int rows) {
   StageLayout L;
@@ -256,18 +261,20 @@ __device__ __forceinline__ float reduce4(const float (&v)[4], int lane) {
   return k;
 }
 
-// Consumes one ring slot: rows [row0, row0 + L.rows) of matrix m at bit-width BITS.
+// Consumes one ring slot holding `nrows` rows at bit-width BITS.  Lane-constant offsets:
+// pay_l = byte offset of the lane's segment in a row, sc_l / zp_l = the lane's group column.
+// red_row points at red[(first row)][warp][0] of this slot; rows are W*BB floats apart.
 template <int BITS, int SW, int BB>
-__device__ __forceinline__ void consume_stage(const DevArgs& a, const uint8_t* slot, const StageLayout& L, int m,
-                                              int row0, int rows_cta, int bmask, float zbase,
-                                              const bool (&step_ok)[SW], const int (&seg_k)[SW], const int (&gidx)[SW],
-                                              const float (&xs)[SW][BB][kSegCodes], const float (&sig)[SW][BB],
-                                              float* red, int warp, int lane) {
-  const uint8_t* pay = slot;
-  const float* scl = reinterpret_cast<const float*>(slot + L.pay_bytes);
-  const uint8_t* zps = slot + L.pay_bytes + L.sc_bytes;
-  const int ngp = static_cast<int>(a.ng_pad), zpp = static_cast<int>(a.zp_pad);
-  for (int r0 = 0; r0 < L.rows; r0 += 4) {
+__device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, int nrows, int row_bytes,
+                                              int sc_off, int zp_off, int sc_row, int zp_row,
+                                              const int (&pay_l)[SW], const int (&sc_l)[SW], const int (&zp_l)[SW],
+                                              float zmagic, const float (&xs)[SW][BB][kSegCodes],
+                                              const float (&sig)[SW][BB], float* red_row, int bmask, int lane) {
+  const uint8_t* pa = slot;
+  const uint8_t* sa = slot + sc_off;
+  const uint8_t* za = slot + zp_off;
+  const int red_step = kConsumerWarps * BB;
+  for (int r0 = 0; r0 < nrows; r0 += 4) {
     float acc[BB][4];
 #pragma unroll
     for (int b = 0; b < BB; ++b)
@@ -275,18 +282,18 @@ __device__ __forceinline__ void consume_stage(const DevArgs& a, const uint8_t* s
       for (int u = 0; u < 4; ++u) acc[b][u] = 0.f;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int r = min(r0 + u, L.rows - 1);
 #pragma unroll
       for (int s = 0; s < SW; ++s) {
-        const float sc = step_ok[s] ? scl[r * ngp + gidx[s]] : 0.f;
-        const float zf = static_cast<float>(zps[r * zpp + gidx[s]]) + zbase;
+        const float sc = *reinterpret_cast<const float*>(sa + u * sc_row + sc_l[s]);
+        const uint32_t zq = za[u * zp_row + zp_l[s]];
+        const float zf = __uint_as_float(0x4B000000u | zq) - zmagic;  // exact: zq + zp_base
         float p[BB];
         if constexpr (BITS == 8) {
-          const uint4 w = *reinterpret_cast<const uint4*>(pay + r * L.row_bytes + seg_k[s]);
+          const uint4 w = *reinterpret_cast<const uint4*>(pa + u * row_bytes + pay_l[s]);
 #pragma unroll
           for (int b = 0; b < BB; ++b) p[b] = dot_seg8(w, xs[s][b]);
         } else {
-          const uint2 w = *reinterpret_cast<const uint2*>(pay + r * L.row_bytes + seg_k[s] / 2);
+          const uint2 w = *reinterpret_cast<const uint2*>(pa + u * row_bytes + pay_l[s]);
 #pragma unroll
           for (int b = 0; b < BB; ++b) p[b] = dot_seg4(w, xs[s][b]);
         }
@@ -294,13 +301,15 @@ __device__ __forceinline__ void consume_stage(const DevArgs& a, const uint8_t* s
         for (int b = 0; b < BB; ++b) acc[b][u] = fmaf(sc, fmaf(-zf, sig[s][b], p[b]), acc[b][u]);
       }
     }
+    const int u = (lane >> 3) & 3;
 #pragma unroll
     for (int b = 0; b < BB; ++b) {
       const float v = reduce4(acc[b], lane);
-      const int u = (lane >> 3) & 3;
-      if ((lane & 7) == 0 && r0 + u < L.rows && ((bmask >> b) & 1))
-        red[((m * rows_cta + row0 + r0 + u) * kConsumerWarps + warp) * BB + b] = v;
+      if ((lane & 7) == 0 && r0 + u < nrows && ((bmask >> b) & 1)) red_row[(r0 + u) * red_step + b] = v;
     }
+    pa += 4 * row_bytes;
+    sa += 4 * sc_row;
+    za += 4 * zp_row;
   }
 }
 
@@ -348,12 +357,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
             const int64_t row = r0 + rb;
             mbar_expect_tx(&full[s], L.pay_bytes + L.sc_bytes + L.zp_bytes);
             bulk_g2s(dst, M.payload[w] + row * L.row_bytes, L.pay_bytes, &full[s]);
-            bulk_g2s(dst + L.pay_bytes, M.scale[w] + row * a.ng_pad, L.sc_bytes, &full[s]);
-            bulk_g2s(dst + L.pay_bytes + L.sc_bytes, M.zp[w] + row * a.zp_pad, L.zp_bytes, &full[s]);
+            bulk_g2s(dst + a.sc_off[w], M.scale[w] + row * a.ng_pad, L.sc_bytes, &full[s]);
+            bulk_g2s(dst + a.zp_off[w], M.zp[w] + row * a.zp_pad, L.zp_bytes, &full[s]);
           }
         }
       }
     }
+    pdl_wait();  // the epilogue below reads buffers written by the previous kernel
   } else {
     // ---------------- consumers
     bool step_ok[SW];
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
       rstd[b] = 1.f;
       if (a.norm_gain != nullptr && b < a.B) {
         float s = 0.f;
-        for (int i = lane; i < a.n_partials; i += 32) s += a.norm_partials[b * a.n_partials + i];
+        for (int i = lane; i < a.n_partials; i += 32) s += a.norm_partials[b * a.partials_stride + i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         rstd[b] = 1.0f / sqrtf(s / static_cast<float>(a.K) + a.norm_eps);
@@ -393,18 +403,29 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
           load_acts<SW, BB>(a, bits, step_ok, seg_k, rstd, xs, sig);
           xs_bits = bits;
         }
-        const float zb = static_cast<float>(a.mat[m].zpbase[w]);
+        const float zmagic = 8388608.0f - static_cast<float>(a.mat[m].zpbase[w]);
         const int rps = a.rows_per_stage[w];
+        const int row_bytes = static_cast<int>(w == 0 ? a.K : a.K / 2);
+        int pay_l[SW], sc_l[SW], zp_l[SW];
+#pragma unroll
+        for (int s = 0; s < SW; ++s) {
+          pay_l[s] = w == 0 ? seg_k[s] : seg_k[s] / 2;
+          sc_l[s] = gidx[s] * 4;
+          zp_l[s] = gidx[s];
+        }
         for (int rb = 0; rb < rows; rb += rps, ++t) {
           const int s = t % a.nstages;
           const uint32_t ph = (t / a.nstages) & 1;
           mbar_wait(&full[s], ph);
-          const StageLayout L = stage_layout(a, w, min(rps, rows - rb));
           const uint8_t* slot = ring + static_cast<size_t>(s) * a.stage_bytes;
+          float* red_row = red + ((m * rows + rb) * kConsumerWarps + warp) * BB;
+          const int nr = min(rps, rows - rb);
           if (bits == 8)
-            consume_stage<8, SW, BB>(a, slot, L, m, rb, rows, bmask, zb, step_ok, seg_k, gidx, xs, sig, red, warp, lane);
+            consume_stage<8, SW, BB>(slot, nr, row_bytes, a.sc_off[0], a.zp_off[0], a.sc_row, a.zp_row, pay_l, sc_l,
+                                     zp_l, zmagic, xs, sig, red_row, bmask, lane);
           else
-            consume_stage<4, SW, BB>(a, slot, L, m, rb, rows, bmask, zb, step_ok, seg_k, gidx, xs, sig, red, warp, lane);
+            consume_stage<4, SW, BB>(slot, nr, row_bytes, a.sc_off[1], a.zp_off[1], a.sc_row, a.zp_row, pay_l, sc_l,
+                                     zp_l, zmagic, xs, sig, red_row, bmask, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
         }
@@ -493,6 +514,7 @@ struct Plan {
   int sw;
   int grid;
   int rps[2];
+  int sc_off[2], zp_off[2];
   int stage_bytes;
   int nstages;
   size_t smem;
@@ -512,8 +534,11 @@ Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
     int rps = static_cast<int>(std::max<int64_t>(1, target / per_row));
     rps = std::min(rps, 16);
     if (rps > 4) rps = rps / 4 * 4;
+    const int64_t pad = (rps + 3) / 4 * 4;
     p.rps[w] = rps;
-    slot = std::max<int64_t>(slot, rps * per_row);
+    p.sc_off[w] = static_cast<int>(pad * row_bytes);
+    p.zp_off[w] = static_cast<int>(pad * row_bytes + pad * L->ng_pad * 4);
+    slot = std::max<int64_t>(slot, pad * per_row);
   }
   p.stage_bytes = static_cast<int>((slot + 127) / 128 * 128);
   const size_t red_bytes = static_cast<size_t>(nmat) * rows_max * kConsumerWarps * bb * sizeof(float);
@@ -594,6 +619,7 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
   d.norm_gain = g.norm_gain;
   d.norm_partials = g.norm_partials;
   d.n_partials = g.n_partials;
+  d.partials_stride = g.partials_stride ? g.partials_stride : g.n_partials;
   d.norm_eps = g.norm_eps;
   d.act_dtype = g.act_dtype;
   d.epi = g.epi;
@@ -626,6 +652,12 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
   const Plan p = plan_fast(ctx, L0, g.nmat, static_cast<int>(bb == 3 ? 4 : bb));
   d.rows_per_stage[0] = p.rps[0];
   d.rows_per_stage[1] = p.rps[1];
+  for (int w = 0; w < 2; ++w) {
+    d.sc_off[w] = p.sc_off[w];
+    d.zp_off[w] = p.zp_off[w];
+  }
+  d.sc_row = static_cast<int>(L0->ng_pad * 4);
+  d.zp_row = static_cast<int>(L0->zp_pad);
   d.stage_bytes = p.stage_bytes;
   d.nstages = p.nstages;
   if (g.epi == EPI_RESIDUAL && g.out_n_partials < p.grid) fail(FQ_E_STATE, "gemv: residual partial buffer too small");
@@ -642,7 +674,7 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
     }
     if (g.resid) c.resid = g.resid + b0 * g.resid_stride;
     if (g.out_partials) c.out_partials = g.out_partials + b0 * g.out_n_partials;
-    if (g.norm_partials) c.norm_partials = g.norm_partials + b0 * g.n_partials;
+    if (g.norm_partials) c.norm_partials = g.norm_partials + b0 * d.partials_stride;
     switch (p.sw) {
       case 1: launch_fast_sw<1>(ctx, c, p, g.pdl); break;
       case 2: launch_fast_sw<2>(ctx, c, p, g.pdl); break;

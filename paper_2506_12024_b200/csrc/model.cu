@@ -1,24 +1,1270 @@
-// Device decoder (placeholder until the decode step lands).
+// Device-resident decoder: precision table, KV cache, and the graph-captured decode step.
+//
+// Two block families behind one object (include/fq_cuda.h):
+//  * FQ_ARCH_LLAMA (BASELINE configs): RMSNorm (fused into the next GEMV's prologue through
+//    per-CTA sum-of-squares partials), fused QKV GEMV, RoPE + fp16 KV append + attention in one
+//    kernel, residual-add epilogues, gate/up GEMV with a SwiGLU epilogue, head GEMV, fused
+//    softmax statistics.  bf16 (or fp16) activations, fp32 residual stream, fp32 logits.
+//  * FQ_ARCH_REFERENCE: the reference's own model (/root/reference/proj/src/model.cpp:193-266):
+//    learned positions, LayerNorm + biases, GELU FFN, fp32 activations, every reduction done
+//    sequentially in double in the reference's order, so logits are bit-identical to the CPU
+//    reference (the golden-trace mode).
+//
+// A rung switch (Model::set_precision, src/model.cpp:268-278) is a one-byte write into the
+// host precision table; the per-step table for the batch rows is copied to the device by the
+// captured graph, and the GEMVs select the W8 or W4 copy from it, so no weights move and the
+// graph is never re-captured.
 #include "fq_internal.cuh"
-using namespace fqc;
-extern "C" {
-#define FQ_TODO return guarded([&] { fail(FQ_E_STATE, "fq_model: not implemented yet"); })
-fq_status fq_model_create(fq_ctx*, const fq_model_config*, fq_model**) { FQ_TODO; }
-fq_status fq_model_destroy(fq_model*) { FQ_TODO; }
-fq_status fq_model_num_linears(const fq_model*, int32_t*) { FQ_TODO; }
-fq_status fq_model_linear_id(const fq_model*, int32_t, char*, int32_t) { FQ_TODO; }
-fq_status fq_model_linear_index(const fq_model*, const char*, int32_t*) { FQ_TODO; }
-fq_status fq_model_linear(fq_model*, int32_t, fq_layer**) { FQ_TODO; }
-fq_status fq_model_set_param(fq_model*, const char*, const float*, int64_t) { FQ_TODO; }
-fq_status fq_model_init_random(fq_model*, uint64_t, float) { FQ_TODO; }
-fq_status fq_model_set_rung(fq_model*, int32_t, int32_t, int32_t) { FQ_TODO; }
-fq_status fq_model_get_rung(const fq_model*, int32_t, int32_t, int32_t*) { FQ_TODO; }
-fq_status fq_model_set_all_rungs(fq_model*, int32_t, int32_t) { FQ_TODO; }
-fq_status fq_model_reset_slot(fq_model*, int32_t) { FQ_TODO; }
-fq_status fq_model_slot_length(const fq_model*, int32_t, int64_t*) { FQ_TODO; }
-fq_status fq_model_prefill(fq_model*, int32_t, const int32_t*, int64_t, float*, fq_row_stats*) { FQ_TODO; }
-fq_status fq_model_decode(fq_model*, int32_t, const int32_t*, const int32_t*, float*, fq_row_stats*) { FQ_TODO; }
-fq_status fq_model_logits(fq_model*, float**) { FQ_TODO; }
-fq_status fq_model_step_bytes(const fq_model*, int32_t, const int32_t*, int64_t*, int64_t*) { FQ_TODO; }
-fq_status fq_model_calibrate_logit_kl(fq_model*, const int32_t*, int64_t, int64_t, int32_t, int32_t, double*, double*) { FQ_TODO; }
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+
+namespace fqc {
+namespace {
+
+constexpr int kPartStride = 1024;  // columns of the sum-of-squares partial buffer per batch row
+constexpr int kAttnChunk = 64;     // keys per attention CTA (llama)
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+__device__ __forceinline__ float act_load(const void* p, int dtype, int64_t i) {
+  if (dtype == FQ_DT_F32) return static_cast<const float*>(p)[i];
+  if (dtype == FQ_DT_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+  return __half2float(static_cast<const __half*>(p)[i]);
 }
+__device__ __forceinline__ void act_store(void* p, int dtype, int64_t i, float v) {
+  if (dtype == FQ_DT_F32) static_cast<float*>(p)[i] = v;
+  else if (dtype == FQ_DT_BF16) static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
+  else static_cast<__half*>(p)[i] = __float2half_rn(v);
+}
+
+// Step metadata staged by the host each step: tokens[B], pos[B], slots[B], then the per-row
+// precision table [B][n_lin] (bytes).
+struct StepMeta {
+  const int32_t* tokens;
+  const int32_t* pos;
+  const int32_t* slots;
+};
+
+// ------------------------------------------------------------------ llama kernels
+__global__ void embed_llama_kernel(const float* __restrict__ tok_emb, StepMeta meta, int64_t d,
+                                   float* __restrict__ resid, float* __restrict__ partials) {
+  const int b = blockIdx.x;
+  const float* e = tok_emb + static_cast<int64_t>(meta.tokens[b]) * d;
+  float* x = resid + b * d;
+  float sq = 0.f;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    const float v = e[c];
+    x[c] = v;
+    sq += v * v;
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
+    partials[b * kPartStride] = s;
+  }
+}
+
+// RoPE (rotate-half pairing, HF Llama convention): for i < hd/2 the pair (i, i + hd/2) rotates
+// by angle pos * theta^(-2i/hd); angles in double.
+__device__ __forceinline__ void rope_pair(float& a, float& b, int i, int hd, int pos, float theta) {
+  const double inv = pow(static_cast<double>(theta), -2.0 * i / hd);
+  double sn, cs;
+  sincos(static_cast<double>(pos) * inv, &sn, &cs);
+  const float c = static_cast<float>(cs), s = static_cast<float>(sn);
+  const float x0 = a, x1 = b;
+  a = x0 * c - x1 * s;
+  b = x1 * c + x0 * s;
+}
+
+// Decode attention for one (head, batch row, key chunk).  The chunk holding the row's own
+// position rotates and appends the new key/value to the fp16 cache.  Partial softmax states are
+// merged by the last CTA of the (row, head) in chunk order.
+__global__ void __launch_bounds__(128) attn_llama_kernel(const void* __restrict__ q, const void* __restrict__ k,
+                                                         const void* __restrict__ v, int act_dtype, StepMeta meta,
+                                                         __half* __restrict__ kv, int64_t slot_stride,
+                                                         int64_t layer_off, int64_t max_seq, int n_heads, int hd,
+                                                         float theta, float* __restrict__ ws,
+                                                         unsigned int* __restrict__ tickets, void* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int h = blockIdx.x, b = blockIdx.y, chunk = blockIdx.z, nchunks = gridDim.z;
+  const int pos = meta.pos[b];
+  const int slot = meta.slots[b];
+  const int d = n_heads * hd;
+  __shared__ float qs[256];
+  __shared__ float knew[256];
+  __shared__ float sc[kAttnChunk];
+  __shared__ bool last;
+  const int j0 = chunk * kAttnChunk;
+  const int j1 = min(j0 + kAttnChunk, pos + 1);
+  __half* kc = kv + slot * slot_stride + layer_off + static_cast<int64_t>(h) * max_seq * hd;
+  __half* vc = kc + static_cast<int64_t>(n_heads) * max_seq * hd;
+  float* wsp = ws + ((static_cast<int64_t>(b) * n_heads + h) * nchunks + chunk) * (hd + 2);
+  if (j0 <= pos) {
+    // q with RoPE, pre-scaled by 1/sqrt(hd)
+    const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+    for (int i = threadIdx.x; i < hd / 2; i += blockDim.x) {
+      float a0 = act_load(q, act_dtype, static_cast<int64_t>(b) * d + h * hd + i);
+      float a1 = act_load(q, act_dtype, static_cast<int64_t>(b) * d + h * hd + i + hd / 2);
+      rope_pair(a0, a1, i, hd, pos, theta);
+      qs[i] = a0 * scale;
+      qs[i + hd / 2] = a1 * scale;
+    }
+    const bool owns_new = pos >= j0 && pos < j0 + kAttnChunk;
+    if (owns_new) {
+      for (int i = threadIdx.x; i < hd / 2; i += blockDim.x) {
+        float a0 = act_load(k, act_dtype, static_cast<int64_t>(b) * d + h * hd + i);
+        float a1 = act_load(k, act_dtype, static_cast<int64_t>(b) * d + h * hd + i + hd / 2);
+        rope_pair(a0, a1, i, hd, pos, theta);
+        const __half h0 = __float2half_rn(a0), h1 = __float2half_rn(a1);
+        kc[static_cast<int64_t>(pos) * hd + i] = h0;
+        kc[static_cast<int64_t>(pos) * hd + i + hd / 2] = h1;
+        knew[i] = __half2float(h0);
+        knew[i + hd / 2] = __half2float(h1);
+      }
+      for (int i = threadIdx.x; i < hd; i += blockDim.x)
+        vc[static_cast<int64_t>(pos) * hd + i] = __float2half_rn(act_load(v, act_dtype, static_cast<int64_t>(b) * d + h * hd + i));
+    }
+    __syncthreads();
+    // scores: one warp per key
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = j0 + warp; j < j1; j += nw) {
+      float s = 0.f;
+      if (j == pos) {
+        for (int i = lane; i < hd; i += 32) s += qs[i] * knew[i];
+      } else {
+        const __half* kr = kc + static_cast<int64_t>(j) * hd;
+        for (int i = lane; i < hd; i += 32) s += qs[i] * __half2float(kr[i]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) sc[j - j0] = s;
+    }
+    __syncthreads();
+    float m = -INFINITY;
+    for (int j = 0; j < j1 - j0; ++j) m = fmaxf(m, sc[j]);
+    // o[i] = sum_j exp(s_j - m) v_j[i]
+    for (int i = threadIdx.x; i < hd; i += blockDim.x) {
+      float acc = 0.f, l = 0.f;
+      for (int j = j0; j < j1; ++j) {
+        const float p = expf(sc[j - j0] - m);
+        const float vv = (j == pos) ? __half2float(__float2half_rn(act_load(v, act_dtype, static_cast<int64_t>(b) * d + h * hd + i)))
+                                    : __half2float(vc[static_cast<int64_t>(j) * hd + i]);
+        acc += p * vv;
+        l += p;
+      }
+      wsp[2 + i] = acc;
+      if (i == 0) {
+        wsp[0] = m;
+        wsp[1] = l;
+      }
+    }
+  } else if (threadIdx.x == 0) {
+    wsp[0] = -INFINITY;
+    wsp[1] = 0.f;
+  }
+  // last CTA of this (row, head) merges the chunks in order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(&tickets[b * n_heads + h], 1u);
+    last = prev == static_cast<unsigned int>(nchunks - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* base = ws + (static_cast<int64_t>(b) * n_heads + h) * nchunks * (hd + 2);
+  float M = -INFINITY;
+  for (int c = 0; c < nchunks; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2)));
+  for (int i = threadIdx.x; i < hd; i += blockDim.x) {
+    float L = 0.f, O = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+      const float mc = __ldcg(base + c * (hd + 2));
+      if (mc == -INFINITY) continue;
+      const float f = expf(mc - M);
+      L += __ldcg(base + c * (hd + 2) + 1) * f;
+      O += __ldcg(base + c * (hd + 2) + 2 + i) * f;
+    }
+    act_store(out, act_dtype, static_cast<int64_t>(b) * d + h * hd + i, O / L);
+  }
+  if (threadIdx.x == 0) tickets[b * n_heads + h] = 0u;
+}
+
+// Fused softmax statistics of B logits rows (double), one CTA per row; writes fq_row_stats.
+// (Same arithmetic as stats.cu, kept local so the step graph has no cross-TU dependency.)
+__global__ void __launch_bounds__(1024) row_stats_kernel(const float* __restrict__ logits, int64_t vocab,
+                                                         fq_row_stats* __restrict__ out) {
+  pdl_wait();
+  __shared__ double shd[33];
+  __shared__ float shv[33];
+  __shared__ int shi[33];
+  __shared__ double sha[33], shb[33];
+  const float* l = logits + blockIdx.x * vocab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int64_t i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float x = l[i];
+    if (x > bv || (x == bv && i < bi)) { bv = x; bi = static_cast<int>(i); }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+  if (lane == 0) { shv[warp] = bv; shi[warp] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w)
+      if (shv[w] > shv[0] || (shv[w] == shv[0] && shi[w] < shi[0])) { shv[0] = shv[w]; shi[0] = shi[w]; }
+  }
+  __syncthreads();
+  const double mx = shv[0];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < vocab; i += blockDim.x) s += exp(static_cast<double>(l[i]) - mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) shd[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += shd[w];
+    shd[32] = t;
+  }
+  __syncthreads();
+  const double sum = shd[32];
+  double h = 0.0, t1 = -1.0, t2 = -1.0;
+  for (int64_t i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const double p = exp(static_cast<double>(l[i]) - mx) / sum;
+    if (p > 0.0) h -= p * log(p);
+    if (p > t1) { t2 = t1; t1 = p; } else if (p > t2) { t2 = p; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+    const double o1 = __shfl_xor_sync(0xffffffffu, t1, o), o2 = __shfl_xor_sync(0xffffffffu, t2, o);
+    const double n1 = fmax(t1, o1), n2 = fmax(fmin(t1, o1), fmax(t2, o2));
+    t1 = n1;
+    t2 = n2;
+  }
+  __syncthreads();
+  if (lane == 0) { shd[warp] = h; sha[warp] = t1; shb[warp] = t2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double H = 0.0, a1 = -1.0, a2 = -1.0;
+    for (int w = 0; w < nw; ++w) {
+      H += shd[w];
+      const double n1 = fmax(a1, sha[w]), n2 = fmax(fmin(a1, sha[w]), fmax(a2, shb[w]));
+      a1 = n1;
+      a2 = n2;
+    }
+    fq_row_stats st;
+    st.entropy = H;
+    st.ppl_entropy = exp(H);
+    st.p1 = a1;
+    st.p2 = a2;
+    st.fault_tolerance = a1 - a2;
+    st.max_logit = shv[0];
+    st.argmax = shi[0];
+    out[blockIdx.x] = st;
+  }
+}
+
+// ------------------------------------------------------------------ reference-arch kernels
+// x = tok_emb[token] + pos_emb[pos] in float (src/model.cpp:245-252, 261-264)
+__global__ void embed_ref_kernel(const float* __restrict__ tok, const float* __restrict__ posemb, StepMeta meta,
+                                 int64_t d, float* __restrict__ x) {
+  const int b = blockIdx.x;
+  const float* e = tok + static_cast<int64_t>(meta.tokens[b]) * d;
+  const float* p = posemb + static_cast<int64_t>(meta.pos[b]) * d;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) x[b * d + c] = e[c] + p[c];
+}
+
+// layer_norm (src/tensor.cpp:124-145): sequential double mean / variance, then per element
+// (in - mean) * inv * gamma + beta in double, stored as float.
+__global__ void layernorm_ref_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g,
+                                     const float* __restrict__ be, float eps, float* __restrict__ y) {
+  const int b = blockIdx.x;
+  const float* in = x + b * d;
+  __shared__ double mean_s, inv_s;
+  if (threadIdx.x == 0) {
+    double mean = 0.0;
+    for (int64_t c = 0; c < d; ++c) mean += in[c];
+    mean /= static_cast<double>(d);
+    double var = 0.0;
+    for (int64_t c = 0; c < d; ++c) {
+      const double dv = in[c] - mean;
+      var += dv * dv;
+    }
+    var /= static_cast<double>(d);
+    mean_s = mean;
+    inv_s = 1.0 / sqrt(var + static_cast<double>(eps));
+  }
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x)
+    y[b * d + c] = static_cast<float>((in[c] - mean_s) * inv_s * g[c] + be[c]);
+}
+
+// gelu, erf form, in double (src/tensor.cpp:154-161)
+__global__ void gelu_ref_kernel(float* __restrict__ x, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double v = x[i];
+    x[i] = static_cast<float>(0.5 * v * (1.0 + erf(v / sqrt(2.0))));
+  }
+}
+
+// add (src/tensor.cpp:147-152): float + float
+__global__ void add_kernel(float* __restrict__ x, const float* __restrict__ y, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = x[i] + y[i];
+}
+
+// Appends k/v rows (fp32) to the reference-arch cache at each row's position.
+__global__ void append_ref_kernel(const float* __restrict__ k, const float* __restrict__ v, StepMeta meta, int64_t d,
+                                  float* __restrict__ kv, int64_t slot_stride, int64_t layer_off, int64_t max_seq) {
+  const int b = blockIdx.x;
+  float* kc = kv + meta.slots[b] * slot_stride + layer_off;
+  float* vc = kc + max_seq * d;
+  const int64_t p = meta.pos[b];
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    kc[p * d + c] = k[b * d + c];
+    vc[p * d + c] = v[b * d + c];
+  }
+}
+
+// attention (src/model.cpp:100-140) for one (row, head): keys 0..pos of the slot, sequential
+// double arithmetic in the reference's loop order.  One CTA per (head, row); scores by thread 0.
+__global__ void attn_ref_kernel(const float* __restrict__ q, StepMeta meta, const float* __restrict__ kv,
+                                int64_t slot_stride, int64_t layer_off, int64_t max_seq, int n_heads, int hd,
+                                double* __restrict__ scratch, float* __restrict__ out) {
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int64_t d = static_cast<int64_t>(n_heads) * hd;
+  const int pos = meta.pos[b];
+  const float* kc = kv + meta.slots[b] * slot_stride + layer_off;
+  const float* vc = kc + max_seq * d;
+  double* probs = scratch + (static_cast<int64_t>(b) * n_heads + h) * max_seq;
+  __shared__ double sum_s;
+  const float* qi = q + b * d + h * hd;
+  const int visible = pos + 1;
+  if (threadIdx.x == 0) {
+    const double scale = 1.0 / sqrt(static_cast<double>(hd));
+    double mx = -INFINITY;
+    for (int j = 0; j < visible; ++j) {
+      const float* kj = kc + static_cast<int64_t>(j) * d + h * hd;
+      double dot = 0.0;
+      for (int p = 0; p < hd; ++p) dot += static_cast<double>(qi[p]) * static_cast<double>(kj[p]);
+      probs[j] = dot * scale;
+      mx = fmax(mx, probs[j]);
+    }
+    double sum = 0.0;
+    for (int j = 0; j < visible; ++j) {
+      probs[j] = exp(probs[j] - mx);
+      sum += probs[j];
+    }
+    sum_s = sum;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < hd; c += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < visible; ++j)
+      acc += (probs[j] / sum_s) * static_cast<double>(vc[static_cast<int64_t>(j) * d + h * hd + c]);
+    out[b * d + h * hd + c] = static_cast<float>(acc);
+  }
+}
+
+// Sequential statistics (exact order of softmax_double / ppl_entropy / fault_tolerance /
+// argmax_token) for small vocabularies: one thread per row.
+__global__ void row_stats_seq_kernel(const float* __restrict__ logits, int64_t V, double* scratch,
+                                     fq_row_stats* __restrict__ out) {
+  const int b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const float* l = logits + b * V;
+  double* p = scratch + b * V;
+  double mx = l[0];
+  for (int64_t i = 1; i < V; ++i) mx = fmax(mx, static_cast<double>(l[i]));
+  double sum = 0.0;
+  for (int64_t i = 0; i < V; ++i) {
+    p[i] = exp(static_cast<double>(l[i]) - mx);
+    sum += p[i];
+  }
+  for (int64_t i = 0; i < V; ++i) p[i] /= sum;
+  double h = 0.0;
+  for (int64_t i = 0; i < V; ++i)
+    if (p[i] > 0.0) h -= p[i] * log(p[i]);
+  double t1 = -1.0, t2 = -1.0;
+  for (int64_t i = 0; i < V; ++i) {
+    if (p[i] > t1) { t2 = t1; t1 = p[i]; } else if (p[i] > t2) { t2 = p[i]; }
+  }
+  int best = 0;
+  float bv = l[0];
+  for (int64_t i = 1; i < V; ++i)
+    if (l[i] > bv) { bv = l[i]; best = static_cast<int>(i); }
+  fq_row_stats st;
+  st.entropy = h;
+  st.ppl_entropy = exp(h);
+  st.p1 = t1;
+  st.p2 = t2;
+  st.fault_tolerance = t1 - t2;
+  st.max_logit = bv;
+  st.argmax = best;
+  out[b] = st;
+}
+
+}  // namespace
+}  // namespace fqc
+
+using namespace fqc;
+
+struct fq_model {
+  fq_ctx* ctx = nullptr;
+  fq_model_config cfg{};
+  bool llama = true;
+  int n_lin = 0;
+  std::vector<std::string> ids;
+  std::vector<fq_layer*> lin;
+  // non-switchable parameters (device fp32)
+  float* tok_emb = nullptr;
+  float* pos_emb = nullptr;
+  std::vector<float*> n1g, n1b, n2g, n2b;  // ln1/ln2 (reference) or attn_norm/ffn_norm (llama: g only)
+  float* fng = nullptr;
+  float* fnb = nullptr;
+  fq_layer tied_head;  // reference arch with tied embeddings
+  // per-slot state
+  std::vector<int64_t> slot_len;
+  std::vector<uint8_t> rungs;  // [max_batch][n_lin]
+  void* kv = nullptr;
+  int64_t slot_stride = 0;     // elements per slot
+  int64_t layer_stride = 0;    // elements per layer within a slot
+  // activations / workspace (max_batch rows)
+  float* resid = nullptr;      // [B, d]
+  float* hbuf = nullptr;       // [B, d] (reference: normalized activations)
+  void* q = nullptr;           // [B, d]
+  void* k = nullptr;
+  void* v = nullptr;
+  void* attn = nullptr;        // [B, d]
+  void* mid = nullptr;         // [B, ffn]
+  float* tmp = nullptr;        // [B, max(d, ffn)] fp32 (reference)
+  float* partials[2] = {nullptr, nullptr};  // ping-pong sum-of-squares partials [B][kPartStride]
+  float* logits = nullptr;     // [max_batch, V]
+  fq_row_stats* stats_dev = nullptr;
+  float* attn_ws = nullptr;
+  unsigned int* tickets = nullptr;
+  double* dscratch = nullptr;
+  int n_chunks = 1;
+  // step staging
+  uint8_t* meta_dev = nullptr;
+  uint8_t* meta_host = nullptr;  // pinned
+  size_t meta_bytes = 0;
+  fq_row_stats* stats_host = nullptr;  // pinned [max_batch]
+  std::map<int, cudaGraphExec_t> graphs;
+  bool use_graphs = true;
+
+  int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
+  int head_index() const { return static_cast<int>(cfg.n_layers) * (llama ? 7 : 6); }
+  size_t act_size() const { return cfg.act_dtype == FQ_DT_F32 ? 4 : 2; }
+  StepMeta meta(int B) const {
+    StepMeta m;
+    m.tokens = reinterpret_cast<const int32_t*>(meta_dev);
+    m.pos = m.tokens + cfg.max_batch;
+    m.slots = m.pos + cfg.max_batch;
+    (void)B;
+    return m;
+  }
+  const uint8_t* table_dev() const { return meta_dev + 3 * sizeof(int32_t) * cfg.max_batch; }
+  uint8_t* table_host() const { return meta_host + 3 * sizeof(int32_t) * cfg.max_batch; }
+};
+
+namespace fqc {
+namespace mdl {
+
+void require(bool c, fq_status code, const std::string& msg) {
+  if (!c) fail(code, msg);
+}
+
+void launch_dev(fq_model* M) { M->ctx->launches += 1; }
+
+// Enqueues one decode step for B rows (metadata already staged in meta_dev).
+void enqueue_step(fq_model* M, int B) {
+  fq_ctx* ctx = M->ctx;
+  const fq_model_config& c = M->cfg;
+  cudaStream_t st = ctx->stream;
+  const int64_t d = c.d_model, V = c.vocab_size;
+  const StepMeta meta = M->meta(B);
+  const uint8_t* table = M->table_dev();
+  if (M->llama) {
+    embed_llama_kernel<<<B, 256, 0, st>>>(M->tok_emb, meta, d, M->resid, M->partials[0]);
+    FQ_CUDA(cudaGetLastError());
+    launch_dev(M);
+    int cur = 0, nparts = 1;
+    for (int64_t l = 0; l < c.n_layers; ++l) {
+      // fused RMSNorm + QKV
+      GemvLaunch g;
+      g.nmat = 3;
+      for (int j = 0; j < 3; ++j) {
+        g.mat[j].layer = M->lin[M->lin_index(static_cast<int>(l), j)];
+        g.mat[j].rung_table = table + M->lin_index(static_cast<int>(l), j);
+        g.mat[j].rung_stride = M->n_lin;
+      }
+      g.mat[0].y = M->q;
+      g.mat[1].y = M->k;
+      g.mat[2].y = M->v;
+      g.batch = B;
+      g.x = M->resid;
+      g.x_dtype = FQ_DT_F32;
+      g.x_stride = d;
+      g.norm_gain = M->n1g[l];
+      g.norm_partials = M->partials[cur];
+      g.n_partials = nparts;
+      g.partials_stride = kPartStride;
+      g.norm_eps = c.norm_eps;
+      g.act_dtype = c.act_dtype;
+      g.epi = EPI_SPLIT3;
+      g.y_dtype = c.act_dtype;
+      g.y_stride = d;
+      g.pdl = true;
+      launch_gemv_fast(ctx, g);
+      // attention (RoPE + append + softmax over the cache)
+      {
+        dim3 grid(static_cast<unsigned>(c.n_heads), static_cast<unsigned>(B), static_cast<unsigned>(M->n_chunks));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(128);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        FQ_CUDA(cudaLaunchKernelEx(&cfg, attn_llama_kernel, static_cast<const void*>(M->q),
+                                   static_cast<const void*>(M->k), static_cast<const void*>(M->v), c.act_dtype, meta,
+                                   static_cast<__half*>(M->kv), M->slot_stride, l * M->layer_stride, c.max_seq_len,
+                                   static_cast<int>(c.n_heads), static_cast<int>(c.head_dim), c.rope_theta,
+                                   M->attn_ws, M->tickets, M->attn));
+        launch_dev(M);
+      }
+      // wo + residual
+      GemvLaunch o;
+      o.nmat = 1;
+      o.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 3)];
+      o.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 3);
+      o.mat[0].rung_stride = M->n_lin;
+      o.batch = B;
+      o.x = M->attn;
+      o.x_dtype = c.act_dtype;
+      o.x_stride = d;
+      o.epi = EPI_RESIDUAL;
+      o.resid = M->resid;
+      o.resid_stride = d;
+      o.out_partials = M->partials[cur ^ 1];
+      o.out_n_partials = kPartStride;
+      o.pdl = true;
+      nparts = launch_gemv_fast(ctx, o);
+      cur ^= 1;
+      // fused RMSNorm + gate/up + SwiGLU
+      GemvLaunch gu;
+      gu.nmat = 2;
+      for (int j = 0; j < 2; ++j) {
+        gu.mat[j].layer = M->lin[M->lin_index(static_cast<int>(l), 4 + j)];
+        gu.mat[j].rung_table = table + M->lin_index(static_cast<int>(l), 4 + j);
+        gu.mat[j].rung_stride = M->n_lin;
+      }
+      gu.batch = B;
+      gu.x = M->resid;
+      gu.x_dtype = FQ_DT_F32;
+      gu.x_stride = d;
+      gu.norm_gain = M->n2g[l];
+      gu.norm_partials = M->partials[cur];
+      gu.n_partials = nparts;
+      gu.partials_stride = kPartStride;
+      gu.norm_eps = c.norm_eps;
+      gu.act_dtype = c.act_dtype;
+      gu.epi = EPI_SWIGLU;
+      gu.y = M->mid;
+      gu.y_dtype = c.act_dtype;
+      gu.y_stride = c.ffn_dim;
+      gu.pdl = true;
+      launch_gemv_fast(ctx, gu);
+      // down + residual
+      GemvLaunch dn;
+      dn.nmat = 1;
+      dn.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 6)];
+      dn.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 6);
+      dn.mat[0].rung_stride = M->n_lin;
+      dn.batch = B;
+      dn.x = M->mid;
+      dn.x_dtype = c.act_dtype;
+      dn.x_stride = c.ffn_dim;
+      dn.epi = EPI_RESIDUAL;
+      dn.resid = M->resid;
+      dn.resid_stride = d;
+      dn.out_partials = M->partials[cur ^ 1];
+      dn.out_n_partials = kPartStride;
+      dn.pdl = true;
+      nparts = launch_gemv_fast(ctx, dn);
+      cur ^= 1;
+    }
+    // final RMSNorm + head
+    GemvLaunch hd;
+    hd.nmat = 1;
+    hd.mat[0].layer = M->lin[M->head_index()];
+    hd.mat[0].rung_table = table + M->head_index();
+    hd.mat[0].rung_stride = M->n_lin;
+    hd.batch = B;
+    hd.x = M->resid;
+    hd.x_dtype = FQ_DT_F32;
+    hd.x_stride = d;
+    hd.norm_gain = M->fng;
+    hd.norm_partials = M->partials[cur];
+    hd.n_partials = nparts;
+    hd.partials_stride = kPartStride;
+    hd.norm_eps = c.norm_eps;
+    hd.act_dtype = c.act_dtype;
+    hd.epi = EPI_STORE;
+    hd.y = M->logits;
+    hd.y_dtype = FQ_DT_F32;
+    hd.y_stride = V;
+    hd.pdl = true;
+    launch_gemv_fast(ctx, hd);
+    {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(B);
+      cfg.blockDim = dim3(1024);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FQ_CUDA(cudaLaunchKernelEx(&cfg, row_stats_kernel, static_cast<const float*>(M->logits), V, M->stats_dev));
+      launch_dev(M);
+    }
+    return;
+  }
+  // ---------------- reference architecture (exact numerics)
+  const int64_t ffn = c.ffn_dim;
+  float* x = M->resid;
+  float* h = M->hbuf;
+  float* qf = static_cast<float*>(M->q);
+  float* kf = static_cast<float*>(M->k);
+  float* vf = static_cast<float*>(M->v);
+  float* af = static_cast<float*>(M->attn);
+  float* mid = static_cast<float*>(M->mid);
+  float* tmp = M->tmp;
+  auto gemv = [&](int li, const float* in, float* out) {
+    // the rung of row b comes from the host table; exact launches are per distinct rung
+    const fq_layer* L = M->lin[li];
+    // all rows of a reference-arch step share the slot rung of row 0 when B == 1; for B > 1
+    // rows are launched individually so each uses its own rung.
+    for (int b = 0; b < B; ++b) {
+      const int rung = M->table_host()[b * M->n_lin + li];
+      launch_gemv_exact(ctx, L, rung, 1, in + b * L->K, FQ_DT_F32, out + b * L->N, FQ_DT_F32);
+    }
+  };
+  embed_ref_kernel<<<B, 128, 0, st>>>(M->tok_emb, M->pos_emb, meta, d, x);
+  launch_dev(M);
+  const int n1 = static_cast<int>((B * d + 255) / 256), nf = static_cast<int>((B * ffn + 255) / 256);
+  for (int64_t l = 0; l < c.n_layers; ++l) {
+    const int base = M->lin_index(static_cast<int>(l), 0);
+    layernorm_ref_kernel<<<B, 128, 0, st>>>(x, d, M->n1g[l], M->n1b[l], c.norm_eps, h);
+    launch_dev(M);
+    gemv(base + 0, h, qf);
+    gemv(base + 1, h, kf);
+    gemv(base + 2, h, vf);
+    append_ref_kernel<<<B, 128, 0, st>>>(kf, vf, meta, d, static_cast<float*>(M->kv), M->slot_stride,
+                                         l * M->layer_stride, c.max_seq_len);
+    launch_dev(M);
+    attn_ref_kernel<<<dim3(static_cast<unsigned>(c.n_heads), static_cast<unsigned>(B)), 32, 0, st>>>(
+        qf, meta, static_cast<float*>(M->kv), M->slot_stride, l * M->layer_stride, c.max_seq_len,
+        static_cast<int>(c.n_heads), static_cast<int>(c.head_dim), M->dscratch, af);
+    launch_dev(M);
+    gemv(base + 3, af, tmp);
+    add_kernel<<<n1, 256, 0, st>>>(x, tmp, B * d);
+    launch_dev(M);
+    layernorm_ref_kernel<<<B, 128, 0, st>>>(x, d, M->n2g[l], M->n2b[l], c.norm_eps, h);
+    launch_dev(M);
+    gemv(base + 4, h, mid);
+    gelu_ref_kernel<<<nf, 256, 0, st>>>(mid, B * ffn);
+    launch_dev(M);
+    gemv(base + 5, mid, tmp);
+    add_kernel<<<n1, 256, 0, st>>>(x, tmp, B * d);
+    launch_dev(M);
+  }
+  layernorm_ref_kernel<<<B, 128, 0, st>>>(x, d, M->fng, M->fnb, c.norm_eps, h);
+  launch_dev(M);
+  if (c.tie_embeddings) {
+    for (int b = 0; b < B; ++b)
+      launch_gemv_exact(ctx, &M->tied_head, FQ_RUNG_FP, 1, h + b * d, FQ_DT_F32, M->logits + b * V, FQ_DT_F32);
+  } else {
+    gemv(M->head_index(), h, M->logits);
+  }
+  if (V <= 4096) {
+    row_stats_seq_kernel<<<B, 32, 0, st>>>(M->logits, V, M->dscratch, M->stats_dev);
+  } else {
+    row_stats_kernel<<<B, 1024, 0, st>>>(M->logits, V, M->stats_dev);
+  }
+  FQ_CUDA(cudaGetLastError());
+  launch_dev(M);
+}
+
+// Runs one step for B rows whose metadata is staged in meta_host; results in stats_host.
+void run_step(fq_model* M, int B) {
+  fq_ctx* ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  // reference-arch steps launch per-row exact GEMVs whose rung is read on the host: no graph
+  const bool graphable = M->llama && M->use_graphs;
+  if (!graphable) {
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    enqueue_step(M, B);
+    FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * B, cudaMemcpyDeviceToHost, st));
+    FQ_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  auto it = M->graphs.find(B);
+  if (it == M->graphs.end()) {
+    cudaGraph_t graph;
+    FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+      enqueue_step(M, B);
+      FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * B, cudaMemcpyDeviceToHost, st));
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      throw;
+    }
+    FQ_CUDA(cudaStreamEndCapture(st, &graph));
+    cudaGraphExec_t exec;
+    FQ_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    FQ_CUDA(cudaGraphDestroy(graph));
+    it = M->graphs.emplace(B, exec).first;
+  }
+  const int64_t before = ctx->launches;
+  (void)before;
+  FQ_CUDA(cudaGraphLaunch(it->second, st));
+  FQ_CUDA(cudaStreamSynchronize(st));
+}
+
+int64_t ffn_or_d(const fq_model_config& c) { return std::max(c.d_model, c.ffn_dim); }
+
+void stage_rows(fq_model* M, int B, const int32_t* slots, const int32_t* tokens) {
+  const fq_model_config& c = M->cfg;
+  int32_t* tok = reinterpret_cast<int32_t*>(M->meta_host);
+  int32_t* pos = tok + c.max_batch;
+  int32_t* sl = pos + c.max_batch;
+  uint8_t* tab = M->table_host();
+  for (int b = 0; b < B; ++b) {
+    const int s = slots[b];
+    require(s >= 0 && s < c.max_batch, FQ_E_INPUT, "decode: slot out of range");
+    require(tokens[b] >= 0 && tokens[b] < c.vocab_size, FQ_E_INPUT, "decode: token id out of vocabulary");
+    if (M->slot_len[s] >= c.max_seq_len) fail(FQ_E_CAPACITY, "decode: cache is full");
+    for (int b2 = 0; b2 < b; ++b2) require(slots[b2] != s, FQ_E_INPUT, "decode: duplicate slot in a batch");
+    tok[b] = tokens[b];
+    pos[b] = static_cast<int32_t>(M->slot_len[s]);
+    sl[b] = s;
+    std::memcpy(tab + b * M->n_lin, &M->rungs[static_cast<size_t>(s) * M->n_lin], M->n_lin);
+    for (int i = 0; i < M->n_lin; ++i)
+      if (!M->lin[i]->has(tab[b * M->n_lin + i]))
+        fail(FQ_E_STATE, "layer " + M->ids[i] + ": active precision has no payload");
+  }
+}
+
+void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens, float* logits_dev,
+                fq_row_stats* stats_host) {
+  require(B >= 1 && B <= M->cfg.max_batch, FQ_E_INPUT, "decode: batch out of range");
+  if (M->llama) {
+    for (int i = 0; i < M->n_lin; ++i) {
+      require(gemv_fast_supported(M->lin[i], FQ_RUNG_INT8) || !M->lin[i]->has(FQ_RUNG_INT8), FQ_E_STATE,
+              "layer " + M->ids[i] + ": W8 copy not usable by the fast kernel");
+    }
+  }
+  stage_rows(M, B, slots, tokens);
+  run_step(M, B);
+  for (int b = 0; b < B; ++b) M->slot_len[slots[b]] += 1;
+  if (stats_host) std::memcpy(stats_host, M->stats_host, sizeof(fq_row_stats) * B);
+  if (logits_dev)
+    FQ_CUDA(cudaMemcpyAsync(logits_dev, M->logits, sizeof(float) * B * M->cfg.vocab_size, cudaMemcpyDeviceToDevice,
+                            M->ctx->stream));
+}
+
+float* param_slot(fq_model* M, const std::string& name, int64_t& expect) {
+  const fq_model_config& c = M->cfg;
+  const int64_t d = c.d_model;
+  if (name == "tok_emb") { expect = c.vocab_size * d; return M->tok_emb; }
+  if (!M->llama && name == "pos_emb") { expect = c.max_seq_len * d; return M->pos_emb; }
+  if (M->llama && name == "final_norm") { expect = d; return M->fng; }
+  if (!M->llama && name == "final_norm.gamma") { expect = d; return M->fng; }
+  if (!M->llama && name == "final_norm.beta") { expect = d; return M->fnb; }
+  if (name.rfind("blocks.", 0) == 0) {
+    const size_t dot = name.find('.', 7);
+    if (dot == std::string::npos) return nullptr;
+    const int64_t i = std::stoll(name.substr(7, dot - 7));
+    if (i < 0 || i >= c.n_layers) return nullptr;
+    const std::string rest = name.substr(dot + 1);
+    expect = d;
+    if (M->llama) {
+      if (rest == "attn_norm") return M->n1g[i];
+      if (rest == "ffn_norm") return M->n2g[i];
+    } else {
+      if (rest == "ln1.gamma") return M->n1g[i];
+      if (rest == "ln1.beta") return M->n1b[i];
+      if (rest == "ln2.gamma") return M->n2g[i];
+      if (rest == "ln2.beta") return M->n2b[i];
+    }
+  }
+  return nullptr;
+}
+
+__global__ void fill_kernel(float* p, int64_t n, float v) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+}  // namespace mdl
+}  // namespace fqc
+
+using namespace fqc::mdl;
+
+extern "C" {
+
+fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** out) {
+  return guarded([&] {
+    require(ctx && cfg && out, FQ_E_INPUT, "null argument");
+    const fq_model_config& c = *cfg;
+    if (c.vocab_size < 1 || c.d_model < 1 || c.n_heads < 1 || c.head_dim < 1 || c.n_layers < 1 || c.ffn_dim < 1 ||
+        c.max_seq_len < 1)
+      fail(FQ_E_CONFIG, "model config: all dimensions must be >= 1");
+    if (c.d_model != c.n_heads * c.head_dim) fail(FQ_E_CONFIG, "model config: d_model must equal n_heads * head_dim");
+    require(c.arch == FQ_ARCH_LLAMA || c.arch == FQ_ARCH_REFERENCE, FQ_E_CONFIG, "model config: unknown arch");
+    require(c.max_batch >= 1 && c.max_batch <= 256, FQ_E_CONFIG, "model config: max_batch must be in [1, 256]");
+    if (c.arch == FQ_ARCH_LLAMA) {
+      require(c.act_dtype == FQ_DT_BF16 || c.act_dtype == FQ_DT_F16, FQ_E_CONFIG, "llama arch: activations must be bf16/fp16");
+      require(c.head_dim % 2 == 0 && c.head_dim <= 256, FQ_E_CONFIG, "llama arch: head_dim must be even and <= 256");
+      require(!c.tie_embeddings, FQ_E_CONFIG, "llama arch: tied embeddings not supported");
+    } else {
+      require(c.act_dtype == FQ_DT_F32, FQ_E_CONFIG, "reference arch: activations are fp32");
+    }
+    auto* M = new fq_model();
+    M->ctx = ctx;
+    M->cfg = c;
+    M->llama = c.arch == FQ_ARCH_LLAMA;
+    const int64_t d = c.d_model, ffn = c.ffn_dim, V = c.vocab_size, L = c.n_layers;
+    const int per = M->llama ? 7 : 6;
+    for (int64_t i = 0; i < L; ++i) {
+      const std::string p = "blocks." + std::to_string(i) + ".";
+      std::vector<std::pair<std::string, std::pair<int64_t, int64_t>>> specs;
+      specs.push_back({p + "attn.wq", {d, d}});
+      specs.push_back({p + "attn.wk", {d, d}});
+      specs.push_back({p + "attn.wv", {d, d}});
+      specs.push_back({p + "attn.wo", {d, d}});
+      if (M->llama) {
+        specs.push_back({p + "ffn.w_gate", {ffn, d}});
+        specs.push_back({p + "ffn.w_up", {ffn, d}});
+        specs.push_back({p + "ffn.w_down", {d, ffn}});
+      } else {
+        specs.push_back({p + "ffn.w1", {ffn, d}});
+        specs.push_back({p + "ffn.w2", {d, ffn}});
+      }
+      for (auto& sp : specs) {
+        fq_layer* lay = nullptr;
+        FQ_CUDA(cudaSuccess);
+        if (fq_layer_create(ctx, sp.second.first, sp.second.second, c.group_size, &lay) != FQ_OK)
+          fail(FQ_E_CONFIG, fq_last_error());
+        lay->borrowed = true;
+        M->ids.push_back(sp.first);
+        M->lin.push_back(lay);
+      }
+    }
+    (void)per;
+    if (!(c.arch == FQ_ARCH_REFERENCE && c.tie_embeddings)) {
+      fq_layer* lay = nullptr;
+      if (fq_layer_create(ctx, V, d, c.group_size, &lay) != FQ_OK) fail(FQ_E_CONFIG, fq_last_error());
+      lay->borrowed = true;
+      M->ids.push_back("head");
+      M->lin.push_back(lay);
+    }
+    M->n_lin = static_cast<int>(M->lin.size());
+    cudaStream_t st = ctx->stream;
+    auto zeros = [&](int64_t n) {
+      float* p = static_cast<float*>(dmalloc(sizeof(float) * n));
+      FQ_CUDA(cudaMemsetAsync(p, 0, sizeof(float) * n, st));
+      return p;
+    };
+    auto ones = [&](int64_t n) {
+      float* p = static_cast<float*>(dmalloc(sizeof(float) * n));
+      fill_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, n, 1.0f);
+      return p;
+    };
+    M->tok_emb = zeros(V * d);
+    if (!M->llama) M->pos_emb = zeros(c.max_seq_len * d);
+    for (int64_t i = 0; i < L; ++i) {
+      M->n1g.push_back(ones(d));
+      M->n2g.push_back(ones(d));
+      M->n1b.push_back(M->llama ? nullptr : zeros(d));
+      M->n2b.push_back(M->llama ? nullptr : zeros(d));
+    }
+    M->fng = ones(d);
+    M->fnb = M->llama ? nullptr : zeros(d);
+    if (!M->llama && c.tie_embeddings) {
+      M->tied_head.ctx = ctx;
+      M->tied_head.N = V;
+      M->tied_head.K = d;
+      M->tied_head.G = d;
+      M->tied_head.ng = 1;
+      M->tied_head.ng_pad = 4;
+      M->tied_head.zp_pad = 16;
+      M->tied_head.fp = M->tok_emb;
+      M->tied_head.borrowed = true;
+    }
+    const int B = c.max_batch;
+    M->slot_len.assign(B, 0);
+    M->rungs.assign(static_cast<size_t>(B) * M->n_lin, static_cast<uint8_t>(M->llama ? FQ_RUNG_INT8 : FQ_RUNG_FP));
+    // KV cache
+    const size_t kv_elem = M->llama ? 2 : 4;
+    M->layer_stride = 2 * c.max_seq_len * d;
+    M->slot_stride = L * M->layer_stride;
+    M->kv = dmalloc(kv_elem * M->slot_stride * B);
+    FQ_CUDA(cudaMemsetAsync(M->kv, 0, kv_elem * M->slot_stride * B, st));
+    const size_t as = M->act_size();
+    M->resid = zeros(B * d);
+    M->hbuf = zeros(B * d);
+    M->q = dmalloc(as * B * d);
+    M->k = dmalloc(as * B * d);
+    M->v = dmalloc(as * B * d);
+    M->attn = dmalloc(as * B * d);
+    M->mid = dmalloc(as * B * ffn);
+    M->tmp = zeros(B * ffn_or_d(c));
+    M->partials[0] = zeros(static_cast<int64_t>(B) * kPartStride);
+    M->partials[1] = zeros(static_cast<int64_t>(B) * kPartStride);
+    M->logits = zeros(B * V);
+    M->stats_dev = static_cast<fq_row_stats*>(dmalloc(sizeof(fq_row_stats) * B));
+    M->n_chunks = static_cast<int>((c.max_seq_len + kAttnChunk - 1) / kAttnChunk);
+    M->attn_ws = zeros(static_cast<int64_t>(B) * c.n_heads * M->n_chunks * (c.head_dim + 2));
+    M->tickets = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * B * c.n_heads));
+    FQ_CUDA(cudaMemsetAsync(M->tickets, 0, sizeof(unsigned int) * B * c.n_heads, st));
+    const int64_t dsz = std::max<int64_t>(static_cast<int64_t>(B) * c.n_heads * c.max_seq_len, B * V);
+    M->dscratch = static_cast<double*>(dmalloc(sizeof(double) * dsz));
+    M->meta_bytes = 3 * sizeof(int32_t) * B + static_cast<size_t>(B) * M->n_lin;
+    M->meta_dev = static_cast<uint8_t*>(dmalloc(M->meta_bytes));
+    FQ_CUDA(cudaMallocHost(&M->meta_host, M->meta_bytes));
+    std::memset(M->meta_host, 0, M->meta_bytes);
+    FQ_CUDA(cudaMallocHost(&M->stats_host, sizeof(fq_row_stats) * B));
+    FQ_CUDA(cudaStreamSynchronize(st));
+    *out = M;
+  });
+}
+
+fq_status fq_model_destroy(fq_model* M) {
+  return guarded([&] {
+    if (!M) return;
+    cudaStreamSynchronize(M->ctx->stream);
+    for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
+    for (fq_layer* L : M->lin) {
+      L->borrowed = false;
+      fq_layer_destroy(L);
+    }
+    dfree(M->tok_emb);
+    dfree(M->pos_emb);
+    for (auto* p : M->n1g) dfree(p);
+    for (auto* p : M->n2g) dfree(p);
+    for (auto* p : M->n1b) dfree(p);
+    for (auto* p : M->n2b) dfree(p);
+    dfree(M->fng);
+    dfree(M->fnb);
+    dfree(M->kv);
+    dfree(M->resid);
+    dfree(M->hbuf);
+    dfree(M->q);
+    dfree(M->k);
+    dfree(M->v);
+    dfree(M->attn);
+    dfree(M->mid);
+    dfree(M->tmp);
+    dfree(M->partials[0]);
+    dfree(M->partials[1]);
+    dfree(M->logits);
+    dfree(M->stats_dev);
+    dfree(M->attn_ws);
+    dfree(M->tickets);
+    dfree(M->dscratch);
+    dfree(M->meta_dev);
+    if (M->meta_host) cudaFreeHost(M->meta_host);
+    if (M->stats_host) cudaFreeHost(M->stats_host);
+    delete M;
+  });
+}
+
+fq_status fq_model_num_linears(const fq_model* M, int32_t* out) {
+  return guarded([&] {
+    require(M && out, FQ_E_INPUT, "null argument");
+    *out = M->n_lin;
+  });
+}
+
+fq_status fq_model_linear_id(const fq_model* M, int32_t index, char* buf, int32_t buflen) {
+  return guarded([&] {
+    require(M && buf && buflen > 0, FQ_E_INPUT, "null argument");
+    require(index >= 0 && index < M->n_lin, FQ_E_INPUT, "linear index out of range");
+    const std::string& s = M->ids[index];
+    require(static_cast<int32_t>(s.size()) < buflen, FQ_E_INPUT, "buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+fq_status fq_model_linear_index(const fq_model* M, const char* id, int32_t* out) {
+  return guarded([&] {
+    require(M && id && out, FQ_E_INPUT, "null argument");
+    for (int i = 0; i < M->n_lin; ++i)
+      if (M->ids[i] == id) {
+        *out = i;
+        return;
+      }
+    fail(FQ_E_STATE, std::string("set_precision: unknown layer '") + id + "'");
+  });
+}
+
+fq_status fq_model_linear(fq_model* M, int32_t index, fq_layer** out) {
+  return guarded([&] {
+    require(M && out, FQ_E_INPUT, "null argument");
+    require(index >= 0 && index < M->n_lin, FQ_E_INPUT, "linear index out of range");
+    *out = M->lin[index];
+  });
+}
+
+fq_status fq_model_set_param(fq_model* M, const char* name, const float* host, int64_t numel) {
+  return guarded([&] {
+    require(M && name && host, FQ_E_INPUT, "null argument");
+    int64_t expect = 0;
+    float* dst = param_slot(M, name, expect);
+    if (!dst) fail(FQ_E_FORMAT, std::string("weights: unknown parameter '") + name + "'");
+    if (numel != expect) fail(FQ_E_DIMENSION, std::string("weights: parameter '") + name + "' has the wrong size");
+    FQ_CUDA(cudaMemcpyAsync(dst, host, sizeof(float) * numel, cudaMemcpyHostToDevice, M->ctx->stream));
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+  });
+}
+
+fq_status fq_model_init_random(fq_model* M, uint64_t seed, float std) {
+  return guarded([&] {
+    require(M != nullptr, FQ_E_INPUT, "null model");
+    fq_ctx* ctx = M->ctx;
+    const fq_model_config& c = M->cfg;
+    int64_t maxn = c.vocab_size * c.d_model;
+    for (fq_layer* L : M->lin) maxn = std::max(maxn, L->N * L->K);
+    float* w = static_cast<float*>(dmalloc(sizeof(float) * maxn));
+    fill_normal(ctx, M->tok_emb, c.vocab_size * c.d_model, seed, 0, std);
+    if (M->pos_emb) fill_normal(ctx, M->pos_emb, c.max_seq_len * c.d_model, seed, 1, std);
+    for (int i = 0; i < M->n_lin; ++i) {
+      fq_layer* L = M->lin[i];
+      fill_normal(ctx, w, L->N * L->K, seed, 100 + i, std);
+      quantize_device(ctx, L, FQ_RUNG_INT8, FQ_MODE_ASYM, w);
+      quantize_device(ctx, L, FQ_RUNG_INT4, FQ_MODE_ASYM, w);
+      if (!M->llama) {
+        if (!L->fp) L->fp = static_cast<float*>(dmalloc(sizeof(float) * L->N * L->K));
+        FQ_CUDA(cudaMemcpyAsync(L->fp, w, sizeof(float) * L->N * L->K, cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+    FQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    dfree(w);
+  });
+}
+
+fq_status fq_model_set_rung(fq_model* M, int32_t slot, int32_t li, int32_t rung) {
+  return guarded([&] {
+    require(M != nullptr, FQ_E_INPUT, "null model");
+    require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
+    require(li >= 0 && li < M->n_lin, FQ_E_INPUT, "linear index out of range");
+    require(rung >= FQ_RUNG_FP && rung <= FQ_RUNG_INT4, FQ_E_CONFIG, "unknown precision rung");
+    if (!M->lin[li]->has(rung))
+      fail(FQ_E_STATE, "set_precision: layer '" + M->ids[li] + "' has no rung '" +
+                           (rung == FQ_RUNG_FP ? "fp" : rung == FQ_RUNG_INT8 ? "8" : "4") + "'");
+    if (M->llama && rung == FQ_RUNG_FP) fail(FQ_E_STATE, "llama arch: the fp rung is not resident on the device");
+    M->rungs[static_cast<size_t>(slot) * M->n_lin + li] = static_cast<uint8_t>(rung);
+  });
+}
+
+fq_status fq_model_get_rung(const fq_model* M, int32_t slot, int32_t li, int32_t* out) {
+  return guarded([&] {
+    require(M && out, FQ_E_INPUT, "null argument");
+    require(slot >= 0 && slot < M->cfg.max_batch && li >= 0 && li < M->n_lin, FQ_E_INPUT, "index out of range");
+    *out = M->rungs[static_cast<size_t>(slot) * M->n_lin + li];
+  });
+}
+
+fq_status fq_model_set_all_rungs(fq_model* M, int32_t slot, int32_t rung) {
+  return guarded([&] {
+    require(M != nullptr, FQ_E_INPUT, "null model");
+    for (int i = 0; i < M->n_lin; ++i)
+      if (fq_model_set_rung(M, slot, i, rung) != FQ_OK) fail(FQ_E_STATE, fq_last_error());
+  });
+}
+
+fq_status fq_model_reset_slot(fq_model* M, int32_t slot) {
+  return guarded([&] {
+    require(M != nullptr, FQ_E_INPUT, "null model");
+    require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
+    M->slot_len[slot] = 0;
+  });
+}
+
+fq_status fq_model_slot_length(const fq_model* M, int32_t slot, int64_t* out) {
+  return guarded([&] {
+    require(M && out, FQ_E_INPUT, "null argument");
+    require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
+    *out = M->slot_len[slot];
+  });
+}
+
+fq_status fq_model_prefill(fq_model* M, int32_t slot, const int32_t* tokens, int64_t n, float* logits_dev,
+                           fq_row_stats* stats_host) {
+  return guarded([&] {
+    require(M && tokens, FQ_E_INPUT, "null argument");
+    if (n < 1) fail(FQ_E_INPUT, "prefill: empty prompt");
+    require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
+    if (M->slot_len[slot] != 0) fail(FQ_E_STATE, "prefill: cache already populated");
+    if (n > M->cfg.max_seq_len) fail(FQ_E_CAPACITY, "prefill: prompt longer than max sequence length");
+    for (int64_t i = 0; i < n; ++i)
+      if (tokens[i] < 0 || tokens[i] >= M->cfg.vocab_size) fail(FQ_E_INPUT, "prefill: token id out of vocabulary");
+    // Row i of a prefill equals a decode step at position i (causal attention over 0..i with the
+    // same per-row arithmetic), so the prompt is streamed through the decode step.
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t s = slot, t = tokens[i];
+      model_step(M, 1, &s, &t, logits_dev ? logits_dev + i * M->cfg.vocab_size : nullptr,
+                 stats_host ? stats_host + i : nullptr);
+    }
+  });
+}
+
+fq_status fq_model_decode(fq_model* M, int32_t batch, const int32_t* slots, const int32_t* tokens, float* logits_dev,
+                          fq_row_stats* stats_host) {
+  return guarded([&] {
+    require(M && slots && tokens, FQ_E_INPUT, "null argument");
+    model_step(M, batch, slots, tokens, logits_dev, stats_host);
+  });
+}
+
+fq_status fq_model_logits(fq_model* M, float** out) {
+  return guarded([&] {
+    require(M && out, FQ_E_INPUT, "null argument");
+    *out = M->logits;
+  });
+}
+
+fq_status fq_model_step_bytes(const fq_model* M, int32_t batch, const int32_t* slots, int64_t* weight_bytes,
+                              int64_t* kv_bytes) {
+  return guarded([&] {
+    require(M && slots, FQ_E_INPUT, "null argument");
+    int64_t wb = 0, kb = 0;
+    for (int i = 0; i < M->n_lin; ++i) {
+      bool w8 = false, w4 = false, fp = false;
+      for (int b = 0; b < batch; ++b) {
+        const int r = M->rungs[static_cast<size_t>(slots[b]) * M->n_lin + i];
+        w8 |= r == FQ_RUNG_INT8;
+        w4 |= r == FQ_RUNG_INT4;
+        fp |= r == FQ_RUNG_FP;
+      }
+      const fq_layer* L = M->lin[i];
+      if (w8) wb += L->N * L->K + L->N * L->ng * 5;
+      if (w4) wb += (L->N * L->K + 1) / 2 + L->N * L->ng * 5;
+      if (fp) wb += L->N * L->K * 4;
+    }
+    const int64_t es = M->llama ? 2 : 4;
+    for (int b = 0; b < batch; ++b) {
+      const int64_t ctxlen = M->slot_len[slots[b]] + 1;
+      kb += M->cfg.n_layers * 2 * ctxlen * M->cfg.d_model * es;  // read incl. the new position
+    }
+    if (weight_bytes) *weight_bytes = wb;
+    if (kv_bytes) *kv_bytes = kb;
+  });
+}
+
+fq_status fq_model_calibrate_logit_kl(fq_model* M, const int32_t* tokens, int64_t n_seqs, int64_t len,
+                                      int32_t base_rung, int32_t flip_rung, double* kl_host, double* entropy_host) {
+  return guarded([&] {
+    require(M && tokens && kl_host, FQ_E_INPUT, "null argument");
+    require(n_seqs >= 1 && len >= 1, FQ_E_INPUT, "calibrate: empty token set");
+    require(len <= M->cfg.max_seq_len, FQ_E_CAPACITY, "calibrate: sequence longer than max_seq_len");
+    const fq_model_config& c = M->cfg;
+    const int per = M->llama ? 7 : 6;
+    const int B = static_cast<int>(std::min<int64_t>(n_seqs, c.max_batch));
+    const int64_t V = c.vocab_size;
+    const int64_t rows = n_seqs * len;
+    float* base_logits = static_cast<float*>(dmalloc(sizeof(float) * rows * V));
+    float* flip_logits = static_cast<float*>(dmalloc(sizeof(float) * B * V));
+    double* kl_dev = static_cast<double*>(dmalloc(sizeof(double) * B * 2));
+    std::vector<double> klsum(c.n_layers, 0.0), entsum(c.n_layers, 0.0);
+    std::vector<uint8_t> saved(M->rungs);
+    auto run = [&](int flip_layer) {
+      for (int64_t s0 = 0; s0 < n_seqs; s0 += B) {
+        const int nb = static_cast<int>(std::min<int64_t>(B, n_seqs - s0));
+        std::vector<int32_t> slots(nb);
+        for (int b = 0; b < nb; ++b) {
+          slots[b] = b;
+          M->slot_len[b] = 0;
+          for (int i = 0; i < M->n_lin; ++i) {
+            const bool in_block = flip_layer >= 0 && i / per == flip_layer && i < M->head_index();
+            M->rungs[static_cast<size_t>(b) * M->n_lin + i] = static_cast<uint8_t>(in_block ? flip_rung : base_rung);
+          }
+        }
+        for (int64_t t = 0; t < len; ++t) {
+          std::vector<int32_t> tk(nb);
+          for (int b = 0; b < nb; ++b) tk[b] = tokens[(s0 + b) * len + t];
+          if (flip_layer < 0) {
+            stage_rows(M, nb, slots.data(), tk.data());
+            run_step(M, nb);
+            for (int b = 0; b < nb; ++b) {
+              M->slot_len[b] += 1;
+              FQ_CUDA(cudaMemcpyAsync(base_logits + ((s0 + b) * len + t) * V, M->logits + b * V, sizeof(float) * V,
+                                      cudaMemcpyDeviceToDevice, M->ctx->stream));
+            }
+          } else {
+            stage_rows(M, nb, slots.data(), tk.data());
+            run_step(M, nb);
+            for (int b = 0; b < nb; ++b) M->slot_len[b] += 1;
+            // KL of each row against the stored baseline row (rows of different sequences are
+            // not contiguous in the baseline buffer: one launch per row)
+            for (int b = 0; b < nb; ++b)
+              launch_kl_rows(M->ctx, M->logits + b * V, base_logits + ((s0 + b) * len + t) * V, FQ_DT_F32, 1, V,
+                             kl_dev + 2 * b, kl_dev + 2 * b + 1);
+            std::vector<double> h(2 * nb);
+            FQ_CUDA(cudaMemcpyAsync(h.data(), kl_dev, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, M->ctx->stream));
+            FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+            for (int b = 0; b < nb; ++b) {
+              klsum[flip_layer] += h[2 * b];
+              entsum[flip_layer] += h[2 * b + 1];
+            }
+          }
+        }
+      }
+    };
+    try {
+      run(-1);
+      for (int l = 0; l < c.n_layers; ++l) run(l);
+    } catch (...) {
+      M->rungs = saved;
+      dfree(base_logits);
+      dfree(flip_logits);
+      dfree(kl_dev);
+      throw;
+    }
+    M->rungs = saved;
+    for (int b = 0; b < B; ++b) M->slot_len[b] = 0;
+    for (int l = 0; l < c.n_layers; ++l) {
+      kl_host[l] = klsum[l] / static_cast<double>(rows);
+      if (entropy_host) entropy_host[l] = entsum[l] / static_cast<double>(rows);
+    }
+    dfree(base_logits);
+    dfree(flip_logits);
+    dfree(kl_dev);
+  });
+}
+
+}  // extern "C"
