@@ -297,3 +297,122 @@ class Layer:
             self.close()
         except Exception:
             pass
+
+
+_CFG_KEYS = ["arch", "act_dtype", "vocab_size", "d_model", "n_heads", "head_dim", "n_layers", "ffn_dim",
+             "max_seq_len", "tie_embeddings", "max_batch", "group_size", "norm_eps", "rope_theta"]
+
+
+def model_config(**kw) -> ModelConfig:
+    c = ModelConfig()
+    c.arch = kw.get("arch", ARCH_LLAMA)
+    c.act_dtype = kw.get("act_dtype", DT_BF16 if c.arch == ARCH_LLAMA else DT_F32)
+    for k in ["vocab_size", "d_model", "n_heads", "head_dim", "n_layers", "ffn_dim", "max_seq_len"]:
+        setattr(c, k, int(kw[k]))
+    c.tie_embeddings = int(kw.get("tie_embeddings", 0))
+    c.max_batch = int(kw.get("max_batch", 1))
+    c.group_size = int(kw.get("group_size", 128))
+    c.norm_eps = float(kw.get("norm_eps", 1e-5))
+    c.rope_theta = float(kw.get("rope_theta", 10000.0))
+    return c
+
+
+class Model:
+    """fq_model: the device-resident decoder (precision table, KV caches, decode step)."""
+
+    def __init__(self, ctx: Context, **cfg):
+        self.ctx = ctx
+        self.L = ctx.L
+        self.cfg = model_config(**cfg)
+        h = C.c_void_p()
+        check(self.L.fq_model_create(ctx.h, C.byref(self.cfg), C.byref(h)))
+        self.h = h
+        n = C.c_int32()
+        check(self.L.fq_model_num_linears(h, C.byref(n)))
+        self.n_linears = n.value
+        self.ids = []
+        buf = C.create_string_buffer(256)
+        for i in range(self.n_linears):
+            check(self.L.fq_model_linear_id(h, i, buf, 256))
+            self.ids.append(buf.value.decode())
+        self.V = self.cfg.vocab_size
+
+    def linear(self, i: int) -> Layer:
+        lh = C.c_void_p()
+        check(self.L.fq_model_linear(self.h, i, C.byref(lh)))
+        return Layer(self.ctx, 0, 0, handle=lh)
+
+    def linear_index(self, layer_id: str) -> int:
+        o = C.c_int32()
+        check(self.L.fq_model_linear_index(self.h, layer_id.encode(), C.byref(o)))
+        return o.value
+
+    def set_param(self, name: str, arr: np.ndarray) -> None:
+        a = np.ascontiguousarray(arr, np.float32)
+        check(self.L.fq_model_set_param(self.h, name.encode(), _ptr(a), a.size))
+
+    def init_random(self, seed: int, std: float = 0.02) -> None:
+        check(self.L.fq_model_init_random(self.h, seed, std))
+
+    def set_rung(self, slot: int, index: int, rung: int) -> None:
+        check(self.L.fq_model_set_rung(self.h, slot, index, rung))
+
+    def get_rung(self, slot: int, index: int) -> int:
+        o = C.c_int32()
+        check(self.L.fq_model_get_rung(self.h, slot, index, C.byref(o)))
+        return o.value
+
+    def set_all_rungs(self, slot: int, rung: int) -> None:
+        check(self.L.fq_model_set_all_rungs(self.h, slot, rung))
+
+    def reset_slot(self, slot: int) -> None:
+        check(self.L.fq_model_reset_slot(self.h, slot))
+
+    def slot_length(self, slot: int) -> int:
+        o = C.c_int64()
+        check(self.L.fq_model_slot_length(self.h, slot, C.byref(o)))
+        return o.value
+
+    def prefill(self, slot: int, tokens, logits_dev=None) -> np.ndarray:
+        t = np.ascontiguousarray(tokens, np.int32)
+        st = np.zeros(t.size, ROW_STATS_DTYPE)
+        check(self.L.fq_model_prefill(self.h, slot, _ptr(t), t.size, _ptr(logits_dev), _ptr(st)))
+        return st
+
+    def decode(self, slots, tokens, logits_dev=None) -> np.ndarray:
+        s = np.ascontiguousarray(slots, np.int32)
+        t = np.ascontiguousarray(tokens, np.int32)
+        st = np.zeros(s.size, ROW_STATS_DTYPE)
+        check(self.L.fq_model_decode(self.h, s.size, _ptr(s), _ptr(t), _ptr(logits_dev), _ptr(st)))
+        return st
+
+    def logits_ptr(self) -> int:
+        p = C.c_void_p()
+        check(self.L.fq_model_logits(self.h, C.byref(p)))
+        return p.value
+
+    def step_bytes(self, slots) -> tuple:
+        s = np.ascontiguousarray(slots, np.int32)
+        w, k = C.c_int64(), C.c_int64()
+        check(self.L.fq_model_step_bytes(self.h, s.size, _ptr(s), C.byref(w), C.byref(k)))
+        return w.value, k.value
+
+    def calibrate_logit_kl(self, tokens: np.ndarray, base_rung: int, flip_rung: int):
+        t = np.ascontiguousarray(tokens, np.int32)
+        n_seqs, length = t.shape
+        kl = np.zeros(self.cfg.n_layers, np.float64)
+        ent = np.zeros(self.cfg.n_layers, np.float64)
+        check(self.L.fq_model_calibrate_logit_kl(self.h, _ptr(t), n_seqs, length, base_rung, flip_rung, _ptr(kl),
+                                                 _ptr(ent)))
+        return kl, ent
+
+    def close(self) -> None:
+        if self.h:
+            check(self.L.fq_model_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

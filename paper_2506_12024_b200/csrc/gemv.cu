@@ -36,7 +36,7 @@ constexpr int kStepCodes = 512;  // codes per row per warp step (32 lanes x 16)
 constexpr int kSegCodes = 16;    // codes per lane per step
 constexpr int kMaxB = 4;         // batch rows per fast launch
 constexpr int kMaxStages = 8;
-constexpr int kConsumerWarps = 8;
+constexpr int kSplit = 8;  // consumer warps splitting the K-steps of a row
 constexpr float kTwo109 = 649037107316853453566312041152512.0f;  // 2^109
 constexpr float kTwo40 = 1099511627776.0f;                        // 2^40
 constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;     // 2^-40
@@ -264,17 +264,17 @@ __device__ __forceinline__ float reduce4(const float (&v)[4], int lane) {
 // Consumes one ring slot holding `nrows` rows at bit-width BITS.  Lane-constant offsets:
 // pay_l = byte offset of the lane's segment in a row, sc_l / zp_l = the lane's group column.
 // red_row points at red[(first row)][warp][0] of this slot; rows are W*BB floats apart.
-template <int BITS, int SW, int BB>
-__device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, int nrows, int row_bytes,
+template <int BITS, int SW, int BB, int RG>
+__device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, int nrows, int rg, int row_bytes,
                                               int sc_off, int zp_off, int sc_row, int zp_row,
                                               const int (&pay_l)[SW], const int (&sc_l)[SW], const int (&zp_l)[SW],
                                               float zmagic, const float (&xs)[SW][BB][kSegCodes],
                                               const float (&sig)[SW][BB], float* red_row, int bmask, int lane) {
-  const uint8_t* pa = slot;
-  const uint8_t* sa = slot + sc_off;
-  const uint8_t* za = slot + zp_off;
-  const int red_step = kConsumerWarps * BB;
-  for (int r0 = 0; r0 < nrows; r0 += 4) {
+  const uint8_t* pa = slot + rg * 4 * row_bytes;
+  const uint8_t* sa = slot + sc_off + rg * 4 * sc_row;
+  const uint8_t* za = slot + zp_off + rg * 4 * zp_row;
+  const int red_step = kSplit * BB;
+  for (int r0 = rg * 4; r0 < nrows; r0 += 4 * RG) {
     float acc[BB][4];
 #pragma unroll
     for (int b = 0; b < BB; ++b)
@@ -307,21 +307,22 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
       const float v = reduce4(acc[b], lane);
       if ((lane & 7) == 0 && r0 + u < nrows && ((bmask >> b) & 1)) red_row[(r0 + u) * red_step + b] = v;
     }
-    pa += 4 * row_bytes;
-    sa += 4 * sc_row;
-    za += 4 * zp_row;
+    pa += 4 * RG * row_bytes;
+    sa += 4 * RG * sc_row;
+    za += 4 * RG * zp_row;
   }
 }
 
 // Fast kernel.  SW = K-steps per consumer warp, BB = batch rows (compile-time bounds).
-template <int SW, int BB>
-__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(const DevArgs a) {
+template <int SW, int BB, int RG>
+__global__ void __launch_bounds__((kSplit * RG + 1) * 32, 1) gemv_tma_kernel(const DevArgs a) {
+  constexpr int NCW = kSplit * RG;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(a.nstages) * a.stage_bytes);
   uint64_t* empty = full + kMaxStages;
   float* red = reinterpret_cast<float*>(empty + kMaxStages);
-  __shared__ float sq_red[kMaxB][kConsumerWarps + 1];
+  __shared__ float sq_red[kMaxB][NCW + 1];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int cta = blockIdx.x;
@@ -333,13 +334,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.nstages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp == NCW) {
     // ---------------- producer: stream this CTA's rows of every matrix through the ring
     if (lane == 0 && rows > 0) {
       int t = 0;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
     int gidx[SW];
 #pragma unroll
     for (int s = 0; s < SW; ++s) {
-      const int step = warp + s * kConsumerWarps;
+      const int step = (warp % kSplit) + s * kSplit;
       seg_k[s] = step * kStepCodes + lane * kSegCodes;
       step_ok[s] = step < a.nsteps && seg_k[s] < a.K;
       gidx[s] = step_ok[s] ? static_cast<int>(seg_k[s] / a.G) : 0;
@@ -418,13 +419,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
           const uint32_t ph = (t / a.nstages) & 1;
           mbar_wait(&full[s], ph);
           const uint8_t* slot = ring + static_cast<size_t>(s) * a.stage_bytes;
-          float* red_row = red + ((m * rows + rb) * kConsumerWarps + warp) * BB;
+          float* red_row = red + ((m * rows + rb) * kSplit + (warp % kSplit)) * BB;
           const int nr = min(rps, rows - rb);
           if (bits == 8)
-            consume_stage<8, SW, BB>(slot, nr, row_bytes, a.sc_off[0], a.zp_off[0], a.sc_row, a.zp_row, pay_l, sc_l,
+            consume_stage<8, SW, BB, RG>(slot, nr, warp / kSplit, row_bytes, a.sc_off[0], a.zp_off[0], a.sc_row, a.zp_row, pay_l, sc_l,
                                      zp_l, zmagic, xs, sig, red_row, bmask, lane);
           else
-            consume_stage<4, SW, BB>(slot, nr, row_bytes, a.sc_off[1], a.zp_off[1], a.sc_row, a.zp_row, pay_l, sc_l,
+            consume_stage<4, SW, BB, RG>(slot, nr, warp / kSplit, row_bytes, a.sc_off[1], a.zp_off[1], a.sc_row, a.zp_row, pay_l, sc_l,
                                      zp_l, zmagic, xs, sig, red_row, bmask, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
     float v[3] = {0.f, 0.f, 0.f};
     for (int m = 0; m < a.nmat; ++m) {
       float s = 0.f;
-      for (int w = 0; w < kConsumerWarps; ++w) s += red[((m * rows + r) * kConsumerWarps + w) * BB + b];
+      for (int w = 0; w < kSplit; ++w) s += red[((m * rows + r) * kSplit + w) * BB + b];
       v[m] = s * kTwo40;
     }
     if (a.epi == EPI_STORE) {
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1) gemv_tma_kernel(
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < a.B) {
       float s = 0.f;
-      for (int w = 0; w <= kConsumerWarps; ++w) s += sq_red[threadIdx.x][w];
+      for (int w = 0; w <= NCW; ++w) s += sq_red[threadIdx.x][w];
       a.out_partials[threadIdx.x * a.out_n_partials + cta] = s;
     }
   }
@@ -512,6 +513,7 @@ __global__ void gemv_exact_kernel(const int64_t N, const int64_t K, const int64_
 
 struct Plan {
   int sw;
+  int rg;
   int grid;
   int rps[2];
   int sc_off[2], zp_off[2];
@@ -523,7 +525,8 @@ struct Plan {
 Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
   Plan p{};
   const int nsteps = ceil_div_i(L->K, kStepCodes);
-  p.sw = (nsteps + kConsumerWarps - 1) / kConsumerWarps;
+  p.sw = (nsteps + kSplit - 1) / kSplit;
+  p.rg = (p.sw == 1 && bb == 1) ? 2 : 1;
   p.grid = static_cast<int>(std::min<int64_t>(ctx->num_sms, L->N));
   const int64_t rows_max = (L->N + p.grid - 1) / p.grid;
   const int64_t target = 24 * 1024;
@@ -533,7 +536,8 @@ Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
     const int64_t per_row = row_bytes + L->ng_pad * 4 + L->zp_pad;
     int rps = static_cast<int>(std::max<int64_t>(1, target / per_row));
     rps = std::min(rps, 16);
-    if (rps > 4) rps = rps / 4 * 4;
+    const int quantum = 4 * p.rg;
+    rps = rps >= quantum ? rps / quantum * quantum : quantum;
     const int64_t pad = (rps + 3) / 4 * 4;
     p.rps[w] = rps;
     p.sc_off[w] = static_cast<int>(pad * row_bytes);
@@ -541,7 +545,7 @@ Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
     slot = std::max<int64_t>(slot, pad * per_row);
   }
   p.stage_bytes = static_cast<int>((slot + 127) / 128 * 128);
-  const size_t red_bytes = static_cast<size_t>(nmat) * rows_max * kConsumerWarps * bb * sizeof(float);
+  const size_t red_bytes = static_cast<size_t>(nmat) * rows_max * kSplit * bb * sizeof(float);
   const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes) - 2 * kMaxStages * 8 - 256;
   p.nstages = static_cast<int>(std::min<int64_t>(kMaxStages, budget / p.stage_bytes));
   if (p.nstages < 2) fail(FQ_E_CONFIG, "gemv: layer rows too large for the shared-memory ring");
@@ -549,9 +553,9 @@ Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
   return p;
 }
 
-template <int SW, int BB>
+template <int SW, int BB, int RG>
 void launch_fast_t(fq_ctx* ctx, const DevArgs& d, const Plan& p, bool pdl) {
-  auto kern = gemv_tma_kernel<SW, BB>;
+  auto kern = gemv_tma_kernel<SW, BB, RG>;
   static std::mutex mu;
   static bool configured = false;
   {
@@ -563,7 +567,7 @@ void launch_fast_t(fq_ctx* ctx, const DevArgs& d, const Plan& p, bool pdl) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.grid);
-  cfg.blockDim = dim3((kConsumerWarps + 1) * 32);
+  cfg.blockDim = dim3((kSplit * RG + 1) * 32);
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
@@ -578,14 +582,19 @@ void launch_fast_t(fq_ctx* ctx, const DevArgs& d, const Plan& p, bool pdl) {
 template <int SW>
 void launch_fast_sw(fq_ctx* ctx, const DevArgs& d, const Plan& p, bool pdl) {
   if constexpr (SW == 1) {
-    if (d.B == 1) launch_fast_t<SW, 1>(ctx, d, p, pdl);
-    else if (d.B == 2) launch_fast_t<SW, 2>(ctx, d, p, pdl);
-    else launch_fast_t<SW, 4>(ctx, d, p, pdl);
+    if (d.B == 1) {
+      if (p.rg == 2) launch_fast_t<SW, 1, 2>(ctx, d, p, pdl);
+      else launch_fast_t<SW, 1, 1>(ctx, d, p, pdl);
+    } else if (d.B == 2) {
+      launch_fast_t<SW, 2, 1>(ctx, d, p, pdl);
+    } else {
+      launch_fast_t<SW, 4, 1>(ctx, d, p, pdl);
+    }
   } else if constexpr (SW == 2) {
-    if (d.B == 1) launch_fast_t<SW, 1>(ctx, d, p, pdl);
-    else launch_fast_t<SW, 2>(ctx, d, p, pdl);
+    if (d.B == 1) launch_fast_t<SW, 1, 1>(ctx, d, p, pdl);
+    else launch_fast_t<SW, 2, 1>(ctx, d, p, pdl);
   } else {
-    launch_fast_t<SW, 1>(ctx, d, p, pdl);
+    launch_fast_t<SW, 1, 1>(ctx, d, p, pdl);
   }
 }
 
@@ -596,7 +605,7 @@ bool gemv_fast_supported(const fq_layer* L, int rung) {
   const fq_rung_store& s = L->store(rung);
   const int nsteps = ceil_div_i(L->K, kStepCodes);
   return s.present && s.zp_fits_u8 && L->K % 32 == 0 && L->G % kSegCodes == 0 && L->G >= kSegCodes &&
-         nsteps <= 4 * kConsumerWarps;
+         nsteps <= 4 * kSplit;
 }
 
 int gemv_fast_grid(const fq_ctx* ctx, int64_t N) {
@@ -646,7 +655,7 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
     M.rung = g.mat[m].rung;
     M.y = g.mat[m].y;
   }
-  const int sw0 = (d.nsteps + kConsumerWarps - 1) / kConsumerWarps;
+  const int sw0 = (d.nsteps + kSplit - 1) / kSplit;
   const int64_t bchunk = sw0 == 1 ? kMaxB : (sw0 == 2 ? 2 : 1);
   const int64_t bb = std::min<int64_t>(bchunk, g.batch);
   const Plan p = plan_fast(ctx, L0, g.nmat, static_cast<int>(bb == 3 ? 4 : bb));
