@@ -176,6 +176,11 @@ fq_status fq_model_linear(fq_model* model, int32_t index, fq_layer** out); /* bo
 fq_status fq_model_set_param(fq_model* model, const char* name, const float* host, int64_t numel);
 /* Fills every parameter / rung from the deterministic generator on the device (bench). */
 fq_status fq_model_init_random(fq_model* model, uint64_t seed, float std);
+/* Same, and while each linear's fp32 weights are on the device computes the reference analyzer's
+ * weight-histogram KL of its W8 and W4 rungs (src/analyzer.cpp:83-94, `bins` bins) into
+ * kl8_host / kl4_host [num_linears] (either may be NULL). */
+fq_status fq_model_init_random_kl(fq_model* model, uint64_t seed, float std, int32_t bins, double* kl8_host,
+                                  double* kl4_host);
 /* Precision table: rung of (sequence slot, linear).  A pointer-of-record write, no payload
  * touched (Model::set_precision, src/model.cpp:268-278).  Takes effect at the next step. */
 fq_status fq_model_set_rung(fq_model* model, int32_t slot, int32_t linear_index, int32_t rung);
@@ -198,6 +203,12 @@ fq_status fq_model_logits(fq_model* model, float** logits_dev);
 /* Algorithmic bytes of one decode step for `batch` slots at their current rungs/lengths. */
 fq_status fq_model_step_bytes(const fq_model* model, int32_t batch, const int32_t* slots_host,
                               int64_t* weight_bytes, int64_t* kv_bytes);
+/* Kernel-level measurement: captures the decode step's GEMV launches alone (same layers, the
+ * slot's current rungs, same launch parameters) into a graph, replays it `reps` times between
+ * CUDA events on the context stream and reports the mean time of one GEMV launch (ms) and the
+ * algorithmic bytes of one pass over the step's GEMVs. */
+fq_status fq_model_profile_gemvs(fq_model* model, int32_t slot, int32_t reps, double* ms_per_launch,
+                                 int64_t* launches_per_pass, int64_t* bytes_per_pass);
 /* Logit-mode calibration (BASELINE config 4): teacher-forced prefill of `n_seqs` token rows
  * of length `len`, all linears at `base_rung`, then for every block b the block's linears at
  * `flip_rung`; kl_host[b] = mean KL(softmax(l_flip) || softmax(l_base)), entropy_host[b] =

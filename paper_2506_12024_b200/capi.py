@@ -32,6 +32,7 @@ ABI_FUNCTIONS = [
     "fq_model_linear_index", "fq_model_linear", "fq_model_set_param", "fq_model_init_random", "fq_model_set_rung",
     "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
     "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
+    "fq_model_init_random_kl", "fq_model_profile_gemvs",
 ]
 
 
@@ -134,6 +135,7 @@ def load(path: str = LIB_PATH):
         "fq_model_linear": [v, i32, C.POINTER(v)],
         "fq_model_set_param": [v, C.c_char_p, v, i64],
         "fq_model_init_random": [v, u64, C.c_float],
+        "fq_model_init_random_kl": [v, u64, C.c_float, i32, v, v],
         "fq_model_set_rung": [v, i32, i32, i32],
         "fq_model_get_rung": [v, i32, i32, C.POINTER(i32)],
         "fq_model_set_all_rungs": [v, i32, i32],
@@ -144,6 +146,7 @@ def load(path: str = LIB_PATH):
         "fq_model_logits": [v, C.POINTER(v)],
         "fq_model_step_bytes": [v, i32, v, C.POINTER(i64), C.POINTER(i64)],
         "fq_model_calibrate_logit_kl": [v, v, i64, i64, i32, i32, v, v],
+        "fq_model_profile_gemvs": [v, i32, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -351,8 +354,16 @@ class Model:
         a = np.ascontiguousarray(arr, np.float32)
         check(self.L.fq_model_set_param(self.h, name.encode(), _ptr(a), a.size))
 
-    def init_random(self, seed: int, std: float = 0.02) -> None:
-        check(self.L.fq_model_init_random(self.h, seed, std))
+    def init_random(self, seed: int, std: float = 0.02, kl_bins: int = 0):
+        """Device-side random init; with kl_bins > 0 also returns the weight-histogram KL of the
+        W8 and W4 rungs of every linear (reference analyzer, src/analyzer.cpp:83-94)."""
+        if kl_bins <= 0:
+            check(self.L.fq_model_init_random(self.h, seed, std))
+            return None
+        kl8 = np.zeros(self.n_linears, np.float64)
+        kl4 = np.zeros(self.n_linears, np.float64)
+        check(self.L.fq_model_init_random_kl(self.h, seed, std, kl_bins, _ptr(kl8), _ptr(kl4)))
+        return kl8, kl4
 
     def set_rung(self, slot: int, index: int, rung: int) -> None:
         check(self.L.fq_model_set_rung(self.h, slot, index, rung))
@@ -396,6 +407,12 @@ class Model:
         w, k = C.c_int64(), C.c_int64()
         check(self.L.fq_model_step_bytes(self.h, s.size, _ptr(s), C.byref(w), C.byref(k)))
         return w.value, k.value
+
+    def profile_gemvs(self, slot: int, reps: int):
+        """(ms per GEMV launch, launches per step, algorithmic bytes per step) of the step's GEMVs."""
+        ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
+        check(self.L.fq_model_profile_gemvs(self.h, slot, reps, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
 
     def calibrate_logit_kl(self, tokens: np.ndarray, base_rung: int, flip_rung: int):
         t = np.ascontiguousarray(tokens, np.int32)

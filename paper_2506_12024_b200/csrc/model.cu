@@ -494,8 +494,9 @@ void require(bool c, fq_status code, const std::string& msg) {
 
 void launch_dev(fq_model* M) { M->ctx->launches += 1; }
 
-// Enqueues one decode step for B rows (metadata already staged in meta_dev).
-void enqueue_step(fq_model* M, int B) {
+// Enqueues one decode step for B rows (metadata already staged in meta_dev).  gemv_only keeps
+// just the GEMV launches (kernel-level profiling; activations are whatever the buffers hold).
+void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
   fq_ctx* ctx = M->ctx;
   const fq_model_config& c = M->cfg;
   cudaStream_t st = ctx->stream;
@@ -503,9 +504,11 @@ void enqueue_step(fq_model* M, int B) {
   const StepMeta meta = M->meta(B);
   const uint8_t* table = M->table_dev();
   if (M->llama) {
-    embed_llama_kernel<<<B, 256, 0, st>>>(M->tok_emb, meta, d, M->resid, M->partials[0]);
-    FQ_CUDA(cudaGetLastError());
-    launch_dev(M);
+    if (!gemv_only) {
+      embed_llama_kernel<<<B, 256, 0, st>>>(M->tok_emb, meta, d, M->resid, M->partials[0]);
+      FQ_CUDA(cudaGetLastError());
+      launch_dev(M);
+    }
     int cur = 0, nparts = 1;
     for (int64_t l = 0; l < c.n_layers; ++l) {
       // fused RMSNorm + QKV
@@ -535,7 +538,7 @@ void enqueue_step(fq_model* M, int B) {
       g.pdl = true;
       launch_gemv_fast(ctx, g);
       // attention (RoPE + append + softmax over the cache)
-      {
+      if (!gemv_only) {
         dim3 grid(static_cast<unsigned>(c.n_heads), static_cast<unsigned>(B), static_cast<unsigned>(M->n_chunks));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
@@ -636,7 +639,7 @@ void enqueue_step(fq_model* M, int B) {
     hd.y_stride = V;
     hd.pdl = true;
     launch_gemv_fast(ctx, hd);
-    {
+    if (!gemv_only) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(B);
       cfg.blockDim = dim3(1024);
@@ -1052,7 +1055,7 @@ fq_status fq_model_set_param(fq_model* M, const char* name, const float* host, i
   });
 }
 
-fq_status fq_model_init_random(fq_model* M, uint64_t seed, float std) {
+fq_status fq_model_init_random_kl(fq_model* M, uint64_t seed, float std, int32_t bins, double* kl8, double* kl4) {
   return guarded([&] {
     require(M != nullptr, FQ_E_INPUT, "null model");
     fq_ctx* ctx = M->ctx;
@@ -1067,6 +1070,18 @@ fq_status fq_model_init_random(fq_model* M, uint64_t seed, float std) {
       fill_normal(ctx, w, L->N * L->K, seed, 100 + i, std);
       quantize_device(ctx, L, FQ_RUNG_INT8, FQ_MODE_ASYM, w);
       quantize_device(ctx, L, FQ_RUNG_INT4, FQ_MODE_ASYM, w);
+      if (kl8 || kl4) {
+        float* keep = L->fp;
+        L->fp = w;  // borrowed for the histogram pass only
+        try {
+          if (kl8) kl8[i] = hist_kl(ctx, L, FQ_RUNG_INT8, bins);
+          if (kl4) kl4[i] = hist_kl(ctx, L, FQ_RUNG_INT4, bins);
+        } catch (...) {
+          L->fp = keep;
+          throw;
+        }
+        L->fp = keep;
+      }
       if (!M->llama) {
         if (!L->fp) L->fp = static_cast<float*>(dmalloc(sizeof(float) * L->N * L->K));
         FQ_CUDA(cudaMemcpyAsync(L->fp, w, sizeof(float) * L->N * L->K, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1075,6 +1090,10 @@ fq_status fq_model_init_random(fq_model* M, uint64_t seed, float std) {
     FQ_CUDA(cudaStreamSynchronize(ctx->stream));
     dfree(w);
   });
+}
+
+fq_status fq_model_init_random(fq_model* M, uint64_t seed, float std) {
+  return fq_model_init_random_kl(M, seed, std, 0, nullptr, nullptr);
 }
 
 fq_status fq_model_set_rung(fq_model* M, int32_t slot, int32_t li, int32_t rung) {
@@ -1183,6 +1202,55 @@ fq_status fq_model_step_bytes(const fq_model* M, int32_t batch, const int32_t* s
     }
     if (weight_bytes) *weight_bytes = wb;
     if (kv_bytes) *kv_bytes = kb;
+  });
+}
+
+fq_status fq_model_profile_gemvs(fq_model* M, int32_t slot, int32_t reps, double* ms_per_launch,
+                                 int64_t* launches_per_pass, int64_t* bytes_per_pass) {
+  return guarded([&] {
+    require(M && ms_per_launch, FQ_E_INPUT, "null argument");
+    require(M->llama, FQ_E_CONFIG, "profile_gemvs: llama arch only");
+    require(reps >= 1, FQ_E_INPUT, "profile_gemvs: reps must be >= 1");
+    const int32_t tok = 0;
+    if (M->slot_len[slot] >= M->cfg.max_seq_len) fail(FQ_E_CAPACITY, "profile_gemvs: slot is full");
+    stage_rows(M, 1, &slot, &tok);
+    fq_ctx* ctx = M->ctx;
+    cudaStream_t st = ctx->stream;
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    const int64_t l0 = ctx->launches;
+    cudaGraph_t graph;
+    FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    enqueue_step(M, 1, true);
+    FQ_CUDA(cudaStreamEndCapture(st, &graph));
+    const int64_t per_pass = ctx->launches - l0;
+    cudaGraphExec_t exec;
+    FQ_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    FQ_CUDA(cudaGraphDestroy(graph));
+    cudaEvent_t e0, e1;
+    FQ_CUDA(cudaEventCreate(&e0));
+    FQ_CUDA(cudaEventCreate(&e1));
+    for (int i = 0; i < 2; ++i) FQ_CUDA(cudaGraphLaunch(exec, st));
+    FQ_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < reps; ++i) FQ_CUDA(cudaGraphLaunch(exec, st));
+    FQ_CUDA(cudaEventRecord(e1, st));
+    FQ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(exec);
+    ctx->launches += per_pass * (reps + 1);
+    *ms_per_launch = static_cast<double>(ms) / reps / static_cast<double>(per_pass);
+    if (launches_per_pass) *launches_per_pass = per_pass;
+    if (bytes_per_pass) {
+      int64_t b = 0;
+      for (int i = 0; i < M->n_lin; ++i) {
+        const fq_layer* L = M->lin[i];
+        const int r = M->rungs[static_cast<size_t>(slot) * M->n_lin + i];
+        b += (r == FQ_RUNG_INT8 ? L->N * L->K : (L->N * L->K + 1) / 2) + L->N * L->ng * 5 + L->K * 2 + L->N * 2;
+      }
+      *bytes_per_pass = b;
+    }
   });
 }
 
