@@ -315,7 +315,7 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
 
 // Fast kernel.  SW = K-steps per consumer warp, BB = batch rows (compile-time bounds).
 template <int SW, int BB, int RG>
-__global__ void __launch_bounds__((kSplit * RG + 1) * 32, 1) gemv_tma_kernel(const DevArgs a) {
+__global__ void __launch_bounds__((kSplit * RG + 1) * 32, RG == 1 ? 2 : 1) gemv_tma_kernel(const DevArgs a) {
   constexpr int NCW = kSplit * RG;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
@@ -339,6 +339,9 @@ __global__ void __launch_bounds__((kSplit * RG + 1) * 32, 1) gemv_tma_kernel(con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // Let the next kernel of the stream become resident beside this one (two CTAs fit per SM):
+  // its producer warp then streams the next weights while this kernel finishes.
+  pdl_launch_dependents();
 
   if (warp == NCW) {
     // ---------------- producer: stream this CTA's rows of every matrix through the ring
@@ -433,7 +436,6 @@ __global__ void __launch_bounds__((kSplit * RG + 1) * 32, 1) gemv_tma_kernel(con
       }
     }
   }
-  pdl_launch_dependents();
   __syncthreads();
 
   // ---------------- cross-warp reduction in warp order + epilogue
@@ -526,7 +528,7 @@ Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
   Plan p{};
   const int nsteps = ceil_div_i(L->K, kStepCodes);
   p.sw = (nsteps + kSplit - 1) / kSplit;
-  p.rg = (p.sw == 1 && bb == 1) ? 2 : 1;
+  p.rg = 1;  // 9 warps x <= 112 registers: two CTAs (this kernel + the next) co-reside per SM
   p.grid = static_cast<int>(std::min<int64_t>(ctx->num_sms, L->N));
   const int64_t rows_max = (L->N + p.grid - 1) / p.grid;
   const int64_t target = 24 * 1024;
@@ -546,7 +548,7 @@ Plan plan_fast(const fq_ctx* ctx, const fq_layer* L, int nmat, int bb) {
   }
   p.stage_bytes = static_cast<int>((slot + 127) / 128 * 128);
   const size_t red_bytes = static_cast<size_t>(nmat) * rows_max * kSplit * bb * sizeof(float);
-  const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes) - 2 * kMaxStages * 8 - 256;
+  const int64_t budget = 100 * 1024 - static_cast<int64_t>(red_bytes) - 2 * kMaxStages * 8 - 256;
   p.nstages = static_cast<int>(std::min<int64_t>(kMaxStages, budget / p.stage_bytes));
   if (p.nstages < 2) fail(FQ_E_CONFIG, "gemv: layer rows too large for the shared-memory ring");
   p.smem = static_cast<size_t>(p.nstages) * p.stage_bytes + 2 * kMaxStages * 8 + red_bytes;
