@@ -12,7 +12,7 @@ CUDA_LIB  := $(PKG)/lib/libfq_cuda.so
 
 all: $(CUDA_LIB)
 
-build/cuda/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/fq_internal.cuh include/fq_cuda.h
+build/cuda/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/fq_internal.cuh include/fq_cuda.h $(PKG)/csrc/gemv_program.cuh
 	@mkdir -p build/cuda
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

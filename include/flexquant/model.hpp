@@ -1,0 +1,174 @@
+// Device-resident multi-precision decoder behind the reference's Model API
+// (/root/reference/proj/include/flexquant/model.hpp:18-215).  Weights live on the B200 as
+// resident per-precision copies; set_precision is a one-byte precision-table write (no payload
+// is touched); forward_* run the captured decode-step graph and return host logits.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <span>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "flexquant/quantizer.hpp"
+#include "flexquant/rung.hpp"
+#include "flexquant/tensor.hpp"
+
+namespace flexquant {
+
+using TokenId = int32_t;
+
+enum class Arch : uint8_t { Reference = FQ_ARCH_REFERENCE, Llama = FQ_ARCH_LLAMA };
+
+struct ModelConfig {
+  int64_t vocab_size = 0;
+  int64_t d_model = 0;
+  int64_t n_heads = 0;
+  int64_t head_dim = 0;
+  int64_t n_layers = 0;
+  int64_t ffn_dim = 0;
+  int64_t max_seq_len = 0;
+  bool tie_embeddings = false;
+  // B200 engine extensions
+  Arch arch = Arch::Reference;
+  int64_t group_size = 0;  // quantization group (0 = per row, the reference scheme)
+  int max_batch = 1;       // resident sequence slots
+  float norm_eps = 1e-5f;
+  float rope_theta = 10000.0f;
+  void validate() const;
+};
+
+// Per-forward accounting (src/model.cpp:77-98).  On the device the linear time buckets are
+// attributed from the step's measured time in proportion to each rung's algorithmic bytes.
+struct StepStats {
+  double weight_bytes = 0.0;
+  uint64_t ns_fp = 0;
+  uint64_t ns_int8 = 0;
+  uint64_t ns_int4 = 0;
+  uint64_t ns_forward = 0;
+  void reset() { *this = StepStats{}; }
+};
+
+class Model;
+
+// One switchable linear: a view of the model's resident fq_layer, or a standalone layer.
+class MultiPrecisionLayer {
+ public:
+  MultiPrecisionLayer() = default;
+  // Standalone layer holding fp weights; quantize_rungs / set_quantized add the integer rungs.
+  MultiPrecisionLayer(std::string id, Tensor weight, Tensor bias, int64_t group_size = 0);
+  ~MultiPrecisionLayer();
+  MultiPrecisionLayer(MultiPrecisionLayer&&) noexcept;
+  MultiPrecisionLayer& operator=(MultiPrecisionLayer&&) noexcept;
+
+  void quantize_rungs(QuantMode mode);
+  const std::string& id() const { return id_; }
+  int64_t out_features() const { return n_; }
+  int64_t in_features() const { return k_; }
+  int64_t param_count() const { return n_ * k_; }
+  Rung current() const;
+  void set_current(Rung r);
+  bool has(Rung r) const;
+  void set_quantized(Rung r, const QuantizedTensor& q);
+  QuantizedTensor quantized(Rung r) const;  // downloaded from the device
+  // y = x * W_active^T + bias on the device (exact numerics: bit-identical to the reference).
+  Tensor forward(const Tensor& x, StepStats* stats) const;
+  double active_weight_bytes() const { return static_cast<double>(param_count()) * accounting_bits(current()) / 8.0; }
+  fq_layer* handle() const { return layer_; }
+
+ private:
+  friend class Model;
+  std::string id_;
+  int64_t n_ = 0, k_ = 0;
+  fq_layer* layer_ = nullptr;
+  bool owned_ = false;
+  Model* model_ = nullptr;  // non-null for model views (rung lives in the model's table)
+  int index_ = -1;
+  Rung standalone_rung_ = Rung::Fp;
+};
+
+// A sequence slot's KV history on the device (KvCache, src/model.cpp:142-171).
+class KvCache {
+ public:
+  KvCache() = default;
+  int64_t length() const;
+  int64_t max_length() const;
+  int slot() const { return slot_; }
+
+ private:
+  friend class Model;
+  const Model* model_ = nullptr;
+  int slot_ = 0;
+};
+
+struct SwitchEvent {
+  std::string layer_id;
+  Rung from = Rung::Fp;
+  Rung to = Rung::Int8;
+};
+
+class Model {
+ public:
+  explicit Model(ModelConfig cfg);
+  ~Model();
+  Model(const Model&) = delete;
+  Model& operator=(const Model&) = delete;
+
+  const ModelConfig& config() const { return cfg_; }
+  KvCache make_cache(int slot = 0);
+
+  Tensor forward_prefill(std::span<const TokenId> tokens, KvCache& cache);
+  Tensor forward_decode(TokenId token, KvCache& cache);
+
+  std::optional<SwitchEvent> set_precision(std::string_view layer_id, Rung bits, int slot = 0);
+  void set_all_precision(Rung bits, int slot = 0);
+  Rung precision(int linear_index, int slot = 0) const;
+
+  double effective_bits(int slot = 0) const;
+  double weight_bytes_per_pass(int slot = 0) const;
+
+  size_t num_linears() const { return layers_.size(); }
+  const std::vector<std::string>& linear_ids() const { return ids_; }
+  int linear_index(std::string_view id) const;  // -1 if unknown
+  MultiPrecisionLayer& linear(int i) { return layers_.at(static_cast<size_t>(i)); }
+  const MultiPrecisionLayer& linear(int i) const { return layers_.at(static_cast<size_t>(i)); }
+  MultiPrecisionLayer* find_layer(std::string_view id);
+  const MultiPrecisionLayer* find_layer(std::string_view id) const;
+
+  const StepStats& step_stats() const { return stats_; }
+  void reset_step_stats() { stats_.reset(); }
+
+  // Parameters by name (see fq_model_set_param) and device-side random initialisation.
+  void set_param(const std::string& name, const Tensor& t);
+  void init_random(uint64_t seed, float std = 0.02f);
+
+  fq_model* handle() const { return model_; }
+
+  // Lower-level batched step used by the engine: one decode step for `slots`, per-row
+  // statistics only (no logits copy).  Returns the rows' statistics.
+  std::vector<fq_row_stats> decode_rows(std::span<const int32_t> slots, std::span<const TokenId> tokens);
+  std::vector<fq_row_stats> prefill_rows(int slot, std::span<const TokenId> tokens);
+
+ private:
+  friend class MultiPrecisionLayer;
+  friend class KvCache;
+  void account_step(uint64_t ns, int slot);
+  ModelConfig cfg_;
+  fq_model* model_ = nullptr;
+  std::vector<std::string> ids_;
+  std::vector<MultiPrecisionLayer> layers_;
+  StepStats stats_;
+};
+
+double effective_bits(std::span<const MultiPrecisionLayer* const> layers);
+
+// The reference's weight container, "flexquant-weights v1" (src/model_io.cpp:130-258), loaded
+// into a reference-architecture device model (fp + W8 + W4 rungs and biases resident).
+std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch = 1);
+
+// Process-wide device context used by the host API (device = $FQ_DEVICE, else $LOCAL_RANK, else 0).
+fq_ctx* runtime();
+
+}  // namespace flexquant

@@ -15,6 +15,7 @@
 // captured graph, and the GEMVs select the W8 or W4 copy from it, so no weights move and the
 // graph is never re-captured.
 #include "fq_internal.cuh"
+#include "gemv_program.cuh"
 
 #include <cmath>
 #include <cstring>
@@ -25,7 +26,6 @@ namespace fqc {
 namespace {
 
 constexpr int kPartStride = 1024;  // columns of the sum-of-squares partial buffer per batch row
-constexpr int kAttnChunk = 64;     // keys per attention CTA (llama)
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
@@ -468,6 +468,8 @@ struct fq_model {
   size_t meta_bytes = 0;
   fq_row_stats* stats_host = nullptr;  // pinned [max_batch]
   std::map<int, cudaGraphExec_t> graphs;
+  std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, gemv_only) -> uploaded program
+  unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
 
   int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
@@ -504,154 +506,162 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
   const StepMeta meta = M->meta(B);
   const uint8_t* table = M->table_dev();
   if (M->llama) {
-    if (!gemv_only) {
-      embed_llama_kernel<<<B, 256, 0, st>>>(M->tok_emb, meta, d, M->resid, M->partials[0]);
-      FQ_CUDA(cudaGetLastError());
-      launch_dev(M);
-    }
-    int cur = 0, nparts = 1;
-    for (int64_t l = 0; l < c.n_layers; ++l) {
-      // fused RMSNorm + QKV
-      GemvLaunch g;
-      g.nmat = 3;
-      for (int j = 0; j < 3; ++j) {
-        g.mat[j].layer = M->lin[M->lin_index(static_cast<int>(l), j)];
-        g.mat[j].rung_table = table + M->lin_index(static_cast<int>(l), j);
-        g.mat[j].rung_stride = M->n_lin;
-      }
-      g.mat[0].y = M->q;
-      g.mat[1].y = M->k;
-      g.mat[2].y = M->v;
-      g.batch = B;
-      g.x = M->resid;
-      g.x_dtype = FQ_DT_F32;
-      g.x_stride = d;
-      g.norm_gain = M->n1g[l];
-      g.norm_partials = M->partials[cur];
-      g.n_partials = nparts;
-      g.partials_stride = kPartStride;
-      g.norm_eps = c.norm_eps;
-      g.act_dtype = c.act_dtype;
-      g.epi = EPI_SPLIT3;
-      g.y_dtype = c.act_dtype;
-      g.y_stride = d;
-      g.pdl = true;
-      launch_gemv_fast(ctx, g);
-      // attention (RoPE + append + softmax over the cache)
+    // The whole llama step is one persistent program (program.cu): embedding, then per layer
+    // QKV GEMV (fused RMSNorm) | attention | WO (+residual) | gate/up (+SwiGLU) | down
+    // (+residual), then the head and the row statistics, with a grid barrier between
+    // dependent phases while the weight stream runs ahead.
+    auto key = std::make_pair(B, gemv_only ? 1 : 0);
+    auto it = M->programs.find(key);
+    if (it == M->programs.end()) {
+      ProgramBuilder pb;
+      pb.grid = ctx->num_sms;
+      const int G = pb.grid;
       if (!gemv_only) {
-        dim3 grid(static_cast<unsigned>(c.n_heads), static_cast<unsigned>(B), static_cast<unsigned>(M->n_chunks));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(128);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        FQ_CUDA(cudaLaunchKernelEx(&cfg, attn_llama_kernel, static_cast<const void*>(M->q),
-                                   static_cast<const void*>(M->k), static_cast<const void*>(M->v), c.act_dtype, meta,
-                                   static_cast<__half*>(M->kv), M->slot_stride, l * M->layer_stride, c.max_seq_len,
-                                   static_cast<int>(c.n_heads), static_cast<int>(c.head_dim), c.rope_theta,
-                                   M->attn_ws, M->tickets, M->attn));
-        launch_dev(M);
+        Phase e{};
+        e.type = PH_EMBED;
+        e.barrier_after = 1;
+        e.B = B;
+        e.tok_emb = M->tok_emb;
+        e.tokens = meta.tokens;
+        e.d = d;
+        e.resid = M->resid;
+        e.resid_stride = d;
+        e.out_partials = M->partials[0];
+        e.out_partials_stride = kPartStride;
+        pb.add(e);
       }
-      // wo + residual
-      GemvLaunch o;
-      o.nmat = 1;
-      o.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 3)];
-      o.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 3);
-      o.mat[0].rung_stride = M->n_lin;
-      o.batch = B;
-      o.x = M->attn;
-      o.x_dtype = c.act_dtype;
-      o.x_stride = d;
-      o.epi = EPI_RESIDUAL;
-      o.resid = M->resid;
-      o.resid_stride = d;
-      o.out_partials = M->partials[cur ^ 1];
-      o.out_n_partials = kPartStride;
-      o.pdl = true;
-      nparts = launch_gemv_fast(ctx, o);
-      cur ^= 1;
-      // fused RMSNorm + gate/up + SwiGLU
-      GemvLaunch gu;
-      gu.nmat = 2;
-      for (int j = 0; j < 2; ++j) {
-        gu.mat[j].layer = M->lin[M->lin_index(static_cast<int>(l), 4 + j)];
-        gu.mat[j].rung_table = table + M->lin_index(static_cast<int>(l), 4 + j);
-        gu.mat[j].rung_stride = M->n_lin;
+      int cur = 0;
+      for (int64_t l = 0; l < c.n_layers; ++l) {
+        GemvLaunch g;
+        g.nmat = 3;
+        for (int j = 0; j < 3; ++j) {
+          g.mat[j].layer = M->lin[M->lin_index(static_cast<int>(l), j)];
+          g.mat[j].rung_table = table + M->lin_index(static_cast<int>(l), j);
+          g.mat[j].rung_stride = M->n_lin;
+        }
+        g.mat[0].y = M->q;
+        g.mat[1].y = M->k;
+        g.mat[2].y = M->v;
+        g.x = M->resid;
+        g.x_dtype = FQ_DT_F32;
+        g.x_stride = d;
+        g.norm_gain = M->n1g[l];
+        g.norm_partials = M->partials[cur];
+        g.n_partials = G;
+        g.partials_stride = kPartStride;
+        g.norm_eps = c.norm_eps;
+        g.act_dtype = c.act_dtype;
+        g.epi = EPI_SPLIT3;
+        g.y_dtype = c.act_dtype;
+        g.y_stride = d;
+        pb.add_gemv(g, 0, B);
+        if (!gemv_only) {
+          Phase a{};
+          a.type = PH_ATTN;
+          a.barrier_after = 1;
+          a.B = B;
+          a.q = M->q;
+          a.k = M->k;
+          a.v = M->v;
+          a.act_dtype = c.act_dtype;
+          a.pos = meta.pos;
+          a.slots = meta.slots;
+          a.kv = static_cast<__half*>(M->kv);
+          a.slot_stride = M->slot_stride;
+          a.layer_off = l * M->layer_stride;
+          a.max_seq = c.max_seq_len;
+          a.n_heads = static_cast<int>(c.n_heads);
+          a.head_dim = static_cast<int>(c.head_dim);
+          a.rope_theta = c.rope_theta;
+          a.attn_ws = M->attn_ws;
+          a.tickets = M->tickets;
+          a.attn_out = M->attn;
+          pb.add(a);
+        }
+        GemvLaunch o;
+        o.nmat = 1;
+        o.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 3)];
+        o.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 3);
+        o.mat[0].rung_stride = M->n_lin;
+        o.x = M->attn;
+        o.x_dtype = c.act_dtype;
+        o.x_stride = d;
+        o.epi = EPI_RESIDUAL;
+        o.resid = M->resid;
+        o.resid_stride = d;
+        o.out_partials = M->partials[cur ^ 1];
+        o.out_n_partials = kPartStride;
+        pb.add_gemv(o, 0, B);
+        cur ^= 1;
+        GemvLaunch gu;
+        gu.nmat = 2;
+        for (int j = 0; j < 2; ++j) {
+          gu.mat[j].layer = M->lin[M->lin_index(static_cast<int>(l), 4 + j)];
+          gu.mat[j].rung_table = table + M->lin_index(static_cast<int>(l), 4 + j);
+          gu.mat[j].rung_stride = M->n_lin;
+        }
+        gu.x = M->resid;
+        gu.x_dtype = FQ_DT_F32;
+        gu.x_stride = d;
+        gu.norm_gain = M->n2g[l];
+        gu.norm_partials = M->partials[cur];
+        gu.n_partials = G;
+        gu.partials_stride = kPartStride;
+        gu.norm_eps = c.norm_eps;
+        gu.act_dtype = c.act_dtype;
+        gu.epi = EPI_SWIGLU;
+        gu.y = M->mid;
+        gu.y_dtype = c.act_dtype;
+        gu.y_stride = c.ffn_dim;
+        pb.add_gemv(gu, 0, B);
+        GemvLaunch dn;
+        dn.nmat = 1;
+        dn.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 6)];
+        dn.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 6);
+        dn.mat[0].rung_stride = M->n_lin;
+        dn.x = M->mid;
+        dn.x_dtype = c.act_dtype;
+        dn.x_stride = c.ffn_dim;
+        dn.epi = EPI_RESIDUAL;
+        dn.resid = M->resid;
+        dn.resid_stride = d;
+        dn.out_partials = M->partials[cur ^ 1];
+        dn.out_n_partials = kPartStride;
+        pb.add_gemv(dn, 0, B);
+        cur ^= 1;
       }
-      gu.batch = B;
-      gu.x = M->resid;
-      gu.x_dtype = FQ_DT_F32;
-      gu.x_stride = d;
-      gu.norm_gain = M->n2g[l];
-      gu.norm_partials = M->partials[cur];
-      gu.n_partials = nparts;
-      gu.partials_stride = kPartStride;
-      gu.norm_eps = c.norm_eps;
-      gu.act_dtype = c.act_dtype;
-      gu.epi = EPI_SWIGLU;
-      gu.y = M->mid;
-      gu.y_dtype = c.act_dtype;
-      gu.y_stride = c.ffn_dim;
-      gu.pdl = true;
-      launch_gemv_fast(ctx, gu);
-      // down + residual
-      GemvLaunch dn;
-      dn.nmat = 1;
-      dn.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 6)];
-      dn.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 6);
-      dn.mat[0].rung_stride = M->n_lin;
-      dn.batch = B;
-      dn.x = M->mid;
-      dn.x_dtype = c.act_dtype;
-      dn.x_stride = c.ffn_dim;
-      dn.epi = EPI_RESIDUAL;
-      dn.resid = M->resid;
-      dn.resid_stride = d;
-      dn.out_partials = M->partials[cur ^ 1];
-      dn.out_n_partials = kPartStride;
-      dn.pdl = true;
-      nparts = launch_gemv_fast(ctx, dn);
-      cur ^= 1;
+      GemvLaunch hd;
+      hd.nmat = 1;
+      hd.mat[0].layer = M->lin[M->head_index()];
+      hd.mat[0].rung_table = table + M->head_index();
+      hd.mat[0].rung_stride = M->n_lin;
+      hd.x = M->resid;
+      hd.x_dtype = FQ_DT_F32;
+      hd.x_stride = d;
+      hd.norm_gain = M->fng;
+      hd.norm_partials = M->partials[cur];
+      hd.n_partials = G;
+      hd.partials_stride = kPartStride;
+      hd.norm_eps = c.norm_eps;
+      hd.act_dtype = c.act_dtype;
+      hd.epi = EPI_STORE;
+      hd.y = M->logits;
+      hd.y_dtype = FQ_DT_F32;
+      hd.y_stride = V;
+      pb.add_gemv(hd, 0, B);
+      if (!gemv_only) {
+        Phase sp{};
+        sp.type = PH_STATS;
+        sp.B = B;
+        sp.logits = M->logits;
+        sp.vocab = V;
+        sp.stats = M->stats_dev;
+        pb.add(sp);
+      }
+      it = M->programs.emplace(key, upload_program(ctx, pb, false)).first;
     }
-    // final RMSNorm + head
-    GemvLaunch hd;
-    hd.nmat = 1;
-    hd.mat[0].layer = M->lin[M->head_index()];
-    hd.mat[0].rung_table = table + M->head_index();
-    hd.mat[0].rung_stride = M->n_lin;
-    hd.batch = B;
-    hd.x = M->resid;
-    hd.x_dtype = FQ_DT_F32;
-    hd.x_stride = d;
-    hd.norm_gain = M->fng;
-    hd.norm_partials = M->partials[cur];
-    hd.n_partials = nparts;
-    hd.partials_stride = kPartStride;
-    hd.norm_eps = c.norm_eps;
-    hd.act_dtype = c.act_dtype;
-    hd.epi = EPI_STORE;
-    hd.y = M->logits;
-    hd.y_dtype = FQ_DT_F32;
-    hd.y_stride = V;
-    hd.pdl = true;
-    launch_gemv_fast(ctx, hd);
-    if (!gemv_only) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(B);
-      cfg.blockDim = dim3(1024);
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      FQ_CUDA(cudaLaunchKernelEx(&cfg, row_stats_kernel, static_cast<const float*>(M->logits), V, M->stats_dev));
-      launch_dev(M);
-    }
+    FQ_CUDA(cudaMemsetAsync(M->grid_barrier, 0, sizeof(unsigned int), st));
+    launch_program(ctx, it->second, M->grid_barrier, false);
     return;
   }
   // ---------------- reference architecture (exact numerics)
@@ -953,6 +963,7 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->n_chunks = static_cast<int>((c.max_seq_len + kAttnChunk - 1) / kAttnChunk);
     M->attn_ws = zeros(static_cast<int64_t>(B) * c.n_heads * M->n_chunks * (c.head_dim + 2));
     M->tickets = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * B * c.n_heads));
+    M->grid_barrier = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * 4));
     FQ_CUDA(cudaMemsetAsync(M->tickets, 0, sizeof(unsigned int) * B * c.n_heads, st));
     const int64_t dsz = std::max<int64_t>(static_cast<int64_t>(B) * c.n_heads * c.max_seq_len, B * V);
     M->dscratch = static_cast<double*>(dmalloc(sizeof(double) * dsz));
@@ -971,6 +982,8 @@ fq_status fq_model_destroy(fq_model* M) {
     if (!M) return;
     cudaStreamSynchronize(M->ctx->stream);
     for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : M->programs) dfree(kv.second.dev_phases);
+    dfree(M->grid_barrier);
     for (fq_layer* L : M->lin) {
       L->borrowed = false;
       fq_layer_destroy(L);
