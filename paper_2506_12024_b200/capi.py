@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfq_cuda.so")
+LIB_PATH = os.environ.get("FQ_CUDA_LIB", os.path.join(_HERE, "lib", "libfq_cuda.so"))
 
 RUNG_FP, RUNG_INT8, RUNG_INT4 = 0, 1, 2
 MODE_ASYM, MODE_SYM = 0, 1

@@ -14,7 +14,10 @@ constexpr int kSegCodes = 16;    // codes per lane per step
 constexpr int kMaxB = 4;         // batch rows per phase
 constexpr int kMaxStages = 8;
 constexpr int kSplit = 8;        // consumer warps splitting the K-steps of a row
-constexpr int kRG = 2;           // row groups of consumer warps
+#ifndef FQ_RG
+#define FQ_RG 2
+#endif
+constexpr int kRG = FQ_RG;       // row groups of consumer warps
 constexpr int kNCW = kSplit * kRG;
 constexpr int kThreads = (kNCW + 1) * 32;  // + one producer warp
 constexpr int kMaxSW = 4;        // K-steps per warp (K <= 16384)

@@ -496,6 +496,12 @@ void require(bool c, fq_status code, const std::string& msg) {
 
 void launch_dev(fq_model* M) { M->ctx->launches += 1; }
 
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  return cs != cudaStreamCaptureStatusNone;
+}
+
 // Enqueues one decode step for B rows (metadata already staged in meta_dev).  gemv_only keeps
 // just the GEMV launches (kernel-level profiling; activations are whatever the buffers hold).
 void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
@@ -513,6 +519,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
     auto key = std::make_pair(B, gemv_only ? 1 : 0);
     auto it = M->programs.find(key);
     if (it == M->programs.end()) {
+      if (capturing(st)) fail(FQ_E_STATE, "step program must be built before graph capture");
       ProgramBuilder pb;
       pb.grid = ctx->num_sms;
       const int G = pb.grid;
@@ -745,6 +752,14 @@ void run_step(fq_model* M, int B) {
   }
   auto it = M->graphs.find(B);
   if (it == M->graphs.end()) {
+    if (M->programs.find(std::make_pair(B, 0)) == M->programs.end()) {
+      // first use: build + upload the step program (allocates) and run the step un-captured
+      FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+      enqueue_step(M, B);
+      FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * B, cudaMemcpyDeviceToHost, st));
+      FQ_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
     cudaGraph_t graph;
     FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
@@ -1230,6 +1245,10 @@ fq_status fq_model_profile_gemvs(fq_model* M, int32_t slot, int32_t reps, double
     fq_ctx* ctx = M->ctx;
     cudaStream_t st = ctx->stream;
     FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    if (M->programs.find(std::make_pair(1, 1)) == M->programs.end()) {
+      enqueue_step(M, 1, true);  // builds + uploads the GEMV-only program (un-captured run)
+      FQ_CUDA(cudaStreamSynchronize(st));
+    }
     const int64_t l0 = ctx->launches;
     cudaGraph_t graph;
     FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
