@@ -87,6 +87,8 @@ class MultiPrecisionLayer {
   Model* model_ = nullptr;  // non-null for model views (rung lives in the model's table)
   int index_ = -1;
   Rung standalone_rung_ = Rung::Fp;
+  int64_t group_ = 0;
+  Tensor host_fp_;  // standalone layers keep their fp weights for quantize_rungs
 };
 
 // A sequence slot's KV history on the device (KvCache, src/model.cpp:142-171).

@@ -157,31 +157,36 @@ struct Ring {
 };
 
 // ---------------------------------------------------------------- producer
-__device__ void produce_phase(const Phase& P, const Ring& R, int& t) {
+// All phase fields are copied into registers before the stage loop: the asm statements carry
+// "memory" clobbers, so anything left in memory would be reloaded after every copy / wait.
+__device__ __forceinline__ void produce_phase(const Phase& P, const Ring R, int& t) {
   int64_t r0;
   int rows;
   cta_rows(P.N, r0, rows);
   if (rows <= 0) return;
-  for (int m = 0; m < P.nmat; ++m) {
+  const int nmat = P.nmat;
+  const int64_t K = P.K, ng_pad = P.ng_pad, zp_pad = P.zp_pad;
+  for (int m = 0; m < nmat; ++m) {
     for (int w = 0; w < 2; ++w) {
       if (pass_mask(P, m, w) == 0) continue;
       const int rps = P.rows_per_stage[w];
-      const int64_t row_bytes = w == 0 ? P.K : P.K / 2;
-      const DevMat& M = P.mat[m];
+      const int64_t row_bytes = w == 0 ? K : K / 2;
+      const uint8_t* pay_src = P.mat[m].payload[w] + r0 * row_bytes;
+      const uint8_t* sc_src = reinterpret_cast<const uint8_t*>(P.mat[m].scale[w] + r0 * ng_pad);
+      const uint8_t* zp_src = P.mat[m].zp[w] + r0 * zp_pad;
+      const uint32_t sc_off = static_cast<uint32_t>(P.sc_off[w]), zp_off = static_cast<uint32_t>(P.zp_off[w]);
+      const uint32_t pay_row = static_cast<uint32_t>(row_bytes), sc_row = static_cast<uint32_t>(ng_pad * 4),
+                     zp_row = static_cast<uint32_t>(zp_pad);
       for (int rb = 0; rb < rows; rb += rps, ++t) {
         const int s = t % R.nstages;
         const uint32_t ph = (t / R.nstages) & 1;
         mbar_wait(&R.empty[s], ph ^ 1);
-        const int nr = min(rps, rows - rb);
-        const uint32_t pay = static_cast<uint32_t>(nr * row_bytes);
-        const uint32_t sc = static_cast<uint32_t>(nr * P.ng_pad * 4);
-        const uint32_t zp = static_cast<uint32_t>(nr * P.zp_pad);
+        const uint32_t nr = static_cast<uint32_t>(min(rps, rows - rb));
         uint8_t* dst = R.base + static_cast<size_t>(s) * R.stage_bytes;
-        const int64_t row = r0 + rb;
-        mbar_expect_tx(&R.full[s], pay + sc + zp);
-        bulk_g2s(dst, M.payload[w] + row * row_bytes, pay, &R.full[s]);
-        bulk_g2s(dst + P.sc_off[w], M.scale[w] + row * P.ng_pad, sc, &R.full[s]);
-        bulk_g2s(dst + P.zp_off[w], M.zp[w] + row * P.zp_pad, zp, &R.full[s]);
+        mbar_expect_tx(&R.full[s], nr * (pay_row + sc_row + zp_row));
+        bulk_g2s(dst, pay_src + static_cast<int64_t>(rb) * pay_row, nr * pay_row, &R.full[s]);
+        bulk_g2s(dst + sc_off, sc_src + static_cast<int64_t>(rb) * sc_row, nr * sc_row, &R.full[s]);
+        bulk_g2s(dst + zp_off, zp_src + static_cast<int64_t>(rb) * zp_row, nr * zp_row, &R.full[s]);
       }
     }
   }
@@ -265,7 +270,7 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
 }
 
 template <int SW, int BB>
-__device__ void consume_gemv(const Phase& P, const Ring& R, float* red, int& t) {
+__device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float* red, int& t) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kw = warp % kSplit, rg = warp / kSplit;
   int64_t r0;
@@ -393,7 +398,7 @@ __device__ void gemv_epilogue(const Phase& P, const float* red, float (*sq_red)[
 }
 
 template <int BB>
-__device__ void run_gemv_phase(const Phase& P, const Ring& R, float* red, float (*sq_red)[kNCW], int& t) {
+__device__ __forceinline__ void run_gemv_phase(const Phase& P, const Ring R, float* red, float (*sq_red)[kNCW], int& t) {
   switch (P.sw) {
     case 1: consume_gemv<1, BB>(P, R, red, t); break;
     case 2:

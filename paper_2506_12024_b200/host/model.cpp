@@ -1,0 +1,474 @@
+// Model / MultiPrecisionLayer / KvCache of the C++ API over the device decoder (fq_model).
+// Reference semantics: /root/reference/proj/src/model.cpp (set_precision :268-278,
+// effective_bits :284-296, linear_layers order :304-330) and src/model_io.cpp (container).
+#include <chrono>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+
+#include "device_buffer.hpp"
+#include "flexquant/model.hpp"
+
+namespace flexquant {
+
+namespace {
+
+uint64_t now_ns() {
+  return static_cast<uint64_t>(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch()).count());
+}
+
+fq_model_config to_c(const ModelConfig& c) {
+  fq_model_config m{};
+  m.arch = static_cast<int32_t>(c.arch);
+  m.act_dtype = c.arch == Arch::Llama ? FQ_DT_BF16 : FQ_DT_F32;
+  m.vocab_size = c.vocab_size;
+  m.d_model = c.d_model;
+  m.n_heads = c.n_heads;
+  m.head_dim = c.head_dim;
+  m.n_layers = c.n_layers;
+  m.ffn_dim = c.ffn_dim;
+  m.max_seq_len = c.max_seq_len;
+  m.tie_embeddings = c.tie_embeddings ? 1 : 0;
+  m.max_batch = c.max_batch;
+  m.group_size = c.group_size;
+  m.norm_eps = c.norm_eps;
+  m.rope_theta = c.rope_theta;
+  return m;
+}
+
+}  // namespace
+
+void ModelConfig::validate() const {
+  if (vocab_size < 1 || d_model < 1 || n_heads < 1 || head_dim < 1 || n_layers < 1 || ffn_dim < 1 || max_seq_len < 1)
+    throw ConfigError("model config: all dimensions must be >= 1");
+  if (d_model != n_heads * head_dim) throw ConfigError("model config: d_model must equal n_heads * head_dim");
+}
+
+// ------------------------------------------------------------------ MultiPrecisionLayer
+MultiPrecisionLayer::MultiPrecisionLayer(std::string id, Tensor weight, Tensor bias, int64_t group_size)
+    : id_(std::move(id)), n_(weight.rows()), k_(weight.cols()), owned_(true), group_(group_size) {
+  if (bias.numel() != 0 && bias.numel() != n_)
+    throw DimensionError("layer " + id_ + ": bias length does not match output features");
+  detail::check(fq_layer_create(runtime(), n_, k_, group_size, &layer_));
+  detail::check(fq_layer_upload_fp(layer_, weight.data()));
+  if (bias.numel()) detail::check(fq_layer_upload_bias(layer_, bias.data()));
+  standalone_rung_ = Rung::Fp;
+  host_fp_ = std::move(weight);
+}
+
+MultiPrecisionLayer::~MultiPrecisionLayer() {
+  if (owned_ && layer_) fq_layer_destroy(layer_);
+}
+
+MultiPrecisionLayer::MultiPrecisionLayer(MultiPrecisionLayer&& o) noexcept { *this = std::move(o); }
+
+MultiPrecisionLayer& MultiPrecisionLayer::operator=(MultiPrecisionLayer&& o) noexcept {
+  if (this != &o) {
+    if (owned_ && layer_) fq_layer_destroy(layer_);
+    id_ = std::move(o.id_);
+    n_ = o.n_;
+    k_ = o.k_;
+    layer_ = o.layer_;
+    owned_ = o.owned_;
+    model_ = o.model_;
+    index_ = o.index_;
+    standalone_rung_ = o.standalone_rung_;
+    group_ = o.group_;
+    host_fp_ = std::move(o.host_fp_);
+    o.layer_ = nullptr;
+    o.owned_ = false;
+  }
+  return *this;
+}
+
+void MultiPrecisionLayer::quantize_rungs(QuantMode mode) {
+  if (host_fp_.numel() == 0) throw StateError("layer " + id_ + ": no fp weights to quantize");
+  set_quantized(Rung::Int8, quantize(host_fp_, 8, mode, group_));
+  set_quantized(Rung::Int4, quantize(host_fp_, 4, mode, group_));
+}
+
+Rung MultiPrecisionLayer::current() const {
+  if (model_) return model_->precision(index_);
+  return standalone_rung_;
+}
+
+bool MultiPrecisionLayer::has(Rung r) const {
+  int32_t o = 0;
+  detail::check(fq_layer_has(layer_, static_cast<int32_t>(r), &o));
+  return o != 0;
+}
+
+void MultiPrecisionLayer::set_current(Rung r) {
+  if (!has(r)) throw StateError("layer " + id_ + ": precision '" + to_string(r) + "' not available");
+  if (model_) {
+    detail::check(fq_model_set_rung(model_->handle(), 0, index_, static_cast<int32_t>(r)));
+  } else {
+    standalone_rung_ = r;
+  }
+}
+
+void MultiPrecisionLayer::set_quantized(Rung r, const QuantizedTensor& q) {
+  q.validate();
+  if (q.rows != n_ || q.cols != k_) throw DimensionError("layer " + id_ + ": quantized payload shape mismatch");
+  if (r == Rung::Fp) throw ConfigError("layer " + id_ + ": fp rung is not a quantized payload");
+  if (q.bits != quantized_bits(r)) throw ConfigError("layer " + id_ + ": expected " + std::to_string(quantized_bits(r)) + "-bit payload");
+  int64_t n = 0, k = 0, g = 0;
+  detail::check(fq_layer_shape(layer_, &n, &k, &g));
+  if (q.group() != g) throw ConfigError("layer " + id_ + ": quantization group does not match the layer");
+  detail::check(fq_layer_upload_quantized(layer_, static_cast<int32_t>(r), static_cast<int32_t>(q.mode),
+                                          q.payload.data(), static_cast<int64_t>(q.payload.size()), q.scale.data(),
+                                          q.zero_point.data(), static_cast<int64_t>(q.scale.size())));
+}
+
+QuantizedTensor MultiPrecisionLayer::quantized(Rung r) const {
+  if (r == Rung::Fp || !has(r))
+    throw StateError("layer " + id_ + ": no quantized payload for rung '" + to_string(r) + "'");
+  int64_t n = 0, k = 0, g = 0;
+  detail::check(fq_layer_shape(layer_, &n, &k, &g));
+  QuantizedTensor q;
+  q.bits = quantized_bits(r);
+  q.rows = n;
+  q.cols = k;
+  q.group_size = g >= k ? 0 : g;
+  q.payload.resize(q.expected_payload_bytes());
+  q.scale.resize(static_cast<size_t>(n * q.groups_per_row()));
+  q.zero_point.resize(q.scale.size());
+  detail::check(fq_layer_download_quantized(layer_, static_cast<int32_t>(r), q.payload.data(), q.scale.data(),
+                                            q.zero_point.data()));
+  return q;
+}
+
+Tensor MultiPrecisionLayer::forward(const Tensor& x, StepStats* stats) const {
+  const Rung r = current();
+  if (!has(r)) throw StateError("layer " + id_ + ": active precision has no payload");
+  if (x.cols() != k_) throw DimensionError("linear: input width " + x.shape_str() + " does not match weight");
+  const uint64_t t0 = now_ns();
+  const int64_t m = x.rows();
+  DeviceBuffer xd(sizeof(float) * x.numel()), yd(sizeof(float) * m * n_);
+  xd.upload(x.data(), sizeof(float) * x.numel());
+  detail::check(fq_gemv(runtime(), layer_, static_cast<int32_t>(r), m, xd.get(), FQ_DT_F32, yd.get(), FQ_DT_F32,
+                        FQ_NUMERICS_EXACT));
+  Tensor y({m, n_});
+  yd.download(y.data(), sizeof(float) * y.numel());
+  if (stats) {
+    const uint64_t dt = now_ns() - t0;
+    (r == Rung::Fp ? stats->ns_fp : r == Rung::Int8 ? stats->ns_int8 : stats->ns_int4) += dt;
+    stats->weight_bytes += static_cast<double>(param_count()) * accounting_bits(r) / 8.0;
+  }
+  return y;
+}
+
+Tensor linear(const Tensor& x, const Tensor& w, const Tensor& bias) {
+  if (w.cols() != x.cols()) throw DimensionError("linear: input width " + x.shape_str() + " does not match weight " + w.shape_str());
+  if (bias.numel() != 0 && bias.numel() != w.rows()) throw DimensionError("linear: bias length mismatch");
+  MultiPrecisionLayer l("linear", w, bias);
+  return l.forward(x, nullptr);
+}
+
+// ------------------------------------------------------------------ KvCache
+int64_t KvCache::length() const {
+  int64_t n = 0;
+  detail::check(fq_model_slot_length(model_->handle(), slot_, &n));
+  return n;
+}
+int64_t KvCache::max_length() const { return model_->config().max_seq_len; }
+
+// ------------------------------------------------------------------ Model
+Model::Model(ModelConfig cfg) : cfg_(cfg) {
+  cfg_.validate();
+  const fq_model_config c = to_c(cfg_);
+  detail::check(fq_model_create(runtime(), &c, &model_));
+  int32_t n = 0;
+  detail::check(fq_model_num_linears(model_, &n));
+  char buf[256];
+  for (int i = 0; i < n; ++i) {
+    detail::check(fq_model_linear_id(model_, i, buf, sizeof(buf)));
+    ids_.emplace_back(buf);
+    MultiPrecisionLayer l;
+    l.id_ = buf;
+    detail::check(fq_model_linear(model_, i, &l.layer_));
+    int64_t rows = 0, cols = 0, g = 0;
+    detail::check(fq_layer_shape(l.layer_, &rows, &cols, &g));
+    l.n_ = rows;
+    l.k_ = cols;
+    l.owned_ = false;
+    l.model_ = this;
+    l.index_ = i;
+    layers_.push_back(std::move(l));
+  }
+}
+
+Model::~Model() {
+  layers_.clear();
+  if (model_) fq_model_destroy(model_);
+}
+
+KvCache Model::make_cache(int slot) {
+  detail::check(fq_model_reset_slot(model_, slot));
+  KvCache c;
+  c.model_ = this;
+  c.slot_ = slot;
+  return c;
+}
+
+void Model::account_step(uint64_t ns, int slot) {
+  // per-rung buckets: the step's time split by each rung's share of the weight bytes
+  double b[3] = {0, 0, 0};
+  for (size_t i = 0; i < layers_.size(); ++i) {
+    const Rung r = precision(static_cast<int>(i), slot);
+    b[static_cast<int>(r)] += static_cast<double>(layers_[i].param_count()) * accounting_bits(r) / 8.0;
+  }
+  const double tot = b[0] + b[1] + b[2];
+  stats_.weight_bytes += tot;
+  stats_.ns_forward += ns;
+  if (tot > 0) {
+    stats_.ns_fp += static_cast<uint64_t>(ns * b[0] / tot);
+    stats_.ns_int8 += static_cast<uint64_t>(ns * b[1] / tot);
+    stats_.ns_int4 += static_cast<uint64_t>(ns * b[2] / tot);
+  }
+}
+
+std::vector<fq_row_stats> Model::prefill_rows(int slot, std::span<const TokenId> tokens) {
+  std::vector<fq_row_stats> st(tokens.size());
+  const uint64_t t0 = now_ns();
+  detail::check(fq_model_prefill(model_, slot, tokens.data(), static_cast<int64_t>(tokens.size()), nullptr, st.data()));
+  account_step(now_ns() - t0, slot);
+  return st;
+}
+
+std::vector<fq_row_stats> Model::decode_rows(std::span<const int32_t> slots, std::span<const TokenId> tokens) {
+  if (slots.size() != tokens.size()) throw DimensionError("decode: slots / tokens length mismatch");
+  std::vector<fq_row_stats> st(slots.size());
+  const uint64_t t0 = now_ns();
+  detail::check(fq_model_decode(model_, static_cast<int32_t>(slots.size()), slots.data(), tokens.data(), nullptr,
+                                st.data()));
+  account_step(now_ns() - t0, slots.empty() ? 0 : slots[0]);
+  return st;
+}
+
+Tensor Model::forward_prefill(std::span<const TokenId> tokens, KvCache& cache) {
+  const int64_t n = static_cast<int64_t>(tokens.size());
+  if (n < 1) throw InputError("prefill: empty prompt");
+  DeviceBuffer l(sizeof(float) * n * cfg_.vocab_size);
+  const uint64_t t0 = now_ns();
+  std::vector<fq_row_stats> st(tokens.size());
+  detail::check(fq_model_prefill(model_, cache.slot(), tokens.data(), n, static_cast<float*>(l.get()), st.data()));
+  account_step(now_ns() - t0, cache.slot());
+  Tensor out({n, cfg_.vocab_size});
+  l.download(out.data(), sizeof(float) * out.numel());
+  return out;
+}
+
+Tensor Model::forward_decode(TokenId token, KvCache& cache) {
+  DeviceBuffer l(sizeof(float) * cfg_.vocab_size);
+  const int32_t slot = cache.slot();
+  fq_row_stats st;
+  const uint64_t t0 = now_ns();
+  detail::check(fq_model_decode(model_, 1, &slot, &token, static_cast<float*>(l.get()), &st));
+  account_step(now_ns() - t0, slot);
+  Tensor out({1, cfg_.vocab_size});
+  l.download(out.data(), sizeof(float) * out.numel());
+  return out;
+}
+
+Rung Model::precision(int linear_index, int slot) const {
+  int32_t r = 0;
+  detail::check(fq_model_get_rung(model_, slot, linear_index, &r));
+  return static_cast<Rung>(r);
+}
+
+int Model::linear_index(std::string_view id) const {
+  for (size_t i = 0; i < ids_.size(); ++i)
+    if (ids_[i] == id) return static_cast<int>(i);
+  return -1;
+}
+
+MultiPrecisionLayer* Model::find_layer(std::string_view id) {
+  const int i = linear_index(id);
+  return i < 0 ? nullptr : &layers_[static_cast<size_t>(i)];
+}
+const MultiPrecisionLayer* Model::find_layer(std::string_view id) const {
+  const int i = linear_index(id);
+  return i < 0 ? nullptr : &layers_[static_cast<size_t>(i)];
+}
+
+std::optional<SwitchEvent> Model::set_precision(std::string_view layer_id, Rung bits, int slot) {
+  const int i = linear_index(layer_id);
+  if (i < 0) throw StateError("set_precision: unknown layer '" + std::string(layer_id) + "'");
+  if (!layers_[static_cast<size_t>(i)].has(bits))
+    throw StateError("set_precision: layer '" + std::string(layer_id) + "' has no rung '" + to_string(bits) + "'");
+  const Rung cur = precision(i, slot);
+  if (cur == bits) return std::nullopt;
+  detail::check(fq_model_set_rung(model_, slot, i, static_cast<int32_t>(bits)));
+  return SwitchEvent{ids_[static_cast<size_t>(i)], cur, bits};
+}
+
+void Model::set_all_precision(Rung bits, int slot) {
+  detail::check(fq_model_set_all_rungs(model_, slot, static_cast<int32_t>(bits)));
+}
+
+double Model::effective_bits(int slot) const {
+  double num = 0.0, den = 0.0;
+  for (size_t i = 0; i < layers_.size(); ++i) {
+    num += static_cast<double>(layers_[i].param_count()) * accounting_bits(precision(static_cast<int>(i), slot));
+    den += static_cast<double>(layers_[i].param_count());
+  }
+  return den > 0.0 ? num / den : 0.0;
+}
+
+double Model::weight_bytes_per_pass(int slot) const {
+  double b = 0.0;
+  for (size_t i = 0; i < layers_.size(); ++i)
+    b += static_cast<double>(layers_[i].param_count()) * accounting_bits(precision(static_cast<int>(i), slot)) / 8.0;
+  return b;
+}
+
+void Model::set_param(const std::string& name, const Tensor& t) {
+  detail::check(fq_model_set_param(model_, name.c_str(), t.data(), t.numel()));
+}
+
+void Model::init_random(uint64_t seed, float std) { detail::check(fq_model_init_random(model_, seed, std)); }
+
+double effective_bits(std::span<const MultiPrecisionLayer* const> layers) {
+  double num = 0.0, den = 0.0;
+  for (const MultiPrecisionLayer* l : layers) {
+    num += static_cast<double>(l->param_count()) * accounting_bits(l->current());
+    den += static_cast<double>(l->param_count());
+  }
+  return den > 0.0 ? num / den : 0.0;
+}
+
+// ------------------------------------------------------------------ weights container
+namespace {
+
+struct Reader {
+  std::ifstream is;
+  uint32_t u32() {
+    uint32_t v;
+    if (!is.read(reinterpret_cast<char*>(&v), 4)) throw FormatError("weights file: unexpected end of file");
+    return v;
+  }
+  uint8_t u8() {
+    char c;
+    if (!is.get(c)) throw FormatError("weights file: unexpected end of file");
+    return static_cast<uint8_t>(c);
+  }
+  void bytes(void* p, size_t n) {
+    if (!is.read(static_cast<char*>(p), static_cast<std::streamsize>(n))) throw FormatError("weights file: unexpected end of file");
+  }
+};
+
+int64_t field(const std::string& line, const std::string& key) {
+  const size_t p = line.find(key + "=");
+  if (p == std::string::npos) throw FormatError("weights file: config field '" + key + "' missing");
+  return std::stoll(line.substr(p + key.size() + 1));
+}
+
+}  // namespace
+
+std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch) {
+  Reader r;
+  r.is.open(path, std::ios::binary);
+  if (!r.is) throw FormatError("cannot open weights file: " + path);
+  std::string line;
+  if (!std::getline(r.is, line) || line != "flexquant-weights v1") throw FormatError("weights file: bad or missing header");
+  if (!std::getline(r.is, line)) throw FormatError("weights file: missing config line");
+  ModelConfig cfg;
+  cfg.vocab_size = field(line, "vocab_size");
+  cfg.d_model = field(line, "d_model");
+  cfg.n_heads = field(line, "n_heads");
+  cfg.head_dim = field(line, "head_dim");
+  cfg.n_layers = field(line, "n_layers");
+  cfg.ffn_dim = field(line, "ffn_dim");
+  cfg.max_seq_len = field(line, "max_seq_len");
+  cfg.tie_embeddings = field(line, "tie_embeddings") != 0;
+  cfg.arch = Arch::Reference;
+  cfg.group_size = 0;
+  cfg.max_batch = max_batch;
+  if (!std::getline(r.is, line)) throw FormatError("weights file: missing tensor count line");
+  const int64_t count = field(line, "tensor_count");
+  auto model = std::make_unique<Model>(cfg);
+  struct Q {
+    int bits, mode;
+    uint32_t rows, cols;
+    std::vector<float> scale;
+    std::vector<int32_t> zp;
+    std::vector<uint8_t> payload;
+  };
+  std::map<std::string, Tensor> tensors;
+  std::map<std::string, Q> quants;
+  for (int64_t i = 0; i < count; ++i) {
+    const uint32_t nl = r.u32();
+    if (nl > 4096) throw FormatError("weights file: unreasonable tensor name length");
+    std::string name(nl, '\0');
+    r.bytes(name.data(), nl);
+    const uint8_t dtype = r.u8();
+    if (dtype == 0) {
+      const uint32_t nd = r.u32();
+      if (nd == 0 || nd > 4) throw FormatError("weights file: bad tensor rank");
+      std::vector<int64_t> shape(nd);
+      int64_t numel = 1;
+      for (auto& s : shape) {
+        s = r.u32();
+        numel *= s;
+      }
+      std::vector<float> data(static_cast<size_t>(numel));
+      r.bytes(data.data(), sizeof(float) * data.size());
+      tensors.emplace(name, Tensor::from_data(shape, std::move(data)));
+    } else if (dtype == 1) {
+      Q q;
+      q.bits = r.u8();
+      q.mode = r.u8();
+      if (q.mode > 1) throw FormatError("weights file: bad quantization mode");
+      q.rows = r.u32();
+      q.cols = r.u32();
+      q.scale.resize(q.rows);
+      q.zp.resize(q.rows);
+      r.bytes(q.scale.data(), 4 * q.scale.size());
+      r.bytes(q.zp.data(), 4 * q.zp.size());
+      q.payload.resize((static_cast<size_t>(q.rows) * q.cols * q.bits + 7) / 8);
+      r.bytes(q.payload.data(), q.payload.size());
+      quants.emplace(name, std::move(q));
+    } else {
+      throw FormatError("weights file: unknown dtype tag");
+    }
+  }
+  auto take = [&](const std::string& n) -> Tensor& {
+    auto it = tensors.find(n);
+    if (it == tensors.end()) throw FormatError("weights file: tensor '" + n + "' missing");
+    return it->second;
+  };
+  model->set_param("tok_emb", take("tok_emb"));
+  model->set_param("pos_emb", take("pos_emb"));
+  for (int64_t i = 0; i < cfg.n_layers; ++i) {
+    const std::string p = "blocks." + std::to_string(i) + ".";
+    for (const char* nm : {"ln1.gamma", "ln1.beta", "ln2.gamma", "ln2.beta"}) model->set_param(p + nm, take(p + nm));
+  }
+  model->set_param("final_norm.gamma", take("ln_f.gamma"));
+  model->set_param("final_norm.beta", take("ln_f.beta"));
+  for (size_t i = 0; i < model->num_linears(); ++i) {
+    const std::string& id = model->linear_ids()[i];
+    fq_layer* L = model->linear(static_cast<int>(i)).handle();
+    detail::check(fq_layer_upload_fp(L, take(id).data()));
+    detail::check(fq_layer_upload_bias(L, take(id + ".bias").data()));
+    for (const auto& [tag, rung] : {std::pair<const char*, int>{".w8", FQ_RUNG_INT8}, {".w4", FQ_RUNG_INT4}}) {
+      auto it = quants.find(id + tag);
+      if (it == quants.end()) {
+        // files without stored rungs are RTN-quantized at load time (src/model_io.cpp:226-229)
+        const QuantizedTensor q = quantize(take(id), rung == FQ_RUNG_INT8 ? 8 : 4, QuantMode::Asymmetric);
+        detail::check(fq_layer_upload_quantized(L, rung, 0, q.payload.data(), static_cast<int64_t>(q.payload.size()),
+                                                q.scale.data(), q.zero_point.data(), static_cast<int64_t>(q.scale.size())));
+        continue;
+      }
+      const Q& q = it->second;
+      detail::check(fq_layer_upload_quantized(L, rung, q.mode, q.payload.data(), static_cast<int64_t>(q.payload.size()),
+                                              q.scale.data(), q.zp.data(), static_cast<int64_t>(q.scale.size())));
+    }
+  }
+  model->set_all_precision(Rung::Fp);
+  return model;
+}
+
+}  // namespace flexquant
