@@ -119,7 +119,8 @@ class Model {
   Model& operator=(const Model&) = delete;
 
   const ModelConfig& config() const { return cfg_; }
-  KvCache make_cache(int slot = 0);
+  KvCache make_cache(int slot = 0);          // empties the slot's history
+  KvCache attach_cache(int slot = 0) const;  // handle on the slot's current history
 
   Tensor forward_prefill(std::span<const TokenId> tokens, KvCache& cache);
   Tensor forward_decode(TokenId token, KvCache& cache);

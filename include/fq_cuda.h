@@ -7,7 +7,7 @@
  * message is available from fq_last_error() (thread-local).  Status codes map
  * one-to-one onto the reference's exception hierarchy
  * (/root/reference/proj/include/flexquant/error.hpp:10-49) so the C++ wrapper
- * (include/flexquant/*.hpp) can rethrow the matching flexquant::Error subclass.
+ * (the headers under include/flexquant) can rethrow the matching flexquant::Error subclass.
  *
  * Pointer convention: arguments named *_host are host memory, *_dev are device
  * (cudaMalloc / torch CUDA) memory.  All device work is ordered on the stream

@@ -213,6 +213,14 @@ KvCache Model::make_cache(int slot) {
   return c;
 }
 
+KvCache Model::attach_cache(int slot) const {
+  if (slot < 0 || slot >= cfg_.max_batch) throw InputError("slot out of range");
+  KvCache c;
+  c.model_ = this;
+  c.slot_ = slot;
+  return c;
+}
+
 void Model::account_step(uint64_t ns, int slot) {
   // per-rung buckets: the step's time split by each rung's share of the weight bytes
   double b[3] = {0, 0, 0};
