@@ -119,12 +119,12 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
     M.y = g.mat[m].y ? static_cast<char*>(g.mat[m].y) + b0 * g.y_stride * ysz : nullptr;
   }
   // ring-slot layout of this phase (per bit-width)
-  const int64_t target = 24 * 1024;
+  const int64_t target = 40 * 1024;
   for (int w = 0; w < 2; ++w) {
     const int64_t row_bytes = w == 0 ? P.K : P.K / 2;
     const int64_t per_row = row_bytes + P.ng_pad * 4 + P.zp_pad;
     int rps = static_cast<int>(std::max<int64_t>(1, target / per_row));
-    rps = std::min(rps, 16);
+    rps = std::min(rps, 32);
     const int quantum = 4 * kRG;
     rps = rps >= quantum ? rps / quantum * quantum : quantum;
     const int64_t pad = (rps + 3) / 4 * 4;
@@ -138,6 +138,7 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
   const int64_t rows_max = (P.N + grid - 1) / grid;
   red_floats = std::max<int64_t>(red_floats, static_cast<int64_t>(g.nmat) * rows_max * kSplit * (bb == 3 ? 4 : bb));
   max_sw = std::max(max_sw, P.sw);
+  max_nsteps = std::max(max_nsteps, P.nsteps);
   max_bb = std::max(max_bb, bb);
   phases.push_back(P);
 }

@@ -103,6 +103,7 @@ struct ProgramBuilder {
   int64_t red_floats = 0;
   int max_sw = 1;
   int max_bb = 1;
+  int max_nsteps = 1;
   void add_gemv(const GemvLaunch& g, int64_t b0, int bb);
   void add(const Phase& p);
 };
@@ -116,6 +117,8 @@ struct ProgramRun {
   int nstages = 0;
   size_t smem = 0;
   int bb = 1;
+  int red_floats = 0;
+  int xs_floats = 0;
   unsigned int* barrier = nullptr;  // grid-barrier counter (reset before every launch)
 };
 

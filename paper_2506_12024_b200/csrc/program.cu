@@ -159,7 +159,7 @@ struct Ring {
 // ---------------------------------------------------------------- producer
 // All phase fields are copied into registers before the stage loop: the asm statements carry
 // "memory" clobbers, so anything left in memory would be reloaded after every copy / wait.
-__device__ __forceinline__ void produce_phase(const Phase& P, const Ring R, int& t) {
+__device__ __forceinline__ void produce_phase(const Phase& P, const Ring R, int& slot_i, uint32_t& phase_bit) {
   int64_t r0;
   int rows;
   cta_rows(P.N, r0, rows);
@@ -177,10 +177,13 @@ __device__ __forceinline__ void produce_phase(const Phase& P, const Ring R, int&
       const uint32_t sc_off = static_cast<uint32_t>(P.sc_off[w]), zp_off = static_cast<uint32_t>(P.zp_off[w]);
       const uint32_t pay_row = static_cast<uint32_t>(row_bytes), sc_row = static_cast<uint32_t>(ng_pad * 4),
                      zp_row = static_cast<uint32_t>(zp_pad);
-      for (int rb = 0; rb < rows; rb += rps, ++t) {
-        const int s = t % R.nstages;
-        const uint32_t ph = (t / R.nstages) & 1;
-        mbar_wait(&R.empty[s], ph ^ 1);
+      for (int rb = 0; rb < rows; rb += rps) {
+        const int s = slot_i;
+        mbar_wait(&R.empty[s], phase_bit ^ 1u);
+        if (++slot_i == R.nstages) {
+          slot_i = 0;
+          phase_bit ^= 1u;
+        }
         const uint32_t nr = static_cast<uint32_t>(min(rps, rows - rb));
         uint8_t* dst = R.base + static_cast<size_t>(s) * R.stage_bytes;
         mbar_expect_tx(&R.full[s], nr * (pay_row + sc_row + zp_row));
@@ -193,38 +196,53 @@ __device__ __forceinline__ void produce_phase(const Phase& P, const Ring R, int&
 }
 
 // ---------------------------------------------------------------- consumers: GEMV
-template <int SW, int BB>
-__device__ __forceinline__ void load_acts(const Phase& P, int bits, const bool (&step_ok)[SW], const int (&seg_k)[SW],
-                                          const float (&rstd)[BB], float (&xs)[SW][BB][kSegCodes],
-                                          float (&sig)[SW][BB]) {
+// Activations of a GEMV phase are staged once per phase (and bit-width) in shared memory,
+// pre-scaled by the bit pattern of the rung: xsm[b][step][j4][lane] float4 (a lane's 16 values
+// of a step as four conflict-free 16-byte chunks) and sigm[b][step][lane] = sum of the 16 values
+// * 2^-40 (zero-point folding).  All consumer threads cooperate.
+template <int BB>
+__device__ void stage_acts(const Phase& P, int bits, const float (&rstd)[BB], float4* xsm, float* sigm) {
+  const int nsteps = P.nsteps;
+  const int nseg = nsteps * 32;
+  const int64_t K = P.K;
+  const void* x = P.x;
+  const int xdt = P.x_dtype, adt = P.act_dtype;
+  const int64_t xstride = P.x_stride;
+  const float* gain = P.norm_gain;
+  for (int i = threadIdx.x; i < nseg * BB; i += kNCW * 32) {
+    const int b = i / nseg, seg = i - b * nseg;
+    const int step = seg >> 5, ln = seg & 31;
+    const int64_t k0 = static_cast<int64_t>(step) * kStepCodes + ln * kSegCodes;
+    float v[kSegCodes];
+    float acc = 0.f;
 #pragma unroll
-  for (int s = 0; s < SW; ++s) {
-#pragma unroll
-    for (int b = 0; b < BB; ++b) {
-      float acc = 0.f;
-#pragma unroll
-      for (int j = 0; j < kSegCodes; ++j) {
-        float v = 0.f;
-        if (step_ok[s] && b < P.B) {
-          const int64_t k = seg_k[s] + j;
-          v = load_act(P.x, P.x_dtype, b * P.x_stride + k);
-          if (P.norm_gain != nullptr) v = round_act(v * rstd[b] * P.norm_gain[k], P.act_dtype);
-        }
-        acc += v;
-        const float sc8 = kTwo109 / static_cast<float>(1u << seg_shift(8, j));
-        const float sc4 = kTwo109 / static_cast<float>(1u << seg_shift(4, j));
-        xs[s][b][j] = v * (bits == 8 ? sc8 : sc4);
+    for (int j = 0; j < kSegCodes; ++j) {
+      float t = 0.f;
+      if (k0 + j < K && b < P.B) {
+        t = load_act(x, xdt, b * xstride + k0 + j);
+        if (gain != nullptr) t = round_act(t * rstd[b] * gain[k0 + j], adt);
       }
-      sig[s][b] = acc * kTwoM40;
+      acc += t;
+      const float sc8 = kTwo109 / static_cast<float>(1u << seg_shift(8, j));
+      const float sc4 = kTwo109 / static_cast<float>(1u << seg_shift(4, j));
+      v[j] = t * (bits == 8 ? sc8 : sc4);
     }
+    float4* dst = xsm + (static_cast<size_t>(b * nsteps + step) * 4) * 32 + ln;
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) dst[j4 * 32] = make_float4(v[4 * j4], v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+    sigm[static_cast<size_t>(b * nsteps + step) * 32 + ln] = acc * kTwoM40;
   }
 }
 
+// Consumes one ring slot holding `nrows` rows at bit-width BITS: row quads are split between the
+// kRG row groups; within a quad the loop runs over this warp's K-steps (activations loaded from
+// shared memory once per step) and then the four rows.
 template <int BITS, int SW, int BB>
 __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, int nrows, int rg, int row_bytes,
                                               int sc_off, int zp_off, int sc_row, int zp_row, const int (&pay_l)[SW],
-                                              const int (&sc_l)[SW], const int (&zp_l)[SW], float zmagic,
-                                              const float (&xs)[SW][BB][kSegCodes], const float (&sig)[SW][BB],
+                                              const int (&sc_l)[SW], const int (&zp_l)[SW], const int (&step_of)[SW],
+                                              const bool (&step_ok)[SW], int nsteps, float zmagic,
+                                              const float4* __restrict__ xsm, const float* __restrict__ sigm,
                                               float* red_row, int bmask, int lane) {
   const uint8_t* pa = slot + rg * 4 * row_bytes;
   const uint8_t* sa = slot + sc_off + rg * 4 * sc_row;
@@ -237,9 +255,25 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc[b][u] = 0.f;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int s = 0; s < SW; ++s) {
+      if (!step_ok[s]) continue;
+      float xs[BB][kSegCodes];
+      float sg[BB];
 #pragma unroll
-      for (int s = 0; s < SW; ++s) {
+      for (int b = 0; b < BB; ++b) {
+        const float4* src = xsm + (static_cast<size_t>(b * nsteps + step_of[s]) * 4) * 32 + lane;
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 f = src[j4 * 32];
+          xs[b][4 * j4] = f.x;
+          xs[b][4 * j4 + 1] = f.y;
+          xs[b][4 * j4 + 2] = f.z;
+          xs[b][4 * j4 + 3] = f.w;
+        }
+        sg[b] = sigm[static_cast<size_t>(b * nsteps + step_of[s]) * 32 + lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
         const float sc = *reinterpret_cast<const float*>(sa + u * sc_row + sc_l[s]);
         const uint32_t zq = za[u * zp_row + zp_l[s]];
         const float zf = __uint_as_float(0x4B000000u | zq) - zmagic;  // exact: zq + zp_base
@@ -247,14 +281,14 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
         if constexpr (BITS == 8) {
           const uint4 w = *reinterpret_cast<const uint4*>(pa + u * row_bytes + pay_l[s]);
 #pragma unroll
-          for (int b = 0; b < BB; ++b) p[b] = dot_seg8(w, xs[s][b]);
+          for (int b = 0; b < BB; ++b) p[b] = dot_seg8(w, xs[b]);
         } else {
           const uint2 w = *reinterpret_cast<const uint2*>(pa + u * row_bytes + pay_l[s]);
 #pragma unroll
-          for (int b = 0; b < BB; ++b) p[b] = dot_seg4(w, xs[s][b]);
+          for (int b = 0; b < BB; ++b) p[b] = dot_seg4(w, xs[b]);
         }
 #pragma unroll
-        for (int b = 0; b < BB; ++b) acc[b][u] = fmaf(sc, fmaf(-zf, sig[s][b], p[b]), acc[b][u]);
+        for (int b = 0; b < BB; ++b) acc[b][u] = fmaf(sc, fmaf(-zf, sg[b], p[b]), acc[b][u]);
       }
     }
     const int u = (lane >> 3) & 3;
@@ -270,21 +304,25 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
 }
 
 template <int SW, int BB>
-__device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float* red, int& t) {
+__device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float* red, float4* xsm, float* sigm,
+                                             int& slot_i, uint32_t& phase_bit) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kw = warp % kSplit, rg = warp / kSplit;
   int64_t r0;
   int rows;
   cta_rows(P.N, r0, rows);
+  const int nsteps = P.nsteps;
+  const int64_t K = P.K, G = P.G;
   bool step_ok[SW];
-  int seg_k[SW], gidx[SW];
+  int step_of[SW], seg_k[SW], gidx[SW];
 #pragma unroll
   for (int s = 0; s < SW; ++s) {
-    const int step = kw + s * kSplit;
-    seg_k[s] = step * kStepCodes + lane * kSegCodes;
-    step_ok[s] = step < P.nsteps && seg_k[s] < P.K;
-    gidx[s] = step_ok[s] ? static_cast<int>(seg_k[s] / P.G) : 0;
-    if (!step_ok[s]) seg_k[s] = 0;
+    step_of[s] = kw + s * kSplit;
+    seg_k[s] = step_of[s] * kStepCodes + lane * kSegCodes;
+    step_ok[s] = step_of[s] < nsteps;
+    gidx[s] = (step_ok[s] && seg_k[s] < K) ? static_cast<int>(seg_k[s] / G) : 0;
+    if (!step_ok[s] || seg_k[s] >= K) seg_k[s] = 0;
+    if (!step_ok[s]) step_of[s] = 0;
   }
   float rstd[BB];
 #pragma unroll
@@ -295,24 +333,26 @@ __device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float
       for (int i = lane; i < P.n_partials; i += 32) s += P.norm_partials[b * P.partials_stride + i];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      rstd[b] = 1.0f / sqrtf(s / static_cast<float>(P.K) + P.norm_eps);
+      rstd[b] = 1.0f / sqrtf(s / static_cast<float>(K) + P.norm_eps);
     }
   }
-  float xs[SW][BB][kSegCodes];
-  float sig[SW][BB];
   int xs_bits = 0;
-  for (int m = 0; m < P.nmat; ++m) {
+  const int nmat = P.nmat;
+  for (int m = 0; m < nmat; ++m) {
     for (int w = 0; w < 2; ++w) {
       const int bmask = pass_mask(P, m, w);
-      if (bmask == 0 || rows == 0) continue;
+      if (bmask == 0) continue;
       const int bits = w == 0 ? 8 : 4;
       if (xs_bits != bits) {
-        load_acts<SW, BB>(P, bits, step_ok, seg_k, rstd, xs, sig);
+        named_sync(1, kNCW * 32);  // previous users of the staging area are done
+        stage_acts<BB>(P, bits, rstd, xsm, sigm);
+        named_sync(1, kNCW * 32);
         xs_bits = bits;
       }
+      if (rows == 0) continue;
       const float zmagic = 8388608.0f - static_cast<float>(P.mat[m].zpbase[w]);
       const int rps = P.rows_per_stage[w];
-      const int row_bytes = static_cast<int>(w == 0 ? P.K : P.K / 2);
+      const int row_bytes = static_cast<int>(w == 0 ? K : K / 2);
       int pay_l[SW], sc_l[SW], zp_l[SW];
 #pragma unroll
       for (int s = 0; s < SW; ++s) {
@@ -321,21 +361,23 @@ __device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float
         zp_l[s] = gidx[s];
       }
       const int sco = P.sc_off[w], zpo = P.zp_off[w], scr = P.sc_row, zpr = P.zp_row;
-      for (int rb = 0; rb < rows; rb += rps, ++t) {
-        const int s = t % R.nstages;
-        const uint32_t ph = (t / R.nstages) & 1;
-        mbar_wait(&R.full[s], ph);
-        const uint8_t* slot = R.base + static_cast<size_t>(s) * R.stage_bytes;
+      for (int rb = 0; rb < rows; rb += rps) {
+        mbar_wait(&R.full[slot_i], phase_bit);
+        const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * R.stage_bytes;
         float* red_row = red + ((m * rows + rb) * kSplit + kw) * BB;
         const int nr = min(rps, rows - rb);
         if (bits == 8)
-          consume_stage<8, SW, BB>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, zmagic, xs, sig,
-                                   red_row, bmask, lane);
+          consume_stage<8, SW, BB>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
+                                   nsteps, zmagic, xsm, sigm, red_row, bmask, lane);
         else
-          consume_stage<4, SW, BB>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, zmagic, xs, sig,
-                                   red_row, bmask, lane);
+          consume_stage<4, SW, BB>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
+                                   nsteps, zmagic, xsm, sigm, red_row, bmask, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[s]);
+        if (lane == 0) mbar_arrive(&R.empty[slot_i]);
+        if (++slot_i == R.nstages) {
+          slot_i = 0;
+          phase_bit ^= 1u;
+        }
       }
     }
   }
@@ -398,17 +440,18 @@ __device__ void gemv_epilogue(const Phase& P, const float* red, float (*sq_red)[
 }
 
 template <int BB>
-__device__ __forceinline__ void run_gemv_phase(const Phase& P, const Ring R, float* red, float (*sq_red)[kNCW], int& t) {
+__device__ __forceinline__ void run_gemv_phase(const Phase& P, const Ring R, float* red, float (*sq_red)[kNCW],
+                                               float4* xsm, float* sigm, int& slot_i, uint32_t& phase_bit) {
   switch (P.sw) {
-    case 1: consume_gemv<1, BB>(P, R, red, t); break;
+    case 1: consume_gemv<1, BB>(P, R, red, xsm, sigm, slot_i, phase_bit); break;
     case 2:
-      if constexpr (BB <= 2) consume_gemv<2, BB>(P, R, red, t);
+      if constexpr (BB <= 2) consume_gemv<2, BB>(P, R, red, xsm, sigm, slot_i, phase_bit);
       break;
     case 3:
-      if constexpr (BB == 1) consume_gemv<3, BB>(P, R, red, t);
+      if constexpr (BB == 1) consume_gemv<3, BB>(P, R, red, xsm, sigm, slot_i, phase_bit);
       break;
     default:
-      if constexpr (BB == 1) consume_gemv<4, BB>(P, R, red, t);
+      if constexpr (BB == 1) consume_gemv<4, BB>(P, R, red, xsm, sigm, slot_i, phase_bit);
       break;
   }
   named_sync(1, kNCW * 32);
@@ -665,7 +708,8 @@ __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
 
 // ---------------------------------------------------------------- the program kernel
 template <int BB>
-__device__ void run_program(const Phase* phases, int nphases, unsigned int* barrier, int stage_bytes, int nstages) {
+__device__ void run_program(const Phase* phases, int nphases, unsigned int* barrier, int stage_bytes, int nstages,
+                            int red_floats, int xs_floats) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float sq_red[kMaxB][kNCW];
   __shared__ AttnSmem attn_smem[kNCW / 4];
@@ -677,6 +721,8 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   R.stage_bytes = stage_bytes;
   R.nstages = nstages;
   float* red = reinterpret_cast<float*>(R.empty + kMaxStages);
+  float4* xsm = reinterpret_cast<float4*>(red + ((red_floats + 3) & ~3));
+  float* sigm = reinterpret_cast<float*>(xsm + xs_floats / 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nstages; ++s) {
@@ -689,18 +735,20 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   if (warp == kNCW) {
     // the weight stream depends on nothing produced at run time: start immediately
     if (lane == 0) {
-      int t = 0;
+      int slot_i = 0;
+      uint32_t phase_bit = 0;
       for (int i = 0; i < nphases; ++i)
-        if (phases[i].type == PH_GEMV) produce_phase(phases[i], R, t);
+        if (phases[i].type == PH_GEMV) produce_phase(phases[i], R, slot_i, phase_bit);
     }
     return;
   }
   pdl_wait();
-  int t = 0;
+  int slot_i = 0;
+  uint32_t phase_bit = 0;
   unsigned int epoch = 0;
   for (int i = 0; i < nphases; ++i) {
     const Phase& P = phases[i];
-    if (P.type == PH_GEMV) run_gemv_phase<BB>(P, R, red, sq_red, t);
+    if (P.type == PH_GEMV) run_gemv_phase<BB>(P, R, red, sq_red, xsm, sigm, slot_i, phase_bit);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
     else if (P.type == PH_ATTN) run_attn(P, attn_smem);
     else run_stats(P, stat_smem);
@@ -710,15 +758,17 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
 
 template <int BB>
 __global__ void __launch_bounds__(kThreads, 1) program_kernel(const Phase* phases, int nphases, unsigned int* barrier,
-                                                              int stage_bytes, int nstages) {
-  run_program<BB>(phases, nphases, barrier, stage_bytes, nstages);
+                                                              int stage_bytes, int nstages, int red_floats,
+                                                              int xs_floats) {
+  run_program<BB>(phases, nphases, barrier, stage_bytes, nstages, red_floats, xs_floats);
 }
 
 template <int BB>
 __global__ void __launch_bounds__(kThreads, 1) program_kernel_inline(const __grid_constant__ InlineProgram prog,
                                                                      int nphases, unsigned int* barrier,
-                                                                     int stage_bytes, int nstages) {
-  run_program<BB>(prog.phases, nphases, barrier, stage_bytes, nstages);
+                                                                     int stage_bytes, int nstages, int red_floats,
+                                                                     int xs_floats) {
+  run_program<BB>(prog.phases, nphases, barrier, stage_bytes, nstages, red_floats, xs_floats);
 }
 
 template <int BB>
@@ -745,10 +795,10 @@ void launch_t(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, bool pd
   cfg.numAttrs = pdl ? 1 : 0;
   if (run.dev_phases)
     FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel<BB>, static_cast<const Phase*>(run.dev_phases), run.nphases,
-                               barrier, run.stage_bytes, run.nstages));
+                               barrier, run.stage_bytes, run.nstages, run.red_floats, run.xs_floats));
   else
     FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel_inline<BB>, run.inl, run.nphases, barrier, run.stage_bytes,
-                               run.nstages));
+                               run.nstages, run.red_floats, run.xs_floats));
   ctx->launches += 1;
 }
 
@@ -760,12 +810,16 @@ ProgramRun upload_program(fq_ctx* ctx, const ProgramBuilder& pb, bool transient)
   r.grid = pb.grid;
   r.bb = pb.max_bb;
   const int64_t stage = std::max<int64_t>(pb.stage_bytes, 128);
-  const size_t red_bytes = static_cast<size_t>(pb.red_floats) * sizeof(float);
-  const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes) - 2 * kMaxStages * 8 - 256;
+  r.red_floats = static_cast<int>((pb.red_floats + 3) & ~int64_t(3));
+  r.xs_floats = static_cast<int>(static_cast<int64_t>(pb.max_nsteps) * kStepCodes * pb.max_bb);
+  const size_t red_bytes = static_cast<size_t>(r.red_floats) * sizeof(float);
+  const size_t xs_bytes = static_cast<size_t>(r.xs_floats) * sizeof(float) +
+                          static_cast<size_t>(pb.max_nsteps) * 32 * pb.max_bb * sizeof(float);
+  const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes + xs_bytes) - 2 * kMaxStages * 8 - 256;
   r.nstages = static_cast<int>(std::min<int64_t>(kMaxStages, budget / stage));
   if (r.nstages < 2) fail(FQ_E_CONFIG, "gemv: layer rows too large for the shared-memory ring");
   r.stage_bytes = static_cast<int>(stage);
-  r.smem = static_cast<size_t>(r.nstages) * r.stage_bytes + 2 * kMaxStages * 8 + red_bytes;
+  r.smem = static_cast<size_t>(r.nstages) * r.stage_bytes + 2 * kMaxStages * 8 + red_bytes + xs_bytes;
   if (r.nphases <= kInlinePhases && transient) {
     for (int i = 0; i < r.nphases; ++i) r.inl.phases[i] = pb.phases[i];
   } else {
