@@ -125,9 +125,10 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
     const int64_t per_row = row_bytes + P.ng_pad * 4 + P.zp_pad;
     int rps = static_cast<int>(std::max<int64_t>(1, target / per_row));
     rps = std::min(rps, 32);
-    const int quantum = 4 * kRG;
+    // row groups consume octets (1 step, B=1), quads (1 step) or pairs (several steps)
+    const int quantum = (P.sw == 1 ? (bb == 1 ? 8 : 4) : 2) * kRG;
     rps = rps >= quantum ? rps / quantum * quantum : quantum;
-    const int64_t pad = (rps + 3) / 4 * 4;
+    const int64_t pad = (rps + 7) / 8 * 8;
     P.rows_per_stage[w] = rps;
     P.sc_off[w] = static_cast<int>(pad * row_bytes);
     P.zp_off[w] = static_cast<int>(pad * row_bytes + pad * P.ng_pad * 4);
@@ -137,6 +138,7 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
   P.zp_row = static_cast<int>(P.zp_pad);
   const int64_t rows_max = (P.N + grid - 1) / grid;
   red_floats = std::max<int64_t>(red_floats, static_cast<int64_t>(g.nmat) * rows_max * kSplit * (bb == 3 ? 4 : bb));
+  if (bb > 1 && P.sw > (bb <= 2 ? 2 : 1)) fail(FQ_E_CONFIG, "gemv: batch chunk too large for the K-steps per warp");
   max_sw = std::max(max_sw, P.sw);
   max_nsteps = std::max(max_nsteps, P.nsteps);
   max_bb = std::max(max_bb, bb);

@@ -496,6 +496,15 @@ void require(bool c, fq_status code, const std::string& msg) {
 
 void launch_dev(fq_model* M) { M->ctx->launches += 1; }
 
+// Adds a GEMV for B batch rows as independent phases of at most gemv_batch_chunk(K) rows.
+void add_chunked(ProgramBuilder& pb, const GemvLaunch& g, int B) {
+  const int chunk = gemv_batch_chunk(g.mat[0].layer->K);
+  for (int b0 = 0; b0 < B; b0 += chunk) {
+    pb.add_gemv(g, b0, std::min(chunk, B - b0));
+    pb.phases.back().barrier_after = b0 + chunk >= B ? 1 : 0;
+  }
+}
+
 bool capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cs);
@@ -561,7 +570,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
         g.epi = EPI_SPLIT3;
         g.y_dtype = c.act_dtype;
         g.y_stride = d;
-        pb.add_gemv(g, 0, B);
+        add_chunked(pb, g, B);
         if (!gemv_only) {
           Phase a{};
           a.type = PH_ATTN;
@@ -598,7 +607,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
         o.resid_stride = d;
         o.out_partials = M->partials[cur ^ 1];
         o.out_n_partials = kPartStride;
-        pb.add_gemv(o, 0, B);
+        add_chunked(pb, o, B);
         cur ^= 1;
         GemvLaunch gu;
         gu.nmat = 2;
@@ -620,7 +629,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
         gu.y = M->mid;
         gu.y_dtype = c.act_dtype;
         gu.y_stride = c.ffn_dim;
-        pb.add_gemv(gu, 0, B);
+        add_chunked(pb, gu, B);
         GemvLaunch dn;
         dn.nmat = 1;
         dn.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 6)];
@@ -634,7 +643,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
         dn.resid_stride = d;
         dn.out_partials = M->partials[cur ^ 1];
         dn.out_n_partials = kPartStride;
-        pb.add_gemv(dn, 0, B);
+        add_chunked(pb, dn, B);
         cur ^= 1;
       }
       GemvLaunch hd;
@@ -655,7 +664,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
       hd.y = M->logits;
       hd.y_dtype = FQ_DT_F32;
       hd.y_stride = V;
-      pb.add_gemv(hd, 0, B);
+      add_chunked(pb, hd, B);
       if (!gemv_only) {
         Phase sp{};
         sp.type = PH_STATS;

@@ -132,6 +132,42 @@ __device__ __forceinline__ void cta_rows(int64_t N, int64_t& r0, int& rows) {
   rows = static_cast<int>((N * (blockIdx.x + 1)) / gridDim.x - r0);
 }
 
+// Reduces v[0..7] across the 32 lanes (9 shuffles); afterwards lane l holds the warp sum of
+// row (l>>2)&7.
+__device__ __forceinline__ float reduce8(const float (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  float k[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float keep = b4 ? v[4 + i] : v[i], send = b4 ? v[i] : v[4 + i];
+    k[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float m[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float keep = b3 ? k[2 + i] : k[i], send = b3 ? k[i] : k[2 + i];
+    m[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const float keep = b2 ? m[1] : m[0], send = b2 ? m[0] : m[1];
+  float r = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
+
+// Reduces v[0..1] across the 32 lanes; afterwards lane l holds the warp sum of row (l>>4)&1.
+__device__ __forceinline__ float reduce2(const float (&v)[2], int lane) {
+  const bool b4 = lane & 16;
+  float k = b4 ? v[1] : v[0];
+  const float t = b4 ? v[0] : v[1];
+  k += __shfl_xor_sync(0xffffffffu, t, 16);
+  k += __shfl_xor_sync(0xffffffffu, k, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;
+}
+
 // Reduces v[0..3] across the 32 lanes; afterwards lane l holds the warp sum of row (l>>3)&3.
 __device__ __forceinline__ float reduce4(const float (&v)[4], int lane) {
   const bool b4 = lane & 16, b3 = lane & 8;
@@ -237,23 +273,23 @@ __device__ void stage_acts(const Phase& P, int bits, const float (&rstd)[BB], fl
 // Consumes one ring slot holding `nrows` rows at bit-width BITS: row quads are split between the
 // kRG row groups; within a quad the loop runs over this warp's K-steps (activations loaded from
 // shared memory once per step) and then the four rows.
-template <int BITS, int SW, int BB>
+template <int BITS, int SW, int BB, int QR>
 __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, int nrows, int rg, int row_bytes,
                                               int sc_off, int zp_off, int sc_row, int zp_row, const int (&pay_l)[SW],
                                               const int (&sc_l)[SW], const int (&zp_l)[SW], const int (&step_of)[SW],
                                               const bool (&step_ok)[SW], int nsteps, float zmagic,
                                               const float4* __restrict__ xsm, const float* __restrict__ sigm,
                                               float* red_row, int bmask, int lane) {
-  const uint8_t* pa = slot + rg * 4 * row_bytes;
-  const uint8_t* sa = slot + sc_off + rg * 4 * sc_row;
-  const uint8_t* za = slot + zp_off + rg * 4 * zp_row;
+  const uint8_t* pa = slot + rg * QR * row_bytes;
+  const uint8_t* sa = slot + sc_off + rg * QR * sc_row;
+  const uint8_t* za = slot + zp_off + rg * QR * zp_row;
   const int red_step = kSplit * BB;
-  for (int r0 = rg * 4; r0 < nrows; r0 += 4 * kRG) {
-    float acc[BB][4];
+  for (int r0 = rg * QR; r0 < nrows; r0 += QR * kRG) {
+    float acc[BB][QR];
 #pragma unroll
     for (int b = 0; b < BB; ++b)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[b][u] = 0.f;
+      for (int u = 0; u < QR; ++u) acc[b][u] = 0.f;
 #pragma unroll
     for (int s = 0; s < SW; ++s) {
       if (!step_ok[s]) continue;
@@ -273,7 +309,7 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
         sg[b] = sigm[static_cast<size_t>(b * nsteps + step_of[s]) * 32 + lane];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < QR; ++u) {
         const float sc = *reinterpret_cast<const float*>(sa + u * sc_row + sc_l[s]);
         const uint32_t zq = za[u * zp_row + zp_l[s]];
         const float zf = __uint_as_float(0x4B000000u | zq) - zmagic;  // exact: zq + zp_base
@@ -291,15 +327,19 @@ __device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, 
         for (int b = 0; b < BB; ++b) acc[b][u] = fmaf(sc, fmaf(-zf, sg[b], p[b]), acc[b][u]);
       }
     }
-    const int u = (lane >> 3) & 3;
+    const int u = QR == 8 ? ((lane >> 2) & 7) : QR == 4 ? ((lane >> 3) & 3) : ((lane >> 4) & 1);
+    const bool writer = QR == 8 ? (lane & 3) == 0 : QR == 4 ? (lane & 7) == 0 : (lane & 15) == 0;
 #pragma unroll
     for (int b = 0; b < BB; ++b) {
-      const float v = reduce4(acc[b], lane);
-      if ((lane & 7) == 0 && r0 + u < nrows && ((bmask >> b) & 1)) red_row[(r0 + u) * red_step + b] = v;
+      float v;
+      if constexpr (QR == 8) v = reduce8(acc[b], lane);
+      else if constexpr (QR == 4) v = reduce4(acc[b], lane);
+      else v = reduce2(acc[b], lane);
+      if (writer && r0 + u < nrows && ((bmask >> b) & 1)) red_row[(r0 + u) * red_step + b] = v;
     }
-    pa += 4 * kRG * row_bytes;
-    sa += 4 * kRG * sc_row;
-    za += 4 * kRG * zp_row;
+    pa += QR * kRG * row_bytes;
+    sa += QR * kRG * sc_row;
+    za += QR * kRG * zp_row;
   }
 }
 
@@ -366,11 +406,12 @@ __device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float
         const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * R.stage_bytes;
         float* red_row = red + ((m * rows + rb) * kSplit + kw) * BB;
         const int nr = min(rps, rows - rb);
+        constexpr int QR = SW == 1 ? (BB == 1 ? 8 : 4) : 2;
         if (bits == 8)
-          consume_stage<8, SW, BB>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
+          consume_stage<8, SW, BB, QR>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
                                    nsteps, zmagic, xsm, sigm, red_row, bmask, lane);
         else
-          consume_stage<4, SW, BB>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
+          consume_stage<4, SW, BB, QR>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
                                    nsteps, zmagic, xsm, sigm, red_row, bmask, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&R.empty[slot_i]);
@@ -811,10 +852,11 @@ ProgramRun upload_program(fq_ctx* ctx, const ProgramBuilder& pb, bool transient)
   r.bb = pb.max_bb;
   const int64_t stage = std::max<int64_t>(pb.stage_bytes, 128);
   r.red_floats = static_cast<int>((pb.red_floats + 3) & ~int64_t(3));
-  r.xs_floats = static_cast<int>(static_cast<int64_t>(pb.max_nsteps) * kStepCodes * pb.max_bb);
+  const int bbk = pb.max_bb <= 1 ? 1 : (pb.max_bb <= 2 ? 2 : 4);  // kernel instantiation's batch bound
+  r.xs_floats = static_cast<int>(static_cast<int64_t>(pb.max_nsteps) * kStepCodes * bbk);
   const size_t red_bytes = static_cast<size_t>(r.red_floats) * sizeof(float);
   const size_t xs_bytes = static_cast<size_t>(r.xs_floats) * sizeof(float) +
-                          static_cast<size_t>(pb.max_nsteps) * 32 * pb.max_bb * sizeof(float);
+                          static_cast<size_t>(pb.max_nsteps) * 32 * bbk * sizeof(float);
   const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes + xs_bytes) - 2 * kMaxStages * 8 - 256;
   r.nstages = static_cast<int>(std::min<int64_t>(kMaxStages, budget / stage));
   if (r.nstages < 2) fail(FQ_E_CONFIG, "gemv: layer rows too large for the shared-memory ring");
