@@ -175,3 +175,29 @@ std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch = 
 fq_ctx* runtime();
 
 }  // namespace flexquant
+
+namespace flexquant {
+
+// Engine extensions used by the benchmark and the calibration tooling.
+struct WeightKl {
+  std::vector<double> kl8, kl4;  // weight-histogram KL of the W8 / W4 rung per linear
+};
+// Random N(0, std) initialisation on the device that also reports the reference analyzer's
+// weight-histogram KL of both rungs of every linear (the fp weights are transient).
+WeightKl init_random_with_kl(Model& model, uint64_t seed, float std, int bins);
+
+struct GemvProfile {
+  double ms_per_launch = 0.0;
+  int64_t launches_per_pass = 0;
+  int64_t bytes_per_pass = 0;
+};
+// Times the decode step's GEMV phases alone (CUDA events on the engine stream).
+GemvProfile profile_gemvs(Model& model, int slot, int reps);
+
+// Algorithmic bytes of one decode step of `slots` (weights at their rungs, KV read).
+std::pair<int64_t, int64_t> step_bytes(const Model& model, std::span<const int32_t> slots);
+
+// The engine's CUDA stream (cudaStream_t) for callers that time with events.
+void* runtime_stream();
+
+}  // namespace flexquant

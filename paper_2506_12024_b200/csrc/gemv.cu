@@ -128,7 +128,7 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
     // row groups consume octets (1 step, B=1), quads (1 step) or pairs (several steps)
     const int quantum = (P.sw == 1 ? (bb == 1 ? 8 : 4) : 2) * kRG;
     rps = rps >= quantum ? rps / quantum * quantum : quantum;
-    const int64_t pad = (rps + 7) / 8 * 8;
+    const int64_t pad = rps;  // a multiple of the row-group quantum: partial stages read stale rows only
     P.rows_per_stage[w] = rps;
     P.sc_off[w] = static_cast<int>(pad * row_bytes);
     P.zp_off[w] = static_cast<int>(pad * row_bytes + pad * P.ng_pad * 4);

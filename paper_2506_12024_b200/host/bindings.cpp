@@ -162,6 +162,12 @@ PYBIND11_MODULE(_flexquant, m) {
         KvCache c = md.attach_cache(slot);
         return to_numpy(md.forward_decode(tok, c));
       }, py::arg("token"), py::arg("slot") = 0)
+      .def("prefill_rows", [](Model& md, int slot, py::array_t<int32_t> t) {
+        py::list out;
+        for (const fq_row_stats& s : md.prefill_rows(slot, to_tokens(t))) out.append(stats_dict(s));
+        return out;
+      })
+      .def("reset_slot", [](Model& md, int slot) { md.make_cache(slot); })
       .def("decode_rows", [](Model& md, std::vector<int32_t> slots, std::vector<int32_t> toks) {
         py::list out;
         for (const fq_row_stats& s : md.decode_rows(slots, toks)) out.append(stats_dict(s));
@@ -171,6 +177,16 @@ PYBIND11_MODULE(_flexquant, m) {
         const StepStats& s = md.step_stats();
         return py::make_tuple(s.weight_bytes, s.ns_fp, s.ns_int8, s.ns_int4, s.ns_forward);
       });
+  m.def("init_random_with_kl", [](Model& md, uint64_t seed, float std, int bins) {
+    const WeightKl k = init_random_with_kl(md, seed, std, bins);
+    return py::make_tuple(k.kl8, k.kl4);
+  });
+  m.def("profile_gemvs", [](Model& md, int slot, int reps) {
+    const GemvProfile p = profile_gemvs(md, slot, reps);
+    return py::make_tuple(p.ms_per_launch, p.launches_per_pass, p.bytes_per_pass);
+  });
+  m.def("step_bytes", [](const Model& md, std::vector<int32_t> slots) { return step_bytes(md, slots); });
+  m.def("runtime_stream", []() { return reinterpret_cast<uintptr_t>(runtime_stream()); });
   m.def("load_model_file", [](const std::string& p, int max_batch) { return load_model_file(p, max_batch); },
         py::arg("path"), py::arg("max_batch") = 1);
 

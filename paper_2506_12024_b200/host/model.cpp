@@ -480,3 +480,34 @@ std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch) {
 }
 
 }  // namespace flexquant
+
+namespace flexquant {
+
+WeightKl init_random_with_kl(Model& model, uint64_t seed, float std, int bins) {
+  WeightKl r;
+  r.kl8.resize(model.num_linears());
+  r.kl4.resize(model.num_linears());
+  detail::check(fq_model_init_random_kl(model.handle(), seed, std, bins, r.kl8.data(), r.kl4.data()));
+  return r;
+}
+
+GemvProfile profile_gemvs(Model& model, int slot, int reps) {
+  GemvProfile p;
+  detail::check(fq_model_profile_gemvs(model.handle(), slot, reps, &p.ms_per_launch, &p.launches_per_pass,
+                                       &p.bytes_per_pass));
+  return p;
+}
+
+std::pair<int64_t, int64_t> step_bytes(const Model& model, std::span<const int32_t> slots) {
+  int64_t w = 0, k = 0;
+  detail::check(fq_model_step_bytes(model.handle(), static_cast<int32_t>(slots.size()), slots.data(), &w, &k));
+  return {w, k};
+}
+
+void* runtime_stream() {
+  void* s = nullptr;
+  detail::check(fq_ctx_get_stream(runtime(), &s));
+  return s;
+}
+
+}  // namespace flexquant
