@@ -209,6 +209,19 @@ fq_status fq_model_step_bytes(const fq_model* model, int32_t batch, const int32_
  * algorithmic bytes of one pass over the step's GEMVs. */
 fq_status fq_model_profile_gemvs(fq_model* model, int32_t slot, int32_t reps, double* ms_per_launch,
                                  int64_t* launches_per_pass, int64_t* bytes_per_pass);
+/* Profiling: runs one decode step of `slot` (appending `token`) with per-phase timestamps.
+ * ticks_host receives (nphases * 2 + 1) * grid %globaltimer values: [(phase * grid + cta) * 2]
+ * = end of the phase's work on that CTA, [... + 1] = after the grid barrier that follows, and
+ * [nphases * grid * 2 + cta] = the CTA's start; then 3 * 16384 ring-trace stamps of CTA 0 (per
+ * weight stage: producer got the slot, consumers saw the data, consumers released it; 0 = unused);
+ * then nphases * grid * 8 GEMV-phase stamps [(phase * grid + cta) * 8 + k] (k = 0 partition set
+ * up, 1 norm factors, 2 first barrier, 3 activations staged, 4 weight loop done, 5 final reduction
+ * done, 6 phase done).
+ * phase_types_host (optional, nphases entries)
+ * receives the phase kinds (0 GEMV, 1 embedding, 2 attention, 3 row statistics). */
+fq_status fq_model_profile_step(fq_model* model, int32_t slot, int32_t token, uint64_t* ticks_host,
+                                int64_t capacity, int32_t* nphases_out, int32_t* grid_out,
+                                int32_t* phase_types_host);
 /* Logit-mode calibration (BASELINE config 4): teacher-forced prefill of `n_seqs` token rows
  * of length `len`, all linears at `base_rung`, then for every block b the block's linears at
  * `flip_rung`; kl_host[b] = mean KL(softmax(l_flip) || softmax(l_base)), entropy_host[b] =

@@ -32,7 +32,7 @@ ABI_FUNCTIONS = [
     "fq_model_linear_index", "fq_model_linear", "fq_model_set_param", "fq_model_init_random", "fq_model_set_rung",
     "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
     "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
-    "fq_model_init_random_kl", "fq_model_profile_gemvs",
+    "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step",
 ]
 
 
@@ -147,6 +147,7 @@ def load(path: str = LIB_PATH):
         "fq_model_step_bytes": [v, i32, v, C.POINTER(i64), C.POINTER(i64)],
         "fq_model_calibrate_logit_kl": [v, v, i64, i64, i32, i32, v, v],
         "fq_model_profile_gemvs": [v, i32, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64)],
+        "fq_model_profile_step": [v, i32, i32, v, i64, C.POINTER(i32), C.POINTER(i32), v],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -413,6 +414,23 @@ class Model:
         ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
         check(self.L.fq_model_profile_gemvs(self.h, slot, reps, C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, n.value, b.value
+
+    def profile_step(self, slot: int, token: int, max_phases: int = 4096):
+        """One decode step with per-phase %globaltimer stamps: returns (types[nphases],
+        end[nphases, grid], after_barrier[nphases, grid], start[grid]) in ns."""
+        nph, grid = C.c_int32(), C.c_int32()
+        cap = (max_phases * 2 + 1) * 256 + 3 * 16384 + max_phases * 256 * 8
+        ticks = np.zeros(cap, np.uint64)
+        types = np.zeros(max_phases, np.int32)
+        check(self.L.fq_model_profile_step(self.h, slot, token, _ptr(ticks), cap, C.byref(nph), C.byref(grid),
+                                           _ptr(types)))
+        n, g = nph.value, grid.value
+        t = ticks[: (2 * n + 1) * g].astype(np.int64)
+        ph = t[: 2 * n * g].reshape(n, g, 2)
+        off = (2 * n + 1) * g
+        self.last_ring_trace = ticks[off: off + 3 * 16384].astype(np.int64).reshape(-1, 3)
+        self.last_gemv_detail = ticks[off + 3 * 16384: off + 3 * 16384 + n * g * 8].astype(np.int64).reshape(n, g, 8)
+        return types[:n], ph[:, :, 0], ph[:, :, 1], t[2 * n * g:]
 
     def calibrate_logit_kl(self, tokens: np.ndarray, base_rung: int, flip_rung: int):
         t = np.ascontiguousarray(tokens, np.int32)

@@ -53,7 +53,7 @@ void require(bool cond, fq_status code, const char* msg) {
 void free_store(fq_rung_store& s) {
   dfree(s.payload);
   dfree(s.scale);
-  dfree(s.zp8);
+  dfree(s.tiles);
   dfree(s.zp32);
   s = fq_rung_store{};
 }
@@ -90,6 +90,8 @@ fq_status fq_ctx_destroy(fq_ctx* ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->stream);
     dfree(ctx->scratch);
+    dfree(ctx->gemv_fix);
+    dfree(ctx->gemv_flags);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });

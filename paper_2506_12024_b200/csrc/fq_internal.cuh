@@ -53,7 +53,29 @@ struct fq_ctx {
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
   void* ensure_scratch(size_t bytes);
+  // stream-K fix-up workspace of transient (stand-alone) GEMV programs
+  float* gemv_fix = nullptr;
+  unsigned int* gemv_flags = nullptr;
 };
+
+// ------------------------------------------------------------------ tiled fast-path layout
+// Each rung of a linear keeps, next to its canonical QuantizedTensor arrays, a tiled copy the
+// decode GEMV streams: blocks of 16 rows x 128 codes, tile-major ([tile][k-block]), each block
+// self-contained:
+//   codes  W8: 2048 B = [i 0..3][lane 0..31] 16-byte words; word i of lane t feeds the m16n8k16
+//              MMAs 2i and 2i+1 of the block: per MMA j two u32
+//              {q(r,k0), q(r,k0+1), q(r+8,k0), q(r+8,k0+1)}, {same at k0+8}
+//              with r = t/4, k0 = 16j + 2(t%4) (the A-fragment order of mma.sync m16n8k16).
+//          W4: 1024 B = [i 0..1][lane] 16-byte words; u32 u of word i feeds MMA 4i+u with nibbles
+//              (low to high) q(r,k0), q(r,k0+8), q(r+8,k0), q(r+8,k0+8), q(r,k0+1), q(r,k0+9),
+//              q(r+8,k0+1), q(r+8,k0+9).
+//   meta   16 f32 scales (rows 0..15) + 16 u8 zero points (z - zp_base).
+// Rows past N and codes past K are zero (scale 0); a block lies in one quantization group, so
+// the layout exists when G % 128 == 0 or G >= K and the zero points span <= 255.
+constexpr int kTileRows = 16;
+constexpr int kBlockK = 128;
+constexpr int kBlockBytes8 = 2048 + 80;
+constexpr int kBlockBytes4 = 1024 + 80;
 
 // One resident precision copy of a linear layer.
 struct fq_rung_store {
@@ -62,10 +84,11 @@ struct fq_rung_store {
   int mode = FQ_MODE_ASYM;
   uint8_t* payload = nullptr;   // canonical row-major packed codes (device)
   int64_t payload_bytes = 0;
-  float* scale = nullptr;       // [N, ng_pad] (rows padded to 16 B for bulk copies)
-  uint8_t* zp8 = nullptr;       // [N, zp_pad] effective zero point - zp_base (fast path)
+  float* scale = nullptr;       // [N, ng_pad]
   int32_t* zp32 = nullptr;      // [N, ng] effective zero point (z + stored offset), always kept
-  int32_t zp_base = 0;
+  uint8_t* tiles = nullptr;     // tiled fast-path copy (see above), or null
+  int64_t tiles_bytes = 0;
+  int32_t zp_base = 0;          // tiles hold z - zp_base in one byte
   bool zp_fits_u8 = false;      // fast kernel usable
 };
 
@@ -135,6 +158,7 @@ struct GemvLaunch {
   float* out_partials = nullptr;  // EPI_RESIDUAL: [batch, out_n_partials]
   int out_n_partials = 0;
   bool pdl = false;            // launch with programmatic stream serialization
+  void* stat_part = nullptr;   // EPI_STORE: fused softmax partials [batch][grid] (StatPart)
 };
 
 bool gemv_fast_supported(const fq_layer* L, int rung);

@@ -8,18 +8,21 @@
 // Fast numerics — a TMA-fed streaming program (program.cu):
 //  * the work is a list of phases (GEMVs, and for the decode step also the token embedding, the
 //    attention of every layer and the row statistics).  One CTA per SM runs the whole list.
-//  * each CTA owns a balanced contiguous row range of every matrix of a GEMV phase; that range
-//    is one contiguous byte range of the row-major payload (plus its padded scale / zero-point
-//    rows).  A producer warp streams all of the CTA's ranges, phase after phase, through a
-//    shared-memory ring with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  It
-//    never waits for activations, so the HBM stream keeps running across phase boundaries while
-//    the consumer warps synchronise on a grid barrier between dependent phases.
-//  * consumer warps split the K-steps of a row (512 codes per step, 16 per lane) and keep their
-//    activations in registers for the phase.  Unpacking is one LOP/SHF per code: the masked
-//    code bits (q << s), s < 24, reinterpreted as fp32 are exactly q * 2^(s-149) (subnormal /
-//    first binade), so an FFMA2 with x * 2^(109-s) accumulates q*x*2^-40 with no int->float
-//    conversion.  The zero point is folded per group: sum_j (q_j - z) x_j = sum_j q_j x_j -
-//    z * sum_j x_j.  fp32 accumulation; fixed reduction order (deterministic, no atomics).
+//  * weights are streamed from the tiled copy of each rung (fq_internal.cuh): self-contained
+//    16-row x 128-code blocks (codes in MMA-fragment order + 16 scales + 16 u8 zero points).
+//    A GEMV phase is the sequence of its blocks; CTA c owns a byte-balanced contiguous slice of
+//    it (stream-K: a 16-row tile may be shared by neighbouring CTAs; the CTA holding the tile's
+//    first block adds the later parts, published through flags, in CTA order).
+//  * a producer warp streams the CTA's slices, phase after phase, through a shared-memory ring
+//    with 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  It never waits for
+//    activations, so the HBM stream keeps running across phase boundaries while the consumer
+//    warps synchronise on a grid barrier between dependent phases.
+//  * 16 consumer warps take whole blocks.  Unpacking is a byte permute (W8: PRMT with 0x64 gives
+//    the fp16 1024+q) or a masked OR (W4: 1024+q for the low nibbles, 64+q for the high ones), so
+//    the dot products run on the tensor cores (mma.sync m16n8k16, fp32 accumulate) with the
+//    batch rows as the MMA's n columns.  Offsets and zero points fold per block:
+//    sum (q-z) x = acc - (D + z * X), D / X from the staged activations.  Fixed reduction order
+//    (deterministic, no float atomics).
 // Exact numerics — golden/parity mode: one thread per output, w = float(code - z) * s in fp32 as
 // dequantize() does, then a sequential double accumulation in k order as linear() does:
 // bit-identical to the reference.  Any group size, fp rung, bias.
@@ -77,11 +80,8 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
   P.B = bb;
   P.N = L0->N;
   P.K = L0->K;
-  P.G = L0->G;
-  P.ng_pad = L0->ng_pad;
-  P.zp_pad = L0->zp_pad;
-  P.nsteps = ceil_div_i(L0->K, kStepCodes);
-  P.sw = (P.nsteps + kSplit - 1) / kSplit;
+  P.n_tiles = ceil_div_i(L0->N, kTileRows);
+  P.nkb = ceil_div_i(L0->K, kBlockK);
   const size_t xsz = g.x_dtype == FQ_DT_F32 ? 4 : 2;
   const int64_t xs = g.x_stride ? g.x_stride : L0->K;
   P.x = static_cast<const char*>(g.x) + b0 * xs * xsz;
@@ -102,15 +102,18 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
   P.resid_stride = g.resid_stride;
   P.out_partials = g.out_partials ? g.out_partials + b0 * g.out_n_partials : nullptr;
   P.out_partials_stride = g.out_n_partials;
+  P.stat_part = g.stat_part ? static_cast<char*>(g.stat_part) + b0 * grid * 32 : nullptr;  // sizeof(StatPart)
+  if (g.nmat < 1 || g.nmat > kMaxMat) fail(FQ_E_CONFIG, "multi-gemv: 1..3 matrices");
+  if (bb < 1 || bb > kMaxB) fail(FQ_E_CONFIG, "gemv: batch chunk out of range");
+  if (static_cast<double>(P.n_tiles) * P.nkb * (kBlockBytes8 + kBlockBytes4) * g.nmat >= 4294967296.0)
+    fail(FQ_E_CONFIG, "gemv: layer too large for one phase (> 4 GiB of blocks)");
   for (int m = 0; m < g.nmat; ++m) {
     const fq_layer* L = g.mat[m].layer;
-    if (L->N != P.N || L->K != P.K || L->G != P.G) fail(FQ_E_DIMENSION, "multi-gemv: matrices differ in shape");
+    if (L->N != P.N || L->K != P.K) fail(FQ_E_DIMENSION, "multi-gemv: matrices differ in shape");
     DevMat& M = P.mat[m];
     const fq_rung_store* st[2] = {&L->r8, &L->r4};
     for (int w = 0; w < 2; ++w) {
-      M.payload[w] = st[w]->payload;
-      M.scale[w] = st[w]->scale;
-      M.zp[w] = st[w]->zp8;
+      M.tiles[w] = st[w]->present ? st[w]->tiles : nullptr;
       M.zpbase[w] = st[w]->zp_base;
     }
     M.rung_table = g.mat[m].rung_table ? g.mat[m].rung_table + b0 * g.mat[m].rung_stride : nullptr;
@@ -118,74 +121,40 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
     M.rung = g.mat[m].rung;
     M.y = g.mat[m].y ? static_cast<char*>(g.mat[m].y) + b0 * g.y_stride * ysz : nullptr;
   }
-  // ring-slot layout of this phase (per bit-width)
-  const int64_t target = 40 * 1024;
-  for (int w = 0; w < 2; ++w) {
-    const int64_t row_bytes = w == 0 ? P.K : P.K / 2;
-    const int64_t per_row = row_bytes + P.ng_pad * 4 + P.zp_pad;
-    int rps = static_cast<int>(std::max<int64_t>(1, target / per_row));
-    rps = std::min(rps, 32);
-    // row groups consume octets (1 step, B=1), quads (1 step) or pairs (several steps)
-    const int quantum = (P.sw == 1 ? (bb == 1 ? 8 : 4) : 2) * kRG;
-    rps = rps >= quantum ? rps / quantum * quantum : quantum;
-    const int64_t pad = rps;  // a multiple of the row-group quantum: partial stages read stale rows only
-    P.rows_per_stage[w] = rps;
-    P.sc_off[w] = static_cast<int>(pad * row_bytes);
-    P.zp_off[w] = static_cast<int>(pad * row_bytes + pad * P.ng_pad * 4);
-    stage_bytes = std::max<int64_t>(stage_bytes, (pad * per_row + 127) / 128 * 128);
-  }
-  P.sc_row = static_cast<int>(P.ng_pad * 4);
-  P.zp_row = static_cast<int>(P.zp_pad);
-  const int64_t rows_max = (P.N + grid - 1) / grid;
-  red_floats = std::max<int64_t>(red_floats, static_cast<int64_t>(g.nmat) * rows_max * kSplit * (bb == 3 ? 4 : bb));
-  if (bb > 1 && P.sw > (bb <= 2 ? 2 : 1)) fail(FQ_E_CONFIG, "gemv: batch chunk too large for the K-steps per warp");
-  max_sw = std::max(max_sw, P.sw);
-  max_nsteps = std::max(max_nsteps, P.nsteps);
+  max_kpad = std::max<int64_t>(max_kpad, static_cast<int64_t>(P.nkb) * kBlockK);
   max_bb = std::max(max_bb, bb);
   phases.push_back(P);
 }
 
 void ProgramBuilder::add(const Phase& p) {
   phases.push_back(p);
-  max_bb = std::max(max_bb, p.B);
-}
-
-int gemv_batch_chunk(int64_t K) {
-  const int sw = (ceil_div_i(K, kStepCodes) + kSplit - 1) / kSplit;
-  return sw == 1 ? kMaxB : (sw == 2 ? 2 : 1);
+  max_bb = std::max(max_bb, std::min(p.B, kMaxB));
 }
 
 bool gemv_fast_supported(const fq_layer* L, int rung) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) return false;
   const fq_rung_store& s = L->store(rung);
-  const int nsteps = ceil_div_i(L->K, kStepCodes);
-  return s.present && s.zp_fits_u8 && L->K % 32 == 0 && L->G % kSegCodes == 0 && L->G >= kSegCodes &&
-         nsteps <= kMaxSW * kSplit;
+  return s.present && s.tiles != nullptr;
 }
 
-int gemv_fast_grid(const fq_ctx* ctx, int64_t N) { return static_cast<int>(std::min<int64_t>(ctx->num_sms, N)); }
+int gemv_fast_grid(const fq_ctx* ctx, int64_t blocks) { return static_cast<int>(std::min<int64_t>(ctx->num_sms, blocks)); }
 
 int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
   // A stand-alone GEMV is a program of independent phases, one per batch chunk.
-  const int64_t bchunk = gemv_batch_chunk(g.mat[0].layer->K);
+  const fq_layer* L = g.mat[0].layer;
+  const int64_t bchunk = gemv_batch_chunk(L->K);
   ProgramBuilder pb;
-  pb.grid = gemv_fast_grid(ctx, g.mat[0].layer->N);
+  pb.grid = gemv_fast_grid(ctx, static_cast<int64_t>(ceil_div_i(L->N, kTileRows)) * ceil_div_i(L->K, kBlockK));
   for (int64_t b0 = 0; b0 < g.batch; b0 += bchunk)
     pb.add_gemv(g, b0, static_cast<int>(std::min<int64_t>(bchunk, g.batch - b0)));
   if (g.epi == EPI_RESIDUAL && g.out_n_partials < pb.grid) fail(FQ_E_STATE, "gemv: residual partial buffer too small");
   for (auto& P : pb.phases) P.barrier_after = 0;
-  if (pb.phases.size() > static_cast<size_t>(kInlinePhases)) {
-    // very large batches: launch chunk groups separately
+  for (size_t i = 0; i < pb.phases.size(); i += kInlinePhases) {
     ProgramBuilder part = pb;
-    for (size_t i = 0; i < pb.phases.size(); i += kInlinePhases) {
-      part.phases.assign(pb.phases.begin() + i, pb.phases.begin() + std::min(pb.phases.size(), i + kInlinePhases));
-      const ProgramRun run = upload_program(ctx, part, true);
-      launch_program(ctx, run, nullptr, g.pdl);
-    }
-    return pb.grid;
+    part.phases.assign(pb.phases.begin() + i, pb.phases.begin() + std::min(pb.phases.size(), i + kInlinePhases));
+    const ProgramRun run = upload_program(ctx, part, true);
+    launch_program(ctx, run, nullptr, g.pdl);
   }
-  const ProgramRun run = upload_program(ctx, pb, true);
-  launch_program(ctx, run, nullptr, g.pdl);
   return pb.grid;
 }
 

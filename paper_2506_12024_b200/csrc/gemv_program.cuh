@@ -1,6 +1,6 @@
 // The TMA-fed streaming program: phase descriptors, the persistent program kernel and its
 // host-side builder.  Shared by the stand-alone GEMV entry point (gemv.cu) and the decode step
-// (model.cu).  See gemv.cu for the design notes.
+// (model.cu).  See gemv.cu for the design notes and fq_internal.cuh for the tiled weight layout.
 #pragma once
 
 #include "fq_internal.cuh"
@@ -9,29 +9,21 @@
 
 namespace fqc {
 
-constexpr int kStepCodes = 512;  // codes per row per warp step (32 lanes x 16)
-constexpr int kSegCodes = 16;    // codes per lane per step
-constexpr int kMaxB = 4;         // batch rows per phase
+constexpr int kMaxB = 8;          // batch rows per GEMV phase (the MMA's n = 8 columns)
+constexpr int kMaxMat = 3;        // matrices sharing one input (QKV)
 constexpr int kMaxStages = 8;
-constexpr int kSplit = 8;        // consumer warps splitting the K-steps of a row
-#ifndef FQ_RG
-#define FQ_RG 2
-#endif
-constexpr int kRG = FQ_RG;       // row groups of consumer warps
-constexpr int kNCW = kSplit * kRG;
+constexpr int kNCW = 8;           // consumer warps (2 blocks in flight each)
 constexpr int kThreads = (kNCW + 1) * 32;  // + one producer warp
-constexpr int kMaxSW = 4;        // K-steps per warp (K <= 16384)
-constexpr int kAttnChunk = 64;   // keys per attention work item
-constexpr float kTwo109 = 649037107316853453566312041152512.0f;  // 2^109
-constexpr float kTwo40 = 1099511627776.0f;                        // 2^40
-constexpr float kTwoM40 = 9.094947017729282379150390625e-13f;     // 2^-40
+constexpr int kAttnChunk = 64;    // keys per attention work item
+constexpr int kStageBytes = 35328;  // max(16 W8 blocks, 32 W4 blocks)
+constexpr int kStageBlocks8 = 16;
+constexpr int kStageBlocks4 = 32;
+constexpr int kSmemBudget = 220 * 1024;
 
 enum PhaseType : int { PH_GEMV = 0, PH_EMBED = 1, PH_ATTN = 2, PH_STATS = 3 };
 
 struct DevMat {
-  const uint8_t* payload[2];  // [0] = W8, [1] = W4
-  const float* scale[2];
-  const uint8_t* zp[2];
+  const uint8_t* tiles[2];    // [0] = W8, [1] = W4 tiled copies (fq_rung_store::tiles)
   int32_t zpbase[2];
   const uint8_t* rung_table;  // per batch row, or null
   int64_t rung_stride;
@@ -40,19 +32,17 @@ struct DevMat {
 };
 
 // One phase of a program.  GEMV fields follow GemvLaunch; EMBED / ATTN / STATS use the extra
-// fields at the end.
-struct Phase {
+// fields at the end.  At most 512 bytes: one warp moves it into shared memory with one 16-byte
+// load per lane.
+struct alignas(16) Phase {
   int type;
   int barrier_after;  // grid barrier between this phase and the next
   // ---- GEMV
-  DevMat mat[3];
+  DevMat mat[kMaxMat];
   int nmat;
   int B;
-  int64_t N, K, G, ng_pad, zp_pad;
-  int nsteps, sw;
-  int rows_per_stage[2];
-  int sc_off[2], zp_off[2];
-  int sc_row, zp_row;
+  int64_t N, K;
+  int n_tiles, nkb;   // 16-row tiles, 128-code blocks per row
   const void* x;
   int x_dtype;
   int64_t x_stride;
@@ -70,6 +60,10 @@ struct Phase {
   int64_t resid_stride;
   float* out_partials;
   int out_partials_stride;
+  void* stat_part;        // GEMV: per-(row, CTA) softmax partials of the stored outputs (fused
+                          // entropy, head only); STATS: their input [B][grid]
+  float* fix;             // stream-K fix-up partials [grid][kMaxMat * 16 * kMaxB]
+  unsigned int* flags;    // [grid] set by a CTA that finished the head of a shared tile
   // ---- EMBED / ATTN / STATS (decode step)
   const float* tok_emb;
   const int32_t* tokens;
@@ -82,14 +76,14 @@ struct Phase {
   __half* kv;
   int64_t slot_stride, layer_off, max_seq;
   int n_heads, head_dim;
-  float rope_theta;
+  const float2* rope_cs;  // [max_seq][head_dim / 2] (cos, sin) of pos * theta^(-2i/hd)
   float* attn_ws;
   unsigned int* tickets;
   void* attn_out;
-  const float* logits;
-  int64_t vocab;
   fq_row_stats* stats;
 };
+
+static_assert(sizeof(Phase) <= 512, "Phase must fit one warp-wide 16-byte load");
 
 constexpr int kInlinePhases = 4;
 struct InlineProgram {
@@ -99,11 +93,8 @@ struct InlineProgram {
 struct ProgramBuilder {
   std::vector<Phase> phases;
   int grid = 148;
-  int64_t stage_bytes = 0;
-  int64_t red_floats = 0;
-  int max_sw = 1;
   int max_bb = 1;
-  int max_nsteps = 1;
+  int64_t max_kpad = 128;  // largest K rounded up to a block
   void add_gemv(const GemvLaunch& g, int64_t b0, int bb);
   void add(const Phase& p);
 };
@@ -113,19 +104,28 @@ struct ProgramRun {
   InlineProgram inl;
   int nphases = 0;
   int grid = 0;
-  int stage_bytes = 0;
   int nstages = 0;
   size_t smem = 0;
   int bb = 1;
-  int red_floats = 0;
-  int xs_floats = 0;
-  unsigned int* barrier = nullptr;  // grid-barrier counter (reset before every launch)
+  int xs_bytes = 0;   // activation fragments
+  int dx_bytes = 0;   // per-block activation sums
+  int red_bytes = 0;  // per-warp tile partials (reduction window)
+  int prefetch = 0;   // L2 prefetch distance in stages (env FQ_PREFETCH overrides; -1 = no loads)
+  int ctl_phases = 0; // phases with a precomputed partition table in shared memory
+  float* fix = nullptr;           // owned stream-K scratch (device programs)
+  unsigned int* flags = nullptr;
 };
 
-// Sizes the ring and the reduction buffer for a program; long programs are copied to device
-// memory owned by the caller (dev_phases must be freed with dfree), short ones go inline.
-ProgramRun upload_program(fq_ctx* ctx, const ProgramBuilder& pb, bool transient);
+// Sizes the ring and the staging buffers for a program; long programs are copied to device
+// memory owned by the caller (dev_phases / fix / flags must be freed with dfree), short ones
+// go inline and use the context's workspace.
+ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient);
 void launch_program(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, bool pdl);
 int gemv_batch_chunk(int64_t K);
+// Profiling hook: device buffer receiving per-phase timestamps of the next programs (null = off).
+void set_phase_profile(unsigned long long* dev);
+// Profiling hook: ring trace of one CTA (3 stamps per stage, see program.cu); null = off.
+void set_ring_trace(unsigned long long* dev, int cta);
+void set_gemv_profile(unsigned long long* dev);
 
 }  // namespace fqc

@@ -458,7 +458,9 @@ struct fq_model {
   float* partials[2] = {nullptr, nullptr};  // ping-pong sum-of-squares partials [B][kPartStride]
   float* logits = nullptr;     // [max_batch, V]
   fq_row_stats* stats_dev = nullptr;
+  void* stat_part = nullptr;  // llama step: [max_batch][grid] softmax partials of the head GEMV
   float* attn_ws = nullptr;
+  float2* rope_cs = nullptr;  // llama: [max_seq][head_dim/2] (cos, sin)
   unsigned int* tickets = nullptr;
   double* dscratch = nullptr;
   int n_chunks = 1;
@@ -468,6 +470,7 @@ struct fq_model {
   size_t meta_bytes = 0;
   fq_row_stats* stats_host = nullptr;  // pinned [max_batch]
   std::map<int, cudaGraphExec_t> graphs;
+  std::map<int, int64_t> graph_kernels;  // kernels inside each captured step graph
   std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, gemv_only) -> uploaded program
   unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
@@ -588,7 +591,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
           a.max_seq = c.max_seq_len;
           a.n_heads = static_cast<int>(c.n_heads);
           a.head_dim = static_cast<int>(c.head_dim);
-          a.rope_theta = c.rope_theta;
+          a.rope_cs = M->rope_cs;
           a.attn_ws = M->attn_ws;
           a.tickets = M->tickets;
           a.attn_out = M->attn;
@@ -664,14 +667,14 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
       hd.y = M->logits;
       hd.y_dtype = FQ_DT_F32;
       hd.y_stride = V;
+      if (!gemv_only) hd.stat_part = M->stat_part;  // fused softmax partials (entropy / top-2 / argmax)
       add_chunked(pb, hd, B);
       if (!gemv_only) {
         Phase sp{};
         sp.type = PH_STATS;
         sp.B = B;
-        sp.logits = M->logits;
-        sp.vocab = V;
         sp.stats = M->stats_dev;
+        sp.stat_part = M->stat_part;
         pb.add(sp);
       }
       it = M->programs.emplace(key, upload_program(ctx, pb, false)).first;
@@ -770,6 +773,7 @@ void run_step(fq_model* M, int B) {
       return;
     }
     cudaGraph_t graph;
+    const int64_t l0 = ctx->launches;
     FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
       FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
@@ -784,10 +788,11 @@ void run_step(fq_model* M, int B) {
     FQ_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     FQ_CUDA(cudaGraphDestroy(graph));
     it = M->graphs.emplace(B, exec).first;
+    M->graph_kernels[B] = ctx->launches - l0;
+    ctx->launches = l0;  // counted when replayed
   }
-  const int64_t before = ctx->launches;
-  (void)before;
   FQ_CUDA(cudaGraphLaunch(it->second, st));
+  ctx->launches += M->graph_kernels[B];
   FQ_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -885,7 +890,7 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     require(c.max_batch >= 1 && c.max_batch <= 256, FQ_E_CONFIG, "model config: max_batch must be in [1, 256]");
     if (c.arch == FQ_ARCH_LLAMA) {
       require(c.act_dtype == FQ_DT_BF16 || c.act_dtype == FQ_DT_F16, FQ_E_CONFIG, "llama arch: activations must be bf16/fp16");
-      require(c.head_dim % 2 == 0 && c.head_dim <= 256, FQ_E_CONFIG, "llama arch: head_dim must be even and <= 256");
+      require(c.head_dim == 64 || c.head_dim == 128, FQ_E_CONFIG, "llama arch: head_dim must be 64 or 128");
       require(!c.tie_embeddings, FQ_E_CONFIG, "llama arch: tied embeddings not supported");
     } else {
       require(c.act_dtype == FQ_DT_F32, FQ_E_CONFIG, "reference arch: activations are fp32");
@@ -983,10 +988,24 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->partials[0] = zeros(static_cast<int64_t>(B) * kPartStride);
     M->partials[1] = zeros(static_cast<int64_t>(B) * kPartStride);
     M->logits = zeros(B * V);
+    M->stat_part = dmalloc(static_cast<size_t>(B) * 1024 * 32);  // [B][grid <= 1024] StatPart
     M->stats_dev = static_cast<fq_row_stats*>(dmalloc(sizeof(fq_row_stats) * B));
     M->n_chunks = static_cast<int>((c.max_seq_len + kAttnChunk - 1) / kAttnChunk);
     M->attn_ws = zeros(static_cast<int64_t>(B) * c.n_heads * M->n_chunks * (c.head_dim + 2));
     M->tickets = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * B * c.n_heads));
+    if (M->llama) {
+      // RoPE table: angle pos * theta^(-2i/hd) in double, cos/sin rounded to fp32
+      const int64_t half = c.head_dim / 2;
+      std::vector<float2> cs(static_cast<size_t>(c.max_seq_len * half));
+      for (int64_t p = 0; p < c.max_seq_len; ++p)
+        for (int64_t i = 0; i < half; ++i) {
+          const double inv = std::pow(static_cast<double>(c.rope_theta), -2.0 * static_cast<double>(i) / c.head_dim);
+          const double a = static_cast<double>(p) * inv;
+          cs[p * half + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+        }
+      M->rope_cs = static_cast<float2*>(dmalloc(sizeof(float2) * cs.size()));
+      FQ_CUDA(cudaMemcpy(M->rope_cs, cs.data(), sizeof(float2) * cs.size(), cudaMemcpyHostToDevice));
+    }
     M->grid_barrier = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * 4));
     FQ_CUDA(cudaMemsetAsync(M->tickets, 0, sizeof(unsigned int) * B * c.n_heads, st));
     const int64_t dsz = std::max<int64_t>(static_cast<int64_t>(B) * c.n_heads * c.max_seq_len, B * V);
@@ -1035,6 +1054,8 @@ fq_status fq_model_destroy(fq_model* M) {
     dfree(M->stats_dev);
     dfree(M->attn_ws);
     dfree(M->tickets);
+    dfree(M->stat_part);
+    dfree(M->rope_cs);
     dfree(M->dscratch);
     dfree(M->meta_dev);
     if (M->meta_host) cudaFreeHost(M->meta_host);
@@ -1239,6 +1260,61 @@ fq_status fq_model_step_bytes(const fq_model* M, int32_t batch, const int32_t* s
     }
     if (weight_bytes) *weight_bytes = wb;
     if (kv_bytes) *kv_bytes = kb;
+  });
+}
+
+fq_status fq_model_profile_step(fq_model* M, int32_t slot, int32_t token, uint64_t* ticks_host, int64_t capacity,
+                                int32_t* nphases_out, int32_t* grid_out, int32_t* phase_types_host) {
+  return guarded([&] {
+    require(M && ticks_host && nphases_out && grid_out, FQ_E_INPUT, "null argument");
+    require(M->llama, FQ_E_CONFIG, "profile_step: llama arch only");
+    fq_ctx* ctx = M->ctx;
+    cudaStream_t st = ctx->stream;
+    stage_rows(M, 1, &slot, &token);
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    if (M->programs.find(std::make_pair(1, 0)) == M->programs.end()) {
+      enqueue_step(M, 1);  // builds the program; this run is not profiled
+      FQ_CUDA(cudaStreamSynchronize(st));
+      stage_rows(M, 1, &slot, &token);
+      FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    }
+    const ProgramRun& run = M->programs.at(std::make_pair(1, 0));
+    const int64_t ring = 3 * 16384;  // ring trace of CTA 0 (program.cu kTraceStages)
+    const int64_t gdet = static_cast<int64_t>(run.nphases) * run.grid * 8;  // GEMV phase detail
+    const int64_t need = (static_cast<int64_t>(run.nphases) * 2 + 1) * run.grid + ring + gdet;
+    *nphases_out = run.nphases;
+    *grid_out = run.grid;
+    require(capacity >= need, FQ_E_CAPACITY, "profile_step: tick buffer too small");
+    auto* dev = static_cast<unsigned long long*>(dmalloc(sizeof(uint64_t) * need));
+    FQ_CUDA(cudaStreamSynchronize(st));
+    FQ_CUDA(cudaMemset(dev, 0, sizeof(uint64_t) * need));
+    set_phase_profile(dev);
+    set_ring_trace(dev + (need - ring - gdet), 0);
+    set_gemv_profile(dev + (need - gdet));
+    try {
+      enqueue_step(M, 1);
+      FQ_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      set_phase_profile(nullptr);
+      set_ring_trace(nullptr, 0);
+      set_gemv_profile(nullptr);
+      dfree(dev);
+      throw;
+    }
+    set_phase_profile(nullptr);
+    set_ring_trace(nullptr, 0);
+    set_gemv_profile(nullptr);
+    FQ_CUDA(cudaMemcpy(ticks_host, dev, sizeof(uint64_t) * need, cudaMemcpyDeviceToHost));
+    dfree(dev);
+    if (phase_types_host) {
+      std::vector<Phase> ph(run.nphases);
+      if (run.dev_phases)
+        FQ_CUDA(cudaMemcpy(ph.data(), run.dev_phases, sizeof(Phase) * run.nphases, cudaMemcpyDeviceToHost));
+      else
+        for (int i = 0; i < run.nphases; ++i) ph[i] = run.inl.phases[i];
+      for (int i = 0; i < run.nphases; ++i) phase_types_host[i] = ph[i].type;
+    }
+    M->slot_len[slot] += 1;
   });
 }
 

@@ -1,30 +1,56 @@
 // Persistent TMA-fed program kernel (see gemv.cu for the design):
-//   warp kNCW        producer: streams every GEMV phase's row ranges through the smem ring
-//   warps 0..kNCW-1  consumers: GEMV compute (kSplit warps split K, kRG row groups),
-//                    embedding, attention (groups of 4 warps) and row statistics, with a
-//                    grid-wide barrier between dependent phases.
+//   warp kNCW        producer: streams every GEMV phase's block range through the smem ring
+//   warps 0..kNCW-1  consumers: GEMV compute (tensor-core m16n8k16 over the unpacked codes, one
+//                    16x128 block per warp at a time), embedding, attention (groups of 4 warps)
+//                    and row statistics, with a grid-wide barrier between dependent phases.
 #include "gemv_program.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <cfloat>
 #include <cstring>
 #include <map>
 #include <mutex>
 
 namespace fqc {
+
+// Per-phase timing hook (profiling only): when set, consumer thread 0 of every CTA records
+// %globaltimer at the end of each phase and after the grid barrier that follows it:
+// prof[(phase * grid + cta) * 2 + {0, 1}], kernel entry at prof[nphases * grid * 2 + cta].
+__device__ unsigned long long* g_phase_prof = nullptr;
+// GEMV phase detail (profiling only): [(phase * grid + cta) * 8 + k], k = 0 setup done (warp 1),
+// 1 norm factors done (warp 0), 2 first barrier, 3 staged, 4 weight loop done, 5 final reduction
+// done, 6 phase done.
+__device__ unsigned long long* g_gemv_prof = nullptr;
+__device__ int g_cur_phase = 0;
+// Ring trace (profiling only): for CTA g_trace_cta, stage s of the whole program records
+// [3s] = producer got the empty slot, [3s+1] = consumer warp 0 saw the data, [3s+2] = consumer warp
+// 0 released the slot; up to kTraceStages stages.
+constexpr int kTraceStages = 16384;
+__device__ unsigned long long* g_ring_trace = nullptr;
+__device__ int g_trace_cta = 0;
+
+void set_phase_profile(unsigned long long* dev) {
+  FQ_CUDA(cudaMemcpyToSymbol(g_phase_prof, &dev, sizeof(dev)));
+}
+void set_gemv_profile(unsigned long long* dev) {
+  FQ_CUDA(cudaMemcpyToSymbol(g_gemv_prof, &dev, sizeof(dev)));
+}
+void set_ring_trace(unsigned long long* dev, int cta) {
+  FQ_CUDA(cudaMemcpyToSymbol(g_ring_trace, &dev, sizeof(dev)));
+  FQ_CUDA(cudaMemcpyToSymbol(g_trace_cta, &cta, sizeof(cta)));
+}
+
 namespace {
 
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ void ffma2(float2& acc, float a0, float a1, float b0, float b1) {
-  asm("{\n\t.reg .b64 pa, pb, pc;\n\t"
-      "mov.b64 pa, {%2, %3};\n\t"
-      "mov.b64 pb, {%4, %5};\n\t"
-      "mov.b64 pc, {%0, %1};\n\t"
-      "fma.rn.f32x2 pc, pa, pb, pc;\n\t"
-      "mov.b64 {%0, %1}, pc;\n\t}"
-      : "+f"(acc.x), "+f"(acc.y)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
+
+// ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -64,41 +90,19 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   return v;
 }
 
-__device__ __forceinline__ float f32(uint32_t u) { return __uint_as_float(u); }
-
-__host__ __device__ constexpr int seg_shift(int bits, int j) {
-  return bits == 8 ? ((j & 3) == 3 ? 0 : 8 * (j & 3)) : ((j & 7) < 6 ? 4 * (j & 7) : 4 * ((j & 7) - 6));
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
 }
 
-__device__ __forceinline__ float dot_seg8(const uint4 w, const float* xs) {
-  float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t v = ws[i];
-    ffma2(i & 1 ? b : a, f32(v & 0xFFu), f32(v & 0xFF00u), xs[4 * i + 0], xs[4 * i + 1]);
-    ffma2(i & 1 ? a : b, f32(v & 0xFF0000u), f32(v >> 24), xs[4 * i + 2], xs[4 * i + 3]);
-  }
-  a.x += b.x;
-  a.y += b.y;
-  return a.x + a.y;
-}
-
-__device__ __forceinline__ float dot_seg4(const uint2 w, const float* xs) {
-  float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
-  const uint32_t ws[2] = {w.x, w.y};
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const uint32_t v = ws[i];
-    const uint32_t t = v >> 24;
-    ffma2(a, f32(v & 0xFu), f32(v & 0xF0u), xs[8 * i + 0], xs[8 * i + 1]);
-    ffma2(b, f32(v & 0xF00u), f32(v & 0xF000u), xs[8 * i + 2], xs[8 * i + 3]);
-    ffma2(a, f32(v & 0xF0000u), f32(v & 0xF00000u), xs[8 * i + 4], xs[8 * i + 5]);
-    ffma2(b, f32(t & 0xFu), f32(t & 0xF0u), xs[8 * i + 6], xs[8 * i + 7]);
-  }
-  a.x += b.x;
-  a.y += b.y;
-  return a.x + a.y;
+// D += A(16x16 f16, row) * B(16x8 f16, col), fp32 accumulators.
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
 __device__ __forceinline__ float load_act(const void* x, int dtype, int64_t i) {
@@ -120,386 +124,850 @@ __device__ __forceinline__ void store_out(void* y, int dtype, int64_t i, float v
 __device__ __forceinline__ int mat_rung(const DevMat& m, int b) {
   return m.rung_table ? static_cast<int>(m.rung_table[b * m.rung_stride]) : m.rung;
 }
-__device__ __forceinline__ int pass_mask(const Phase& P, int m, int w) {
-  int mask = 0;
-  const int want = w == 0 ? FQ_RUNG_INT8 : FQ_RUNG_INT4;
-  for (int b = 0; b < P.B; ++b) mask |= (mat_rung(P.mat[m], b) == want) << b;
-  return mask;
+
+// ---------------------------------------------------------------- the block sequence
+// A GEMV phase is a sequence of 16x128 blocks: tile-major, and inside a tile one segment of nkb
+// blocks per (matrix, copy) the batch needs.  CTA c owns the blocks whose first byte lies in
+// [c, c+1) * total / grid (byte-balanced across the grid, a tile may be shared by neighbours).
+struct Segs {
+  int n;
+  int m[2 * kMaxMat], w[2 * kMaxMat], mask[2 * kMaxMat];
+  int64_t tile_bytes;
+};
+
+__device__ __forceinline__ int blk_bytes(int w) { return w == 0 ? kBlockBytes8 : kBlockBytes4; }
+
+__device__ void phase_segs(const Phase& P, Segs& S) {
+  // all rung bytes are loaded first (independent loads, one round trip), then the masks
+  uint8_t rg[kMaxMat][kMaxB];
+#pragma unroll
+  for (int m = 0; m < kMaxMat; ++m)
+#pragma unroll
+    for (int b = 0; b < kMaxB; ++b)
+      rg[m][b] = (m < P.nmat && b < P.B)
+                     ? (P.mat[m].rung_table ? P.mat[m].rung_table[b * P.mat[m].rung_stride] : static_cast<uint8_t>(P.mat[m].rung))
+                     : static_cast<uint8_t>(0xFF);
+  S.n = 0;
+  S.tile_bytes = 0;
+#pragma unroll
+  for (int m = 0; m < kMaxMat; ++m)
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const uint8_t want = w == 0 ? FQ_RUNG_INT8 : FQ_RUNG_INT4;
+      int mask = 0;
+#pragma unroll
+      for (int b = 0; b < kMaxB; ++b) mask |= (rg[m][b] == want) << b;
+      if (mask == 0) continue;
+      S.m[S.n] = m;
+      S.w[S.n] = w;
+      S.mask[S.n] = mask;
+      S.tile_bytes += static_cast<int64_t>(P.nkb) * blk_bytes(w);
+      ++S.n;
+    }
 }
 
-__device__ __forceinline__ void cta_rows(int64_t N, int64_t& r0, int& rows) {
-  r0 = (N * blockIdx.x) / gridDim.x;
-  rows = static_cast<int>((N * (blockIdx.x + 1)) / gridDim.x - r0);
+// 32-bit arithmetic: the builder guarantees a phase's bytes fit in 32 bits.
+__device__ int64_t cta_start(const Phase& P, const Segs& S, int c) {
+  if (S.n == 0) return 0;
+  const uint32_t tb = static_cast<uint32_t>(S.tile_bytes);
+  const uint32_t total = static_cast<uint32_t>(P.n_tiles) * tb;
+  const uint32_t grid = gridDim.x;
+  const uint32_t target = (total / grid) * c + ((total % grid) * c) / grid;
+  const uint32_t t = target / tb;
+  uint32_t r = target - t * tb;
+  int64_t gb = static_cast<int64_t>(t) * S.n * P.nkb;
+  for (int s = 0; s < S.n; ++s) {
+    const uint32_t bb = blk_bytes(S.w[s]);
+    const uint32_t sb = static_cast<uint32_t>(P.nkb) * bb;
+    if (r < sb) return gb + (r + bb - 1) / bb;
+    r -= sb;
+    gb += P.nkb;
+  }
+  return gb;
 }
 
-// Reduces v[0..7] across the 32 lanes (9 shuffles); afterwards lane l holds the warp sum of
-// row (l>>2)&7.
-__device__ __forceinline__ float reduce8(const float (&v)[8], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-  float k[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float keep = b4 ? v[4 + i] : v[i], send = b4 ? v[i] : v[4 + i];
-    k[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-  float m[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float keep = b3 ? k[2 + i] : k[i], send = b3 ? k[i] : k[2 + i];
-    m[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  const float keep = b2 ? m[1] : m[0], send = b2 ? m[0] : m[1];
-  float r = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  r += __shfl_xor_sync(0xffffffffu, r, 2);
-  r += __shfl_xor_sync(0xffffffffu, r, 1);
+struct StageRef {
+  int64_t tile;
+  int seg, kb, nb;
+};
+
+__device__ __forceinline__ StageRef next_stage(const Phase& P, const Segs& S, int64_t gb, int64_t gend) {
+  const int64_t bpt = static_cast<int64_t>(S.n) * P.nkb;
+  StageRef r;
+  r.tile = gb / bpt;
+  const int rem = static_cast<int>(gb - r.tile * bpt);
+  r.seg = rem / P.nkb;
+  r.kb = rem - r.seg * P.nkb;
+  const int cap = S.w[r.seg] == 0 ? kStageBlocks8 : kStageBlocks4;
+  r.nb = static_cast<int>(min(static_cast<int64_t>(min(cap, P.nkb - r.kb)), gend - gb));
   return r;
-}
-
-// Reduces v[0..1] across the 32 lanes; afterwards lane l holds the warp sum of row (l>>4)&1.
-__device__ __forceinline__ float reduce2(const float (&v)[2], int lane) {
-  const bool b4 = lane & 16;
-  float k = b4 ? v[1] : v[0];
-  const float t = b4 ? v[0] : v[1];
-  k += __shfl_xor_sync(0xffffffffu, t, 16);
-  k += __shfl_xor_sync(0xffffffffu, k, 8);
-  k += __shfl_xor_sync(0xffffffffu, k, 4);
-  k += __shfl_xor_sync(0xffffffffu, k, 2);
-  k += __shfl_xor_sync(0xffffffffu, k, 1);
-  return k;
-}
-
-// Reduces v[0..3] across the 32 lanes; afterwards lane l holds the warp sum of row (l>>3)&3.
-__device__ __forceinline__ float reduce4(const float (&v)[4], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8;
-  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
-  const float t0 = b4 ? v[0] : v[2], t1 = b4 ? v[1] : v[3];
-  k0 += __shfl_xor_sync(0xffffffffu, t0, 16);
-  k1 += __shfl_xor_sync(0xffffffffu, t1, 16);
-  float k = b3 ? k1 : k0;
-  const float t = b3 ? k0 : k1;
-  k += __shfl_xor_sync(0xffffffffu, t, 8);
-  k += __shfl_xor_sync(0xffffffffu, k, 4);
-  k += __shfl_xor_sync(0xffffffffu, k, 2);
-  k += __shfl_xor_sync(0xffffffffu, k, 1);
-  return k;
 }
 
 struct Ring {
   uint8_t* base;
   uint64_t* full;
   uint64_t* empty;
-  int stage_bytes;
   int nstages;
 };
 
 // ---------------------------------------------------------------- producer
-// All phase fields are copied into registers before the stage loop: the asm statements carry
-// "memory" clobbers, so anything left in memory would be reloaded after every copy / wait.
-__device__ __forceinline__ void produce_phase(const Phase& P, const Ring R, int& slot_i, uint32_t& phase_bit) {
-  int64_t r0;
-  int rows;
-  cta_rows(P.N, r0, rows);
-  if (rows <= 0) return;
-  const int nmat = P.nmat;
-  const int64_t K = P.K, ng_pad = P.ng_pad, zp_pad = P.zp_pad;
-  for (int m = 0; m < nmat; ++m) {
-    for (int w = 0; w < 2; ++w) {
-      if (pass_mask(P, m, w) == 0) continue;
-      const int rps = P.rows_per_stage[w];
-      const int64_t row_bytes = w == 0 ? K : K / 2;
-      const uint8_t* pay_src = P.mat[m].payload[w] + r0 * row_bytes;
-      const uint8_t* sc_src = reinterpret_cast<const uint8_t*>(P.mat[m].scale[w] + r0 * ng_pad);
-      const uint8_t* zp_src = P.mat[m].zp[w] + r0 * zp_pad;
-      const uint32_t sc_off = static_cast<uint32_t>(P.sc_off[w]), zp_off = static_cast<uint32_t>(P.zp_off[w]);
-      const uint32_t pay_row = static_cast<uint32_t>(row_bytes), sc_row = static_cast<uint32_t>(ng_pad * 4),
-                     zp_row = static_cast<uint32_t>(zp_pad);
-      for (int rb = 0; rb < rows; rb += rps) {
-        const int s = slot_i;
-        mbar_wait(&R.empty[s], phase_bit ^ 1u);
-        if (++slot_i == R.nstages) {
-          slot_i = 0;
-          phase_bit ^= 1u;
-        }
-        const uint32_t nr = static_cast<uint32_t>(min(rps, rows - rb));
-        uint8_t* dst = R.base + static_cast<size_t>(s) * R.stage_bytes;
-        mbar_expect_tx(&R.full[s], nr * (pay_row + sc_row + zp_row));
-        bulk_g2s(dst, pay_src + static_cast<int64_t>(rb) * pay_row, nr * pay_row, &R.full[s]);
-        bulk_g2s(dst + sc_off, sc_src + static_cast<int64_t>(rb) * sc_row, nr * sc_row, &R.full[s]);
-        bulk_g2s(dst + zp_off, zp_src + static_cast<int64_t>(rb) * zp_row, nr * zp_row, &R.full[s]);
-      }
+// Walks the weight stages of every GEMV phase of the program in order.
+struct StageWalk {
+  const Phase* phases;
+  int nphases, ph;
+  Segs S;
+  int64_t gb, g1;
+
+  __device__ void init(const Phase* p, int n) {
+    phases = p;
+    nphases = n;
+    ph = -1;
+    gb = g1 = 0;
+  }
+  // Next stage: source address and byte count; false at the end of the program.
+  __device__ bool next(const uint8_t*& src, uint32_t& bytes) {
+    while (gb >= g1) {
+      if (++ph >= nphases) return false;
+      const Phase& P = phases[ph];
+      if (P.type != PH_GEMV) continue;
+      phase_segs(P, S);
+      if (S.n == 0) continue;
+      gb = cta_start(P, S, blockIdx.x);
+      g1 = cta_start(P, S, blockIdx.x + 1);
     }
+    const Phase& P = phases[ph];
+    const StageRef st = next_stage(P, S, gb, g1);
+    gb += st.nb;
+    const int w = S.w[st.seg];
+    const int bb = blk_bytes(w);
+    src = P.mat[S.m[st.seg]].tiles[w] + (st.tile * P.nkb + st.kb) * bb;
+    bytes = static_cast<uint32_t>(st.nb * bb);
+    return true;
+  }
+};
+
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// The producer streams every stage through the ring; a second walk runs kPrefetchStages ahead
+// and issues L2 prefetches, so HBM keeps streaming while the ring is full (the consumers are in a
+// grid barrier, the activation staging or a non-GEMV phase) and ring refills hit L2.
+constexpr int kPrefetchStages = 8;
+
+__device__ void produce_all(const Phase* phases, int nphases, const Ring R, unsigned long long* tr, int prefetch) {
+  StageWalk main, ahead;
+  main.init(phases, nphases);
+  ahead.init(phases, nphases);
+  const uint8_t* psrc;
+  uint32_t pbytes;
+  bool more_ahead = prefetch > 0;  // < 0: no loads at all (FQ_PREFETCH=-1, profiling only)
+  for (int i = 0; i < prefetch && more_ahead; ++i)
+    if ((more_ahead = ahead.next(psrc, pbytes))) prefetch_l2(psrc, pbytes);
+  int slot_i = 0, tn = 0;
+  uint32_t phase_bit = 0;
+  const uint8_t* src;
+  uint32_t bytes;
+  while (main.next(src, bytes)) {
+    if (more_ahead && (more_ahead = ahead.next(psrc, pbytes))) prefetch_l2(psrc, pbytes);
+    const int s = slot_i;
+    mbar_wait(&R.empty[s], phase_bit ^ 1u);
+    if (tr && tn < kTraceStages) tr[3 * tn] = gtimer();
+    ++tn;
+    if (++slot_i == R.nstages) {
+      slot_i = 0;
+      phase_bit ^= 1u;
+    }
+    if (prefetch < 0) {  // profiling: consumer-only timing, the ring keeps whatever it holds
+      mbar_arrive(&R.full[s]);
+      continue;
+    }
+    mbar_expect_tx(&R.full[s], bytes);
+    bulk_g2s(R.base + static_cast<size_t>(s) * kStageBytes, src, bytes, &R.full[s]);
   }
 }
 
 // ---------------------------------------------------------------- consumers: GEMV
-// Activations of a GEMV phase are staged once per phase (and bit-width) in shared memory,
-// pre-scaled by the bit pattern of the rung: xsm[b][step][j4][lane] float4 (a lane's 16 values
-// of a step as four conflict-free 16-byte chunks) and sigm[b][step][lane] = sum of the 16 values
-// * 2^-40 (zero-point folding).  All consumer threads cooperate.
-template <int BB>
-__device__ void stage_acts(const Phase& P, int bits, const float (&rstd)[BB], float4* xsm, float* sigm) {
-  const int nsteps = P.nsteps;
-  const int nseg = nsteps * 32;
+// Shared-memory staging of a GEMV phase's activations (once per phase, all consumer threads):
+//   xs[((kb*4 + p)*B + b)*4 + tig] = uint4: the m16n8k16 B fragments {b0b1, b2b3} of MMAs 2p and
+//       2p+1 of block kb for batch column b and thread-in-group tig (fp16, x converted exactly
+//       from bf16/fp16 activations);
+//   dx[kb*B + b] = {1024*X, 64*X, X, 0}: X = sum of the block's activations; the offsets the
+//       magic-number unpack adds per block (fp16 0x6400|q = 1024+q for W8 bytes, 0x5400|q<<4 =
+//       64+q for W4 nibbles).
+struct GemvSmem {
+  uint4* xs;
+  float4* dx;
+  float* red;   // reduction window: [slot][nmat][kNCW][16][B]
+  float* sq;    // [kNCW * 32]
+  float* rstd;  // [kMaxB]
+  float* mbuf;  // [kMaxMat][16][B] owner's part of a shared tile
+  unsigned long long* tr;  // ring trace (profiling) or null
+  int* tn;
+};
+
+__device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+  const int B = P.B;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    // RMSNorm factors: every partial loaded up front (one round trip), fixed-order sums
+    constexpr int kMaxParts = 8;  // 8 x 32 >= partials (grid <= 256)
+    for (int b = 0; b < B; ++b) {
+      float r = 1.f;
+      if (P.norm_gain != nullptr) {
+        float v[kMaxParts];
+#pragma unroll
+        for (int j = 0; j < kMaxParts; ++j) {
+          const int i = tid + 32 * j;
+          v[j] = i < P.n_partials ? P.norm_partials[b * P.partials_stride + i] : 0.f;
+        }
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < kMaxParts; ++j) s += v[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        r = 1.0f / sqrtf(s / static_cast<float>(P.K) + P.norm_eps);
+      }
+      if (tid == 0) G.rstd[b] = r;
+    }
+    if (gp) gp[1] = gtimer();
+  }
+  named_sync(1, kNCW * 32);
+  if (gp) gp[2] = gtimer();
+  const int items = P.nkb * B * 16;
   const int64_t K = P.K;
   const void* x = P.x;
   const int xdt = P.x_dtype, adt = P.act_dtype;
-  const int64_t xstride = P.x_stride;
   const float* gain = P.norm_gain;
-  for (int i = threadIdx.x; i < nseg * BB; i += kNCW * 32) {
-    const int b = i / nseg, seg = i - b * nseg;
-    const int step = seg >> 5, ln = seg & 31;
-    const int64_t k0 = static_cast<int64_t>(step) * kStepCodes + ln * kSegCodes;
-    float v[kSegCodes];
-    float acc = 0.f;
+  for (int base = 0; base < items; base += kNCW * 32) {
+    const int it = base + tid;
+    const bool active = it < items;
+    const int kb = it / (B * 16);
+    const int rem = it - kb * B * 16;
+    const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
+    // the 8 activations of this item: loads are unconditional (index clamped into the row, the
+    // value zeroed past K) so they issue back to back
+    float raw[8], gn[8];
+    int64_t kk[8], kc[8];
 #pragma unroll
-    for (int j = 0; j < kSegCodes; ++j) {
-      float t = 0.f;
-      if (k0 + j < K && b < P.B) {
-        t = load_act(x, xdt, b * xstride + k0 + j);
-        if (gain != nullptr) t = round_act(t * rstd[b] * gain[k0 + j], adt);
-      }
-      acc += t;
-      const float sc8 = kTwo109 / static_cast<float>(1u << seg_shift(8, j));
-      const float sc4 = kTwo109 / static_cast<float>(1u << seg_shift(4, j));
-      v[j] = t * (bits == 8 ? sc8 : sc4);
+    for (int e = 0; e < 8; ++e) {
+      const int hh = e >> 2, q = e & 3;
+      kk[e] = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
+      kc[e] = b * P.x_stride + (active ? min(kk[e], K - 1) : 0);
     }
-    float4* dst = xsm + (static_cast<size_t>(b * nsteps + step) * 4) * 32 + ln;
+    // one dtype branch around all eight loads (a branch per load would serialise them)
+    if (xdt == FQ_DT_F32) {
+      const float* xf = static_cast<const float*>(x);
 #pragma unroll
-    for (int j4 = 0; j4 < 4; ++j4) dst[j4 * 32] = make_float4(v[4 * j4], v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
-    sigm[static_cast<size_t>(b * nsteps + step) * 32 + ln] = acc * kTwoM40;
-  }
-}
-
-// Consumes one ring slot holding `nrows` rows at bit-width BITS: row quads are split between the
-// kRG row groups; within a quad the loop runs over this warp's K-steps (activations loaded from
-// shared memory once per step) and then the four rows.
-template <int BITS, int SW, int BB, int QR>
-__device__ __forceinline__ void consume_stage(const uint8_t* __restrict__ slot, int nrows, int rg, int row_bytes,
-                                              int sc_off, int zp_off, int sc_row, int zp_row, const int (&pay_l)[SW],
-                                              const int (&sc_l)[SW], const int (&zp_l)[SW], const int (&step_of)[SW],
-                                              const bool (&step_ok)[SW], int nsteps, float zmagic,
-                                              const float4* __restrict__ xsm, const float* __restrict__ sigm,
-                                              float* red_row, int bmask, int lane) {
-  const uint8_t* pa = slot + rg * QR * row_bytes;
-  const uint8_t* sa = slot + sc_off + rg * QR * sc_row;
-  const uint8_t* za = slot + zp_off + rg * QR * zp_row;
-  const int red_step = kSplit * BB;
-  for (int r0 = rg * QR; r0 < nrows; r0 += QR * kRG) {
-    float acc[BB][QR];
-#pragma unroll
-    for (int b = 0; b < BB; ++b)
-#pragma unroll
-      for (int u = 0; u < QR; ++u) acc[b][u] = 0.f;
-#pragma unroll
-    for (int s = 0; s < SW; ++s) {
-      if (!step_ok[s]) continue;
-      float xs[BB][kSegCodes];
-      float sg[BB];
-#pragma unroll
-      for (int b = 0; b < BB; ++b) {
-        const float4* src = xsm + (static_cast<size_t>(b * nsteps + step_of[s]) * 4) * 32 + lane;
-#pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4) {
-          const float4 f = src[j4 * 32];
-          xs[b][4 * j4] = f.x;
-          xs[b][4 * j4 + 1] = f.y;
-          xs[b][4 * j4 + 2] = f.z;
-          xs[b][4 * j4 + 3] = f.w;
-        }
-        sg[b] = sigm[static_cast<size_t>(b * nsteps + step_of[s]) * 32 + lane];
-      }
-#pragma unroll
-      for (int u = 0; u < QR; ++u) {
-        const float sc = *reinterpret_cast<const float*>(sa + u * sc_row + sc_l[s]);
-        const uint32_t zq = za[u * zp_row + zp_l[s]];
-        const float zf = __uint_as_float(0x4B000000u | zq) - zmagic;  // exact: zq + zp_base
-        float p[BB];
-        if constexpr (BITS == 8) {
-          const uint4 w = *reinterpret_cast<const uint4*>(pa + u * row_bytes + pay_l[s]);
-#pragma unroll
-          for (int b = 0; b < BB; ++b) p[b] = dot_seg8(w, xs[b]);
-        } else {
-          const uint2 w = *reinterpret_cast<const uint2*>(pa + u * row_bytes + pay_l[s]);
-#pragma unroll
-          for (int b = 0; b < BB; ++b) p[b] = dot_seg4(w, xs[b]);
-        }
-#pragma unroll
-        for (int b = 0; b < BB; ++b) acc[b][u] = fmaf(sc, fmaf(-zf, sg[b], p[b]), acc[b][u]);
-      }
-    }
-    const int u = QR == 8 ? ((lane >> 2) & 7) : QR == 4 ? ((lane >> 3) & 3) : ((lane >> 4) & 1);
-    const bool writer = QR == 8 ? (lane & 3) == 0 : QR == 4 ? (lane & 7) == 0 : (lane & 15) == 0;
-#pragma unroll
-    for (int b = 0; b < BB; ++b) {
-      float v;
-      if constexpr (QR == 8) v = reduce8(acc[b], lane);
-      else if constexpr (QR == 4) v = reduce4(acc[b], lane);
-      else v = reduce2(acc[b], lane);
-      if (writer && r0 + u < nrows && ((bmask >> b) & 1)) red_row[(r0 + u) * red_step + b] = v;
-    }
-    pa += QR * kRG * row_bytes;
-    sa += QR * kRG * sc_row;
-    za += QR * kRG * zp_row;
-  }
-}
-
-template <int SW, int BB>
-__device__ __forceinline__ void consume_gemv(const Phase& P, const Ring R, float* red, float4* xsm, float* sigm,
-                                             int& slot_i, uint32_t& phase_bit) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int kw = warp % kSplit, rg = warp / kSplit;
-  int64_t r0;
-  int rows;
-  cta_rows(P.N, r0, rows);
-  const int nsteps = P.nsteps;
-  const int64_t K = P.K, G = P.G;
-  bool step_ok[SW];
-  int step_of[SW], seg_k[SW], gidx[SW];
-#pragma unroll
-  for (int s = 0; s < SW; ++s) {
-    step_of[s] = kw + s * kSplit;
-    seg_k[s] = step_of[s] * kStepCodes + lane * kSegCodes;
-    step_ok[s] = step_of[s] < nsteps;
-    gidx[s] = (step_ok[s] && seg_k[s] < K) ? static_cast<int>(seg_k[s] / G) : 0;
-    if (!step_ok[s] || seg_k[s] >= K) seg_k[s] = 0;
-    if (!step_ok[s]) step_of[s] = 0;
-  }
-  float rstd[BB];
-#pragma unroll
-  for (int b = 0; b < BB; ++b) {
-    rstd[b] = 1.f;
-    if (P.norm_gain != nullptr && b < P.B) {
-      float s = 0.f;
-      for (int i = lane; i < P.n_partials; i += 32) s += P.norm_partials[b * P.partials_stride + i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      rstd[b] = 1.0f / sqrtf(s / static_cast<float>(K) + P.norm_eps);
-    }
-  }
-  int xs_bits = 0;
-  const int nmat = P.nmat;
-  for (int m = 0; m < nmat; ++m) {
-    for (int w = 0; w < 2; ++w) {
-      const int bmask = pass_mask(P, m, w);
-      if (bmask == 0) continue;
-      const int bits = w == 0 ? 8 : 4;
-      if (xs_bits != bits) {
-        named_sync(1, kNCW * 32);  // previous users of the staging area are done
-        stage_acts<BB>(P, bits, rstd, xsm, sigm);
-        named_sync(1, kNCW * 32);
-        xs_bits = bits;
-      }
-      if (rows == 0) continue;
-      const float zmagic = 8388608.0f - static_cast<float>(P.mat[m].zpbase[w]);
-      const int rps = P.rows_per_stage[w];
-      const int row_bytes = static_cast<int>(w == 0 ? K : K / 2);
-      int pay_l[SW], sc_l[SW], zp_l[SW];
-#pragma unroll
-      for (int s = 0; s < SW; ++s) {
-        pay_l[s] = w == 0 ? seg_k[s] : seg_k[s] / 2;
-        sc_l[s] = gidx[s] * 4;
-        zp_l[s] = gidx[s];
-      }
-      const int sco = P.sc_off[w], zpo = P.zp_off[w], scr = P.sc_row, zpr = P.zp_row;
-      for (int rb = 0; rb < rows; rb += rps) {
-        mbar_wait(&R.full[slot_i], phase_bit);
-        const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * R.stage_bytes;
-        float* red_row = red + ((m * rows + rb) * kSplit + kw) * BB;
-        const int nr = min(rps, rows - rb);
-        constexpr int QR = SW == 1 ? (BB == 1 ? 8 : 4) : 2;
-        if (bits == 8)
-          consume_stage<8, SW, BB, QR>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
-                                   nsteps, zmagic, xsm, sigm, red_row, bmask, lane);
-        else
-          consume_stage<4, SW, BB, QR>(slot, nr, rg, row_bytes, sco, zpo, scr, zpr, pay_l, sc_l, zp_l, step_of, step_ok,
-                                   nsteps, zmagic, xsm, sigm, red_row, bmask, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[slot_i]);
-        if (++slot_i == R.nstages) {
-          slot_i = 0;
-          phase_bit ^= 1u;
-        }
-      }
-    }
-  }
-}
-
-// Cross-warp reduction (kSplit partials per row, warp order) + epilogue, consumer threads only.
-template <int BB>
-__device__ void gemv_epilogue(const Phase& P, const float* red, float (*sq_red)[kNCW]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t r0;
-  int rows;
-  cta_rows(P.N, r0, rows);
-  const int items = rows * BB;
-  float local_sq[BB];
-#pragma unroll
-  for (int b = 0; b < BB; ++b) local_sq[b] = 0.f;
-  for (int it = threadIdx.x; it < items; it += kNCW * 32) {
-    const int r = it / BB;
-    const int b = it % BB;
-    if (b >= P.B) continue;
-    const int64_t row = r0 + r;
-    float v[3] = {0.f, 0.f, 0.f};
-    for (int m = 0; m < P.nmat; ++m) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < kSplit; ++w) s += red[((m * rows + r) * kSplit + w) * BB + b];
-      v[m] = s * kTwo40;
-    }
-    if (P.epi == EPI_STORE) {
-      for (int m = 0; m < P.nmat; ++m) store_out(P.y, P.y_dtype, b * P.y_stride + m * P.N + row, v[m]);
-    } else if (P.epi == EPI_SPLIT3) {
-      for (int m = 0; m < P.nmat; ++m) store_out(P.mat[m].y, P.y_dtype, b * P.y_stride + row, v[m]);
-    } else if (P.epi == EPI_SWIGLU) {
-      const float g = v[0];
-      const float silu = g / (1.0f + expf(-g));
-      store_out(P.y, P.y_dtype, b * P.y_stride + row, round_act(silu * v[1], P.act_dtype));
+      for (int e = 0; e < 8; ++e) raw[e] = xf[kc[e]];
     } else {
-      float* xp = P.resid + b * P.resid_stride + row;
-      const float nv = *xp + v[0];
-      *xp = nv;
-      local_sq[b] += nv * nv;
+      const unsigned short* xh = static_cast<const unsigned short*>(x);
+      unsigned short u[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) u[e] = xh[kc[e]];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        raw[e] = xdt == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[e]) << 16)
+                                   : __half2float(__ushort_as_half(u[e]));
+    }
+    if (gain != nullptr) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) gn[e] = gain[kc[e] - b * P.x_stride];
+    }
+    const float rs = G.rstd[b];
+    float lo = 0.f, hi = 0.f;
+    uint32_t h[4];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      float v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = 4 * hh + q;
+        float t = raw[e];
+        if (gain != nullptr) t = round_act(t * rs * gn[e], adt);
+        t = (active && kk[e] < K) ? t : 0.f;
+        v[q] = __half2float(__float2half_rn(t));
+      }
+      lo += v[0] + v[1];
+      hi += v[2] + v[3];
+      const __half2 p01 = __floats2half2_rn(v[0], v[1]), p89 = __floats2half2_rn(v[2], v[3]);
+      h[2 * hh] = *reinterpret_cast<const uint32_t*>(&p01);
+      h[2 * hh + 1] = *reinterpret_cast<const uint32_t*>(&p89);
+    }
+    if (active) G.xs[((kb * 4 + p) * B + b) * 4 + tig] = make_uint4(h[0], h[1], h[2], h[3]);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      lo += __shfl_xor_sync(0xffffffffu, lo, o);
+      hi += __shfl_xor_sync(0xffffffffu, hi, o);
+    }
+    if (active && (rem & 15) == 0) G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
+  }
+  named_sync(1, kNCW * 32);
+}
+
+// NBLK 16x128 blocks on one warp (interleaved: independent MMA chains): 8 MMAs per block over
+// the unpacked codes, then the per-row group fold y += s * (acc - (D + z*X)) for the columns
+// (batch rows) that use this copy.  xl: this lane's B-fragment base for the first block (null
+// when its column is past the batch); blocks are kbs apart in the block sequence.
+template <int W, int NBLK>
+__device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, int bstride, const uint4* __restrict__ xl,
+                                            int xstep, int kbstep, const float4* __restrict__ dxa, int dxstep, int lane,
+                                            bool ca, bool cb_, float zmagic, float (&y)[4]) {
+  const int g = lane >> 2;
+  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+  float c[NBLK][4];
+#pragma unroll
+  for (int n = 0; n < NBLK; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) c[n][e] = 0.f;
+  if constexpr (W == 0) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+#pragma unroll
+      for (int n = 0; n < NBLK; ++n) {
+        const uint4 wv = reinterpret_cast<const uint4*>(blk + n * bstride)[p * 32 + lane];
+        const uint4 xv = xl ? xl[n * kbstep + p * xstep] : z4;
+        mma16816(c[n], prmt(wv.x, 0x64646464u, 0x4140u), prmt(wv.x, 0x64646464u, 0x4342u),
+                 prmt(wv.y, 0x64646464u, 0x4140u), prmt(wv.y, 0x64646464u, 0x4342u), xv.x, xv.y);
+        mma16816(c[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
+                 prmt(wv.w, 0x64646464u, 0x4140u), prmt(wv.w, 0x64646464u, 0x4342u), xv.z, xv.w);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+#pragma unroll
+      for (int n = 0; n < NBLK; ++n) {
+        const uint4 wv = reinterpret_cast<const uint4*>(blk + n * bstride)[i * 32 + lane];
+        const uint4 x0 = xl ? xl[n * kbstep + (2 * i) * xstep] : z4;
+        const uint4 x1 = xl ? xl[n * kbstep + (2 * i + 1) * xstep] : z4;
+        const uint32_t qs[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          // every nibble pair is moved to bits 4-7 / 20-23 of the halves: fp16 0x5400 | q<<4 = 64 + q
+          const uint32_t q = qs[u];
+          const uint4 xv = u < 2 ? x0 : x1;
+          mma16816(c[n], ((q << 4) & 0x00F000F0u) | 0x54005400u, ((q >> 4) & 0x00F000F0u) | 0x54005400u,
+                   (q & 0x00F000F0u) | 0x54005400u, ((q >> 8) & 0x00F000F0u) | 0x54005400u, (u & 1) ? xv.z : xv.x,
+                   (u & 1) ? xv.w : xv.y);
+        }
+      }
     }
   }
-  if (P.epi == EPI_RESIDUAL) {
+  constexpr int cbytes = W == 0 ? 2048 : 1024;
 #pragma unroll
-    for (int b = 0; b < BB; ++b) {
-      float v = local_sq[b];
+  for (int n = 0; n < NBLK; ++n) {
+    const uint8_t* bk = blk + n * bstride;
+    const float s0 = *reinterpret_cast<const float*>(bk + cbytes + 4 * g);
+    const float s1 = *reinterpret_cast<const float*>(bk + cbytes + 4 * (g + 8));
+    const float z0 = __uint_as_float(0x4B000000u | bk[cbytes + 64 + g]) - zmagic;  // exact: zq + zp_base
+    const float z1 = __uint_as_float(0x4B000000u | bk[cbytes + 64 + g + 8]) - zmagic;
+    if (ca) {
+      const float4 d = dxa[n * dxstep];
+      const float D = W == 0 ? d.x : d.y;
+      y[0] = fmaf(s0, c[n][0] - fmaf(z0, d.z, D), y[0]);
+      y[2] = fmaf(s1, c[n][2] - fmaf(z1, d.z, D), y[2]);
+    }
+    if (cb_) {
+      const float4 d = dxa[n * dxstep + 1];
+      const float D = W == 0 ? d.x : d.y;
+      y[1] = fmaf(s0, c[n][1] - fmaf(z0, d.z, D), y[1]);
+      y[3] = fmaf(s1, c[n][3] - fmaf(z1, d.z, D), y[3]);
+    }
+  }
+}
+
+// Per-phase control block, computed once per phase by consumer thread 0.
+struct PhaseCtl {
+  Segs S;
+  float zmagic[2 * kMaxMat];
+  int64_t g0, g1;      // this CTA's block range
+  int64_t tile0;       // first tile of the range
+  int ntiles;          // tiles the range touches
+  int cap;             // tiles per reduction window
+  int head_shared;     // first tile started on an earlier CTA: publish its part
+  int nfollow;         // later CTAs holding parts of our last tile (we own it)
+  short follow[512];
+};
+
+// Writes this warp's partial of local tile `loc` into its window slot.
+__device__ __forceinline__ void flush_partial(const GemvSmem& G, int slot, int nmat, int B, int warp, int lane,
+                                              const float (&y)[kMaxMat][4]) {
+  const int g = lane >> 2, tig = lane & 3;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) sq_red[b][warp] = v;
+  for (int m = 0; m < kMaxMat; ++m) {
+    if (m >= nmat) break;
+    float* r = G.red + (static_cast<size_t>(slot * nmat + m) * kNCW + warp) * 16 * B;
+    if (2 * tig < B) {
+      r[g * B + 2 * tig] = y[m][0];
+      r[(g + 8) * B + 2 * tig] = y[m][2];
+    }
+    if (2 * tig + 1 < B) {
+      r[g * B + 2 * tig + 1] = y[m][1];
+      r[(g + 8) * B + 2 * tig + 1] = y[m][3];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fused softmax statistics
+// Running softmax statistics of a set of logits (softmax_double / ppl_entropy /
+// fault_tolerance / argmax_token, src/scheduler.cpp:13-49, src/engine.cpp:144-155), mergeable:
+//   m = max, S = sum exp(l - m), T = sum exp(l - m) (l - m)  (double),
+//   v1 >= v2 the two largest logits (duplicates count), arg = lowest index of the max.
+// H = ln S - T / S, PPLE = exp(H), p1 = exp(v1 - m) / S, p2 = exp(v2 - m) / S.
+struct StatPart {
+  double S, T;
+  float m, v1, v2;
+  int arg;
+};
+static_assert(sizeof(StatPart) == 32, "StatPart layout");
+
+__device__ __forceinline__ void stat_init(StatPart& a) {
+  a.S = 0.0;
+  a.T = 0.0;
+  a.m = -INFINITY;
+  a.v1 = -INFINITY;
+  a.v2 = -INFINITY;
+  a.arg = 0x7fffffff;
+}
+
+__device__ __forceinline__ void stat_add(StatPart& a, float l, int idx) {
+  if (l > a.m) {
+    if (a.m != -INFINITY) {
+      const double d = static_cast<double>(a.m) - static_cast<double>(l);
+      const double e = exp(d);
+      a.T = e * (a.T + d * a.S);
+      a.S *= e;
+    }
+    a.S += 1.0;
+    a.m = l;
+  } else {
+    const double d = static_cast<double>(l) - static_cast<double>(a.m);
+    const double e = exp(d);
+    a.S += e;
+    a.T += e * d;
+  }
+  if (l > a.v1) {
+    a.v2 = a.v1;
+    a.v1 = l;
+    a.arg = idx;
+  } else if (l > a.v2) {
+    a.v2 = l;
+  }
+}
+
+__device__ __forceinline__ StatPart stat_merge(const StatPart& a, const StatPart& b) {
+  if (b.m == -INFINITY) return a;
+  if (a.m == -INFINITY) return b;
+  StatPart r;
+  r.m = fmaxf(a.m, b.m);
+  const double da = static_cast<double>(a.m) - r.m, db = static_cast<double>(b.m) - r.m;
+  const double ea = exp(da), eb = exp(db);
+  r.S = a.S * ea + b.S * eb;
+  r.T = ea * (a.T + da * a.S) + eb * (b.T + db * b.S);
+  r.v1 = fmaxf(a.v1, b.v1);
+  r.v2 = fmaxf(fminf(a.v1, b.v1), fmaxf(a.v2, b.v2));
+  r.arg = a.v1 > b.v1 ? a.arg : (b.v1 > a.v1 ? b.arg : min(a.arg, b.arg));
+  return r;
+}
+
+__device__ __forceinline__ StatPart stat_shfl(const StatPart& a, int src_lane_xor) {
+  StatPart r;
+  r.S = __shfl_xor_sync(0xffffffffu, a.S, src_lane_xor);
+  r.T = __shfl_xor_sync(0xffffffffu, a.T, src_lane_xor);
+  r.m = __shfl_xor_sync(0xffffffffu, a.m, src_lane_xor);
+  r.v1 = __shfl_xor_sync(0xffffffffu, a.v1, src_lane_xor);
+  r.v2 = __shfl_xor_sync(0xffffffffu, a.v2, src_lane_xor);
+  r.arg = __shfl_xor_sync(0xffffffffu, a.arg, src_lane_xor);
+  return r;
+}
+
+__device__ __forceinline__ void gemv_epilogue(const Phase& P, int64_t tile, int r, int b, const float (&v)[kMaxMat],
+                                              float (&sqb)[kMaxB], StatPart& st) {
+  const int64_t row = tile * kTileRows + r;
+  if (row >= P.N) return;
+  if (P.epi == EPI_STORE) {
+    for (int m = 0; m < P.nmat; ++m) store_out(P.y, P.y_dtype, b * P.y_stride + m * P.N + row, v[m]);
+    if (P.stat_part) stat_add(st, v[0], static_cast<int>(row));
+  } else if (P.epi == EPI_SPLIT3) {
+    for (int m = 0; m < P.nmat; ++m) store_out(P.mat[m].y, P.y_dtype, b * P.y_stride + row, v[m]);
+  } else if (P.epi == EPI_SWIGLU) {
+    const float gt = v[0];
+    const float silu = gt / (1.0f + expf(-gt));
+    store_out(P.y, P.y_dtype, b * P.y_stride + row, round_act(silu * v[1], P.act_dtype));
+  } else {
+    float* xp = P.resid + b * P.resid_stride + row;
+    const float nv = *xp + v[0];
+    *xp = nv;
+#pragma unroll
+    for (int bb = 0; bb < kMaxB; ++bb)
+      if (bb == b) sqb[bb] += nv * nv;
+  }
+}
+
+// Reduces the window of local tiles [lo, hi): fixed-order sums over the warps, then per tile the
+// publication (a later part of a tile owned by an earlier CTA), the merge of the later parts
+// (our last tile continues on following CTAs) or the epilogue.
+__device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem& G, int lo, int hi, float (&sqb)[kMaxB],
+                              StatPart& st) {
+  named_sync(1, kNCW * 32);
+  const int B = P.B, nmat = P.nmat;
+  const int per = 16 * B;
+  const int fstride = kMaxMat * 16 * B;
+  const bool merge_last = C.nfollow > 0 && hi == C.ntiles;
+  bool published = false;
+  // item stride a multiple of `per` (and so of B): a thread's items all belong to batch row
+  // threadIdx.x % B (the fused softmax statistics rely on it)
+  const int stride = (kNCW * 32 / per) * per;
+  for (int it = threadIdx.x; threadIdx.x < stride && it < (hi - lo) * per; it += stride) {
+    const int l = lo + it / per, i = it % per;
+    float v[kMaxMat] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int m = 0; m < kMaxMat; ++m) {
+      if (m >= nmat) break;
+      const float* r = G.red + (static_cast<size_t>(((l - lo) * nmat + m) * kNCW)) * per + i;
+      float a = 0.f;
+#pragma unroll
+      for (int w = 0; w < kNCW; ++w) a += r[w * per];
+      v[m] = a;
+    }
+    if (l == 0 && C.head_shared) {
+      for (int m = 0; m < nmat; ++m) P.fix[static_cast<size_t>(blockIdx.x) * fstride + m * per + i] = v[m];
+      published = true;
+    } else if (merge_last && l == hi - 1) {
+      for (int m = 0; m < nmat; ++m) G.mbuf[m * per + i] = v[m];
+    } else {
+      gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
+    }
+  }
+  named_sync(1, kNCW * 32);
+  if (lo == 0 && C.head_shared && threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + blockIdx.x), "r"(1u) : "memory");
+  }
+  (void)published;
+  if (merge_last) {
+    // every output thread waits for the followers' flags itself (acquire) and adds their parts
+    const int i = threadIdx.x;
+    if (i < per) {
+      float v[kMaxMat] = {0.f, 0.f, 0.f};
+      for (int m = 0; m < nmat; ++m) v[m] = G.mbuf[m * per + i];
+      for (int f = 0; f < C.nfollow; ++f) {
+        const int c = C.follow[f];
+        while (ld_acquire(P.flags + c) == 0u) __nanosleep(20);
+        for (int m = 0; m < nmat; ++m) v[m] += __ldcg(P.fix + static_cast<size_t>(c) * fstride + m * per + i);
+      }
+      gemv_epilogue(P, C.tile0 + hi - 1, i / B, i % B, v, sqb, st);
     }
     named_sync(1, kNCW * 32);
-    if (static_cast<int>(threadIdx.x) < P.B) {
+    if (threadIdx.x == 0)
+      for (int f = 0; f < C.nfollow; ++f) P.flags[C.follow[f]] = 0u;  // consumed: all-zero again at the end
+  }
+}
+
+__device__ __forceinline__ int64_t cta_start_or_end(const Phase& P, const Segs& S, int c) {
+  return c <= static_cast<int>(gridDim.x) ? cta_start(P, S, c) : INT64_MAX;
+}
+
+// Compact per-phase partition of this CTA, computed for every phase of the program at kernel
+// start (one consumer thread per phase, in parallel) so no phase pays for it on its critical path.
+struct alignas(16) CtlEntry {
+  int g0, g1, tile0;
+  short ntiles;
+  uint8_t nseg, head_shared, nfollow, valid;  // nfollow 0xFF: more than 4, recompute
+  uint8_t segmw[2 * kMaxMat], mask[2 * kMaxMat];
+  short follow[4];
+};
+
+__device__ void compute_ctl(const Phase& P, CtlEntry& E) {
+  E.valid = 0;
+  if (P.type != PH_GEMV) return;
+  Segs S;
+  phase_segs(P, S);
+  E.nseg = static_cast<uint8_t>(S.n);
+  E.g0 = E.g1 = E.tile0 = 0;
+  E.ntiles = 0;
+  E.head_shared = 0;
+  E.nfollow = 0;
+  for (int s = 0; s < S.n; ++s) {
+    E.segmw[s] = static_cast<uint8_t>(S.m[s] << 1 | S.w[s]);
+    E.mask[s] = static_cast<uint8_t>(S.mask[s]);
+  }
+  E.valid = 1;
+  if (S.n == 0) return;
+  const int64_t bpt = static_cast<int64_t>(S.n) * P.nkb;
+  const int64_t g0 = cta_start(P, S, blockIdx.x), g1 = cta_start(P, S, blockIdx.x + 1);
+  E.g0 = static_cast<int>(g0);
+  E.g1 = static_cast<int>(g1);
+  if (g0 >= g1) return;
+  const int64_t tile0 = g0 / bpt, tl = (g1 - 1) / bpt;
+  E.tile0 = static_cast<int>(tile0);
+  E.ntiles = static_cast<short>(tl - tile0 + 1);
+  E.head_shared = g0 > tile0 * bpt;
+  const int64_t t1 = (tl + 1) * bpt;
+  if (t1 > g1 && tl * bpt >= g0) {
+    int64_t cs = g1;
+    for (int c = blockIdx.x + 1; c < static_cast<int>(gridDim.x) && cs < t1; ++c) {
+      const int64_t cn = cta_start(P, S, c + 1);
+      if (cn > cs) {
+        if (E.nfollow < 4) E.follow[E.nfollow++] = static_cast<short>(c);
+        else { E.nfollow = 0xFF; break; }
+      }
+      cs = cn;
+    }
+  }
+}
+
+// Per-phase control block, computed by consumer warp 1 (the lanes evaluate the range starts of
+// this CTA and its followers in parallel) while warp 0 computes the RMSNorm factors.
+__device__ void phase_setup(const Phase& P, PhaseCtl& C, int red_floats, int lane, unsigned long long* gpa,
+                            const CtlEntry* E) {
+  if (E && E->valid && E->nfollow != 0xFF) {
+    // precomputed at kernel start: copy into the working control block
+    if (lane == 0) {
+      C.S.n = E->nseg;
+      C.S.tile_bytes = 0;
+      for (int s = 0; s < E->nseg; ++s) {
+        C.S.m[s] = E->segmw[s] >> 1;
+        C.S.w[s] = E->segmw[s] & 1;
+        C.S.mask[s] = E->mask[s];
+        C.zmagic[s] = 8388608.0f - static_cast<float>(P.mat[C.S.m[s]].zpbase[C.S.w[s]]);
+      }
+      C.g0 = E->g0;
+      C.g1 = E->g1;
+      C.tile0 = E->tile0;
+      C.ntiles = E->ntiles;
+      C.head_shared = E->head_shared;
+      C.nfollow = E->nfollow;
+      for (int f = 0; f < E->nfollow; ++f) C.follow[f] = E->follow[f];
+      C.cap = E->nseg > 0 ? max(1, red_floats / (P.nmat * kNCW * 16 * P.B)) : 1;
+      if (gpa) gpa[7] = gtimer();
+    }
+    __syncwarp();
+    return;
+  }
+  Segs S;
+  phase_segs(P, S);
+  if (gpa && lane == 0) gpa[7] = gtimer();
+  int64_t g0 = 0, g1 = 0, tile0 = 0;
+  int ntiles = 0, head_shared = 0, nfollow = 0;
+  if (S.n > 0) {
+    const int64_t bpt = static_cast<int64_t>(S.n) * P.nkb;
+    const int64_t mine = cta_start_or_end(P, S, blockIdx.x + lane);
+    g0 = __shfl_sync(0xffffffffu, mine, 0);
+    g1 = __shfl_sync(0xffffffffu, mine, 1);
+    if (g0 < g1) {
+      tile0 = g0 / bpt;
+      const int64_t tl = (g1 - 1) / bpt;
+      ntiles = static_cast<int>(tl - tile0 + 1);
+      head_shared = g0 > tile0 * bpt;
+      const int64_t t1 = (tl + 1) * bpt;
+      if (t1 > g1 && tl * bpt >= g0) {
+        // we hold the head of our last tile and it continues: followers are the later CTAs with a
+        // non-empty range starting inside it
+        for (int base = 1;; base += 32) {
+          const int c = blockIdx.x + base + lane;
+          const int64_t cs = cta_start_or_end(P, S, c), cn = cta_start_or_end(P, S, c + 1);
+          const bool ok = c < static_cast<int>(gridDim.x) && cs < t1 && cn > cs;
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (lane == 0)
+            for (unsigned mm = m; mm; mm &= mm - 1)
+              if (nfollow < 512) C.follow[nfollow++] = static_cast<short>(blockIdx.x + base + __ffs(mm) - 1);
+          const int64_t last = __shfl_sync(0xffffffffu, cn, 31);
+          if (last >= t1 || blockIdx.x + base + 32 >= gridDim.x) break;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    C.S = S;
+    for (int s = 0; s < S.n; ++s) C.zmagic[s] = 8388608.0f - static_cast<float>(P.mat[S.m[s]].zpbase[S.w[s]]);
+    C.g0 = g0;
+    C.g1 = g1;
+    C.tile0 = tile0;
+    C.ntiles = ntiles;
+    C.head_shared = head_shared;
+    C.nfollow = nfollow;
+    C.cap = S.n > 0 ? max(1, red_floats / (P.nmat * kNCW * 16 * P.B)) : 1;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void add_into(float (&y)[kMaxMat][4], int m, float (&yc)[4]) {
+  switch (m) {
+    case 0:
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[0][e] += yc[e];
+      break;
+    case 1:
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[1][e] += yc[e];
+      break;
+    default:
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[2][e] += yc[e];
+      break;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) yc[e] = 0.f;
+}
+
+__device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, PhaseCtl& C, int red_floats,
+                               int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long* gpa = g_gemv_prof ? g_gemv_prof + (static_cast<size_t>(phase_idx) * gridDim.x + blockIdx.x) * 8 : nullptr;
+  unsigned long long* gp = threadIdx.x == 0 ? gpa : nullptr;
+  if (warp == 1) {
+    phase_setup(P, C, red_floats, lane, gpa, ctab ? ctab + phase_idx : nullptr);  // warp 0: norm factors
+    if (gpa && lane == 0) gpa[0] = gtimer();
+  }
+  stage_acts(P, G, gp);  // ends with a consumer barrier: C is visible
+  if (gp) gp[3] = gtimer();
+  const int B = P.B, nmat = P.nmat;
+  float sqb[kMaxB];
+#pragma unroll
+  for (int b = 0; b < kMaxB; ++b) sqb[b] = 0.f;
+  StatPart st;
+  stat_init(st);
+  if (C.ntiles > 0) {
+    int slot_i = slot_ref;
+    uint32_t phase_bit = phase_ref;
+    const int g = lane >> 2, tig = lane & 3;
+    const uint4* xl = g < B ? G.xs + static_cast<size_t>(g) * 4 + tig : nullptr;
+    const int xstep = B * 4;            // uint4s between MMA pairs
+    const int kbstep = 4 * B * 4;       // uint4s between blocks
+    const bool ca0 = 2 * tig < B, cb0 = 2 * tig + 1 < B;
+    float y[kMaxMat][4], yc[4];
+#pragma unroll
+    for (int m = 0; m < kMaxMat; ++m)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y[m][e] = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) yc[e] = 0.f;
+    // incremental walk of the block sequence (no divisions per stage)
+    const int nkb = P.nkb, nseg = C.S.n;
+    const int64_t bpt = static_cast<int64_t>(nseg) * nkb;
+    int rem = static_cast<int>(C.g0 - C.tile0 * bpt);
+    int seg = rem / nkb, kb = rem - seg * nkb;
+    int left = static_cast<int>(C.g1 - C.g0);
+    int loc = 0, wlo = 0;
+    const int cap = C.cap;
+    // segment state (refreshed when the segment changes)
+    int m = 0, w = 0, bsz = kBlockBytes8, capb = kStageBlocks8;
+    bool ca = false, cb = false;
+    float zm = 0.f;
+    auto load_seg = [&]() {
+      m = C.S.m[seg];
+      w = C.S.w[seg];
+      bsz = w == 0 ? kBlockBytes8 : kBlockBytes4;
+      capb = w == 0 ? kStageBlocks8 : kStageBlocks4;
+      const int cmask = C.S.mask[seg];
+      ca = ca0 && ((cmask >> (2 * tig)) & 1);
+      cb = cb0 && ((cmask >> (2 * tig + 1)) & 1);
+      zm = C.zmagic[seg];
+    };
+    load_seg();
+    while (left > 0) {
+      const int nb = min(min(capb, nkb - kb), left);
+      mbar_wait(&R.full[slot_i], phase_bit);
+      const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * kStageBytes;
+      const float4* dxa = G.dx + static_cast<size_t>(kb) * B + 2 * tig;
+      for (int j = warp; j < nb; j += 2 * kNCW) {
+        const uint8_t* bk = slot + j * bsz;
+        const uint4* xj = xl ? xl + (kb + j) * kbstep : nullptr;
+        const float4* dj = dxa + j * B;
+        if (j + kNCW < nb) {
+          if (w == 0) gemv_blocks<0, 2>(bk, kNCW * bsz, xj, xstep, kNCW * kbstep, dj, kNCW * B, lane, ca, cb, zm, yc);
+          else gemv_blocks<1, 2>(bk, kNCW * bsz, xj, xstep, kNCW * kbstep, dj, kNCW * B, lane, ca, cb, zm, yc);
+        } else {
+          if (w == 0) gemv_blocks<0, 1>(bk, 0, xj, xstep, 0, dj, 0, lane, ca, cb, zm, yc);
+          else gemv_blocks<1, 1>(bk, 0, xj, xstep, 0, dj, 0, lane, ca, cb, zm, yc);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[slot_i]);
+      if (++slot_i == R.nstages) {
+        slot_i = 0;
+        phase_bit ^= 1u;
+      }
+      left -= nb;
+      kb += nb;
+      if (kb == nkb) {  // segment finished
+        kb = 0;
+        add_into(y, m, yc);
+        if (++seg == nseg) {
+          seg = 0;
+          // tile finished on this CTA: flush this warp's partial into the window
+          flush_partial(G, loc - wlo, nmat, B, warp, lane, y);
+#pragma unroll
+          for (int mm = 0; mm < kMaxMat; ++mm)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) y[mm][e] = 0.f;
+          ++loc;
+          if (left > 0 && (loc - wlo == cap || (loc == 1 && C.head_shared))) {
+            reduce_window(P, C, G, wlo, loc, sqb, st);
+            wlo = loc;
+          }
+        }
+        load_seg();
+      }
+    }
+    if (kb != 0 || seg != 0) {  // the range ended inside a tile
+      add_into(y, m, yc);
+      flush_partial(G, loc - wlo, nmat, B, warp, lane, y);
+      ++loc;
+    }
+    if (gp) gp[4] = gtimer();
+    reduce_window(P, C, G, wlo, loc, sqb, st);
+    if (gp) gp[5] = gtimer();
+    slot_ref = slot_i;
+    phase_ref = phase_bit;
+  }
+  if (P.stat_part) {
+    // per-CTA softmax partial of each batch row over the logits this CTA finalised: thread t's
+    // items belong to row t % B; fixed-order tree merge over j = t / B in shared memory
+    named_sync(1, kNCW * 32);
+    StatPart* sp = reinterpret_cast<StatPart*>(G.red);
+    sp[threadIdx.x] = st;
+    const int per = 16 * B;
+    const int nb = ((kNCW * 32 / per) * per) / B;  // entries per row
+    for (int len = nb; len > 1;) {
+      const int up = (len + 1) >> 1;
+      named_sync(1, kNCW * 32);
+      const int j = threadIdx.x / B, b = threadIdx.x - j * B;
+      if (j < len - up) sp[j * B + b] = stat_merge(sp[j * B + b], sp[(j + up) * B + b]);
+      len = up;
+    }
+    named_sync(1, kNCW * 32);
+    if (static_cast<int>(threadIdx.x) < B)
+      reinterpret_cast<StatPart*>(P.stat_part)[threadIdx.x * gridDim.x + blockIdx.x] = sp[threadIdx.x];
+  }
+  if (P.epi == EPI_RESIDUAL) {
+    // per-CTA sum of squares of the rows this CTA finalised (RMSNorm of the next phase)
+#pragma unroll
+    for (int b = 0; b < kMaxB; ++b) {
+      float v = sqb[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) G.sq[b * kNCW + warp] = v;
+    }
+    named_sync(1, kNCW * 32);
+    if (static_cast<int>(threadIdx.x) < B) {
       float s = 0.f;
-      for (int w = 0; w < kNCW; ++w) s += sq_red[threadIdx.x][w];
+      for (int w2 = 0; w2 < kNCW; ++w2) s += G.sq[threadIdx.x * kNCW + w2];
       P.out_partials[threadIdx.x * P.out_partials_stride + blockIdx.x] = s;
     }
   }
-  named_sync(1, kNCW * 32);  // red / sq_red are reused by the next phase
-}
-
-template <int BB>
-__device__ __forceinline__ void run_gemv_phase(const Phase& P, const Ring R, float* red, float (*sq_red)[kNCW],
-                                               float4* xsm, float* sigm, int& slot_i, uint32_t& phase_bit) {
-  switch (P.sw) {
-    case 1: consume_gemv<1, BB>(P, R, red, xsm, sigm, slot_i, phase_bit); break;
-    case 2:
-      if constexpr (BB <= 2) consume_gemv<2, BB>(P, R, red, xsm, sigm, slot_i, phase_bit);
-      break;
-    case 3:
-      if constexpr (BB == 1) consume_gemv<3, BB>(P, R, red, xsm, sigm, slot_i, phase_bit);
-      break;
-    default:
-      if constexpr (BB == 1) consume_gemv<4, BB>(P, R, red, xsm, sigm, slot_i, phase_bit);
-      break;
-  }
-  named_sync(1, kNCW * 32);
-  gemv_epilogue<BB>(P, red, sq_red);
+  named_sync(1, kNCW * 32);  // staging / reduction buffers and C are reused by the next phase
+  if (gp) gp[6] = gtimer();
 }
 
 // ---------------------------------------------------------------- consumers: embedding
+__device__ __forceinline__ void cta_rows(int64_t N, int64_t& r0, int& rows) {
+  r0 = (N * blockIdx.x) / gridDim.x;
+  rows = static_cast<int>((N * (blockIdx.x + 1)) / gridDim.x - r0);
+}
+
 __device__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int64_t c0;
@@ -527,124 +995,191 @@ __device__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
 }
 
 // ---------------------------------------------------------------- consumers: attention
+// One (row, head, 64-key chunk) item per warp; lane l owns head dims [DPL*l, DPL*l + DPL) of q,
+// the keys, the values and the output (coalesced fp16 rows of the cache).  Scores: per-lane
+// partial dots for the chunk's 64 keys, then a transposing butterfly (62 shuffles) leaves lane l
+// with the full scores of keys base(l), base(l)+1.  The chunk's (max, sum, o) partial goes to the
+// workspace; the last chunk of a head (ticket) merges them.  RoPE pairs (i, i + hd/2) live on
+// lanes l and l^16; cos/sin come from the model's table (double-computed angles).
 struct AttnSmem {
-  float qs[256];
-  float knew[256];
-  float sc[kAttnChunk];
-  int last;
+  int last[kNCW];
 };
 
-__device__ __forceinline__ void rope_pair(float& a, float& b, int i, int hd, int pos, float theta) {
-  const double inv = pow(static_cast<double>(theta), -2.0 * i / hd);
-  double sn, cs;
-  sincos(static_cast<double>(pos) * inv, &sn, &cs);
-  const float c = static_cast<float>(cs), s = static_cast<float>(sn);
-  const float x0 = a, x1 = b;
-  a = x0 * c - x1 * s;
-  b = x1 * c + x0 * s;
+template <int DPL>
+__device__ __forceinline__ void rope_lane(float (&x)[DPL], const float2* __restrict__ cs, int lane) {
+  // lane < 16 holds the first halves (dims i), lane >= 16 the second (i + hd/2), i = DPL*(lane&15)+e
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) {
+    const float other = __shfl_xor_sync(0xffffffffu, x[e], 16);
+    const float2 t = cs[DPL * (lane & 15) + e];
+    x[e] = lane < 16 ? x[e] * t.x - other * t.y : x[e] * t.x + other * t.y;
+  }
 }
 
-// One (row, head, key chunk) item on a 128-thread group (4 warps, named barrier `bar`).
-__device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, AttnSmem& S, int gtid, int bar) {
-  const int hd = P.head_dim, H = P.n_heads;
+template <int DPL>
+__device__ __forceinline__ void load_lane(const void* src, int dtype, int64_t off, float (&x)[DPL]) {
+  // activations of the attention phase are bf16 / fp16: DPL consecutive 16-bit values
+  const unsigned short* h = static_cast<const unsigned short*>(src) + off;
+  unsigned short u[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) u[e] = h[e];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e)
+    x[e] = dtype == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[e]) << 16) : __half2float(__ushort_as_half(u[e]));
+}
+
+template <int DPL>
+__device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int lane, int warp, AttnSmem& S) {
+  constexpr int hd = DPL * 32;
+  const int H = P.n_heads;
   const int d = H * hd;
   const int pos = P.pos[b];
   const int slot = P.slots[b];
   const int j0 = chunk * kAttnChunk;
-  const int j1 = min(j0 + kAttnChunk, pos + 1);
+  const int nk = min(kAttnChunk, pos + 1 - j0);
   __half* kc = P.kv + slot * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
   __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
-  float* wsp = P.attn_ws + ((static_cast<int64_t>(b) * H + h) * nch + chunk) * (hd + 2);
   const int adt = P.act_dtype;
+  const int64_t qoff = static_cast<int64_t>(b) * d + h * hd + DPL * lane;
+  const float2* cs = P.rope_cs + static_cast<int64_t>(pos) * (hd / 2);
+  float q[DPL];
+  load_lane<DPL>(P.q, adt, qoff, q);
+  rope_lane<DPL>(q, cs, lane);
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-  for (int i = gtid; i < hd / 2; i += 128) {
-    float a0 = load_act(P.q, adt, static_cast<int64_t>(b) * d + h * hd + i);
-    float a1 = load_act(P.q, adt, static_cast<int64_t>(b) * d + h * hd + i + hd / 2);
-    rope_pair(a0, a1, i, hd, pos, P.rope_theta);
-    S.qs[i] = a0 * scale;
-    S.qs[i + hd / 2] = a1 * scale;
-  }
-  const bool owns_new = pos >= j0 && pos < j0 + kAttnChunk;
-  if (owns_new) {
-    for (int i = gtid; i < hd / 2; i += 128) {
-      float a0 = load_act(P.k, adt, static_cast<int64_t>(b) * d + h * hd + i);
-      float a1 = load_act(P.k, adt, static_cast<int64_t>(b) * d + h * hd + i + hd / 2);
-      rope_pair(a0, a1, i, hd, pos, P.rope_theta);
-      const __half h0 = __float2half_rn(a0), h1 = __float2half_rn(a1);
-      kc[static_cast<int64_t>(pos) * hd + i] = h0;
-      kc[static_cast<int64_t>(pos) * hd + i + hd / 2] = h1;
-      S.knew[i] = __half2float(h0);
-      S.knew[i + hd / 2] = __half2float(h1);
-    }
-    for (int i = gtid; i < hd; i += 128)
-      vc[static_cast<int64_t>(pos) * hd + i] = __float2half_rn(load_act(P.v, adt, static_cast<int64_t>(b) * d + h * hd + i));
-  }
-  named_sync(bar, 128);
-  const int lane = gtid & 31, gw = gtid >> 5;
-  for (int j = j0 + gw; j < j1; j += 4) {
-    float s = 0.f;
-    if (j == pos) {
-      for (int i = lane; i < hd; i += 32) s += S.qs[i] * S.knew[i];
-    } else {
-      const __half* kr = kc + static_cast<int64_t>(j) * hd;
-      for (int i = lane; i < hd; i += 32) s += S.qs[i] * __half2float(kr[i]);
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) S.sc[j - j0] = s;
+  for (int e = 0; e < DPL; ++e) q[e] *= scale;
+  if (pos >= j0 && pos < j0 + kAttnChunk) {
+    // this chunk holds the new position: RoPE'd key and the value go to the cache first (the
+    // same lane reads them back below: program order makes the row current)
+    float kn[DPL], vn[DPL];
+    load_lane<DPL>(P.k, adt, qoff, kn);
+    rope_lane<DPL>(kn, cs, lane);
+    load_lane<DPL>(P.v, adt, qoff, vn);
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) {
+      kc[static_cast<int64_t>(pos) * hd + DPL * lane + e] = __float2half_rn(kn[e]);
+      vc[static_cast<int64_t>(pos) * hd + DPL * lane + e] = __float2half_rn(vn[e]);
+    }
+    __syncwarp();  // orders the row writes before the reads below
   }
-  named_sync(bar, 128);
-  float m = -INFINITY;
-  for (int j = 0; j < j1 - j0; ++j) m = fmaxf(m, S.sc[j]);
-  for (int i = gtid; i < hd; i += 128) {
-    float acc = 0.f, l = 0.f;
-    for (int j = j0; j < j1; ++j) {
-      const float p = expf(S.sc[j - j0] - m);
-      const float vv = (j == pos) ? __half2float(__float2half_rn(load_act(P.v, adt, static_cast<int64_t>(b) * d + h * hd + i)))
-                                  : __half2float(vc[static_cast<int64_t>(j) * hd + i]);
-      acc += p * vv;
-      l += p;
+  using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
+  const int last_row = static_cast<int>(P.max_seq) - 1;
+  // per-lane partial dots of the chunk's keys: loads are unconditional (rows clamped into the
+  // cache, scores past the valid keys masked later) and issued 16 keys at a time
+  float part[kAttnChunk];
+#pragma unroll
+  for (int j16 = 0; j16 < kAttnChunk; j16 += 16) {
+    Raw raw[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      raw[t] = *reinterpret_cast<const Raw*>(kc + static_cast<int64_t>(min(j0 + j16 + t, last_row)) * hd + DPL * lane);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const __half2* hp = reinterpret_cast<const __half2*>(&raw[t]);
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < DPL / 2; ++e) {
+        const float2 f = __half22float2(hp[e]);
+        acc = fmaf(q[2 * e], f.x, acc);
+        acc = fmaf(q[2 * e + 1], f.y, acc);
+      }
+      part[j16 + t] = acc;
     }
-    wsp[2 + i] = acc;
-    if (i == 0) {
-      wsp[0] = m;
-      wsp[1] = l;
+  }
+  // transposing butterfly: after the step with mask m a lane keeps the upper half when (lane & m)
+  int base = 0;
+#pragma unroll
+  for (int step = 0; step < 5; ++step) {
+    const int m = 16 >> step;
+    const int half = kAttnChunk >> (step + 1);
+    const bool up = lane & m;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float keep = up ? part[i + half] : part[i];
+      const float send = up ? part[i] : part[i + half];
+      part[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
     }
+    if (up) base += half;
+  }
+  // lane holds the scores of keys base, base + 1
+  const float sc0 = base < nk ? part[0] : -INFINITY;
+  const float sc1 = base + 1 < nk ? part[1] : -INFINITY;
+  float mx = fmaxf(sc0, sc1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float p0 = base < nk ? expf(sc0 - mx) : 0.f;
+  const float p1 = base + 1 < nk ? expf(sc1 - mx) : 0.f;
+  float l = p0 + p1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  // P V: key j's weight lives on the lane whose base is j & ~1
+  float o[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+#pragma unroll
+  for (int j16 = 0; j16 < kAttnChunk; j16 += 16) {
+    Raw raw[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      raw[t] = *reinterpret_cast<const Raw*>(vc + static_cast<int64_t>(min(j0 + j16 + t, last_row)) * hd + DPL * lane);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int j = j16 + t;
+      const int owner = ((j >> 5) & 1) << 4 | ((j >> 4) & 1) << 3 | ((j >> 3) & 1) << 2 | ((j >> 2) & 1) << 1 | ((j >> 1) & 1);
+      const float pj = __shfl_sync(0xffffffffu, (j & 1) ? p1 : p0, owner);  // 0 past the valid keys
+      const __half2* hp = reinterpret_cast<const __half2*>(&raw[t]);
+#pragma unroll
+      for (int e = 0; e < DPL / 2; ++e) {
+        const float2 f = __half22float2(hp[e]);
+        o[2 * e] = fmaf(pj, f.x, o[2 * e]);
+        o[2 * e + 1] = fmaf(pj, f.y, o[2 * e + 1]);
+      }
+    }
+  }
+  const int64_t bh = static_cast<int64_t>(b) * H + h;
+  if (nch == 1) {
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, o[e] / l);
+    return;
+  }
+  float* wsp = P.attn_ws + (bh * nch + chunk) * (hd + 2);
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) wsp[2 + DPL * lane + e] = o[e];
+  if (lane == 0) {
+    wsp[0] = mx;
+    wsp[1] = l;
   }
   __threadfence();
-  named_sync(bar, 128);
-  if (gtid == 0) {
-    const unsigned int prev = atomicAdd(&P.tickets[b * H + h], 1u);
-    S.last = prev == static_cast<unsigned int>(nch - 1);
+  __syncwarp();
+  if (lane == 0) S.last[warp] = atomicAdd(&P.tickets[bh], 1u) == static_cast<unsigned int>(nch - 1);
+  __syncwarp();
+  if (!S.last[warp]) return;
+  __threadfence();
+  const float* base_ws = P.attn_ws + bh * nch * (hd + 2);
+  float M = -INFINITY;
+  for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base_ws + c * (hd + 2)));
+  float L = 0.f, O[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) O[e] = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    const float* w = base_ws + c * (hd + 2);
+    const float f = expf(__ldcg(w) - M);
+    L += __ldcg(w + 1) * f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) O[e] += __ldcg(w + 2 + DPL * lane + e) * f;
   }
-  named_sync(bar, 128);
-  if (S.last) {
-    __threadfence();
-    const float* base = P.attn_ws + (static_cast<int64_t>(b) * H + h) * nch * (hd + 2);
-    float M = -INFINITY;
-    for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2)));
-    for (int i = gtid; i < hd; i += 128) {
-      float L = 0.f, O = 0.f;
-      for (int c = 0; c < nch; ++c) {
-        const float f = expf(__ldcg(base + c * (hd + 2)) - M);
-        L += __ldcg(base + c * (hd + 2) + 1) * f;
-        O += __ldcg(base + c * (hd + 2) + 2 + i) * f;
-      }
-      store_out(P.attn_out, adt, static_cast<int64_t>(b) * d + h * hd + i, O / L);
-    }
-    if (gtid == 0) P.tickets[b * H + h] = 0u;
-  }
-  named_sync(bar, 128);
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, O[e] / L);
+  if (lane == 0) P.tickets[bh] = 0u;
 }
 
-__device__ void run_attn(const Phase& P, AttnSmem* S) {
-  const int group = threadIdx.x >> 7;  // 4 groups of 4 warps
-  const int gtid = threadIdx.x & 127;
-  const int groups = kNCW / 4;
-  // items: for every row b and head h, the active key chunks of that row
+__device__ void run_attn(const Phase& P, AttnSmem& S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // items: for every row b and head h, the active key chunks of that row; item i runs on CTA
+  // i % grid, warp (i / grid) % kNCW (spread over the whole GPU)
   int total = 0;
   for (int b = 0; b < P.B; ++b) total += P.n_heads * ((P.pos[b] + kAttnChunk) / kAttnChunk);
-  for (int item = blockIdx.x * groups + group; item < total; item += gridDim.x * groups) {
+  for (int item = warp * gridDim.x + blockIdx.x; item < total; item += gridDim.x * kNCW) {
     int rem = item, b = 0;
     for (;; ++b) {
       const int per = P.n_heads * ((P.pos[b] + kAttnChunk) / kAttnChunk);
@@ -652,83 +1187,42 @@ __device__ void run_attn(const Phase& P, AttnSmem* S) {
       rem -= per;
     }
     const int nch = (P.pos[b] + kAttnChunk) / kAttnChunk;
-    attn_item(P, b, rem / nch, rem % nch, nch, S[group], gtid, 2 + group);
+    const int h = rem / nch, c = rem % nch;
+    if (P.head_dim == 128) attn_item<4>(P, b, h, c, nch, lane, warp, S);
+    else attn_item<2>(P, b, h, c, nch, lane, warp, S);
   }
 }
 
 // ---------------------------------------------------------------- consumers: row statistics
-// softmax_double / ppl_entropy / fault_tolerance / argmax_token of logits row b on CTA b.
-__device__ void run_stats(const Phase& P, double* shd) {
+// Combines the head GEMV's per-CTA softmax partials of row b (warp b of CTA 0, fixed-order merge)
+// into fq_row_stats: ppl_entropy / fault_tolerance / argmax_token (src/scheduler.cpp:13-49,
+// src/engine.cpp:144-155) in double.
+__device__ void run_stats(const Phase& P) {
+  if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nthreads = kNCW * 32;
-  for (int b = blockIdx.x; b < P.B; b += gridDim.x) {
-    const float* l = P.logits + b * P.vocab;
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-    for (int64_t i = threadIdx.x; i < P.vocab; i += nthreads) {
-      const float x = l[i];
-      if (x > bv || (x == bv && i < bi)) { bv = x; bi = static_cast<int>(i); }
-    }
+  const StatPart* parts = static_cast<const StatPart*>(P.stat_part);
+  const int n = gridDim.x;
+  for (int b = warp; b < P.B; b += kNCW) {
+    StatPart a;
+    stat_init(a);
+    for (int c = lane; c < n; c += 32) a = stat_merge(a, parts[b * n + c]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    for (int o = 1; o < 32; o <<= 1) {
+      const StatPart o2 = stat_shfl(a, o);
+      a = (lane & o) ? stat_merge(o2, a) : stat_merge(a, o2);
     }
-    float* shv = reinterpret_cast<float*>(shd + 3 * kNCW);
-    int* shi = reinterpret_cast<int*>(shv + kNCW);
-    if (lane == 0) { shv[warp] = bv; shi[warp] = bi; }
-    named_sync(1, nthreads);
-    float mxv = shv[0];
-    int mxi = shi[0];
-    for (int w = 1; w < kNCW; ++w)
-      if (shv[w] > mxv || (shv[w] == mxv && shi[w] < mxi)) { mxv = shv[w]; mxi = shi[w]; }
-    const double mx = mxv;
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < P.vocab; i += nthreads) s += exp(static_cast<double>(l[i]) - mx);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    named_sync(1, nthreads);
-    if (lane == 0) shd[warp] = s;
-    named_sync(1, nthreads);
-    double sum = 0.0;
-    for (int w = 0; w < kNCW; ++w) sum += shd[w];
-    double h = 0.0, t1 = -1.0, t2 = -1.0;
-    for (int64_t i = threadIdx.x; i < P.vocab; i += nthreads) {
-      const double p = exp(static_cast<double>(l[i]) - mx) / sum;
-      if (p > 0.0) h -= p * log(p);
-      if (p > t1) { t2 = t1; t1 = p; } else if (p > t2) { t2 = p; }
+    if (lane == 0) {
+      fq_row_stats r;
+      const double H = log(a.S) - a.T / a.S;
+      r.entropy = H;
+      r.ppl_entropy = exp(H);
+      r.p1 = exp(static_cast<double>(a.v1) - a.m) / a.S;
+      r.p2 = a.v2 == -INFINITY ? -1.0 : exp(static_cast<double>(a.v2) - a.m) / a.S;
+      r.fault_tolerance = r.p1 - r.p2;
+      r.max_logit = a.m;
+      r.argmax = a.arg == 0x7fffffff ? 0 : a.arg;
+      P.stats[b] = r;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      h += __shfl_xor_sync(0xffffffffu, h, o);
-      const double o1 = __shfl_xor_sync(0xffffffffu, t1, o), o2 = __shfl_xor_sync(0xffffffffu, t2, o);
-      const double n1 = fmax(t1, o1), n2 = fmax(fmin(t1, o1), fmax(t2, o2));
-      t1 = n1;
-      t2 = n2;
-    }
-    named_sync(1, nthreads);
-    if (lane == 0) { shd[warp] = h; shd[kNCW + warp] = t1; shd[2 * kNCW + warp] = t2; }
-    named_sync(1, nthreads);
-    if (threadIdx.x == 0) {
-      double H = 0.0, a1 = -1.0, a2 = -1.0;
-      for (int w = 0; w < kNCW; ++w) {
-        H += shd[w];
-        const double n1 = fmax(a1, shd[kNCW + w]), n2 = fmax(fmin(a1, shd[kNCW + w]), fmax(a2, shd[2 * kNCW + w]));
-        a1 = n1;
-        a2 = n2;
-      }
-      fq_row_stats st;
-      st.entropy = H;
-      st.ppl_entropy = exp(H);
-      st.p1 = a1;
-      st.p2 = a2;
-      st.fault_tolerance = a1 - a2;
-      st.max_logit = mxv;
-      st.argmax = mxi;
-      P.stats[b] = st;
-    }
-    named_sync(1, nthreads);
   }
 }
 
@@ -748,25 +1242,46 @@ __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
 }
 
 // ---------------------------------------------------------------- the program kernel
-template <int BB>
-__device__ void run_program(const Phase* phases, int nphases, unsigned int* barrier, int stage_bytes, int nstages,
-                            int red_floats, int xs_floats) {
+// Dynamic shared memory: ring stages | full/empty mbarriers | xs | dx | red | sq | rstd.
+struct SmemLayout {
+  int nstages, xs_bytes, dx_bytes, red_bytes;
+  int ctl_phases;  // phases with a precomputed partition table in shared memory (0 = none)
+  int prefetch;  // L2 prefetch distance of the weight stream, in stages
+};
+
+__device__ void run_program(const Phase* phases, int nphases, unsigned int* barrier, SmemLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float sq_red[kMaxB][kNCW];
-  __shared__ AttnSmem attn_smem[kNCW / 4];
-  __shared__ double stat_smem[5 * kNCW];
+  __shared__ AttnSmem attn_smem;
+  __shared__ PhaseCtl ctl;
+  __shared__ int trace_n;
+  __shared__ Phase pbuf[2];
   Ring R;
   R.base = smem;
-  R.full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(nstages) * stage_bytes);
+  R.nstages = L.nstages;
+  R.full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(L.nstages) * kStageBytes);
   R.empty = R.full + kMaxStages;
-  R.stage_bytes = stage_bytes;
-  R.nstages = nstages;
-  float* red = reinterpret_cast<float*>(R.empty + kMaxStages);
-  float4* xsm = reinterpret_cast<float4*>(red + ((red_floats + 3) & ~3));
-  float* sigm = reinterpret_cast<float*>(xsm + xs_floats / 4);
+  GemvSmem G;
+  uint8_t* p = reinterpret_cast<uint8_t*>(R.empty + kMaxStages);
+  G.xs = reinterpret_cast<uint4*>(p);
+  p += L.xs_bytes;
+  G.dx = reinterpret_cast<float4*>(p);
+  p += L.dx_bytes;
+  G.red = reinterpret_cast<float*>(p);
+  p += L.red_bytes;
+  G.sq = reinterpret_cast<float*>(p);
+  p += kNCW * 32 * sizeof(float);
+  G.rstd = reinterpret_cast<float*>(p);
+  p += kMaxB * sizeof(float);
+  G.mbuf = reinterpret_cast<float*>(p);
+  p += kMaxMat * 16 * kMaxB * sizeof(float);
+  CtlEntry* ctab = L.ctl_phases > 0 ? reinterpret_cast<CtlEntry*>(p) : nullptr;
+  G.tr = blockIdx.x == static_cast<unsigned>(g_trace_cta) ? g_ring_trace : nullptr;
+  G.tn = &trace_n;
+  if (threadIdx.x == 0) trace_n = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nstages; ++s) {
+    for (int s = 0; s < L.nstages; ++s) {
       mbar_init(&R.full[s], 1);
       mbar_init(&R.empty[s], kNCW);
     }
@@ -776,10 +1291,8 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   if (warp == kNCW) {
     // the weight stream depends on nothing produced at run time: start immediately
     if (lane == 0) {
-      int slot_i = 0;
-      uint32_t phase_bit = 0;
-      for (int i = 0; i < nphases; ++i)
-        if (phases[i].type == PH_GEMV) produce_phase(phases[i], R, slot_i, phase_bit);
+      unsigned long long* tr = blockIdx.x == static_cast<unsigned>(g_trace_cta) ? g_ring_trace : nullptr;
+      produce_all(phases, nphases, R, tr, L.prefetch);
     }
     return;
   }
@@ -787,82 +1300,139 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   int slot_i = 0;
   uint32_t phase_bit = 0;
   unsigned int epoch = 0;
+  unsigned long long* prof = threadIdx.x == 0 ? g_phase_prof : nullptr;
+  if (prof) prof[static_cast<size_t>(nphases) * gridDim.x * 2 + blockIdx.x] = gtimer();
+  // Phase descriptors live in shared memory: warp 0 loads descriptor i+1 into registers during
+  // phase i (one 16-byte load per lane, latency hidden by the phase) and stores it at the end.
+  if (ctab)
+    for (int t = threadIdx.x; t < nphases; t += kNCW * 32) compute_ctl(phases[t], ctab[t]);
+  constexpr int kPW = static_cast<int>(sizeof(Phase) / 16);
+  uint4 next_desc = make_uint4(0u, 0u, 0u, 0u);
+  if (warp == 0) {
+    if (lane < kPW) reinterpret_cast<uint4*>(&pbuf[0])[lane] = reinterpret_cast<const uint4*>(&phases[0])[lane];
+    if (nphases > 1 && lane < kPW) next_desc = reinterpret_cast<const uint4*>(&phases[1])[lane];
+  }
+  named_sync(1, kNCW * 32);
   for (int i = 0; i < nphases; ++i) {
-    const Phase& P = phases[i];
-    if (P.type == PH_GEMV) run_gemv_phase<BB>(P, R, red, sq_red, xsm, sigm, slot_i, phase_bit);
+    const Phase& P = pbuf[i & 1];
+    if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
     else if (P.type == PH_ATTN) run_attn(P, attn_smem);
-    else run_stats(P, stat_smem);
-    if (P.barrier_after && i + 1 < nphases) grid_barrier(barrier, epoch);
-  }
-}
-
-template <int BB>
-__global__ void __launch_bounds__(kThreads, 1) program_kernel(const Phase* phases, int nphases, unsigned int* barrier,
-                                                              int stage_bytes, int nstages, int red_floats,
-                                                              int xs_floats) {
-  run_program<BB>(phases, nphases, barrier, stage_bytes, nstages, red_floats, xs_floats);
-}
-
-template <int BB>
-__global__ void __launch_bounds__(kThreads, 1) program_kernel_inline(const __grid_constant__ InlineProgram prog,
-                                                                     int nphases, unsigned int* barrier,
-                                                                     int stage_bytes, int nstages, int red_floats,
-                                                                     int xs_floats) {
-  run_program<BB>(prog.phases, nphases, barrier, stage_bytes, nstages, red_floats, xs_floats);
-}
-
-template <int BB>
-void launch_t(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, bool pdl) {
-  static std::mutex mu;
-  static bool configured = false;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (!configured) {
-      FQ_CUDA(cudaFuncSetAttribute(program_kernel<BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      FQ_CUDA(cudaFuncSetAttribute(program_kernel_inline<BB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      configured = true;
+    else run_stats(P);
+    if (prof) prof[(static_cast<size_t>(i) * gridDim.x + blockIdx.x) * 2] = gtimer();
+    const bool bar = P.barrier_after && i + 1 < nphases;
+    named_sync(1, kNCW * 32);  // everyone is done with descriptor i
+    if (warp == 0 && i + 1 < nphases) {
+      if (lane < kPW) reinterpret_cast<uint4*>(&pbuf[(i + 1) & 1])[lane] = next_desc;
+      if (i + 2 < nphases && lane < kPW) next_desc = reinterpret_cast<const uint4*>(&phases[i + 2])[lane];
     }
+    if (bar) grid_barrier(barrier, epoch);
+    else named_sync(1, kNCW * 32);
+    if (prof) prof[(static_cast<size_t>(i) * gridDim.x + blockIdx.x) * 2 + 1] = gtimer();
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(run.grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = run.smem;
-  cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  if (run.dev_phases)
-    FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel<BB>, static_cast<const Phase*>(run.dev_phases), run.nphases,
-                               barrier, run.stage_bytes, run.nstages, run.red_floats, run.xs_floats));
-  else
-    FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel_inline<BB>, run.inl, run.nphases, barrier, run.stage_bytes,
-                               run.nstages, run.red_floats, run.xs_floats));
-  ctx->launches += 1;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) program_kernel(const Phase* phases, int nphases, unsigned int* barrier,
+                                                              SmemLayout L) {
+  run_program(phases, nphases, barrier, L);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) program_kernel_inline(const __grid_constant__ InlineProgram prog,
+                                                                     int nphases, unsigned int* barrier, SmemLayout L) {
+  run_program(prog.phases, nphases, barrier, L);
+}
+
+int max_dynamic_smem() {
+  static int v = -1;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (v < 0) {
+    int dev = 0, optin = 0;
+    FQ_CUDA(cudaGetDevice(&dev));
+    FQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes a1{}, a2{};
+    FQ_CUDA(cudaFuncGetAttributes(&a1, program_kernel));
+    FQ_CUDA(cudaFuncGetAttributes(&a2, program_kernel_inline));
+    v = optin - static_cast<int>(std::max(a1.sharedSizeBytes, a2.sharedSizeBytes)) - 1024;
+    FQ_CUDA(cudaFuncSetAttribute(program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+    FQ_CUDA(cudaFuncSetAttribute(program_kernel_inline, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+  }
+  return v;
+}
+
+constexpr int kMaxCtlPhases = 512;  // longer programs compute their partitions per phase
+
+SmemLayout layout_for(int64_t kpad, int bb, int nphases, int& nstages_out, size_t& total_out) {
+  SmemLayout L{};
+  L.xs_bytes = static_cast<int>(kpad * 2 * bb);
+  L.dx_bytes = static_cast<int>(kpad / kBlockK * bb * 16);
+  L.red_bytes = std::max(16 * 1024, 2 * kMaxMat * kNCW * 16 * bb * 4);
+  L.ctl_phases = nphases <= kMaxCtlPhases ? nphases : 0;
+  const int fixed = 2 * kMaxStages * 8 + L.xs_bytes + L.dx_bytes + L.red_bytes + kNCW * 32 * 4 + kMaxB * 4 +
+                    kMaxMat * 16 * kMaxB * 4 + L.ctl_phases * static_cast<int>(sizeof(CtlEntry));
+  const int budget = max_dynamic_smem();
+  L.nstages = std::min(kMaxStages, (budget - fixed) / kStageBytes);
+  nstages_out = L.nstages;
+  total_out = static_cast<size_t>(L.nstages) * kStageBytes + fixed;
+  return L;
 }
 
 }  // namespace
 
-ProgramRun upload_program(fq_ctx* ctx, const ProgramBuilder& pb, bool transient) {
+int gemv_batch_chunk(int64_t K) {
+  const int64_t kpad = (K + kBlockK - 1) / kBlockK * kBlockK;
+  for (int bb = kMaxB; bb > 1; --bb) {
+    int ns = 0;
+    size_t tot = 0;
+    layout_for(kpad, bb, 200, ns, tot);
+    if (ns >= 3) return bb;
+  }
+  return 1;
+}
+
+ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   ProgramRun r;
   r.nphases = static_cast<int>(pb.phases.size());
   r.grid = pb.grid;
   r.bb = pb.max_bb;
-  const int64_t stage = std::max<int64_t>(pb.stage_bytes, 128);
-  r.red_floats = static_cast<int>((pb.red_floats + 3) & ~int64_t(3));
-  const int bbk = pb.max_bb <= 1 ? 1 : (pb.max_bb <= 2 ? 2 : 4);  // kernel instantiation's batch bound
-  r.xs_floats = static_cast<int>(static_cast<int64_t>(pb.max_nsteps) * kStepCodes * bbk);
-  const size_t red_bytes = static_cast<size_t>(r.red_floats) * sizeof(float);
-  const size_t xs_bytes = static_cast<size_t>(r.xs_floats) * sizeof(float) +
-                          static_cast<size_t>(pb.max_nsteps) * 32 * bbk * sizeof(float);
-  const int64_t budget = 200 * 1024 - static_cast<int64_t>(red_bytes + xs_bytes) - 2 * kMaxStages * 8 - 256;
-  r.nstages = static_cast<int>(std::min<int64_t>(kMaxStages, budget / stage));
-  if (r.nstages < 2) fail(FQ_E_CONFIG, "gemv: layer rows too large for the shared-memory ring");
-  r.stage_bytes = static_cast<int>(stage);
-  r.smem = static_cast<size_t>(r.nstages) * r.stage_bytes + 2 * kMaxStages * 8 + red_bytes + xs_bytes;
-  if (r.nphases <= kInlinePhases && transient) {
+  int ns = 0;
+  size_t tot = 0;
+  const SmemLayout L = layout_for(pb.max_kpad, pb.max_bb, r.nphases, ns, tot);
+  if (ns < 2) fail(FQ_E_CONFIG, "gemv: activations of this width do not fit in shared memory");
+  r.nstages = ns;
+  r.smem = tot;
+  r.xs_bytes = L.xs_bytes;
+  r.dx_bytes = L.dx_bytes;
+  r.red_bytes = L.red_bytes;
+  r.ctl_phases = L.ctl_phases;
+  if (const char* e = std::getenv("FQ_PREFETCH")) r.prefetch = std::atoi(e);
+  const size_t fstride = static_cast<size_t>(kMaxMat) * 16 * pb.max_bb;
+  const bool inl = r.nphases <= kInlinePhases && transient;
+  float* fix;
+  unsigned int* flags;
+  if (inl) {
+    if (ctx->gemv_fix == nullptr) {
+      ctx->gemv_fix = static_cast<float*>(dmalloc(sizeof(float) * kInlinePhases * 1024 * kMaxMat * 16 * kMaxB));
+      ctx->gemv_flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * kInlinePhases * 1024));
+      FQ_CUDA(cudaMemset(ctx->gemv_flags, 0, sizeof(unsigned int) * kInlinePhases * 1024));
+    }
+    if (r.grid > 1024) fail(FQ_E_CONFIG, "gemv: grid too large");
+    fix = ctx->gemv_fix;
+    flags = ctx->gemv_flags;
+  } else {
+    r.fix = static_cast<float*>(dmalloc(sizeof(float) * r.nphases * r.grid * fstride));
+    r.flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * r.nphases * r.grid));
+    FQ_CUDA(cudaMemset(r.flags, 0, sizeof(unsigned int) * r.nphases * r.grid));
+    fix = r.fix;
+    flags = r.flags;
+  }
+  for (int i = 0; i < r.nphases; ++i) {
+    Phase& P = pb.phases[i];
+    if (P.type != PH_GEMV) continue;
+    P.fix = fix + static_cast<size_t>(i) * r.grid * (inl ? kMaxMat * 16 * kMaxB : fstride);
+    P.flags = flags + static_cast<size_t>(i) * (inl ? 1024 : r.grid);
+  }
+  if (inl) {
     for (int i = 0; i < r.nphases; ++i) r.inl.phases[i] = pb.phases[i];
   } else {
     r.dev_phases = static_cast<Phase*>(dmalloc(sizeof(Phase) * r.nphases));
@@ -874,9 +1444,29 @@ ProgramRun upload_program(fq_ctx* ctx, const ProgramBuilder& pb, bool transient)
 }
 
 void launch_program(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, bool pdl) {
-  if (run.bb <= 1) launch_t<1>(ctx, run, barrier, pdl);
-  else if (run.bb == 2) launch_t<2>(ctx, run, barrier, pdl);
-  else launch_t<4>(ctx, run, barrier, pdl);
+  SmemLayout L{};
+  L.nstages = run.nstages;
+  L.xs_bytes = run.xs_bytes;
+  L.dx_bytes = run.dx_bytes;
+  L.red_bytes = run.red_bytes;
+  L.prefetch = run.prefetch;
+  L.ctl_phases = run.ctl_phases;
+  max_dynamic_smem();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(run.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = run.smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (run.dev_phases)
+    FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel, static_cast<const Phase*>(run.dev_phases), run.nphases, barrier, L));
+  else
+    FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel_inline, run.inl, run.nphases, barrier, L));
+  ctx->launches += 1;
 }
 
 }  // namespace fqc

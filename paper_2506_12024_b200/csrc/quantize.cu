@@ -141,13 +141,66 @@ __global__ void zp_range_kernel(const int32_t* __restrict__ zp, int64_t n, int* 
   }
 }
 
-__global__ void zp_pack_kernel(const int32_t* __restrict__ zp, int64_t N, int64_t ng, int64_t zp_pad, int32_t base,
-                               uint8_t* __restrict__ out) {
-  const int64_t n = N * zp_pad;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / zp_pad, g = i % zp_pad;
-    out[i] = g < ng ? static_cast<uint8_t>(zp[r * ng + g] - base) : 0;
+// Builds the tiled fast-path copy (fq_internal.cuh) of one rung from its canonical arrays:
+// one CTA per 16x128 block, 128 threads = (word i, lane t) of the code region, then the meta.
+__device__ __forceinline__ uint32_t canon_code(const uint8_t* __restrict__ p, int bits, int64_t N, int64_t K,
+                                               int64_t row, int64_t k) {
+  if (row >= N || k >= K) return 0u;
+  const int64_t idx = row * K + k;
+  if (bits == 8) return p[idx];
+  const uint32_t b = p[idx >> 1];
+  return (idx & 1) ? (b >> 4) : (b & 0xFu);
+}
+
+__global__ void tile_pack_kernel(const uint8_t* __restrict__ payload, const float* __restrict__ scale,
+                                 const int32_t* __restrict__ zp32, int64_t N, int64_t K, int64_t G, int64_t ng,
+                                 int64_t ng_pad, int bits, int32_t zbase, int64_t nkb, uint8_t* __restrict__ out) {
+  const int64_t blk = blockIdx.x;
+  const int64_t tile = blk / nkb, kb = blk % nkb;
+  const int bb = bits == 8 ? kBlockBytes8 : kBlockBytes4;
+  uint8_t* dst = out + blk * bb;
+  const int64_t row0 = tile * kTileRows;
+  const int t = threadIdx.x & 31, i = threadIdx.x >> 5;
+  const int r = t >> 2, c2 = 2 * (t & 3);
+  if (bits == 8) {
+    uint32_t u[4];
+    for (int h = 0; h < 2; ++h) {
+      const int64_t k0 = kb * kBlockK + 16 * (2 * i + h) + c2;
+      for (int e = 0; e < 2; ++e) {
+        const int64_t k = k0 + 8 * e;
+        u[2 * h + e] = canon_code(payload, 8, N, K, row0 + r, k) | canon_code(payload, 8, N, K, row0 + r, k + 1) << 8 |
+                       canon_code(payload, 8, N, K, row0 + r + 8, k) << 16 |
+                       canon_code(payload, 8, N, K, row0 + r + 8, k + 1) << 24;
+      }
+    }
+    reinterpret_cast<uint4*>(dst)[i * 32 + t] = make_uint4(u[0], u[1], u[2], u[3]);
+  } else if (i < 2) {
+    uint32_t u[4];
+    for (int v = 0; v < 4; ++v) {
+      const int64_t k0 = kb * kBlockK + 16 * (4 * i + v) + c2;
+      const int64_t ra = row0 + r, rb = row0 + r + 8;
+      const uint32_t n[8] = {canon_code(payload, 4, N, K, ra, k0),     canon_code(payload, 4, N, K, ra, k0 + 8),
+                             canon_code(payload, 4, N, K, rb, k0),     canon_code(payload, 4, N, K, rb, k0 + 8),
+                             canon_code(payload, 4, N, K, ra, k0 + 1), canon_code(payload, 4, N, K, ra, k0 + 9),
+                             canon_code(payload, 4, N, K, rb, k0 + 1), canon_code(payload, 4, N, K, rb, k0 + 9)};
+      uint32_t w = 0;
+      for (int e = 0; e < 8; ++e) w |= n[e] << (4 * e);
+      u[v] = w;
+    }
+    reinterpret_cast<uint4*>(dst)[i * 32 + t] = make_uint4(u[0], u[1], u[2], u[3]);
+  }
+  if (threadIdx.x < kTileRows) {
+    const int64_t row = row0 + threadIdx.x;
+    const int64_t g = (kb * kBlockK) / G;
+    const int codes = bits == 8 ? 2048 : 1024;
+    float sc = 0.f;
+    uint8_t z = 0;
+    if (row < N) {
+      sc = scale[row * ng_pad + g];
+      z = static_cast<uint8_t>(zp32[row * ng + g] - zbase);
+    }
+    reinterpret_cast<float*>(dst + codes)[threadIdx.x] = sc;
+    dst[codes + 64 + threadIdx.x] = z;
   }
 }
 
@@ -167,10 +220,16 @@ void finalize_rung_meta(fq_ctx* ctx, fq_layer* L, int rung) {
   FQ_CUDA(cudaStreamSynchronize(ctx->stream));
   st.zp_fits_u8 = (static_cast<int64_t>(h[1]) - h[0]) <= 255;
   st.zp_base = st.zp_fits_u8 ? h[0] : 0;
-  if (st.zp_fits_u8) {
-    if (st.zp8 == nullptr) st.zp8 = static_cast<uint8_t*>(dmalloc(static_cast<size_t>(L->N * L->zp_pad)));
-    const int pblocks = static_cast<int>(std::min<int64_t>(1024, (L->N * L->zp_pad + 255) / 256));
-    zp_pack_kernel<<<std::max(pblocks, 1), 256, 0, ctx->stream>>>(st.zp32, L->N, L->ng, L->zp_pad, st.zp_base, st.zp8);
+  const bool one_group_per_block = L->G % kBlockK == 0 || L->G >= L->K;
+  dfree(st.tiles);
+  st.tiles = nullptr;
+  st.tiles_bytes = 0;
+  if (st.zp_fits_u8 && one_group_per_block) {
+    const int64_t n_tiles = (L->N + kTileRows - 1) / kTileRows, nkb = (L->K + kBlockK - 1) / kBlockK;
+    st.tiles_bytes = n_tiles * nkb * (st.bits == 8 ? kBlockBytes8 : kBlockBytes4);
+    st.tiles = static_cast<uint8_t*>(dmalloc(static_cast<size_t>(st.tiles_bytes)));
+    tile_pack_kernel<<<static_cast<unsigned>(n_tiles * nkb), 128, 0, ctx->stream>>>(
+        st.payload, st.scale, st.zp32, L->N, L->K, L->G, L->ng, L->ng_pad, st.bits, st.zp_base, nkb, st.tiles);
     FQ_CUDA(cudaGetLastError());
     ctx->launches += 1;
   }

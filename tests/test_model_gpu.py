@@ -207,8 +207,11 @@ def test_llama_batched_slots_match_single(ctx):
         single.append(rows)
     for t in range(8):
         for s in range(3):
+            # a heterogeneous batch streams both copies, so the stream-K split (and with it the fp32
+            # summation grouping) differs from the single-row run: equal within the north-star
+            # entropy tolerance, not bit-equal
             assert outs[t]["argmax"][s] == single[s][t]["argmax"]
-            assert abs(outs[t]["entropy"][s] - single[s][t]["entropy"]) <= 1e-5
+            assert abs(outs[t]["entropy"][s] - single[s][t]["entropy"]) <= 1e-4
 
 
 def test_llama_capacity_and_errors(ctx):

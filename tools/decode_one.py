@@ -16,6 +16,7 @@ ap.add_argument("--prompt", type=int, default=8)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--w4", action="store_true")
 ap.add_argument("--layers", type=int, default=32)
+ap.add_argument("--fixed-token", type=int, default=-1)
 a = ap.parse_args()
 ctx = capi.Context(0)
 m = capi.Model(ctx, arch=capi.ARCH_LLAMA, act_dtype=capi.DT_BF16, max_batch=1, group_size=128, max_seq_len=512,
@@ -29,7 +30,7 @@ row = st[-1]
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 for _ in range(a.steps):
-    row = m.decode([0], [int(row["argmax"])])[0]
+    row = m.decode([0], [int(row["argmax"]) if a.fixed_token < 0 else a.fixed_token])[0]
 torch.cuda.synchronize()
 dt = (time.perf_counter() - t0) / a.steps
 ms, n, b = m.profile_gemvs(0, 10)
