@@ -14,7 +14,7 @@ constexpr int kMaxMat = 3;        // matrices sharing one input (QKV)
 constexpr int kMaxStages = 8;
 constexpr int kNCW = 8;           // consumer warps (2 blocks in flight each)
 constexpr int kThreads = (kNCW + 1) * 32;  // + one producer warp
-constexpr int kAttnChunk = 64;    // keys per attention work item
+constexpr int kAttnChunk = 16;    // keys per attention work item (one warp)
 constexpr int kStageBytes = 35328;  // max(16 W8 blocks, 32 W4 blocks)
 constexpr int kStageBlocks8 = 16;
 constexpr int kStageBlocks4 = 32;

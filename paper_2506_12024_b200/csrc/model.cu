@@ -49,156 +49,6 @@ struct StepMeta {
   const int32_t* slots;
 };
 
-// ------------------------------------------------------------------ llama kernels
-__global__ void embed_llama_kernel(const float* __restrict__ tok_emb, StepMeta meta, int64_t d,
-                                   float* __restrict__ resid, float* __restrict__ partials) {
-  const int b = blockIdx.x;
-  const float* e = tok_emb + static_cast<int64_t>(meta.tokens[b]) * d;
-  float* x = resid + b * d;
-  float sq = 0.f;
-  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-    const float v = e[c];
-    x[c] = v;
-    sq += v * v;
-  }
-  __shared__ float red[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
-    partials[b * kPartStride] = s;
-  }
-}
-
-// RoPE (rotate-half pairing, HF Llama convention): for i < hd/2 the pair (i, i + hd/2) rotates
-// by angle pos * theta^(-2i/hd); angles in double.
-__device__ __forceinline__ void rope_pair(float& a, float& b, int i, int hd, int pos, float theta) {
-  const double inv = pow(static_cast<double>(theta), -2.0 * i / hd);
-  double sn, cs;
-  sincos(static_cast<double>(pos) * inv, &sn, &cs);
-  const float c = static_cast<float>(cs), s = static_cast<float>(sn);
-  const float x0 = a, x1 = b;
-  a = x0 * c - x1 * s;
-  b = x1 * c + x0 * s;
-}
-
-// Decode attention for one (head, batch row, key chunk).  The chunk holding the row's own
-// position rotates and appends the new key/value to the fp16 cache.  Partial softmax states are
-// merged by the last CTA of the (row, head) in chunk order.
-__global__ void __launch_bounds__(128) attn_llama_kernel(const void* __restrict__ q, const void* __restrict__ k,
-                                                         const void* __restrict__ v, int act_dtype, StepMeta meta,
-                                                         __half* __restrict__ kv, int64_t slot_stride,
-                                                         int64_t layer_off, int64_t max_seq, int n_heads, int hd,
-                                                         float theta, float* __restrict__ ws,
-                                                         unsigned int* __restrict__ tickets, void* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  const int h = blockIdx.x, b = blockIdx.y, chunk = blockIdx.z, nchunks = gridDim.z;
-  const int pos = meta.pos[b];
-  const int slot = meta.slots[b];
-  const int d = n_heads * hd;
-  __shared__ float qs[256];
-  __shared__ float knew[256];
-  __shared__ float sc[kAttnChunk];
-  __shared__ bool last;
-  const int j0 = chunk * kAttnChunk;
-  const int j1 = min(j0 + kAttnChunk, pos + 1);
-  __half* kc = kv + slot * slot_stride + layer_off + static_cast<int64_t>(h) * max_seq * hd;
-  __half* vc = kc + static_cast<int64_t>(n_heads) * max_seq * hd;
-  float* wsp = ws + ((static_cast<int64_t>(b) * n_heads + h) * nchunks + chunk) * (hd + 2);
-  if (j0 <= pos) {
-    // q with RoPE, pre-scaled by 1/sqrt(hd)
-    const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-    for (int i = threadIdx.x; i < hd / 2; i += blockDim.x) {
-      float a0 = act_load(q, act_dtype, static_cast<int64_t>(b) * d + h * hd + i);
-      float a1 = act_load(q, act_dtype, static_cast<int64_t>(b) * d + h * hd + i + hd / 2);
-      rope_pair(a0, a1, i, hd, pos, theta);
-      qs[i] = a0 * scale;
-      qs[i + hd / 2] = a1 * scale;
-    }
-    const bool owns_new = pos >= j0 && pos < j0 + kAttnChunk;
-    if (owns_new) {
-      for (int i = threadIdx.x; i < hd / 2; i += blockDim.x) {
-        float a0 = act_load(k, act_dtype, static_cast<int64_t>(b) * d + h * hd + i);
-        float a1 = act_load(k, act_dtype, static_cast<int64_t>(b) * d + h * hd + i + hd / 2);
-        rope_pair(a0, a1, i, hd, pos, theta);
-        const __half h0 = __float2half_rn(a0), h1 = __float2half_rn(a1);
-        kc[static_cast<int64_t>(pos) * hd + i] = h0;
-        kc[static_cast<int64_t>(pos) * hd + i + hd / 2] = h1;
-        knew[i] = __half2float(h0);
-        knew[i + hd / 2] = __half2float(h1);
-      }
-      for (int i = threadIdx.x; i < hd; i += blockDim.x)
-        vc[static_cast<int64_t>(pos) * hd + i] = __float2half_rn(act_load(v, act_dtype, static_cast<int64_t>(b) * d + h * hd + i));
-    }
-    __syncthreads();
-    // scores: one warp per key
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = j0 + warp; j < j1; j += nw) {
-      float s = 0.f;
-      if (j == pos) {
-        for (int i = lane; i < hd; i += 32) s += qs[i] * knew[i];
-      } else {
-        const __half* kr = kc + static_cast<int64_t>(j) * hd;
-        for (int i = lane; i < hd; i += 32) s += qs[i] * __half2float(kr[i]);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) sc[j - j0] = s;
-    }
-    __syncthreads();
-    float m = -INFINITY;
-    for (int j = 0; j < j1 - j0; ++j) m = fmaxf(m, sc[j]);
-    // o[i] = sum_j exp(s_j - m) v_j[i]
-    for (int i = threadIdx.x; i < hd; i += blockDim.x) {
-      float acc = 0.f, l = 0.f;
-      for (int j = j0; j < j1; ++j) {
-        const float p = expf(sc[j - j0] - m);
-        const float vv = (j == pos) ? __half2float(__float2half_rn(act_load(v, act_dtype, static_cast<int64_t>(b) * d + h * hd + i)))
-                                    : __half2float(vc[static_cast<int64_t>(j) * hd + i]);
-        acc += p * vv;
-        l += p;
-      }
-      wsp[2 + i] = acc;
-      if (i == 0) {
-        wsp[0] = m;
-        wsp[1] = l;
-      }
-    }
-  } else if (threadIdx.x == 0) {
-    wsp[0] = -INFINITY;
-    wsp[1] = 0.f;
-  }
-  // last CTA of this (row, head) merges the chunks in order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(&tickets[b * n_heads + h], 1u);
-    last = prev == static_cast<unsigned int>(nchunks - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const float* base = ws + (static_cast<int64_t>(b) * n_heads + h) * nchunks * (hd + 2);
-  float M = -INFINITY;
-  for (int c = 0; c < nchunks; ++c) M = fmaxf(M, __ldcg(base + c * (hd + 2)));
-  for (int i = threadIdx.x; i < hd; i += blockDim.x) {
-    float L = 0.f, O = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      const float mc = __ldcg(base + c * (hd + 2));
-      if (mc == -INFINITY) continue;
-      const float f = expf(mc - M);
-      L += __ldcg(base + c * (hd + 2) + 1) * f;
-      O += __ldcg(base + c * (hd + 2) + 2 + i) * f;
-    }
-    act_store(out, act_dtype, static_cast<int64_t>(b) * d + h * hd + i, O / L);
-  }
-  if (threadIdx.x == 0) tickets[b * n_heads + h] = 0u;
-}
-
 // Fused softmax statistics of B logits rows (double), one CTA per row; writes fq_row_stats.
 // (Same arithmetic as stats.cu, kept local so the step graph has no cross-TU dependency.)
 __global__ void __launch_bounds__(1024) row_stats_kernel(const float* __restrict__ logits, int64_t vocab,

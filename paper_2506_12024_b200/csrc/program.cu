@@ -8,6 +8,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
+#ifndef FQ_DBG
+#define FQ_DBG 0
+#endif
 #include <cfloat>
 #include <cstring>
 #include <map>
@@ -63,9 +66,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Deadlock watchdog: a wait that has not completed after kWatchdogNs reports where it is stuck
+// and traps (the launch fails with an error instead of hanging the device).
+constexpr unsigned long long kWatchdogNs = 4000000000ull;
+__device__ __noinline__ void watchdog_fire(const char* what, int a, int b) {
+  printf("fq watchdog: %s stuck (cta %d, thread %d, %d, %d)\n", what, blockIdx.x, threadIdx.x, a, b);
+  __trap();
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
-  do {
+  unsigned long long t0 = 0;
+  for (uint32_t spins = 0;; ++spins) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -73,7 +90,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
-  } while (!ok);
+    if (ok) return;
+    if ((spins & 1023u) == 1023u) {
+      const unsigned long long t = gtimer_now();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > kWatchdogNs) watchdog_fire("mbarrier", static_cast<int>(parity), static_cast<int>(spins));
+    }
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -654,7 +677,11 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
       for (int m = 0; m < nmat; ++m) v[m] = G.mbuf[m * per + i];
       for (int f = 0; f < C.nfollow; ++f) {
         const int c = C.follow[f];
-        while (ld_acquire(P.flags + c) == 0u) __nanosleep(20);
+        const unsigned long long t0 = gtimer_now();
+        while (ld_acquire(P.flags + c) == 0u) {
+          __nanosleep(20);
+          if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("stream-K flag", c, f);
+        }
         for (int m = 0; m < nmat; ++m) v[m] += __ldcg(P.fix + static_cast<size_t>(c) * fstride + m * per + i);
       }
       gemv_epilogue(P, C.tile0 + hi - 1, i / B, i % B, v, sqb, st);
@@ -1031,67 +1058,81 @@ __device__ __forceinline__ void load_lane(const void* src, int dtype, int64_t of
 template <int DPL>
 __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int lane, int warp, AttnSmem& S) {
   constexpr int hd = DPL * 32;
+  constexpr int CH = kAttnChunk;  // 16 keys
   const int H = P.n_heads;
   const int d = H * hd;
   const int pos = P.pos[b];
   const int slot = P.slots[b];
-  const int j0 = chunk * kAttnChunk;
-  const int nk = min(kAttnChunk, pos + 1 - j0);
+  const int j0 = chunk * CH;
+  const int nk = min(CH, pos + 1 - j0);
   __half* kc = P.kv + slot * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
   __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
   const int adt = P.act_dtype;
   const int64_t qoff = static_cast<int64_t>(b) * d + h * hd + DPL * lane;
   const float2* cs = P.rope_cs + static_cast<int64_t>(pos) * (hd / 2);
+  using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
+  const bool owns_new = pos >= j0 && pos < j0 + CH;
+  const int last_row = static_cast<int>(P.max_seq) - 1;
+  // 1) all loads of the item in flight together: the chunk's K and V rows (clamped into the
+  //    cache; the new row is patched below), q, and for the chunk holding `pos` the new k / v
+  Raw kr[CH], vr[CH];
+#pragma unroll
+  for (int t = 0; t < CH; ++t) {
+    const int64_t row = static_cast<int64_t>(min(j0 + t, last_row)) * hd + DPL * lane;
+    kr[t] = *reinterpret_cast<const Raw*>(kc + row);
+    vr[t] = *reinterpret_cast<const Raw*>(vc + row);
+  }
   float q[DPL];
   load_lane<DPL>(P.q, adt, qoff, q);
+  float kn[DPL], vn[DPL];
+  if (owns_new) {
+    load_lane<DPL>(P.k, adt, qoff, kn);
+    load_lane<DPL>(P.v, adt, qoff, vn);
+  }
   rope_lane<DPL>(q, cs, lane);
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
 #pragma unroll
   for (int e = 0; e < DPL; ++e) q[e] *= scale;
-  if (pos >= j0 && pos < j0 + kAttnChunk) {
-    // this chunk holds the new position: RoPE'd key and the value go to the cache first (the
-    // same lane reads them back below: program order makes the row current)
-    float kn[DPL], vn[DPL];
-    load_lane<DPL>(P.k, adt, qoff, kn);
+  if (owns_new) {
+    // the new position: RoPE'd key and the value go to the cache (fp16) and into this chunk
     rope_lane<DPL>(kn, cs, lane);
-    load_lane<DPL>(P.v, adt, qoff, vn);
+    Raw kw, vw;
+    __half* kh = reinterpret_cast<__half*>(&kw);
+    __half* vh = reinterpret_cast<__half*>(&vw);
 #pragma unroll
     for (int e = 0; e < DPL; ++e) {
-      kc[static_cast<int64_t>(pos) * hd + DPL * lane + e] = __float2half_rn(kn[e]);
-      vc[static_cast<int64_t>(pos) * hd + DPL * lane + e] = __float2half_rn(vn[e]);
+      kh[e] = __float2half_rn(kn[e]);
+      vh[e] = __float2half_rn(vn[e]);
     }
-    __syncwarp();  // orders the row writes before the reads below
-  }
-  using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
-  const int last_row = static_cast<int>(P.max_seq) - 1;
-  // per-lane partial dots of the chunk's keys: loads are unconditional (rows clamped into the
-  // cache, scores past the valid keys masked later) and issued 16 keys at a time
-  float part[kAttnChunk];
+    *reinterpret_cast<Raw*>(kc + static_cast<int64_t>(pos) * hd + DPL * lane) = kw;
+    *reinterpret_cast<Raw*>(vc + static_cast<int64_t>(pos) * hd + DPL * lane) = vw;
 #pragma unroll
-  for (int j16 = 0; j16 < kAttnChunk; j16 += 16) {
-    Raw raw[16];
-#pragma unroll
-    for (int t = 0; t < 16; ++t)
-      raw[t] = *reinterpret_cast<const Raw*>(kc + static_cast<int64_t>(min(j0 + j16 + t, last_row)) * hd + DPL * lane);
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const __half2* hp = reinterpret_cast<const __half2*>(&raw[t]);
-      float acc = 0.f;
-#pragma unroll
-      for (int e = 0; e < DPL / 2; ++e) {
-        const float2 f = __half22float2(hp[e]);
-        acc = fmaf(q[2 * e], f.x, acc);
-        acc = fmaf(q[2 * e + 1], f.y, acc);
+    for (int t = 0; t < CH; ++t)
+      if (j0 + t == pos) {
+        kr[t] = kw;
+        vr[t] = vw;
       }
-      part[j16 + t] = acc;
-    }
   }
-  // transposing butterfly: after the step with mask m a lane keeps the upper half when (lane & m)
-  int base = 0;
+  // 2) per-lane partial dots, then a transposing butterfly over lane bits 4..1: lanes l and l^1
+  //    end with the full score of key base(l) = 8*b4 + 4*b3 + 2*b2 + b1
+  float part[CH];
 #pragma unroll
-  for (int step = 0; step < 5; ++step) {
+  for (int t = 0; t < CH; ++t) {
+    const __half2* hp = reinterpret_cast<const __half2*>(&kr[t]);
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL / 2; ++e) {
+      const float2 f = __half22float2(hp[e]);
+      acc = fmaf(q[2 * e], f.x, acc);
+      acc = fmaf(q[2 * e + 1], f.y, acc);
+    }
+    part[t] = acc;
+  }
+  int key = 0;
+#pragma unroll
+  for (int step = 0; step < 4; ++step) {
     const int m = 16 >> step;
-    const int half = kAttnChunk >> (step + 1);
+    const int half = CH >> (step + 1);
     const bool up = lane & m;
 #pragma unroll
     for (int i = 0; i < half; ++i) {
@@ -1099,41 +1140,31 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
       const float send = up ? part[i] : part[i + half];
       part[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
     }
-    if (up) base += half;
+    if (up) key += half;
   }
-  // lane holds the scores of keys base, base + 1
-  const float sc0 = base < nk ? part[0] : -INFINITY;
-  const float sc1 = base + 1 < nk ? part[1] : -INFINITY;
-  float mx = fmaxf(sc0, sc1);
+  const float pair = __shfl_xor_sync(0xffffffffu, part[0], 1);  // every lane takes part in the shuffle
+  const float sc = key < nk ? part[0] + pair : -INFINITY;
+  float mx = sc;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const float p0 = base < nk ? expf(sc0 - mx) : 0.f;
-  const float p1 = base + 1 < nk ? expf(sc1 - mx) : 0.f;
-  float l = p0 + p1;
+  for (int o = 16; o > 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float p = key < nk ? expf(sc - mx) : 0.f;
+  float l = (lane & 1) ? 0.f : p;  // each key lives on two lanes
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-  // P V: key j's weight lives on the lane whose base is j & ~1
+  // 3) P V: key t's weight lives on lane (t>>3&1)<<4 | (t>>2&1)<<3 | (t>>1&1)<<2 | (t&1)<<1
   float o[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) o[e] = 0.f;
 #pragma unroll
-  for (int j16 = 0; j16 < kAttnChunk; j16 += 16) {
-    Raw raw[16];
+  for (int t = 0; t < CH; ++t) {
+    const int owner = ((t >> 3) & 1) << 4 | ((t >> 2) & 1) << 3 | ((t >> 1) & 1) << 2 | (t & 1) << 1;
+    const float pj = __shfl_sync(0xffffffffu, p, owner);
+    const __half2* hp = reinterpret_cast<const __half2*>(&vr[t]);
 #pragma unroll
-    for (int t = 0; t < 16; ++t)
-      raw[t] = *reinterpret_cast<const Raw*>(vc + static_cast<int64_t>(min(j0 + j16 + t, last_row)) * hd + DPL * lane);
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int j = j16 + t;
-      const int owner = ((j >> 5) & 1) << 4 | ((j >> 4) & 1) << 3 | ((j >> 3) & 1) << 2 | ((j >> 2) & 1) << 1 | ((j >> 1) & 1);
-      const float pj = __shfl_sync(0xffffffffu, (j & 1) ? p1 : p0, owner);  // 0 past the valid keys
-      const __half2* hp = reinterpret_cast<const __half2*>(&raw[t]);
-#pragma unroll
-      for (int e = 0; e < DPL / 2; ++e) {
-        const float2 f = __half22float2(hp[e]);
-        o[2 * e] = fmaf(pj, f.x, o[2 * e]);
-        o[2 * e + 1] = fmaf(pj, f.y, o[2 * e + 1]);
-      }
+    for (int e = 0; e < DPL / 2; ++e) {
+      const float2 f = __half22float2(hp[e]);
+      o[2 * e] = fmaf(pj, f.x, o[2 * e]);
+      o[2 * e + 1] = fmaf(pj, f.y, o[2 * e + 1]);
     }
   }
   const int64_t bh = static_cast<int64_t>(b) * H + h;
@@ -1142,6 +1173,7 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
     for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, o[e] / l);
     return;
   }
+  // 4) chunk partial to the workspace; the last chunk of the head (ticket) merges all of them
   float* wsp = P.attn_ws + (bh * nch + chunk) * (hd + 2);
 #pragma unroll
   for (int e = 0; e < DPL; ++e) wsp[2 + DPL * lane + e] = o[e];
@@ -1156,17 +1188,33 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
   if (!S.last[warp]) return;
   __threadfence();
   const float* base_ws = P.attn_ws + bh * nch * (hd + 2);
+  // lane c holds chunk c's (max, sum) (nch <= 32 here; larger contexts loop)
   float M = -INFINITY;
-  for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(base_ws + c * (hd + 2)));
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(base_ws + c * (hd + 2)));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
   float L = 0.f, O[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) O[e] = 0.f;
-  for (int c = 0; c < nch; ++c) {
-    const float* w = base_ws + c * (hd + 2);
-    const float f = expf(__ldcg(w) - M);
-    L += __ldcg(w + 1) * f;
+  for (int c = 0; c < nch; c += 4) {
+    float mm[4], ll[4], oo[4][DPL];
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) O[e] += __ldcg(w + 2 + DPL * lane + e) * f;
+    for (int u = 0; u < 4; ++u) {
+      const int cc = min(c + u, nch - 1);
+      const float* w = base_ws + cc * (hd + 2);
+      mm[u] = __ldcg(w);
+      ll[u] = __ldcg(w + 1);
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) oo[u][e] = __ldcg(w + 2 + DPL * lane + e);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c + u >= nch) break;
+      const float f = expf(mm[u] - M);
+      L += ll[u] * f;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) O[e] += oo[u][e] * f;
+    }
   }
 #pragma unroll
   for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, O[e] / L);
@@ -1233,7 +1281,11 @@ __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
     __threadfence();
     atomicAdd(counter, 1u);
     const unsigned int target = (++epoch) * gridDim.x;
-    while (ld_acquire(counter) < target) __nanosleep(32);
+    const unsigned long long t0 = gtimer_now();
+    while (ld_acquire(counter) < target) {
+      __nanosleep(32);
+      if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_acquire(counter)));
+    }
     __threadfence();
   } else {
     ++epoch;
