@@ -92,6 +92,7 @@ fq_status fq_ctx_destroy(fq_ctx* ctx) {
     dfree(ctx->scratch);
     dfree(ctx->gemv_fix);
     dfree(ctx->gemv_flags);
+    dfree(ctx->launch_ctr);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });

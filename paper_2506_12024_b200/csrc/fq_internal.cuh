@@ -56,6 +56,7 @@ struct fq_ctx {
   // stream-K fix-up workspace of transient (stand-alone) GEMV programs
   float* gemv_fix = nullptr;
   unsigned int* gemv_flags = nullptr;
+  unsigned int* launch_ctr = nullptr;  // [epoch, done] of the program kernels on this context
 };
 
 // ------------------------------------------------------------------ tiled fast-path layout

@@ -107,6 +107,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void named_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+__device__ __forceinline__ float2 ld_volatile_f2(const float2* p) {
+  float2 v;
+  asm volatile("ld.volatile.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -510,6 +515,7 @@ struct PhaseCtl {
   int cap;             // tiles per reduction window
   int head_shared;     // first tile started on an earlier CTA: publish its part
   int nfollow;         // later CTAs holding parts of our last tile (we own it)
+  unsigned int tag;    // (launch epoch, phase) stamp of this phase's stream-K parts
   short follow[512];
 };
 
@@ -632,13 +638,16 @@ __device__ __forceinline__ void gemv_epilogue(const Phase& P, int64_t tile, int 
 // publication (a later part of a tile owned by an earlier CTA), the merge of the later parts
 // (our last tile continues on following CTAs) or the epilogue.
 __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem& G, int lo, int hi, float (&sqb)[kMaxB],
-                              StatPart& st) {
+                              StatPart& st, unsigned long long* gp = nullptr) {
   named_sync(1, kNCW * 32);
+  if (gp) gp[7] = gtimer();
   const int B = P.B, nmat = P.nmat;
   const int per = 16 * B;
   const int fstride = kMaxMat * 16 * B;
   const bool merge_last = C.nfollow > 0 && hi == C.ntiles;
-  bool published = false;
+  // stream-K parts travel as (value, tag) pairs in one 8-byte store: the tag (launch epoch and
+  // phase) tells the owner the value is current, no flag / fence / extra round trip
+  float2* fix = reinterpret_cast<float2*>(P.fix);
   // item stride a multiple of `per` (and so of B): a thread's items all belong to batch row
   // threadIdx.x % B (the fused softmax statistics rely on it)
   const int stride = (kNCW * 32 / per) * per;
@@ -655,41 +664,33 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
       v[m] = a;
     }
     if (l == 0 && C.head_shared) {
-      for (int m = 0; m < nmat; ++m) P.fix[static_cast<size_t>(blockIdx.x) * fstride + m * per + i] = v[m];
-      published = true;
+      for (int m = 0; m < nmat; ++m)
+        __stcg(fix + static_cast<size_t>(blockIdx.x) * fstride + m * per + i, make_float2(v[m], __uint_as_float(C.tag)));
     } else if (merge_last && l == hi - 1) {
-      for (int m = 0; m < nmat; ++m) G.mbuf[m * per + i] = v[m];
+      // owner of the last tile: add the followers' parts in CTA order (each thread polls its own
+      // (value, tag) words)
+      for (int f = 0; f < C.nfollow; ++f) {
+        const int c = C.follow[f];
+        for (int m = 0; m < nmat; ++m) {
+          const float2* src = fix + static_cast<size_t>(c) * fstride + m * per + i;
+          float2 w = ld_volatile_f2(src);
+          if (__float_as_uint(w.y) != C.tag) {
+            const unsigned long long t0 = gtimer_now();
+            do {
+              __nanosleep(20);
+              w = ld_volatile_f2(src);
+              if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("stream-K part", c, f);
+            } while (__float_as_uint(w.y) != C.tag);
+          }
+          v[m] += w.x;
+        }
+      }
+      gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
     } else {
       gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
     }
   }
-  named_sync(1, kNCW * 32);
-  if (lo == 0 && C.head_shared && threadIdx.x == 0) {
-    __threadfence();
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + blockIdx.x), "r"(1u) : "memory");
-  }
-  (void)published;
-  if (merge_last) {
-    // every output thread waits for the followers' flags itself (acquire) and adds their parts
-    const int i = threadIdx.x;
-    if (i < per) {
-      float v[kMaxMat] = {0.f, 0.f, 0.f};
-      for (int m = 0; m < nmat; ++m) v[m] = G.mbuf[m * per + i];
-      for (int f = 0; f < C.nfollow; ++f) {
-        const int c = C.follow[f];
-        const unsigned long long t0 = gtimer_now();
-        while (ld_acquire(P.flags + c) == 0u) {
-          __nanosleep(20);
-          if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("stream-K flag", c, f);
-        }
-        for (int m = 0; m < nmat; ++m) v[m] += __ldcg(P.fix + static_cast<size_t>(c) * fstride + m * per + i);
-      }
-      gemv_epilogue(P, C.tile0 + hi - 1, i / B, i % B, v, sqb, st);
-    }
-    named_sync(1, kNCW * 32);
-    if (threadIdx.x == 0)
-      for (int f = 0; f < C.nfollow; ++f) P.flags[C.follow[f]] = 0u;  // consumed: all-zero again at the end
-  }
+  named_sync(1, kNCW * 32);  // the window's slots are rewritten next
 }
 
 __device__ __forceinline__ int64_t cta_start_or_end(const Phase& P, const Segs& S, int c) {
@@ -768,14 +769,13 @@ __device__ void phase_setup(const Phase& P, PhaseCtl& C, int red_floats, int lan
       C.nfollow = E->nfollow;
       for (int f = 0; f < E->nfollow; ++f) C.follow[f] = E->follow[f];
       C.cap = E->nseg > 0 ? max(1, red_floats / (P.nmat * kNCW * 16 * P.B)) : 1;
-      if (gpa) gpa[7] = gtimer();
     }
     __syncwarp();
     return;
   }
   Segs S;
   phase_segs(P, S);
-  if (gpa && lane == 0) gpa[7] = gtimer();
+
   int64_t g0 = 0, g1 = 0, tile0 = 0;
   int ntiles = 0, head_shared = 0, nfollow = 0;
   if (S.n > 0) {
@@ -840,12 +840,13 @@ __device__ __forceinline__ void add_into(float (&y)[kMaxMat][4], int m, float (&
 }
 
 __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, PhaseCtl& C, int red_floats,
-                               int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab) {
+                               int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab, unsigned int tag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long* gpa = g_gemv_prof ? g_gemv_prof + (static_cast<size_t>(phase_idx) * gridDim.x + blockIdx.x) * 8 : nullptr;
   unsigned long long* gp = threadIdx.x == 0 ? gpa : nullptr;
   if (warp == 1) {
     phase_setup(P, C, red_floats, lane, gpa, ctab ? ctab + phase_idx : nullptr);  // warp 0: norm factors
+    if (lane == 0) C.tag = tag;
     if (gpa && lane == 0) gpa[0] = gtimer();
   }
   stage_acts(P, G, gp);  // ends with a consumer barrier: C is visible
@@ -945,7 +946,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
       ++loc;
     }
     if (gp) gp[4] = gtimer();
-    reduce_window(P, C, G, wlo, loc, sqb, st);
+    reduce_window(P, C, G, wlo, loc, sqb, st, gp);
     if (gp) gp[5] = gtimer();
     slot_ref = slot_i;
     phase_ref = phase_bit;
@@ -1275,6 +1276,7 @@ __device__ void run_stats(const Phase& P) {
 }
 
 // ---------------------------------------------------------------- grid barrier (consumers)
+// Grid barrier (consumer threads): arrival counter in global memory, reset before every launch.
 __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
   named_sync(1, kNCW * 32);
   if (threadIdx.x == 0) {
@@ -1283,7 +1285,6 @@ __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
     const unsigned int target = (++epoch) * gridDim.x;
     const unsigned long long t0 = gtimer_now();
     while (ld_acquire(counter) < target) {
-      __nanosleep(32);
       if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_acquire(counter)));
     }
     __threadfence();
@@ -1298,6 +1299,7 @@ __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
 struct SmemLayout {
   int nstages, xs_bytes, dx_bytes, red_bytes;
   int ctl_phases;  // phases with a precomputed partition table in shared memory (0 = none)
+  unsigned int* lctr;  // [launch epoch, CTAs done]: the epoch tags this launch's stream-K parts
   int prefetch;  // L2 prefetch distance of the weight stream, in stages
 };
 
@@ -1349,6 +1351,8 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     return;
   }
   pdl_wait();
+  __shared__ unsigned int s_lepoch;
+  if (threadIdx.x == 0) s_lepoch = *reinterpret_cast<volatile unsigned int*>(L.lctr);
   int slot_i = 0;
   uint32_t phase_bit = 0;
   unsigned int epoch = 0;
@@ -1367,7 +1371,7 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   named_sync(1, kNCW * 32);
   for (int i = 0; i < nphases; ++i) {
     const Phase& P = pbuf[i & 1];
-    if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab);
+    if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
     else if (P.type == PH_ATTN) run_attn(P, attn_smem);
     else run_stats(P);
@@ -1381,6 +1385,12 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     if (bar) grid_barrier(barrier, epoch);
     else named_sync(1, kNCW * 32);
     if (prof) prof[(static_cast<size_t>(i) * gridDim.x + blockIdx.x) * 2 + 1] = gtimer();
+  }
+  // the last CTA to finish advances the launch epoch (every CTA read it at its start)
+  if (threadIdx.x == 0 && atomicAdd(&L.lctr[1], 1u) == gridDim.x - 1) {
+    L.lctr[1] = 0u;
+    __threadfence();
+    atomicAdd(&L.lctr[0], 1u);
   }
 }
 
@@ -1464,15 +1474,17 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   unsigned int* flags;
   if (inl) {
     if (ctx->gemv_fix == nullptr) {
-      ctx->gemv_fix = static_cast<float*>(dmalloc(sizeof(float) * kInlinePhases * 1024 * kMaxMat * 16 * kMaxB));
+      ctx->gemv_fix = static_cast<float*>(dmalloc(sizeof(float2) * kInlinePhases * 1024 * kMaxMat * 16 * kMaxB));
       ctx->gemv_flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * kInlinePhases * 1024));
       FQ_CUDA(cudaMemset(ctx->gemv_flags, 0, sizeof(unsigned int) * kInlinePhases * 1024));
+      FQ_CUDA(cudaMemset(ctx->gemv_fix, 0, sizeof(float2) * kInlinePhases * 1024 * kMaxMat * 16 * kMaxB));
     }
     if (r.grid > 1024) fail(FQ_E_CONFIG, "gemv: grid too large");
     fix = ctx->gemv_fix;
     flags = ctx->gemv_flags;
   } else {
-    r.fix = static_cast<float*>(dmalloc(sizeof(float) * r.nphases * r.grid * fstride));
+    r.fix = static_cast<float*>(dmalloc(sizeof(float2) * r.nphases * r.grid * fstride));
+    FQ_CUDA(cudaMemset(r.fix, 0, sizeof(float2) * r.nphases * r.grid * fstride));
     r.flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * r.nphases * r.grid));
     FQ_CUDA(cudaMemset(r.flags, 0, sizeof(unsigned int) * r.nphases * r.grid));
     fix = r.fix;
@@ -1481,7 +1493,7 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   for (int i = 0; i < r.nphases; ++i) {
     Phase& P = pb.phases[i];
     if (P.type != PH_GEMV) continue;
-    P.fix = fix + static_cast<size_t>(i) * r.grid * (inl ? kMaxMat * 16 * kMaxB : fstride);
+    P.fix = fix + 2 * static_cast<size_t>(i) * r.grid * (inl ? kMaxMat * 16 * kMaxB : fstride);  // float2 parts
     P.flags = flags + static_cast<size_t>(i) * (inl ? 1024 : r.grid);
   }
   if (inl) {
@@ -1503,6 +1515,12 @@ void launch_program(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, b
   L.red_bytes = run.red_bytes;
   L.prefetch = run.prefetch;
   L.ctl_phases = run.ctl_phases;
+  if (ctx->launch_ctr == nullptr) {
+    ctx->launch_ctr = static_cast<unsigned int*>(dmalloc(2 * sizeof(unsigned int)));
+    const unsigned int init[2] = {1u, 0u};  // epoch 0 never tags anything (fresh memory is zero)
+    FQ_CUDA(cudaMemcpy(ctx->launch_ctr, init, sizeof(init), cudaMemcpyHostToDevice));
+  }
+  L.lctr = ctx->launch_ctr;
   max_dynamic_smem();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(run.grid);

@@ -76,7 +76,7 @@ if len(tr):
         print(f"   stage {i:3d} issue {(tr[i,0]-t0)/1e3:8.2f} ready {(tr[i,1]-t0)/1e3:8.2f} done {(tr[i,2]-t0)/1e3:8.2f}")
 # GEMV phase detail: per role, sums over phases of the per-phase max over CTAs of each interval
 det = m.last_gemv_detail
-labels = ["segs(w1)", "setup(w1)", "rstd(w0)", "bar1", "stage", "loop", "reduce", "tail"]
+labels = ["setup(w1)", "rstd(w0)", "bar1", "stage", "loop", "red.sync", "red.rest", "tail"]
 segs = {}
 for i in range(len(types)):
     if names[int(types[i])] != "gemv":
@@ -85,7 +85,14 @@ for i in range(len(types)):
     d = det[i].astype(np.float64)
     r = "head" if i == len(types) - 2 else ["qkv", "attn", "o", "gate_up", "down"][(i - 1) % 5]
     e = segs.setdefault(r, np.zeros(8))
-    e += [np.max(d[:, 7] - st), np.max(d[:, 0] - st), np.max(d[:, 1] - st), np.max(d[:, 2] - st), np.max(d[:, 3] - d[:, 2]),
-          np.max(d[:, 4] - d[:, 3]), np.max(d[:, 5] - d[:, 4]), np.max(d[:, 6] - d[:, 5])]
+    e += [np.max(d[:, 0] - st), np.max(d[:, 1] - st), np.max(d[:, 2] - st), np.max(d[:, 3] - d[:, 2]),
+          np.max(d[:, 4] - d[:, 3]), np.max(d[:, 7] - d[:, 4]), np.max(d[:, 5] - d[:, 7]), np.max(d[:, 6] - d[:, 5])]
 for r, v in segs.items():
     print(f"  detail {r:8s}: " + "  ".join(f"{l} {x/1e3:7.1f}" for l, x in zip(labels, v)) + " us")
+# raw stamps of phase 3 (O-proj of layer 0) for a few CTAs, relative to the previous release
+i = 3
+st = after[i - 1]
+for c in (0, 5, 77, 147):
+    d = det[i, c]
+    print(f"  phase {i} cta {c:3d}: " + " ".join(f"{l}={(d[k] - st[c]) / 1e3:6.2f}" for k, l in
+          [(0, "setup"), (1, "rstd"), (2, "bar1"), (3, "staged"), (4, "loop"), (7, "redsync"), (5, "red"), (6, "end")]))
