@@ -122,14 +122,12 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
     M.y = g.mat[m].y ? static_cast<char*>(g.mat[m].y) + b0 * g.y_stride * ysz : nullptr;
   }
   max_kpad = std::max<int64_t>(max_kpad, static_cast<int64_t>(P.nkb) * kBlockK);
+  max_xs = std::max<int64_t>(max_xs, static_cast<int64_t>(P.nkb) * kBlockK * 2 * bb);
   max_bb = std::max(max_bb, bb);
   phases.push_back(P);
 }
 
-void ProgramBuilder::add(const Phase& p) {
-  phases.push_back(p);
-  max_bb = std::max(max_bb, std::min(p.B, kMaxB));
-}
+void ProgramBuilder::add(const Phase& p) { phases.push_back(p); }
 
 bool gemv_fast_supported(const fq_layer* L, int rung) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) return false;

@@ -20,7 +20,7 @@ constexpr int kStageBlocks8 = 16;
 constexpr int kStageBlocks4 = 32;
 constexpr int kSmemBudget = 220 * 1024;
 
-enum PhaseType : int { PH_GEMV = 0, PH_EMBED = 1, PH_ATTN = 2, PH_STATS = 3 };
+enum PhaseType : int { PH_GEMV = 0, PH_EMBED = 1, PH_ATTN = 2, PH_STATS = 3, PH_APPEND = 4 };
 
 struct DevMat {
   const uint8_t* tiles[2];    // [0] = W8, [1] = W4 tiled copies (fq_rung_store::tiles)
@@ -76,6 +76,7 @@ struct alignas(16) Phase {
   __half* kv;
   int64_t slot_stride, layer_off, max_seq;
   int n_heads, head_dim;
+  int appended;           // ATTN: the rows' keys / values are already in the cache (prefill)
   const float2* rope_cs;  // [max_seq][head_dim / 2] (cos, sin) of pos * theta^(-2i/hd)
   float* attn_ws;
   unsigned int* tickets;
@@ -93,8 +94,9 @@ struct InlineProgram {
 struct ProgramBuilder {
   std::vector<Phase> phases;
   int grid = 148;
-  int max_bb = 1;
+  int max_bb = 1;          // largest GEMV batch chunk
   int64_t max_kpad = 128;  // largest K rounded up to a block
+  int64_t max_xs = 0;      // largest activation staging (K_pad * 2 * chunk) of a GEMV phase
   void add_gemv(const GemvLaunch& g, int64_t b0, int bb);
   void add(const Phase& p);
 };

@@ -25,7 +25,8 @@
 namespace fqc {
 namespace {
 
-constexpr int kPartStride = 1024;  // columns of the sum-of-squares partial buffer per batch row
+constexpr int kPartStride = 1024;
+constexpr int kPrefillRows = 8;  // prompt positions per prefill step (llama): the GEMV's MMA n  // columns of the sum-of-squares partial buffer per batch row
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
@@ -321,9 +322,10 @@ struct fq_model {
   fq_row_stats* stats_host = nullptr;  // pinned [max_batch]
   std::map<int, cudaGraphExec_t> graphs;
   std::map<int, int64_t> graph_kernels;  // kernels inside each captured step graph
-  std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, gemv_only) -> uploaded program
+  std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, StepMode) -> uploaded program
   unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
+  int rows = 1;  // activation rows: max(max_batch, prefill chunk) (llama); max_batch (reference)
 
   int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
   int head_index() const { return static_cast<int>(cfg.n_layers) * (llama ? 7 : 6); }
@@ -331,13 +333,13 @@ struct fq_model {
   StepMeta meta(int B) const {
     StepMeta m;
     m.tokens = reinterpret_cast<const int32_t*>(meta_dev);
-    m.pos = m.tokens + cfg.max_batch;
-    m.slots = m.pos + cfg.max_batch;
+    m.pos = m.tokens + rows;
+    m.slots = m.pos + rows;
     (void)B;
     return m;
   }
-  const uint8_t* table_dev() const { return meta_dev + 3 * sizeof(int32_t) * cfg.max_batch; }
-  uint8_t* table_host() const { return meta_host + 3 * sizeof(int32_t) * cfg.max_batch; }
+  const uint8_t* table_dev() const { return meta_dev + 3 * sizeof(int32_t) * rows; }
+  uint8_t* table_host() const { return meta_host + 3 * sizeof(int32_t) * rows; }
 };
 
 namespace fqc {
@@ -366,7 +368,14 @@ bool capturing(cudaStream_t st) {
 
 // Enqueues one decode step for B rows (metadata already staged in meta_dev).  gemv_only keeps
 // just the GEMV launches (kernel-level profiling; activations are whatever the buffers hold).
-void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
+enum StepMode : int { STEP_DECODE = 0, STEP_GEMV_ONLY = 1, STEP_PREFILL = 2 };
+
+// Prefill steps (STEP_PREFILL) take B consecutive positions of one sequence as their rows: an
+// append phase writes every row's RoPE'd key / value to the cache before the attention phase, so
+// row b attends to the rows before it in the same step.
+void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
+  const bool gemv_only = mode == STEP_GEMV_ONLY;
+  const bool prefill = mode == STEP_PREFILL;
   fq_ctx* ctx = M->ctx;
   const fq_model_config& c = M->cfg;
   cudaStream_t st = ctx->stream;
@@ -378,7 +387,7 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
     // QKV GEMV (fused RMSNorm) | attention | WO (+residual) | gate/up (+SwiGLU) | down
     // (+residual), then the head and the row statistics, with a grid barrier between
     // dependent phases while the weight stream runs ahead.
-    auto key = std::make_pair(B, gemv_only ? 1 : 0);
+    auto key = std::make_pair(B, mode);
     auto it = M->programs.find(key);
     if (it == M->programs.end()) {
       if (capturing(st)) fail(FQ_E_STATE, "step program must be built before graph capture");
@@ -424,9 +433,29 @@ void enqueue_step(fq_model* M, int B, bool gemv_only = false) {
         g.y_dtype = c.act_dtype;
         g.y_stride = d;
         add_chunked(pb, g, B);
+        if (prefill) {
+          Phase ap{};
+          ap.type = PH_APPEND;
+          ap.barrier_after = 1;
+          ap.B = B;
+          ap.k = M->k;
+          ap.v = M->v;
+          ap.act_dtype = c.act_dtype;
+          ap.pos = meta.pos;
+          ap.slots = meta.slots;
+          ap.kv = static_cast<__half*>(M->kv);
+          ap.slot_stride = M->slot_stride;
+          ap.layer_off = l * M->layer_stride;
+          ap.max_seq = c.max_seq_len;
+          ap.n_heads = static_cast<int>(c.n_heads);
+          ap.head_dim = static_cast<int>(c.head_dim);
+          ap.rope_cs = M->rope_cs;
+          pb.add(ap);
+        }
         if (!gemv_only) {
           Phase a{};
           a.type = PH_ATTN;
+          a.appended = prefill ? 1 : 0;
           a.barrier_after = 1;
           a.B = B;
           a.q = M->q;
@@ -651,8 +680,8 @@ int64_t ffn_or_d(const fq_model_config& c) { return std::max(c.d_model, c.ffn_di
 void stage_rows(fq_model* M, int B, const int32_t* slots, const int32_t* tokens) {
   const fq_model_config& c = M->cfg;
   int32_t* tok = reinterpret_cast<int32_t*>(M->meta_host);
-  int32_t* pos = tok + c.max_batch;
-  int32_t* sl = pos + c.max_batch;
+  int32_t* pos = tok + M->rows;
+  int32_t* sl = pos + M->rows;
   uint8_t* tab = M->table_host();
   for (int b = 0; b < B; ++b) {
     const int s = slots[b];
@@ -686,6 +715,35 @@ void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens,
   if (logits_dev)
     FQ_CUDA(cudaMemcpyAsync(logits_dev, M->logits, sizeof(float) * B * M->cfg.vocab_size, cudaMemcpyDeviceToDevice,
                             M->ctx->stream));
+}
+
+// One llama prefill step: R consecutive prompt positions of `slot` as the rows of a prefill
+// program (append phase, then causal attention over the cache).
+void prefill_step(fq_model* M, int slot, const int32_t* tokens, int R, float* logits_dev, fq_row_stats* stats_host) {
+  const fq_model_config& c = M->cfg;
+  int32_t* tok = reinterpret_cast<int32_t*>(M->meta_host);
+  int32_t* pos = tok + M->rows;
+  int32_t* sl = pos + M->rows;
+  uint8_t* tab = M->table_host();
+  if (M->slot_len[slot] + R > c.max_seq_len) fail(FQ_E_CAPACITY, "prefill: cache is full");
+  for (int b = 0; b < R; ++b) {
+    tok[b] = tokens[b];
+    pos[b] = static_cast<int32_t>(M->slot_len[slot] + b);
+    sl[b] = slot;
+    std::memcpy(tab + b * M->n_lin, &M->rungs[static_cast<size_t>(slot) * M->n_lin], M->n_lin);
+  }
+  for (int i = 0; i < M->n_lin; ++i)
+    if (!M->lin[i]->has(tab[i])) fail(FQ_E_STATE, "layer " + M->ids[i] + ": active precision has no payload");
+  fq_ctx* ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+  enqueue_step(M, R, STEP_PREFILL);
+  FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * R, cudaMemcpyDeviceToHost, st));
+  FQ_CUDA(cudaStreamSynchronize(st));
+  M->slot_len[slot] += R;
+  if (stats_host) std::memcpy(stats_host, M->stats_host, sizeof(fq_row_stats) * R);
+  if (logits_dev)
+    FQ_CUDA(cudaMemcpyAsync(logits_dev, M->logits, sizeof(float) * R * c.vocab_size, cudaMemcpyDeviceToDevice, st));
 }
 
 float* param_slot(fq_model* M, const std::string& name, int64_t& expect) {
@@ -827,6 +885,9 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->kv = dmalloc(kv_elem * M->slot_stride * B);
     FQ_CUDA(cudaMemsetAsync(M->kv, 0, kv_elem * M->slot_stride * B, st));
     const size_t as = M->act_size();
+    M->rows = M->llama ? std::max(B, kPrefillRows) : B;
+    {
+      const int B = M->rows;  // activation buffers hold a prefill chunk too
     M->resid = zeros(B * d);
     M->hbuf = zeros(B * d);
     M->q = dmalloc(as * B * d);
@@ -843,6 +904,15 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->n_chunks = static_cast<int>((c.max_seq_len + kAttnChunk - 1) / kAttnChunk);
     M->attn_ws = zeros(static_cast<int64_t>(B) * c.n_heads * M->n_chunks * (c.head_dim + 2));
     M->tickets = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * B * c.n_heads));
+    FQ_CUDA(cudaMemsetAsync(M->tickets, 0, sizeof(unsigned int) * B * c.n_heads, st));
+    const int64_t dsz = std::max<int64_t>(static_cast<int64_t>(B) * c.n_heads * c.max_seq_len, B * V);
+    M->dscratch = static_cast<double*>(dmalloc(sizeof(double) * dsz));
+    M->meta_bytes = 3 * sizeof(int32_t) * B + static_cast<size_t>(B) * M->n_lin;
+    M->meta_dev = static_cast<uint8_t*>(dmalloc(M->meta_bytes));
+    FQ_CUDA(cudaMallocHost(&M->meta_host, M->meta_bytes));
+    std::memset(M->meta_host, 0, M->meta_bytes);
+    FQ_CUDA(cudaMallocHost(&M->stats_host, sizeof(fq_row_stats) * B));
+    }
     if (M->llama) {
       // RoPE table: angle pos * theta^(-2i/hd) in double, cos/sin rounded to fp32
       const int64_t half = c.head_dim / 2;
@@ -857,14 +927,6 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
       FQ_CUDA(cudaMemcpy(M->rope_cs, cs.data(), sizeof(float2) * cs.size(), cudaMemcpyHostToDevice));
     }
     M->grid_barrier = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * 4));
-    FQ_CUDA(cudaMemsetAsync(M->tickets, 0, sizeof(unsigned int) * B * c.n_heads, st));
-    const int64_t dsz = std::max<int64_t>(static_cast<int64_t>(B) * c.n_heads * c.max_seq_len, B * V);
-    M->dscratch = static_cast<double*>(dmalloc(sizeof(double) * dsz));
-    M->meta_bytes = 3 * sizeof(int32_t) * B + static_cast<size_t>(B) * M->n_lin;
-    M->meta_dev = static_cast<uint8_t*>(dmalloc(M->meta_bytes));
-    FQ_CUDA(cudaMallocHost(&M->meta_host, M->meta_bytes));
-    std::memset(M->meta_host, 0, M->meta_bytes);
-    FQ_CUDA(cudaMallocHost(&M->stats_host, sizeof(fq_row_stats) * B));
     FQ_CUDA(cudaStreamSynchronize(st));
     *out = M;
   });
@@ -1060,12 +1122,21 @@ fq_status fq_model_prefill(fq_model* M, int32_t slot, const int32_t* tokens, int
     if (n > M->cfg.max_seq_len) fail(FQ_E_CAPACITY, "prefill: prompt longer than max sequence length");
     for (int64_t i = 0; i < n; ++i)
       if (tokens[i] < 0 || tokens[i] >= M->cfg.vocab_size) fail(FQ_E_INPUT, "prefill: token id out of vocabulary");
-    // Row i of a prefill equals a decode step at position i (causal attention over 0..i with the
-    // same per-row arithmetic), so the prompt is streamed through the decode step.
-    for (int64_t i = 0; i < n; ++i) {
-      const int32_t s = slot, t = tokens[i];
-      model_step(M, 1, &s, &t, logits_dev ? logits_dev + i * M->cfg.vocab_size : nullptr,
-                 stats_host ? stats_host + i : nullptr);
+    if (!M->llama) {
+      // reference architecture: row i of a prefill equals a decode step at position i (causal
+      // attention over 0..i with the same per-row arithmetic)
+      for (int64_t i = 0; i < n; ++i) {
+        const int32_t s = slot, t = tokens[i];
+        model_step(M, 1, &s, &t, logits_dev ? logits_dev + i * M->cfg.vocab_size : nullptr,
+                   stats_host ? stats_host + i : nullptr);
+      }
+      return;
+    }
+    // llama: kPrefillRows consecutive positions per step (rows of one program launch)
+    for (int64_t p0 = 0; p0 < n; p0 += kPrefillRows) {
+      const int R = static_cast<int>(std::min<int64_t>(kPrefillRows, n - p0));
+      prefill_step(M, slot, tokens + p0, R, logits_dev ? logits_dev + p0 * M->cfg.vocab_size : nullptr,
+                   stats_host ? stats_host + p0 : nullptr);
     }
   });
 }
@@ -1181,13 +1252,13 @@ fq_status fq_model_profile_gemvs(fq_model* M, int32_t slot, int32_t reps, double
     cudaStream_t st = ctx->stream;
     FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
     if (M->programs.find(std::make_pair(1, 1)) == M->programs.end()) {
-      enqueue_step(M, 1, true);  // builds + uploads the GEMV-only program (un-captured run)
+      enqueue_step(M, 1, STEP_GEMV_ONLY);  // builds + uploads the GEMV-only program (un-captured run)
       FQ_CUDA(cudaStreamSynchronize(st));
     }
     const int64_t l0 = ctx->launches;
     cudaGraph_t graph;
     FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    enqueue_step(M, 1, true);
+    enqueue_step(M, 1, STEP_GEMV_ONLY);
     FQ_CUDA(cudaStreamEndCapture(st, &graph));
     const int64_t per_pass = ctx->launches - l0;
     cudaGraphExec_t exec;

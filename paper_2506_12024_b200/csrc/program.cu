@@ -1072,7 +1072,7 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
   const int64_t qoff = static_cast<int64_t>(b) * d + h * hd + DPL * lane;
   const float2* cs = P.rope_cs + static_cast<int64_t>(pos) * (hd / 2);
   using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
-  const bool owns_new = pos >= j0 && pos < j0 + CH;
+  const bool owns_new = !P.appended && pos >= j0 && pos < j0 + CH;  // prefill: appended beforehand
   const int last_row = static_cast<int>(P.max_seq) - 1;
   // 1) all loads of the item in flight together: the chunk's K and V rows (clamped into the
   //    cache; the new row is patched below), q, and for the chunk holding `pos` the new k / v
@@ -1220,6 +1220,37 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
 #pragma unroll
   for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, O[e] / L);
   if (lane == 0) P.tickets[bh] = 0u;
+}
+
+// Prefill append: row b's RoPE'd key and value (fp16) go to its cache position before the
+// attention phase (one (row, head) item per warp, lane-owned dims as in attn_item).
+template <int DPL>
+__device__ void append_item(const Phase& P, int b, int h, int lane) {
+  constexpr int hd = DPL * 32;
+  const int H = P.n_heads;
+  const int pos = P.pos[b];
+  __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+  __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
+  const int64_t off = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
+  float kn[DPL], vn[DPL];
+  load_lane<DPL>(P.k, P.act_dtype, off, kn);
+  load_lane<DPL>(P.v, P.act_dtype, off, vn);
+  rope_lane<DPL>(kn, P.rope_cs + static_cast<int64_t>(pos) * (hd / 2), lane);
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) {
+    kc[static_cast<int64_t>(pos) * hd + DPL * lane + e] = __float2half_rn(kn[e]);
+    vc[static_cast<int64_t>(pos) * hd + DPL * lane + e] = __float2half_rn(vn[e]);
+  }
+}
+
+__device__ void run_append(const Phase& P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int total = P.B * P.n_heads;
+  for (int item = warp * gridDim.x + blockIdx.x; item < total; item += gridDim.x * kNCW) {
+    const int b = item / P.n_heads, h = item - b * P.n_heads;
+    if (P.head_dim == 128) append_item<4>(P, b, h, lane);
+    else append_item<2>(P, b, h, lane);
+  }
 }
 
 __device__ void run_attn(const Phase& P, AttnSmem& S) {
@@ -1374,6 +1405,7 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
     else if (P.type == PH_ATTN) run_attn(P, attn_smem);
+    else if (P.type == PH_APPEND) run_append(P);
     else run_stats(P);
     if (prof) prof[(static_cast<size_t>(i) * gridDim.x + blockIdx.x) * 2] = gtimer();
     const bool bar = P.barrier_after && i + 1 < nphases;
@@ -1424,10 +1456,10 @@ int max_dynamic_smem() {
 
 constexpr int kMaxCtlPhases = 512;  // longer programs compute their partitions per phase
 
-SmemLayout layout_for(int64_t kpad, int bb, int nphases, int& nstages_out, size_t& total_out) {
+SmemLayout layout_for(int64_t kpad, int bb, int nphases, int& nstages_out, size_t& total_out, int64_t xs_bytes = -1) {
   SmemLayout L{};
-  L.xs_bytes = static_cast<int>(kpad * 2 * bb);
-  L.dx_bytes = static_cast<int>(kpad / kBlockK * bb * 16);
+  L.xs_bytes = static_cast<int>(xs_bytes >= 0 ? xs_bytes : kpad * 2 * bb);
+  L.dx_bytes = static_cast<int>(L.xs_bytes / 256 * 16);  // one float4 per (block, row)
   L.red_bytes = std::max(16 * 1024, 2 * kMaxMat * kNCW * 16 * bb * 4);
   L.ctl_phases = nphases <= kMaxCtlPhases ? nphases : 0;
   const int fixed = 2 * kMaxStages * 8 + L.xs_bytes + L.dx_bytes + L.red_bytes + kNCW * 32 * 4 + kMaxB * 4 +
@@ -1459,7 +1491,7 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   r.bb = pb.max_bb;
   int ns = 0;
   size_t tot = 0;
-  const SmemLayout L = layout_for(pb.max_kpad, pb.max_bb, r.nphases, ns, tot);
+  const SmemLayout L = layout_for(pb.max_kpad, pb.max_bb, r.nphases, ns, tot, std::max<int64_t>(pb.max_xs, 256));
   if (ns < 2) fail(FQ_E_CONFIG, "gemv: activations of this width do not fit in shared memory");
   r.nstages = ns;
   r.smem = tot;

@@ -243,3 +243,33 @@ def test_llama_logit_kl_calibration_small(ctx):
             b = orc.step(int(t), c4, r4)
             tot += oracle.kl_logits(b, a)[0]
     assert abs(kl[0] - tot / 16) <= 1e-3 * max(1.0, tot / 16) + 1e-4
+
+
+@pytest.mark.parametrize("n", [1, 8, 13, 21])
+def test_llama_chunked_prefill_matches_oracle_and_decode(ctx, n):
+    """Prefill runs 8 prompt positions per step (append phase + causal attention over the cache):
+    every row's logits follow the numpy restatement, and the cache it leaves behind continues
+    exactly like a position-by-position run."""
+    m, orc = _llama(ctx, max_batch=2)
+    toks = oracle.random_tokens(n + 3, 8192, 100 + n)
+    out = torch.zeros((n, 8192), dtype=torch.float32, device="cuda")
+    st = m.prefill(0, toks[:n], out)
+    ctx.synchronize()
+    got = out.cpu().numpy()
+    cache = orc.new_cache()
+    for i in range(n):
+        want = orc.step(int(toks[i]), cache, [8] * len(orc.ids))
+        rel = np.max(np.abs(got[i] - want)) / np.max(np.abs(want))
+        assert rel < 1e-2, (i, rel)
+        o = oracle.row_stats(got[i])
+        assert abs(st["entropy"][i] - o["entropy"]) <= 1e-6
+        assert int(st["argmax"][i]) == o["argmax"]
+    # slot 1: the same prompt one position at a time; the continuation must agree with slot 0
+    single = [m.decode([1], [int(t)])[0] for t in toks[:n]]
+    for i in range(n):
+        assert abs(single[i]["entropy"] - st["entropy"][i]) <= 1e-4
+    for t in toks[n:]:
+        a = m.decode([0], [int(t)])[0]
+        b = m.decode([1], [int(t)])[0]
+        assert abs(a["entropy"] - b["entropy"]) <= 1e-4
+        assert a["argmax"] == b["argmax"]
