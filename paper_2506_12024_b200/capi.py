@@ -94,10 +94,12 @@ _lib = None
 
 
 def load(path: str = LIB_PATH):
-    """Loads libfq_cuda.so; raises if it is missing (no fallback path exists)."""
+    """Loads libfq_cuda.so; raises if it is missing (no fallback path exists).  FQ_CUDA_LIB
+    selects another build of the same library (A/B profiling)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("FQ_CUDA_LIB", path)
     if not os.path.exists(path):
         raise ImportError(f"CUDA extension {path} is not built; run `make` or __graft_entry__.build()")
     L = C.CDLL(path)

@@ -902,7 +902,7 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->stat_part = dmalloc(static_cast<size_t>(B) * 1024 * 32);  // [B][grid <= 1024] StatPart
     M->stats_dev = static_cast<fq_row_stats*>(dmalloc(sizeof(fq_row_stats) * B));
     M->n_chunks = static_cast<int>((c.max_seq_len + kAttnChunk - 1) / kAttnChunk);
-    M->attn_ws = zeros(static_cast<int64_t>(B) * c.n_heads * M->n_chunks * (c.head_dim + 2));
+    M->attn_ws = zeros(static_cast<int64_t>(B) * c.n_heads * M->n_chunks * (c.head_dim + 4));
     M->tickets = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * B * c.n_heads));
     FQ_CUDA(cudaMemsetAsync(M->tickets, 0, sizeof(unsigned int) * B * c.n_heads, st));
     const int64_t dsz = std::max<int64_t>(static_cast<int64_t>(B) * c.n_heads * c.max_seq_len, B * V);

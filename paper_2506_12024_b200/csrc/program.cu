@@ -1174,13 +1174,16 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
     for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, o[e] / l);
     return;
   }
-  // 4) chunk partial to the workspace; the last chunk of the head (ticket) merges all of them
-  float* wsp = P.attn_ws + (bh * nch + chunk) * (hd + 2);
-#pragma unroll
-  for (int e = 0; e < DPL; ++e) wsp[2 + DPL * lane + e] = o[e];
+  // 4) chunk partial to the workspace ([chunk][hd + 4]: o, then max and sum; 16-byte aligned
+  //    lane slices); the last chunk of the head (ticket) merges all of them
+  using OV = typename std::conditional<DPL == 4, float4, float2>::type;
+  constexpr int CS = hd + 4;
+  float* wsp = P.attn_ws + (bh * nch + chunk) * CS;
+  if constexpr (DPL == 4) *reinterpret_cast<float4*>(wsp + 4 * lane) = make_float4(o[0], o[1], o[2], o[3]);
+  else *reinterpret_cast<float2*>(wsp + 2 * lane) = make_float2(o[0], o[1]);
   if (lane == 0) {
-    wsp[0] = mx;
-    wsp[1] = l;
+    wsp[hd] = mx;
+    wsp[hd + 1] = l;
   }
   __threadfence();
   __syncwarp();
@@ -1188,33 +1191,32 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
   __syncwarp();
   if (!S.last[warp]) return;
   __threadfence();
-  const float* base_ws = P.attn_ws + bh * nch * (hd + 2);
-  // lane c holds chunk c's (max, sum) (nch <= 32 here; larger contexts loop)
+  const float* base_ws = P.attn_ws + bh * nch * CS;
   float M = -INFINITY;
-  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(base_ws + c * (hd + 2)));
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(base_ws + c * CS + hd));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
   float L = 0.f, O[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) O[e] = 0.f;
-  for (int c = 0; c < nch; c += 4) {
-    float mm[4], ll[4], oo[4][DPL];
+  // up to 16 chunks per round: all their loads in flight together
+  for (int c0 = 0; c0 < nch; c0 += 16) {
+    OV oo[16];
+    float2 ml[16];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int cc = min(c + u, nch - 1);
-      const float* w = base_ws + cc * (hd + 2);
-      mm[u] = __ldcg(w);
-      ll[u] = __ldcg(w + 1);
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) oo[u][e] = __ldcg(w + 2 + DPL * lane + e);
+    for (int u = 0; u < 16; ++u) {
+      const float* w = base_ws + min(c0 + u, nch - 1) * CS;
+      oo[u] = __ldcg(reinterpret_cast<const OV*>(w + DPL * lane));
+      ml[u] = __ldcg(reinterpret_cast<const float2*>(w + hd));
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (c + u >= nch) break;
-      const float f = expf(mm[u] - M);
-      L += ll[u] * f;
+    for (int u = 0; u < 16; ++u) {
+      if (c0 + u >= nch) break;
+      const float f = expf(ml[u].x - M);
+      L += ml[u].y * f;
+      const float* ov = reinterpret_cast<const float*>(&oo[u]);
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) O[e] += oo[u][e] * f;
+      for (int e = 0; e < DPL; ++e) O[e] += ov[e] * f;
     }
   }
 #pragma unroll

@@ -13,7 +13,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--prompt", type=int, default=256)
 ap.add_argument("--w4", action="store_true")
 ap.add_argument("--layers", type=int, default=32)
-ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--reps", type=int, default=9)
 a = ap.parse_args()
 ctx = capi.Context(0)
 m = capi.Model(ctx, arch=capi.ARCH_LLAMA, act_dtype=capi.DT_BF16, max_batch=1, group_size=128, max_seq_len=512,
@@ -23,7 +23,8 @@ if a.w4:
     m.set_all_rungs(0, capi.RUNG_INT4)
 toks = (np.arange(a.prompt, dtype=np.int32) * 37) % 32000
 m.prefill(0, toks)
-names = {0: "gemv", 1: "embed", 2: "attn", 3: "stats"}
+names = {0: "gemv", 1: "embed", 2: "attn", 3: "stats", 4: "append"}
+totals = []
 for rep in range(a.reps):
     types, end, after, start = m.profile_step(0, 5)
     t0 = start.min()
@@ -34,7 +35,9 @@ for rep in range(a.reps):
         work.append((types[i], w.max(), w.mean(), after[i].max() - end[i].max()))
         prev = after[i]
     total = after[-1].max() - t0
+    totals.append(total / 1e3)
     if rep == a.reps - 1:
+        print("step totals (us):", " ".join(f"{x:.0f}" for x in totals), " median", f"{np.median(totals):.0f}")
         agg = {}
         for ty, wmax, wmean, bar in work:
             k = names[int(ty)]
