@@ -63,20 +63,18 @@ for rep in range(a.reps):
         for i in range(min(12, len(types))):
             ty, wmax, wmean, bar = work[i]
             print(f"    phase {i:3d} {names[int(ty)]:5s} max {wmax/1e3:7.2f} mean {wmean/1e3:7.2f} bar {bar/1e3:6.2f} us")
-# ring trace of CTA 0 over the last profiled step: per weight stage (producer got slot, consumer saw
-# data, consumer released)
+# ring trace of CTA 0 over the last profiled step, per weight stage: producer got the slot (issue),
+# consumer warp 0 started waiting for it, data ready
 tr = m.last_ring_trace
 tr = tr[tr[:, 0] > 0]
 if len(tr):
     t0 = tr[0, 0]
-    d_ready = tr[:, 1] - tr[:, 0]   # slot handed to TMA -> data consumed-ready (latency + queueing)
-    d_proc = tr[:, 2] - tr[:, 1]    # consumer time on the stage
-    gap = np.diff(tr[:, 0])         # producer issue interval
-    print(f"ring trace CTA0: {len(tr)} stages over {(tr[-1,2]-t0)/1e3:.1f} us; "
-          f"issue->ready median {np.median(d_ready)/1e3:.2f} us p90 {np.percentile(d_ready,90)/1e3:.2f}; "
-          f"consume median {np.median(d_proc)/1e3:.2f} us; issue interval median {np.median(gap)/1e3:.2f} us")
-    for i in range(0, min(len(tr), 40)):
-        print(f"   stage {i:3d} issue {(tr[i,0]-t0)/1e3:8.2f} ready {(tr[i,1]-t0)/1e3:8.2f} done {(tr[i,2]-t0)/1e3:8.2f}")
+    lat = tr[:, 2] - tr[:, 0]
+    waited = np.maximum(tr[:, 2] - tr[:, 1], 0)
+    print(f"ring trace CTA0: {len(tr)} stages; issue->ready median {np.median(lat)/1e3:.2f} us; consumer wait total "
+          f"{waited.sum()/1e3:.1f} us (stages waited >0.2us: {(waited > 200).sum()})")
+    for i in range(0, min(len(tr), 48)):
+        print(f"   stage {i:3d} issue {(tr[i,0]-t0)/1e3:8.2f} want {(tr[i,1]-t0)/1e3:8.2f} ready {(tr[i,2]-t0)/1e3:8.2f}")
 # GEMV phase detail: per role, sums over phases of the per-phase max over CTAs of each interval
 det = m.last_gemv_detail
 labels = ["setup(w1)", "rstd(w0)", "bar1", "stage", "loop", "red.sync", "red.rest", "tail"]
@@ -99,3 +97,17 @@ for c in (0, 5, 77, 147):
     d = det[i, c]
     print(f"  phase {i} cta {c:3d}: " + " ".join(f"{l}={(d[k] - st[c]) / 1e3:6.2f}" for k, l in
           [(0, "setup"), (1, "rstd"), (2, "bar1"), (3, "staged"), (4, "loop"), (7, "redsync"), (5, "red"), (6, "end")]))
+# attention work distribution over CTAs (layer 0 and the median layer)
+att = [i for i in range(len(types)) if names[int(types[i])] == "attn"]
+for i in att[:1] + att[len(att) // 2: len(att) // 2 + 1]:
+    w = (end[i] - after[i - 1]) / 1e3
+    print(f"  attn phase {i}: work us p0 {np.min(w):.2f} p50 {np.median(w):.2f} p90 {np.percentile(w, 90):.2f} "
+          f"max {np.max(w):.2f} (argmax cta {int(np.argmax(w))})")
+for i in att[:4]:
+    w = (end[i] - after[i - 1]) / 1e3
+    top = np.argsort(-w)[:4]
+    print(f"  attn phase {i}: slowest ctas " + ", ".join(f"{int(c)}:{w[c]:.2f}" for c in top))
+for i in [1, 3, 4, 5]:
+    w = (end[i] - (after[i - 1] if i > 0 else start)) / 1e3
+    top = np.argsort(-w)[:4]
+    print(f"  {names[int(types[i])]} phase {i}: slowest ctas " + ", ".join(f"{int(c)}:{w[c]:.2f}" for c in top) + f"  median {np.median(w):.2f}")
