@@ -303,6 +303,13 @@ def main():
 
     # ---- kernel roofline of the dominant kernel (the GEMV), live CUDA events on the launch stream
     ms_gemv, gemv_per_step, gemv_bytes = model.profile_gemvs(0, 20)
+    traffic = None  # DRAM bytes per launch of the same program from the committed ncu capture
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        if tj.get("config") == args.config:
+            traffic = tj["dram_bytes_per_step"]
+    except Exception:
+        pass
     gemv_achieved = gemv_bytes / gemv_per_step / (ms_gemv / 1000.0) / 1e9
 
     # ---- e2e through the public API with host buffers: a fresh generate over the whole
@@ -382,8 +389,8 @@ def main():
             "step_algorithmic_bytes": int(step_bytes),
             "roofline": {
                 "bound": "hbm", "achieved": gemv_achieved, "peak": hbm, "unit": "GB/s",
-                "frac": gemv_achieved / hbm, "traffic": None,
-                "kernel": "gemv_tma_kernel (W8/W4 g128 dequant-GEMV)",
+                "frac": gemv_achieved / hbm, "traffic": traffic,
+                "kernel": "program_kernel GEMV phases (tiled W8/W4 g128 dequant, mma.sync m16n8k16)",
                 "peak_kind": peak_kind,
                 "per_launch_bytes": gemv_bytes / gemv_per_step, "per_launch_ms": ms_gemv,
             },
