@@ -1030,7 +1030,8 @@ __device__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
 // workspace; the last chunk of a head (ticket) merges them.  RoPE pairs (i, i + hd/2) live on
 // lanes l and l^16; cos/sin come from the model's table (double-computed angles).
 struct AttnSmem {
-  int last[kNCW];
+  float o[kNCW][128];
+  float m[kNCW], l[kNCW];
 };
 
 template <int DPL>
@@ -1056,26 +1057,24 @@ __device__ __forceinline__ void load_lane(const void* src, int dtype, int64_t of
     x[e] = dtype == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[e]) << 16) : __half2float(__ushort_as_half(u[e]));
 }
 
+// One 16-key chunk of head (b, h) on one warp: returns the chunk's max score, exp-sum and the
+// unnormalised P.V slice of this lane (dims DPL*lane ...).  The chunk holding the row's own
+// position writes the RoPE'd key / value to the cache first (decode; prefill appended them in a
+// phase of its own).
 template <int DPL>
-__device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int lane, int warp, AttnSmem& S) {
+__device__ __forceinline__ void attn_chunk(const Phase& P, int b, int h, int chunk, const float (&q)[DPL], int lane,
+                                           float& mx, float& l, float (&o)[DPL]) {
   constexpr int hd = DPL * 32;
   constexpr int CH = kAttnChunk;  // 16 keys
   const int H = P.n_heads;
-  const int d = H * hd;
   const int pos = P.pos[b];
-  const int slot = P.slots[b];
   const int j0 = chunk * CH;
   const int nk = min(CH, pos + 1 - j0);
-  __half* kc = P.kv + slot * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+  __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
   __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
-  const int adt = P.act_dtype;
-  const int64_t qoff = static_cast<int64_t>(b) * d + h * hd + DPL * lane;
-  const float2* cs = P.rope_cs + static_cast<int64_t>(pos) * (hd / 2);
   using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
-  const bool owns_new = !P.appended && pos >= j0 && pos < j0 + CH;  // prefill: appended beforehand
+  const bool owns_new = !P.appended && pos >= j0 && pos < j0 + CH;
   const int last_row = static_cast<int>(P.max_seq) - 1;
-  // 1) all loads of the item in flight together: the chunk's K and V rows (clamped into the
-  //    cache; the new row is patched below), q, and for the chunk holding `pos` the new k / v
   Raw kr[CH], vr[CH];
 #pragma unroll
   for (int t = 0; t < CH; ++t) {
@@ -1083,20 +1082,12 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
     kr[t] = *reinterpret_cast<const Raw*>(kc + row);
     vr[t] = *reinterpret_cast<const Raw*>(vc + row);
   }
-  float q[DPL];
-  load_lane<DPL>(P.q, adt, qoff, q);
-  float kn[DPL], vn[DPL];
   if (owns_new) {
-    load_lane<DPL>(P.k, adt, qoff, kn);
-    load_lane<DPL>(P.v, adt, qoff, vn);
-  }
-  rope_lane<DPL>(q, cs, lane);
-  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-#pragma unroll
-  for (int e = 0; e < DPL; ++e) q[e] *= scale;
-  if (owns_new) {
-    // the new position: RoPE'd key and the value go to the cache (fp16) and into this chunk
-    rope_lane<DPL>(kn, cs, lane);
+    const int64_t off = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
+    float kn[DPL], vn[DPL];
+    load_lane<DPL>(P.k, P.act_dtype, off, kn);
+    load_lane<DPL>(P.v, P.act_dtype, off, vn);
+    rope_lane<DPL>(kn, P.rope_cs + static_cast<int64_t>(pos) * (hd / 2), lane);
     Raw kw, vw;
     __half* kh = reinterpret_cast<__half*>(&kw);
     __half* vh = reinterpret_cast<__half*>(&vw);
@@ -1114,8 +1105,8 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
         vr[t] = vw;
       }
   }
-  // 2) per-lane partial dots, then a transposing butterfly over lane bits 4..1: lanes l and l^1
-  //    end with the full score of key base(l) = 8*b4 + 4*b3 + 2*b2 + b1
+  // per-lane partial dots, then a transposing butterfly over lane bits 4..1: lanes l and l^1 end
+  // with the full score of key base(l) = 8*b4 + 4*b3 + 2*b2 + b1
   float part[CH];
 #pragma unroll
   for (int t = 0; t < CH; ++t) {
@@ -1145,15 +1136,13 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
   }
   const float pair = __shfl_xor_sync(0xffffffffu, part[0], 1);  // every lane takes part in the shuffle
   const float sc = key < nk ? part[0] + pair : -INFINITY;
-  float mx = sc;
+  mx = sc;
 #pragma unroll
-  for (int o = 16; o > 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  for (int off = 16; off > 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   const float p = key < nk ? expf(sc - mx) : 0.f;
-  float l = (lane & 1) ? 0.f : p;  // each key lives on two lanes
+  l = (lane & 1) ? 0.f : p;  // each key lives on two lanes
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-  // 3) P V: key t's weight lives on lane (t>>3&1)<<4 | (t>>2&1)<<3 | (t>>1&1)<<2 | (t&1)<<1
-  float o[DPL];
+  for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
 #pragma unroll
   for (int e = 0; e < DPL; ++e) o[e] = 0.f;
 #pragma unroll
@@ -1168,60 +1157,62 @@ __device__ void attn_item(const Phase& P, int b, int h, int chunk, int nch, int 
       o[2 * e + 1] = fmaf(pj, f.y, o[2 * e + 1]);
     }
   }
-  const int64_t bh = static_cast<int64_t>(b) * H + h;
-  if (nch == 1) {
+}
+
+// Attention of one (row, head) on one CTA: warp w takes chunks w, w + 8, ... with an online
+// softmax across its chunks; the eight warp states merge in shared memory (fixed order, no
+// global workspace, no atomics).
+template <int DPL>
+__device__ void attn_head(const Phase& P, int b, int h, int lane, int warp, AttnSmem& S) {
+  constexpr int hd = DPL * 32;
+  const int H = P.n_heads;
+  const int pos = P.pos[b];
+  const int nch = (pos + kAttnChunk) / kAttnChunk;
+  const int64_t qoff = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
+  float q[DPL];
+  load_lane<DPL>(P.q, P.act_dtype, qoff, q);
+  rope_lane<DPL>(q, P.rope_cs + static_cast<int64_t>(pos) * (hd / 2), lane);
+  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, o[e] / l);
-    return;
-  }
-  // 4) chunk partial to the workspace ([chunk][hd + 4]: o, then max and sum; 16-byte aligned
-  //    lane slices); the last chunk of the head (ticket) merges all of them
-  using OV = typename std::conditional<DPL == 4, float4, float2>::type;
-  constexpr int CS = hd + 4;
-  float* wsp = P.attn_ws + (bh * nch + chunk) * CS;
-  if constexpr (DPL == 4) *reinterpret_cast<float4*>(wsp + 4 * lane) = make_float4(o[0], o[1], o[2], o[3]);
-  else *reinterpret_cast<float2*>(wsp + 2 * lane) = make_float2(o[0], o[1]);
-  if (lane == 0) {
-    wsp[hd] = mx;
-    wsp[hd + 1] = l;
-  }
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) S.last[warp] = atomicAdd(&P.tickets[bh], 1u) == static_cast<unsigned int>(nch - 1);
-  __syncwarp();
-  if (!S.last[warp]) return;
-  __threadfence();
-  const float* base_ws = P.attn_ws + bh * nch * CS;
-  float M = -INFINITY;
-  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(base_ws + c * CS + hd));
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  float L = 0.f, O[DPL];
+  for (int e = 0; e < DPL; ++e) q[e] *= scale;
+  float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) O[e] = 0.f;
-  // up to 16 chunks per round: all their loads in flight together
-  for (int c0 = 0; c0 < nch; c0 += 16) {
-    OV oo[16];
-    float2 ml[16];
+  for (int c = warp; c < nch; c += kNCW) {
+    float mx, l, o[DPL];
+    attn_chunk<DPL>(P, b, h, c, q, lane, mx, l, o);
+    const float Mn = fmaxf(M, mx);
+    const float fa = M == -INFINITY ? 0.f : expf(M - Mn), fb = expf(mx - Mn);
+    L = L * fa + l * fb;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const float* w = base_ws + min(c0 + u, nch - 1) * CS;
-      oo[u] = __ldcg(reinterpret_cast<const OV*>(w + DPL * lane));
-      ml[u] = __ldcg(reinterpret_cast<const float2*>(w + hd));
-    }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      if (c0 + u >= nch) break;
-      const float f = expf(ml[u].x - M);
-      L += ml[u].y * f;
-      const float* ov = reinterpret_cast<const float*>(&oo[u]);
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) O[e] += ov[e] * f;
-    }
+    for (int e = 0; e < DPL; ++e) O[e] = O[e] * fa + o[e] * fb;
+    M = Mn;
   }
 #pragma unroll
-  for (int e = 0; e < DPL; ++e) store_out(P.attn_out, adt, qoff + e, O[e] / L);
-  if (lane == 0) P.tickets[bh] = 0u;
+  for (int e = 0; e < DPL; ++e) S.o[warp][DPL * lane + e] = O[e];
+  if (lane == 0) {
+    S.m[warp] = M;
+    S.l[warp] = L;
+  }
+  named_sync(1, kNCW * 32);
+  if (warp == 0) {
+    float Mt = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kNCW; ++w) Mt = fmaxf(Mt, S.m[w]);
+    float Lt = 0.f, Ot[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) Ot[e] = 0.f;
+#pragma unroll
+    for (int w = 0; w < kNCW; ++w) {
+      const float f = S.m[w] == -INFINITY ? 0.f : expf(S.m[w] - Mt);
+      Lt += S.l[w] * f;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) Ot[e] += S.o[w][DPL * lane + e] * f;
+    }
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) store_out(P.attn_out, P.act_dtype, qoff + e, Ot[e] / Lt);
+  }
+  named_sync(1, kNCW * 32);
 }
 
 // Prefill append: row b's RoPE'd key and value (fp16) go to its cache position before the
@@ -1257,21 +1248,11 @@ __device__ void run_append(const Phase& P) {
 
 __device__ void run_attn(const Phase& P, AttnSmem& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // items: for every row b and head h, the active key chunks of that row; item i runs on CTA
-  // i % grid, warp (i / grid) % kNCW (spread over the whole GPU)
-  int total = 0;
-  for (int b = 0; b < P.B; ++b) total += P.n_heads * ((P.pos[b] + kAttnChunk) / kAttnChunk);
-  for (int item = warp * gridDim.x + blockIdx.x; item < total; item += gridDim.x * kNCW) {
-    int rem = item, b = 0;
-    for (;; ++b) {
-      const int per = P.n_heads * ((P.pos[b] + kAttnChunk) / kAttnChunk);
-      if (rem < per) break;
-      rem -= per;
-    }
-    const int nch = (P.pos[b] + kAttnChunk) / kAttnChunk;
-    const int h = rem / nch, c = rem % nch;
-    if (P.head_dim == 128) attn_item<4>(P, b, h, c, nch, lane, warp, S);
-    else attn_item<2>(P, b, h, c, nch, lane, warp, S);
+  // one (row, head) per CTA at a time, spread over the grid
+  for (int item = blockIdx.x; item < P.B * P.n_heads; item += gridDim.x) {
+    const int b = item / P.n_heads, h = item - b * P.n_heads;
+    if (P.head_dim == 128) attn_head<4>(P, b, h, lane, warp, S);
+    else attn_head<2>(P, b, h, lane, warp, S);
   }
 }
 
