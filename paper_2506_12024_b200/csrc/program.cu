@@ -707,7 +707,7 @@ struct alignas(16) CtlEntry {
   short follow[4];
 };
 
-__device__ void compute_ctl(const Phase& P, CtlEntry& E) {
+__device__ __noinline__ void compute_ctl(const Phase& P, CtlEntry& E) {
   E.valid = 0;
   if (P.type != PH_GEMV) return;
   Segs S;
@@ -996,7 +996,7 @@ __device__ __forceinline__ void cta_rows(int64_t N, int64_t& r0, int& rows) {
   rows = static_cast<int>((N * (blockIdx.x + 1)) / gridDim.x - r0);
 }
 
-__device__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
+__device__ __noinline__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int64_t c0;
   int cnt;
@@ -1236,7 +1236,7 @@ __device__ void append_item(const Phase& P, int b, int h, int lane) {
   }
 }
 
-__device__ void run_append(const Phase& P) {
+__device__ __noinline__ void run_append(const Phase& P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = P.B * P.n_heads;
   for (int item = warp * gridDim.x + blockIdx.x; item < total; item += gridDim.x * kNCW) {
@@ -1246,7 +1246,7 @@ __device__ void run_append(const Phase& P) {
   }
 }
 
-__device__ void run_attn(const Phase& P, AttnSmem& S) {
+__device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // one (row, head) per CTA at a time, spread over the grid
   for (int item = blockIdx.x; item < P.B * P.n_heads; item += gridDim.x) {
@@ -1260,7 +1260,7 @@ __device__ void run_attn(const Phase& P, AttnSmem& S) {
 // Combines the head GEMV's per-CTA softmax partials of row b (warp b of CTA 0, fixed-order merge)
 // into fq_row_stats: ppl_entropy / fault_tolerance / argmax_token (src/scheduler.cpp:13-49,
 // src/engine.cpp:144-155) in double.
-__device__ void run_stats(const Phase& P) {
+__device__ __noinline__ void run_stats(const Phase& P) {
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const StatPart* parts = static_cast<const StatPart*>(P.stat_part);
