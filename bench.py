@@ -248,7 +248,10 @@ def main():
     plan = build_plan(model.ids, kl4)
     model.set_all_rungs(0, capi.RUNG_INT8)
 
-    rng = np.random.default_rng(1000 + rank)
+    from paper_2506_12024_b200 import parallel  # noqa: E402
+    # weak scaling: every rank decodes its own sequence(s) (global index = rank), seeded by the
+    # global sequence index so the workload per sequence does not depend on the GPU count
+    rng = np.random.default_rng(parallel.prompt_seed(1000, parallel.shard(world, rank, world)[0]))
     prompt = rng.integers(0, cfg["vocab_size"], cfg["prompt"]).astype(np.int32)
 
     # ---- prefill (untimed) and threshold: derive_threshold (src/scheduler.cpp:51-60)
@@ -290,13 +293,11 @@ def main():
         torch.cuda.synchronize()
     launches_timed = ctx.launches() - launches_before
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.barrier()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = parallel.max_over_ranks(ms, device="cuda")
     sec = ms_max / 1000.0
-    value = world * args.steps / sec
+    value = parallel.aggregate_throughput(args.steps, world, sec)
     hbm, peak_kind = peaks()
     step_bytes = statistics.mean(bytes_w_steps)
     step_frac = (step_bytes / (ms_max / args.steps / 1000.0)) / 1e9 / hbm
@@ -338,10 +339,8 @@ def main():
             row = model.decode([0], [generated[-1]])[0]
     f1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * e2e_tokens / (float(e2e_ms.item()) / 1000.0)
+    e2e_ms = parallel.max_over_ranks(f0.elapsed_time(f1), device="cuda")
+    e2e_value = parallel.aggregate_throughput(e2e_tokens, world, e2e_ms / 1000.0)
     row_bytes = capi.ROW_STATS_DTYPE.itemsize
     h2d = (cfg["prompt"] * 4 + (e2e_tokens - 1) * 4) / e2e_tokens
     d2h = (cfg["prompt"] + e2e_tokens - 1) * row_bytes / e2e_tokens

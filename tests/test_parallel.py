@@ -1,0 +1,69 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the data-parallel plumbing: sequence sharding,
+max-over-ranks timing, aggregate throughput and the trace gather."""
+import os
+import socket
+
+import pytest
+
+from paper_2506_12024_b200 import parallel
+
+
+def test_shard_partitions_and_balances():
+    for n in (0, 1, 7, 8, 256):
+        for world in (1, 2, 3, 8):
+            shards = [parallel.shard(n, r, world) for r in range(world)]
+            flat = [i for s in shards for i in s]
+            assert flat == list(range(n))
+            sizes = [len(s) for s in shards]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        parallel.shard(4, 2, 2)
+
+
+def test_prompt_seed_independent_of_world():
+    assert parallel.prompt_seed(7, 3) == parallel.prompt_seed(7, 3)
+    assert parallel.prompt_seed(7, 3) != parallel.prompt_seed(7, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_seqs, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = parallel.shard(n_seqs, rank, world)
+        # a stand-in per-sequence result: (sequence, seed) from this rank's shard
+        results = [(i, parallel.prompt_seed(5, i)) for i in mine]
+        t = parallel.max_over_ranks(1.0 + rank)  # rank r "took" 1 + r seconds
+        gathered = parallel.gather_objects(results)
+        merged = parallel.merge_shards(gathered, n_seqs)
+        thr = parallel.aggregate_throughput(len(mine), world, t)
+        q.put((rank, t, merged, thr))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharding_timing_and_gather():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n = 9
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, t, merged, thr in outs:
+        assert t == 2.0  # max over ranks
+        assert merged == [(i, parallel.prompt_seed(5, i)) for i in range(n)]
+        assert thr == pytest.approx(2 * len(parallel.shard(n, rank, 2)) / 2.0)
