@@ -125,6 +125,14 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int64_t batc
                   const void* x_dev, int32_t x_dtype, void* y_dev, int32_t y_dtype,
                   int32_t numerics);
 
+/* Prefill / calibration contraction on the tcgen05 tensor cores (BASELINE config 4):
+ * y[rows, N] (fp32, row stride y_stride) = x[rows, K] (bf16, row stride x_stride) . dequant(W_rung)^T,
+ * the dequantisation of the resident tiled W8/W4 copy fused into the tile loads (fp16 operands,
+ * fp32 accumulation in tensor memory).  MultiPrecisionLayer::forward (src/model.cpp:77-98) on
+ * many rows at once. */
+fq_status fq_gemm(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int64_t rows, const void* x_dev,
+                  int64_t x_stride, float* y_dev, int64_t y_stride);
+
 /* ------------------------------------------------------- statistics (a10, a11, a18) */
 /* One fq_row_stats per logits row (fp32 [rows, vocab] on device); stats_dev on device. */
 fq_status fq_softmax_stats(fq_ctx* ctx, const float* logits_dev, int64_t rows, int64_t vocab,

@@ -32,7 +32,7 @@ ABI_FUNCTIONS = [
     "fq_model_linear_index", "fq_model_linear", "fq_model_set_param", "fq_model_init_random", "fq_model_set_rung",
     "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
     "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
-    "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step",
+    "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step", "fq_gemm",
 ]
 
 
@@ -150,6 +150,7 @@ def load(path: str = LIB_PATH):
         "fq_model_calibrate_logit_kl": [v, v, i64, i64, i32, i32, v, v],
         "fq_model_profile_gemvs": [v, i32, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64)],
         "fq_model_profile_step": [v, i32, i32, v, i64, C.POINTER(i32), C.POINTER(i32), v],
+        "fq_gemm": [v, v, i32, i64, v, i64, v, i64],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -222,6 +223,11 @@ class Context:
     def gemv(self, layer: "Layer", rung: int, batch: int, x, x_dtype: int, y, y_dtype: int,
              numerics: int = NUMERICS_FAST) -> None:
         check(self.L.fq_gemv(self.h, layer.h, rung, batch, _ptr(x), x_dtype, _ptr(y), y_dtype, numerics))
+
+    def gemm(self, layer: "Layer", rung: int, rows: int, x_bf16, y_f32, x_stride: int = 0, y_stride: int = 0) -> None:
+        """y[rows, N] = x[rows, K] . dequant(W_rung)^T on the tcgen05 tensor cores."""
+        check(self.L.fq_gemm(self.h, layer.h, rung, rows, _ptr(x_bf16), x_stride or layer.K, _ptr(y_f32),
+                             y_stride or layer.N))
 
     def softmax_stats(self, logits, rows: int, vocab: int, stats_dev) -> None:
         check(self.L.fq_softmax_stats(self.h, _ptr(logits), rows, vocab, _ptr(stats_dev)))

@@ -308,6 +308,16 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t batch, c
   });
 }
 
+fq_status fq_gemm(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t rows, const void* x_dev, int64_t x_stride,
+                  float* y_dev, int64_t y_stride) {
+  return guarded([&] {
+    require(ctx != nullptr && L != nullptr && x_dev != nullptr && y_dev != nullptr, FQ_E_INPUT, "null argument");
+    require(rows >= 1, FQ_E_DIMENSION, "gemm: rows must be >= 1");
+    require(x_stride >= L->K && y_stride >= L->N, FQ_E_DIMENSION, "gemm: row stride smaller than the row");
+    launch_gemm_dq(ctx, L, rung, rows, x_dev, x_stride, y_dev, y_stride);
+  });
+}
+
 fq_status fq_softmax_stats(fq_ctx* ctx, const float* logits_dev, int64_t rows, int64_t vocab, fq_row_stats* stats_dev) {
   return guarded([&] {
     require(ctx != nullptr && logits_dev != nullptr && stats_dev != nullptr, FQ_E_INPUT, "null argument");

@@ -170,6 +170,10 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
                        int x_dtype, void* y, int y_dtype);
 
+// tcgen05 dequant-GEMM: y[T, N] (fp32, row stride y_stride) = x[T, K] (bf16) . dequant(W_rung)^T
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x_bf16, int64_t x_stride, float* y,
+                    int64_t y_stride);
+
 // statistics
 void launch_softmax_stats(fq_ctx* ctx, const float* logits, int64_t rows, int64_t vocab,
                           int64_t row_stride, fq_row_stats* out);

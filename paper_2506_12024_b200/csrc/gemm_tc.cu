@@ -1,0 +1,286 @@
+// Prefill / calibration contraction on the 5th-generation tensor cores (tcgen05 + TMEM):
+//   Y[T, N] (fp32) = X[T, K] (bf16) . dequant(W_rung[N, K])^T
+// straight from the tiled W8 / W4 copy the decode GEMV streams (fq_internal.cuh), so prefill and
+// calibration use the same resident weights.  This is the dense contraction of SURVEY §7 step 6
+// (BASELINE config 4): MultiPrecisionLayer::forward on many rows at once
+// (/root/reference/proj/src/model.cpp:77-98 = dequantize src/quantizer.cpp:205-219 + linear
+// src/tensor.cpp:83-101).
+//
+// One CTA = 128 weight rows x 128 tokens, 4 warps:
+//   * every k-step (128 codes = one quantization group) all threads dequantize the 8 tiled
+//     16x128 blocks of the CTA's rows to fp16 (q - z) * s and convert the 128x128 activation
+//     tile bf16 -> fp16 (exact), both written into shared memory in the UMMA canonical K-major
+//     layout (no swizzle: 8x16-byte core matrices, LBO = 128 B along K, SBO = 2 KB along M/N);
+//   * one elected thread issues 8 tcgen05.mma (M=128, N=128, K=16, fp32 accumulate in TMEM) and
+//     commits them to the stage's mbarrier; two stages, so the dequantisation of step k+1
+//     overlaps the MMAs of step k;
+//   * epilogue: tcgen05.ld of the 128x128 fp32 accumulator (warp w reads TMEM lanes 32w..32w+31).
+#include "gemv_program.cuh"
+
+namespace fqc {
+namespace {
+
+constexpr int kTM = 128;   // weight rows per CTA (UMMA M)
+constexpr int kTN = 128;   // tokens per CTA (UMMA N)
+constexpr int kTK = 128;   // codes per k-step (one tiled block / quantization group)
+constexpr int kTileBytes = kTM * kTK * 2;  // one fp16 operand tile: 32 KB
+constexpr int kGemmThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// canonical K-major no-swizzle offset of element (row, k) inside a 128x128 fp16 tile
+__device__ __forceinline__ uint32_t kmajor_off(int row, int k) {
+  return static_cast<uint32_t>((row >> 3) * 2048 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);          // start address
+  d |= static_cast<uint64_t>(128u >> 4) << 16;                  // LBO: K-adjacent core matrices
+  d |= static_cast<uint64_t>(2048u >> 4) << 32;                 // SBO: 8-row groups
+  d |= static_cast<uint64_t>(1u) << 46;                         // descriptor version (sm_100)
+  return d;                                                     // base offset 0, SWIZZLE_NONE
+}
+
+// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N = 128, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
+
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+}
+__device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  unsigned long long t0 = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((spins & 1023u) == 1023u) {  // deadlock watchdog: report and trap instead of hanging
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) {
+        printf("fq gemm watchdog: mma barrier stuck (cta %d,%d parity %u)\n", blockIdx.x, blockIdx.y, parity);
+        __trap();
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Dequantises k-step kb of the CTA's 8 row tiles into the fp16 A tile (rows 0..127 of the tile).
+template <int W>
+__device__ __forceinline__ void dequant_step(const uint8_t* __restrict__ tiles, int64_t tile0, int n_tiles, int nkb, int kb,
+                                             int32_t zbase, uint8_t* a_tile) {
+  constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
+  constexpr int cbytes = W == 0 ? 2048 : 1024;
+  constexpr int words = W == 0 ? 4 : 2;  // 16-byte words per lane
+  const int tid = threadIdx.x;
+  // 8 row tiles x words x 32 lanes work items; 128 threads
+  for (int it = tid; it < 8 * words * 32; it += kGemmThreads) {
+    const int rt = it / (words * 32), rem = it - rt * words * 32;
+    const int i = rem >> 5, t = rem & 31;
+    const int64_t tile = tile0 + rt;
+    const int r = t >> 2, c2 = 2 * (t & 3);
+    const int row = rt * 16 + r;
+    if (tile >= n_tiles) {
+      // rows past N: zeros
+#pragma unroll
+      for (int h = 0; h < (W == 0 ? 2 : 4); ++h) {
+        const int j = W == 0 ? 2 * i + h : 4 * i + h;
+        const int k0 = 16 * j + c2;
+        for (int e = 0; e < 2; ++e)
+          for (int rr = 0; rr < 2; ++rr)
+            *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8 * rr, k0 + 8 * e)) = 0u;
+      }
+      continue;
+    }
+    const uint8_t* blk = tiles + (tile * nkb + kb) * bb;
+    const uint4 wv = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
+    const float s0 = reinterpret_cast<const float*>(blk + cbytes)[r];
+    const float s1 = reinterpret_cast<const float*>(blk + cbytes)[r + 8];
+    const float z0 = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r]) + zbase);
+    const float z1 = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r + 8]) + zbase);
+    const uint32_t u[4] = {wv.x, wv.y, wv.z, wv.w};
+    if constexpr (W == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k0 = 16 * (2 * i + h) + c2;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {  // e = 0: codes at k0, k0+1; e = 1: at k0+8, k0+9
+          const uint32_t q = u[2 * h + e];
+          const float a0 = (static_cast<float>(q & 0xFFu) - z0) * s0, a1 = (static_cast<float>((q >> 8) & 0xFFu) - z0) * s0;
+          const float b0 = (static_cast<float>((q >> 16) & 0xFFu) - z1) * s1, b1 = (static_cast<float>(q >> 24) - z1) * s1;
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_h2(a0, a1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8 * e)) = pack_h2(b0, b1);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int k0 = 16 * (4 * i + v) + c2;
+        const uint32_t q = u[v];
+        // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
+        auto nib = [&](int n) { return static_cast<float>((q >> (4 * n)) & 0xFu); };
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_h2((nib(0) - z0) * s0, (nib(4) - z0) * s0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = pack_h2((nib(1) - z0) * s0, (nib(5) - z0) * s0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = pack_h2((nib(2) - z1) * s1, (nib(6) - z1) * s1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = pack_h2((nib(3) - z1) * s1, (nib(7) - z1) * s1);
+      }
+    }
+  }
+}
+
+// Loads k-step kb of tokens t0..t0+127 (bf16 [T][x_stride]) as the fp16 B tile.
+__device__ __forceinline__ void stage_tokens(const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T, int64_t K, int t0,
+                                             int kb, uint8_t* b_tile) {
+  for (int it = threadIdx.x; it < kTN * (kTK / 8); it += kGemmThreads) {
+    const int tok = it >> 4, kc = it & 15;  // 16 chunks of 8 codes per token
+    const int t = t0 + tok;
+    const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
+    uint4 out = make_uint4(0u, 0u, 0u, 0u);
+    if (t < T && k < K) {
+      const __nv_bfloat16* src = x + static_cast<int64_t>(t) * x_stride + k;
+      float f[8];
+      if (k + 8 <= K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(src);
+        const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          f[2 * e] = __uint_as_float(rw[e] << 16);
+          f[2 * e + 1] = __uint_as_float(rw[e] & 0xFFFF0000u);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = k + e < K ? __bfloat162float(src[e]) : 0.f;
+      }
+      out = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
+    }
+    *reinterpret_cast<uint4*>(b_tile + kmajor_off(tok, kc * 8)) = out;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb,
+                                                                  int32_t zbase, int64_t N, int64_t K,
+                                                                  const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T,
+                                                                  float* __restrict__ y, int64_t y_stride) {
+  extern __shared__ __align__(1024) uint8_t gsm[];
+  __shared__ uint64_t mma_done[2];
+  __shared__ uint32_t tmem_base_s;
+  uint8_t* a_tiles = gsm;                      // 2 x 32 KB
+  uint8_t* b_tiles = gsm + 2 * kTileBytes;     // 2 x 32 KB
+  const int warp = threadIdx.x >> 5;
+  const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
+  const int t0 = blockIdx.y * kTN;
+  if (threadIdx.x == 0) {
+    mbar_init1(&mma_done[0]);
+    mbar_init1(&mma_done[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_s)),
+                 "r"(kTN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+  uint32_t phase[2] = {0u, 0u};
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int s = kb & 1;
+    if (kb >= 2) {  // the MMAs that read this stage (k-step kb - 2) are done
+      mbar_wait1(&mma_done[s], phase[s]);
+      phase[s] ^= 1u;
+    }
+    uint8_t* at = a_tiles + s * kTileBytes;
+    uint8_t* bt = b_tiles + s * kTileBytes;
+    dequant_step<W>(tiles, tile0, n_tiles, nkb, kb, zbase, at);
+    stage_tokens(x, x_stride, T, K, t0, kb, bt);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a0 = smem_addr(at), b0 = smem_addr(bt);
+#pragma unroll
+      for (int j = 0; j < kTK / 16; ++j) {
+        const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
+        const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+            ::"r"(tmem), "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_addr(&mma_done[s]))
+                   : "memory");
+    }
+  }
+  // wait for the last commit (it covers every earlier MMA of this thread)
+  const int last = (nkb - 1) & 1;
+  mbar_wait1(&mma_done[last], phase[last]);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // epilogue: warp w owns accumulator lanes (weight rows) 32w .. 32w+31, columns = tokens
+  const int lane = threadIdx.x & 31;
+  const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + warp * 32 + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < kTN; c0 += 8) {
+    uint32_t v[8];
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (n < N) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int t = t0 + c0 + e;
+        if (t < T) y[static_cast<int64_t>(t) * y_stride + n] = __uint_as_float(v[e]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTN));
+}
+
+}  // namespace
+
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x_bf16, int64_t x_stride, float* y,
+                    int64_t y_stride) {
+  if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
+  const fq_rung_store& st = L->store(rung);
+  if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
+  if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
+  const int n_tiles = ceil_div_i(L->N, kTileRows), nkb = ceil_div_i(L->K, kBlockK);
+  const dim3 grid(static_cast<unsigned>(ceil_div_i(L->N, kTM)), static_cast<unsigned>(ceil_div_i(T, kTN)));
+  const size_t smem = 4 * static_cast<size_t>(kTileBytes);
+  static bool configured = false;
+  if (!configured) {
+    FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    configured = true;
+  }
+  const auto* xb = static_cast<const __nv_bfloat16*>(x_bf16);
+  if (rung == FQ_RUNG_INT8)
+    gemm_dq_kernel<0><<<grid, kGemmThreads, smem, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, L->K, xb, x_stride,
+                                                                 static_cast<int>(T), y, y_stride);
+  else
+    gemm_dq_kernel<1><<<grid, kGemmThreads, smem, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, L->K, xb, x_stride,
+                                                                 static_cast<int>(T), y, y_stride);
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+}  // namespace fqc

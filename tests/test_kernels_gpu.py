@@ -236,3 +236,25 @@ def test_fill_normal_matches_host_generator(ctx):
     same = dd.view(np.uint32) == h.view(np.uint32)
     assert same.mean() > 0.999  # libm vs CUDA double transcendentals may differ in the last ulp
     assert np.max(np.abs(dd - h)) <= 1e-8
+
+
+@pytest.mark.parametrize("N,K,T", [(128, 128, 1), (256, 512, 64), (200, 1376, 130), (1024, 4096, 256)])
+@pytest.mark.parametrize("bits", [8, 4])
+def test_tcgen05_gemm_vs_oracle(ctx, N, K, T, bits):
+    """Prefill / calibration contraction on tcgen05: fp16 dequantised weights, fp32 accumulation
+    in tensor memory; within 1e-2 (max-norm relative) of the reference dequant + linear."""
+    w = _w(N, K, N + 7 * K)
+    L, ref = _layer(ctx, w, 128, (bits,))
+    x = np.random.default_rng(T + K).standard_normal((T, K)).astype(np.float32)
+    xb = torch.from_numpy(x).cuda().to(torch.bfloat16).contiguous()
+    y = torch.full((T, N), float("nan"), dtype=torch.float32, device="cuda")
+    rung = capi.RUNG_INT8 if bits == 8 else capi.RUNG_INT4
+    ctx.gemm(L, rung, T, xb, y)
+    ctx.synchronize()
+    p, s, z = ref[bits]
+    yref = np.zeros((T, N), np.float32)
+    oracle.lib().fqo_quant_linear(np.ascontiguousarray(xb.float().cpu().numpy()), T, p, N, K, 128, bits, 0, s.ravel(),
+                                  z.ravel(), None, yref)
+    got = y.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert _rel(got, yref) < 1e-2, _rel(got, yref)
