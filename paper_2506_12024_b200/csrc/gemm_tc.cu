@@ -6,7 +6,7 @@
 // (/root/reference/proj/src/model.cpp:77-98 = dequantize src/quantizer.cpp:205-219 + linear
 // src/tensor.cpp:83-101).
 //
-// One CTA = 128 weight rows x 128 tokens, 4 warps:
+// One CTA = 128 weight rows x 128 tokens, 8 warps:
 //   * every k-step (128 codes = one quantization group) all threads dequantize the 8 tiled
 //     16x128 blocks of the CTA's rows to fp16 (q - z) * s and convert the 128x128 activation
 //     tile bf16 -> fp16 (exact), both written into shared memory in the UMMA canonical K-major
@@ -14,7 +14,10 @@
 //   * one elected thread issues 8 tcgen05.mma (M=128, N=128, K=16, fp32 accumulate in TMEM) and
 //     commits them to the stage's mbarrier; two stages, so the dequantisation of step k+1
 //     overlaps the MMAs of step k;
-//   * epilogue: tcgen05.ld of the 128x128 fp32 accumulator (warp w reads TMEM lanes 32w..32w+31).
+//   * the global loads of step k+1 (code words, scales, activations) are issued into registers
+//     before step k's operands are written, so their latency hides behind the previous step;
+//   * epilogue: tcgen05.ld of the 128x128 fp32 accumulator (warps w and w+4 read TMEM lanes
+//     32w..32w+31, half of the token columns each).
 #include "gemv_program.cuh"
 
 namespace fqc {
@@ -24,7 +27,7 @@ constexpr int kTM = 128;   // weight rows per CTA (UMMA M)
 constexpr int kTN = 128;   // tokens per CTA (UMMA N)
 constexpr int kTK = 128;   // codes per k-step (one tiled block / quantization group)
 constexpr int kTileBytes = kTM * kTK * 2;  // one fp16 operand tile: 32 KB
-constexpr int kGemmThreads = 128;
+constexpr int kGemmThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -77,47 +80,85 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// Dequantises k-step kb of the CTA's 8 row tiles into the fp16 A tile (rows 0..127 of the tile).
+// Global-side raw data of one k-step for one thread: its 16-byte code words of the 8 tiled blocks
+// (+ the two rows' scale / zero point) and its 16-byte chunks of the activation tile.  Loaded one
+// k-step ahead (registers), so the global latency hides behind the previous step.
 template <int W>
-__device__ __forceinline__ void dequant_step(const uint8_t* __restrict__ tiles, int64_t tile0, int n_tiles, int nkb, int kb,
-                                             int32_t zbase, uint8_t* a_tile) {
+struct StepRaw {
+  static constexpr int kWords = W == 0 ? 4 : 2;                       // 16-byte code words per lane per block
+  static constexpr int kA = 8 * kWords * 32 / kGemmThreads;           // per thread
+  static constexpr int kX = kTN * (kTK / 8) / kGemmThreads;           // per thread
+  uint4 w[kA];
+  float s0[kA], s1[kA], z0[kA], z1[kA];
+  uint4 x[kX];
+};
+
+template <int W>
+__device__ __forceinline__ void load_step(const uint8_t* __restrict__ tiles, int64_t tile0, int n_tiles, int nkb, int kb,
+                                          int32_t zbase, const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T,
+                                          int64_t K, int t0, StepRaw<W>& r) {
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
-  constexpr int words = W == 0 ? 4 : 2;  // 16-byte words per lane
-  const int tid = threadIdx.x;
-  // 8 row tiles x words x 32 lanes work items; 128 threads
-  for (int it = tid; it < 8 * words * 32; it += kGemmThreads) {
+  constexpr int words = StepRaw<W>::kWords;
+#pragma unroll
+  for (int u = 0; u < StepRaw<W>::kA; ++u) {
+    const int it = threadIdx.x + u * kGemmThreads;
     const int rt = it / (words * 32), rem = it - rt * words * 32;
     const int i = rem >> 5, t = rem & 31;
-    const int64_t tile = tile0 + rt;
-    const int r = t >> 2, c2 = 2 * (t & 3);
-    const int row = rt * 16 + r;
-    if (tile >= n_tiles) {
-      // rows past N: zeros
-#pragma unroll
-      for (int h = 0; h < (W == 0 ? 2 : 4); ++h) {
-        const int j = W == 0 ? 2 * i + h : 4 * i + h;
-        const int k0 = 16 * j + c2;
-        for (int e = 0; e < 2; ++e)
-          for (int rr = 0; rr < 2; ++rr)
-            *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8 * rr, k0 + 8 * e)) = 0u;
-      }
-      continue;
-    }
+    const int64_t tile = min(tile0 + rt, static_cast<int64_t>(n_tiles) - 1);  // rows past N masked at store
     const uint8_t* blk = tiles + (tile * nkb + kb) * bb;
-    const uint4 wv = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
-    const float s0 = reinterpret_cast<const float*>(blk + cbytes)[r];
-    const float s1 = reinterpret_cast<const float*>(blk + cbytes)[r + 8];
-    const float z0 = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r]) + zbase);
-    const float z1 = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r + 8]) + zbase);
-    const uint32_t u[4] = {wv.x, wv.y, wv.z, wv.w};
+    const int rr = t >> 2;
+    r.w[u] = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
+    r.s0[u] = reinterpret_cast<const float*>(blk + cbytes)[rr];
+    r.s1[u] = reinterpret_cast<const float*>(blk + cbytes)[rr + 8];
+    r.z0[u] = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + rr]) + zbase);
+    r.z1[u] = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + rr + 8]) + zbase);
+  }
+#pragma unroll
+  for (int u = 0; u < StepRaw<W>::kX; ++u) {
+    const int it = threadIdx.x + u * kGemmThreads;
+    const int tok = it >> 4, kc = it & 15;  // 16 chunks of 8 codes per token
+    const int t = t0 + tok;
+    const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (t < T && k < K) {
+      const __nv_bfloat16* src = x + static_cast<int64_t>(t) * x_stride + k;
+      if (k + 8 <= K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        v = *reinterpret_cast<const uint4*>(src);
+      } else {
+        unsigned short h[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) h[e] = k + e < K ? reinterpret_cast<const unsigned short*>(src)[e] : 0;
+        v = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16), h[4] | (uint32_t(h[5]) << 16),
+                       h[6] | (uint32_t(h[7]) << 16));
+      }
+    }
+    r.x[u] = v;
+  }
+}
+
+// Writes one k-step's operands into the stage's shared-memory tiles (UMMA K-major layout):
+// A = fp16 (q - z) * s of the CTA's 128 weight rows, B = the activation tile converted bf16 -> fp16.
+template <int W>
+__device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, int n_tiles, uint8_t* a_tile, uint8_t* b_tile) {
+  constexpr int words = StepRaw<W>::kWords;
+#pragma unroll
+  for (int u = 0; u < StepRaw<W>::kA; ++u) {
+    const int it = threadIdx.x + u * kGemmThreads;
+    const int rt = it / (words * 32), rem = it - rt * words * 32;
+    const int i = rem >> 5, t = rem & 31;
+    const bool live = tile0 + rt < n_tiles;
+    const int rrow = t >> 2, c2 = 2 * (t & 3);
+    const int row = rt * 16 + rrow;
+    const float s0 = live ? r.s0[u] : 0.f, s1 = live ? r.s1[u] : 0.f, z0 = r.z0[u], z1 = r.z1[u];
+    const uint32_t q4[4] = {r.w[u].x, r.w[u].y, r.w[u].z, r.w[u].w};
     if constexpr (W == 0) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int k0 = 16 * (2 * i + h) + c2;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {  // e = 0: codes at k0, k0+1; e = 1: at k0+8, k0+9
-          const uint32_t q = u[2 * h + e];
+          const uint32_t q = q4[2 * h + e];
           const float a0 = (static_cast<float>(q & 0xFFu) - z0) * s0, a1 = (static_cast<float>((q >> 8) & 0xFFu) - z0) * s0;
           const float b0 = (static_cast<float>((q >> 16) & 0xFFu) - z1) * s1, b1 = (static_cast<float>(q >> 24) - z1) * s1;
           *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_h2(a0, a1);
@@ -128,7 +169,7 @@ __device__ __forceinline__ void dequant_step(const uint8_t* __restrict__ tiles, 
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int k0 = 16 * (4 * i + v) + c2;
-        const uint32_t q = u[v];
+        const uint32_t q = q4[v];
         // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
         auto nib = [&](int n) { return static_cast<float>((q >> (4 * n)) & 0xFu); };
         *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_h2((nib(0) - z0) * s0, (nib(4) - z0) * s0);
@@ -138,34 +179,15 @@ __device__ __forceinline__ void dequant_step(const uint8_t* __restrict__ tiles, 
       }
     }
   }
-}
-
-// Loads k-step kb of tokens t0..t0+127 (bf16 [T][x_stride]) as the fp16 B tile.
-__device__ __forceinline__ void stage_tokens(const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T, int64_t K, int t0,
-                                             int kb, uint8_t* b_tile) {
-  for (int it = threadIdx.x; it < kTN * (kTK / 8); it += kGemmThreads) {
-    const int tok = it >> 4, kc = it & 15;  // 16 chunks of 8 codes per token
-    const int t = t0 + tok;
-    const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
-    uint4 out = make_uint4(0u, 0u, 0u, 0u);
-    if (t < T && k < K) {
-      const __nv_bfloat16* src = x + static_cast<int64_t>(t) * x_stride + k;
-      float f[8];
-      if (k + 8 <= K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(src);
-        const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          f[2 * e] = __uint_as_float(rw[e] << 16);
-          f[2 * e + 1] = __uint_as_float(rw[e] & 0xFFFF0000u);
-        }
-      } else {
+  for (int u = 0; u < StepRaw<W>::kX; ++u) {
+    const int it = threadIdx.x + u * kGemmThreads;
+    const int tok = it >> 4, kc = it & 15;
+    const uint32_t rw[4] = {r.x[u].x, r.x[u].y, r.x[u].z, r.x[u].w};
+    uint32_t h[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = k + e < K ? __bfloat162float(src[e]) : 0.f;
-      }
-      out = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
-    }
-    *reinterpret_cast<uint4*>(b_tile + kmajor_off(tok, kc * 8)) = out;
+    for (int e = 0; e < 4; ++e) h[e] = pack_h2(__uint_as_float(rw[e] << 16), __uint_as_float(rw[e] & 0xFFFF0000u));
+    *reinterpret_cast<uint4*>(b_tile + kmajor_off(tok, kc * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
   }
 }
 
@@ -197,16 +219,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
   uint32_t phase[2] = {0u, 0u};
+  StepRaw<W> cur, nxt;
+  load_step<W>(tiles, tile0, n_tiles, nkb, 0, zbase, x, x_stride, T, K, t0, cur);
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;
+    const bool more = kb + 1 < nkb;
+    if (more) load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, x, x_stride, T, K, t0, nxt);
     if (kb >= 2) {  // the MMAs that read this stage (k-step kb - 2) are done
       mbar_wait1(&mma_done[s], phase[s]);
       phase[s] ^= 1u;
     }
     uint8_t* at = a_tiles + s * kTileBytes;
     uint8_t* bt = b_tiles + s * kTileBytes;
-    dequant_step<W>(tiles, tile0, n_tiles, nkb, kb, zbase, at);
-    stage_tokens(x, x_stride, T, K, t0, kb, bt);
+    store_step<W>(cur, tile0, n_tiles, at, bt);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -226,18 +251,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
                        smem_addr(&mma_done[s]))
                    : "memory");
     }
+    if (more) cur = nxt;
   }
   // wait for the last commit (it covers every earlier MMA of this thread)
   const int last = (nkb - 1) & 1;
   mbar_wait1(&mma_done[last], phase[last]);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // epilogue: warp w owns accumulator lanes (weight rows) 32w .. 32w+31, columns = tokens
+  // epilogue: warp w (of the first four) owns accumulator lanes 32w .. 32w+31 (weight rows);
+  // warps 4..7 take the second half of the token columns
   const int lane = threadIdx.x & 31;
-  const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + warp * 32 + lane;
+  const int wl = warp & 3;
+  const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + wl * 32 + lane;
+  const int cbeg = (warp >> 2) * (kTN / 2);
 #pragma unroll 1
-  for (int c0 = 0; c0 < kTN; c0 += 8) {
+  for (int c0 = cbeg; c0 < cbeg + kTN / 2; c0 += 8) {
     uint32_t v[8];
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(wl * 32) << 16) + c0;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "r"(taddr));
