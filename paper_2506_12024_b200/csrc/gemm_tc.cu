@@ -6,12 +6,12 @@
 // (/root/reference/proj/src/model.cpp:77-98 = dequantize src/quantizer.cpp:205-219 + linear
 // src/tensor.cpp:83-101).
 //
-// One CTA = 128 weight rows x 128 tokens, 8 warps:
+// One CTA = 128 weight rows x 256 tokens, 8 warps:
 //   * every k-step (128 codes = one quantization group) all threads dequantize the 8 tiled
-//     16x128 blocks of the CTA's rows to fp16 (q - z) * s and convert the 128x128 activation
-//     tile bf16 -> fp16 (exact), both written into shared memory in the UMMA canonical K-major
-//     layout (no swizzle: 8x16-byte core matrices, LBO = 128 B along K, SBO = 2 KB along M/N);
-//   * one elected thread issues 8 tcgen05.mma (M=128, N=128, K=16, fp32 accumulate in TMEM) and
+//     16x128 blocks of the CTA's rows to bf16 (q - z) * s into shared memory in the UMMA canonical
+//     K-major layout (no swizzle: 8x16-byte core matrices, LBO = 128 B along K, SBO = 2 KB along
+//     M/N), while the 256x128 bf16 activation tile arrives by cp.async in the same layout;
+//   * one elected thread issues 8 tcgen05.mma (M=128, N=256, K=16, fp32 accumulate in TMEM) and
 //     commits them to the stage's mbarrier; two stages, so the dequantisation of step k+1
 //     overlaps the MMAs of step k;
 //   * the global loads of step k+1 (code words, scales, activations) are issued into registers
@@ -24,9 +24,11 @@ namespace fqc {
 namespace {
 
 constexpr int kTM = 128;   // weight rows per CTA (UMMA M)
-constexpr int kTN = 128;   // tokens per CTA (UMMA N)
+constexpr int kTN = 256;   // tokens per CTA (UMMA N)
 constexpr int kTK = 128;   // codes per k-step (one tiled block / quantization group)
-constexpr int kTileBytes = kTM * kTK * 2;  // one fp16 operand tile: 32 KB
+constexpr int kATileBytes = kTM * kTK * 2;  // bf16 weight tile: 32 KB
+constexpr int kBTileBytes = kTN * kTK * 2;  // bf16 activation tile: 64 KB
+constexpr int kStageBytesG = kATileBytes + kBTileBytes;
 constexpr int kGemmThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -45,8 +47,8 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return d;                                                     // base offset 0, SWIZZLE_NONE
 }
 
-// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, N = 128, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = kTN, M = kTM
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
 
 __device__ __forceinline__ void mbar_init1(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
@@ -75,8 +77,8 @@ __device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
+__device__ __forceinline__ uint32_t pack_b2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
@@ -87,16 +89,31 @@ template <int W>
 struct StepRaw {
   static constexpr int kWords = W == 0 ? 4 : 2;                       // 16-byte code words per lane per block
   static constexpr int kA = 8 * kWords * 32 / kGemmThreads;           // per thread
-  static constexpr int kX = kTN * (kTK / 8) / kGemmThreads;           // per thread
   uint4 w[kA];
   float s0[kA], s1[kA], z0[kA], z1[kA];
-  uint4 x[kX];
 };
+
+// Activation tile of a k-step straight into shared memory (cp.async, 16-byte chunks = one core-
+// matrix row; rows past T / codes past K are zero-filled), bf16 as stored.
+__device__ __forceinline__ void load_tokens_async(const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T, int64_t K,
+                                                  int t0, int kb, uint8_t* b_tile) {
+#pragma unroll 4
+  for (int it = threadIdx.x; it < kTN * (kTK / 8); it += kGemmThreads) {
+    const int tok = it >> 4, kc = it & 15;
+    const int t = t0 + tok;
+    const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
+    const bool in = t < T && k < K;
+    const __nv_bfloat16* src = in ? x + static_cast<int64_t>(t) * x_stride + k : x;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(b_tile + kmajor_off(tok, kc * 8))),
+                 "l"(src), "r"(in ? 16 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 template <int W>
 __device__ __forceinline__ void load_step(const uint8_t* __restrict__ tiles, int64_t tile0, int n_tiles, int nkb, int kb,
-                                          int32_t zbase, const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T,
-                                          int64_t K, int t0, StepRaw<W>& r) {
+                                          int32_t zbase, StepRaw<W>& r) {
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
   constexpr int words = StepRaw<W>::kWords;
@@ -114,33 +131,12 @@ __device__ __forceinline__ void load_step(const uint8_t* __restrict__ tiles, int
     r.z0[u] = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + rr]) + zbase);
     r.z1[u] = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + rr + 8]) + zbase);
   }
-#pragma unroll
-  for (int u = 0; u < StepRaw<W>::kX; ++u) {
-    const int it = threadIdx.x + u * kGemmThreads;
-    const int tok = it >> 4, kc = it & 15;  // 16 chunks of 8 codes per token
-    const int t = t0 + tok;
-    const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (t < T && k < K) {
-      const __nv_bfloat16* src = x + static_cast<int64_t>(t) * x_stride + k;
-      if (k + 8 <= K && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        v = *reinterpret_cast<const uint4*>(src);
-      } else {
-        unsigned short h[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) h[e] = k + e < K ? reinterpret_cast<const unsigned short*>(src)[e] : 0;
-        v = make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16), h[4] | (uint32_t(h[5]) << 16),
-                       h[6] | (uint32_t(h[7]) << 16));
-      }
-    }
-    r.x[u] = v;
-  }
 }
 
-// Writes one k-step's operands into the stage's shared-memory tiles (UMMA K-major layout):
-// A = fp16 (q - z) * s of the CTA's 128 weight rows, B = the activation tile converted bf16 -> fp16.
+// Writes one k-step's weight operand into the stage's shared-memory tile (UMMA K-major layout):
+// A = bf16 (q - z) * s of the CTA's 128 weight rows.
 template <int W>
-__device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, int n_tiles, uint8_t* a_tile, uint8_t* b_tile) {
+__device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, int n_tiles, uint8_t* a_tile) {
   constexpr int words = StepRaw<W>::kWords;
 #pragma unroll
   for (int u = 0; u < StepRaw<W>::kA; ++u) {
@@ -161,8 +157,8 @@ __device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, i
           const uint32_t q = q4[2 * h + e];
           const float a0 = (static_cast<float>(q & 0xFFu) - z0) * s0, a1 = (static_cast<float>((q >> 8) & 0xFFu) - z0) * s0;
           const float b0 = (static_cast<float>((q >> 16) & 0xFFu) - z1) * s1, b1 = (static_cast<float>(q >> 24) - z1) * s1;
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_h2(a0, a1);
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8 * e)) = pack_h2(b0, b1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_b2(a0, a1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8 * e)) = pack_b2(b0, b1);
         }
       }
     } else {
@@ -172,22 +168,12 @@ __device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, i
         const uint32_t q = q4[v];
         // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
         auto nib = [&](int n) { return static_cast<float>((q >> (4 * n)) & 0xFu); };
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_h2((nib(0) - z0) * s0, (nib(4) - z0) * s0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = pack_h2((nib(1) - z0) * s0, (nib(5) - z0) * s0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = pack_h2((nib(2) - z1) * s1, (nib(6) - z1) * s1);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = pack_h2((nib(3) - z1) * s1, (nib(7) - z1) * s1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_b2((nib(0) - z0) * s0, (nib(4) - z0) * s0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = pack_b2((nib(1) - z0) * s0, (nib(5) - z0) * s0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = pack_b2((nib(2) - z1) * s1, (nib(6) - z1) * s1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = pack_b2((nib(3) - z1) * s1, (nib(7) - z1) * s1);
       }
     }
-  }
-#pragma unroll
-  for (int u = 0; u < StepRaw<W>::kX; ++u) {
-    const int it = threadIdx.x + u * kGemmThreads;
-    const int tok = it >> 4, kc = it & 15;
-    const uint32_t rw[4] = {r.x[u].x, r.x[u].y, r.x[u].z, r.x[u].w};
-    uint32_t h[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) h[e] = pack_h2(__uint_as_float(rw[e] << 16), __uint_as_float(rw[e] & 0xFFFF0000u));
-    *reinterpret_cast<uint4*>(b_tile + kmajor_off(tok, kc * 8)) = make_uint4(h[0], h[1], h[2], h[3]);
   }
 }
 
@@ -199,8 +185,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   extern __shared__ __align__(1024) uint8_t gsm[];
   __shared__ uint64_t mma_done[2];
   __shared__ uint32_t tmem_base_s;
-  uint8_t* a_tiles = gsm;                      // 2 x 32 KB
-  uint8_t* b_tiles = gsm + 2 * kTileBytes;     // 2 x 32 KB
+  uint8_t* stage_base = gsm;  // 2 stages x (A 32 KB | B 64 KB)
   const int warp = threadIdx.x >> 5;
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
   const int t0 = blockIdx.y * kTN;
@@ -220,23 +205,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   const uint32_t tmem = tmem_base_s;
   uint32_t phase[2] = {0u, 0u};
   StepRaw<W> cur, nxt;
-  load_step<W>(tiles, tile0, n_tiles, nkb, 0, zbase, x, x_stride, T, K, t0, cur);
+  load_tokens_async(x, x_stride, T, K, t0, 0, stage_base + kATileBytes);
+  load_step<W>(tiles, tile0, n_tiles, nkb, 0, zbase, cur);
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb & 1;
     const bool more = kb + 1 < nkb;
-    if (more) load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, x, x_stride, T, K, t0, nxt);
-    if (kb >= 2) {  // the MMAs that read this stage (k-step kb - 2) are done
-      mbar_wait1(&mma_done[s], phase[s]);
-      phase[s] ^= 1u;
+    uint8_t* at = stage_base + s * kStageBytesG;
+    if (more) {
+      // the other stage was read by the MMAs of k-step kb - 1: once they are done, its
+      // activation tile is refilled for k-step kb + 1 (cp.async) and its weights prefetched
+      if (kb >= 1) {
+        mbar_wait1(&mma_done[s ^ 1], phase[s ^ 1]);
+        phase[s ^ 1] ^= 1u;
+      }
+      load_tokens_async(x, x_stride, T, K, t0, kb + 1, stage_base + (s ^ 1) * kStageBytesG + kATileBytes);
+      load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, nxt);
     }
-    uint8_t* at = a_tiles + s * kTileBytes;
-    uint8_t* bt = b_tiles + s * kTileBytes;
-    store_step<W>(cur, tile0, n_tiles, at, bt);
+    store_step<W>(cur, tile0, n_tiles, at);
+    // this step's activation group has landed (the next step's may still be in flight)
+    if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
     __syncthreads();
     if (threadIdx.x == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_addr(at), b0 = smem_addr(bt);
+      const uint32_t a0 = smem_addr(at), b0 = smem_addr(at + kATileBytes);
 #pragma unroll
       for (int j = 0; j < kTK / 16; ++j) {
         const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
@@ -292,9 +285,11 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
   const fq_rung_store& st = L->store(rung);
   if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
   if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
+  if (x_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(x_bf16) & 15) != 0)
+    fail(FQ_E_CONFIG, "gemm: activation rows must be 16-byte aligned (row stride a multiple of 8)");
   const int n_tiles = ceil_div_i(L->N, kTileRows), nkb = ceil_div_i(L->K, kBlockK);
   const dim3 grid(static_cast<unsigned>(ceil_div_i(L->N, kTM)), static_cast<unsigned>(ceil_div_i(T, kTN)));
-  const size_t smem = 4 * static_cast<size_t>(kTileBytes);
+  const size_t smem = 2 * static_cast<size_t>(kStageBytesG);
   static bool configured = false;
   if (!configured) {
     FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
