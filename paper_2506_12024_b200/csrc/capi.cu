@@ -93,6 +93,7 @@ fq_status fq_ctx_destroy(fq_ctx* ctx) {
     dfree(ctx->gemv_fix);
     dfree(ctx->gemv_flags);
     dfree(ctx->launch_ctr);
+    dfree(ctx->gemm_ws);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -314,7 +315,7 @@ fq_status fq_gemm(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t rows, co
     require(ctx != nullptr && L != nullptr && x_dev != nullptr && y_dev != nullptr, FQ_E_INPUT, "null argument");
     require(rows >= 1, FQ_E_DIMENSION, "gemm: rows must be >= 1");
     require(x_stride >= L->K && y_stride >= L->N, FQ_E_DIMENSION, "gemm: row stride smaller than the row");
-    launch_gemm_dq(ctx, L, rung, rows, x_dev, x_stride, y_dev, y_stride);
+    launch_gemm_dq(ctx, L, rung, rows, x_dev, FQ_DT_BF16, x_stride, y_dev, y_stride);
   });
 }
 

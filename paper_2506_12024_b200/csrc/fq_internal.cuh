@@ -57,6 +57,8 @@ struct fq_ctx {
   float* gemv_fix = nullptr;
   unsigned int* gemv_flags = nullptr;
   unsigned int* launch_ctr = nullptr;  // [epoch, done] of the program kernels on this context
+  float* gemm_ws = nullptr;  // split-K partial sums of the tensor-core GEMM (grown on demand)
+  size_t gemm_ws_bytes = 0;
 };
 
 // ------------------------------------------------------------------ tiled fast-path layout
@@ -170,9 +172,20 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
                        int x_dtype, void* y, int y_dtype);
 
-// tcgen05 dequant-GEMM: y[T, N] (fp32, row stride y_stride) = x[T, K] (bf16) . dequant(W_rung)^T
-void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x_bf16, int64_t x_stride, float* y,
-                    int64_t y_stride);
+// tcgen05 dequant-GEMM: y[T, N] (fp32, row stride y_stride) = x[T, K] . dequant(W_rung)^T with x
+// bf16 (weights dequantised to bf16) or fp16 (weights to fp16: 3 more mantissa bits, the
+// prefill's choice); accumulate: y += instead (the residual add of the O / down projections)
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x, int x_dtype, int64_t x_stride,
+                    float* y, int64_t y_stride, bool accumulate = false);
+
+// row-parallel prefill kernels (prefill.cu; llama arch; GEMM operands bf16-rounded, stored fp16)
+void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev, int T, int64_t d, float* x);
+void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16);
+void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,
+                     const float2* cs, float* qr, __half* kv_layer, int64_t max_seq);
+void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
+                       void* out16);
+void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, void* out16);
 
 // statistics
 void launch_softmax_stats(fq_ctx* ctx, const float* logits, int64_t rows, int64_t vocab,

@@ -47,8 +47,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   return d;                                                     // base offset 0, SWIZZLE_NONE
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = kTN, M = kTM
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
+// kind::f16 instruction descriptor: D f32, A/B bf16 (F16 = 0) or fp16 (F16 = 1), both K-major,
+// N = kTN, M = kTM
+template <int F16>
+constexpr uint32_t idesc() {
+  return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
+}
 
 __device__ __forceinline__ void mbar_init1(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
@@ -77,9 +81,15 @@ __device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
   }
 }
 
+template <int F16>
 __device__ __forceinline__ uint32_t pack_b2(float a, float b) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
+  if constexpr (F16) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
 }
 
 // Global-side raw data of one k-step for one thread: its 16-byte code words of the 8 tiled blocks
@@ -95,7 +105,7 @@ struct StepRaw {
 
 // Activation tile of a k-step straight into shared memory (cp.async, 16-byte chunks = one core-
 // matrix row; rows past T / codes past K are zero-filled), bf16 as stored.
-__device__ __forceinline__ void load_tokens_async(const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T, int64_t K,
+__device__ __forceinline__ void load_tokens_async(const uint16_t* __restrict__ x, int64_t x_stride, int T, int64_t K,
                                                   int t0, int kb, uint8_t* b_tile) {
 #pragma unroll 4
   for (int it = threadIdx.x; it < kTN * (kTK / 8); it += kGemmThreads) {
@@ -103,7 +113,7 @@ __device__ __forceinline__ void load_tokens_async(const __nv_bfloat16* __restric
     const int t = t0 + tok;
     const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
     const bool in = t < T && k < K;
-    const __nv_bfloat16* src = in ? x + static_cast<int64_t>(t) * x_stride + k : x;
+    const uint16_t* src = in ? x + static_cast<int64_t>(t) * x_stride + k : x;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(b_tile + kmajor_off(tok, kc * 8))),
                  "l"(src), "r"(in ? 16 : 0)
                  : "memory");
@@ -134,8 +144,8 @@ __device__ __forceinline__ void load_step(const uint8_t* __restrict__ tiles, int
 }
 
 // Writes one k-step's weight operand into the stage's shared-memory tile (UMMA K-major layout):
-// A = bf16 (q - z) * s of the CTA's 128 weight rows.
-template <int W>
+// A = 16-bit (q - z) * s of the CTA's 128 weight rows.
+template <int W, int F16>
 __device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, int n_tiles, uint8_t* a_tile) {
   constexpr int words = StepRaw<W>::kWords;
 #pragma unroll
@@ -157,8 +167,8 @@ __device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, i
           const uint32_t q = q4[2 * h + e];
           const float a0 = (static_cast<float>(q & 0xFFu) - z0) * s0, a1 = (static_cast<float>((q >> 8) & 0xFFu) - z0) * s0;
           const float b0 = (static_cast<float>((q >> 16) & 0xFFu) - z1) * s1, b1 = (static_cast<float>(q >> 24) - z1) * s1;
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_b2(a0, a1);
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8 * e)) = pack_b2(b0, b1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_b2<F16>(a0, a1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8 * e)) = pack_b2<F16>(b0, b1);
         }
       }
     } else {
@@ -168,20 +178,21 @@ __device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, i
         const uint32_t q = q4[v];
         // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
         auto nib = [&](int n) { return static_cast<float>((q >> (4 * n)) & 0xFu); };
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_b2((nib(0) - z0) * s0, (nib(4) - z0) * s0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = pack_b2((nib(1) - z0) * s0, (nib(5) - z0) * s0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = pack_b2((nib(2) - z1) * s1, (nib(6) - z1) * s1);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = pack_b2((nib(3) - z1) * s1, (nib(7) - z1) * s1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_b2<F16>((nib(0) - z0) * s0, (nib(4) - z0) * s0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = pack_b2<F16>((nib(1) - z0) * s0, (nib(5) - z0) * s0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = pack_b2<F16>((nib(2) - z1) * s1, (nib(6) - z1) * s1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = pack_b2<F16>((nib(3) - z1) * s1, (nib(7) - z1) * s1);
       }
     }
   }
 }
 
-template <int W>
+template <int W, int F16>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb,
                                                                   int32_t zbase, int64_t N, int64_t K,
-                                                                  const __nv_bfloat16* __restrict__ x, int64_t x_stride, int T,
-                                                                  float* __restrict__ y, int64_t y_stride) {
+                                                                  const uint16_t* __restrict__ x, int64_t x_stride, int T,
+                                                                  float* __restrict__ y, int64_t y_stride, int accumulate,
+                                                                  int splits, int64_t split_stride) {
   extern __shared__ __align__(1024) uint8_t gsm[];
   __shared__ uint64_t mma_done[2];
   __shared__ uint32_t tmem_base_s;
@@ -189,6 +200,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   const int warp = threadIdx.x >> 5;
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
   const int t0 = blockIdx.y * kTN;
+  // split-K: this CTA's k-steps [kb0, kb1); partial sums go to y + z * split_stride
+  const int kb0 = static_cast<int>(static_cast<int64_t>(nkb) * blockIdx.z / splits);
+  const int kb1 = static_cast<int>(static_cast<int64_t>(nkb) * (blockIdx.z + 1) / splits);
+  y += blockIdx.z * split_stride;
   if (threadIdx.x == 0) {
     mbar_init1(&mma_done[0]);
     mbar_init1(&mma_done[1]);
@@ -205,26 +220,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   const uint32_t tmem = tmem_base_s;
   uint32_t phase[2] = {0u, 0u};
   StepRaw<W> cur, nxt;
-  load_tokens_async(x, x_stride, T, K, t0, 0, stage_base + kATileBytes);
-  load_step<W>(tiles, tile0, n_tiles, nkb, 0, zbase, cur);
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int s = kb & 1;
-    const bool more = kb + 1 < nkb;
+  load_tokens_async(x, x_stride, T, K, t0, kb0, stage_base + kATileBytes);
+  load_step<W>(tiles, tile0, n_tiles, nkb, kb0, zbase, cur);
+  // Pipeline: k-step kb dequantises into stage s = kb & 1 while the MMAs of kb - 1 run; right
+  // after kb's MMAs are issued, the MMAs of kb - 1 (the other stage's last reader) are waited for
+  // and that stage's activation tile refilled for kb + 1, so neither the tensor pipe nor the
+  // dequantisation waits on the other in steady state.
+  for (int kb = kb0; kb < kb1; ++kb) {
+    const int i = kb - kb0;
+    const int s = i & 1;
+    const bool more = kb + 1 < kb1;
     uint8_t* at = stage_base + s * kStageBytesG;
-    if (more) {
-      // the other stage was read by the MMAs of k-step kb - 1: once they are done, its
-      // activation tile is refilled for k-step kb + 1 (cp.async) and its weights prefetched
-      if (kb >= 1) {
-        mbar_wait1(&mma_done[s ^ 1], phase[s ^ 1]);
-        phase[s ^ 1] ^= 1u;
-      }
-      load_tokens_async(x, x_stride, T, K, t0, kb + 1, stage_base + (s ^ 1) * kStageBytesG + kATileBytes);
-      load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, nxt);
-    }
-    store_step<W>(cur, tile0, n_tiles, at);
-    // this step's activation group has landed (the next step's may still be in flight)
-    if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (more) load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, nxt);
+    store_step<W, F16>(cur, tile0, n_tiles, at);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -233,21 +242,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
 #pragma unroll
       for (int j = 0; j < kTK / 16; ++j) {
         const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
-        const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
+        const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-            ::"r"(tmem), "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+            ::"r"(tmem), "l"(da), "l"(db), "r"(idesc<F16>()), "r"(acc));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_addr(&mma_done[s]))
                    : "memory");
     }
-    if (more) cur = nxt;
+    if (more) {
+      if (i >= 1) {
+        mbar_wait1(&mma_done[s ^ 1], phase[s ^ 1]);
+        phase[s ^ 1] ^= 1u;
+      }
+      load_tokens_async(x, x_stride, T, K, t0, kb + 1, stage_base + (s ^ 1) * kStageBytesG + kATileBytes);
+      cur = nxt;
+    }
   }
   // wait for the last commit (it covers every earlier MMA of this thread)
-  const int last = (nkb - 1) & 1;
+  const int last = (kb1 - kb0 - 1) & 1;
   mbar_wait1(&mma_done[last], phase[last]);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue: warp w (of the first four) owns accumulator lanes 32w .. 32w+31 (weight rows);
@@ -257,7 +273,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + wl * 32 + lane;
   const int cbeg = (warp >> 2) * (kTN / 2);
 #pragma unroll 1
-  for (int c0 = cbeg; c0 < cbeg + kTN / 2; c0 += 8) {
+  for (int c0 = cbeg; c0 < cbeg + kTN / 2 && t0 + c0 < T; c0 += 8) {
     uint32_t v[8];
     const uint32_t taddr = tmem + (static_cast<uint32_t>(wl * 32) << 16) + c0;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -268,7 +284,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int t = t0 + c0 + e;
-        if (t < T) y[static_cast<int64_t>(t) * y_stride + n] = __uint_as_float(v[e]);
+        if (t < T) {
+          float* yp = y + static_cast<int64_t>(t) * y_stride + n;
+          *yp = accumulate ? *yp + __uint_as_float(v[e]) : __uint_as_float(v[e]);
+        }
       }
     }
   }
@@ -277,34 +296,99 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTN));
 }
 
+// y[t][n] (+)= sum over the splits in order of ws[z][t][n] (deterministic split-K reduction)
+__global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, int64_t T, int64_t N, float* __restrict__ y,
+                                    int64_t y_stride, int accumulate) {
+  const int64_t total = T * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / N, n = i - t * N;
+    float v = ws[i];
+    for (int z = 1; z < splits; ++z) v += ws[z * total + i];
+    float* yp = y + t * y_stride + n;
+    *yp = accumulate ? *yp + v : v;
+  }
+}
+
+template <int W, int F16>
+void configure_gemm(size_t smem) {
+  static bool done = false;
+  if (!done) {
+    FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<W, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    done = true;
+  }
+}
+
 }  // namespace
 
-void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x_bf16, int64_t x_stride, float* y,
-                    int64_t y_stride) {
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x, int x_dtype, int64_t x_stride,
+                    float* y, int64_t y_stride, bool accumulate) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
+  if (x_dtype != FQ_DT_BF16 && x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: activations must be bf16 or fp16");
   const fq_rung_store& st = L->store(rung);
   if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
   if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
-  if (x_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(x_bf16) & 15) != 0)
+  if (x_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0)
     fail(FQ_E_CONFIG, "gemm: activation rows must be 16-byte aligned (row stride a multiple of 8)");
   const int n_tiles = ceil_div_i(L->N, kTileRows), nkb = ceil_div_i(L->K, kBlockK);
-  const dim3 grid(static_cast<unsigned>(ceil_div_i(L->N, kTM)), static_cast<unsigned>(ceil_div_i(T, kTN)));
-  const size_t smem = 2 * static_cast<size_t>(kStageBytesG);
-  static bool configured = false;
-  if (!configured) {
-    FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    configured = true;
+  const int gx = ceil_div_i(L->N, kTM), gy = ceil_div_i(T, kTN);
+  // split K when the output tiles alone leave SMs idle: the fewest splits with the lowest
+  // (waves x work per split), at least 4 k-steps per split
+  int splits = 1;
+  {
+    const int64_t cta = gx * static_cast<int64_t>(gy);
+    double best = static_cast<double>((cta + ctx->num_sms - 1) / ctx->num_sms);
+    for (int sp = 2; sp <= 8 && nkb / sp >= 4; ++sp) {
+      const double cost = static_cast<double>((cta * sp + ctx->num_sms - 1) / ctx->num_sms) / sp;
+      if (cost < best - 1e-9) {
+        best = cost;
+        splits = sp;
+      }
+    }
   }
-  const auto* xb = static_cast<const __nv_bfloat16*>(x_bf16);
-  if (rung == FQ_RUNG_INT8)
-    gemm_dq_kernel<0><<<grid, kGemmThreads, smem, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, L->K, xb, x_stride,
-                                                                 static_cast<int>(T), y, y_stride);
-  else
-    gemm_dq_kernel<1><<<grid, kGemmThreads, smem, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, L->K, xb, x_stride,
-                                                                 static_cast<int>(T), y, y_stride);
+  float* out = y;
+  int64_t out_stride = y_stride, split_stride = 0;
+  if (splits > 1) {
+    const size_t need = sizeof(float) * static_cast<size_t>(splits) * T * L->N;
+    if (ctx->gemm_ws_bytes < need) {
+      dfree(ctx->gemm_ws);
+      ctx->gemm_ws = static_cast<float*>(dmalloc(need));
+      ctx->gemm_ws_bytes = need;
+    }
+    out = ctx->gemm_ws;
+    out_stride = L->N;
+    split_stride = T * L->N;
+  }
+  const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
+  const size_t smem = 2 * static_cast<size_t>(kStageBytesG);
+  const auto* xs = static_cast<const uint16_t*>(x);
+  const int acc = splits > 1 ? 0 : (accumulate ? 1 : 0);
+  const int Ti = static_cast<int>(T);
+#define FQ_GEMM_LAUNCH(Wv, Fv)                                                                                     \
+  do {                                                                                                             \
+    configure_gemm<Wv, Fv>(smem);                                                                                  \
+    gemm_dq_kernel<Wv, Fv><<<grid, kGemmThreads, smem, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, L->K, \
+                                                                      xs, x_stride, Ti, out, out_stride, acc,       \
+                                                                      splits, split_stride);                        \
+  } while (0)
+  const bool f16 = x_dtype == FQ_DT_F16;
+  if (rung == FQ_RUNG_INT8) {
+    if (f16) FQ_GEMM_LAUNCH(0, 1);
+    else FQ_GEMM_LAUNCH(0, 0);
+  } else {
+    if (f16) FQ_GEMM_LAUNCH(1, 1);
+    else FQ_GEMM_LAUNCH(1, 0);
+  }
+#undef FQ_GEMM_LAUNCH
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
+  if (splits > 1) {
+    const int64_t total = T * L->N;
+    const int blocks = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
+    split_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->gemm_ws, splits, T, L->N, y, y_stride, accumulate ? 1 : 0);
+    FQ_CUDA(cudaGetLastError());
+    ctx->launches += 1;
+  }
 }
 
 }  // namespace fqc

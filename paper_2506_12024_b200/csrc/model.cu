@@ -18,6 +18,7 @@
 #include "gemv_program.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -325,6 +326,15 @@ struct fq_model {
   std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, StepMode) -> uploaded program
   unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
+  // tensor-core prefill workspace (llama; grown to the longest prompt seen, prefill_gemm)
+  struct PrefillWs {
+    int64_t cap = 0;
+    float *x = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *qr = nullptr, *g = nullptr, *u = nullptr,
+          *logits = nullptr;
+    void *h = nullptr, *a = nullptr, *m = nullptr;
+    fq_row_stats* stats = nullptr;
+    int32_t* tok = nullptr;
+  } pw;
   int rows = 1;  // activation rows: max(max_batch, prefill chunk) (llama); max_batch (reference)
 
   int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
@@ -746,6 +756,118 @@ void prefill_step(fq_model* M, int slot, const int32_t* tokens, int R, float* lo
     FQ_CUDA(cudaMemcpyAsync(logits_dev, M->logits, sizeof(float) * R * c.vocab_size, cudaMemcpyDeviceToDevice, st));
 }
 
+// ---------------------------------------------------------------- tensor-core prefill (llama)
+// A prompt of T tokens goes through each block as T rows at once: the seven linears and the head
+// on the tcgen05 dequant-GEMM (gemm_tc.cu, weights read once per 256 rows instead of once per
+// 8), norms / RoPE + cache append / causal attention / SwiGLU on the row kernels of prefill.cu.
+// Same arithmetic contract as the decode program; used for prompts of at least
+// gemm_prefill_min() tokens (env FQ_GEMM_PREFILL_MIN, 0 = off) when every linear's active rung
+// is W8/W4 in the tiled layout and activations are bf16.
+
+int64_t gemm_prefill_min() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("FQ_GEMM_PREFILL_MIN");
+    return e ? static_cast<int64_t>(std::atoll(e)) : static_cast<int64_t>(16);
+  }();
+  return v;
+}
+
+bool gemm_prefill_usable(const fq_model* M, int slot, int64_t T) {
+  const fq_model_config& c = M->cfg;
+  const int64_t lo = gemm_prefill_min();
+  if (!M->llama || lo <= 0 || T < lo || c.act_dtype != FQ_DT_BF16) return false;
+  if (c.d_model % 8 != 0 || c.ffn_dim % 8 != 0) return false;
+  for (int i = 0; i < M->n_lin; ++i) {
+    const int r = M->rungs[static_cast<size_t>(slot) * M->n_lin + i];
+    if (r != FQ_RUNG_INT8 && r != FQ_RUNG_INT4) return false;
+    const fq_rung_store& st = M->lin[i]->store(r);
+    if (!st.present || st.tiles == nullptr) return false;
+  }
+  return true;
+}
+
+void free_prefill_ws(fq_model* M) {
+  auto& w = M->pw;
+  for (void* p : {static_cast<void*>(w.x), static_cast<void*>(w.q), static_cast<void*>(w.k), static_cast<void*>(w.v),
+                  static_cast<void*>(w.qr), static_cast<void*>(w.g), static_cast<void*>(w.u),
+                  static_cast<void*>(w.logits), w.h, w.a, w.m, static_cast<void*>(w.stats), static_cast<void*>(w.tok)})
+    dfree(p);
+  w = fq_model::PrefillWs{};
+}
+
+void ensure_prefill_ws(fq_model* M, int64_t T) {
+  auto& w = M->pw;
+  if (T <= w.cap) return;
+  free_prefill_ws(M);
+  const fq_model_config& c = M->cfg;
+  const int64_t cap = std::min<int64_t>(c.max_seq_len, (T + 63) / 64 * 64);
+  const int64_t d = c.d_model, f = c.ffn_dim, V = c.vocab_size;
+  auto f32 = [&](int64_t n) { return static_cast<float*>(dmalloc(sizeof(float) * n)); };
+  w.x = f32(cap * d);
+  w.q = f32(cap * d);
+  w.k = f32(cap * d);
+  w.v = f32(cap * d);
+  w.qr = f32(cap * d);
+  w.g = f32(cap * f);
+  w.u = f32(cap * f);
+  w.logits = f32(cap * V);
+  w.h = dmalloc(2 * cap * d);
+  w.a = dmalloc(2 * cap * d);
+  w.m = dmalloc(2 * cap * f);
+  w.stats = static_cast<fq_row_stats*>(dmalloc(sizeof(fq_row_stats) * cap));
+  w.tok = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * cap));
+  w.cap = cap;
+}
+
+// Enqueues the whole prefill of `slot` (cache rows 0..T-1).  logits_out: [T, V] fp32 (null = the
+// workspace); stats_dev: [T] row statistics (null = none).  Does not synchronise.
+void prefill_gemm_enqueue(fq_model* M, int slot, const int32_t* tokens_host, int64_t T, float* logits_out,
+                          fq_row_stats* stats_dev) {
+  fq_ctx* ctx = M->ctx;
+  const fq_model_config& c = M->cfg;
+  cudaStream_t st = ctx->stream;
+  ensure_prefill_ws(M, T);
+  auto& w = M->pw;
+  const int64_t d = c.d_model, f = c.ffn_dim, V = c.vocab_size;
+  const int H = static_cast<int>(c.n_heads), hd = static_cast<int>(c.head_dim);
+  const int Ti = static_cast<int>(T);
+  const uint8_t* r = &M->rungs[static_cast<size_t>(slot) * M->n_lin];
+  FQ_CUDA(cudaMemcpyAsync(w.tok, tokens_host, sizeof(int32_t) * T, cudaMemcpyHostToDevice, st));
+  prefill_embed(ctx, M->tok_emb, w.tok, Ti, d, w.x);
+  __half* kv_slot = static_cast<__half*>(M->kv) + static_cast<int64_t>(slot) * M->slot_stride;
+  for (int l = 0; l < c.n_layers; ++l) {
+    const int b = M->lin_index(l, 0);
+    __half* kvl = kv_slot + static_cast<int64_t>(l) * M->layer_stride;
+    prefill_rmsnorm(ctx, w.x, Ti, d, M->n1g[l], c.norm_eps, w.h);
+    launch_gemm_dq(ctx, M->lin[b + 0], r[b + 0], T, w.h, FQ_DT_F16, d, w.q, d);
+    launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, FQ_DT_F16, d, w.k, d);
+    launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, FQ_DT_F16, d, w.v, d);
+    prefill_rope_kv(ctx, w.q, w.k, w.v, Ti, H, hd, M->rope_cs, w.qr, kvl, c.max_seq_len);
+    prefill_attention(ctx, w.qr, kvl, H, hd, c.max_seq_len, Ti, w.a);
+    launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, FQ_DT_F16, d, w.x, d, true);  // x += attn . Wo^T
+    prefill_rmsnorm(ctx, w.x, Ti, d, M->n2g[l], c.norm_eps, w.h);
+    launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, FQ_DT_F16, d, w.g, f);
+    launch_gemm_dq(ctx, M->lin[b + 5], r[b + 5], T, w.h, FQ_DT_F16, d, w.u, f);
+    prefill_swiglu(ctx, w.g, w.u, T * f, w.m);
+    launch_gemm_dq(ctx, M->lin[b + 6], r[b + 6], T, w.m, FQ_DT_F16, f, w.x, d, true);  // x += mid . Wdown^T
+  }
+  prefill_rmsnorm(ctx, w.x, Ti, d, M->fng, c.norm_eps, w.h);
+  float* lg = logits_out ? logits_out : w.logits;
+  const int hi = M->head_index();
+  launch_gemm_dq(ctx, M->lin[hi], r[hi], T, w.h, FQ_DT_F16, d, lg, V);
+  if (stats_dev) launch_softmax_stats(ctx, lg, T, V, V, stats_dev);
+}
+
+void prefill_gemm(fq_model* M, int slot, const int32_t* tokens, int64_t T, float* logits_dev, fq_row_stats* stats_host) {
+  if (T > M->cfg.max_seq_len) fail(FQ_E_CAPACITY, "prefill: cache is full");
+  ensure_prefill_ws(M, T);
+  prefill_gemm_enqueue(M, slot, tokens, T, logits_dev, stats_host ? M->pw.stats : nullptr);
+  if (stats_host)
+    FQ_CUDA(cudaMemcpyAsync(stats_host, M->pw.stats, sizeof(fq_row_stats) * T, cudaMemcpyDeviceToHost, M->ctx->stream));
+  FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+  M->slot_len[slot] = T;
+}
+
 float* param_slot(fq_model* M, const std::string& name, int64_t& expect) {
   const fq_model_config& c = M->cfg;
   const int64_t d = c.d_model;
@@ -939,6 +1061,7 @@ fq_status fq_model_destroy(fq_model* M) {
     for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
     dfree(M->grid_barrier);
+    free_prefill_ws(M);
     for (fq_layer* L : M->lin) {
       L->borrowed = false;
       fq_layer_destroy(L);
@@ -1132,6 +1255,10 @@ fq_status fq_model_prefill(fq_model* M, int32_t slot, const int32_t* tokens, int
       }
       return;
     }
+    if (gemm_prefill_usable(M, slot, n)) {
+      prefill_gemm(M, slot, tokens, n, logits_dev, stats_host);
+      return;
+    }
     // llama: kPrefillRows consecutive positions per step (rows of one program launch)
     for (int64_t p0 = 0; p0 < n; p0 += kPrefillRows) {
       const int R = static_cast<int>(std::min<int64_t>(kPrefillRows, n - p0));
@@ -1308,6 +1435,62 @@ fq_status fq_model_calibrate_logit_kl(fq_model* M, const int32_t* tokens, int64_
     double* kl_dev = static_cast<double*>(dmalloc(sizeof(double) * B * 2));
     std::vector<double> klsum(c.n_layers, 0.0), entsum(c.n_layers, 0.0);
     std::vector<uint8_t> saved(M->rungs);
+    // llama with W8/W4 rungs: every sequence is one tensor-core prefill (all len rows at once)
+    // and the KL of all its rows one launch
+    auto gemm_path = [&](int flip_layer) {
+      for (int i = 0; i < M->n_lin; ++i) {
+        const bool in_block = flip_layer >= 0 && i / per == flip_layer && i < M->head_index();
+        M->rungs[i] = static_cast<uint8_t>(in_block ? flip_rung : base_rung);
+      }
+      return gemm_prefill_usable(M, 0, len);
+    };
+    if (gemm_path(-1) && gemm_path(0)) {
+      try {
+        double* kl_rows = static_cast<double*>(dmalloc(sizeof(double) * 2 * len));
+        float* flip_all = static_cast<float*>(dmalloc(sizeof(float) * len * V));
+        try {
+          std::vector<double> h(2 * len);
+          for (int fl = -1; fl < c.n_layers; ++fl) {
+            gemm_path(fl);
+            for (int64_t s = 0; s < n_seqs; ++s) {
+              float* base = base_logits + s * len * V;
+              prefill_gemm_enqueue(M, 0, tokens + s * len, len, fl < 0 ? base : flip_all, nullptr);
+              if (fl < 0) continue;
+              launch_kl_rows(M->ctx, flip_all, base, FQ_DT_F32, len, V, kl_rows, kl_rows + len);
+              FQ_CUDA(cudaMemcpyAsync(h.data(), kl_rows, sizeof(double) * 2 * len, cudaMemcpyDeviceToHost, M->ctx->stream));
+              FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+              for (int64_t t = 0; t < len; ++t) {
+                klsum[fl] += h[t];
+                entsum[fl] += h[len + t];
+              }
+            }
+          }
+        } catch (...) {
+          dfree(kl_rows);
+          dfree(flip_all);
+          throw;
+        }
+        dfree(kl_rows);
+        dfree(flip_all);
+      } catch (...) {
+        M->rungs = saved;
+        dfree(base_logits);
+        dfree(flip_logits);
+        dfree(kl_dev);
+        throw;
+      }
+      M->rungs = saved;
+      M->slot_len[0] = 0;
+      for (int l = 0; l < c.n_layers; ++l) {
+        kl_host[l] = klsum[l] / static_cast<double>(rows);
+        if (entropy_host) entropy_host[l] = entsum[l] / static_cast<double>(rows);
+      }
+      dfree(base_logits);
+      dfree(flip_logits);
+      dfree(kl_dev);
+      return;
+    }
+    M->rungs = saved;
     auto run = [&](int flip_layer) {
       for (int64_t s0 = 0; s0 < n_seqs; s0 += B) {
         const int nb = static_cast<int>(std::min<int64_t>(B, n_seqs - s0));

@@ -1,0 +1,157 @@
+// Row-parallel kernels of the tensor-core prefill (llama arch): the T prompt rows of one sequence
+// go through each layer at once, the seven linears of a block and the head on the tcgen05 GEMM
+// (gemm_tc.cu), everything else here.  Precision contract as in the decode program:
+// fp32 residual, bf16-rounded activations (normalised inputs, q/k/v, attention output, SwiGLU
+// product), RoPE from the model's cos/sin table, fp16 K/V cache, fp32 softmax.
+#include "fq_internal.cuh"
+
+namespace fqc {
+namespace {
+
+__device__ __forceinline__ float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+// GEMM operand: the bf16-rounded activation (the decode contract) carried as fp16, exact in fp16's
+// normal range, so the GEMM can dequantise its weights to fp16 (kind::f16 takes one operand type)
+__device__ __forceinline__ __half act16(float v) { return __float2half_rn(bf16r(v)); }
+
+__global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32_t* __restrict__ tokens, int64_t d,
+                                  float* __restrict__ x) {
+  const int t = blockIdx.x;
+  const float* e = tok_emb + static_cast<int64_t>(tokens[t]) * d;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) x[t * d + i] = e[i];
+}
+
+// h[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * g)
+__global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g, float eps,
+                                    __half* __restrict__ h) {
+  const int t = blockIdx.x;
+  const float* xr = x + t * d;
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s += xr[i] * xr[i];
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float rstd = 1.0f / sqrtf(red[0] / static_cast<float>(d) + eps);
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) h[t * d + i] = act16(xr[i] * rstd * g[i]);
+}
+
+// q/k/v rows (fp32 GEMM outputs, rounded to bf16 as the decode step stores them) -> RoPE'd and
+// pre-scaled q (fp32) and the fp16 K / V cache rows 0..T-1 of the slot.
+__global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+                                    int H, int hd, const float2* __restrict__ cs, float* __restrict__ qr,
+                                    __half* __restrict__ kv_layer, int64_t max_seq) {
+  const int t = blockIdx.x;
+  const int d = H * hd, half = hd / 2;
+  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+  for (int idx = threadIdx.x; idx < H * half; idx += blockDim.x) {
+    const int h = idx / half, i = idx - h * half;
+    const int64_t o0 = static_cast<int64_t>(t) * d + h * hd + i, o1 = o0 + half;
+    const float2 c = cs[static_cast<int64_t>(t) * half + i];
+    const float q0 = bf16r(q[o0]), q1 = bf16r(q[o1]);
+    qr[o0] = (q0 * c.x - q1 * c.y) * scale;
+    qr[o1] = (q1 * c.x + q0 * c.y) * scale;
+    const float k0 = bf16r(k[o0]), k1 = bf16r(k[o1]);
+    __half* kc = kv_layer + static_cast<int64_t>(h) * max_seq * hd + static_cast<int64_t>(t) * hd;
+    __half* vc = kc + static_cast<int64_t>(H) * max_seq * hd;
+    kc[i] = __float2half_rn(k0 * c.x - k1 * c.y);
+    kc[i + half] = __float2half_rn(k1 * c.x + k0 * c.y);
+    vc[i] = __float2half_rn(bf16r(v[o0]));
+    vc[i + half] = __float2half_rn(bf16r(v[o1]));
+  }
+}
+
+// Causal attention of query row t, head h on one warp (lanes own hd/32 dims), online softmax over
+// the keys 0..t of the fp16 cache; output bf16.
+template <int DPL>
+__global__ void attn_rows_kernel(const float* __restrict__ qr, const __half* __restrict__ kv_layer, int H, int64_t max_seq,
+                                 int T, __half* __restrict__ out) {
+  constexpr int hd = DPL * 32;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= T * H) return;
+  const int t = warp / H, h = warp - t * H;
+  const int d = H * hd;
+  float q[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) q[e] = qr[static_cast<int64_t>(t) * d + h * hd + DPL * lane + e];
+  const __half* kc = kv_layer + static_cast<int64_t>(h) * max_seq * hd;
+  const __half* vc = kc + static_cast<int64_t>(H) * max_seq * hd;
+  float m = -INFINITY, l = 0.f, o[DPL];
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) o[e] = 0.f;
+  for (int j = 0; j <= t; ++j) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) s += q[e] * __half2float(kc[static_cast<int64_t>(j) * hd + DPL * lane + e]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float mn = fmaxf(m, s);
+    const float fa = m == -INFINITY ? 0.f : expf(m - mn), p = expf(s - mn);
+    l = l * fa + p;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) o[e] = o[e] * fa + p * __half2float(vc[static_cast<int64_t>(j) * hd + DPL * lane + e]);
+    m = mn;
+  }
+#pragma unroll
+  for (int e = 0; e < DPL; ++e) out[static_cast<int64_t>(t) * d + h * hd + DPL * lane + e] = act16(o[e] / l);
+}
+
+__global__ void swiglu_rows_kernel(const float* __restrict__ g, const float* __restrict__ u, int64_t n,
+                                   __half* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float gv = g[i];  // unrounded GEMM sums, as the decode step's SwiGLU epilogue reads them
+    const float silu = gv / (1.0f + expf(-gv));
+    out[i] = act16(silu * u[i]);
+  }
+}
+
+int elem_grid(const fq_ctx* ctx, int64_t n) { return static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, (n + 255) / 256)); }
+
+}  // namespace
+
+void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev, int T, int64_t d, float* x) {
+  embed_rows_kernel<<<T, 256, 0, ctx->stream>>>(tok_emb, tokens_dev, d, x);
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16) {
+  rmsnorm_rows_kernel<<<T, 256, 0, ctx->stream>>>(x, d, g, eps, static_cast<__half*>(h16));
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,
+                     const float2* cs, float* qr, __half* kv_layer, int64_t max_seq) {
+  rope_kv_rows_kernel<<<T, 256, 0, ctx->stream>>>(q, k, v, H, hd, cs, qr, kv_layer, max_seq);
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
+                       void* out16) {
+  const int warps = T * H;
+  const int blocks = (warps * 32 + 255) / 256;
+  if (hd == 128)
+    attn_rows_kernel<4><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<__half*>(out16));
+  else
+    attn_rows_kernel<2><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<__half*>(out16));
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, void* out16) {
+  swiglu_rows_kernel<<<elem_grid(ctx, n), 256, 0, ctx->stream>>>(g, u, n, static_cast<__half*>(out16));
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+}  // namespace fqc

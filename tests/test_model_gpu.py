@@ -273,3 +273,57 @@ def test_llama_chunked_prefill_matches_oracle_and_decode(ctx, n):
         b = m.decode([1], [int(t)])[0]
         assert abs(a["entropy"] - b["entropy"]) <= 1e-4
         assert a["argmax"] == b["argmax"]
+
+
+@pytest.mark.parametrize("n,mixed", [(16, False), (100, True)])
+def test_llama_tensor_core_prefill_matches_oracle(ctx, n, mixed):
+    """Prompts of >= 16 tokens go through the tcgen05 prefill (all rows of a block at once, weights
+    dequantised to bf16 tiles): every row's logits within the north-star 1e-2 relative of the numpy
+    restatement, and the cache it leaves behind continues like the oracle's."""
+    m, orc = _llama(ctx)
+    rungs = [8 if (i % 3 or not mixed) else 4 for i in range(len(orc.ids))]
+    for i, r in enumerate(rungs):
+        m.set_rung(0, i, capi.RUNG_INT8 if r == 8 else capi.RUNG_INT4)
+    toks = oracle.random_tokens(n + 4, 8192, 300 + n)
+    out = torch.zeros((n, 8192), dtype=torch.float32, device="cuda")
+    st = m.prefill(0, toks[:n], out)
+    ctx.synchronize()
+    assert m.slot_length(0) == n
+    got = out.cpu().numpy()
+    cache = orc.new_cache()
+    for i in range(n):
+        want = orc.step(int(toks[i]), cache, rungs)
+        rel = np.max(np.abs(got[i] - want)) / np.max(np.abs(want))
+        assert rel < 1e-2, (i, rel)
+        o = oracle.row_stats(got[i])
+        assert abs(st["entropy"][i] - o["entropy"]) <= 1e-5
+        assert int(st["argmax"][i]) == o["argmax"]
+        assert abs(st["entropy"][i] - oracle.row_stats(want)["entropy"]) <= 1e-3
+    # decode continues from the cache the prefill wrote (K/V rows 0..n-1 of every layer)
+    dec = torch.zeros((1, 8192), dtype=torch.float32, device="cuda")
+    for t in toks[n:]:
+        m.decode([0], [int(t)], dec)
+        ctx.synchronize()
+        want = orc.step(int(t), cache, rungs)
+        got1 = dec.cpu().numpy()[0]
+        assert np.max(np.abs(got1 - want)) / np.max(np.abs(want)) < 1e-2
+
+
+def test_llama_logit_kl_calibration_tensor_core(ctx):
+    """Sequences of >= 16 tokens calibrate through the tcgen05 prefill (one prefill + one KL launch
+    per sequence and flipped block); block 0's mean KL follows the teacher-forced oracle."""
+    m, orc = _llama(ctx, max_batch=1, cfg=dict(LLAMA_TINY, max_seq_len=32))
+    toks = oracle.random_tokens(2 * 20, 8192, 6).reshape(2, 20)
+    kl, ent = m.calibrate_logit_kl(toks, capi.RUNG_INT8, capi.RUNG_INT4)
+    assert kl.shape == (4,) and np.all(kl > 0) and np.all(ent > 0)
+    tot = 0.0
+    for s in range(2):
+        c8, c4 = orc.new_cache(), orc.new_cache()
+        r4 = [4 if i < 7 else 8 for i in range(len(orc.ids))]
+        for t in toks[s]:
+            a = orc.step(int(t), c8, [8] * len(orc.ids))
+            b = orc.step(int(t), c4, r4)
+            tot += oracle.kl_logits(b, a)[0]
+    want = tot / 40
+    assert abs(kl[0] - want) <= 5e-2 * want + 1e-4, (kl[0], want)
+    assert m.slot_length(0) == 0
