@@ -206,6 +206,10 @@ fq_status fq_model_prefill(fq_model* model, int32_t slot, const int32_t* tokens_
  * replayed from a captured CUDA graph. logits_dev optional [batch, V] copy-out. */
 fq_status fq_model_decode(fq_model* model, int32_t batch, const int32_t* slots_host,
                           const int32_t* tokens_host, float* logits_dev, fq_row_stats* stats_host);
+/* Device time of the decode-step program kernels (CUDA events recorded around the launch inside
+ * the step graph): total ms and number of steps since the last reset (reset != 0 clears after
+ * reading).  bench.py's roofline divides the step's algorithmic bytes by this per-launch time. */
+fq_status fq_model_step_kernel_time(fq_model* model, int32_t reset, double* ms_total, int64_t* steps);
 /* Device pointer of the model's internal logits buffer [max_batch, V] (valid after a step). */
 fq_status fq_model_logits(fq_model* model, float** logits_dev);
 /* Algorithmic bytes of one decode step for `batch` slots at their current rungs/lengths. */

@@ -33,6 +33,7 @@ ABI_FUNCTIONS = [
     "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
     "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
     "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step", "fq_gemm",
+    "fq_model_step_kernel_time",
 ]
 
 
@@ -146,6 +147,7 @@ def load(path: str = LIB_PATH):
         "fq_model_prefill": [v, i32, v, i64, v, v],
         "fq_model_decode": [v, i32, v, v, v, v],
         "fq_model_logits": [v, C.POINTER(v)],
+        "fq_model_step_kernel_time": [v, i32, C.POINTER(C.c_double), C.POINTER(i64)],
         "fq_model_step_bytes": [v, i32, v, C.POINTER(i64), C.POINTER(i64)],
         "fq_model_calibrate_logit_kl": [v, v, i64, i64, i32, i32, v, v],
         "fq_model_profile_gemvs": [v, i32, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64)],
@@ -405,6 +407,12 @@ class Model:
         st = np.zeros(s.size, ROW_STATS_DTYPE)
         check(self.L.fq_model_decode(self.h, s.size, _ptr(s), _ptr(t), _ptr(logits_dev), _ptr(st)))
         return st
+
+    def step_kernel_time(self, reset: bool = True) -> tuple:
+        """(total ms, steps) of the decode-step program kernels since the last reset (device events)."""
+        ms, n = C.c_double(), C.c_int64()
+        check(self.L.fq_model_step_kernel_time(self.h, 1 if reset else 0, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def logits_ptr(self) -> int:
         p = C.c_void_p()

@@ -18,6 +18,7 @@
 #include "gemv_program.cuh"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -326,6 +327,10 @@ struct fq_model {
   std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, StepMode) -> uploaded program
   unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
+  // device time of the step program kernels (events around the launch, captured into the graph)
+  cudaEvent_t ev_prog[2] = {nullptr, nullptr};
+  double prog_ms = 0.0;
+  int64_t prog_steps = 0;
   // tensor-core prefill workspace (llama; grown to the longest prompt seen, prefill_gemm)
   struct PrefillWs {
     int64_t cap = 0;
@@ -569,7 +574,12 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       it = M->programs.emplace(key, upload_program(ctx, pb, false)).first;
     }
     FQ_CUDA(cudaMemsetAsync(M->grid_barrier, 0, sizeof(unsigned int), st));
+    const bool timed = mode == STEP_DECODE && M->ev_prog[0] != nullptr;
+    // inside a capture the records must be external nodes to record at replay
+    const unsigned int ev_flags = capturing(st) ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (timed) FQ_CUDA(cudaEventRecordWithFlags(M->ev_prog[0], st, ev_flags));
     launch_program(ctx, it->second, M->grid_barrier, false);
+    if (timed) FQ_CUDA(cudaEventRecordWithFlags(M->ev_prog[1], st, ev_flags));
     return;
   }
   // ---------------- reference architecture (exact numerics)
@@ -683,6 +693,21 @@ void run_step(fq_model* M, int B) {
   FQ_CUDA(cudaGraphLaunch(it->second, st));
   ctx->launches += M->graph_kernels[B];
   FQ_CUDA(cudaStreamSynchronize(st));
+  if (M->ev_prog[0]) {
+    float ms = 0.f;
+    const cudaError_t e = cudaEventElapsedTime(&ms, M->ev_prog[0], M->ev_prog[1]);
+    if (e == cudaSuccess) {
+      M->prog_ms += ms;
+      M->prog_steps += 1;
+    } else {
+      cudaGetLastError();  // not sticky: keep it out of the next launch check
+      static bool once = false;
+      if (!once && std::getenv("FQ_DEBUG_TIMING")) {
+        std::fprintf(stderr, "fq: step timing unavailable: %s\n", cudaGetErrorString(e));
+        once = true;
+      }
+    }
+  }
 }
 
 int64_t ffn_or_d(const fq_model_config& c) { return std::max(c.d_model, c.ffn_dim); }
@@ -1049,6 +1074,10 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
       FQ_CUDA(cudaMemcpy(M->rope_cs, cs.data(), sizeof(float2) * cs.size(), cudaMemcpyHostToDevice));
     }
     M->grid_barrier = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * 4));
+    if (M->llama) {
+      FQ_CUDA(cudaEventCreate(&M->ev_prog[0]));
+      FQ_CUDA(cudaEventCreate(&M->ev_prog[1]));
+    }
     FQ_CUDA(cudaStreamSynchronize(st));
     *out = M;
   });
@@ -1062,6 +1091,8 @@ fq_status fq_model_destroy(fq_model* M) {
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
     dfree(M->grid_barrier);
     free_prefill_ws(M);
+    for (cudaEvent_t e : M->ev_prog)
+      if (e) cudaEventDestroy(e);
     for (fq_layer* L : M->lin) {
       L->borrowed = false;
       fq_layer_destroy(L);
@@ -1273,6 +1304,18 @@ fq_status fq_model_decode(fq_model* M, int32_t batch, const int32_t* slots, cons
   return guarded([&] {
     require(M && slots && tokens, FQ_E_INPUT, "null argument");
     model_step(M, batch, slots, tokens, logits_dev, stats_host);
+  });
+}
+
+fq_status fq_model_step_kernel_time(fq_model* M, int32_t reset, double* ms_total, int64_t* steps) {
+  return guarded([&] {
+    require(M != nullptr, FQ_E_INPUT, "null model");
+    if (ms_total) *ms_total = M->prog_ms;
+    if (steps) *steps = M->prog_steps;
+    if (reset) {
+      M->prog_ms = 0.0;
+      M->prog_steps = 0;
+    }
   });
 }
 
