@@ -12,7 +12,10 @@ namespace fqc {
 constexpr int kMaxB = 8;          // batch rows per GEMV phase (the MMA's n = 8 columns)
 constexpr int kMaxMat = 3;        // matrices sharing one input (QKV)
 constexpr int kMaxStages = 8;
-constexpr int kNCW = 8;           // consumer warps (2 blocks in flight each)
+#ifndef FQ_NCW
+#define FQ_NCW 8
+#endif
+constexpr int kNCW = FQ_NCW;      // consumer warps (2 blocks in flight each)
 constexpr int kThreads = (kNCW + 1) * 32;  // + one producer warp
 constexpr int kAttnChunk = 16;    // keys per attention work item (one warp)
 constexpr int kStageBytes = 35328;  // max(16 W8 blocks, 32 W4 blocks)

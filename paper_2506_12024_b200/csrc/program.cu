@@ -124,6 +124,15 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+// (v & 0x00F000F0) | 0x54005400 in one LOP3: the two nibbles at bits 4-7 / 20-23 as fp16 64 + q.
+// Written as PTX with both constants immediate so ptxas keeps one in a register instead of
+// splitting the AND and the OR (the W4 unpack is ALU-bound).
+__device__ __forceinline__ uint32_t nib_f16(uint32_t v) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x00F000F0, 0x54005400, 0xEA;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // D += A(16x16 f16, row) * B(16x8 f16, col), fp32 accumulators.
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                          uint32_t b1) {
@@ -316,6 +325,9 @@ __device__ void produce_all(const Phase* phases, int nphases, const Ring R, unsi
 }
 
 // ---------------------------------------------------------------- consumers: GEMV
+#ifndef FQ_RING_TRACE
+#define FQ_RING_TRACE 0  // consumer-side ring stamps (tools/phase_profile.py; build with -DFQ_RING_TRACE=1)
+#endif
 // Shared-memory staging of a GEMV phase's activations (once per phase, all consumer threads):
 //   xs[((kb*4 + p)*B + b)*4 + tig] = uint4: the m16n8k16 B fragments {b0b1, b2b3} of MMAs 2p and
 //       2p+1 of block kb for batch column b and thread-in-group tig (fp16, x converted exactly
@@ -475,8 +487,7 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, int
           // every nibble pair is moved to bits 4-7 / 20-23 of the halves: fp16 0x5400 | q<<4 = 64 + q
           const uint32_t q = qs[u];
           const uint4 xv = u < 2 ? x0 : x1;
-          mma16816(c[n], ((q << 4) & 0x00F000F0u) | 0x54005400u, ((q >> 4) & 0x00F000F0u) | 0x54005400u,
-                   (q & 0x00F000F0u) | 0x54005400u, ((q >> 8) & 0x00F000F0u) | 0x54005400u, (u & 1) ? xv.z : xv.x,
+          mma16816(c[n], nib_f16(q << 4), nib_f16(q >> 4), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
                    (u & 1) ? xv.w : xv.y);
         }
       }
@@ -897,7 +908,14 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     load_seg();
     while (left > 0) {
       const int nb = min(min(capb, nkb - kb), left);
+#if FQ_RING_TRACE
+      const bool stamp = G.tr != nullptr && warp == 0 && lane == 0 && *G.tn < kTraceStages;
+      if (stamp) G.tr[3 * *G.tn + 1] = gtimer();
+#endif
       mbar_wait(&R.full[slot_i], phase_bit);
+#if FQ_RING_TRACE
+      if (stamp) G.tr[3 * (*G.tn)++ + 2] = gtimer();
+#endif
       const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * kStageBytes;
       const float4* dxa = G.dx + static_cast<size_t>(kb) * B + 2 * tig;
       for (int j = warp; j < nb; j += 2 * kNCW) {

@@ -67,13 +67,19 @@ for rep in range(a.reps):
 # consumer warp 0 started waiting for it, data ready
 tr = m.last_ring_trace
 tr = tr[tr[:, 0] > 0]
-if len(tr):
+if len(tr) and not tr[:, 1].any():
+    print(f"ring trace CTA0: {len(tr)} producer stamps; consumer stamps off (build program.cu with -DFQ_RING_TRACE=1, "
+          "e.g. tools/ab_build.sh trace -DFQ_RING_TRACE=1 and FQ_CUDA_LIB=...)")
+elif len(tr):
     t0 = tr[0, 0]
     lat = tr[:, 2] - tr[:, 0]
     waited = np.maximum(tr[:, 2] - tr[:, 1], 0)
     print(f"ring trace CTA0: {len(tr)} stages; issue->ready median {np.median(lat)/1e3:.2f} us; consumer wait total "
           f"{waited.sum()/1e3:.1f} us (stages waited >0.2us: {(waited > 200).sum()})")
-    for i in range(0, min(len(tr), 48)):
+    proc = tr[1:, 1] - tr[:-1, 2]
+    print(f"  warp-0 time per stage between ready and the next want: median {np.median(proc)/1e3:.2f} us, "
+          f"p90 {np.percentile(proc, 90)/1e3:.2f} us")
+    for i in list(range(0, min(len(tr), 24))) + list(range(min(len(tr), 200), min(len(tr), 240))):
         print(f"   stage {i:3d} issue {(tr[i,0]-t0)/1e3:8.2f} want {(tr[i,1]-t0)/1e3:8.2f} ready {(tr[i,2]-t0)/1e3:8.2f}")
 # GEMV phase detail: per role, sums over phases of the per-phase max over CTAs of each interval
 det = m.last_gemv_detail
