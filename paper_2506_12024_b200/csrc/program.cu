@@ -203,9 +203,19 @@ __device__ void phase_segs(const Phase& P, Segs& S) {
     }
 }
 
+#ifndef FQ_TILE_PART
+#define FQ_TILE_PART 1
+#endif
 // 32-bit arithmetic: the builder guarantees a phase's bytes fit in 32 bits.
+// FQ_TILE_PART: whole 16-row tiles per CTA (floor/ceil of n_tiles / grid): no tile is split, so no
+// CTA waits for another's stream-K part; the <= 1 tile of imbalance is absorbed by the weight
+// stream running ahead.  Otherwise byte-balanced ranges with stream-K fix-up of split tiles.
 __device__ int64_t cta_start(const Phase& P, const Segs& S, int c) {
   if (S.n == 0) return 0;
+  if (FQ_TILE_PART) {
+    const int64_t t = (static_cast<int64_t>(P.n_tiles) * c) / gridDim.x;
+    return t * S.n * P.nkb;
+  }
   const uint32_t tb = static_cast<uint32_t>(S.tile_bytes);
   const uint32_t total = static_cast<uint32_t>(P.n_tiles) * tb;
   const uint32_t grid = gridDim.x;
@@ -329,7 +339,7 @@ __device__ void produce_all(const Phase* phases, int nphases, const Ring R, unsi
 #define FQ_RING_TRACE 0  // consumer-side ring stamps (tools/phase_profile.py; build with -DFQ_RING_TRACE=1)
 #endif
 // Shared-memory staging of a GEMV phase's activations (once per phase, all consumer threads):
-//   xs[((kb*4 + p)*B + b)*4 + tig] = uint4: the m16n8k16 B fragments {b0b1, b2b3} of MMAs 2p and
+//   xs[((b*nkb + kb)*4 + p)*4 + tig] = uint4 (batch-major: a lane's fragments sit at immediate offsets): the m16n8k16 B fragments {b0b1, b2b3} of MMAs 2p and
 //       2p+1 of block kb for batch column b and thread-in-group tig (fp16, x converted exactly
 //       from bf16/fp16 activations);
 //   dx[kb*B + b] = {1024*X, 64*X, X, 0}: X = sum of the block's activations; the offsets the
@@ -346,103 +356,125 @@ struct GemvSmem {
   int* tn;
 };
 
+// Issue order: every global load of the first item batch (activations, norm gains) and the RMSNorm
+// partials go out together, so the phase pays one round trip before its first MMA; warp b reduces
+// row b's partials while the activation loads are in flight.
+constexpr int kStageItems = 2;  // items per thread per batch (loads in flight together)
+static_assert(kMaxB <= kNCW, "one consumer warp per batch row computes its RMSNorm factor");
+
 __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
   const int B = P.B;
-  const int tid = threadIdx.x;
-  if (tid < 32) {
-    // RMSNorm factors: every partial loaded up front (one round trip), fixed-order sums
-    constexpr int kMaxParts = 8;  // 8 x 32 >= partials (grid <= 256)
-    for (int b = 0; b < B; ++b) {
-      float r = 1.f;
-      if (P.norm_gain != nullptr) {
-        float v[kMaxParts];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = kNCW * 32;
+  const float* gain = P.norm_gain;
+  // RMSNorm partials of row `warp` (fixed-order sums, as before)
+  constexpr int kMaxParts = 8;  // 8 x 32 >= partials (grid <= 256)
+  float pv[kMaxParts];
+  if (warp < B && gain != nullptr) {
 #pragma unroll
-        for (int j = 0; j < kMaxParts; ++j) {
-          const int i = tid + 32 * j;
-          v[j] = i < P.n_partials ? P.norm_partials[b * P.partials_stride + i] : 0.f;
-        }
-        float s = 0.f;
-#pragma unroll
-        for (int j = 0; j < kMaxParts; ++j) s += v[j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        r = 1.0f / sqrtf(s / static_cast<float>(P.K) + P.norm_eps);
-      }
-      if (tid == 0) G.rstd[b] = r;
+    for (int j = 0; j < kMaxParts; ++j) {
+      const int i = lane + 32 * j;
+      pv[j] = i < P.n_partials ? P.norm_partials[warp * P.partials_stride + i] : 0.f;
     }
-    if (gp) gp[1] = gtimer();
   }
-  named_sync(1, kNCW * 32);
-  if (gp) gp[2] = gtimer();
   const int items = P.nkb * B * 16;
   const int64_t K = P.K;
   const void* x = P.x;
   const int xdt = P.x_dtype, adt = P.act_dtype;
-  const float* gain = P.norm_gain;
-  for (int base = 0; base < items; base += kNCW * 32) {
-    const int it = base + tid;
-    const bool active = it < items;
-    const int kb = it / (B * 16);
-    const int rem = it - kb * B * 16;
-    const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
-    // the 8 activations of this item: loads are unconditional (index clamped into the row, the
-    // value zeroed past K) so they issue back to back
-    float raw[8], gn[8];
-    int64_t kk[8], kc[8];
+  for (int base = 0;; base += NT * kStageItems) {
+    float raw[kStageItems][8], gn[kStageItems][8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int hh = e >> 2, q = e & 3;
-      kk[e] = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
-      kc[e] = b * P.x_stride + (active ? min(kk[e], K - 1) : 0);
-    }
-    // one dtype branch around all eight loads (a branch per load would serialise them)
-    if (xdt == FQ_DT_F32) {
-      const float* xf = static_cast<const float*>(x);
+    for (int s = 0; s < kStageItems; ++s) {
+      const int it = base + s * NT + tid;
+      const bool active = it < items;
+      const int kb = it / (B * 16);
+      const int rem = it - kb * B * 16;
+      const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
+      int64_t kc[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) raw[e] = xf[kc[e]];
-    } else {
-      const unsigned short* xh = static_cast<const unsigned short*>(x);
-      unsigned short u[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) u[e] = xh[kc[e]];
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        raw[e] = xdt == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[e]) << 16)
-                                   : __half2float(__ushort_as_half(u[e]));
-    }
-    if (gain != nullptr) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) gn[e] = gain[kc[e] - b * P.x_stride];
-    }
-    const float rs = G.rstd[b];
-    float lo = 0.f, hi = 0.f;
-    uint32_t h[4];
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int e = 4 * hh + q;
-        float t = raw[e];
-        if (gain != nullptr) t = round_act(t * rs * gn[e], adt);
-        t = (active && kk[e] < K) ? t : 0.f;
-        v[q] = __half2float(__float2half_rn(t));
+      for (int e = 0; e < 8; ++e) {
+        const int hh = e >> 2, q = e & 3;
+        const int64_t kk = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
+        kc[e] = active ? min(kk, K - 1) : 0;
       }
-      lo += v[0] + v[1];
-      hi += v[2] + v[3];
-      const __half2 p01 = __floats2half2_rn(v[0], v[1]), p89 = __floats2half2_rn(v[2], v[3]);
-      h[2 * hh] = *reinterpret_cast<const uint32_t*>(&p01);
-      h[2 * hh + 1] = *reinterpret_cast<const uint32_t*>(&p89);
-    }
-    if (active) G.xs[((kb * 4 + p) * B + b) * 4 + tig] = make_uint4(h[0], h[1], h[2], h[3]);
+      // loads are unconditional (index clamped into the row) so they issue back to back; one
+      // dtype branch around all eight
+      if (xdt == FQ_DT_F32) {
+        const float* xf = static_cast<const float*>(x) + b * P.x_stride;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-      lo += __shfl_xor_sync(0xffffffffu, lo, o);
-      hi += __shfl_xor_sync(0xffffffffu, hi, o);
+        for (int e = 0; e < 8; ++e) raw[s][e] = xf[kc[e]];
+      } else {
+        const unsigned short* xh = static_cast<const unsigned short*>(x) + b * P.x_stride;
+        unsigned short u[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) u[e] = xh[kc[e]];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          raw[s][e] = xdt == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[e]) << 16)
+                                        : __half2float(__ushort_as_half(u[e]));
+      }
+      if (gain != nullptr) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) gn[s][e] = gain[kc[e]];
+      }
     }
-    if (active && (rem & 15) == 0) G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
+    if (base == 0) {
+      if (warp < B) {
+        float r = 1.f;
+        if (gain != nullptr) {
+          float sm = 0.f;
+#pragma unroll
+          for (int j = 0; j < kMaxParts; ++j) sm += pv[j];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+          r = 1.0f / sqrtf(sm / static_cast<float>(P.K) + P.norm_eps);
+        }
+        if (lane == 0) G.rstd[warp] = r;
+      }
+      if (gp) gp[1] = gtimer();
+      named_sync(1, NT);
+      if (gp) gp[2] = gtimer();
+    }
+#pragma unroll
+    for (int s = 0; s < kStageItems; ++s) {
+      const int it = base + s * NT + tid;
+      const bool active = it < items;
+      const int kb = it / (B * 16);
+      const int rem = it - kb * B * 16;
+      const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
+      const float rs = G.rstd[b];
+      float lo = 0.f, hi = 0.f;
+      uint32_t h[4];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = 4 * hh + q;
+          const int64_t kk = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
+          float t = raw[s][e];
+          if (gain != nullptr) t = round_act(t * rs * gn[s][e], adt);
+          t = (active && kk < K) ? t : 0.f;
+          v[q] = __half2float(__float2half_rn(t));
+        }
+        lo += v[0] + v[1];
+        hi += v[2] + v[3];
+        const __half2 p01 = __floats2half2_rn(v[0], v[1]), p89 = __floats2half2_rn(v[2], v[3]);
+        h[2 * hh] = *reinterpret_cast<const uint32_t*>(&p01);
+        h[2 * hh + 1] = *reinterpret_cast<const uint32_t*>(&p89);
+      }
+      if (active) G.xs[(static_cast<size_t>(b) * P.nkb + kb) * 16 + p * 4 + tig] = make_uint4(h[0], h[1], h[2], h[3]);
+      // the 16 lanes of an item group share (kb, b): items are 16-aligned and NT is a multiple of 16
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      if (active && (rem & 15) == 0) G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
+    }
+    if (base + NT * kStageItems >= items) break;
   }
-  named_sync(1, kNCW * 32);
+  named_sync(1, NT);
 }
 
 // NBLK 16x128 blocks on one warp (interleaved: independent MMA chains): 8 MMAs per block over
@@ -450,11 +482,13 @@ __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long
 // (batch rows) that use this copy.  xl: this lane's B-fragment base for the first block (null
 // when its column is past the batch); blocks are kbs apart in the block sequence.
 template <int W, int NBLK>
-__device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, int bstride, const uint4* __restrict__ xl,
-                                            int xstep, int kbstep, const float4* __restrict__ dxa, int dxstep, int lane,
+__device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, const uint4* __restrict__ xl,
+                                            const float4* __restrict__ dxa, int dxstep, int lane,
                                             bool ca, bool cb_, float zmagic, float (&y)[4]) {
   const int g = lane >> 2;
-  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+  // blocks j and j + kNCW of a stage: codes kNCW blocks apart, activations kNCW * 16 uint4s apart
+  constexpr int bstride = (W == 0 ? kBlockBytes8 : kBlockBytes4) * kNCW;
+  constexpr int kXBlk = kNCW * 16;
   float c[NBLK][4];
 #pragma unroll
   for (int n = 0; n < NBLK; ++n)
@@ -466,7 +500,7 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, int
 #pragma unroll
       for (int n = 0; n < NBLK; ++n) {
         const uint4 wv = reinterpret_cast<const uint4*>(blk + n * bstride)[p * 32 + lane];
-        const uint4 xv = xl ? xl[n * kbstep + p * xstep] : z4;
+        const uint4 xv = xl[n * kXBlk + p * 4];
         mma16816(c[n], prmt(wv.x, 0x64646464u, 0x4140u), prmt(wv.x, 0x64646464u, 0x4342u),
                  prmt(wv.y, 0x64646464u, 0x4140u), prmt(wv.y, 0x64646464u, 0x4342u), xv.x, xv.y);
         mma16816(c[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
@@ -479,8 +513,8 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, int
 #pragma unroll
       for (int n = 0; n < NBLK; ++n) {
         const uint4 wv = reinterpret_cast<const uint4*>(blk + n * bstride)[i * 32 + lane];
-        const uint4 x0 = xl ? xl[n * kbstep + (2 * i) * xstep] : z4;
-        const uint4 x1 = xl ? xl[n * kbstep + (2 * i + 1) * xstep] : z4;
+        const uint4 x0 = xl[n * kXBlk + (2 * i) * 4];
+        const uint4 x1 = xl[n * kXBlk + (2 * i + 1) * 4];
         const uint32_t qs[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -757,6 +791,155 @@ __device__ __noinline__ void compute_ctl(const Phase& P, CtlEntry& E) {
   }
 }
 
+// Table-driven producer: the per-phase partition comes from the shared-memory control table the
+// consumers fill at kernel start (CtlEntry), so a stage costs a few integer ops (no divisions, no
+// rung-table or descriptor loads on the issue path).  The tile base pointers of the next GEMV phase
+// are loaded into registers one phase ahead, so a phase switch never waits on global memory.
+struct ProdPhase {
+  const uint8_t* t[2 * kMaxMat];  // [m * 2 + w]
+  int nkb;
+};
+
+__device__ __forceinline__ void prod_load(const Phase& P, ProdPhase& q) {
+#pragma unroll
+  for (int m = 0; m < kMaxMat; ++m)
+#pragma unroll
+    for (int w = 0; w < 2; ++w) q.t[m * 2 + w] = P.mat[m].tiles[w];
+  q.nkb = P.nkb;
+}
+
+__device__ __forceinline__ int next_gemv_phase(const CtlEntry* ctab, int from, int nphases) {
+  for (int p = from; p < nphases; ++p)
+    if (ctab[p].valid && ctab[p].nseg > 0 && ctab[p].g1 > ctab[p].g0) return p;
+  return nphases;
+}
+
+// Second walk of the same stage sequence, `prefetch` stages ahead of the ring: L2 prefetches keep
+// HBM streaming while the ring is full (consumers in a grid barrier, staging, a reduction or a
+// non-GEMV phase), so ring refills hit L2.  Its descriptor loads block, which is fine: it is ahead.
+struct AheadWalk {
+  const Phase* phases;
+  const CtlEntry* ctab;
+  const uint8_t** tab;  // shared [2 * kMaxMat]
+  int nphases, ph, nseg, nkb, tile, seg, kb, left, mw;
+  __device__ void init(const Phase* p, const CtlEntry* c, int n, const uint8_t** t) {
+    phases = p;
+    ctab = c;
+    nphases = n;
+    tab = t;
+    ph = -1;
+    left = 0;
+  }
+  __device__ bool next(const uint8_t*& src, uint32_t& bytes) {
+    if (left == 0) {
+      ph = next_gemv_phase(ctab, ph + 1, nphases);
+      if (ph >= nphases) return false;
+      const Phase& P = phases[ph];
+#pragma unroll
+      for (int m = 0; m < kMaxMat; ++m)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) tab[m * 2 + w] = P.mat[m].tiles[w];
+      nkb = P.nkb;
+      const CtlEntry& E = ctab[ph];
+      nseg = E.nseg;
+      const int bpt = nseg * nkb;
+      tile = E.g0 / bpt;
+      const int rem = E.g0 - tile * bpt;
+      seg = rem / nkb;
+      kb = rem - seg * nkb;
+      left = E.g1 - E.g0;
+      mw = E.segmw[seg];
+    }
+    const int w = mw & 1;
+    const int bb = w == 0 ? kBlockBytes8 : kBlockBytes4;
+    const int nb = min(min(w == 0 ? kStageBlocks8 : kStageBlocks4, nkb - kb), left);
+    src = tab[mw] + (static_cast<int64_t>(tile) * nkb + kb) * bb;
+    bytes = static_cast<uint32_t>(nb * bb);
+    left -= nb;
+    kb += nb;
+    if (kb == nkb) {
+      kb = 0;
+      if (++seg == nseg) {
+        seg = 0;
+        ++tile;
+      }
+      mw = ctab[ph].segmw[seg];
+    }
+    return true;
+  }
+};
+
+__device__ void produce_table(const Phase* phases, int nphases, const CtlEntry* ctab, const Ring R,
+                              unsigned long long* tr, const uint8_t** s_base, bool noload, int prefetch,
+                              const uint8_t** s_base2) {
+  AheadWalk ahead;
+  ahead.init(phases, ctab, nphases, s_base2);
+  bool more_ahead = prefetch > 0;
+  for (int i = 0; i < prefetch && more_ahead; ++i) {
+    const uint8_t* psrc;
+    uint32_t pbytes;
+    if ((more_ahead = ahead.next(psrc, pbytes))) prefetch_l2(psrc, pbytes);
+  }
+  int slot_i = 0, tn = 0;
+
+  uint32_t phase_bit = 0;
+  int ph = next_gemv_phase(ctab, 0, nphases);
+  ProdPhase cur, nxt;
+  if (ph < nphases) prod_load(phases[ph], cur);
+  while (ph < nphases) {
+    const int phn = next_gemv_phase(ctab, ph + 1, nphases);
+    if (phn < nphases) prod_load(phases[phn], nxt);  // in flight while this phase streams
+    const CtlEntry& E = ctab[ph];
+    const int nseg = E.nseg, nkb = cur.nkb;
+#pragma unroll
+    for (int i = 0; i < 2 * kMaxMat; ++i) s_base[i] = cur.t[i];
+    const int bpt = nseg * nkb;
+    int tile = E.g0 / bpt;
+    int rem = E.g0 - tile * bpt;
+    int seg = rem / nkb, kb = rem - seg * nkb;
+    int left = E.g1 - E.g0;
+    int mw = E.segmw[seg];
+    while (left > 0) {
+      const int w = mw & 1;
+      const int bb = w == 0 ? kBlockBytes8 : kBlockBytes4;
+      const int nb = min(min(w == 0 ? kStageBlocks8 : kStageBlocks4, nkb - kb), left);
+      const uint8_t* src = s_base[mw] + (static_cast<int64_t>(tile) * nkb + kb) * bb;
+      if (more_ahead) {
+        const uint8_t* psrc;
+        uint32_t pbytes;
+        if ((more_ahead = ahead.next(psrc, pbytes))) prefetch_l2(psrc, pbytes);
+      }
+      const int s = slot_i;
+      mbar_wait(&R.empty[s], phase_bit ^ 1u);
+      if (tr && tn < kTraceStages) tr[3 * tn] = gtimer();
+      ++tn;
+      if (++slot_i == R.nstages) {
+        slot_i = 0;
+        phase_bit ^= 1u;
+      }
+      const uint32_t bytes = static_cast<uint32_t>(nb * bb);
+      if (noload) {  // profiling: consumer-only timing, the ring keeps whatever it holds
+        mbar_arrive(&R.full[s]);
+      } else {
+        mbar_expect_tx(&R.full[s], bytes);
+        bulk_g2s(R.base + static_cast<size_t>(s) * kStageBytes, src, bytes, &R.full[s]);
+      }
+      left -= nb;
+      kb += nb;
+      if (kb == nkb) {
+        kb = 0;
+        if (++seg == nseg) {
+          seg = 0;
+          ++tile;
+        }
+        mw = E.segmw[seg];
+      }
+    }
+    ph = phn;
+    cur = nxt;
+  }
+}
+
 // Per-phase control block, computed by consumer warp 1 (the lanes evaluate the range starts of
 // this CTA and its followers in parallel) while warp 0 computes the RMSNorm factors.
 __device__ void phase_setup(const Phase& P, PhaseCtl& C, int red_floats, int lane, unsigned long long* gpa,
@@ -851,9 +1034,10 @@ __device__ __forceinline__ void add_into(float (&y)[kMaxMat][4], int m, float (&
 }
 
 __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, PhaseCtl& C, int red_floats,
-                               int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab, unsigned int tag) {
+                               int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab, unsigned int tag,
+                               unsigned long long* gprof) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long* gpa = g_gemv_prof ? g_gemv_prof + (static_cast<size_t>(phase_idx) * gridDim.x + blockIdx.x) * 8 : nullptr;
+  unsigned long long* gpa = gprof ? gprof + (static_cast<size_t>(phase_idx) * gridDim.x + blockIdx.x) * 8 : nullptr;
   unsigned long long* gp = threadIdx.x == 0 ? gpa : nullptr;
   if (warp == 1) {
     phase_setup(P, C, red_floats, lane, gpa, ctab ? ctab + phase_idx : nullptr);  // warp 0: norm factors
@@ -872,9 +1056,8 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     int slot_i = slot_ref;
     uint32_t phase_bit = phase_ref;
     const int g = lane >> 2, tig = lane & 3;
-    const uint4* xl = g < B ? G.xs + static_cast<size_t>(g) * 4 + tig : nullptr;
-    const int xstep = B * 4;            // uint4s between MMA pairs
-    const int kbstep = 4 * B * 4;       // uint4s between blocks
+    // lanes of batch columns past B read column B-1 (valid data; those MMA columns are ignored)
+    const uint4* xl = G.xs + static_cast<size_t>(min(g, B - 1)) * P.nkb * 16 + tig;
     const bool ca0 = 2 * tig < B, cb0 = 2 * tig + 1 < B;
     float y[kMaxMat][4], yc[4];
 #pragma unroll
@@ -918,16 +1101,19 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
 #endif
       const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * kStageBytes;
       const float4* dxa = G.dx + static_cast<size_t>(kb) * B + 2 * tig;
-      for (int j = warp; j < nb; j += 2 * kNCW) {
+#ifndef FQ_SKIP_MMA
+#define FQ_SKIP_MMA 0  // profiling A/B only: consumers release stages without computing
+#endif
+      for (int j = warp; j < (FQ_SKIP_MMA ? 0 : nb); j += 2 * kNCW) {
         const uint8_t* bk = slot + j * bsz;
-        const uint4* xj = xl ? xl + (kb + j) * kbstep : nullptr;
+        const uint4* xj = xl + (kb + j) * 16;
         const float4* dj = dxa + j * B;
         if (j + kNCW < nb) {
-          if (w == 0) gemv_blocks<0, 2>(bk, kNCW * bsz, xj, xstep, kNCW * kbstep, dj, kNCW * B, lane, ca, cb, zm, yc);
-          else gemv_blocks<1, 2>(bk, kNCW * bsz, xj, xstep, kNCW * kbstep, dj, kNCW * B, lane, ca, cb, zm, yc);
+          if (w == 0) gemv_blocks<0, 2>(bk, xj, dj, kNCW * B, lane, ca, cb, zm, yc);
+          else gemv_blocks<1, 2>(bk, xj, dj, kNCW * B, lane, ca, cb, zm, yc);
         } else {
-          if (w == 0) gemv_blocks<0, 1>(bk, 0, xj, xstep, 0, dj, 0, lane, ca, cb, zm, yc);
-          else gemv_blocks<1, 1>(bk, 0, xj, xstep, 0, dj, 0, lane, ca, cb, zm, yc);
+          if (w == 0) gemv_blocks<0, 1>(bk, xj, dj, 0, lane, ca, cb, zm, yc);
+          else gemv_blocks<1, 1>(bk, xj, dj, 0, lane, ca, cb, zm, yc);
         }
       }
       __syncwarp();
@@ -1374,10 +1560,15 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  __shared__ const uint8_t* s_pbase[2][2 * kMaxMat];
   if (warp == kNCW) {
-    // the weight stream depends on nothing produced at run time: start immediately
-    if (lane == 0) {
-      unsigned long long* tr = blockIdx.x == static_cast<unsigned>(g_trace_cta) ? g_ring_trace : nullptr;
+    unsigned long long* tr = blockIdx.x == static_cast<unsigned>(g_trace_cta) ? g_ring_trace : nullptr;
+    if (ctab != nullptr) {
+      // the weight stream depends on nothing produced at run time, only on the partition table
+      // the consumers compute first (named barrier 2)
+      named_sync(2, kThreads);
+      if (lane == 0) produce_table(phases, nphases, ctab, R, tr, s_pbase[0], L.prefetch < 0, L.prefetch, s_pbase[1]);
+    } else if (lane == 0) {
       produce_all(phases, nphases, R, tr, L.prefetch);
     }
     return;
@@ -1389,11 +1580,14 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   uint32_t phase_bit = 0;
   unsigned int epoch = 0;
   unsigned long long* prof = threadIdx.x == 0 ? g_phase_prof : nullptr;
+  unsigned long long* const gprof = g_gemv_prof;  // read once: a per-phase load would sit on the critical path
   if (prof) prof[static_cast<size_t>(nphases) * gridDim.x * 2 + blockIdx.x] = gtimer();
   // Phase descriptors live in shared memory: warp 0 loads descriptor i+1 into registers during
   // phase i (one 16-byte load per lane, latency hidden by the phase) and stores it at the end.
-  if (ctab)
+  if (ctab) {
     for (int t = threadIdx.x; t < nphases; t += kNCW * 32) compute_ctl(phases[t], ctab[t]);
+    asm volatile("bar.arrive 2, %0;" ::"r"(kThreads) : "memory");  // table ready: producer starts
+  }
   constexpr int kPW = static_cast<int>(sizeof(Phase) / 16);
   uint4 next_desc = make_uint4(0u, 0u, 0u, 0u);
   if (warp == 0) {
@@ -1403,7 +1597,7 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   named_sync(1, kNCW * 32);
   for (int i = 0; i < nphases; ++i) {
     const Phase& P = pbuf[i & 1];
-    if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i);
+    if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i, gprof);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
     else if (P.type == PH_ATTN) run_attn(P, attn_smem);
     else if (P.type == PH_APPEND) run_append(P);
