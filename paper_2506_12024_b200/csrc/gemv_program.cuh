@@ -80,6 +80,9 @@ struct alignas(16) Phase {
   int64_t slot_stride, layer_off, max_seq;
   int n_heads, head_dim;
   int appended;           // ATTN: the rows' keys / values are already in the cache (prefill)
+  int attn_splits;        // ATTN: CTAs per (row, head), each over a contiguous chunk range; > 1:
+                          // unnormalised partials (O[hd], m, l) in attn_ws, merged by the next
+                          // GEMV phase's staging (the O projection reads them as its input)
   const float2* rope_cs;  // [max_seq][head_dim / 2] (cos, sin) of pos * theta^(-2i/hd)
   float* attn_ws;
   unsigned int* tickets;

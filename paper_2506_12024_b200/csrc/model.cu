@@ -424,6 +424,14 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         pb.add(e);
       }
       int cur = 0;
+      // attention work items: (row, head, split); with few rows the keys of a head are split over
+      // up to kMaxAttnSplit CTAs and the O projection's staging merges the partials
+      // (measured: the merge costs the O projection's staging more than the split saves; off by
+      // default, FQ_ATTN_SPLITS=n to experiment)
+      const char* se = std::getenv("FQ_ATTN_SPLITS");
+      const int kMaxAttnSplit = se ? std::max(1, std::min(4, std::atoi(se))) : 1;
+      const int attn_splits = gemv_only ? 1
+          : std::max(1, std::min(std::min(kMaxAttnSplit, M->n_chunks), G / std::max(1, B * static_cast<int>(c.n_heads))));
       for (int64_t l = 0; l < c.n_layers; ++l) {
         GemvLaunch g;
         g.nmat = 3;
@@ -489,6 +497,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
           a.attn_ws = M->attn_ws;
           a.tickets = M->tickets;
           a.attn_out = M->attn;
+          a.attn_splits = attn_splits;
           pb.add(a);
         }
         GemvLaunch o;
@@ -504,7 +513,16 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         o.resid_stride = d;
         o.out_partials = M->partials[cur ^ 1];
         o.out_n_partials = kPartStride;
+        const size_t o_first = pb.phases.size();
         add_chunked(pb, o, B);
+        if (attn_splits > 1) {
+          if (pb.phases.size() != o_first + 1) fail(FQ_E_STATE, "split attention needs one O-projection phase");
+          Phase& op = pb.phases.back();
+          op.attn_splits = attn_splits;
+          op.attn_ws = M->attn_ws;
+          op.n_heads = static_cast<int>(c.n_heads);
+          op.head_dim = static_cast<int>(c.head_dim);
+        }
         cur ^= 1;
         GemvLaunch gu;
         gu.nmat = 2;

@@ -362,7 +362,116 @@ struct GemvSmem {
 constexpr int kStageItems = 2;  // items per thread per batch (loads in flight together)
 static_assert(kMaxB <= kNCW, "one consumer warp per batch row computes its RMSNorm factor");
 
+// Staging of the O projection's input when the attention phase ran split (attn_splits > 1): the
+// splits' unnormalised partials are merged here, x = sum_s O_s e^(m_s - M) / sum_s l_s e^(m_s - M),
+// rounded to the activation dtype exactly as the unsplit attention rounds its output.  All loads
+// (every split's O values of this thread's items and the (m, l) pairs) go out together.
+constexpr int kMaxAttnSplits = 4;
+__device__ __forceinline__ void stage_attn_merge(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+  const int B = P.B;
+  const int tid = threadIdx.x;
+  constexpr int NT = kNCW * 32;
+  const int H = P.n_heads, hd = P.head_dim, ns = P.attn_splits;
+  const int64_t pst = hd + 4;
+  const float* parts = P.attn_ws;
+  float* wsm = G.red;  // [b * H + h][ns] merge weights (the reduction window is free while staging)
+  const int items = P.nkb * B * 16;
+  const int64_t K = P.K;
+  const int adt = P.act_dtype;
+  for (int base = 0;; base += NT * kStageItems) {
+    float raw[kStageItems][kMaxAttnSplits][8];
+#pragma unroll
+    for (int s = 0; s < kStageItems; ++s) {
+      const int it = base + s * NT + tid;
+      const bool active = it < items;
+      const int kb = it / (B * 16);
+      const int rem = it - kb * B * 16;
+      const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int hh = e >> 2, q = e & 3;
+        int64_t kk = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
+        kk = active ? min(kk, K - 1) : 0;
+        const int h = static_cast<int>(kk / hd), j = static_cast<int>(kk - static_cast<int64_t>(h) * hd);
+        const float* src = parts + (static_cast<int64_t>(b) * H + h) * ns * pst + j;
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp) raw[s][sp][e] = sp < ns ? src[sp * pst] : 0.f;
+      }
+    }
+    if (base == 0) {
+      for (int bh = tid; bh < B * H; bh += NT) {
+        const float* src = parts + static_cast<int64_t>(bh) * ns * pst + hd;
+        float2 ml[kMaxAttnSplits];
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+          ml[sp] = sp < ns ? *reinterpret_cast<const float2*>(src + sp * pst) : make_float2(-INFINITY, 0.f);
+        float M = -INFINITY;
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp) M = fmaxf(M, ml[sp].x);
+        float Lt = 0.f, f[kMaxAttnSplits];
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp) {
+          f[sp] = ml[sp].x == -INFINITY ? 0.f : expf(ml[sp].x - M);
+          Lt += ml[sp].y * f[sp];
+        }
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+          if (sp < ns) wsm[bh * ns + sp] = f[sp] / Lt;
+      }
+      if (gp) gp[1] = gtimer();
+      named_sync(1, NT);
+      if (gp) gp[2] = gtimer();
+    }
+#pragma unroll
+    for (int s = 0; s < kStageItems; ++s) {
+      const int it = base + s * NT + tid;
+      const bool active = it < items;
+      const int kb = it / (B * 16);
+      const int rem = it - kb * B * 16;
+      const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
+      float lo = 0.f, hi = 0.f;
+      uint32_t hq[4];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = 4 * hh + q;
+          const int64_t kk = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
+          const int h = static_cast<int>(min(kk, K - 1) / hd);
+          const float* w = wsm + (b * H + h) * ns;
+          float t = 0.f;
+#pragma unroll
+          for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+            if (sp < ns) t += raw[s][sp][e] * w[sp];
+          t = round_act(t, adt);
+          t = (active && kk < K) ? t : 0.f;
+          v[q] = __half2float(__float2half_rn(t));
+        }
+        lo += v[0] + v[1];
+        hi += v[2] + v[3];
+        const __half2 p01 = __floats2half2_rn(v[0], v[1]), p89 = __floats2half2_rn(v[2], v[3]);
+        hq[2 * hh] = *reinterpret_cast<const uint32_t*>(&p01);
+        hq[2 * hh + 1] = *reinterpret_cast<const uint32_t*>(&p89);
+      }
+      if (active) G.xs[(static_cast<size_t>(b) * P.nkb + kb) * 16 + p * 4 + tig] = make_uint4(hq[0], hq[1], hq[2], hq[3]);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      if (active && (rem & 15) == 0) G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
+    }
+    if (base + NT * kStageItems >= items) break;
+  }
+  named_sync(1, NT);
+}
+
 __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+  if (P.attn_splits > 1) {
+    stage_attn_merge(P, G, gp);
+    return;
+  }
   const int B = P.B;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = kNCW * 32;
@@ -1261,32 +1370,48 @@ __device__ __forceinline__ void load_lane(const void* src, int dtype, int64_t of
     x[e] = dtype == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[e]) << 16) : __half2float(__ushort_as_half(u[e]));
 }
 
-// One 16-key chunk of head (b, h) on one warp: returns the chunk's max score, exp-sum and the
-// unnormalised P.V slice of this lane (dims DPL*lane ...).  The chunk holding the row's own
-// position writes the RoPE'd key / value to the cache first (decode; prefill appended them in a
-// phase of its own).
+// One 16-key chunk of head (b, h) on one warp, in two parts so the K/V loads of a warp's first
+// chunk go out before its query is loaded and rotated (one round trip for both).
 template <int DPL>
-__device__ __forceinline__ void attn_chunk(const Phase& P, int b, int h, int chunk, const float (&q)[DPL], int lane,
-                                           float& mx, float& l, float (&o)[DPL]) {
+struct AttnRaw {
+  using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
+  Raw kr[kAttnChunk], vr[kAttnChunk];
+};
+
+template <int DPL>
+__device__ __forceinline__ void attn_load(const Phase& P, int b, int h, int chunk, int lane, AttnRaw<DPL>& R) {
+  constexpr int hd = DPL * 32;
+  using Raw = typename AttnRaw<DPL>::Raw;
+  const int H = P.n_heads;
+  const __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+  const __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
+  const int j0 = chunk * kAttnChunk;
+  const int last_row = static_cast<int>(P.max_seq) - 1;
+#pragma unroll
+  for (int t = 0; t < kAttnChunk; ++t) {
+    const int64_t row = static_cast<int64_t>(min(j0 + t, last_row)) * hd + DPL * lane;
+    R.kr[t] = *reinterpret_cast<const Raw*>(kc + row);
+    R.vr[t] = *reinterpret_cast<const Raw*>(vc + row);
+  }
+}
+
+// Returns the chunk's max score, exp-sum and the unnormalised P.V slice of this lane (dims
+// DPL*lane ...).  The chunk holding the row's own position writes the RoPE'd key / value to the
+// cache first (decode; prefill appended them in a phase of its own).
+template <int DPL>
+__device__ __forceinline__ void attn_compute(const Phase& P, int b, int h, int chunk, const float (&q)[DPL], int lane,
+                                             AttnRaw<DPL>& R, float& mx, float& l, float (&o)[DPL]) {
   constexpr int hd = DPL * 32;
   constexpr int CH = kAttnChunk;  // 16 keys
+  using Raw = typename AttnRaw<DPL>::Raw;
   const int H = P.n_heads;
   const int pos = P.pos[b];
   const int j0 = chunk * CH;
   const int nk = min(CH, pos + 1 - j0);
-  __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
-  __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
-  using Raw = typename std::conditional<DPL == 4, uint2, uint32_t>::type;
   const bool owns_new = !P.appended && pos >= j0 && pos < j0 + CH;
-  const int last_row = static_cast<int>(P.max_seq) - 1;
-  Raw kr[CH], vr[CH];
-#pragma unroll
-  for (int t = 0; t < CH; ++t) {
-    const int64_t row = static_cast<int64_t>(min(j0 + t, last_row)) * hd + DPL * lane;
-    kr[t] = *reinterpret_cast<const Raw*>(kc + row);
-    vr[t] = *reinterpret_cast<const Raw*>(vc + row);
-  }
   if (owns_new) {
+    __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+    __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
     const int64_t off = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
     float kn[DPL], vn[DPL];
     load_lane<DPL>(P.k, P.act_dtype, off, kn);
@@ -1305,8 +1430,8 @@ __device__ __forceinline__ void attn_chunk(const Phase& P, int b, int h, int chu
 #pragma unroll
     for (int t = 0; t < CH; ++t)
       if (j0 + t == pos) {
-        kr[t] = kw;
-        vr[t] = vw;
+        R.kr[t] = kw;
+        R.vr[t] = vw;
       }
   }
   // per-lane partial dots, then a transposing butterfly over lane bits 4..1: lanes l and l^1 end
@@ -1314,7 +1439,7 @@ __device__ __forceinline__ void attn_chunk(const Phase& P, int b, int h, int chu
   float part[CH];
 #pragma unroll
   for (int t = 0; t < CH; ++t) {
-    const __half2* hp = reinterpret_cast<const __half2*>(&kr[t]);
+    const __half2* hp = reinterpret_cast<const __half2*>(&R.kr[t]);
     float acc = 0.f;
 #pragma unroll
     for (int e = 0; e < DPL / 2; ++e) {
@@ -1353,7 +1478,7 @@ __device__ __forceinline__ void attn_chunk(const Phase& P, int b, int h, int chu
   for (int t = 0; t < CH; ++t) {
     const int owner = ((t >> 3) & 1) << 4 | ((t >> 2) & 1) << 3 | ((t >> 1) & 1) << 2 | (t & 1) << 1;
     const float pj = __shfl_sync(0xffffffffu, p, owner);
-    const __half2* hp = reinterpret_cast<const __half2*>(&vr[t]);
+    const __half2* hp = reinterpret_cast<const __half2*>(&R.vr[t]);
 #pragma unroll
     for (int e = 0; e < DPL / 2; ++e) {
       const float2 f = __half22float2(hp[e]);
@@ -1363,28 +1488,36 @@ __device__ __forceinline__ void attn_chunk(const Phase& P, int b, int h, int chu
   }
 }
 
-// Attention of one (row, head) on one CTA: warp w takes chunks w, w + 8, ... with an online
-// softmax across its chunks; the eight warp states merge in shared memory (fixed order, no
-// global workspace, no atomics).
+// Attention of one (row, head) over split sp of ns contiguous chunk ranges on one CTA: warp w
+// takes chunks c0 + w, c0 + w + 8, ... with an online softmax across its chunks; the eight warp
+// states merge in shared memory (fixed order, no atomics).  ns == 1: the normalised output goes to
+// attn_out; ns > 1: the CTA's unnormalised partial (O[hd], m, l) goes to attn_ws and the next GEMV
+// phase (the O projection) merges the splits while staging its input.
 template <int DPL>
-__device__ void attn_head(const Phase& P, int b, int h, int lane, int warp, AttnSmem& S) {
+__device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane, int warp, AttnSmem& S) {
   constexpr int hd = DPL * 32;
   const int H = P.n_heads;
   const int pos = P.pos[b];
   const int nch = (pos + kAttnChunk) / kAttnChunk;
+  const int c0 = (nch * sp) / ns, c1 = (nch * (sp + 1)) / ns;
   const int64_t qoff = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
   float q[DPL];
-  load_lane<DPL>(P.q, P.act_dtype, qoff, q);
-  rope_lane<DPL>(q, P.rope_cs + static_cast<int64_t>(pos) * (hd / 2), lane);
-  const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-#pragma unroll
-  for (int e = 0; e < DPL; ++e) q[e] *= scale;
   float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) O[e] = 0.f;
-  for (int c = warp; c < nch; c += kNCW) {
+  for (int c = c0 + warp; c < c1; c += kNCW) {
+    AttnRaw<DPL> R;
+    attn_load<DPL>(P, b, h, c, lane, R);
+    if (c == c0 + warp) {
+      // first chunk: the query loads go out behind its K/V loads (one round trip for both)
+      load_lane<DPL>(P.q, P.act_dtype, qoff, q);
+      rope_lane<DPL>(q, P.rope_cs + static_cast<int64_t>(pos) * (hd / 2), lane);
+      const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) q[e] *= scale;
+    }
     float mx, l, o[DPL];
-    attn_chunk<DPL>(P, b, h, c, q, lane, mx, l, o);
+    attn_compute<DPL>(P, b, h, c, q, lane, R, mx, l, o);
     const float Mn = fmaxf(M, mx);
     const float fa = M == -INFINITY ? 0.f : expf(M - Mn), fb = expf(mx - Mn);
     L = L * fa + l * fb;
@@ -1413,8 +1546,15 @@ __device__ void attn_head(const Phase& P, int b, int h, int lane, int warp, Attn
 #pragma unroll
       for (int e = 0; e < DPL; ++e) Ot[e] += S.o[w][DPL * lane + e] * f;
     }
+    if (ns == 1) {
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) store_out(P.attn_out, P.act_dtype, qoff + e, Ot[e] / Lt);
+      for (int e = 0; e < DPL; ++e) store_out(P.attn_out, P.act_dtype, qoff + e, Ot[e] / Lt);
+    } else {
+      float* part = P.attn_ws + ((static_cast<int64_t>(b) * H + h) * ns + sp) * (hd + 4);
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) part[DPL * lane + e] = Ot[e];
+      if (lane == 0) *reinterpret_cast<float2*>(part + hd) = make_float2(Mt, Lt);
+    }
   }
   named_sync(1, kNCW * 32);
 }
@@ -1452,11 +1592,13 @@ __device__ __noinline__ void run_append(const Phase& P) {
 
 __device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // one (row, head) per CTA at a time, spread over the grid
-  for (int item = blockIdx.x; item < P.B * P.n_heads; item += gridDim.x) {
-    const int b = item / P.n_heads, h = item - b * P.n_heads;
-    if (P.head_dim == 128) attn_head<4>(P, b, h, lane, warp, S);
-    else attn_head<2>(P, b, h, lane, warp, S);
+  // one (row, head, split) per CTA at a time, spread over the grid
+  const int ns = max(1, P.attn_splits);
+  for (int item = blockIdx.x; item < P.B * P.n_heads * ns; item += gridDim.x) {
+    const int bh = item / ns, sp = item - bh * ns;
+    const int b = bh / P.n_heads, h = bh - b * P.n_heads;
+    if (P.head_dim == 128) attn_head<4>(P, b, h, sp, ns, lane, warp, S);
+    else attn_head<2>(P, b, h, sp, ns, lane, warp, S);
   }
 }
 
@@ -1495,17 +1637,35 @@ __device__ __noinline__ void run_stats(const Phase& P) {
 
 // ---------------------------------------------------------------- grid barrier (consumers)
 // Grid barrier (consumer threads): arrival counter in global memory, reset before every launch.
+// Arrival is one release reduction (no returned value to wait for); the poll is relaxed (an
+// acquire load per iteration would invalidate L1 each time) and one acquire fence follows it.
+#ifndef FQ_OLD_BARRIER
+#define FQ_OLD_BARRIER 0
+#endif
+__device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
   named_sync(1, kNCW * 32);
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(counter, 1u);
     const unsigned int target = (++epoch) * gridDim.x;
     const unsigned long long t0 = gtimer_now();
-    while (ld_acquire(counter) < target) {
-      if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_acquire(counter)));
+    if (FQ_OLD_BARRIER) {
+      __threadfence();
+      atomicAdd(counter, 1u);
+      while (ld_acquire(counter) < target) {
+        if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_acquire(counter)));
+      }
+      __threadfence();
+    } else {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+      for (uint32_t spins = 0; ld_relaxed(counter) < target; ++spins)
+        if ((spins & 255u) == 255u && gtimer_now() - t0 > kWatchdogNs)
+          watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_relaxed(counter)));
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
-    __threadfence();
   } else {
     ++epoch;
   }

@@ -153,8 +153,17 @@ void run(const char* name) {
   float* out; long long* cyc; cudaMalloc(&out, 1 << 20); cudaMalloc(&cyc, 8);
   const int reps = 2000, smem = 60000;
   cudaFuncSetAttribute(k<W, V, VOL, RING, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k<W, V, VOL, RING, NB><<<148, 288, smem>>>(out, reps, cyc);  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
   k<W, V, VOL, RING, NB><<<148, 288, smem>>>(out, reps, cyc);
+  cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("  [%s] %.2f ns per block per SM (wall), ", name, ms * 1e6 / (reps * (W == 0 ? 16 : 32)));
   long long h; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
   const int nb = W == 0 ? 16 : 32;
   printf("%-28s %s: %.1f cycles per block per SM (%.1f codes/cycle/SM)\n", name, cudaGetErrorString(e), double(h) / (reps * nb),
