@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <type_traits>
 #ifndef FQ_DBG
 #define FQ_DBG 0
@@ -467,9 +468,140 @@ __device__ __forceinline__ void stage_attn_merge(const Phase& P, const GemvSmem&
   named_sync(1, NT);
 }
 
+// Vectorised staging (16-byte loads of 8 consecutive activations): one load per 8 values (two
+// for fp32 inputs / gains), every load of the phase in flight together when they fit VB vectors
+// per thread (K = 11008 at B = 1: 6), so the phase pays one round trip.  Vector v covers
+// k = kb*128 + 8c .. +7 of batch row b (v = (b*nkb + kb)*16 + c); its pairs (k, k+1) land in
+// fragment slot xs[(b*nkb + kb)*16 + (c>>2)*4 + i].comp[c&3] for pair i (the m16n8k16 B layout:
+// k16 = c>>1 -> (p, hh) = (c>>2, (c>>1)&1), half c&1, thread-in-group i).
+template <int VB, bool F32, bool norm>
+__device__ __forceinline__ void stage_vec(const Phase& P, const GemvSmem& G, unsigned long long* gp, const float (&pv)[8]) {
+  const int B = P.B;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = kNCW * 32;
+  const float* gain = P.norm_gain;
+  const int nkb = P.nkb;
+  const int nvec = B * nkb * 16;
+  const int64_t K = P.K;
+  const int adt = P.act_dtype;
+  for (int base = 0;; base += NT * VB) {
+    uint4 raw[VB][F32 ? 2 : 1];
+    float4 gv[VB][norm ? 2 : 1];
+#pragma unroll
+    for (int s = 0; s < VB; ++s) {
+      const int v = base + s * NT + tid;
+      const int b = v / (nkb * 16), r = v - b * nkb * 16;
+      const int64_t k0 = static_cast<int64_t>(r >> 4) * kBlockK + (r & 15) * 8;
+      const bool on = v < nvec && k0 < K;
+      const int64_t off = on ? b * P.x_stride + k0 : 0;
+      if (F32) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const float*>(P.x) + off);
+        raw[s][0] = src[0];
+        raw[s][1] = src[1];
+      } else {
+        raw[s][0] = *reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(P.x) + off);
+      }
+      if (norm) {
+        const float4* g4 = reinterpret_cast<const float4*>(gain + (on ? k0 : 0));
+        gv[s][0] = g4[0];
+        gv[s][1] = g4[1];
+      }
+    }
+    if (base == 0) {
+      if (warp < B) {
+        float r = 1.f;
+        if (norm) {
+          float sm = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sm += pv[j];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+          r = 1.0f / sqrtf(sm / static_cast<float>(P.K) + P.norm_eps);
+        }
+        if (lane == 0) G.rstd[warp] = r;
+      }
+      if (gp) gp[1] = gtimer();
+      named_sync(1, NT);
+      if (gp) gp[2] = gtimer();
+    }
+#pragma unroll
+    for (int s = 0; s < VB; ++s) {
+      const int v = base + s * NT + tid;
+      const int b = v / (nkb * 16), r = v - b * nkb * 16;
+      const int kb = r >> 4, c = r & 15;
+      const int64_t k0 = static_cast<int64_t>(kb) * kBlockK + c * 8;
+      const bool on = v < nvec && k0 < K;
+      float x[8];
+      if (F32) {
+        const float* f = reinterpret_cast<const float*>(&raw[s][0]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = f[i];
+      } else {
+        const unsigned short* u = reinterpret_cast<const unsigned short*>(&raw[s][0]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          x[i] = P.x_dtype == FQ_DT_BF16 ? __uint_as_float(static_cast<uint32_t>(u[i]) << 16)
+                                         : __half2float(__ushort_as_half(u[i]));
+      }
+      const float rs = G.rstd[on ? b : 0];
+      const float* g8 = norm ? reinterpret_cast<const float*>(&gv[s][0]) : nullptr;
+      float sum = 0.f;
+      uint32_t hp[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float a = x[2 * i], bq = x[2 * i + 1];
+        if (norm) {
+          a = round_act(a * rs * g8[2 * i], adt);
+          bq = round_act(bq * rs * g8[2 * i + 1], adt);
+        }
+        a = on ? __half2float(__float2half_rn(a)) : 0.f;
+        bq = on ? __half2float(__float2half_rn(bq)) : 0.f;
+        sum += a + bq;
+        const __half2 h2 = __floats2half2_rn(a, bq);
+        hp[i] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+      if (v < nvec) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(G.xs + (static_cast<size_t>(b) * nkb + kb) * 16 + (c >> 2) * 4) + (c & 3);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[4 * i] = hp[i];
+      }
+      // the 16 vectors of a block sit on 16 consecutive lanes (v is 16-aligned per half-warp)
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (v < nvec && c == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
+    }
+    if (base + NT * VB >= nvec) break;
+  }
+  named_sync(1, NT);
+}
+
+__device__ __forceinline__ bool stage_vec_ok(const Phase& P) {
+  const size_t es = P.x_dtype == FQ_DT_F32 ? 4 : 2;
+  return (reinterpret_cast<uintptr_t>(P.x) & 15) == 0 && ((P.x_stride * es) & 15) == 0 && (P.K & 7) == 0 &&
+         (P.norm_gain == nullptr || (reinterpret_cast<uintptr_t>(P.norm_gain) & 15) == 0);
+}
+
+#ifndef FQ_VEC_STAGE
+#define FQ_VEC_STAGE 0  // measured 2.5% slower per step (code size), kept for A/B
+#endif
 __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
   if (P.attn_splits > 1) {
     stage_attn_merge(P, G, gp);
+    return;
+  }
+  const bool vnorm = P.norm_gain != nullptr;
+  if (FQ_VEC_STAGE && stage_vec_ok(P) && vnorm == (P.x_dtype == FQ_DT_F32)) {
+    const bool norm = vnorm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float pv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = lane + 32 * j;
+      pv[j] = (norm && warp < P.B && i < P.n_partials) ? P.norm_partials[warp * P.partials_stride + i] : 0.f;
+    }
+    // the two shapes of the decode step: fp32 residual + RMSNorm, bf16/fp16 activations
+    if (norm) stage_vec<4, true, true>(P, G, gp, pv);
+    else stage_vec<6, false, false>(P, G, gp, pv);
     return;
   }
   const int B = P.B;
@@ -853,12 +985,13 @@ __device__ __forceinline__ int64_t cta_start_or_end(const Phase& P, const Segs& 
 
 // Compact per-phase partition of this CTA, computed for every phase of the program at kernel
 // start (one consumer thread per phase, in parallel) so no phase pays for it on its critical path.
+constexpr int kCtlFollow = FQ_TILE_PART ? 1 : 4;
 struct alignas(16) CtlEntry {
   int g0, g1, tile0;
   short ntiles;
-  uint8_t nseg, head_shared, nfollow, valid;  // nfollow 0xFF: more than 4, recompute
+  uint8_t nseg, head_shared, nfollow, valid;  // nfollow 0xFF: more than kCtlFollow, recompute
   uint8_t segmw[2 * kMaxMat], mask[2 * kMaxMat];
-  short follow[4];
+  short follow[kCtlFollow];  // whole-tile partition: never used (kept 32 bytes per entry)
 };
 
 __device__ __noinline__ void compute_ctl(const Phase& P, CtlEntry& E) {
@@ -892,7 +1025,7 @@ __device__ __noinline__ void compute_ctl(const Phase& P, CtlEntry& E) {
     for (int c = blockIdx.x + 1; c < static_cast<int>(gridDim.x) && cs < t1; ++c) {
       const int64_t cn = cta_start(P, S, c + 1);
       if (cn > cs) {
-        if (E.nfollow < 4) E.follow[E.nfollow++] = static_cast<short>(c);
+        if (E.nfollow < kCtlFollow) E.follow[E.nfollow++] = static_cast<short>(c);
         else { E.nfollow = 0xFF; break; }
       }
       cs = cn;
@@ -1809,13 +1942,16 @@ int max_dynamic_smem() {
   return v;
 }
 
-constexpr int kMaxCtlPhases = 512;  // longer programs compute their partitions per phase
+constexpr int kMaxCtlPhases = 512;
+static_assert(sizeof(CtlEntry) == 32 || !FQ_TILE_PART, "partition table entry grew: it costs ring stages");  // longer programs compute their partitions per phase
 
 SmemLayout layout_for(int64_t kpad, int bb, int nphases, int& nstages_out, size_t& total_out, int64_t xs_bytes = -1) {
   SmemLayout L{};
   L.xs_bytes = static_cast<int>(xs_bytes >= 0 ? xs_bytes : kpad * 2 * bb);
   L.dx_bytes = static_cast<int>(L.xs_bytes / 256 * 16);  // one float4 per (block, row)
-  L.red_bytes = std::max(16 * 1024, 2 * kMaxMat * kNCW * 16 * bb * 4);
+  // >= 8 KB: the fused softmax statistics use it as kNCW * 32 StatPart scratch; every byte saved
+  // here goes to the weight ring (a 5th stage at the 7B shape)
+  L.red_bytes = std::max(kNCW * 32 * 32, 2 * kMaxMat * kNCW * 16 * bb * 4);
   L.ctl_phases = nphases <= kMaxCtlPhases ? nphases : 0;
   const int fixed = 2 * kMaxStages * 8 + L.xs_bytes + L.dx_bytes + L.red_bytes + kNCW * 32 * 4 + kMaxB * 4 +
                     kMaxMat * 16 * kMaxB * 4 + L.ctl_phases * static_cast<int>(sizeof(CtlEntry));
@@ -1849,6 +1985,9 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   const SmemLayout L = layout_for(pb.max_kpad, pb.max_bb, r.nphases, ns, tot, std::max<int64_t>(pb.max_xs, 256));
   if (ns < 2) fail(FQ_E_CONFIG, "gemv: activations of this width do not fit in shared memory");
   r.nstages = ns;
+  if (std::getenv("FQ_DEBUG_LAYOUT"))
+    std::fprintf(stderr, "fq program: %d phases, ring %d x %d B, xs %d, red %d, ctl %d, smem %zu B\n", r.nphases, ns,
+                 kStageBytes, L.xs_bytes, L.red_bytes, L.ctl_phases, tot);
   r.smem = tot;
   r.xs_bytes = L.xs_bytes;
   r.dx_bytes = L.dx_bytes;
