@@ -162,6 +162,8 @@ struct GemvLaunch {
   int out_n_partials = 0;
   bool pdl = false;            // launch with programmatic stream serialization
   void* stat_part = nullptr;   // EPI_STORE: fused softmax partials [batch][grid] (StatPart)
+  const void* xfrag = nullptr; // input in B-fragment order (see Phase::xfrag), or null
+  void* yfrag = nullptr;       // EPI_SWIGLU: also write the output in B-fragment order
 };
 
 bool gemv_fast_supported(const fq_layer* L, int rung);

@@ -103,6 +103,9 @@ void ProgramBuilder::add_gemv(const GemvLaunch& g, int64_t b0, int bb) {
   P.out_partials = g.out_partials ? g.out_partials + b0 * g.out_n_partials : nullptr;
   P.out_partials_stride = g.out_n_partials;
   P.stat_part = g.stat_part ? static_cast<char*>(g.stat_part) + b0 * grid * 32 : nullptr;  // sizeof(StatPart)
+  P.xfrag = g.xfrag ? static_cast<const uint4*>(g.xfrag) + b0 * P.nkb * 16 : nullptr;
+  P.yfrag_nkb = static_cast<int>(ceil_div_i(P.N, kBlockK));
+  P.yfrag = g.yfrag ? static_cast<__half*>(g.yfrag) + b0 * P.yfrag_nkb * 128 : nullptr;
   if (g.nmat < 1 || g.nmat > kMaxMat) fail(FQ_E_CONFIG, "multi-gemv: 1..3 matrices");
   if (bb < 1 || bb > kMaxB) fail(FQ_E_CONFIG, "gemv: batch chunk out of range");
   if (static_cast<double>(P.n_tiles) * P.nkb * (kBlockBytes8 + kBlockBytes4) * g.nmat >= 4294967296.0)

@@ -9,6 +9,11 @@
 
 namespace fqc {
 
+// Split attention with the O projection's staging merging the partials (measured slower than
+// one CTA per (row, head) at the 7B shape; compiled out by default: its code costs i-cache)
+#ifndef FQ_ATTN_MERGE
+#define FQ_ATTN_MERGE 0
+#endif
 constexpr int kMaxB = 8;          // batch rows per GEMV phase (the MMA's n = 8 columns)
 constexpr int kMaxMat = 3;        // matrices sharing one input (QKV)
 constexpr int kMaxStages = 8;
@@ -65,8 +70,11 @@ struct alignas(16) Phase {
   int out_partials_stride;
   void* stat_part;        // GEMV: per-(row, CTA) softmax partials of the stored outputs (fused
                           // entropy, head only); STATS: their input [B][grid]
+  const uint4* xfrag;     // GEMV: input already in B-fragment order (fp16, batch-major, the smem
+                          // xs layout) written by the producing phase's epilogue: staging is a copy
+  __half* yfrag;          // GEMV (SwiGLU epilogue) / ATTN: also write the output in that order
+  int yfrag_nkb;          // 128-blocks per batch row of yfrag
   float* fix;             // stream-K fix-up partials [grid][kMaxMat * 16 * kMaxB]
-  unsigned int* flags;    // [grid] set by a CTA that finished the head of a shared tile
   // ---- EMBED / ATTN / STATS (decode step)
   const float* tok_emb;
   const int32_t* tokens;
@@ -85,7 +93,6 @@ struct alignas(16) Phase {
                           // GEMV phase's staging (the O projection reads them as its input)
   const float2* rope_cs;  // [max_seq][head_dim / 2] (cos, sin) of pos * theta^(-2i/hd)
   float* attn_ws;
-  unsigned int* tickets;
   void* attn_out;
   fq_row_stats* stats;
 };

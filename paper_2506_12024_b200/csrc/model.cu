@@ -307,6 +307,8 @@ struct fq_model {
   void* v = nullptr;
   void* attn = nullptr;        // [B, d]
   void* mid = nullptr;         // [B, ffn]
+  void* attn_frag = nullptr;   // [B][d/128][16] uint4: attention output in B-fragment order (fp16)
+  void* mid_frag = nullptr;    // [B][ffn/128][16] uint4: SwiGLU output in B-fragment order
   float* tmp = nullptr;        // [B, max(d, ffn)] fp32 (reference)
   float* partials[2] = {nullptr, nullptr};  // ping-pong sum-of-squares partials [B][kPartStride]
   float* logits = nullptr;     // [max_batch, V]
@@ -424,12 +426,15 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         pb.add(e);
       }
       int cur = 0;
+      // the O and down projections read their inputs pre-staged in B-fragment order (written by the
+      // attention / SwiGLU epilogues); FQ_NO_FRAG=1 stages them from the plain activations
+      const bool use_frag = std::getenv("FQ_NO_FRAG") == nullptr;
       // attention work items: (row, head, split); with few rows the keys of a head are split over
       // up to kMaxAttnSplit CTAs and the O projection's staging merges the partials
       // (measured: the merge costs the O projection's staging more than the split saves; off by
       // default, FQ_ATTN_SPLITS=n to experiment)
       const char* se = std::getenv("FQ_ATTN_SPLITS");
-      const int kMaxAttnSplit = se ? std::max(1, std::min(4, std::atoi(se))) : 1;
+      const int kMaxAttnSplit = (se && FQ_ATTN_MERGE) ? std::max(1, std::min(4, std::atoi(se))) : 1;
       const int attn_splits = gemv_only ? 1
           : std::max(1, std::min(std::min(kMaxAttnSplit, M->n_chunks), G / std::max(1, B * static_cast<int>(c.n_heads))));
       for (int64_t l = 0; l < c.n_layers; ++l) {
@@ -495,9 +500,12 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
           a.head_dim = static_cast<int>(c.head_dim);
           a.rope_cs = M->rope_cs;
           a.attn_ws = M->attn_ws;
-          a.tickets = M->tickets;
           a.attn_out = M->attn;
           a.attn_splits = attn_splits;
+          if (use_frag && attn_splits == 1) {
+            a.yfrag = static_cast<__half*>(M->attn_frag);
+            a.yfrag_nkb = static_cast<int>((d + kBlockK - 1) / kBlockK);
+          }
           pb.add(a);
         }
         GemvLaunch o;
@@ -506,6 +514,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         o.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 3);
         o.mat[0].rung_stride = M->n_lin;
         o.x = M->attn;
+        if (use_frag && attn_splits == 1 && !gemv_only) o.xfrag = M->attn_frag;
         o.x_dtype = c.act_dtype;
         o.x_stride = d;
         o.epi = EPI_RESIDUAL;
@@ -542,6 +551,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         gu.act_dtype = c.act_dtype;
         gu.epi = EPI_SWIGLU;
         gu.y = M->mid;
+        if (use_frag) gu.yfrag = M->mid_frag;
         gu.y_dtype = c.act_dtype;
         gu.y_stride = c.ffn_dim;
         add_chunked(pb, gu, B);
@@ -551,6 +561,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         dn.mat[0].rung_table = table + M->lin_index(static_cast<int>(l), 6);
         dn.mat[0].rung_stride = M->n_lin;
         dn.x = M->mid;
+        if (use_frag) dn.xfrag = M->mid_frag;
         dn.x_dtype = c.act_dtype;
         dn.x_stride = c.ffn_dim;
         dn.epi = EPI_RESIDUAL;
@@ -1060,6 +1071,13 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->v = dmalloc(as * B * d);
     M->attn = dmalloc(as * B * d);
     M->mid = dmalloc(as * B * ffn);
+    {
+      const int64_t fd = (d + kBlockK - 1) / kBlockK * kBlockK, ff = (ffn + kBlockK - 1) / kBlockK * kBlockK;
+      M->attn_frag = dmalloc(2 * B * fd);
+      M->mid_frag = dmalloc(2 * B * ff);
+      FQ_CUDA(cudaMemsetAsync(M->attn_frag, 0, 2 * B * fd, st));  // padding past K stays zero
+      FQ_CUDA(cudaMemsetAsync(M->mid_frag, 0, 2 * B * ff, st));
+    }
     M->tmp = zeros(B * ffn_or_d(c));
     M->partials[0] = zeros(static_cast<int64_t>(B) * kPartStride);
     M->partials[1] = zeros(static_cast<int64_t>(B) * kPartStride);
@@ -1131,6 +1149,8 @@ fq_status fq_model_destroy(fq_model* M) {
     dfree(M->v);
     dfree(M->attn);
     dfree(M->mid);
+    dfree(M->attn_frag);
+    dfree(M->mid_frag);
     dfree(M->tmp);
     dfree(M->partials[0]);
     dfree(M->partials[1]);

@@ -159,6 +159,15 @@ __device__ __forceinline__ void store_out(void* y, int dtype, int64_t i, float v
   else static_cast<__half*>(y)[i] = __float2half_rn(v);
 }
 
+// Activation k of batch row b in B-fragment order (the smem xs layout, fp16): block kb = k/128,
+// k16 = (k%128)/16 -> (p, hh) = (k16>>1, k16&1), r = k%16 -> (tig, half, lo) = ((r&7)>>1, r>>3, r&1);
+// uint4 (b*nkb + kb)*16 + p*4 + tig, half-word 2*(2*hh + half) + lo.
+__device__ __forceinline__ void frag_store(__half* frag, int nkb, int b, int64_t k, float v) {
+  const int kb = static_cast<int>(k >> 7), r = static_cast<int>(k & 127), j16 = r >> 4, r16 = r & 15;
+  const int p = j16 >> 1, hh = j16 & 1, tig = (r16 & 7) >> 1, comp = 2 * hh + (r16 >> 3);
+  frag[((static_cast<int64_t>(b) * nkb + kb) * 16 + p * 4 + tig) * 8 + comp * 2 + (r16 & 1)] = __float2half_rn(v);
+}
+
 __device__ __forceinline__ int mat_rung(const DevMat& m, int b) {
   return m.rung_table ? static_cast<int>(m.rung_table[b * m.rung_stride]) : m.rung;
 }
@@ -175,7 +184,7 @@ struct Segs {
 
 __device__ __forceinline__ int blk_bytes(int w) { return w == 0 ? kBlockBytes8 : kBlockBytes4; }
 
-__device__ void phase_segs(const Phase& P, Segs& S) {
+__device__ __noinline__ void phase_segs(const Phase& P, Segs& S) {  // one copy: setup paths only
   // all rung bytes are loaded first (independent loads, one round trip), then the masks
   uint8_t rg[kMaxMat][kMaxB];
 #pragma unroll
@@ -367,8 +376,9 @@ static_assert(kMaxB <= kNCW, "one consumer warp per batch row computes its RMSNo
 // splits' unnormalised partials are merged here, x = sum_s O_s e^(m_s - M) / sum_s l_s e^(m_s - M),
 // rounded to the activation dtype exactly as the unsplit attention rounds its output.  All loads
 // (every split's O values of this thread's items and the (m, l) pairs) go out together.
+#if FQ_ATTN_MERGE
 constexpr int kMaxAttnSplits = 4;
-__device__ __forceinline__ void stage_attn_merge(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+__device__ __noinline__ void stage_attn_merge(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
   const int B = P.B;
   const int tid = threadIdx.x;
   constexpr int NT = kNCW * 32;
@@ -467,6 +477,8 @@ __device__ __forceinline__ void stage_attn_merge(const Phase& P, const GemvSmem&
   }
   named_sync(1, NT);
 }
+
+#endif  // FQ_ATTN_MERGE
 
 // Vectorised staging (16-byte loads of 8 consecutive activations): one load per 8 values (two
 // for fp32 inputs / gains), every load of the phase in flight together when they fit VB vectors
@@ -581,13 +593,59 @@ __device__ __forceinline__ bool stage_vec_ok(const Phase& P) {
          (P.norm_gain == nullptr || (reinterpret_cast<uintptr_t>(P.norm_gain) & 15) == 0);
 }
 
+// Staging of an input the producing phase already wrote in fragment order: a straight copy (all
+// loads of the phase in flight together), then the per-block sums dx from shared memory (one warp
+// per 128-block: four halves per lane, shuffle tree).
+constexpr int kCopyVec = 6;  // uint4s per thread per round (K = 11008 at B = 1: 1376 -> one round)
+__device__ __noinline__ void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+  const int B = P.B, nkb = P.nkb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = kNCW * 32;
+  const int n = B * nkb * 16;
+  for (int base = 0; base < n; base += NT * kCopyVec) {
+    uint4 v[kCopyVec];
+#pragma unroll
+    for (int s = 0; s < kCopyVec; ++s) {
+      const int i = base + s * NT + tid;
+      v[s] = i < n ? P.xfrag[i] : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int s = 0; s < kCopyVec; ++s) {
+      const int i = base + s * NT + tid;
+      if (i < n) G.xs[i] = v[s];
+    }
+  }
+  if (gp) gp[1] = gtimer();
+  named_sync(1, NT);
+  if (gp) gp[2] = gtimer();
+  for (int blk = warp; blk < B * nkb; blk += kNCW) {
+    const uint2 h4 = reinterpret_cast<const uint2*>(G.xs + static_cast<size_t>(blk) * 16)[lane];
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h4.x));
+    const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h4.y));
+    float sum = (a.x + a.y) + (c.x + c.y);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int b = blk / nkb, kb = blk - b * nkb;
+    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
+  }
+  named_sync(1, NT);
+}
+
 #ifndef FQ_VEC_STAGE
 #define FQ_VEC_STAGE 0  // measured 2.5% slower per step (code size), kept for A/B
 #endif
 __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+  if (P.xfrag != nullptr) {
+    stage_frag_copy(P, G, gp);
+    return;
+  }
   if (P.attn_splits > 1) {
+#if FQ_ATTN_MERGE
     stage_attn_merge(P, G, gp);
     return;
+#else
+    __trap();  // the builder only splits attention when the merge is compiled in
+#endif
   }
   const bool vnorm = P.norm_gain != nullptr;
   if (FQ_VEC_STAGE && stage_vec_ok(P) && vnorm == (P.x_dtype == FQ_DT_F32)) {
@@ -871,7 +929,7 @@ __device__ __forceinline__ void stat_add(StatPart& a, float l, int idx) {
   }
 }
 
-__device__ __forceinline__ StatPart stat_merge(const StatPart& a, const StatPart& b) {
+__device__ __noinline__ StatPart stat_merge(const StatPart& a, const StatPart& b) {
   if (b.m == -INFINITY) return a;
   if (a.m == -INFINITY) return b;
   StatPart r;
@@ -909,7 +967,9 @@ __device__ __forceinline__ void gemv_epilogue(const Phase& P, int64_t tile, int 
   } else if (P.epi == EPI_SWIGLU) {
     const float gt = v[0];
     const float silu = gt / (1.0f + expf(-gt));
-    store_out(P.y, P.y_dtype, b * P.y_stride + row, round_act(silu * v[1], P.act_dtype));
+    const float o = round_act(silu * v[1], P.act_dtype);
+    store_out(P.y, P.y_dtype, b * P.y_stride + row, o);
+    if (P.yfrag) frag_store(P.yfrag, P.yfrag_nkb, b, row, o);
   } else {
     float* xp = P.resid + b * P.resid_stride + row;
     const float nv = *xp + v[0];
@@ -1681,7 +1741,11 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
     }
     if (ns == 1) {
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) store_out(P.attn_out, P.act_dtype, qoff + e, Ot[e] / Lt);
+      for (int e = 0; e < DPL; ++e) {
+        const float o = round_act(Ot[e] / Lt, P.act_dtype);
+        store_out(P.attn_out, P.act_dtype, qoff + e, o);
+        if (P.yfrag) frag_store(P.yfrag, P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e, o);
+      }
     } else {
       float* part = P.attn_ws + ((static_cast<int64_t>(b) * H + h) * ns + sp) * (hd + 4);
 #pragma unroll
@@ -2020,7 +2084,6 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
     Phase& P = pb.phases[i];
     if (P.type != PH_GEMV) continue;
     P.fix = fix + 2 * static_cast<size_t>(i) * r.grid * (inl ? kMaxMat * 16 * kMaxB : fstride);  // float2 parts
-    P.flags = flags + static_cast<size_t>(i) * (inl ? 1024 : r.grid);
   }
   if (inl) {
     for (int i = 0; i < r.nphases; ++i) r.inl.phases[i] = pb.phases[i];
