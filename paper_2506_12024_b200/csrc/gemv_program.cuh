@@ -18,14 +18,18 @@ constexpr int kMaxB = 8;          // batch rows per GEMV phase (the MMA's n = 8 
 constexpr int kMaxMat = 3;        // matrices sharing one input (QKV)
 constexpr int kMaxStages = 8;
 #ifndef FQ_NCW
-#define FQ_NCW 8
+#define FQ_NCW 11  // 12 warps = 3 per SM sub-partition: same 168-register cap as 9 warps, 37% more consumers
 #endif
 constexpr int kNCW = FQ_NCW;      // consumer warps (2 blocks in flight each)
 constexpr int kThreads = (kNCW + 1) * 32;  // + one producer warp
 constexpr int kAttnChunk = 16;    // keys per attention work item (one warp)
-constexpr int kStageBytes = 35328;  // max(16 W8 blocks, 32 W4 blocks)
-constexpr int kStageBlocks8 = 16;
-constexpr int kStageBlocks4 = 32;
+#ifndef FQ_STAGE8
+#define FQ_STAGE8 16
+#endif
+constexpr int kStageBlocks8 = FQ_STAGE8;       // W8 blocks per ring stage (2 per consumer warp)
+constexpr int kStageBlocks4 = 2 * FQ_STAGE8;   // W4 blocks per ring stage
+constexpr int kStageBytes = kStageBlocks8 * (2048 + 80) > kStageBlocks4 * (1024 + 80) ? kStageBlocks8 * (2048 + 80)
+                                                                                      : kStageBlocks4 * (1024 + 80);
 constexpr int kSmemBudget = 220 * 1024;
 
 enum PhaseType : int { PH_GEMV = 0, PH_EMBED = 1, PH_ATTN = 2, PH_STATS = 3, PH_APPEND = 4 };
