@@ -600,7 +600,11 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         sp.stat_part = M->stat_part;
         pb.add(sp);
       }
-      it = M->programs.emplace(key, upload_program(ctx, pb, false)).first;
+      ProgramRun run = upload_program(ctx, pb, false);
+      run.pos = meta.pos;  // constant per (batch, mode): the step's row metadata lives in fixed buffers
+      run.slots = meta.slots;
+      run.nrows = B;
+      it = M->programs.emplace(key, run).first;
     }
     FQ_CUDA(cudaMemsetAsync(M->grid_barrier, 0, sizeof(unsigned int), st));
     const bool timed = mode == STEP_DECODE && M->ev_prog[0] != nullptr;

@@ -369,7 +369,10 @@ struct GemvSmem {
 // Issue order: every global load of the first item batch (activations, norm gains) and the RMSNorm
 // partials go out together, so the phase pays one round trip before its first MMA; warp b reduces
 // row b's partials while the activation loads are in flight.
-constexpr int kStageItems = 2;  // items per thread per batch (loads in flight together)
+#ifndef FQ_STAGE_ITEMS
+#define FQ_STAGE_ITEMS 2
+#endif
+constexpr int kStageItems = FQ_STAGE_ITEMS;  // items per thread per batch (loads in flight together)
 static_assert(kMaxB <= kNCW, "one consumer warp per batch row computes its RMSNorm factor");
 
 // Staging of the O projection's input when the attention phase ran split (attn_splits > 1): the
@@ -632,7 +635,7 @@ __device__ __noinline__ void stage_frag_copy(const Phase& P, const GemvSmem& G, 
 }
 
 #ifndef FQ_VEC_STAGE
-#define FQ_VEC_STAGE 0  // measured 2.5% slower per step (code size), kept for A/B
+#define FQ_VEC_STAGE 1  // one round trip for K = 11008 (measured -0.6% per step at 11 consumer warps)
 #endif
 __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
   if (P.xfrag != nullptr) {
@@ -1171,6 +1174,25 @@ struct AheadWalk {
   }
 };
 
+// The KV rows the next attention phase reads on this CTA (decode: one (row, head) item per CTA)
+// are prefetched into L2 when the producer starts the GEMV phase before it, so the attention's
+// loads hit L2 instead of HBM (the cache region of a head is contiguous: rows 0..pos).
+#ifndef FQ_KV_PREFETCH
+#define FQ_KV_PREFETCH 0  // measured: attention -20 us but GEMV phases +30 us per step
+#endif
+__device__ __forceinline__ void prefetch_attn_kv(const Phase& A) {
+  if (A.type != PH_ATTN || A.appended || A.attn_splits > 1) return;
+  const int H = A.n_heads, hd = A.head_dim;
+  for (int item = blockIdx.x; item < A.B * H; item += gridDim.x) {
+    const int b = item / H, h = item - b * H;
+    const int pos = A.pos[b];
+    const __half* kc = A.kv + A.slots[b] * A.slot_stride + A.layer_off + static_cast<int64_t>(h) * A.max_seq * hd;
+    const uint32_t bytes = static_cast<uint32_t>(pos + 1) * hd * 2;  // a multiple of 16
+    prefetch_l2(kc, bytes);
+    prefetch_l2(kc + static_cast<int64_t>(H) * A.max_seq * hd, bytes);
+  }
+}
+
 __device__ void produce_table(const Phase* phases, int nphases, const CtlEntry* ctab, const Ring R,
                               unsigned long long* tr, const uint8_t** s_base, bool noload, int prefetch,
                               const uint8_t** s_base2) {
@@ -1191,6 +1213,7 @@ __device__ void produce_table(const Phase* phases, int nphases, const CtlEntry* 
   while (ph < nphases) {
     const int phn = next_gemv_phase(ctab, ph + 1, nphases);
     if (phn < nphases) prod_load(phases[phn], nxt);  // in flight while this phase streams
+    if (FQ_KV_PREFETCH && ph + 1 < nphases) prefetch_attn_kv(phases[ph + 1]);
     const CtlEntry& E = ctab[ph];
     const int nseg = E.nseg, nkb = cur.nkb;
 #pragma unroll
@@ -1535,6 +1558,20 @@ __device__ __noinline__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
 // with the full scores of keys base(l), base(l)+1.  The chunk's (max, sum, o) partial goes to the
 // workspace; the last chunk of a head (ticket) merges them.  RoPE pairs (i, i + hd/2) live on
 // lanes l and l^16; cos/sin come from the model's table (double-computed angles).
+constexpr int kMaxMetaRows = 64;
+struct MetaSmem {
+  const int32_t* pos;
+  const int32_t* slots;
+  int n;
+  int p[kMaxMetaRows], s[kMaxMetaRows];
+};
+__device__ __forceinline__ int meta_pos(const MetaSmem& M, const int32_t* pos, int b) {
+  return (pos == M.pos && b < M.n) ? M.p[b] : pos[b];
+}
+__device__ __forceinline__ int meta_slot(const MetaSmem& M, const int32_t* slots, int b) {
+  return (slots == M.slots && b < M.n) ? M.s[b] : slots[b];
+}
+
 struct AttnSmem {
   float o[kNCW][128];
   float m[kNCW], l[kNCW];
@@ -1572,11 +1609,11 @@ struct AttnRaw {
 };
 
 template <int DPL>
-__device__ __forceinline__ void attn_load(const Phase& P, int b, int h, int chunk, int lane, AttnRaw<DPL>& R) {
+__device__ __forceinline__ void attn_load(const Phase& P, int slot, int h, int chunk, int lane, AttnRaw<DPL>& R) {
   constexpr int hd = DPL * 32;
   using Raw = typename AttnRaw<DPL>::Raw;
   const int H = P.n_heads;
-  const __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+  const __half* kc = P.kv + slot * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
   const __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
   const int j0 = chunk * kAttnChunk;
   const int last_row = static_cast<int>(P.max_seq) - 1;
@@ -1593,17 +1630,16 @@ __device__ __forceinline__ void attn_load(const Phase& P, int b, int h, int chun
 // cache first (decode; prefill appended them in a phase of its own).
 template <int DPL>
 __device__ __forceinline__ void attn_compute(const Phase& P, int b, int h, int chunk, const float (&q)[DPL], int lane,
-                                             AttnRaw<DPL>& R, float& mx, float& l, float (&o)[DPL]) {
+                                             AttnRaw<DPL>& R, float& mx, float& l, float (&o)[DPL], int pos, int slot) {
   constexpr int hd = DPL * 32;
   constexpr int CH = kAttnChunk;  // 16 keys
   using Raw = typename AttnRaw<DPL>::Raw;
   const int H = P.n_heads;
-  const int pos = P.pos[b];
   const int j0 = chunk * CH;
   const int nk = min(CH, pos + 1 - j0);
   const bool owns_new = !P.appended && pos >= j0 && pos < j0 + CH;
   if (owns_new) {
-    __half* kc = P.kv + P.slots[b] * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+    __half* kc = P.kv + slot * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
     __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
     const int64_t off = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
     float kn[DPL], vn[DPL];
@@ -1687,10 +1723,10 @@ __device__ __forceinline__ void attn_compute(const Phase& P, int b, int h, int c
 // attn_out; ns > 1: the CTA's unnormalised partial (O[hd], m, l) goes to attn_ws and the next GEMV
 // phase (the O projection) merges the splits while staging its input.
 template <int DPL>
-__device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane, int warp, AttnSmem& S) {
+__device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane, int warp, AttnSmem& S, int pos,
+                          int slot) {
   constexpr int hd = DPL * 32;
   const int H = P.n_heads;
-  const int pos = P.pos[b];
   const int nch = (pos + kAttnChunk) / kAttnChunk;
   const int c0 = (nch * sp) / ns, c1 = (nch * (sp + 1)) / ns;
   const int64_t qoff = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
@@ -1700,7 +1736,7 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
   for (int e = 0; e < DPL; ++e) O[e] = 0.f;
   for (int c = c0 + warp; c < c1; c += kNCW) {
     AttnRaw<DPL> R;
-    attn_load<DPL>(P, b, h, c, lane, R);
+    attn_load<DPL>(P, slot, h, c, lane, R);
     if (c == c0 + warp) {
       // first chunk: the query loads go out behind its K/V loads (one round trip for both)
       load_lane<DPL>(P.q, P.act_dtype, qoff, q);
@@ -1710,7 +1746,7 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
       for (int e = 0; e < DPL; ++e) q[e] *= scale;
     }
     float mx, l, o[DPL];
-    attn_compute<DPL>(P, b, h, c, q, lane, R, mx, l, o);
+    attn_compute<DPL>(P, b, h, c, q, lane, R, mx, l, o, pos, slot);
     const float Mn = fmaxf(M, mx);
     const float fa = M == -INFINITY ? 0.f : expf(M - Mn), fb = expf(mx - Mn);
     L = L * fa + l * fb;
@@ -1787,15 +1823,16 @@ __device__ __noinline__ void run_append(const Phase& P) {
   }
 }
 
-__device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S) {
+__device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S, const MetaSmem& MS) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // one (row, head, split) per CTA at a time, spread over the grid
   const int ns = max(1, P.attn_splits);
   for (int item = blockIdx.x; item < P.B * P.n_heads * ns; item += gridDim.x) {
     const int bh = item / ns, sp = item - bh * ns;
     const int b = bh / P.n_heads, h = bh - b * P.n_heads;
-    if (P.head_dim == 128) attn_head<4>(P, b, h, sp, ns, lane, warp, S);
-    else attn_head<2>(P, b, h, sp, ns, lane, warp, S);
+    const int pos = meta_pos(MS, P.pos, b), slot = meta_slot(MS, P.slots, b);
+    if (P.head_dim == 128) attn_head<4>(P, b, h, sp, ns, lane, warp, S, pos, slot);
+    else attn_head<2>(P, b, h, sp, ns, lane, warp, S, pos, slot);
   }
 }
 
@@ -1876,6 +1913,9 @@ struct SmemLayout {
   int ctl_phases;  // phases with a precomputed partition table in shared memory (0 = none)
   unsigned int* lctr;  // [launch epoch, CTAs done]: the epoch tags this launch's stream-K parts
   int prefetch;  // L2 prefetch distance of the weight stream, in stages
+  const int32_t* pos;    // per-row positions / cache slots of the step (shared-memory copies)
+  const int32_t* slots;
+  int nrows;
 };
 
 __device__ void run_program(const Phase* phases, int nphases, unsigned int* barrier, SmemLayout L) {
@@ -1931,6 +1971,16 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     return;
   }
   pdl_wait();
+  __shared__ MetaSmem meta_smem;
+  if (threadIdx.x == 0) {
+    meta_smem.pos = L.pos;
+    meta_smem.slots = L.slots;
+    meta_smem.n = min(L.nrows, kMaxMetaRows);
+  }
+  for (int b = threadIdx.x; b < min(L.nrows, kMaxMetaRows); b += kNCW * 32) {
+    meta_smem.p[b] = L.pos[b];
+    meta_smem.s[b] = L.slots[b];
+  }
   __shared__ unsigned int s_lepoch;
   if (threadIdx.x == 0) s_lepoch = *reinterpret_cast<volatile unsigned int*>(L.lctr);
   int slot_i = 0;
@@ -1956,7 +2006,7 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     const Phase& P = pbuf[i & 1];
     if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i, gprof);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
-    else if (P.type == PH_ATTN) run_attn(P, attn_smem);
+    else if (P.type == PH_ATTN) run_attn(P, attn_smem, meta_smem);
     else if (P.type == PH_APPEND) run_append(P);
     else run_stats(P);
     if (prof) prof[(static_cast<size_t>(i) * gridDim.x + blockIdx.x) * 2] = gtimer();
@@ -2104,6 +2154,9 @@ void launch_program(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, b
   L.red_bytes = run.red_bytes;
   L.prefetch = run.prefetch;
   L.ctl_phases = run.ctl_phases;
+  L.pos = run.pos;
+  L.slots = run.slots;
+  L.nrows = run.pos && run.slots ? run.nrows : 0;
   if (ctx->launch_ctr == nullptr) {
     ctx->launch_ctr = static_cast<unsigned int*>(dmalloc(2 * sizeof(unsigned int)));
     const unsigned int init[2] = {1u, 0u};  // epoch 0 never tags anything (fresh memory is zero)
