@@ -76,8 +76,9 @@ struct alignas(16) Phase {
                           // entropy, head only); STATS: their input [B][grid]
   const uint4* xfrag;     // GEMV: input already in B-fragment order (fp16, batch-major, the smem
                           // xs layout) written by the producing phase's epilogue: staging is a copy
-  __half* yfrag;          // GEMV (SwiGLU epilogue) / ATTN: also write the output in that order
-  int yfrag_nkb;          // 128-blocks per batch row of yfrag
+  __half* yfrag;          // GEMV (SwiGLU epilogue) / ATTN: also write the output in that order; as
+                          // (half2, tag) words when the next phase has no barrier (yfrag_tagged)
+  int yfrag_nkb;          // 128-blocks per batch row of yfrag; < 0: tagged words, nkb = -yfrag_nkb
   float* fix;             // stream-K fix-up partials [grid][kMaxMat * 16 * kMaxB]
   // ---- EMBED / ATTN / STATS (decode step)
   const float* tok_emb;
@@ -91,7 +92,11 @@ struct alignas(16) Phase {
   __half* kv;
   int64_t slot_stride, layer_off, max_seq;
   int n_heads, head_dim;
-  int appended;           // ATTN: the rows' keys / values are already in the cache (prefill)
+  union {
+    int appended;         // ATTN: the rows' keys / values are already in the cache (prefill)
+    int xfrag_tagged;     // GEMV: xfrag holds (half2, tag) 8-byte words written by the previous
+                          // phase (no grid barrier before this phase: staging polls the tags)
+  };
   int attn_splits;        // ATTN: CTAs per (row, head), each over a contiguous chunk range; > 1:
                           // unnormalised partials (O[hd], m, l) in attn_ws, merged by the next
                           // GEMV phase's staging (the O projection reads them as its input)

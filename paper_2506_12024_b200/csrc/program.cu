@@ -168,6 +168,20 @@ __device__ __forceinline__ void frag_store(__half* frag, int nkb, int b, int64_t
   frag[((static_cast<int64_t>(b) * nkb + kb) * 16 + p * 4 + tig) * 8 + comp * 2 + (r16 & 1)] = __float2half_rn(v);
 }
 
+// Tagged variant: the pair (k, k+1), k even, as one 8-byte word {half2, tag} at word index
+// uint4_index * 4 + comp of the fragment layout (single-copy atomic: the consumer polls the tag).
+__device__ __forceinline__ void frag_store_pair(__half* frag, int nkb, int b, int64_t k, float v0, float v1,
+                                                unsigned int tag) {
+  const int kb = static_cast<int>(k >> 7), r = static_cast<int>(k & 127), j16 = r >> 4, r16 = r & 15;
+  const int p = j16 >> 1, hh = j16 & 1, tig = (r16 & 7) >> 1, comp = 2 * hh + (r16 >> 3);
+  const __half2 h = __floats2half2_rn(v0, v1);
+  const unsigned long long w = static_cast<unsigned long long>(*reinterpret_cast<const uint32_t*>(&h)) |
+                               (static_cast<unsigned long long>(tag) << 32);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(frag) +
+                            ((static_cast<int64_t>(b) * nkb + kb) * 16 + p * 4 + tig) * 4 + comp;
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+}
+
 __device__ __forceinline__ int mat_rung(const DevMat& m, int b) {
   return m.rung_table ? static_cast<int>(m.rung_table[b * m.rung_stride]) : m.rung;
 }
@@ -600,12 +614,73 @@ __device__ __forceinline__ bool stage_vec_ok(const Phase& P) {
 // loads of the phase in flight together), then the per-block sums dx from shared memory (one warp
 // per 128-block: four halves per lane, shuffle tree).
 constexpr int kCopyVec = 6;  // uint4s per thread per round (K = 11008 at B = 1: 1376 -> one round)
-__device__ __noinline__ void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+constexpr int kTagWords = 16;
+#ifndef FQ_POLL_NS
+#define FQ_POLL_NS 256
+#endif  // tagged words per thread per round (K = 11008 at B = 1: 5504 -> one round)
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __noinline__ void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp, unsigned int tag) {
   const int B = P.B, nkb = P.nkb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = kNCW * 32;
   const int n = B * nkb * 16;
-  for (int base = 0; base < n; base += NT * kCopyVec) {
+  if (P.xfrag_tagged) {
+    // no grid barrier before this phase: every word is polled until it carries the producing
+    // phase's tag (words past K are the zero padding and never written)
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(P.xfrag);
+    uint32_t* xs32 = reinterpret_cast<uint32_t*>(G.xs);
+    const int nw = n * 4;
+    const int64_t K = P.K;
+    // one poller per warp first (lane 0, on the warp's last word, backing off), so the grid does not
+    // flood the L2 slices holding the activations while their producers are still writing them
+    if (lane == 0) {
+      const int wl = min(nw - 1, (warp + 1) * 32 - 1 + (((nw - 1) / NT) * NT));
+      const int u = wl >> 2, comp = wl & 3, r = u % (nkb * 16);
+      const int64_t k = static_cast<int64_t>(r >> 4) * kBlockK + 16 * (2 * ((r >> 2) & 3) + (comp >> 1)) + 2 * (r & 3) + 8 * (comp & 1);
+      if (k < K) {
+        const unsigned long long t0 = gtimer_now();
+        while (static_cast<unsigned int>(ld_relaxed_u64(src + wl) >> 32) != tag) {
+          __nanosleep(FQ_POLL_NS);
+          if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("tagged activation (warp poll)", wl, static_cast<int>(tag));
+        }
+      }
+    }
+    __syncwarp();
+    for (int base = 0; base < nw; base += NT * kTagWords) {
+      unsigned long long v[kTagWords];
+#pragma unroll
+      for (int s = 0; s < kTagWords; ++s) {
+        const int w = base + s * NT + tid;
+        v[s] = w < nw ? ld_relaxed_u64(src + w) : 0ull;
+      }
+#pragma unroll
+      for (int s = 0; s < kTagWords; ++s) {
+        const int w = base + s * NT + tid;
+        if (w >= nw) continue;
+        const int u = w >> 2, comp = w & 3, r = u % (nkb * 16);
+        const int kb = r >> 4, p = (r >> 2) & 3, tg = r & 3;
+        const int64_t k = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + (comp >> 1)) + 2 * tg + 8 * (comp & 1);
+        if (k >= K) {
+          xs32[w] = 0u;
+          continue;
+        }
+        if (static_cast<unsigned int>(v[s] >> 32) != tag) {
+          const unsigned long long t0 = gtimer_now();
+          do {
+            __nanosleep(FQ_POLL_NS);
+            v[s] = ld_relaxed_u64(src + w);
+            if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("tagged activation", w, static_cast<int>(tag));
+          } while (static_cast<unsigned int>(v[s] >> 32) != tag);
+        }
+        xs32[w] = static_cast<uint32_t>(v[s]);
+      }
+    }
+  }
+  for (int base = 0; !P.xfrag_tagged && base < n; base += NT * kCopyVec) {
     uint4 v[kCopyVec];
 #pragma unroll
     for (int s = 0; s < kCopyVec; ++s) {
@@ -637,9 +712,9 @@ __device__ __noinline__ void stage_frag_copy(const Phase& P, const GemvSmem& G, 
 #ifndef FQ_VEC_STAGE
 #define FQ_VEC_STAGE 1  // one round trip for K = 11008 (measured -0.6% per step at 11 consumer warps)
 #endif
-__device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+__device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp, unsigned int xtag) {
   if (P.xfrag != nullptr) {
-    stage_frag_copy(P, G, gp);
+    stage_frag_copy(P, G, gp, xtag);
     return;
   }
   if (P.attn_splits > 1) {
@@ -972,7 +1047,7 @@ __device__ __forceinline__ void gemv_epilogue(const Phase& P, int64_t tile, int 
     const float silu = gt / (1.0f + expf(-gt));
     const float o = round_act(silu * v[1], P.act_dtype);
     store_out(P.y, P.y_dtype, b * P.y_stride + row, o);
-    if (P.yfrag) frag_store(P.yfrag, P.yfrag_nkb, b, row, o);
+    if (P.yfrag && P.yfrag_nkb > 0) frag_store(P.yfrag, P.yfrag_nkb, b, row, o);
   } else {
     float* xp = P.resid + b * P.resid_stride + row;
     const float nv = *xp + v[0];
@@ -1037,6 +1112,27 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
       gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
     } else {
       gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
+    }
+    if (P.epi == EPI_SWIGLU && P.yfrag != nullptr && P.yfrag_nkb < 0 && ((i / B) & 1) == 0) {
+      // tagged fragment output: the even row of each pair also sums the odd row's partials (same
+      // tile, item i + B) and writes both as one (half2, tag) word
+      const int64_t row = (C.tile0 + l) * static_cast<int64_t>(kTileRows) + i / B;
+      if (row < P.N) {
+        float o2 = 0.f;
+        if (row + 1 < P.N) {
+          float g2 = 0.f, u2 = 0.f;
+          const float* r0 = G.red + (static_cast<size_t>(((l - lo) * nmat) * kNCW)) * per + i + B;
+#pragma unroll
+          for (int w = 0; w < kNCW; ++w) {
+            g2 += r0[w * per];
+            u2 += r0[(kNCW + w) * per];
+          }
+          o2 = round_act(g2 / (1.0f + expf(-g2)) * u2, P.act_dtype);
+        }
+        const float gt = v[0];
+        const float o1 = round_act(gt / (1.0f + expf(-gt)) * v[1], P.act_dtype);
+        frag_store_pair(P.yfrag, -P.yfrag_nkb, i % B, row, o1, o2, C.tag);
+      }
     }
   }
   named_sync(1, kNCW * 32);  // the window's slots are rewritten next
@@ -1369,7 +1465,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     if (lane == 0) C.tag = tag;
     if (gpa && lane == 0) gpa[0] = gtimer();
   }
-  stage_acts(P, G, gp);  // ends with a consumer barrier: C is visible
+  stage_acts(P, G, gp, tag - 1);  // ends with a consumer barrier: C is visible (tag - 1: the previous phase)
   if (gp) gp[3] = gtimer();
   const int B = P.B, nmat = P.nmat;
   float sqb[kMaxB];
@@ -1724,7 +1820,7 @@ __device__ __forceinline__ void attn_compute(const Phase& P, int b, int h, int c
 // phase (the O projection) merges the splits while staging its input.
 template <int DPL>
 __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane, int warp, AttnSmem& S, int pos,
-                          int slot) {
+                          int slot, unsigned int tag) {
   constexpr int hd = DPL * 32;
   const int H = P.n_heads;
   const int nch = (pos + kAttnChunk) / kAttnChunk;
@@ -1780,7 +1876,13 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
       for (int e = 0; e < DPL; ++e) {
         const float o = round_act(Ot[e] / Lt, P.act_dtype);
         store_out(P.attn_out, P.act_dtype, qoff + e, o);
-        if (P.yfrag) frag_store(P.yfrag, P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e, o);
+        if (P.yfrag && P.yfrag_nkb > 0) frag_store(P.yfrag, P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e, o);
+      }
+      if (P.yfrag && P.yfrag_nkb < 0) {
+#pragma unroll
+        for (int e = 0; e < DPL; e += 2)
+          frag_store_pair(P.yfrag, -P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e,
+                          round_act(Ot[e] / Lt, P.act_dtype), round_act(Ot[e + 1] / Lt, P.act_dtype), tag);
       }
     } else {
       float* part = P.attn_ws + ((static_cast<int64_t>(b) * H + h) * ns + sp) * (hd + 4);
@@ -1823,7 +1925,7 @@ __device__ __noinline__ void run_append(const Phase& P) {
   }
 }
 
-__device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S, const MetaSmem& MS) {
+__device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S, const MetaSmem& MS, unsigned int tag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // one (row, head, split) per CTA at a time, spread over the grid
   const int ns = max(1, P.attn_splits);
@@ -1831,8 +1933,8 @@ __device__ __noinline__ void run_attn(const Phase& P, AttnSmem& S, const MetaSme
     const int bh = item / ns, sp = item - bh * ns;
     const int b = bh / P.n_heads, h = bh - b * P.n_heads;
     const int pos = meta_pos(MS, P.pos, b), slot = meta_slot(MS, P.slots, b);
-    if (P.head_dim == 128) attn_head<4>(P, b, h, sp, ns, lane, warp, S, pos, slot);
-    else attn_head<2>(P, b, h, sp, ns, lane, warp, S, pos, slot);
+    if (P.head_dim == 128) attn_head<4>(P, b, h, sp, ns, lane, warp, S, pos, slot, tag);
+    else attn_head<2>(P, b, h, sp, ns, lane, warp, S, pos, slot, tag);
   }
 }
 
@@ -2006,7 +2108,7 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
     const Phase& P = pbuf[i & 1];
     if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i, gprof);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
-    else if (P.type == PH_ATTN) run_attn(P, attn_smem, meta_smem);
+    else if (P.type == PH_ATTN) run_attn(P, attn_smem, meta_smem, s_lepoch * 1024u + i);
     else if (P.type == PH_APPEND) run_append(P);
     else run_stats(P);
     if (prof) prof[(static_cast<size_t>(i) * gridDim.x + blockIdx.x) * 2] = gtimer();
