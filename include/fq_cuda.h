@@ -125,6 +125,15 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int64_t batc
                   const void* x_dev, int32_t x_dtype, void* y_dev, int32_t y_dtype,
                   int32_t numerics);
 
+/* Benchmark form of fq_gemv (BASELINE config 2): n independent GEMVs y_i = x . dequant(W_i)^T
+ * (same x, fast numerics) as ONE persistent step-program launch with no grid barrier between
+ * them, so the TMA weight stream runs across layer boundaries as it does inside a decode step.
+ * Launched `reps` times on the context stream; *ms_per_launch = mean device time of one launch
+ * (CUDA events around the launches).  The outputs are those of n fq_gemv calls. */
+fq_status fq_gemv_chain_time(fq_ctx* ctx, const fq_layer* const* layers, int32_t n, int32_t rung, int64_t batch,
+                             const void* x_dev, int32_t x_dtype, void* const* y_devs, int32_t y_dtype,
+                             int32_t reps, double* ms_per_launch);
+
 /* Prefill / calibration contraction on the tcgen05 tensor cores (BASELINE config 4):
  * y[rows, N] (fp32, row stride y_stride) = x[rows, K] (bf16, row stride x_stride) . dequant(W_rung)^T,
  * the dequantisation of the resident tiled W8/W4 copy fused into the tile loads (fp16 operands,

@@ -33,7 +33,7 @@ ABI_FUNCTIONS = [
     "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
     "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
     "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step", "fq_gemm",
-    "fq_model_step_kernel_time",
+    "fq_model_step_kernel_time", "fq_gemv_chain_time",
 ]
 
 
@@ -126,6 +126,7 @@ def load(path: str = LIB_PATH):
         "fq_layer_shape": [v, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],
         "fq_layer_bytes": [v, i32, i64, C.POINTER(i64)],
         "fq_gemv": [v, v, i32, i64, v, i32, v, i32, i32],
+        "fq_gemv_chain_time": [v, C.POINTER(v), i32, i32, i64, v, i32, C.POINTER(v), i32, i32, C.POINTER(C.c_double)],
         "fq_softmax_stats": [v, v, i64, i64, v],
         "fq_kl_rows": [v, v, v, i32, i64, i64, v, v],
         "fq_hist_kl": [v, v, i32, i32, C.POINTER(C.c_double)],
@@ -225,6 +226,15 @@ class Context:
     def gemv(self, layer: "Layer", rung: int, batch: int, x, x_dtype: int, y, y_dtype: int,
              numerics: int = NUMERICS_FAST) -> None:
         check(self.L.fq_gemv(self.h, layer.h, rung, batch, _ptr(x), x_dtype, _ptr(y), y_dtype, numerics))
+
+    def gemv_chain_time(self, layers, rung: int, batch: int, x, x_dtype: int, ys, y_dtype: int, reps: int) -> float:
+        """n independent GEMVs (same x) as one step-program launch without barriers; ms per launch."""
+        n = len(layers)
+        lh = (C.c_void_p * n)(*[l.h for l in layers])
+        yh = (C.c_void_p * n)(*[_ptr(y) for y in ys])
+        ms = C.c_double()
+        check(self.L.fq_gemv_chain_time(self.h, lh, n, rung, batch, _ptr(x), x_dtype, yh, y_dtype, reps, C.byref(ms)))
+        return ms.value
 
     def gemm(self, layer: "Layer", rung: int, rows: int, x_bf16, y_f32, x_stride: int = 0, y_stride: int = 0) -> None:
         """y[rows, N] = x[rows, K] . dequant(W_rung)^T on the tcgen05 tensor cores."""

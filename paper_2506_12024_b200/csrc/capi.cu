@@ -1,5 +1,6 @@
 // C-ABI implementation: contexts, the resident weight store and the stateless kernels.
 // Every entry point converts internal failures into an fq_status + fq_last_error().
+#include <vector>
 #include "fq_internal.cuh"
 
 #include <cstring>
@@ -306,6 +307,38 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t batch, c
     g.y_dtype = y_dtype;
     g.y_stride = L->N;
     launch_gemv_fast(ctx, g);
+  });
+}
+
+fq_status fq_gemv_chain_time(fq_ctx* ctx, const fq_layer* const* layers, int32_t n, int32_t rung, int64_t batch,
+                             const void* x_dev, int32_t x_dtype, void* const* y_devs, int32_t y_dtype, int32_t reps,
+                             double* ms_per_launch) {
+  return guarded([&] {
+    require(ctx != nullptr && layers != nullptr && x_dev != nullptr && y_devs != nullptr && ms_per_launch != nullptr,
+            FQ_E_INPUT, "null argument");
+    require(n >= 1 && batch >= 1 && reps >= 1, FQ_E_DIMENSION, "gemv chain: n, batch and reps must be >= 1");
+    require(x_dtype >= FQ_DT_F32 && x_dtype <= FQ_DT_BF16 && y_dtype >= FQ_DT_F32 && y_dtype <= FQ_DT_BF16,
+            FQ_E_CONFIG, "gemv: bad dtype");
+    std::vector<GemvLaunch> gs(n);
+    for (int i = 0; i < n; ++i) {
+      const fq_layer* L = layers[i];
+      require(L != nullptr && y_devs[i] != nullptr, FQ_E_INPUT, "null argument");
+      require(L->K == layers[0]->K && L->N == layers[0]->N, FQ_E_DIMENSION, "gemv chain: layers differ in shape");
+      require(gemv_fast_supported(L, rung) && L->bias == nullptr, FQ_E_STATE, "gemv chain: rung not on the fast path");
+      GemvLaunch& g = gs[i];
+      g.mat[0].layer = L;
+      g.mat[0].rung = rung;
+      g.nmat = 1;
+      g.batch = batch;
+      g.x = x_dev;
+      g.x_dtype = x_dtype;
+      g.x_stride = L->K;
+      g.epi = EPI_STORE;
+      g.y = y_devs[i];
+      g.y_dtype = y_dtype;
+      g.y_stride = L->N;
+    }
+    *ms_per_launch = time_gemv_chain(ctx, gs.data(), n, reps);
   });
 }
 

@@ -171,6 +171,7 @@ int gemv_fast_grid(const fq_ctx* ctx, int64_t N);
 // Returns the grid size used (the residual epilogue writes one sum-of-squares partial per CTA;
 // out_n_partials must be >= #SM x 4).
 int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);
+double time_gemv_chain(fq_ctx* ctx, const GemvLaunch* gs, int n, int reps);
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
                        int x_dtype, void* y, int y_dtype);
 

@@ -159,6 +159,36 @@ int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g) {
   return pb.grid;
 }
 
+double time_gemv_chain(fq_ctx* ctx, const GemvLaunch* gs, int n, int reps) {
+  // one device program of n independent GEMV phases (no barriers), launched reps times
+  ProgramBuilder pb;
+  const fq_layer* L0 = gs[0].mat[0].layer;
+  pb.grid = gemv_fast_grid(ctx, static_cast<int64_t>(ceil_div_i(L0->N, kTileRows)) * ceil_div_i(L0->K, kBlockK));
+  for (int i = 0; i < n; ++i) {
+    const int64_t bchunk = gemv_batch_chunk(gs[i].mat[0].layer->K);
+    for (int64_t b0 = 0; b0 < gs[i].batch; b0 += bchunk)
+      pb.add_gemv(gs[i], b0, static_cast<int>(std::min<int64_t>(bchunk, gs[i].batch - b0)));
+  }
+  for (auto& P : pb.phases) P.barrier_after = 0;
+  ProgramRun run = upload_program(ctx, pb, false);
+  cudaEvent_t e0, e1;
+  FQ_CUDA(cudaEventCreate(&e0));
+  FQ_CUDA(cudaEventCreate(&e1));
+  launch_program(ctx, run, nullptr, false);  // warm-up
+  FQ_CUDA(cudaEventRecord(e0, ctx->stream));
+  for (int r = 0; r < reps; ++r) launch_program(ctx, run, nullptr, false);
+  FQ_CUDA(cudaEventRecord(e1, ctx->stream));
+  FQ_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  FQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  FQ_CUDA(cudaEventDestroy(e0));
+  FQ_CUDA(cudaEventDestroy(e1));
+  dfree(run.dev_phases);
+  dfree(run.fix);
+  dfree(run.flags);
+  return static_cast<double>(ms) / std::max(reps, 1);
+}
+
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x, int x_dtype, void* y,
                        int y_dtype) {
   if (!L->has(rung)) fail(FQ_E_STATE, "gemv: rung not resident on the device");

@@ -27,7 +27,10 @@ constexpr int kAttnChunk = 16;    // keys per attention work item (one warp)
 #define FQ_STAGE8 16
 #endif
 constexpr int kStageBlocks8 = FQ_STAGE8;       // W8 blocks per ring stage (2 per consumer warp)
-constexpr int kStageBlocks4 = 2 * FQ_STAGE8;   // W4 blocks per ring stage
+#ifndef FQ_STAGE4
+#define FQ_STAGE4 (2 * FQ_STAGE8)
+#endif
+constexpr int kStageBlocks4 = FQ_STAGE4;       // W4 blocks per ring stage
 constexpr int kStageBytes = kStageBlocks8 * (2048 + 80) > kStageBlocks4 * (1024 + 80) ? kStageBlocks8 * (2048 + 80)
                                                                                       : kStageBlocks4 * (1024 + 80);
 constexpr int kSmemBudget = 220 * 1024;

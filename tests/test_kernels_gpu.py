@@ -64,6 +64,31 @@ def test_gemv_fast_vs_oracle(ctx, N, K, bits, B):
 
 
 @pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("B", [1, 3])
+def test_gemv_chain_program_matches_oracle(ctx, bits, B):
+    # fq_gemv_chain_time: n independent GEMVs as one step-program launch (the C2 sweep's
+    # "program" timing) produce every layer's reference dequant+linear
+    N, K, n = 256, 1376, 3
+    rung = capi.RUNG_INT8 if bits == 8 else capi.RUNG_INT4
+    layers, refs = [], []
+    for i in range(n):
+        L, ref = _layer(ctx, _w(N, K, 900 + i), 128, (bits,))
+        layers.append(L)
+        refs.append(ref[bits])
+    x = np.random.default_rng(5).standard_normal((B, K)).astype(np.float32)
+    xt = torch.from_numpy(x).to("cuda").half().contiguous()
+    ys = [torch.empty((B, N), dtype=torch.float32, device="cuda") for _ in range(n)]
+    ms = ctx.gemv_chain_time(layers, rung, B, xt, capi.DT_F16, ys, capi.DT_F32, 2)
+    assert ms > 0
+    x16 = xt.float().cpu().numpy()
+    for y, (p, s, z) in zip(ys, refs):
+        yref = np.zeros((B, N), np.float32)
+        oracle.lib().fqo_quant_linear(np.ascontiguousarray(x16), B, p, N, K, 128, bits, 0, s.ravel(), z.ravel(), None,
+                                      yref)
+        assert _rel(y.cpu().numpy(), yref) < 1e-4
+
+
+@pytest.mark.parametrize("bits", [8, 4])
 def test_gemv_bf16_activations(ctx, bits):
     N, K = 512, 4096
     w = _w(N, K, 5)

@@ -6,8 +6,10 @@ on the launching stream:
 
 * ``cold``  — one launch after a 256 MiB L2 flush (median of --iters);
 * ``chain`` — R distinct copies of the layer (> 2x L2 in total, so every launch streams from
-  HBM) launched back to back inside one CUDA graph, as the decode step issues them; per-launch
-  time = graph time / R.
+  HBM) launched back to back inside one CUDA graph; per-launch time = graph time / R (each
+  launch pays the persistent program's start-up, ~10 us);
+* ``program`` — the same R layers as R independent phases of ONE step-program launch (no grid
+  barrier between them), as the decode step streams its linears; per-GEMV time = launch / R.
 
 Prints one JSON line per case: algorithmic bytes / time and the fraction of measured HBM peak.
 """
@@ -96,11 +98,23 @@ def main():
                         ch.append(e0.elapsed_time(e1) * 1e-3 / len(layers))
                     ch.sort()
                     t_chain = ch[len(ch) // 2]
+                    # the same layers as ONE step-program launch (independent phases, no barrier):
+                    # the TMA weight stream runs across layer boundaries as inside a decode step
+                    ys = [torch.empty(B, N, device="cuda", dtype=torch.float32) for _ in layers]
+                    t_prog = ctx.gemv_chain_time(layers, rung, B, x, capi.DT_F16, ys, capi.DT_F32,
+                                                 max(3, args.iters // 4)) * 1e-3 / len(layers)
+                    # the program's outputs are the stand-alone GEMV's
+                    ctx.gemv(layers[-1], rung, B, x, capi.DT_F16, y, capi.DT_F32)
+                    torch.cuda.synchronize()
+                    prog_err = float((ys[-1] - y).abs().max() / y.abs().max().clamp_min(1e-30))
                 byts = L0.algorithmic_bytes(rung, B)
                 print(json.dumps({"K": K, "N": N, "bits": bits, "B": B, "bytes": byts,
                                   "cold_us": round(t_cold * 1e6, 2), "cold_GBps": round(byts / t_cold / 1e9, 1),
                                   "chain_us": round(t_chain * 1e6, 2), "chain_GBps": round(byts / t_chain / 1e9, 1),
-                                  "chain_frac": round(byts / t_chain / 1e9 / hbm, 3), "peak": hbm,
+                                  "chain_frac": round(byts / t_chain / 1e9 / hbm, 3),
+                                  "program_us": round(t_prog * 1e6, 2), "program_GBps": round(byts / t_prog / 1e9, 1),
+                                  "program_frac": round(byts / t_prog / 1e9 / hbm, 3), "program_vs_gemv_maxrel": prog_err,
+                                  "layers": len(layers), "peak": hbm,
                                   "peak_kind": kind}), flush=True)
         for L in layers:
             L.close()
