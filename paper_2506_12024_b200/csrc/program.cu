@@ -1830,6 +1830,23 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
   float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) O[e] = 0.f;
+#ifndef FQ_ATTN_L2PF
+#define FQ_ATTN_L2PF 1
+#endif
+  if (FQ_ATTN_L2PF && (lane & 15) == 0) {
+    // the warp's later chunks: L2 prefetch of their K / V rows (no registers), in flight with the
+    // first chunk's loads, so the later rounds hit L2 instead of HBM
+    const __half* kc = P.kv + slot * P.slot_stride + P.layer_off + static_cast<int64_t>(h) * P.max_seq * hd;
+    const __half* vc = kc + static_cast<int64_t>(H) * P.max_seq * hd;
+    const int half = (lane >> 4) * (hd / 2);
+    for (int c = c0 + warp + kNCW; c < c1; c += kNCW) {
+      const int r1 = min((c + 1) * kAttnChunk, pos + 1);
+      for (int r = c * kAttnChunk; r < r1; ++r) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(kc + static_cast<int64_t>(r) * hd + half));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(vc + static_cast<int64_t>(r) * hd + half));
+      }
+    }
+  }
   for (int c = c0 + warp; c < c1; c += kNCW) {
     AttnRaw<DPL> R;
     attn_load<DPL>(P, slot, h, c, lane, R);
