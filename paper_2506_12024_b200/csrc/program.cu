@@ -56,7 +56,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -143,11 +142,6 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ float load_act(const void* x, int dtype, int64_t i) {
-  if (dtype == FQ_DT_F32) return static_cast<const float*>(x)[i];
-  if (dtype == FQ_DT_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(x)[i]);
-  return __half2float(static_cast<const __half*>(x)[i]);
-}
 __device__ __forceinline__ float round_act(float v, int dtype) {
   if (dtype == FQ_DT_BF16) return __bfloat162float(__float2bfloat16_rn(v));
   if (dtype == FQ_DT_F16) return __half2float(__float2half_rn(v));
@@ -180,10 +174,6 @@ __device__ __forceinline__ void frag_store_pair(__half* frag, int nkb, int b, in
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(frag) +
                             ((static_cast<int64_t>(b) * nkb + kb) * 16 + p * 4 + tig) * 4 + comp;
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
-}
-
-__device__ __forceinline__ int mat_rung(const DevMat& m, int b) {
-  return m.rung_table ? static_cast<int>(m.rung_table[b * m.rung_stride]) : m.rung;
 }
 
 // ---------------------------------------------------------------- the block sequence
@@ -324,7 +314,6 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 // The producer streams every stage through the ring; a second walk runs kPrefetchStages ahead
 // and issues L2 prefetches, so HBM keeps streaming while the ring is full (the consumers are in a
 // grid barrier, the activation staging or a non-GEMV phase) and ring refills hit L2.
-constexpr int kPrefetchStages = 8;
 
 __device__ void produce_all(const Phase* phases, int nphases, const Ring R, unsigned long long* tr, int prefetch) {
   StageWalk main, ahead;
@@ -2229,25 +2218,19 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   if (const char* e = std::getenv("FQ_PREFETCH")) r.prefetch = std::atoi(e);
   const size_t fstride = static_cast<size_t>(kMaxMat) * 16 * pb.max_bb;
   const bool inl = r.nphases <= kInlinePhases && transient;
+  // stream-K fix-up parts (only the byte-balanced partition, -DFQ_TILE_PART=0, writes them)
   float* fix;
-  unsigned int* flags;
   if (inl) {
     if (ctx->gemv_fix == nullptr) {
       ctx->gemv_fix = static_cast<float*>(dmalloc(sizeof(float2) * kInlinePhases * 1024 * kMaxMat * 16 * kMaxB));
-      ctx->gemv_flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * kInlinePhases * 1024));
-      FQ_CUDA(cudaMemset(ctx->gemv_flags, 0, sizeof(unsigned int) * kInlinePhases * 1024));
       FQ_CUDA(cudaMemset(ctx->gemv_fix, 0, sizeof(float2) * kInlinePhases * 1024 * kMaxMat * 16 * kMaxB));
     }
     if (r.grid > 1024) fail(FQ_E_CONFIG, "gemv: grid too large");
     fix = ctx->gemv_fix;
-    flags = ctx->gemv_flags;
   } else {
     r.fix = static_cast<float*>(dmalloc(sizeof(float2) * r.nphases * r.grid * fstride));
     FQ_CUDA(cudaMemset(r.fix, 0, sizeof(float2) * r.nphases * r.grid * fstride));
-    r.flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * r.nphases * r.grid));
-    FQ_CUDA(cudaMemset(r.flags, 0, sizeof(unsigned int) * r.nphases * r.grid));
     fix = r.fix;
-    flags = r.flags;
   }
   for (int i = 0; i < r.nphases; ++i) {
     Phase& P = pb.phases[i];

@@ -170,6 +170,28 @@ def test_llama_teacher_forced_logits(ctx, rung):
     assert worst <= 1e-2, worst
 
 
+@pytest.mark.parametrize("env", ["FQ_TAGS", "FQ_NO_FRAG", "FQ_NO_TAGS"])
+def test_llama_step_program_variants_match_oracle(ctx, monkeypatch, env):
+    # the opt-in hand-off variants of the step program (tagged activation words instead of the
+    # grid barrier before the O / down projections; plain staging instead of pre-staged fragments)
+    # compute the same step: teacher-forced logits within the north-star tolerance
+    monkeypatch.setenv(env, "1")
+    m, orc = _llama(ctx)
+    rungs = [8 if i % 2 else 4 for i in range(len(orc.ids))]
+    for i, r in enumerate(rungs):
+        m.set_rung(0, i, capi.RUNG_INT8 if r == 8 else capi.RUNG_INT4)
+    toks = oracle.random_tokens(10, 8192, 13)
+    out = torch.zeros((1, 8192), dtype=torch.float32, device="cuda")
+    cache = orc.new_cache()
+    for t in toks:
+        st = m.decode([0], [int(t)], out)
+        ctx.synchronize()
+        want = orc.step(int(t), cache, rungs)
+        got = out.cpu().numpy()[0]
+        assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= 1e-2
+        assert abs(st["entropy"][0] - oracle.row_stats(want)["entropy"]) <= 1e-3
+
+
 def test_llama_mixed_rungs_and_switch_is_pointer_swap(ctx):
     m, orc = _llama(ctx)
     L = m.linear(3)
@@ -207,9 +229,9 @@ def test_llama_batched_slots_match_single(ctx):
         single.append(rows)
     for t in range(8):
         for s in range(3):
-            # a heterogeneous batch streams both copies, so the stream-K split (and with it the fp32
-            # summation grouping) differs from the single-row run: equal within the north-star
-            # entropy tolerance, not bit-equal
+            # a heterogeneous batch streams both copies, so the segment layout of a tile (and with it
+            # the fp32 summation grouping) differs from the single-row run: equal within the
+            # north-star entropy tolerance, not bit-equal
             assert outs[t]["argmax"][s] == single[s][t]["argmax"]
             assert abs(outs[t]["entropy"][s] - single[s][t]["entropy"]) <= 1e-4
 
