@@ -12,6 +12,9 @@
 #ifndef FQ_DBG
 #define FQ_DBG 0
 #endif
+#ifndef FQ_SQ_B
+#define FQ_SQ_B 1  // residual tail: shuffle only the batch rows present
+#endif
 #include <cfloat>
 #include <cstring>
 #include <map>
@@ -1588,6 +1591,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     // per-CTA sum of squares of the rows this CTA finalised (RMSNorm of the next phase)
 #pragma unroll
     for (int b = 0; b < kMaxB; ++b) {
+      if (FQ_SQ_B && b >= B) break;  // warp-uniform: no shuffles for absent batch rows
       float v = sqb[b];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
