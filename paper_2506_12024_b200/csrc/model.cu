@@ -440,7 +440,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       // (measured: the merge costs the O projection's staging more than the split saves; off by
       // default, FQ_ATTN_SPLITS=n to experiment)
       const char* se = std::getenv("FQ_ATTN_SPLITS");
-      const int kMaxAttnSplit = (se && FQ_ATTN_MERGE) ? std::max(1, std::min(4, std::atoi(se))) : 1;
+      const int kMaxAttnSplit = se ? std::max(1, std::min(4, std::atoi(se))) : 1;  // needs FQ_ATTN_MERGE device code
       const int attn_splits = gemv_only ? 1
           : std::max(1, std::min(std::min(kMaxAttnSplit, M->n_chunks), G / std::max(1, B * static_cast<int>(c.n_heads))));
       for (int64_t l = 0; l < c.n_layers; ++l) {

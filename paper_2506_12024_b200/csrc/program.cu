@@ -385,109 +385,6 @@ static_assert(kMaxB <= kNCW, "one consumer warp per batch row computes its RMSNo
 // splits' unnormalised partials are merged here, x = sum_s O_s e^(m_s - M) / sum_s l_s e^(m_s - M),
 // rounded to the activation dtype exactly as the unsplit attention rounds its output.  All loads
 // (every split's O values of this thread's items and the (m, l) pairs) go out together.
-#if FQ_ATTN_MERGE
-constexpr int kMaxAttnSplits = 4;
-__device__ __noinline__ void stage_attn_merge(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
-  const int B = P.B;
-  const int tid = threadIdx.x;
-  constexpr int NT = kNCW * 32;
-  const int H = P.n_heads, hd = P.head_dim, ns = P.attn_splits;
-  const int64_t pst = hd + 4;
-  const float* parts = P.attn_ws;
-  float* wsm = G.red;  // [b * H + h][ns] merge weights (the reduction window is free while staging)
-  const int items = P.nkb * B * 16;
-  const int64_t K = P.K;
-  const int adt = P.act_dtype;
-  for (int base = 0;; base += NT * kStageItems) {
-    float raw[kStageItems][kMaxAttnSplits][8];
-#pragma unroll
-    for (int s = 0; s < kStageItems; ++s) {
-      const int it = base + s * NT + tid;
-      const bool active = it < items;
-      const int kb = it / (B * 16);
-      const int rem = it - kb * B * 16;
-      const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int hh = e >> 2, q = e & 3;
-        int64_t kk = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
-        kk = active ? min(kk, K - 1) : 0;
-        const int h = static_cast<int>(kk / hd), j = static_cast<int>(kk - static_cast<int64_t>(h) * hd);
-        const float* src = parts + (static_cast<int64_t>(b) * H + h) * ns * pst + j;
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp) raw[s][sp][e] = sp < ns ? src[sp * pst] : 0.f;
-      }
-    }
-    if (base == 0) {
-      for (int bh = tid; bh < B * H; bh += NT) {
-        const float* src = parts + static_cast<int64_t>(bh) * ns * pst + hd;
-        float2 ml[kMaxAttnSplits];
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-          ml[sp] = sp < ns ? *reinterpret_cast<const float2*>(src + sp * pst) : make_float2(-INFINITY, 0.f);
-        float M = -INFINITY;
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp) M = fmaxf(M, ml[sp].x);
-        float Lt = 0.f, f[kMaxAttnSplits];
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp) {
-          f[sp] = ml[sp].x == -INFINITY ? 0.f : expf(ml[sp].x - M);
-          Lt += ml[sp].y * f[sp];
-        }
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-          if (sp < ns) wsm[bh * ns + sp] = f[sp] / Lt;
-      }
-      if (gp) gp[1] = gtimer();
-      named_sync(1, NT);
-      if (gp) gp[2] = gtimer();
-    }
-#pragma unroll
-    for (int s = 0; s < kStageItems; ++s) {
-      const int it = base + s * NT + tid;
-      const bool active = it < items;
-      const int kb = it / (B * 16);
-      const int rem = it - kb * B * 16;
-      const int b = active ? rem >> 4 : 0, p = (rem >> 2) & 3, tig = rem & 3;
-      float lo = 0.f, hi = 0.f;
-      uint32_t hq[4];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = 4 * hh + q;
-          const int64_t kk = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + hh) + 2 * tig + (q & 1) + 8 * (q >> 1);
-          const int h = static_cast<int>(min(kk, K - 1) / hd);
-          const float* w = wsm + (b * H + h) * ns;
-          float t = 0.f;
-#pragma unroll
-          for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-            if (sp < ns) t += raw[s][sp][e] * w[sp];
-          t = round_act(t, adt);
-          t = (active && kk < K) ? t : 0.f;
-          v[q] = __half2float(__float2half_rn(t));
-        }
-        lo += v[0] + v[1];
-        hi += v[2] + v[3];
-        const __half2 p01 = __floats2half2_rn(v[0], v[1]), p89 = __floats2half2_rn(v[2], v[3]);
-        hq[2 * hh] = *reinterpret_cast<const uint32_t*>(&p01);
-        hq[2 * hh + 1] = *reinterpret_cast<const uint32_t*>(&p89);
-      }
-      if (active) G.xs[(static_cast<size_t>(b) * P.nkb + kb) * 16 + p * 4 + tig] = make_uint4(hq[0], hq[1], hq[2], hq[3]);
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        lo += __shfl_xor_sync(0xffffffffu, lo, o);
-        hi += __shfl_xor_sync(0xffffffffu, hi, o);
-      }
-      if (active && (rem & 15) == 0) G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
-    }
-    if (base + NT * kStageItems >= items) break;
-  }
-  named_sync(1, NT);
-}
-
-#endif  // FQ_ATTN_MERGE
 
 // Vectorised staging (16-byte loads of 8 consecutive activations): one load per 8 values (two
 // for fp32 inputs / gains), every load of the phase in flight together when they fit VB vectors
@@ -602,6 +499,115 @@ __device__ __forceinline__ bool stage_vec_ok(const Phase& P) {
          (P.norm_gain == nullptr || (reinterpret_cast<uintptr_t>(P.norm_gain) & 15) == 0);
 }
 
+// Per-block activation sums dx from fragment-ordered activations in shared memory (one warp per
+// 128-block: four halves per lane, shuffle tree), then a consumer barrier.
+__device__ __forceinline__ void frag_block_sums(const Phase& P, const GemvSmem& G) {
+  const int B = P.B, nkb = P.nkb, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int blk = warp; blk < B * nkb; blk += kNCW) {
+    const uint2 h4 = reinterpret_cast<const uint2*>(G.xs + static_cast<size_t>(blk) * 16)[lane];
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h4.x));
+    const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h4.y));
+    float sum = (a.x + a.y) + (c.x + c.y);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int b = blk / nkb, kb = blk - b * nkb;
+    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
+  }
+  named_sync(1, kNCW * 32);
+}
+
+#if FQ_ATTN_MERGE
+// Staging of the O projection's input when the attention phase ran split (attn_splits > 1): each
+// split wrote its unnormalised partial (O[hd] fp32, m, l); this thread's fragment slots load the
+// (k, k+1) pairs of every split (float2 loads, all in flight with the (m, l) loads of the merge
+// weights), then x = sum_s O_s w_s with w_s = e^(m_s - M) / sum_t l_t e^(m_t - M), rounded to the
+// activation dtype as the unsplit attention rounds its output, then fp16 into fragment order.
+constexpr int kMaxAttnSplits = 4;
+constexpr int kMergeSlots = 2;  // uint4 fragment slots per thread per round (K = 4096 at B = 1: 512)
+__device__ __forceinline__ void stage_attn_merge(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
+  const int B = P.B, nkb = P.nkb;
+  const int tid = threadIdx.x;
+  constexpr int NT = kNCW * 32;
+  const int H = P.n_heads, hd = P.head_dim, ns = P.attn_splits;
+  const int64_t pst = hd + 4;
+  const float* parts = P.attn_ws;
+  float* wsm = G.red;  // [b * H + h][ns] merge weights (the reduction window is free while staging)
+  uint32_t* xs32 = reinterpret_cast<uint32_t*>(G.xs);
+  const int n = B * nkb * 16;
+  const int64_t K = P.K;
+  const int adt = P.act_dtype;
+  for (int base = 0; base < n || base == 0; base += NT * kMergeSlots) {
+    float2 o[kMergeSlots][4][kMaxAttnSplits];
+#pragma unroll
+    for (int i = 0; i < kMergeSlots; ++i) {
+      const int u = base + i * NT + tid;
+      const int b = u / (nkb * 16), r = u - b * nkb * 16, kb = r >> 4, p = (r >> 2) & 3, tg = r & 3;
+#pragma unroll
+      for (int comp = 0; comp < 4; ++comp) {
+        const int64_t k = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + (comp >> 1)) + 2 * tg + 8 * (comp & 1);
+        const bool on = u < n && k < K;
+        const int h = on ? static_cast<int>(k / hd) : 0, j = on ? static_cast<int>(k - static_cast<int64_t>(h) * hd) : 0;
+        const float* src = parts + (static_cast<int64_t>(on ? b : 0) * H + h) * ns * pst + j;
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+          o[i][comp][sp] = (on && sp < ns) ? *reinterpret_cast<const float2*>(src + sp * pst) : make_float2(0.f, 0.f);
+      }
+    }
+    if (base == 0) {
+      for (int bh = tid; bh < B * H; bh += NT) {
+        const float* src = parts + static_cast<int64_t>(bh) * ns * pst + hd;
+        float2 ml[kMaxAttnSplits];
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+          ml[sp] = sp < ns ? *reinterpret_cast<const float2*>(src + sp * pst) : make_float2(-INFINITY, 0.f);
+        float M = -INFINITY;
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp) M = fmaxf(M, ml[sp].x);
+        float Lt = 0.f, f[kMaxAttnSplits];
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp) {
+          f[sp] = ml[sp].x == -INFINITY ? 0.f : expf(ml[sp].x - M);
+          Lt += ml[sp].y * f[sp];
+        }
+#pragma unroll
+        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+          if (sp < ns) wsm[bh * ns + sp] = f[sp] / Lt;
+      }
+      if (gp) gp[1] = gtimer();
+      named_sync(1, NT);
+      if (gp) gp[2] = gtimer();
+    }
+#pragma unroll
+    for (int i = 0; i < kMergeSlots; ++i) {
+      const int u = base + i * NT + tid;
+      if (u >= n) continue;
+      const int b = u / (nkb * 16), r = u - b * nkb * 16, kb = r >> 4, p = (r >> 2) & 3, tg = r & 3;
+#pragma unroll
+      for (int comp = 0; comp < 4; ++comp) {
+        const int64_t k = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + (comp >> 1)) + 2 * tg + 8 * (comp & 1);
+        float v0 = 0.f, v1 = 0.f;
+        if (k < K) {
+          const float* w = wsm + (b * H + static_cast<int>(k / hd)) * ns;
+#pragma unroll
+          for (int sp = 0; sp < kMaxAttnSplits; ++sp)
+            if (sp < ns) {
+              v0 = fmaf(o[i][comp][sp].x, w[sp], v0);
+              v1 = fmaf(o[i][comp][sp].y, w[sp], v1);
+            }
+          v0 = round_act(v0, adt);
+          v1 = round_act(v1, adt);
+        }
+        const __half2 h2 = __floats2half2_rn(v0, v1);
+        xs32[u * 4 + comp] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+    }
+    if (base + NT * kMergeSlots >= n) break;
+  }
+  named_sync(1, NT);
+  frag_block_sums(P, G);
+}
+#endif  // FQ_ATTN_MERGE
+
 // Staging of an input the producing phase already wrote in fragment order: a straight copy (all
 // loads of the phase in flight together), then the per-block sums dx from shared memory (one warp
 // per 128-block: four halves per lane, shuffle tree).
@@ -688,17 +694,7 @@ __device__ __noinline__ void stage_frag_copy(const Phase& P, const GemvSmem& G, 
   if (gp) gp[1] = gtimer();
   named_sync(1, NT);
   if (gp) gp[2] = gtimer();
-  for (int blk = warp; blk < B * nkb; blk += kNCW) {
-    const uint2 h4 = reinterpret_cast<const uint2*>(G.xs + static_cast<size_t>(blk) * 16)[lane];
-    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h4.x));
-    const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h4.y));
-    float sum = (a.x + a.y) + (c.x + c.y);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const int b = blk / nkb, kb = blk - b * nkb;
-    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
-  }
-  named_sync(1, NT);
+  frag_block_sums(P, G);
 }
 
 #ifndef FQ_VEC_STAGE
