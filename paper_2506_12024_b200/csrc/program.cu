@@ -12,6 +12,15 @@
 #ifndef FQ_DBG
 #define FQ_DBG 0
 #endif
+// once-per-step phases (embedding, statistics, prefill append): out of line unless FQ_STEP_INLINE
+#ifndef FQ_STEP_INLINE
+#define FQ_STEP_INLINE 0
+#endif
+#if FQ_STEP_INLINE
+#define FQ_ONCE __device__ __forceinline__
+#else
+#define FQ_ONCE __device__ __noinline__
+#endif
 #ifndef FQ_SQ_B
 #define FQ_SQ_B 1  // residual tail: shuffle only the batch rows present
 #endif
@@ -1626,7 +1635,7 @@ __device__ __forceinline__ void cta_rows(int64_t N, int64_t& r0, int& rows) {
   rows = static_cast<int>((N * (blockIdx.x + 1)) / gridDim.x - r0);
 }
 
-__device__ __noinline__ void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
+FQ_ONCE void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int64_t c0;
   int cnt;
@@ -1937,7 +1946,7 @@ __device__ void append_item(const Phase& P, int b, int h, int lane) {
   }
 }
 
-__device__ __noinline__ void run_append(const Phase& P) {
+FQ_ONCE void run_append(const Phase& P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = P.B * P.n_heads;
   for (int item = warp * gridDim.x + blockIdx.x; item < total; item += gridDim.x * kNCW) {
@@ -1948,7 +1957,7 @@ __device__ __noinline__ void run_append(const Phase& P) {
 }
 
 #ifndef FQ_ATTN_INLINE
-#define FQ_ATTN_INLINE 0
+#define FQ_ATTN_INLINE 1  // measured -1.2% per step vs an out-of-line call
 #endif
 #if FQ_ATTN_INLINE
 __device__ __forceinline__
@@ -1972,7 +1981,7 @@ void run_attn(const Phase& P, AttnSmem& S, const MetaSmem& MS, unsigned int tag)
 // Combines the head GEMV's per-CTA softmax partials of row b (warp b of CTA 0, fixed-order merge)
 // into fq_row_stats: ppl_entropy / fault_tolerance / argmax_token (src/scheduler.cpp:13-49,
 // src/engine.cpp:144-155) in double.
-__device__ __noinline__ void run_stats(const Phase& P) {
+FQ_ONCE void run_stats(const Phase& P) {
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const StatPart* parts = static_cast<const StatPart*>(P.stat_part);
