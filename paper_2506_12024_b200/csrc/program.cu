@@ -21,6 +21,12 @@
 #else
 #define FQ_ONCE __device__ __noinline__
 #endif
+#ifndef FQ_W4_LO
+// W4 unpack with one shift per word: the k%16 < 8 halves of each 16-column chunk as 1024 + q
+// (bits 0-3), the k%16 >= 8 halves as 64 + q (bits 4-7); the block fold subtracts
+// 1024 X_lo + 64 X_hi (dx.y) instead of 64 X
+#define FQ_W4_LO 0  // opt-in: -5% W4 step, but 15-25x the W4 cancellation error (tools/w4_error_probe.py)
+#endif
 #ifndef FQ_SQ_B
 #define FQ_SQ_B 1  // residual tail: shuffle only the batch rows present
 #endif
@@ -139,6 +145,12 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 // (v & 0x00F000F0) | 0x54005400 in one LOP3: the two nibbles at bits 4-7 / 20-23 as fp16 64 + q.
 // Written as PTX with both constants immediate so ptxas keeps one in a register instead of
 // splitting the AND and the OR (the W4 unpack is ALU-bound).
+// (v & 0x000F000F) | 0x64006400: the nibbles at bits 0-3 / 16-19 as fp16 1024 + q (no shift).
+__device__ __forceinline__ uint32_t nib_lo_f16(uint32_t v) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(r) : "r"(v));
+  return r;
+}
 __device__ __forceinline__ uint32_t nib_f16(uint32_t v) {
   uint32_t r;
   asm("lop3.b32 %0, %1, 0x00F000F0, 0x54005400, 0xEA;" : "=r"(r) : "r"(v));
@@ -493,9 +505,14 @@ __device__ __forceinline__ void stage_vec(const Phase& P, const GemvSmem& G, uns
         for (int i = 0; i < 4; ++i) dst[4 * i] = hp[i];
       }
       // the 16 vectors of a block sit on 16 consecutive lanes (v is 16-aligned per half-warp)
+      float slo = (c & 1) ? 0.f : sum;  // k % 16 < 8 (the W4 1024-offset halves)
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (v < nvec && c == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
+      for (int o = 8; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (FQ_W4_LO) slo += __shfl_xor_sync(0xffffffffu, slo, o);
+      }
+      if (v < nvec && c == 0)
+        G.dx[kb * B + b] = make_float4(1024.f * sum, FQ_W4_LO ? 1024.f * slo + 64.f * (sum - slo) : 64.f * sum, sum, 0.f);
     }
     if (base + NT * VB >= nvec) break;
   }
@@ -516,11 +533,18 @@ __device__ __forceinline__ void frag_block_sums(const Phase& P, const GemvSmem& 
     const uint2 h4 = reinterpret_cast<const uint2*>(G.xs + static_cast<size_t>(blk) * 16)[lane];
     const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h4.x));
     const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h4.y));
+    float lo = a.x + a.y, hi = c.x + c.y;  // h4.x: k % 16 < 8, h4.y: k % 16 >= 8
     float sum = (a.x + a.y) + (c.x + c.y);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (FQ_W4_LO) {
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
+        hi += __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+    }
     const int b = blk / nkb, kb = blk - b * nkb;
-    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
+    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, FQ_W4_LO ? 1024.f * lo + 64.f * hi : 64.f * sum, sum, 0.f);
   }
   named_sync(1, kNCW * 32);
 }
@@ -852,7 +876,8 @@ __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long
         lo += __shfl_xor_sync(0xffffffffu, lo, o);
         hi += __shfl_xor_sync(0xffffffffu, hi, o);
       }
-      if (active && (rem & 15) == 0) G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
+      if (active && (rem & 15) == 0)
+        G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), FQ_W4_LO ? 1024.f * lo + 64.f * hi : 64.f * (lo + hi), lo + hi, 0.f);
     }
     if (base + NT * kStageItems >= items) break;
   }
@@ -903,6 +928,10 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
           // every nibble pair is moved to bits 4-7 / 20-23 of the halves: fp16 0x5400 | q<<4 = 64 + q
           const uint32_t q = qs[u];
           const uint4 xv = u < 2 ? x0 : x1;
+          if (FQ_W4_LO)
+            mma16816(c[n], nib_lo_f16(q), nib_lo_f16(q >> 8), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
+                     (u & 1) ? xv.w : xv.y);
+          else
           mma16816(c[n], nib_f16(q << 4), nib_f16(q >> 4), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
                    (u & 1) ? xv.w : xv.y);
         }
