@@ -383,7 +383,7 @@ def main():
             "dtype": "bf16",
             "data": "synthetic",
             "config": {
-                "workload": f"{cfg['name']} (BASELINE config 3): B=1 per GPU, {cfg['prompt']}-token random prompt, "
+                "workload": f"{cfg['name']} (BASELINE config {3 if args.config == 'c3' else 1}): B=1 per GPU, {cfg['prompt']}-token random prompt, "
                             f"decode positions {cfg['prompt']}..{cfg['prompt'] + args.warmup + args.steps}, "
                             "W8 start, 8->4 plan ordered by weight-histogram KL (2048 bins)",
                 "model": cfg["name"], "global_batch": world, "seq_len": cfg["prompt"] + args.warmup + args.steps,
