@@ -1,0 +1,52 @@
+"""BASELINE config 4 at full scale: KL layer-sensitivity calibration on the 7B shape.
+
+64 random-token sequences x 512 tokens; for each of the 32 blocks that block's linears are set to
+W4 with all others W8, and the mean KL(softmax(logits_q) || softmax(logits_w8)) over the 32000
+vocabulary plus the mean entropy are measured (fq_model_calibrate_logit_kl: the prefill runs on
+the tcgen05 dequant-GEMM, KL / entropy on the device).  Prints one JSON line: wall time, the
+implied tensor throughput (2 * params * tokens * 33 forwards), and the block ranking that
+build_switch_plan orders (ascending KL, ties by index).
+
+  python tools/calibrate_c4.py --seqs 64 --len 512
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_12024_b200 import capi  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seqs", type=int, default=64)
+    ap.add_argument("--len", type=int, default=512)
+    ap.add_argument("--layers", type=int, default=32)
+    a = ap.parse_args()
+    ctx = capi.Context(0)
+    m = capi.Model(ctx, arch=capi.ARCH_LLAMA, act_dtype=capi.DT_BF16, max_batch=1, group_size=128,
+                   max_seq_len=a.len + 8, vocab_size=32000, d_model=4096, n_heads=32, head_dim=128,
+                   n_layers=a.layers, ffn_dim=11008)
+    m.init_random(1234, 0.02)
+    toks = np.random.default_rng(4).integers(0, 32000, (a.seqs, a.len)).astype(np.int32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    kl, ent = m.calibrate_logit_kl(toks, capi.RUNG_INT8, capi.RUNG_INT4)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    params = a.layers * (4 * 4096 * 4096 + 3 * 4096 * 11008) + 32000 * 4096
+    flops = 2.0 * params * a.seqs * a.len * (a.layers + 1)
+    order = sorted(range(a.layers), key=lambda i: (kl[i], i))
+    print(json.dumps({"config": "C4", "seqs": a.seqs, "len": a.len, "blocks": a.layers, "forwards": a.layers + 1,
+                      "seconds": round(dt, 2), "tflops": round(flops / dt / 1e12, 1),
+                      "kl_min": float(np.min(kl)), "kl_max": float(np.max(kl)),
+                      "entropy_mean": float(np.mean(ent)), "switch_order_blocks": order}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
