@@ -23,8 +23,15 @@
 namespace fqc {
 namespace {
 
+#ifndef FQ_GEMM_TN
+#define FQ_GEMM_TN 256
+#endif
+#ifndef FQ_GEMM_STAGES
+#define FQ_GEMM_STAGES 2
+#endif
 constexpr int kTM = 128;   // weight rows per CTA (UMMA M)
-constexpr int kTN = 256;   // tokens per CTA (UMMA N)
+constexpr int kTN = FQ_GEMM_TN;  // tokens per CTA (UMMA N)
+constexpr int kStagesG = FQ_GEMM_STAGES;  // smem stages: activations are loaded kStagesG - 1 k-steps ahead
 constexpr int kTK = 128;   // codes per k-step (one tiled block / quantization group)
 constexpr int kATileBytes = kTM * kTK * 2;  // bf16 weight tile: 32 KB
 constexpr int kBTileBytes = kTN * kTK * 2;  // bf16 activation tile: 64 KB
@@ -194,9 +201,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
                                                                   float* __restrict__ y, int64_t y_stride, int accumulate,
                                                                   int splits, int64_t split_stride) {
   extern __shared__ __align__(1024) uint8_t gsm[];
-  __shared__ uint64_t mma_done[2];
+  __shared__ uint64_t mma_done[kStagesG];
   __shared__ uint32_t tmem_base_s;
-  uint8_t* stage_base = gsm;  // 2 stages x (A 32 KB | B 64 KB)
+  uint8_t* stage_base = gsm;  // kStagesG stages x (A 32 KB | B kTN x 256 B)
   const int warp = threadIdx.x >> 5;
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
   const int t0 = blockIdx.y * kTN;
@@ -205,8 +212,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   const int kb1 = static_cast<int>(static_cast<int64_t>(nkb) * (blockIdx.z + 1) / splits);
   y += blockIdx.z * split_stride;
   if (threadIdx.x == 0) {
-    mbar_init1(&mma_done[0]);
-    mbar_init1(&mma_done[1]);
+    for (int q = 0; q < kStagesG; ++q) mbar_init1(&mma_done[q]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -218,9 +224,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phase[kStagesG];
+#pragma unroll
+  for (int q = 0; q < kStagesG; ++q) phase[q] = 0u;
   StepRaw<W> cur, nxt;
-  load_tokens_async(x, x_stride, T, K, t0, kb0, stage_base + kATileBytes);
+  // activation tiles of the first kStagesG - 1 k-steps (one cp.async group each, empty past kb1)
+#pragma unroll
+  for (int q = 0; q < kStagesG - 1; ++q) {
+    if (kb0 + q < kb1) load_tokens_async(x, x_stride, T, K, t0, kb0 + q, stage_base + q * kStageBytesG + kATileBytes);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   load_step<W>(tiles, tile0, n_tiles, nkb, kb0, zbase, cur);
   // Pipeline: k-step kb dequantises into stage s = kb & 1 while the MMAs of kb - 1 run; right
   // after kb's MMAs are issued, the MMAs of kb - 1 (the other stage's last reader) are waited for
@@ -228,12 +241,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
   // dequantisation waits on the other in steady state.
   for (int kb = kb0; kb < kb1; ++kb) {
     const int i = kb - kb0;
-    const int s = i & 1;
+    const int s = i % kStagesG;
     const bool more = kb + 1 < kb1;
     uint8_t* at = stage_base + s * kStageBytesG;
     if (more) load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, nxt);
     store_step<W, F16>(cur, tile0, n_tiles, at);
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // this step's activation group is complete; the kStagesG - 2 newer ones may still be in flight
+    asm volatile("cp.async.wait_group %0;" ::"n"(kStagesG - 2) : "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -253,17 +267,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t*
                        smem_addr(&mma_done[s]))
                    : "memory");
     }
-    if (more) {
-      if (i >= 1) {
-        mbar_wait1(&mma_done[s ^ 1], phase[s ^ 1]);
-        phase[s ^ 1] ^= 1u;
-      }
-      load_tokens_async(x, x_stride, T, K, t0, kb + 1, stage_base + (s ^ 1) * kStageBytesG + kATileBytes);
-      cur = nxt;
+    // the stage of step i - 1 (= that of step i + kStagesG - 1) is free once MMA(i - 1) is done:
+    // refill its activation tile kStagesG - 1 steps ahead (an empty group past kb1)
+    if (i >= 1) {
+      const int sp = (i - 1) % kStagesG;
+      mbar_wait1(&mma_done[sp], phase[sp]);
+      phase[sp] ^= 1u;
     }
+    if (kb + kStagesG - 1 < kb1)
+      load_tokens_async(x, x_stride, T, K, t0, kb + kStagesG - 1,
+                        stage_base + ((i + kStagesG - 1) % kStagesG) * kStageBytesG + kATileBytes);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    if (more) cur = nxt;
   }
   // wait for the last commit (it covers every earlier MMA of this thread)
-  const int last = (kb1 - kb0 - 1) & 1;
+  const int last = (kb1 - kb0 - 1) % kStagesG;
   mbar_wait1(&mma_done[last], phase[last]);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // epilogue: warp w (of the first four) owns accumulator lanes 32w .. 32w+31 (weight rows);
@@ -360,7 +379,7 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
     split_stride = T * L->N;
   }
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
-  const size_t smem = 2 * static_cast<size_t>(kStageBytesG);
+  const size_t smem = static_cast<size_t>(kStagesG) * kStageBytesG;
   const auto* xs = static_cast<const uint16_t*>(x);
   const int acc = splits > 1 ? 0 : (accumulate ? 1 : 0);
   const int Ti = static_cast<int>(T);
