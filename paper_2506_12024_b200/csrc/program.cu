@@ -27,6 +27,9 @@
 // 1024 X_lo + 64 X_hi (dx.y) instead of 64 X
 #define FQ_W4_LO 0  // opt-in: -5% W4 step, but 15-25x the W4 cancellation error (tools/w4_error_probe.py)
 #endif
+#ifndef FQ_GEMV_HOOKS
+#define FQ_GEMV_HOOKS 1  // per-phase GEMV detail stamps (tools/phase_profile.py); 0 compiles them out
+#endif
 #ifndef FQ_SQ_B
 #define FQ_SQ_B 1  // residual tail: shuffle only the batch rows present
 #endif
@@ -1500,7 +1503,8 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
                                int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab, unsigned int tag,
                                unsigned long long* gprof) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long* gpa = gprof ? gprof + (static_cast<size_t>(phase_idx) * gridDim.x + blockIdx.x) * 8 : nullptr;
+  unsigned long long* gpa = (FQ_GEMV_HOOKS && gprof) ? gprof + (static_cast<size_t>(phase_idx) * gridDim.x + blockIdx.x) * 8
+                                                      : nullptr;  // compiled out: every gp test folds away
   unsigned long long* gp = threadIdx.x == 0 ? gpa : nullptr;
   if (warp == 1) {
     phase_setup(P, C, red_floats, lane, gpa, ctab ? ctab + phase_idx : nullptr);  // warp 0: norm factors
