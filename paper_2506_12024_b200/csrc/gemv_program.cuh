@@ -84,7 +84,11 @@ struct alignas(16) Phase {
   int yfrag_nkb;          // 128-blocks per batch row of yfrag; < 0: tagged words, nkb = -yfrag_nkb
   float* fix;             // stream-K fix-up partials [grid][kMaxMat * 16 * kMaxB]
   // ---- EMBED / ATTN / STATS (decode step)
-  const float* tok_emb;
+  union {
+    const float* tok_emb;     // EMBED
+    unsigned int* tile_flags; // QKV GEMV: stamps each finished 16-row tile with the phase tag;
+                              // ATTN: polls its head's tiles instead of a grid barrier (decode)
+  };
   const int32_t* tokens;
   const int32_t* pos;
   const int32_t* slots;

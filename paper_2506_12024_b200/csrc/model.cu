@@ -307,6 +307,7 @@ struct fq_model {
   void* v = nullptr;
   void* attn = nullptr;        // [B, d]
   void* mid = nullptr;         // [B, ffn]
+  unsigned int* tile_flags = nullptr;  // [d/16] QKV tile stamps (FQ_HEAD_FLAGS)
   void* attn_frag = nullptr;   // [B][d/128][16] uint4: attention output in B-fragment order (fp16)
   void* mid_frag = nullptr;    // [B][ffn/128][16] uint4: SwiGLU output in B-fragment order
   float* tmp = nullptr;        // [B, max(d, ffn)] fp32 (reference)
@@ -434,6 +435,10 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       // consumers see the words ~6 us after the attention CTAs finish vs ~3.5 us for barrier +
       // staging, so the barriers stay the default.
       const bool tagged = use_frag && std::getenv("FQ_TAGS") != nullptr;
+      // QKV -> attention through per-tile flags instead of a grid barrier (decode, one QKV phase,
+      // unsplit attention over whole 16-row tiles per head)
+      const bool head_flags = std::getenv("FQ_HEAD_FLAGS") != nullptr && mode == STEP_DECODE && B <= kMaxB &&
+                              c.head_dim % 16 == 0 && M->tile_flags != nullptr;
       const int frag_nkb_d = static_cast<int>((d + kBlockK - 1) / kBlockK);
       // attention work items: (row, head, split); with few rows the keys of a head are split over
       // up to kMaxAttnSplit CTAs and the O projection's staging merges the partials
@@ -467,6 +472,10 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         g.y_dtype = c.act_dtype;
         g.y_stride = d;
         add_chunked(pb, g, B);
+        if (head_flags) {
+          pb.phases.back().tile_flags = M->tile_flags;
+          pb.phases.back().barrier_after = 0;
+        }
         if (prefill) {
           Phase ap{};
           ap.type = PH_APPEND;
@@ -508,6 +517,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
           a.attn_ws = M->attn_ws;
           a.attn_out = M->attn;
           a.attn_splits = attn_splits;
+          if (head_flags) a.tile_flags = M->tile_flags;
           if (use_frag && attn_splits == 1) {
             a.yfrag = static_cast<__half*>(M->attn_frag);
             a.yfrag_nkb = tagged ? -frag_nkb_d : frag_nkb_d;
@@ -1091,6 +1101,8 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     {
       const int64_t fd = (d + kBlockK - 1) / kBlockK * kBlockK, ff = (ffn + kBlockK - 1) / kBlockK * kBlockK;
       // room for the tagged form: one 8-byte (half2, tag) word per activation pair
+      M->tile_flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * ((d + 15) / 16)));
+      FQ_CUDA(cudaMemsetAsync(M->tile_flags, 0, sizeof(unsigned int) * ((d + 15) / 16), st));
       M->attn_frag = dmalloc(4 * B * fd);
       M->mid_frag = dmalloc(4 * B * ff);
       FQ_CUDA(cudaMemsetAsync(M->attn_frag, 0, 4 * B * fd, st));  // padding past K stays zero
@@ -1167,6 +1179,7 @@ fq_status fq_model_destroy(fq_model* M) {
     dfree(M->v);
     dfree(M->attn);
     dfree(M->mid);
+    dfree(M->tile_flags);
     dfree(M->attn_frag);
     dfree(M->mid_frag);
     dfree(M->tmp);

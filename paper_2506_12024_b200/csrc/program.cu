@@ -1659,6 +1659,12 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     }
   }
   named_sync(1, kNCW * 32);  // staging / reduction buffers and C are reused by the next phase
+  if (P.tile_flags != nullptr && threadIdx.x == 0 && C.ntiles > 0) {
+    // every epilogue store of this CTA's tiles is ordered before the stamps (bar.sync + fence)
+    __threadfence();
+    for (int l = 0; l < C.ntiles; ++l)
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.tile_flags + C.tile0 + l), "r"(tag) : "memory");
+  }
   if (gp) gp[6] = gtimer();
 }
 
@@ -1873,6 +1879,21 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
   const int nch = (pos + kAttnChunk) / kAttnChunk;
   const int c0 = (nch * sp) / ns, c1 = (nch * (sp + 1)) / ns;
   const int64_t qoff = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
+  if (P.tile_flags != nullptr) {
+    // no grid barrier after the QKV phase: wait for the head's hd / 16 tiles of q / k / v only
+    const int fph = hd / 16;
+    const unsigned int want = tag - 1;  // the QKV phase precedes this one
+    const unsigned long long t0 = gtimer_now();
+    for (;;) {
+      unsigned int f = want;
+      if (lane < fph)
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.tile_flags + h * fph + lane) : "memory");
+      if (__all_sync(0xffffffffu, f == want)) break;
+      __nanosleep(32);
+      if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("head tile flags", h, static_cast<int>(want));
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
   float q[DPL];
   float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
