@@ -437,7 +437,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       const bool tagged = use_frag && std::getenv("FQ_TAGS") != nullptr;
       // QKV -> attention through per-tile flags instead of a grid barrier (decode, one QKV phase,
       // unsplit attention over whole 16-row tiles per head)
-      const bool head_flags = std::getenv("FQ_HEAD_FLAGS") != nullptr && mode == STEP_DECODE && B <= kMaxB &&
+      const bool head_flags = FQ_HEAD_FLAGS_DEV && std::getenv("FQ_HEAD_FLAGS") != nullptr && mode == STEP_DECODE && B <= kMaxB &&
                               c.head_dim % 16 == 0 && M->tile_flags != nullptr;
       const int frag_nkb_d = static_cast<int>((d + kBlockK - 1) / kBlockK);
       // attention work items: (row, head, split); with few rows the keys of a head are split over

@@ -1659,7 +1659,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     }
   }
   named_sync(1, kNCW * 32);  // staging / reduction buffers and C are reused by the next phase
-  if (P.tile_flags != nullptr && threadIdx.x == 0 && C.ntiles > 0) {
+  if (FQ_HEAD_FLAGS_DEV && P.tile_flags != nullptr && threadIdx.x == 0 && C.ntiles > 0) {
     // every epilogue store of this CTA's tiles is ordered before the stamps (bar.sync + fence)
     __threadfence();
     for (int l = 0; l < C.ntiles; ++l)
@@ -1879,7 +1879,7 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
   const int nch = (pos + kAttnChunk) / kAttnChunk;
   const int c0 = (nch * sp) / ns, c1 = (nch * (sp + 1)) / ns;
   const int64_t qoff = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
-  if (P.tile_flags != nullptr) {
+  if (FQ_HEAD_FLAGS_DEV && P.tile_flags != nullptr) {
     // no grid barrier after the QKV phase: wait for the head's hd / 16 tiles of q / k / v only
     const int fph = hd / 16;
     const unsigned int want = tag - 1;  // the QKV phase precedes this one

@@ -170,7 +170,7 @@ def test_llama_teacher_forced_logits(ctx, rung):
     assert worst <= 1e-2, worst
 
 
-@pytest.mark.parametrize("env", ["FQ_TAGS", "FQ_NO_FRAG", "FQ_NO_TAGS"])
+@pytest.mark.parametrize("env", ["FQ_TAGS", "FQ_NO_FRAG", "FQ_NO_TAGS", "FQ_HEAD_FLAGS"])
 def test_llama_step_program_variants_match_oracle(ctx, monkeypatch, env):
     # the opt-in hand-off variants of the step program (tagged activation words instead of the
     # grid barrier before the O / down projections; plain staging instead of pre-staged fragments)
