@@ -434,7 +434,7 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       // phase per projection, i.e. B <= kMaxB).  Measured +18% per step at the 7B shape: the
       // consumers see the words ~6 us after the attention CTAs finish vs ~3.5 us for barrier +
       // staging, so the barriers stay the default.
-      const bool tagged = use_frag && std::getenv("FQ_TAGS") != nullptr;
+      const bool tagged = FQ_TAGS_DEV && use_frag && std::getenv("FQ_TAGS") != nullptr;
       // QKV -> attention through per-tile flags instead of a grid barrier (decode, one QKV phase,
       // unsplit attention over whole 16-row tiles per head)
       const bool head_flags = FQ_HEAD_FLAGS_DEV && std::getenv("FQ_HEAD_FLAGS") != nullptr && mode == STEP_DECODE && B <= kMaxB &&

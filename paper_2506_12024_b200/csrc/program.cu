@@ -670,7 +670,7 @@ void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = kNCW * 32;
   const int n = B * nkb * 16;
-  if (P.xfrag_tagged) {
+  if (FQ_TAGS_DEV && P.xfrag_tagged) {
     // no grid barrier before this phase: every word is polled until it carries the producing
     // phase's tag (words past K are the zero padding and never written)
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(P.xfrag);
@@ -722,7 +722,7 @@ void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp, 
       }
     }
   }
-  for (int base = 0; !P.xfrag_tagged && base < n; base += NT * kCopyVec) {
+  for (int base = 0; !(FQ_TAGS_DEV && P.xfrag_tagged) && base < n; base += NT * kCopyVec) {
     uint4 v[kCopyVec];
 #pragma unroll
     for (int s = 0; s < kCopyVec; ++s) {
@@ -1113,7 +1113,7 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
   const int B = P.B, nmat = P.nmat;
   const int per = 16 * B;
   const int fstride = kMaxMat * 16 * B;
-  const bool merge_last = C.nfollow > 0 && hi == C.ntiles;
+  const bool merge_last = !FQ_TILE_PART && C.nfollow > 0 && hi == C.ntiles;  // stream-K only
   // stream-K parts travel as (value, tag) pairs in one 8-byte store: the tag (launch epoch and
   // phase) tells the owner the value is current, no flag / fence / extra round trip
   float2* fix = reinterpret_cast<float2*>(P.fix);
@@ -1132,7 +1132,7 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
       for (int w = 0; w < kNCW; ++w) a += r[w * per];
       v[m] = a;
     }
-    if (l == 0 && C.head_shared) {
+    if (!FQ_TILE_PART && l == 0 && C.head_shared) {
       for (int m = 0; m < nmat; ++m)
         __stcg(fix + static_cast<size_t>(blockIdx.x) * fstride + m * per + i, make_float2(v[m], __uint_as_float(C.tag)));
     } else if (merge_last && l == hi - 1) {
@@ -1158,7 +1158,7 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
     } else {
       gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
     }
-    if (P.epi == EPI_SWIGLU && P.yfrag != nullptr && P.yfrag_nkb < 0 && ((i / B) & 1) == 0) {
+    if (FQ_TAGS_DEV && P.epi == EPI_SWIGLU && P.yfrag != nullptr && P.yfrag_nkb < 0 && ((i / B) & 1) == 0) {
       // tagged fragment output: the even row of each pair also sums the odd row's partials (same
       // tile, item i + B) and writes both as one (half2, tag) word
       const int64_t row = (C.tile0 + l) * static_cast<int64_t>(kTileRows) + i / B;
@@ -1603,7 +1603,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
 #pragma unroll
             for (int e = 0; e < 4; ++e) y[mm][e] = 0.f;
           ++loc;
-          if (left > 0 && (loc - wlo == cap || (loc == 1 && C.head_shared))) {
+          if (left > 0 && (loc - wlo == cap || (!FQ_TILE_PART && loc == 1 && C.head_shared))) {
             reduce_window(P, C, G, wlo, loc, sqb, st);
             wlo = loc;
           }
@@ -1963,7 +1963,7 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
         store_out(P.attn_out, P.act_dtype, qoff + e, o);
         if (P.yfrag && P.yfrag_nkb > 0) frag_store(P.yfrag, P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e, o);
       }
-      if (P.yfrag && P.yfrag_nkb < 0) {
+      if (FQ_TAGS_DEV && P.yfrag && P.yfrag_nkb < 0) {
 #pragma unroll
         for (int e = 0; e < DPL; e += 2)
           frag_store_pair(P.yfrag, -P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e,
