@@ -154,6 +154,7 @@ struct ProgramRun {
   int red_bytes = 0;  // per-warp tile partials (reduction window)
   int prefetch = 0;   // L2 prefetch distance in stages (env FQ_PREFETCH overrides; -1 = no loads)
   int ctl_phases = 0; // phases with a precomputed partition table in shared memory
+  bool lean = false;  // decode / prefill step program: launch the lean kernel (program.cu)
   const int32_t* pos = nullptr;   // decode step: per-row positions / cache slots, copied into shared
   const int32_t* slots = nullptr; // memory at kernel start (the attention phases read them there)
   int nrows = 0;

@@ -744,9 +744,24 @@ void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp, 
 #ifndef FQ_VEC_STAGE
 #define FQ_VEC_STAGE 1  // one round trip for K = 11008 (measured -0.6% per step at 11 consumer warps)
 #endif
+// LEAN (the decode / prefill step program, checked by the host builder): every GEMV input is either
+// pre-staged fragments or the aligned fp32 residual under an RMSNorm, so only those two staging
+// paths are compiled into that kernel (less code around the weight loop)
+template <bool LEAN>
 __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long* gp, unsigned int xtag) {
   if (P.xfrag != nullptr) {
     stage_frag_copy(P, G, gp, xtag);
+    return;
+  }
+  if constexpr (LEAN) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float pv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = lane + 32 * j;
+      pv[j] = (warp < P.B && i < P.n_partials) ? P.norm_partials[warp * P.partials_stride + i] : 0.f;
+    }
+    stage_vec<4, true, true>(P, G, gp, pv);
     return;
   }
   if (P.attn_splits > 1) {
@@ -1499,6 +1514,7 @@ __device__ __forceinline__ void add_into(float (&y)[kMaxMat][4], int m, float (&
   for (int e = 0; e < 4; ++e) yc[e] = 0.f;
 }
 
+template <bool LEAN>
 __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, PhaseCtl& C, int red_floats,
                                int& slot_ref, uint32_t& phase_ref, int phase_idx, const CtlEntry* ctab, unsigned int tag,
                                unsigned long long* gprof) {
@@ -1511,7 +1527,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     if (lane == 0) C.tag = tag;
     if (gpa && lane == 0) gpa[0] = gtimer();
   }
-  stage_acts(P, G, gp, tag - 1);  // ends with a consumer barrier: C is visible (tag - 1: the previous phase)
+  stage_acts<LEAN>(P, G, gp, tag - 1);  // ends with a consumer barrier: C is visible (tag - 1: the previous phase)
   if (gp) gp[3] = gtimer();
   const int B = P.B, nmat = P.nmat;
   float sqb[kMaxB];
@@ -2113,6 +2129,7 @@ struct SmemLayout {
   int nrows;
 };
 
+template <bool LEAN>
 __device__ void run_program(const Phase* phases, int nphases, unsigned int* barrier, SmemLayout L) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float sq_red[kMaxB][kNCW];
@@ -2199,7 +2216,8 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   named_sync(1, kNCW * 32);
   for (int i = 0; i < nphases; ++i) {
     const Phase& P = pbuf[i & 1];
-    if (P.type == PH_GEMV) run_gemv_phase(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i, gprof);
+    if (P.type == PH_GEMV)
+      run_gemv_phase<LEAN>(P, R, G, ctl, L.red_bytes / 4, slot_i, phase_bit, i, ctab, s_lepoch * 1024u + i, gprof);
     else if (P.type == PH_EMBED) run_embed(P, sq_red);
     else if (P.type == PH_ATTN) run_attn(P, attn_smem, meta_smem, s_lepoch * 1024u + i);
     else if (P.type == PH_APPEND) run_append(P);
@@ -2225,12 +2243,17 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
 
 __global__ void __launch_bounds__(kThreads, 1) program_kernel(const Phase* phases, int nphases, unsigned int* barrier,
                                                               SmemLayout L) {
-  run_program(phases, nphases, barrier, L);
+  run_program<false>(phases, nphases, barrier, L);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) program_kernel_inline(const __grid_constant__ InlineProgram prog,
                                                                      int nphases, unsigned int* barrier, SmemLayout L) {
-  run_program(prog.phases, nphases, barrier, L);
+  run_program<false>(prog.phases, nphases, barrier, L);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) program_kernel_lean(const Phase* phases, int nphases, unsigned int* barrier,
+                                                                   SmemLayout L) {
+  run_program<true>(phases, nphases, barrier, L);
 }
 
 int max_dynamic_smem() {
@@ -2241,12 +2264,14 @@ int max_dynamic_smem() {
     int dev = 0, optin = 0;
     FQ_CUDA(cudaGetDevice(&dev));
     FQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes a1{}, a2{};
+    cudaFuncAttributes a1{}, a2{}, a3{};
     FQ_CUDA(cudaFuncGetAttributes(&a1, program_kernel));
     FQ_CUDA(cudaFuncGetAttributes(&a2, program_kernel_inline));
-    v = optin - static_cast<int>(std::max(a1.sharedSizeBytes, a2.sharedSizeBytes)) - 1024;
+    FQ_CUDA(cudaFuncGetAttributes(&a3, program_kernel_lean));
+    v = optin - static_cast<int>(std::max({a1.sharedSizeBytes, a2.sharedSizeBytes, a3.sharedSizeBytes})) - 1024;
     FQ_CUDA(cudaFuncSetAttribute(program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
     FQ_CUDA(cudaFuncSetAttribute(program_kernel_inline, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
+    FQ_CUDA(cudaFuncSetAttribute(program_kernel_lean, cudaFuncAttributeMaxDynamicSharedMemorySize, v));
   }
   return v;
 }
@@ -2294,6 +2319,15 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   const SmemLayout L = layout_for(pb.max_kpad, pb.max_bb, r.nphases, ns, tot, std::max<int64_t>(pb.max_xs, 256));
   if (ns < 2) fail(FQ_E_CONFIG, "gemv: activations of this width do not fit in shared memory");
   r.nstages = ns;
+  // the lean kernel when every GEMV phase stages through one of its two paths
+  r.lean = !transient && std::getenv("FQ_NO_LEAN") == nullptr;
+  for (const Phase& P : pb.phases) {
+    if (P.type != PH_GEMV || P.xfrag != nullptr) continue;
+    const bool ok = P.x_dtype == FQ_DT_F32 && P.norm_gain != nullptr && P.attn_splits <= 1 &&
+                    (reinterpret_cast<uintptr_t>(P.x) & 15) == 0 && ((P.x_stride * 4) & 15) == 0 && (P.K & 7) == 0 &&
+                    (reinterpret_cast<uintptr_t>(P.norm_gain) & 15) == 0;
+    if (!ok) r.lean = false;
+  }
   if (std::getenv("FQ_DEBUG_LAYOUT"))
     std::fprintf(stderr, "fq program: %d phases, ring %d x %d B, xs %d, red %d, ctl %d, smem %zu B\n", r.nphases, ns,
                  kStageBytes, L.xs_bytes, L.red_bytes, L.ctl_phases, tot);
@@ -2363,7 +2397,10 @@ void launch_program(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, b
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (run.dev_phases)
+  if (run.dev_phases && run.lean)
+    FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel_lean, static_cast<const Phase*>(run.dev_phases), run.nphases, barrier,
+                               L));
+  else if (run.dev_phases)
     FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel, static_cast<const Phase*>(run.dev_phases), run.nphases, barrier, L));
   else
     FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel_inline, run.inl, run.nphases, barrier, L));
