@@ -1423,9 +1423,11 @@ __device__ void produce_table(const Phase* phases, int nphases, const CtlEntry* 
 
 // Per-phase control block, computed by consumer warp 1 (the lanes evaluate the range starts of
 // this CTA and its followers in parallel) while warp 0 computes the RMSNorm factors.
+template <bool LEAN = false>
 __device__ void phase_setup(const Phase& P, PhaseCtl& C, int red_floats, int lane, unsigned long long* gpa,
                             const CtlEntry* E) {
-  if (E && E->valid && E->nfollow != 0xFF) {
+  // LEAN: the partition table always covers the program and whole tiles never have followers
+  if (LEAN || (E && E->valid && E->nfollow != 0xFF)) {
     // precomputed at kernel start: copy into the working control block
     if (lane == 0) {
       C.S.n = E->nseg;
@@ -1448,6 +1450,7 @@ __device__ void phase_setup(const Phase& P, PhaseCtl& C, int red_floats, int lan
     __syncwarp();
     return;
   }
+  if constexpr (!LEAN) {
   Segs S;
   phase_segs(P, S);
 
@@ -1493,6 +1496,7 @@ __device__ void phase_setup(const Phase& P, PhaseCtl& C, int red_floats, int lan
     C.cap = S.n > 0 ? max(1, red_floats / (P.nmat * kNCW * 16 * P.B)) : 1;
   }
   __syncwarp();
+  }
 }
 
 __device__ __forceinline__ void add_into(float (&y)[kMaxMat][4], int m, float (&yc)[4]) {
@@ -1523,7 +1527,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
                                                       : nullptr;  // compiled out: every gp test folds away
   unsigned long long* gp = threadIdx.x == 0 ? gpa : nullptr;
   if (warp == 1) {
-    phase_setup(P, C, red_floats, lane, gpa, ctab ? ctab + phase_idx : nullptr);  // warp 0: norm factors
+    phase_setup<LEAN>(P, C, red_floats, lane, gpa, ctab ? ctab + phase_idx : nullptr);  // warp 0: norm factors
     if (lane == 0) C.tag = tag;
     if (gpa && lane == 0) gpa[0] = gtimer();
   }
@@ -2172,7 +2176,7 @@ __device__ void run_program(const Phase* phases, int nphases, unsigned int* barr
   __shared__ const uint8_t* s_pbase[2][2 * kMaxMat];
   if (warp == kNCW) {
     unsigned long long* tr = blockIdx.x == static_cast<unsigned>(g_trace_cta) ? g_ring_trace : nullptr;
-    if (ctab != nullptr) {
+    if (LEAN || ctab != nullptr) {
       // the weight stream depends on nothing produced at run time, only on the partition table
       // the consumers compute first (named barrier 2)
       named_sync(2, kThreads);
@@ -2320,7 +2324,7 @@ ProgramRun upload_program(fq_ctx* ctx, ProgramBuilder& pb, bool transient) {
   if (ns < 2) fail(FQ_E_CONFIG, "gemv: activations of this width do not fit in shared memory");
   r.nstages = ns;
   // the lean kernel when every GEMV phase stages through one of its two paths
-  r.lean = !transient && std::getenv("FQ_NO_LEAN") == nullptr;
+  r.lean = !transient && std::getenv("FQ_NO_LEAN") == nullptr && L.ctl_phases > 0 && FQ_TILE_PART;
   for (const Phase& P : pb.phases) {
     if (P.type != PH_GEMV || P.xfrag != nullptr) continue;
     const bool ok = P.x_dtype == FQ_DT_F32 && P.norm_gain != nullptr && P.attn_splits <= 1 &&
