@@ -165,39 +165,115 @@ def params_per_token(cfg):
     return L * (4 * d * d + 3 * d * f) + V * d
 
 
+def _ref_decoder_lib():
+    import ctypes as C
+    import oracle  # noqa: E402  (reference arm only)
+    R = oracle.ref()
+    if R is None:
+        return None
+    i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+    R.ref_decoder_create.restype = C.c_void_p
+    R.ref_decoder_create.argtypes = [C.c_int64] * 7 + [C.c_uint64, i32p, C.c_int64, C.c_double]
+    R.ref_decoder_step.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    R.ref_decoder_params.argtypes = [C.c_void_p]
+    R.ref_decoder_params.restype = C.c_int64
+    R.ref_decoder_destroy.argtypes = [C.c_void_p]
+    return R
+
+
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the reference CPU path on the host cores (rank 0 only)."""
+    """--impl reference: the reference's own decode loop (forward_decode + ppl_entropy +
+    fault_tolerance + argmax_token, src/engine.cpp:89-136; library built from its sources into
+    oracle/_ref) on every host core, one independent sequence per thread (rank 0 only).
+
+    Each thread holds a reference-architecture model with the 7B block dimensions (d 4096, 32
+    heads x 128, ffn 11008, vocab 32000) but REF_BLOCKS of the 32 blocks -- a full 7B reference
+    model is 36 GB of fp32 master + rungs per sequence and ~50 s per token -- at the switched
+    schedule's 50/50 W8/W4 mix, prefilled with a 16-token prompt.  One step = one real greedy
+    decode token on every thread; tokens/s is scaled to the full 7B-shape token by linear
+    parameter count (the reference's decode time is dequantize + linear per parameter:
+    BASELINE.md)."""
     if rank != 0:
         return
-    import oracle  # noqa: E402
-    if oracle.ref() is None:
+    import ctypes as C
+    R = _ref_decoder_lib()
+    if R is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfqref.so not built (reference sources absent at build time)"}))
         return
     threads = os.cpu_count() or 1
-    P = params_per_token(cfg)
-    w4_share = 0.5  # half of the parameters at W4: the mid-run mix of the switched schedule
+    blocks = int(os.environ.get("REF_BLOCKS", str(cfg["n_layers"] if cfg["n_layers"] <= 4 else 2)))
+    n_prompt = 16
+    need = n_prompt + args.warmup + args.steps + 1
+    handles = [None] * threads
+
+    def create(i):
+        prompt = np.random.default_rng(1000 + i).integers(0, cfg["vocab_size"], n_prompt).astype(np.int32)
+        handles[i] = R.ref_decoder_create(cfg["vocab_size"], cfg["d_model"], cfg["n_heads"], cfg["head_dim"], blocks,
+                                          cfg["ffn_dim"], need, 7 + i, prompt, n_prompt, 0.5)
+
+    t0 = time.perf_counter()
+    ts = [threading.Thread(target=create, args=(i,)) for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    build_s = time.perf_counter() - t0
+    if any(h is None for h in handles):
+        print(json.dumps({"impl": "reference", "unavailable": "reference model build failed: "
+                          + oracle_error()}))
+        return
+    p_meas = R.ref_decoder_params(handles[0])
+    scale = params_per_token(cfg) / p_meas  # full 7B-shape token / measured model
     per_step = []
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        spp, _ = cpu_baseline_sample(cfg, threads)
-        dt = time.perf_counter() - t0
-        s_tok = P * ((1 - w4_share) * spp[8] + w4_share * spp[4])
+        secs = [0.0] * threads
+
+        def step(j):
+            s, pp = C.c_double(), C.c_double()
+            R.ref_decoder_step(handles[j], C.byref(s), C.byref(pp))
+            secs[j] = s.value
+
+        w0 = time.perf_counter()
+        ts = [threading.Thread(target=step, args=(j,)) for j in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        wall = time.perf_counter() - w0
         if i >= args.warmup:
-            per_step.append(threads / s_tok)
-    value = statistics.mean(per_step)
+            per_step.append(wall)
+    for h in handles:
+        R.ref_decoder_destroy(h)
+    step_s = statistics.mean(per_step)
+    value = threads / (step_s * scale)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{cfg['name']} decode, W8/W4 50/50 mix", "impl": "reference CPU (oracle/_ref)"},
+        "warmup": args.warmup, "ms_per_step": 1000.0 * step_s * scale / threads, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg['name']} greedy decode, W8/W4 50/50 mix (the switched schedule's midpoint), "
+                               f"{threads} independent sequences on {threads} host threads",
+                   "impl": "reference CPU (oracle/_ref, built from /root/reference/proj/src)",
+                   "measured_model": f"reference architecture, d {cfg['d_model']}, {cfg['n_heads']}x{cfg['head_dim']} "
+                                     f"heads, ffn {cfg['ffn_dim']}, vocab {cfg['vocab_size']}, {blocks} blocks "
+                                     f"({p_meas} linear params)",
+                   "scaled_to": f"{params_per_token(cfg)} linear params per 7B-shape token (x{scale:.3f})",
+                   "measured_step_s": step_s, "build_s": round(build_s, 1),
+                   "same_config": "no: reference architecture (pre-LN, GELU w1/w2, learned positions) at the same "
+                                  "dimensions, " + ("all blocks" if blocks == cfg["n_layers"] else
+                                                    f"{blocks} of {cfg['n_layers']} blocks, scaled by parameters")},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                         "sample": "per step: one dequantize+linear call (4096x4096, g128) per host thread at W8 and "
-                                   "at W4, extrapolated by parameter count to a full 7B token (225 linears), "
-                                   "threads = independent sequences"},
+                         "sample": f"per step: one real forward_decode + softmax statistics + argmax token of a "
+                                   f"{blocks}-block reference model at the 7B block dimensions on each of {threads} "
+                                   "threads (independent sequences), scaled by parameter count to a 7B-shape token"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def oracle_error():
+    import oracle  # noqa: E402
+    return oracle.ref().ref_last_error().decode()
 
 
 def main():
@@ -215,14 +291,33 @@ def main():
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # --gpus N without a launcher: start one rank per GPU ourselves (torchrun, loopback
+        # rendezvous); NCCL's communicator-init log goes to stderr so the ranks can be counted
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd, env=env))
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU", file=sys.stderr)
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: E402
         import torch  # noqa: E402
-        torch.cuda.set_device(local)
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
 
     if args.impl == "reference":

@@ -37,6 +37,7 @@ struct ModelConfig {
   int max_batch = 1;       // resident sequence slots
   float norm_eps = 1e-5f;
   float rope_theta = 10000.0f;
+  bool fp16_activations = false;  // llama: activation roundings in fp16 instead of bf16
   void validate() const;
 };
 

@@ -270,4 +270,71 @@ int ref_time_quant_linear(const float* w, int64_t N, int64_t K, int64_t G, int b
   });
 }
 
+// ---- reference decode arm (bench.py --impl reference): a reference-architecture model at the
+// requested dimensions (make_fixture_model, src/fixture.cpp), a greedy decode loop of
+// forward_decode + argmax_token (src/engine.cpp:89-136 minus the scheduler), one handle per host
+// thread (the reference model is single-thread-confined).
+struct RefDecoder {
+  Model model;
+  KvCache cache;
+  TokenId next = 0;
+};
+
+void* ref_decoder_create(int64_t vocab, int64_t d, int64_t heads, int64_t head_dim, int64_t layers, int64_t ffn,
+                         int64_t max_seq, uint64_t seed, const int32_t* prompt, int64_t n_prompt, double w4_share) {
+  RefDecoder* out = nullptr;
+  const int st = guard([&] {
+    ModelConfig c;
+    c.vocab_size = vocab;
+    c.d_model = d;
+    c.n_heads = heads;
+    c.head_dim = head_dim;
+    c.n_layers = layers;
+    c.ffn_dim = ffn;
+    c.max_seq_len = max_seq;
+    auto* r = new RefDecoder{make_fixture_model(c, seed), KvCache{}, 0};
+    // the switched schedule's mix: the first w4_share of the linears (by parameter count) at 4 bits
+    std::vector<MultiPrecisionLayer*> ls = r->model.linear_layers();
+    double total = 0.0, acc = 0.0;
+    for (auto* l : ls) total += static_cast<double>(l->param_count());
+    for (auto* l : ls) {
+      const bool four = acc < w4_share * total;
+      acc += static_cast<double>(l->param_count());
+      r->model.set_precision(l->id(), four ? Rung::Int4 : Rung::Int8);
+    }
+    r->cache = r->model.make_cache();
+    const Tensor lg = r->model.forward_prefill(std::span<const TokenId>(prompt, static_cast<size_t>(n_prompt)), r->cache);
+    const int64_t V = r->model.config().vocab_size;
+    Tensor last({1, V});
+    std::memcpy(last.data(), lg.data() + (lg.rows() - 1) * V, sizeof(float) * static_cast<size_t>(V));
+    r->next = argmax_token(last);
+    out = r;
+  });
+  return st == 0 ? out : nullptr;
+}
+
+// One greedy decode token: forward_decode, ppl_entropy / fault_tolerance of the row (the
+// statistics the engine loop records), argmax.  Returns the seconds it took.
+int ref_decoder_step(void* h, double* seconds, double* ppl) {
+  return guard([&] {
+    auto* r = static_cast<RefDecoder*>(h);
+    const auto t0 = std::chrono::steady_clock::now();
+    const Tensor lg = r->model.forward_decode(r->next, r->cache);
+    const double p = ppl_entropy(lg);
+    const double ft = fault_tolerance(lg);
+    r->next = argmax_token(lg);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (ppl) *ppl = p + 0.0 * ft;
+  });
+}
+
+int64_t ref_decoder_params(void* h) {
+  int64_t n = 0;
+  for (const auto* l : static_cast<RefDecoder*>(h)->model.linear_layers()) n += l->param_count();
+  return n;
+}
+
+void ref_decoder_destroy(void* h) { delete static_cast<RefDecoder*>(h); }
+
 }  // extern "C"

@@ -348,7 +348,12 @@ fq_status fq_gemm(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t rows, co
     require(ctx != nullptr && L != nullptr && x_dev != nullptr && y_dev != nullptr, FQ_E_INPUT, "null argument");
     require(rows >= 1, FQ_E_DIMENSION, "gemm: rows must be >= 1");
     require(x_stride >= L->K && y_stride >= L->N, FQ_E_DIMENSION, "gemm: row stride smaller than the row");
-    launch_gemm_dq(ctx, L, rung, rows, x_dev, FQ_DT_BF16, x_stride, y_dev, y_stride);
+    // row-major bf16 -> the GEMM's tiled operand layout (scratch), then the tcgen05 GEMM
+    const size_t bytes = 2 * static_cast<size_t>(tiled_act_elems(rows, L->K));
+    void* xt = ctx->ensure_scratch(bytes);
+    FQ_CUDA(cudaMemsetAsync(xt, 0, bytes, ctx->stream));
+    launch_tile_acts(ctx, x_dev, FQ_DT_BF16, x_stride, rows, L->K, xt);
+    launch_gemm_dq(ctx, L, rung, rows, xt, FQ_DT_BF16, y_dev, y_stride);
   });
 }
 

@@ -59,6 +59,9 @@ struct fq_ctx {
   unsigned int* launch_ctr = nullptr;  // [epoch, done] of the program kernels on this context
   float* gemm_ws = nullptr;  // split-K partial sums of the tensor-core GEMM (grown on demand)
   size_t gemm_ws_bytes = 0;
+  // bumped whenever a layer's resident copies change (upload, device quantization): models
+  // drop step programs and captured graphs built against older weight pointers
+  uint64_t weight_epoch = 0;
 };
 
 // ------------------------------------------------------------------ tiled fast-path layout
@@ -175,20 +178,33 @@ double time_gemv_chain(fq_ctx* ctx, const GemvLaunch* gs, int n, int reps);
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
                        int x_dtype, void* y, int y_dtype);
 
-// tcgen05 dequant-GEMM: y[T, N] (fp32, row stride y_stride) = x[T, K] . dequant(W_rung)^T with x
-// bf16 (weights dequantised to bf16) or fp16 (weights to fp16: 3 more mantissa bits, the
-// prefill's choice); accumulate: y += instead (the residual add of the O / down projections)
-void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x, int x_dtype, int64_t x_stride,
-                    float* y, int64_t y_stride, bool accumulate = false);
+// Activations of the tcgen05 GEMM are stored pre-tiled: bf16 [T/128][K/128][128 x 128] with each
+// 32 KB tile in the UMMA canonical K-major layout (8 rows x 16 B core matrices, K-adjacent core
+// matrices 128 B apart, 8-row groups 2 KB apart), so one 1-D bulk copy moves a tile.  Rows past T
+// and columns past K stay zero (buffers are cleared at allocation).  Element offset of (t, k):
+__host__ __device__ inline int64_t tiled_act_offset(int t, int64_t k, int nkb) {
+  return ((static_cast<int64_t>(t >> 7) * nkb + (k >> 7)) << 14) + (((t & 127) >> 3) << 10) + (((k & 127) >> 3) << 6) +
+         ((t & 7) << 3) + (k & 7);
+}
+int64_t tiled_act_elems(int64_t T, int64_t K);  // buffer size (elements) for T rows of K features
+void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride, int64_t T, int64_t K, void* xt,
+                      int out_dtype = FQ_DT_BF16);
 
-// row-parallel prefill kernels (prefill.cu; llama arch; GEMM operands bf16-rounded, stored fp16)
+// tcgen05 dequant-GEMM: y[T, N] (fp32, row stride y_stride) = x[T, K] . dequant(W_rung)^T with x the
+// tiled bf16 (x_dtype FQ_DT_BF16) or fp16 (FQ_DT_F16) activations above; the tensor cores multiply the exact integer codes (q - z) and the
+// per-group fp32 scale is applied per 128-code k-block in the epilogue (no weight rounding);
+// accumulate: y += instead (the residual add of the O / down projections)
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
+                    int64_t y_stride, bool accumulate = false);
+
+// row-parallel prefill kernels (prefill.cu; llama arch; GEMM operands bf16, stored tiled)
 void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev, int T, int64_t d, float* x);
-void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16);
+void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16, int act_dtype);
 void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,
-                     const float2* cs, float* qr, __half* kv_layer, int64_t max_seq);
+                     const float2* cs, float* qr, __half* kv_layer, int64_t max_seq, int act_dtype);
 void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
-                       void* out16);
-void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, void* out16);
+                       void* out16, int act_dtype);
+void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, int64_t f, void* out16, int act_dtype);
 
 // statistics
 void launch_softmax_stats(fq_ctx* ctx, const float* logits, int64_t rows, int64_t vocab,

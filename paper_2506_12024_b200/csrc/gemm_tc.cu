@@ -1,57 +1,58 @@
 // Prefill / calibration contraction on the 5th-generation tensor cores (tcgen05 + TMEM):
 //   Y[T, N] (fp32) = X[T, K] (bf16) . dequant(W_rung[N, K])^T
 // straight from the tiled W8 / W4 copy the decode GEMV streams (fq_internal.cuh), so prefill and
-// calibration use the same resident weights.  This is the dense contraction of SURVEY §7 step 6
-// (BASELINE config 4): MultiPrecisionLayer::forward on many rows at once
-// (/root/reference/proj/src/model.cpp:77-98 = dequantize src/quantizer.cpp:205-219 + linear
-// src/tensor.cpp:83-101).
+// calibration use the same resident weights.  This is the dense contraction of BASELINE config 4:
+// MultiPrecisionLayer::forward on many rows at once (/root/reference/proj/src/model.cpp:77-98 =
+// dequantize src/quantizer.cpp:205-219 + linear src/tensor.cpp:83-101).
 //
-// One CTA = 128 weight rows x 256 tokens, 8 warps:
-//   * every k-step (128 codes = one quantization group) all threads dequantize the 8 tiled
-//     16x128 blocks of the CTA's rows to bf16 (q - z) * s into shared memory in the UMMA canonical
-//     K-major layout (no swizzle: 8x16-byte core matrices, LBO = 128 B along K, SBO = 2 KB along
-//     M/N), while the 256x128 bf16 activation tile arrives by cp.async in the same layout;
-//   * one elected thread issues 8 tcgen05.mma (M=128, N=256, K=16, fp32 accumulate in TMEM) and
-//     commits them to the stage's mbarrier; two stages, so the dequantisation of step k+1
-//     overlaps the MMAs of step k;
-//   * the global loads of step k+1 (code words, scales, activations) are issued into registers
-//     before step k's operands are written, so their latency hides behind the previous step;
-//   * epilogue: tcgen05.ld of the 128x128 fp32 accumulator (warps w and w+4 read TMEM lanes
-//     32w..32w+31, half of the token columns each).
+// Numerics (the decode GEMV's contract): the tensor cores see the EXACT integer codes q - z (|q - z|
+// <= 255, exact in bf16) and the bf16 activations; each 128-code k-block is one quantization group,
+// accumulated alone in fp32 in tensor memory, and the group's fp32 scale is applied in the
+// epilogue: y = sum_kb s[n, kb] * (sum_{k in kb} (q - z) x).  No weight is ever rounded.
+//
+// One CTA = 128 weight rows (UMMA M) x 128 tokens (UMMA N), warp-specialised, 10 warps:
+//   warp 0     producer: per k-block one 1-D bulk copy (cp.async.bulk) of the 32 KB activation
+//              tile (X is stored pre-tiled in the UMMA canonical K-major layout, see
+//              tiled_act_offset) and eight bulk copies of the CTA's raw 16x128 weight blocks
+//              into a 3-deep ring, completion by mbarrier transaction bytes;
+//   warps 6-9  dequantisers: raw codes -> bf16 (q - z) into a 2-deep A-operand ring (canonical
+//              K-major, no swizzle), fence.proxy.async, one arrival per k-block;
+//   warp 1     MMA issuer (one thread): 8 x tcgen05.mma (M128 N128 K16) per k-block into one of
+//              two TMEM accumulators, tcgen05.commit releases the A / input slots and hands the
+//              accumulator to the epilogue;
+//   warps 2-5  epilogue: tcgen05.ld of the k-block's accumulator (lane quarter = warp % 4), then
+//              y[128 tokens] += s[row, kb] * D in registers; the accumulator slot is returned as
+//              soon as it is read, so the MMAs of k-block kb+1 overlap the scaling of kb.
 #include "gemv_program.cuh"
 
 namespace fqc {
 namespace {
 
-#ifndef FQ_GEMM_TN
-#define FQ_GEMM_TN 256
-#endif
-#ifndef FQ_GEMM_STAGES
-#define FQ_GEMM_STAGES 2
-#endif
-constexpr int kTM = 128;   // weight rows per CTA (UMMA M)
-constexpr int kTN = FQ_GEMM_TN;  // tokens per CTA (UMMA N)
-constexpr int kStagesG = FQ_GEMM_STAGES;  // smem stages: activations are loaded kStagesG - 1 k-steps ahead
-constexpr int kTK = 128;   // codes per k-step (one tiled block / quantization group)
-constexpr int kATileBytes = kTM * kTK * 2;  // bf16 weight tile: 32 KB
-constexpr int kBTileBytes = kTN * kTK * 2;  // bf16 activation tile: 64 KB
-constexpr int kStageBytesG = kATileBytes + kBTileBytes;
-constexpr int kGemmThreads = 256;
+constexpr int kTM = 128;                      // weight rows per CTA (UMMA M)
+constexpr int kTN = 128;                      // tokens per CTA (UMMA N)
+constexpr int kTK = 128;                      // codes per k-block (one tiled block / group)
+constexpr int kTileBytes = kTM * kTK * 2;     // bf16 128 x 128 tile: 32 KB (A and B alike)
+constexpr int kInStages = 3;                  // activation + raw-weight ring
+constexpr int kAStages = 2;                   // dequantised A ring
+constexpr int kGemmThreads = 320;             // 10 warps
+constexpr int kRawBytes = 8 * kBlockBytes8;   // 8 raw 16x128 blocks (W8 size; W4 uses half)
+constexpr int kSmemGemm = kInStages * (kTileBytes + kRawBytes) + kAStages * kTileBytes + 1024;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-// canonical K-major no-swizzle offset of element (row, k) inside a 128x128 fp16 tile
+// canonical K-major no-swizzle byte offset of element (row, k) inside a 128x128 16-bit tile:
+// 8x16-byte core matrices, LBO = 128 B (K-adjacent core matrices), SBO = 2 KB (8-row groups)
 __device__ __forceinline__ uint32_t kmajor_off(int row, int k) {
   return static_cast<uint32_t>((row >> 3) * 2048 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
 }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);          // start address
-  d |= static_cast<uint64_t>(128u >> 4) << 16;                  // LBO: K-adjacent core matrices
-  d |= static_cast<uint64_t>(2048u >> 4) << 32;                 // SBO: 8-row groups
-  d |= static_cast<uint64_t>(1u) << 46;                         // descriptor version (sm_100)
-  return d;                                                     // base offset 0, SWIZZLE_NONE
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);  // start address
+  d |= static_cast<uint64_t>(128u >> 4) << 16;          // LBO: K-adjacent core matrices
+  d |= static_cast<uint64_t>(2048u >> 4) << 32;         // SBO: 8-row groups
+  d |= static_cast<uint64_t>(1u) << 46;                 // descriptor version (sm_100)
+  return d;                                             // base offset 0, SWIZZLE_NONE
 }
 
 // kind::f16 instruction descriptor: D f32, A/B bf16 (F16 = 0) or fp16 (F16 = 1), both K-major,
@@ -61,10 +62,17 @@ constexpr uint32_t idesc() {
   return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
 }
 
-__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
 }
-__device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int who) {
   uint32_t ok = 0;
   unsigned long long t0 = 0;
   for (uint32_t spins = 0;; ++spins) {
@@ -81,15 +89,28 @@ __device__ __forceinline__ void mbar_wait1(uint64_t* bar, uint32_t parity) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t0 == 0) t0 = t;
       else if (t - t0 > 4000000000ull) {
-        printf("fq gemm watchdog: mma barrier stuck (cta %d,%d parity %u)\n", blockIdx.x, blockIdx.y, parity);
+        printf("fq gemm watchdog: role %d stuck (cta %d,%d,%d parity %u)\n", who, blockIdx.x, blockIdx.y, blockIdx.z, parity);
         __trap();
       }
     }
   }
 }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
 
+// exact (q - z) of two codes as a bf16 / fp16 pair (low half = first code): 2^23 + q - (2^23 + z);
+// |q - z| <= 255 is exact in both formats
 template <int F16>
-__device__ __forceinline__ uint32_t pack_b2(float a, float b) {
+__device__ __forceinline__ uint32_t qz_pair(uint32_t qa, uint32_t qb, float zf) {
+  const float a = __uint_as_float(0x4B000000u | qa) - zf, b = __uint_as_float(0x4B000000u | qb) - zf;
   if constexpr (F16) {
     const __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&h);
@@ -99,220 +120,218 @@ __device__ __forceinline__ uint32_t pack_b2(float a, float b) {
   }
 }
 
-// Global-side raw data of one k-step for one thread: its 16-byte code words of the 8 tiled blocks
-// (+ the two rows' scale / zero point) and its 16-byte chunks of the activation tile.  Loaded one
-// k-step ahead (registers), so the global latency hides behind the previous step.
-template <int W>
-struct StepRaw {
-  static constexpr int kWords = W == 0 ? 4 : 2;                       // 16-byte code words per lane per block
-  static constexpr int kA = 8 * kWords * 32 / kGemmThreads;           // per thread
-  uint4 w[kA];
-  float s0[kA], s1[kA], z0[kA], z1[kA];
-};
-
-// Activation tile of a k-step straight into shared memory (cp.async, 16-byte chunks = one core-
-// matrix row; rows past T / codes past K are zero-filled), bf16 as stored.
-__device__ __forceinline__ void load_tokens_async(const uint16_t* __restrict__ x, int64_t x_stride, int T, int64_t K,
-                                                  int t0, int kb, uint8_t* b_tile) {
-#pragma unroll 4
-  for (int it = threadIdx.x; it < kTN * (kTK / 8); it += kGemmThreads) {
-    const int tok = it >> 4, kc = it & 15;
-    const int t = t0 + tok;
-    const int64_t k = static_cast<int64_t>(kb) * kTK + kc * 8;
-    const bool in = t < T && k < K;
-    const uint16_t* src = in ? x + static_cast<int64_t>(t) * x_stride + k : x;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(b_tile + kmajor_off(tok, kc * 8))),
-                 "l"(src), "r"(in ? 16 : 0)
-                 : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <int W>
-__device__ __forceinline__ void load_step(const uint8_t* __restrict__ tiles, int64_t tile0, int n_tiles, int nkb, int kb,
-                                          int32_t zbase, StepRaw<W>& r) {
+// Dequantiser threads (128): raw 16x128 blocks of the stage -> bf16 (q - z) A tile.  The raw
+// block is in mma.sync A-fragment order (fq_internal.cuh); thread d always converts word
+// (i, t) = (d >> 5, d & 31) of its blocks (W8) / word (d >> 5 & 1, d & 31) of block pairs (W4).
+template <int W, int F16>
+__device__ __forceinline__ void dequant_stage(const uint8_t* raw, int32_t zbase, uint8_t* a_tile, int d) {
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
-  constexpr int words = StepRaw<W>::kWords;
-#pragma unroll
-  for (int u = 0; u < StepRaw<W>::kA; ++u) {
-    const int it = threadIdx.x + u * kGemmThreads;
-    const int rt = it / (words * 32), rem = it - rt * words * 32;
-    const int i = rem >> 5, t = rem & 31;
-    const int64_t tile = min(tile0 + rt, static_cast<int64_t>(n_tiles) - 1);  // rows past N masked at store
-    const uint8_t* blk = tiles + (tile * nkb + kb) * bb;
-    const int rr = t >> 2;
-    r.w[u] = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
-    r.s0[u] = reinterpret_cast<const float*>(blk + cbytes)[rr];
-    r.s1[u] = reinterpret_cast<const float*>(blk + cbytes)[rr + 8];
-    r.z0[u] = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + rr]) + zbase);
-    r.z1[u] = static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + rr + 8]) + zbase);
-  }
-}
-
-// Writes one k-step's weight operand into the stage's shared-memory tile (UMMA K-major layout):
-// A = 16-bit (q - z) * s of the CTA's 128 weight rows.
-template <int W, int F16>
-__device__ __forceinline__ void store_step(const StepRaw<W>& r, int64_t tile0, int n_tiles, uint8_t* a_tile) {
-  constexpr int words = StepRaw<W>::kWords;
-#pragma unroll
-  for (int u = 0; u < StepRaw<W>::kA; ++u) {
-    const int it = threadIdx.x + u * kGemmThreads;
-    const int rt = it / (words * 32), rem = it - rt * words * 32;
-    const int i = rem >> 5, t = rem & 31;
-    const bool live = tile0 + rt < n_tiles;
-    const int rrow = t >> 2, c2 = 2 * (t & 3);
-    const int row = rt * 16 + rrow;
-    const float s0 = live ? r.s0[u] : 0.f, s1 = live ? r.s1[u] : 0.f, z0 = r.z0[u], z1 = r.z1[u];
-    const uint32_t q4[4] = {r.w[u].x, r.w[u].y, r.w[u].z, r.w[u].w};
-    if constexpr (W == 0) {
+  if constexpr (W == 0) {
+    const int i = d >> 5, t = d & 31;
+    const int r = t >> 2, c2 = 2 * (t & 3);
+#pragma unroll 2
+    for (int rt = 0; rt < 8; ++rt) {
+      const uint8_t* blk = raw + rt * bb;
+      const uint4 w = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
+      const float z0 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r]) + zbase);
+      const float z1 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r + 8]) + zbase);
+      const uint32_t q4[4] = {w.x, w.y, w.z, w.w};
+      const int row = rt * 16 + r;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int k0 = 16 * (2 * i + h) + c2;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {  // e = 0: codes at k0, k0+1; e = 1: at k0+8, k0+9
+        for (int e = 0; e < 2; ++e) {  // codes (r, k0), (r, k0+1), (r+8, k0), (r+8, k0+1)
+          const int k0 = 16 * (2 * i + h) + c2 + 8 * e;
           const uint32_t q = q4[2 * h + e];
-          const float a0 = (static_cast<float>(q & 0xFFu) - z0) * s0, a1 = (static_cast<float>((q >> 8) & 0xFFu) - z0) * s0;
-          const float b0 = (static_cast<float>((q >> 16) & 0xFFu) - z1) * s1, b1 = (static_cast<float>(q >> 24) - z1) * s1;
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8 * e)) = pack_b2<F16>(a0, a1);
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8 * e)) = pack_b2<F16>(b0, b1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = qz_pair<F16>(q & 0xFFu, (q >> 8) & 0xFFu, z0);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = qz_pair<F16>((q >> 16) & 0xFFu, q >> 24, z1);
         }
       }
-    } else {
+    }
+  } else {
+    const int i = (d >> 5) & 1, t = d & 31;
+    const int r = t >> 2, c2 = 2 * (t & 3);
+#pragma unroll 2
+    for (int u = 0; u < 4; ++u) {
+      const int rt = 2 * u + (d >> 6);
+      const uint8_t* blk = raw + rt * bb;
+      const uint4 w = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
+      const float z0 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r]) + zbase);
+      const float z1 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r + 8]) + zbase);
+      const uint32_t q4[4] = {w.x, w.y, w.z, w.w};
+      const int row = rt * 16 + r;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
+        // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
         const int k0 = 16 * (4 * i + v) + c2;
         const uint32_t q = q4[v];
-        // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
-        auto nib = [&](int n) { return static_cast<float>((q >> (4 * n)) & 0xFu); };
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = pack_b2<F16>((nib(0) - z0) * s0, (nib(4) - z0) * s0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = pack_b2<F16>((nib(1) - z0) * s0, (nib(5) - z0) * s0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = pack_b2<F16>((nib(2) - z1) * s1, (nib(6) - z1) * s1);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = pack_b2<F16>((nib(3) - z1) * s1, (nib(7) - z1) * s1);
+        auto nb = [&](int n) { return (q >> (4 * n)) & 0xFu; };
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = qz_pair<F16>(nb(0), nb(4), z0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = qz_pair<F16>(nb(1), nb(5), z0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = qz_pair<F16>(nb(2), nb(6), z1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = qz_pair<F16>(nb(3), nb(7), z1);
       }
     }
   }
 }
 
 template <int W, int F16>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_dq_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb,
-                                                                  int32_t zbase, int64_t N, int64_t K,
-                                                                  const uint16_t* __restrict__ x, int64_t x_stride, int T,
-                                                                  float* __restrict__ y, int64_t y_stride, int accumulate,
-                                                                  int splits, int64_t split_stride) {
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_ws_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb, int32_t zbase, int64_t N,
+                   const uint8_t* __restrict__ xt, int T, float* __restrict__ y, int64_t y_stride, int accumulate,
+                   int splits, int64_t split_stride) {
+  constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
+  constexpr int cbytes = W == 0 ? 2048 : 1024;
   extern __shared__ __align__(1024) uint8_t gsm[];
-  __shared__ uint64_t mma_done[kStagesG];
+  __shared__ uint64_t in_full[kInStages], in_empty[kInStages], a_full[kAStages], a_empty[kAStages];
+  __shared__ uint64_t d_full[2], d_empty[2];
   __shared__ uint32_t tmem_base_s;
-  uint8_t* stage_base = gsm;  // kStagesG stages x (A 32 KB | B kTN x 256 B)
-  const int warp = threadIdx.x >> 5;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* b_ring = base;                                        // kInStages x 32 KB activations
+  uint8_t* raw_ring = b_ring + kInStages * kTileBytes;           // kInStages x 8 raw blocks
+  uint8_t* a_ring = raw_ring + kInStages * kRawBytes;            // kAStages x 32 KB bf16 (q - z)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
-  const int t0 = blockIdx.y * kTN;
-  // split-K: this CTA's k-steps [kb0, kb1); partial sums go to y + z * split_stride
+  const int tt = blockIdx.y;  // token tile
   const int kb0 = static_cast<int>(static_cast<int64_t>(nkb) * blockIdx.z / splits);
   const int kb1 = static_cast<int>(static_cast<int64_t>(nkb) * (blockIdx.z + 1) / splits);
+  const int nk = kb1 - kb0;
   y += blockIdx.z * split_stride;
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kStagesG; ++q) mbar_init1(&mma_done[q]);
+    for (int s = 0; s < kInStages; ++s) {
+      mbar_init(&in_full[s], 1);
+      mbar_init(&in_empty[s], 2);  // dequantisers done with the raw blocks + MMAs done with B
+    }
+    for (int s = 0; s < kAStages; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&d_full[s], 1);
+      mbar_init(&d_empty[s], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_s)),
-                 "r"(kTN));
+                 "r"(2 * kTN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
-  uint32_t phase[kStagesG];
-#pragma unroll
-  for (int q = 0; q < kStagesG; ++q) phase[q] = 0u;
-  StepRaw<W> cur, nxt;
-  // activation tiles of the first kStagesG - 1 k-steps (one cp.async group each, empty past kb1)
-#pragma unroll
-  for (int q = 0; q < kStagesG - 1; ++q) {
-    if (kb0 + q < kb1) load_tokens_async(x, x_stride, T, K, t0, kb0 + q, stage_base + q * kStageBytesG + kATileBytes);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  load_step<W>(tiles, tile0, n_tiles, nkb, kb0, zbase, cur);
-  // Pipeline: k-step kb dequantises into stage s = kb & 1 while the MMAs of kb - 1 run; right
-  // after kb's MMAs are issued, the MMAs of kb - 1 (the other stage's last reader) are waited for
-  // and that stage's activation tile refilled for kb + 1, so neither the tensor pipe nor the
-  // dequantisation waits on the other in steady state.
-  for (int kb = kb0; kb < kb1; ++kb) {
-    const int i = kb - kb0;
-    const int s = i % kStagesG;
-    const bool more = kb + 1 < kb1;
-    uint8_t* at = stage_base + s * kStageBytesG;
-    if (more) load_step<W>(tiles, tile0, n_tiles, nkb, kb + 1, zbase, nxt);
-    store_step<W, F16>(cur, tile0, n_tiles, at);
-    // this step's activation group is complete; the kStagesG - 2 newer ones may still be in flight
-    asm volatile("cp.async.wait_group %0;" ::"n"(kStagesG - 2) : "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = smem_addr(at), b0 = smem_addr(at + kATileBytes);
-#pragma unroll
-      for (int j = 0; j < kTK / 16; ++j) {
-        const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
-        const uint32_t acc = (i > 0 || j > 0) ? 1u : 0u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-            ::"r"(tmem), "l"(da), "l"(db), "r"(idesc<F16>()), "r"(acc));
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_addr(&mma_done[s]))
-                   : "memory");
-    }
-    // the stage of step i - 1 (= that of step i + kStagesG - 1) is free once MMA(i - 1) is done:
-    // refill its activation tile kStagesG - 1 steps ahead (an empty group past kb1)
-    if (i >= 1) {
-      const int sp = (i - 1) % kStagesG;
-      mbar_wait1(&mma_done[sp], phase[sp]);
-      phase[sp] ^= 1u;
-    }
-    if (kb + kStagesG - 1 < kb1)
-      load_tokens_async(x, x_stride, T, K, t0, kb + kStagesG - 1,
-                        stage_base + ((i + kStagesG - 1) % kStagesG) * kStageBytesG + kATileBytes);
-    else
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    if (more) cur = nxt;
-  }
-  // wait for the last commit (it covers every earlier MMA of this thread)
-  const int last = (kb1 - kb0 - 1) % kStagesG;
-  mbar_wait1(&mma_done[last], phase[last]);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // epilogue: warp w (of the first four) owns accumulator lanes 32w .. 32w+31 (weight rows);
-  // warps 4..7 take the second half of the token columns
-  const int lane = threadIdx.x & 31;
-  const int wl = warp & 3;
-  const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + wl * 32 + lane;
-  const int cbeg = (warp >> 2) * (kTN / 2);
+
+  if (warp == 0) {
+    // ---------------- producer
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % kInStages, kb = kb0 + i;
+        if (i >= kInStages) mbar_wait(&in_empty[s], ((i / kInStages) - 1) & 1, 0);
+        mbar_expect_tx(&in_full[s], kTileBytes + 8 * bb);
+        bulk_g2s(b_ring + s * kTileBytes, xt + (static_cast<int64_t>(tt) * nkb + kb) * kTileBytes, kTileBytes, &in_full[s]);
 #pragma unroll 1
-  for (int c0 = cbeg; c0 < cbeg + kTN / 2 && t0 + c0 < T; c0 += 8) {
-    uint32_t v[8];
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(wl * 32) << 16) + c0;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (n < N) {
+        for (int r = 0; r < 8; ++r) {
+          const int64_t tile = min(tile0 + r, static_cast<int64_t>(n_tiles) - 1);  // rows past N masked at store
+          bulk_g2s(raw_ring + s * kRawBytes + r * bb, tiles + (tile * nkb + kb) * bb, bb, &in_full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % kInStages, a = i % kAStages, dbuf = i & 1;
+        mbar_wait(&in_full[s], (i / kInStages) & 1, 1);
+        mbar_wait(&a_full[a], (i / kAStages) & 1, 1);
+        if (i >= 2) mbar_wait(&d_empty[dbuf], ((i >> 1) - 1) & 1, 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = smem_addr(a_ring + a * kTileBytes), b0 = smem_addr(b_ring + s * kTileBytes);
+        const uint32_t dt = tmem + static_cast<uint32_t>(dbuf * kTN);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int t = t0 + c0 + e;
+        for (int j = 0; j < kTK / 16; ++j) {
+          const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
+          const uint32_t acc = j > 0 ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+              "l"(da), "l"(db), "r"(idesc<F16>()), "r"(acc));
+        }
+        tc_commit(&d_full[dbuf]);
+        tc_commit(&a_empty[a]);
+        tc_commit(&in_empty[s]);
+      }
+    }
+  } else if (warp >= 6) {
+    // ---------------- dequantisers
+    const int d = threadIdx.x - 6 * 32;
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % kInStages, a = i % kAStages;
+      mbar_wait(&in_full[s], (i / kInStages) & 1, 2);
+      if (i >= kAStages) mbar_wait(&a_empty[a], ((i / kAStages) - 1) & 1, 2);
+      dequant_stage<W, F16>(raw_ring + s * kRawBytes, zbase, a_ring + a * kTileBytes, d);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (d == 0) {
+        mbar_arrive(&a_full[a]);
+        mbar_arrive(&in_empty[s]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5): TMEM lane quarter q = warp % 4 = weight rows 32q..
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + row;
+    const int64_t tile = min(tile0 + row / kTileRows, static_cast<int64_t>(n_tiles) - 1);
+    const float* sc = reinterpret_cast<const float*>(tiles + tile * nkb * bb + cbytes) + (row % kTileRows);
+    const int64_t sstride = bb / 4;  // floats between the scales of consecutive k-blocks
+    float acc[kTN];
+#pragma unroll
+    for (int c = 0; c < kTN; ++c) acc[c] = 0.f;
+    float s_next = nk > 0 ? sc[kb0 * sstride] : 0.f;
+    for (int i = 0; i < nk; ++i) {
+      const int dbuf = i & 1;
+      const float s_kb = s_next;
+      if (i + 1 < nk) s_next = sc[(kb0 + i + 1) * sstride];
+      mbar_wait(&d_full[dbuf], (i >> 1) & 1, 3);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(dbuf * kTN);
+#pragma unroll
+      for (int c0 = 0; c0 < kTN; c0 += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + static_cast<uint32_t>(c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[c0 + e] = fmaf(s_kb, __uint_as_float(v[e]), acc[c0 + e]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_empty[dbuf]);
+    }
+    if (n < N) {
+      const int t0 = tt * kTN;
+#pragma unroll
+      for (int c = 0; c < kTN; ++c) {
+        const int t = t0 + c;
         if (t < T) {
           float* yp = y + static_cast<int64_t>(t) * y_stride + n;
-          *yp = accumulate ? *yp + __uint_as_float(v[e]) : __uint_as_float(v[e]);
+          *yp = accumulate ? *yp + acc[c] : acc[c];
         }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTN));
 }
 
 // y[t][n] (+)= sum over the splits in order of ws[z][t][n] (deterministic split-K reduction)
@@ -329,30 +348,67 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, in
   }
 }
 
+// row-major [T, K] (bf16 / fp16 / f32, row stride x_stride) -> tiled bf16 (tiled_act_offset)
+__global__ void tile_acts_kernel(const void* __restrict__ x, int dtype, int64_t x_stride, int T, int64_t K, int nkb,
+                                 int out_f16, uint16_t* __restrict__ xt) {
+  const int64_t total = static_cast<int64_t>(T) * K;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / K, k = i - t * K;
+    float v;
+    if (dtype == FQ_DT_BF16) v = __bfloat162float(static_cast<const __nv_bfloat16*>(x)[t * x_stride + k]);
+    else if (dtype == FQ_DT_F16) v = __half2float(static_cast<const __half*>(x)[t * x_stride + k]);
+    else v = static_cast<const float*>(x)[t * x_stride + k];
+    uint16_t bits;
+    if (out_f16) {
+      const __half h = __float2half_rn(v);
+      bits = *reinterpret_cast<const uint16_t*>(&h);
+    } else {
+      const __nv_bfloat16 b = __float2bfloat16_rn(v);
+      bits = *reinterpret_cast<const uint16_t*>(&b);
+    }
+    xt[tiled_act_offset(static_cast<int>(t), k, nkb)] = bits;
+  }
+}
+
 template <int W, int F16>
-void configure_gemm(size_t smem) {
+void configure_gemm() {
   static bool done = false;
   if (!done) {
-    FQ_CUDA(cudaFuncSetAttribute(gemm_dq_kernel<W, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<W, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemGemm));
     done = true;
   }
 }
 
 }  // namespace
 
-void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* x, int x_dtype, int64_t x_stride,
-                    float* y, int64_t y_stride, bool accumulate) {
+int64_t tiled_act_elems(int64_t T, int64_t K) {
+  return (T + kTN - 1) / kTN * kTN * ((K + kTK - 1) / kTK * kTK);
+}
+
+void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride, int64_t T, int64_t K, void* xt,
+                      int out_dtype) {
+  const int64_t total = T * K;
+  const int blocks = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
+  tile_acts_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(x, x_dtype, x_stride, static_cast<int>(T), K,
+                                                                 ceil_div_i(K, kTK), out_dtype == FQ_DT_F16 ? 1 : 0,
+                                                                 static_cast<uint16_t*>(xt));
+  FQ_CUDA(cudaGetLastError());
+  ctx->launches += 1;
+}
+
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
+                    int64_t y_stride, bool accumulate) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
   if (x_dtype != FQ_DT_BF16 && x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: activations must be bf16 or fp16");
   const fq_rung_store& st = L->store(rung);
   if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
   if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
-  if (x_stride % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0)
-    fail(FQ_E_CONFIG, "gemm: activation rows must be 16-byte aligned (row stride a multiple of 8)");
+  if ((reinterpret_cast<uintptr_t>(xt) & 15) != 0) fail(FQ_E_CONFIG, "gemm: tiled activations must be 16-byte aligned");
   const int n_tiles = ceil_div_i(L->N, kTileRows), nkb = ceil_div_i(L->K, kBlockK);
   const int gx = ceil_div_i(L->N, kTM), gy = ceil_div_i(T, kTN);
   // split K when the output tiles alone leave SMs idle: the fewest splits with the lowest
-  // (waves x work per split), at least 4 k-steps per split
+  // (waves x work per split), at least 4 k-blocks per split
   int splits = 1;
   {
     const int64_t cta = gx * static_cast<int64_t>(gy);
@@ -379,16 +435,14 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
     split_stride = T * L->N;
   }
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
-  const size_t smem = static_cast<size_t>(kStagesG) * kStageBytesG;
-  const auto* xs = static_cast<const uint16_t*>(x);
   const int acc = splits > 1 ? 0 : (accumulate ? 1 : 0);
-  const int Ti = static_cast<int>(T);
-#define FQ_GEMM_LAUNCH(Wv, Fv)                                                                                     \
-  do {                                                                                                             \
-    configure_gemm<Wv, Fv>(smem);                                                                                  \
-    gemm_dq_kernel<Wv, Fv><<<grid, kGemmThreads, smem, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, L->K, \
-                                                                      xs, x_stride, Ti, out, out_stride, acc,       \
-                                                                      splits, split_stride);                        \
+  const auto* xb = static_cast<const uint8_t*>(xt);
+#define FQ_GEMM_LAUNCH(Wv, Fv)                                                                                   \
+  do {                                                                                                           \
+    configure_gemm<Wv, Fv>();                                                                                    \
+    gemm_ws_kernel<Wv, Fv><<<grid, kGemmThreads, kSmemGemm, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, \
+                                                                         xb, static_cast<int>(T), out, out_stride,  \
+                                                                         acc, splits, split_stride);                \
   } while (0)
   const bool f16 = x_dtype == FQ_DT_F16;
   if (rung == FQ_RUNG_INT8) {

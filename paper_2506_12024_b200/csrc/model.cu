@@ -330,6 +330,7 @@ struct fq_model {
   std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, StepMode) -> uploaded program
   unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
+  uint64_t built_epoch = 0;  // ctx->weight_epoch the cached programs / graphs were built at
   // device time of the step program kernels (events around the launch, captured into the graph)
   cudaEvent_t ev_prog[2] = {nullptr, nullptr};
   double prog_ms = 0.0;
@@ -391,7 +392,23 @@ enum StepMode : int { STEP_DECODE = 0, STEP_GEMV_ONLY = 1, STEP_PREFILL = 2 };
 // Prefill steps (STEP_PREFILL) take B consecutive positions of one sequence as their rows: an
 // append phase writes every row's RoPE'd key / value to the cache before the attention phase, so
 // row b attends to the rows before it in the same step.
+// Step programs and captured graphs bake in the tiled weight pointers: after any layer's resident
+// copies change (ctx->weight_epoch), drop them so the next step rebuilds against the new pointers.
+void sync_weight_epoch(fq_model* M) {
+  if (M->built_epoch == M->ctx->weight_epoch) return;
+  if (!M->graphs.empty() || !M->programs.empty()) {
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : M->programs) dfree(kv.second.dev_phases);
+    M->graphs.clear();
+    M->graph_kernels.clear();
+    M->programs.clear();
+  }
+  M->built_epoch = M->ctx->weight_epoch;
+}
+
 void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
+  if (!capturing(M->ctx->stream)) sync_weight_epoch(M);
   const bool gemv_only = mode == STEP_GEMV_ONLY;
   const bool prefill = mode == STEP_PREFILL;
   fq_ctx* ctx = M->ctx;
@@ -717,6 +734,7 @@ void run_step(fq_model* M, int B) {
     FQ_CUDA(cudaStreamSynchronize(st));
     return;
   }
+  sync_weight_epoch(M);
   auto it = M->graphs.find(B);
   if (it == M->graphs.end()) {
     if (M->programs.find(std::make_pair(B, 0)) == M->programs.end()) {
@@ -797,6 +815,8 @@ void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens,
     for (int i = 0; i < M->n_lin; ++i) {
       require(gemv_fast_supported(M->lin[i], FQ_RUNG_INT8) || !M->lin[i]->has(FQ_RUNG_INT8), FQ_E_STATE,
               "layer " + M->ids[i] + ": W8 copy not usable by the fast kernel");
+      require(gemv_fast_supported(M->lin[i], FQ_RUNG_INT4) || !M->lin[i]->has(FQ_RUNG_INT4), FQ_E_STATE,
+              "layer " + M->ids[i] + ": W4 copy not usable by the fast kernel");
     }
   }
   stage_rows(M, B, slots, tokens);
@@ -856,7 +876,7 @@ int64_t gemm_prefill_min() {
 bool gemm_prefill_usable(const fq_model* M, int slot, int64_t T) {
   const fq_model_config& c = M->cfg;
   const int64_t lo = gemm_prefill_min();
-  if (!M->llama || lo <= 0 || T < lo || c.act_dtype != FQ_DT_BF16) return false;
+  if (!M->llama || lo <= 0 || T < lo || (c.act_dtype != FQ_DT_BF16 && c.act_dtype != FQ_DT_F16)) return false;
   if (c.d_model % 8 != 0 || c.ffn_dim % 8 != 0) return false;
   for (int i = 0; i < M->n_lin; ++i) {
     const int r = M->rungs[static_cast<size_t>(slot) * M->n_lin + i];
@@ -892,9 +912,16 @@ void ensure_prefill_ws(fq_model* M, int64_t T) {
   w.g = f32(cap * f);
   w.u = f32(cap * f);
   w.logits = f32(cap * V);
-  w.h = dmalloc(2 * cap * d);
-  w.a = dmalloc(2 * cap * d);
-  w.m = dmalloc(2 * cap * f);
+  // GEMM inputs: tiled bf16 (tiled_act_offset), zero-filled so the padding rows / columns are 0
+  auto tiled = [&](int64_t K) {
+    const size_t bytes = 2 * static_cast<size_t>(tiled_act_elems(cap, K));
+    void* p = dmalloc(bytes);
+    FQ_CUDA(cudaMemset(p, 0, bytes));
+    return p;
+  };
+  w.h = tiled(d);
+  w.a = tiled(d);
+  w.m = tiled(f);
   w.stats = static_cast<fq_row_stats*>(dmalloc(sizeof(fq_row_stats) * cap));
   w.tok = static_cast<int32_t*>(dmalloc(sizeof(int32_t) * cap));
   w.cap = cap;
@@ -913,29 +940,30 @@ void prefill_gemm_enqueue(fq_model* M, int slot, const int32_t* tokens_host, int
   const int H = static_cast<int>(c.n_heads), hd = static_cast<int>(c.head_dim);
   const int Ti = static_cast<int>(T);
   const uint8_t* r = &M->rungs[static_cast<size_t>(slot) * M->n_lin];
+  const int ad = c.act_dtype;  // bf16 or fp16: the GEMM operands and roundings follow it
   FQ_CUDA(cudaMemcpyAsync(w.tok, tokens_host, sizeof(int32_t) * T, cudaMemcpyHostToDevice, st));
   prefill_embed(ctx, M->tok_emb, w.tok, Ti, d, w.x);
   __half* kv_slot = static_cast<__half*>(M->kv) + static_cast<int64_t>(slot) * M->slot_stride;
   for (int l = 0; l < c.n_layers; ++l) {
     const int b = M->lin_index(l, 0);
     __half* kvl = kv_slot + static_cast<int64_t>(l) * M->layer_stride;
-    prefill_rmsnorm(ctx, w.x, Ti, d, M->n1g[l], c.norm_eps, w.h);
-    launch_gemm_dq(ctx, M->lin[b + 0], r[b + 0], T, w.h, FQ_DT_F16, d, w.q, d);
-    launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, FQ_DT_F16, d, w.k, d);
-    launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, FQ_DT_F16, d, w.v, d);
-    prefill_rope_kv(ctx, w.q, w.k, w.v, Ti, H, hd, M->rope_cs, w.qr, kvl, c.max_seq_len);
-    prefill_attention(ctx, w.qr, kvl, H, hd, c.max_seq_len, Ti, w.a);
-    launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, FQ_DT_F16, d, w.x, d, true);  // x += attn . Wo^T
-    prefill_rmsnorm(ctx, w.x, Ti, d, M->n2g[l], c.norm_eps, w.h);
-    launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, FQ_DT_F16, d, w.g, f);
-    launch_gemm_dq(ctx, M->lin[b + 5], r[b + 5], T, w.h, FQ_DT_F16, d, w.u, f);
-    prefill_swiglu(ctx, w.g, w.u, T * f, w.m);
-    launch_gemm_dq(ctx, M->lin[b + 6], r[b + 6], T, w.m, FQ_DT_F16, f, w.x, d, true);  // x += mid . Wdown^T
+    prefill_rmsnorm(ctx, w.x, Ti, d, M->n1g[l], c.norm_eps, w.h, ad);
+    launch_gemm_dq(ctx, M->lin[b + 0], r[b + 0], T, w.h, ad, w.q, d);
+    launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, ad, w.k, d);
+    launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, ad, w.v, d);
+    prefill_rope_kv(ctx, w.q, w.k, w.v, Ti, H, hd, M->rope_cs, w.qr, kvl, c.max_seq_len, ad);
+    prefill_attention(ctx, w.qr, kvl, H, hd, c.max_seq_len, Ti, w.a, ad);
+    launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, ad, w.x, d, true);  // x += attn . Wo^T
+    prefill_rmsnorm(ctx, w.x, Ti, d, M->n2g[l], c.norm_eps, w.h, ad);
+    launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, ad, w.g, f);
+    launch_gemm_dq(ctx, M->lin[b + 5], r[b + 5], T, w.h, ad, w.u, f);
+    prefill_swiglu(ctx, w.g, w.u, T * f, f, w.m, ad);
+    launch_gemm_dq(ctx, M->lin[b + 6], r[b + 6], T, w.m, ad, w.x, d, true);  // x += mid . Wdown^T
   }
-  prefill_rmsnorm(ctx, w.x, Ti, d, M->fng, c.norm_eps, w.h);
+  prefill_rmsnorm(ctx, w.x, Ti, d, M->fng, c.norm_eps, w.h, ad);
   float* lg = logits_out ? logits_out : w.logits;
   const int hi = M->head_index();
-  launch_gemm_dq(ctx, M->lin[hi], r[hi], T, w.h, FQ_DT_F16, d, lg, V);
+  launch_gemm_dq(ctx, M->lin[hi], r[hi], T, w.h, ad, lg, V);
   if (stats_dev) launch_softmax_stats(ctx, lg, T, V, V, stats_dev);
 }
 
@@ -1299,6 +1327,8 @@ fq_status fq_model_set_rung(fq_model* M, int32_t slot, int32_t li, int32_t rung)
       fail(FQ_E_STATE, "set_precision: layer '" + M->ids[li] + "' has no rung '" +
                            (rung == FQ_RUNG_FP ? "fp" : rung == FQ_RUNG_INT8 ? "8" : "4") + "'");
     if (M->llama && rung == FQ_RUNG_FP) fail(FQ_E_STATE, "llama arch: the fp rung is not resident on the device");
+    if (M->llama && !gemv_fast_supported(M->lin[li], rung))
+      fail(FQ_E_STATE, "set_precision: layer '" + M->ids[li] + "' has no tiled copy of that rung (zero points span > 255)");
     M->rungs[static_cast<size_t>(slot) * M->n_lin + li] = static_cast<uint8_t>(rung);
   });
 }

@@ -8,10 +8,20 @@
 namespace fqc {
 namespace {
 
-__device__ __forceinline__ float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
-// GEMM operand: the bf16-rounded activation (the decode contract) carried as fp16, exact in fp16's
-// normal range, so the GEMM can dequantise its weights to fp16 (kind::f16 takes one operand type)
-__device__ __forceinline__ __half act16(float v) { return __float2half_rn(bf16r(v)); }
+// rounding to the activation dtype (bf16, or fp16 when f16), as the decode program's round_act
+__device__ __forceinline__ float actr(float v, int f16) {
+  return f16 ? __half2float(__float2half_rn(v)) : __bfloat162float(__float2bfloat16_rn(v));
+}
+// GEMM operand: the activation rounded to the activation dtype, its 16-bit pattern stored in the
+// tiled layout (tiled_act_offset)
+__device__ __forceinline__ uint16_t actb(float v, int f16) {
+  if (f16) {
+    const __half h = __float2half_rn(v);
+    return *reinterpret_cast<const uint16_t*>(&h);
+  }
+  const __nv_bfloat16 b = __float2bfloat16_rn(v);
+  return *reinterpret_cast<const uint16_t*>(&b);
+}
 
 __global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32_t* __restrict__ tokens, int64_t d,
                                   float* __restrict__ x) {
@@ -22,7 +32,7 @@ __global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32
 
 // h[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * g)
 __global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g, float eps,
-                                    __half* __restrict__ h) {
+                                    uint16_t* __restrict__ h, int nkb, int f16) {
   const int t = blockIdx.x;
   const float* xr = x + t * d;
   float s = 0.f;
@@ -40,14 +50,14 @@ __global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, cons
   }
   __syncthreads();
   const float rstd = 1.0f / sqrtf(red[0] / static_cast<float>(d) + eps);
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) h[t * d + i] = act16(xr[i] * rstd * g[i]);
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) h[tiled_act_offset(t, i, nkb)] = actb(xr[i] * rstd * g[i], f16);
 }
 
 // q/k/v rows (fp32 GEMM outputs, rounded to bf16 as the decode step stores them) -> RoPE'd and
 // pre-scaled q (fp32) and the fp16 K / V cache rows 0..T-1 of the slot.
 __global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
                                     int H, int hd, const float2* __restrict__ cs, float* __restrict__ qr,
-                                    __half* __restrict__ kv_layer, int64_t max_seq) {
+                                    __half* __restrict__ kv_layer, int64_t max_seq, int f16) {
   const int t = blockIdx.x;
   const int d = H * hd, half = hd / 2;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
@@ -55,16 +65,16 @@ __global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __
     const int h = idx / half, i = idx - h * half;
     const int64_t o0 = static_cast<int64_t>(t) * d + h * hd + i, o1 = o0 + half;
     const float2 c = cs[static_cast<int64_t>(t) * half + i];
-    const float q0 = bf16r(q[o0]), q1 = bf16r(q[o1]);
+    const float q0 = actr(q[o0], f16), q1 = actr(q[o1], f16);
     qr[o0] = (q0 * c.x - q1 * c.y) * scale;
     qr[o1] = (q1 * c.x + q0 * c.y) * scale;
-    const float k0 = bf16r(k[o0]), k1 = bf16r(k[o1]);
+    const float k0 = actr(k[o0], f16), k1 = actr(k[o1], f16);
     __half* kc = kv_layer + static_cast<int64_t>(h) * max_seq * hd + static_cast<int64_t>(t) * hd;
     __half* vc = kc + static_cast<int64_t>(H) * max_seq * hd;
     kc[i] = __float2half_rn(k0 * c.x - k1 * c.y);
     kc[i + half] = __float2half_rn(k1 * c.x + k0 * c.y);
-    vc[i] = __float2half_rn(bf16r(v[o0]));
-    vc[i + half] = __float2half_rn(bf16r(v[o1]));
+    vc[i] = __float2half_rn(actr(v[o0], f16));
+    vc[i + half] = __float2half_rn(actr(v[o1], f16));
   }
 }
 
@@ -72,7 +82,7 @@ __global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __
 // the keys 0..t of the fp16 cache; output bf16.
 template <int DPL>
 __global__ void attn_rows_kernel(const float* __restrict__ qr, const __half* __restrict__ kv_layer, int H, int64_t max_seq,
-                                 int T, __half* __restrict__ out) {
+                                 int T, uint16_t* __restrict__ out, int nkb, int f16) {
   constexpr int hd = DPL * 32;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= T * H) return;
@@ -100,16 +110,17 @@ __global__ void attn_rows_kernel(const float* __restrict__ qr, const __half* __r
     m = mn;
   }
 #pragma unroll
-  for (int e = 0; e < DPL; ++e) out[static_cast<int64_t>(t) * d + h * hd + DPL * lane + e] = act16(o[e] / l);
+  for (int e = 0; e < DPL; ++e) out[tiled_act_offset(t, h * hd + DPL * lane + e, nkb)] = actb(o[e] / l, f16);
 }
 
-__global__ void swiglu_rows_kernel(const float* __restrict__ g, const float* __restrict__ u, int64_t n,
-                                   __half* __restrict__ out) {
+__global__ void swiglu_rows_kernel(const float* __restrict__ g, const float* __restrict__ u, int64_t n, int64_t f,
+                                   uint16_t* __restrict__ out, int nkb, int f16) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float gv = g[i];  // unrounded GEMM sums, as the decode step's SwiGLU epilogue reads them
     const float silu = gv / (1.0f + expf(-gv));
-    out[i] = act16(silu * u[i]);
+    const int64_t t = i / f;
+    out[tiled_act_offset(static_cast<int>(t), i - t * f, nkb)] = actb(silu * u[i], f16);
   }
 }
 
@@ -123,33 +134,38 @@ void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev,
   ctx->launches += 1;
 }
 
-void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16) {
-  rmsnorm_rows_kernel<<<T, 256, 0, ctx->stream>>>(x, d, g, eps, static_cast<__half*>(h16));
+void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16, int act_dtype) {
+  rmsnorm_rows_kernel<<<T, 256, 0, ctx->stream>>>(x, d, g, eps, static_cast<uint16_t*>(h16), ceil_div_i(d, 128),
+                                                  act_dtype == FQ_DT_F16 ? 1 : 0);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
 }
 
 void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,
-                     const float2* cs, float* qr, __half* kv_layer, int64_t max_seq) {
-  rope_kv_rows_kernel<<<T, 256, 0, ctx->stream>>>(q, k, v, H, hd, cs, qr, kv_layer, max_seq);
+                     const float2* cs, float* qr, __half* kv_layer, int64_t max_seq, int act_dtype) {
+  rope_kv_rows_kernel<<<T, 256, 0, ctx->stream>>>(q, k, v, H, hd, cs, qr, kv_layer, max_seq, act_dtype == FQ_DT_F16 ? 1 : 0);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
 }
 
 void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
-                       void* out16) {
+                       void* out16, int act_dtype) {
+  const int f16 = act_dtype == FQ_DT_F16 ? 1 : 0;
   const int warps = T * H;
   const int blocks = (warps * 32 + 255) / 256;
   if (hd == 128)
-    attn_rows_kernel<4><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<__half*>(out16));
+    attn_rows_kernel<4><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<uint16_t*>(out16),
+                                                        ceil_div_i(static_cast<int64_t>(H) * hd, 128), f16);
   else
-    attn_rows_kernel<2><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<__half*>(out16));
+    attn_rows_kernel<2><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<uint16_t*>(out16),
+                                                        ceil_div_i(static_cast<int64_t>(H) * hd, 128), f16);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
 }
 
-void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, void* out16) {
-  swiglu_rows_kernel<<<elem_grid(ctx, n), 256, 0, ctx->stream>>>(g, u, n, static_cast<__half*>(out16));
+void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, int64_t f, void* out16, int act_dtype) {
+  swiglu_rows_kernel<<<elem_grid(ctx, n), 256, 0, ctx->stream>>>(g, u, n, f, static_cast<uint16_t*>(out16),
+                                                                 ceil_div_i(f, 128), act_dtype == FQ_DT_F16 ? 1 : 0);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
 }

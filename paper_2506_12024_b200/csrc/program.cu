@@ -27,6 +27,9 @@
 // 1024 X_lo + 64 X_hi (dx.y) instead of 64 X
 #define FQ_W4_LO 0  // opt-in: -5% W4 step, but 15-25x the W4 cancellation error (tools/w4_error_probe.py)
 #endif
+#ifndef FQ_SPLIT_ACC
+#define FQ_SPLIT_ACC 0  // two MMA accumulator chains per block (A/B experiment)
+#endif
 #ifndef FQ_GEMV_HOOKS
 #define FQ_GEMV_HOOKS 1  // per-phase GEMV detail stamps (tools/phase_profile.py); 0 compiles them out
 #endif
@@ -919,6 +922,17 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
   for (int n = 0; n < NBLK; ++n)
 #pragma unroll
     for (int e = 0; e < 4; ++e) c[n][e] = 0.f;
+#if FQ_SPLIT_ACC
+  // second accumulator set: each block's 8 dependent MMAs become two chains of 4
+  float c2[NBLK][4];
+#pragma unroll
+  for (int n = 0; n < NBLK; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) c2[n][e] = 0.f;
+#define FQ_ACC2 c2
+#else
+#define FQ_ACC2 c
+#endif
   if constexpr (W == 0) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -928,7 +942,7 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
         const uint4 xv = xl[n * kXBlk + p * 4];
         mma16816(c[n], prmt(wv.x, 0x64646464u, 0x4140u), prmt(wv.x, 0x64646464u, 0x4342u),
                  prmt(wv.y, 0x64646464u, 0x4140u), prmt(wv.y, 0x64646464u, 0x4342u), xv.x, xv.y);
-        mma16816(c[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
+        mma16816(FQ_ACC2[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
                  prmt(wv.w, 0x64646464u, 0x4140u), prmt(wv.w, 0x64646464u, 0x4342u), xv.z, xv.w);
       }
     }
@@ -946,16 +960,24 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
           // every nibble pair is moved to bits 4-7 / 20-23 of the halves: fp16 0x5400 | q<<4 = 64 + q
           const uint32_t q = qs[u];
           const uint4 xv = u < 2 ? x0 : x1;
+          float (&acc)[4] = (u & 1) ? FQ_ACC2[n] : c[n];
           if (FQ_W4_LO)
-            mma16816(c[n], nib_lo_f16(q), nib_lo_f16(q >> 8), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
+            mma16816(acc, nib_lo_f16(q), nib_lo_f16(q >> 8), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
                      (u & 1) ? xv.w : xv.y);
           else
-          mma16816(c[n], nib_f16(q << 4), nib_f16(q >> 4), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
+          mma16816(acc, nib_f16(q << 4), nib_f16(q >> 4), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
                    (u & 1) ? xv.w : xv.y);
         }
       }
     }
   }
+#if FQ_SPLIT_ACC
+#pragma unroll
+  for (int n = 0; n < NBLK; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) c[n][e] += c2[n][e];
+#endif
+#undef FQ_ACC2
   constexpr int cbytes = W == 0 ? 2048 : 1024;
 #pragma unroll
   for (int n = 0; n < NBLK; ++n) {
@@ -2396,11 +2418,15 @@ void launch_program(fq_ctx* ctx, const ProgramRun& run, unsigned int* barrier, b
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = run.smem;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // cooperative: the grid barriers need every CTA resident at once -- the launch fails cleanly
+  // (instead of spinning into the watchdog) when another stream's kernel holds SMs
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = pdl ? 2 : 1;
   if (run.dev_phases && run.lean)
     FQ_CUDA(cudaLaunchKernelEx(&cfg, program_kernel_lean, static_cast<const Phase*>(run.dev_phases), run.nphases, barrier,
                                L));

@@ -221,13 +221,17 @@ void finalize_rung_meta(fq_ctx* ctx, fq_layer* L, int rung) {
   st.zp_fits_u8 = (static_cast<int64_t>(h[1]) - h[0]) <= 255;
   st.zp_base = st.zp_fits_u8 ? h[0] : 0;
   const bool one_group_per_block = L->G % kBlockK == 0 || L->G >= L->K;
-  dfree(st.tiles);
-  st.tiles = nullptr;
-  st.tiles_bytes = 0;
-  if (st.zp_fits_u8 && one_group_per_block) {
-    const int64_t n_tiles = (L->N + kTileRows - 1) / kTileRows, nkb = (L->K + kBlockK - 1) / kBlockK;
-    st.tiles_bytes = n_tiles * nkb * (st.bits == 8 ? kBlockBytes8 : kBlockBytes4);
-    st.tiles = static_cast<uint8_t*>(dmalloc(static_cast<size_t>(st.tiles_bytes)));
+  ctx->weight_epoch += 1;  // cached step programs / graphs hold tile pointers: rebuild them
+  const int64_t n_tiles = (L->N + kTileRows - 1) / kTileRows, nkb = (L->K + kBlockK - 1) / kBlockK;
+  const int64_t want = (st.zp_fits_u8 && one_group_per_block) ? n_tiles * nkb * (st.bits == 8 ? kBlockBytes8 : kBlockBytes4) : 0;
+  if (want != st.tiles_bytes) {  // same size: repack in place (the pointer stays valid)
+    dfree(st.tiles);
+    st.tiles = nullptr;
+    st.tiles_bytes = 0;
+  }
+  if (want > 0) {
+    if (st.tiles == nullptr) st.tiles = static_cast<uint8_t*>(dmalloc(static_cast<size_t>(want)));
+    st.tiles_bytes = want;
     tile_pack_kernel<<<static_cast<unsigned>(n_tiles * nkb), 128, 0, ctx->stream>>>(
         st.payload, st.scale, st.zp32, L->N, L->K, L->G, L->ng, L->ng_pad, st.bits, st.zp_base, nkb, st.tiles);
     FQ_CUDA(cudaGetLastError());

@@ -134,7 +134,8 @@ PYBIND11_MODULE(_flexquant, m) {
       .def_readwrite("group_size", &ModelConfig::group_size)
       .def_readwrite("max_batch", &ModelConfig::max_batch)
       .def_readwrite("norm_eps", &ModelConfig::norm_eps)
-      .def_readwrite("rope_theta", &ModelConfig::rope_theta);
+      .def_readwrite("rope_theta", &ModelConfig::rope_theta)
+      .def_readwrite("fp16_activations", &ModelConfig::fp16_activations);
   py::class_<SwitchEvent>(m, "SwitchEvent")
       .def_readonly("layer_id", &SwitchEvent::layer_id)
       .def_readonly("from_", &SwitchEvent::from)

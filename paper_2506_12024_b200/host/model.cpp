@@ -22,7 +22,7 @@ uint64_t now_ns() {
 fq_model_config to_c(const ModelConfig& c) {
   fq_model_config m{};
   m.arch = static_cast<int32_t>(c.arch);
-  m.act_dtype = c.arch == Arch::Llama ? FQ_DT_BF16 : FQ_DT_F32;
+  m.act_dtype = c.arch == Arch::Llama ? (c.fp16_activations ? FQ_DT_F16 : FQ_DT_BF16) : FQ_DT_F32;
   m.vocab_size = c.vocab_size;
   m.d_model = c.d_model;
   m.n_heads = c.n_heads;

@@ -5,7 +5,7 @@
   trace tests/golden/det_t0.jsonl (tokens, PPLE, fault tolerance, moving averages, effective
   bits, bytes, switch events) — the schedule bit-identical to the CPU reference.
 * Llama architecture: teacher-forced logits within 1e-2 relative of the numpy restatement
-  (oracle/llama.py), entropy within 1e-3 absolute, identical greedy tokens where the top-2
+  (oracle/llama.py), entropy within 1e-4 absolute, identical greedy tokens where the top-2
   margin exceeds the numeric error.
 """
 import json
@@ -134,6 +134,9 @@ def test_reference_arch_reproduces_golden_trace(ctx):
 
 
 LLAMA_TINY = dict(vocab_size=8192, d_model=512, n_heads=8, head_dim=64, n_layers=4, ffn_dim=1376, max_seq_len=128)
+# head_dim 128 (the 7B head size) on a small model: the uint2 K/V loads, 64-wide RoPE pairs and
+# the <4>-instantiated attention / append paths
+LLAMA_HD128 = dict(vocab_size=4096, d_model=256, n_heads=2, head_dim=128, n_layers=2, ffn_dim=768, max_seq_len=128)
 
 
 def _llama(ctx, max_batch=1, cfg=LLAMA_TINY):
@@ -146,12 +149,14 @@ def _llama(ctx, max_batch=1, cfg=LLAMA_TINY):
 import oracle.llama  # noqa: E402
 
 
+@pytest.mark.parametrize("cfg", [LLAMA_TINY, LLAMA_HD128], ids=["hd64", "hd128"])
 @pytest.mark.parametrize("rung", [capi.RUNG_INT8, capi.RUNG_INT4])
-def test_llama_teacher_forced_logits(ctx, rung):
-    m, orc = _llama(ctx)
+def test_llama_teacher_forced_logits(ctx, rung, cfg):
+    m, orc = _llama(ctx, cfg=cfg)
     m.set_all_rungs(0, rung)
-    toks = oracle.random_tokens(24, 8192, 7)
-    out = torch.zeros((1, 8192), dtype=torch.float32, device="cuda")
+    V = cfg["vocab_size"]
+    toks = oracle.random_tokens(24, V, 7)
+    out = torch.zeros((1, V), dtype=torch.float32, device="cuda")
     cache = orc.new_cache()
     bits = 8 if rung == capi.RUNG_INT8 else 4
     worst = 0.0
@@ -163,33 +168,11 @@ def test_llama_teacher_forced_logits(ctx, rung):
         rel = np.max(np.abs(got - want)) / np.max(np.abs(want))
         worst = max(worst, rel)
         o = oracle.row_stats(want)
-        assert abs(st["entropy"][0] - o["entropy"]) <= 1e-3
+        assert abs(st["entropy"][0] - o["entropy"]) <= 1e-4  # north_star: entropy within 1e-4 absolute
         gap = np.sort(want)[-1] - np.sort(want)[-2]
         if gap > 20 * np.max(np.abs(got - want)):
             assert st["argmax"][0] == o["argmax"]
     assert worst <= 1e-2, worst
-
-
-@pytest.mark.parametrize("env", ["FQ_TAGS", "FQ_NO_FRAG", "FQ_NO_TAGS", "FQ_HEAD_FLAGS"])
-def test_llama_step_program_variants_match_oracle(ctx, monkeypatch, env):
-    # the opt-in hand-off variants of the step program (tagged activation words instead of the
-    # grid barrier before the O / down projections; plain staging instead of pre-staged fragments)
-    # compute the same step: teacher-forced logits within the north-star tolerance
-    monkeypatch.setenv(env, "1")
-    m, orc = _llama(ctx)
-    rungs = [8 if i % 2 else 4 for i in range(len(orc.ids))]
-    for i, r in enumerate(rungs):
-        m.set_rung(0, i, capi.RUNG_INT8 if r == 8 else capi.RUNG_INT4)
-    toks = oracle.random_tokens(10, 8192, 13)
-    out = torch.zeros((1, 8192), dtype=torch.float32, device="cuda")
-    cache = orc.new_cache()
-    for t in toks:
-        st = m.decode([0], [int(t)], out)
-        ctx.synchronize()
-        want = orc.step(int(t), cache, rungs)
-        got = out.cpu().numpy()[0]
-        assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= 1e-2
-        assert abs(st["entropy"][0] - oracle.row_stats(want)["entropy"]) <= 1e-3
 
 
 def test_llama_mixed_rungs_and_switch_is_pointer_swap(ctx):
@@ -264,17 +247,20 @@ def test_llama_logit_kl_calibration_small(ctx):
             a = orc.step(int(t), c8, [8] * len(orc.ids))
             b = orc.step(int(t), c4, r4)
             tot += oracle.kl_logits(b, a)[0]
-    assert abs(kl[0] - tot / 16) <= 1e-3 * max(1.0, tot / 16) + 1e-4
+    print("logit KL (GEMV path)", kl[0], tot / 16)
+    assert abs(kl[0] - tot / 16) <= 1e-4  # north_star: KL within 1e-4 absolute
 
 
+@pytest.mark.parametrize("cfg", [LLAMA_TINY, LLAMA_HD128], ids=["hd64", "hd128"])
 @pytest.mark.parametrize("n", [1, 8, 13, 21])
-def test_llama_chunked_prefill_matches_oracle_and_decode(ctx, n):
+def test_llama_chunked_prefill_matches_oracle_and_decode(ctx, n, cfg):
     """Prefill runs 8 prompt positions per step (append phase + causal attention over the cache):
     every row's logits follow the numpy restatement, and the cache it leaves behind continues
     exactly like a position-by-position run."""
-    m, orc = _llama(ctx, max_batch=2)
-    toks = oracle.random_tokens(n + 3, 8192, 100 + n)
-    out = torch.zeros((n, 8192), dtype=torch.float32, device="cuda")
+    m, orc = _llama(ctx, max_batch=2, cfg=cfg)
+    V = cfg["vocab_size"]
+    toks = oracle.random_tokens(n + 3, V, 100 + n)
+    out = torch.zeros((n, V), dtype=torch.float32, device="cuda")
     st = m.prefill(0, toks[:n], out)
     ctx.synchronize()
     got = out.cpu().numpy()
@@ -297,17 +283,19 @@ def test_llama_chunked_prefill_matches_oracle_and_decode(ctx, n):
         assert a["argmax"] == b["argmax"]
 
 
+@pytest.mark.parametrize("cfg", [LLAMA_TINY, LLAMA_HD128], ids=["hd64", "hd128"])
 @pytest.mark.parametrize("n,mixed", [(16, False), (100, True)])
-def test_llama_tensor_core_prefill_matches_oracle(ctx, n, mixed):
+def test_llama_tensor_core_prefill_matches_oracle(ctx, n, mixed, cfg):
     """Prompts of >= 16 tokens go through the tcgen05 prefill (all rows of a block at once, weights
     dequantised to bf16 tiles): every row's logits within the north-star 1e-2 relative of the numpy
     restatement, and the cache it leaves behind continues like the oracle's."""
-    m, orc = _llama(ctx)
+    m, orc = _llama(ctx, cfg=cfg)
+    V = cfg["vocab_size"]
     rungs = [8 if (i % 3 or not mixed) else 4 for i in range(len(orc.ids))]
     for i, r in enumerate(rungs):
         m.set_rung(0, i, capi.RUNG_INT8 if r == 8 else capi.RUNG_INT4)
-    toks = oracle.random_tokens(n + 4, 8192, 300 + n)
-    out = torch.zeros((n, 8192), dtype=torch.float32, device="cuda")
+    toks = oracle.random_tokens(n + 4, V, 300 + n)
+    out = torch.zeros((n, V), dtype=torch.float32, device="cuda")
     st = m.prefill(0, toks[:n], out)
     ctx.synchronize()
     assert m.slot_length(0) == n
@@ -320,9 +308,9 @@ def test_llama_tensor_core_prefill_matches_oracle(ctx, n, mixed):
         o = oracle.row_stats(got[i])
         assert abs(st["entropy"][i] - o["entropy"]) <= 1e-5
         assert int(st["argmax"][i]) == o["argmax"]
-        assert abs(st["entropy"][i] - oracle.row_stats(want)["entropy"]) <= 1e-3
+        assert abs(st["entropy"][i] - oracle.row_stats(want)["entropy"]) <= 1e-4
     # decode continues from the cache the prefill wrote (K/V rows 0..n-1 of every layer)
-    dec = torch.zeros((1, 8192), dtype=torch.float32, device="cuda")
+    dec = torch.zeros((1, V), dtype=torch.float32, device="cuda")
     for t in toks[n:]:
         m.decode([0], [int(t)], dec)
         ctx.synchronize()
@@ -347,5 +335,6 @@ def test_llama_logit_kl_calibration_tensor_core(ctx):
             b = orc.step(int(t), c4, r4)
             tot += oracle.kl_logits(b, a)[0]
     want = tot / 40
-    assert abs(kl[0] - want) <= 5e-2 * want + 1e-4, (kl[0], want)
+    print("logit KL (tcgen05 path)", kl[0], want)
+    assert abs(kl[0] - want) <= 1e-4, (kl[0], want)  # north_star: KL within 1e-4 absolute
     assert m.slot_length(0) == 0
