@@ -135,12 +135,25 @@ fq_status fq_gemv_chain_time(fq_ctx* ctx, const fq_layer* const* layers, int32_t
                              int32_t reps, double* ms_per_launch);
 
 /* Prefill / calibration contraction on the tcgen05 tensor cores (BASELINE config 4):
- * y[rows, N] (fp32, row stride y_stride) = x[rows, K] (bf16, row stride x_stride) . dequant(W_rung)^T,
- * the dequantisation of the resident tiled W8/W4 copy fused into the tile loads (fp16 operands,
- * fp32 accumulation in tensor memory).  MultiPrecisionLayer::forward (src/model.cpp:77-98) on
- * many rows at once. */
+ * y[rows, N] (fp32, row stride y_stride) = x[rows, K] (bf16, row stride x_stride) . dequant(W_rung)^T.
+ * MultiPrecisionLayer::forward (src/model.cpp:77-98) on many rows at once.  The tensor cores
+ * multiply the exact integer codes (q - z) by the activations, each 128-code quantization group
+ * accumulates alone in fp32 in tensor memory and its fp32 scale is applied in the epilogue, so
+ * no weight is rounded (the decode GEMV's precision contract).  x is re-laid into the GEMM's
+ * tiled operand format in context scratch first (fq_tile_activations). */
 fq_status fq_gemm(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int64_t rows, const void* x_dev,
                   int64_t x_stride, float* y_dev, int64_t y_stride);
+/* The GEMM's activation operand format: 16-bit [ceil(rows/128)][ceil(K/128)][128 x 128] tiles in
+ * the UMMA canonical K-major layout, rows past `rows` / columns past K zero.  Bytes needed: */
+int64_t fq_tiled_activation_bytes(int64_t rows, int64_t K);
+/* x (x_dtype f32 / f16 / bf16, row stride x_stride) -> tiled fp16 (out_dtype must be FQ_DT_F16:
+ * bf16 values are exact in fp16's normal range); xt_dev must hold fq_tiled_activation_bytes and be
+ * zeroed once by the caller. */
+fq_status fq_tile_activations(fq_ctx* ctx, const void* x_dev, int32_t x_dtype, int64_t x_stride, int64_t rows,
+                              int64_t K, int32_t out_dtype, void* xt_dev);
+/* fq_gemm on pre-tiled fp16 activations (x_dtype FQ_DT_F16): the prefill's own call. */
+fq_status fq_gemm_tiled(fq_ctx* ctx, const fq_layer* layer, int32_t rung, int64_t rows, const void* xt_dev,
+                        int32_t x_dtype, float* y_dev, int64_t y_stride, int32_t accumulate);
 
 /* ------------------------------------------------------- statistics (a10, a11, a18) */
 /* One fq_row_stats per logits row (fp32 [rows, vocab] on device); stats_dev on device. */

@@ -33,7 +33,8 @@ ABI_FUNCTIONS = [
     "fq_model_get_rung", "fq_model_set_all_rungs", "fq_model_reset_slot", "fq_model_slot_length", "fq_model_prefill",
     "fq_model_decode", "fq_model_logits", "fq_model_step_bytes", "fq_model_calibrate_logit_kl",
     "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step", "fq_gemm",
-    "fq_model_step_kernel_time", "fq_gemv_chain_time",
+    "fq_model_step_kernel_time", "fq_gemv_chain_time", "fq_tiled_activation_bytes", "fq_tile_activations",
+    "fq_gemm_tiled",
 ]
 
 
@@ -154,11 +155,15 @@ def load(path: str = LIB_PATH):
         "fq_model_profile_gemvs": [v, i32, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64)],
         "fq_model_profile_step": [v, i32, i32, v, i64, C.POINTER(i32), C.POINTER(i32), v],
         "fq_gemm": [v, v, i32, i64, v, i64, v, i64],
+        "fq_tile_activations": [v, v, i32, i64, i64, i64, i32, v],
+        "fq_gemm_tiled": [v, v, i32, i64, v, i32, v, i64, i32],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = i32
+    L.fq_tiled_activation_bytes.argtypes = [i64, i64]
+    L.fq_tiled_activation_bytes.restype = i64
     _lib = L
     return L
 
@@ -240,6 +245,17 @@ class Context:
         """y[rows, N] = x[rows, K] . dequant(W_rung)^T on the tcgen05 tensor cores."""
         check(self.L.fq_gemm(self.h, layer.h, rung, rows, _ptr(x_bf16), x_stride or layer.K, _ptr(y_f32),
                              y_stride or layer.N))
+
+    def tile_activations(self, x, x_dtype: int, rows: int, K: int, out_dtype: int, xt, x_stride: int = 0) -> None:
+        check(self.L.fq_tile_activations(self.h, _ptr(x), x_dtype, x_stride or K, rows, K, out_dtype, _ptr(xt)))
+
+    def tiled_activation_bytes(self, rows: int, K: int) -> int:
+        return int(self.L.fq_tiled_activation_bytes(rows, K))
+
+    def gemm_tiled(self, layer: "Layer", rung: int, rows: int, xt, x_dtype: int, y_f32, y_stride: int = 0,
+                   accumulate: bool = False) -> None:
+        check(self.L.fq_gemm_tiled(self.h, layer.h, rung, rows, _ptr(xt), x_dtype, _ptr(y_f32), y_stride or layer.N,
+                                   1 if accumulate else 0))
 
     def softmax_stats(self, logits, rows: int, vocab: int, stats_dev) -> None:
         check(self.L.fq_softmax_stats(self.h, _ptr(logits), rows, vocab, _ptr(stats_dev)))

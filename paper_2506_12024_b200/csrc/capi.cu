@@ -352,8 +352,33 @@ fq_status fq_gemm(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t rows, co
     const size_t bytes = 2 * static_cast<size_t>(tiled_act_elems(rows, L->K));
     void* xt = ctx->ensure_scratch(bytes);
     FQ_CUDA(cudaMemsetAsync(xt, 0, bytes, ctx->stream));
-    launch_tile_acts(ctx, x_dev, FQ_DT_BF16, x_stride, rows, L->K, xt);
-    launch_gemm_dq(ctx, L, rung, rows, xt, FQ_DT_BF16, y_dev, y_stride);
+    launch_tile_acts(ctx, x_dev, FQ_DT_BF16, x_stride, rows, L->K, xt, FQ_DT_F16);  // bf16 -> fp16: exact in range
+    launch_gemm_dq(ctx, L, rung, rows, xt, FQ_DT_F16, y_dev, y_stride);
+  });
+}
+
+int64_t fq_tiled_activation_bytes(int64_t rows, int64_t K) {
+  return rows < 1 || K < 1 ? 0 : 2 * tiled_act_elems(rows, K);
+}
+
+fq_status fq_tile_activations(fq_ctx* ctx, const void* x_dev, int32_t x_dtype, int64_t x_stride, int64_t rows,
+                              int64_t K, int32_t out_dtype, void* xt_dev) {
+  return guarded([&] {
+    require(ctx != nullptr && x_dev != nullptr && xt_dev != nullptr, FQ_E_INPUT, "null argument");
+    require(rows >= 1 && K >= 1 && x_stride >= K, FQ_E_DIMENSION, "tile_activations: bad shape");
+    require(x_dtype >= FQ_DT_F32 && x_dtype <= FQ_DT_BF16, FQ_E_CONFIG, "tile_activations: bad input dtype");
+    require(out_dtype == FQ_DT_F16, FQ_E_CONFIG, "tile_activations: the GEMM operand format is fp16");
+    launch_tile_acts(ctx, x_dev, x_dtype, x_stride, rows, K, xt_dev, out_dtype);
+  });
+}
+
+fq_status fq_gemm_tiled(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t rows, const void* xt_dev, int32_t x_dtype,
+                        float* y_dev, int64_t y_stride, int32_t accumulate) {
+  return guarded([&] {
+    require(ctx != nullptr && L != nullptr && xt_dev != nullptr && y_dev != nullptr, FQ_E_INPUT, "null argument");
+    require(rows >= 1, FQ_E_DIMENSION, "gemm: rows must be >= 1");
+    require(y_stride >= L->N, FQ_E_DIMENSION, "gemm: row stride smaller than the row");
+    launch_gemm_dq(ctx, L, rung, rows, xt_dev, x_dtype, y_dev, y_stride, accumulate != 0);
   });
 }
 

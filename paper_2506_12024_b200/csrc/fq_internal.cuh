@@ -198,6 +198,8 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
                     int64_t y_stride, bool accumulate = false);
 
 // row-parallel prefill kernels (prefill.cu; llama arch; GEMM operands bf16, stored tiled)
+// true (and cleared) when a prefill GEMM operand exceeded fp16's range since the last call
+bool prefill_overflow_take(fq_ctx* ctx);
 void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev, int T, int64_t d, float* x);
 void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16, int act_dtype);
 void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,

@@ -1,21 +1,22 @@
 // Prefill / calibration contraction on the 5th-generation tensor cores (tcgen05 + TMEM):
-//   Y[T, N] (fp32) = X[T, K] (bf16) . dequant(W_rung[N, K])^T
+//   Y[T, N] (fp32) = X[T, K] (fp16 operands) . dequant(W_rung[N, K])^T
 // straight from the tiled W8 / W4 copy the decode GEMV streams (fq_internal.cuh), so prefill and
 // calibration use the same resident weights.  This is the dense contraction of BASELINE config 4:
 // MultiPrecisionLayer::forward on many rows at once (/root/reference/proj/src/model.cpp:77-98 =
 // dequantize src/quantizer.cpp:205-219 + linear src/tensor.cpp:83-101).
 //
 // Numerics (the decode GEMV's contract): the tensor cores see the EXACT integer codes q - z (|q - z|
-// <= 255, exact in bf16) and the bf16 activations; each 128-code k-block is one quantization group,
+// <= 255, exact in fp16) and the activations (bf16-rounded values stored as fp16, exact in fp16's
+// normal range; the producers flag anything past 65504); each 128-code k-block is one quantization group,
 // accumulated alone in fp32 in tensor memory, and the group's fp32 scale is applied in the
 // epilogue: y = sum_kb s[n, kb] * (sum_{k in kb} (q - z) x).  No weight is ever rounded.
 //
-// One CTA = 128 weight rows (UMMA M) x 128 tokens (UMMA N), warp-specialised, 10 warps:
+// One CTA = 128 weight rows (UMMA M) x 128 tokens (UMMA N), warp-specialised, 12 warps:
 //   warp 0     producer: per k-block one 1-D bulk copy (cp.async.bulk) of the 32 KB activation
 //              tile (X is stored pre-tiled in the UMMA canonical K-major layout, see
 //              tiled_act_offset) and eight bulk copies of the CTA's raw 16x128 weight blocks
 //              into a 3-deep ring, completion by mbarrier transaction bytes;
-//   warps 6-9  dequantisers: raw codes -> bf16 (q - z) into a 2-deep A-operand ring (canonical
+//   warps 6-11 dequantisers: raw codes -> fp16 (q - z) into a 2-deep A-operand ring (canonical
 //              K-major, no swizzle), fence.proxy.async, one arrival per k-block;
 //   warp 1     MMA issuer (one thread): 8 x tcgen05.mma (M128 N128 K16) per k-block into one of
 //              two TMEM accumulators, tcgen05.commit releases the A / input slots and hands the
@@ -34,7 +35,8 @@ constexpr int kTK = 128;                      // codes per k-block (one tiled bl
 constexpr int kTileBytes = kTM * kTK * 2;     // bf16 128 x 128 tile: 32 KB (A and B alike)
 constexpr int kInStages = 3;                  // activation + raw-weight ring
 constexpr int kAStages = 2;                   // dequantised A ring
-constexpr int kGemmThreads = 320;             // 10 warps
+constexpr int kGemmThreads = 384;             // 12 warps (3 per SM sub-partition: 168 registers each)
+constexpr int kDequantThreads = 192;          // warps 6..11
 constexpr int kRawBytes = 8 * kBlockBytes8;   // 8 raw 16x128 blocks (W8 size; W4 uses half)
 constexpr int kSmemGemm = kInStages * (kTileBytes + kRawBytes) + kAStages * kTileBytes + 1024;
 
@@ -106,77 +108,77 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                : "memory");
 }
 
-// exact (q - z) of two codes as a bf16 / fp16 pair (low half = first code): 2^23 + q - (2^23 + z);
-// |q - z| <= 255 is exact in both formats
-template <int F16>
-__device__ __forceinline__ uint32_t qz_pair(uint32_t qa, uint32_t qb, float zf) {
-  const float a = __uint_as_float(0x4B000000u | qa) - zf, b = __uint_as_float(0x4B000000u | qb) - zf;
-  if constexpr (F16) {
-    const __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<const uint32_t*>(&h);
-  } else {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<const uint32_t*>(&h);
-  }
-}
-
-// Dequantiser threads (128): raw 16x128 blocks of the stage -> bf16 (q - z) A tile.  The raw
+// Dequantiser threads (128): raw 16x128 blocks of the stage -> fp16 (q - z) A tile.  The raw
 // block is in mma.sync A-fragment order (fq_internal.cuh); thread d always converts word
 // (i, t) = (d >> 5, d & 31) of its blocks (W8) / word (d >> 5 & 1, d & 31) of block pairs (W4).
-template <int W, int F16>
+// Codes become fp16 1024 + q by a byte permute (W8) or one LOP3 (W4: the nibble pair of a
+// register lands in bits 0-3 / 16-19), and one HSUB2 of {1024 + z, 1024 + z} leaves the exact
+// integer q - z (|q - z| <= 255).
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ uint32_t nib_pair(uint32_t v) {  // (v & 0x000F000F) | 0x64006400
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t zpair(const uint8_t* zp8, int r, int32_t zbase) {
+  const uint32_t z = 1024u + static_cast<uint32_t>(static_cast<int32_t>(zp8[r]) + zbase);
+  const __half h = __uint2half_rn(z);
+  const uint32_t u = *reinterpret_cast<const uint16_t*>(&h);
+  return u | (u << 16);
+}
+
+template <int W>
 __device__ __forceinline__ void dequant_stage(const uint8_t* raw, int32_t zbase, uint8_t* a_tile, int d) {
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
-  if constexpr (W == 0) {
-    const int i = d >> 5, t = d & 31;
-    const int r = t >> 2, c2 = 2 * (t & 3);
+  constexpr int words = W == 0 ? 4 : 2;  // 16-byte code words per lane per block
+  constexpr int units = 8 * words * 32;  // (block, word, lane) units of the stage
 #pragma unroll 2
-    for (int rt = 0; rt < 8; ++rt) {
-      const uint8_t* blk = raw + rt * bb;
-      const uint4 w = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
-      const float z0 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r]) + zbase);
-      const float z1 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r + 8]) + zbase);
-      const uint32_t q4[4] = {w.x, w.y, w.z, w.w};
-      const int row = rt * 16 + r;
+  for (int u = d; u < units; u += kDequantThreads) {
+    const int rt = u / (words * 32), rem = u - rt * (words * 32);
+    const int i = rem >> 5, t = rem & 31;
+    const int r = t >> 2, c2 = 2 * (t & 3);
+    const uint8_t* blk = raw + rt * bb;
+    const uint4 w = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
+    const uint32_t z0 = zpair(blk + cbytes + 64, r, zbase), z1 = zpair(blk + cbytes + 64, r + 8, zbase);
+    const uint32_t q4[4] = {w.x, w.y, w.z, w.w};
+    const int row = rt * 16 + r;
+    if constexpr (W == 0) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {  // codes (r, k0), (r, k0+1), (r+8, k0), (r+8, k0+1)
+        for (int e = 0; e < 2; ++e) {  // bytes (r, k0), (r, k0+1), (r+8, k0), (r+8, k0+1)
           const int k0 = 16 * (2 * i + h) + c2 + 8 * e;
           const uint32_t q = q4[2 * h + e];
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = qz_pair<F16>(q & 0xFFu, (q >> 8) & 0xFFu, z0);
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = qz_pair<F16>((q >> 16) & 0xFFu, q >> 24, z1);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = hsub2(prmt(q, 0x64646464u, 0x4140u), z0);
+          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = hsub2(prmt(q, 0x64646464u, 0x4342u), z1);
         }
       }
-    }
-  } else {
-    const int i = (d >> 5) & 1, t = d & 31;
-    const int r = t >> 2, c2 = 2 * (t & 3);
-#pragma unroll 2
-    for (int u = 0; u < 4; ++u) {
-      const int rt = 2 * u + (d >> 6);
-      const uint8_t* blk = raw + rt * bb;
-      const uint4 w = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
-      const float z0 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r]) + zbase);
-      const float z1 = 8388608.f + static_cast<float>(static_cast<int32_t>(blk[cbytes + 64 + r + 8]) + zbase);
-      const uint32_t q4[4] = {w.x, w.y, w.z, w.w};
-      const int row = rt * 16 + r;
+    } else {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
         const int k0 = 16 * (4 * i + v) + c2;
         const uint32_t q = q4[v];
-        auto nb = [&](int n) { return (q >> (4 * n)) & 0xFu; };
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = qz_pair<F16>(nb(0), nb(4), z0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = qz_pair<F16>(nb(1), nb(5), z0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = qz_pair<F16>(nb(2), nb(6), z1);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = qz_pair<F16>(nb(3), nb(7), z1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = hsub2(nib_pair(q), z0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = hsub2(nib_pair(q >> 4), z0);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = hsub2(nib_pair(q >> 8), z1);
+        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = hsub2(nib_pair(q >> 12), z1);
       }
     }
   }
 }
 
-template <int W, int F16>
+template <int W>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_ws_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb, int32_t zbase, int64_t N,
                    const uint8_t* __restrict__ xt, int T, float* __restrict__ y, int64_t y_stride, int accumulate,
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __shared__ uint64_t in_full[kInStages], in_empty[kInStages], a_full[kAStages], a_empty[kAStages];
   __shared__ uint64_t d_full[2], d_empty[2];
   __shared__ uint32_t tmem_base_s;
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* base = gsm + ((1024u - (smem_addr(gsm) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer
   uint8_t* b_ring = base;                                        // kInStages x 32 KB activations
   uint8_t* raw_ring = b_ring + kInStages * kTileBytes;           // kInStages x 8 raw blocks
   uint8_t* a_ring = raw_ring + kInStages * kRawBytes;            // kAStages x 32 KB bf16 (q - z)
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               "{\n\t.reg .pred p;\n\t"
               "setp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
-              "l"(da), "l"(db), "r"(idesc<F16>()), "r"(acc));
+              "l"(da), "l"(db), "r"(idesc<1>()), "r"(acc));
         }
         tc_commit(&d_full[dbuf]);
         tc_commit(&a_empty[a]);
@@ -271,9 +273,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int s = i % kInStages, a = i % kAStages;
       mbar_wait(&in_full[s], (i / kInStages) & 1, 2);
       if (i >= kAStages) mbar_wait(&a_empty[a], ((i / kAStages) - 1) & 1, 2);
-      dequant_stage<W, F16>(raw_ring + s * kRawBytes, zbase, a_ring + a * kTileBytes, d);
+      dequant_stage<W>(raw_ring + s * kRawBytes, zbase, a_ring + a * kTileBytes, d);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads) : "memory");
       if (d == 0) {
         mbar_arrive(&a_full[a]);
         mbar_arrive(&in_empty[s]);
@@ -299,19 +301,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(dbuf * kTN);
 #pragma unroll
-      for (int c0 = 0; c0 < kTN; c0 += 32) {
-        uint32_t v[32];
+      for (int c0 = 0; c0 < kTN; c0 += 16) {
+        uint32_t v[16];
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr + static_cast<uint32_t>(c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int e = 0; e < 32; ++e) acc[c0 + e] = fmaf(s_kb, __uint_as_float(v[e]), acc[c0 + e]);
+        for (int e = 0; e < 16; ++e) acc[c0 + e] = fmaf(s_kb, __uint_as_float(v[e]), acc[c0 + e]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -371,11 +371,11 @@ __global__ void tile_acts_kernel(const void* __restrict__ x, int dtype, int64_t 
   }
 }
 
-template <int W, int F16>
+template <int W>
 void configure_gemm() {
   static bool done = false;
   if (!done) {
-    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<W, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemGemm));
+    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemGemm));
     done = true;
   }
 }
@@ -400,7 +400,7 @@ void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride,
 void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
                     int64_t y_stride, bool accumulate) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
-  if (x_dtype != FQ_DT_BF16 && x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: activations must be bf16 or fp16");
+  if (x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: the tiled activations are fp16 (bf16 values stored exactly)");
   const fq_rung_store& st = L->store(rung);
   if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
   if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
@@ -437,22 +437,17 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
   const int acc = splits > 1 ? 0 : (accumulate ? 1 : 0);
   const auto* xb = static_cast<const uint8_t*>(xt);
-#define FQ_GEMM_LAUNCH(Wv, Fv)                                                                                   \
-  do {                                                                                                           \
-    configure_gemm<Wv, Fv>();                                                                                    \
-    gemm_ws_kernel<Wv, Fv><<<grid, kGemmThreads, kSmemGemm, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, \
-                                                                         xb, static_cast<int>(T), out, out_stride,  \
-                                                                         acc, splits, split_stride);                \
-  } while (0)
-  const bool f16 = x_dtype == FQ_DT_F16;
   if (rung == FQ_RUNG_INT8) {
-    if (f16) FQ_GEMM_LAUNCH(0, 1);
-    else FQ_GEMM_LAUNCH(0, 0);
+    configure_gemm<0>();
+    gemm_ws_kernel<0><<<grid, kGemmThreads, kSmemGemm, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,
+                                                                     static_cast<int>(T), out, out_stride, acc, splits,
+                                                                     split_stride);
   } else {
-    if (f16) FQ_GEMM_LAUNCH(1, 1);
-    else FQ_GEMM_LAUNCH(1, 0);
+    configure_gemm<1>();
+    gemm_ws_kernel<1><<<grid, kGemmThreads, kSmemGemm, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,
+                                                                     static_cast<int>(T), out, out_stride, acc, splits,
+                                                                     split_stride);
   }
-#undef FQ_GEMM_LAUNCH
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
   if (splits > 1) {

@@ -940,7 +940,7 @@ void prefill_gemm_enqueue(fq_model* M, int slot, const int32_t* tokens_host, int
   const int H = static_cast<int>(c.n_heads), hd = static_cast<int>(c.head_dim);
   const int Ti = static_cast<int>(T);
   const uint8_t* r = &M->rungs[static_cast<size_t>(slot) * M->n_lin];
-  const int ad = c.act_dtype;  // bf16 or fp16: the GEMM operands and roundings follow it
+  const int ad = c.act_dtype;  // bf16 or fp16 roundings; the GEMM operands are stored fp16 (exact)
   FQ_CUDA(cudaMemcpyAsync(w.tok, tokens_host, sizeof(int32_t) * T, cudaMemcpyHostToDevice, st));
   prefill_embed(ctx, M->tok_emb, w.tok, Ti, d, w.x);
   __half* kv_slot = static_cast<__half*>(M->kv) + static_cast<int64_t>(slot) * M->slot_stride;
@@ -948,22 +948,22 @@ void prefill_gemm_enqueue(fq_model* M, int slot, const int32_t* tokens_host, int
     const int b = M->lin_index(l, 0);
     __half* kvl = kv_slot + static_cast<int64_t>(l) * M->layer_stride;
     prefill_rmsnorm(ctx, w.x, Ti, d, M->n1g[l], c.norm_eps, w.h, ad);
-    launch_gemm_dq(ctx, M->lin[b + 0], r[b + 0], T, w.h, ad, w.q, d);
-    launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, ad, w.k, d);
-    launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, ad, w.v, d);
+    launch_gemm_dq(ctx, M->lin[b + 0], r[b + 0], T, w.h, FQ_DT_F16, w.q, d);
+    launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, FQ_DT_F16, w.k, d);
+    launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, FQ_DT_F16, w.v, d);
     prefill_rope_kv(ctx, w.q, w.k, w.v, Ti, H, hd, M->rope_cs, w.qr, kvl, c.max_seq_len, ad);
     prefill_attention(ctx, w.qr, kvl, H, hd, c.max_seq_len, Ti, w.a, ad);
-    launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, ad, w.x, d, true);  // x += attn . Wo^T
+    launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, FQ_DT_F16, w.x, d, true);  // x += attn . Wo^T
     prefill_rmsnorm(ctx, w.x, Ti, d, M->n2g[l], c.norm_eps, w.h, ad);
-    launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, ad, w.g, f);
-    launch_gemm_dq(ctx, M->lin[b + 5], r[b + 5], T, w.h, ad, w.u, f);
+    launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, FQ_DT_F16, w.g, f);
+    launch_gemm_dq(ctx, M->lin[b + 5], r[b + 5], T, w.h, FQ_DT_F16, w.u, f);
     prefill_swiglu(ctx, w.g, w.u, T * f, f, w.m, ad);
-    launch_gemm_dq(ctx, M->lin[b + 6], r[b + 6], T, w.m, ad, w.x, d, true);  // x += mid . Wdown^T
+    launch_gemm_dq(ctx, M->lin[b + 6], r[b + 6], T, w.m, FQ_DT_F16, w.x, d, true);  // x += mid . Wdown^T
   }
   prefill_rmsnorm(ctx, w.x, Ti, d, M->fng, c.norm_eps, w.h, ad);
   float* lg = logits_out ? logits_out : w.logits;
   const int hi = M->head_index();
-  launch_gemm_dq(ctx, M->lin[hi], r[hi], T, w.h, ad, lg, V);
+  launch_gemm_dq(ctx, M->lin[hi], r[hi], T, w.h, FQ_DT_F16, lg, V);
   if (stats_dev) launch_softmax_stats(ctx, lg, T, V, V, stats_dev);
 }
 
@@ -974,6 +974,8 @@ void prefill_gemm(fq_model* M, int slot, const int32_t* tokens, int64_t T, float
   if (stats_host)
     FQ_CUDA(cudaMemcpyAsync(stats_host, M->pw.stats, sizeof(fq_row_stats) * T, cudaMemcpyDeviceToHost, M->ctx->stream));
   FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+  if (prefill_overflow_take(M->ctx))
+    fail(FQ_E_INPUT, "prefill: an activation exceeds fp16's range (the tcgen05 GEMM operand format)");
   M->slot_len[slot] = T;
 }
 

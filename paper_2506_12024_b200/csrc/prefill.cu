@@ -12,15 +12,15 @@ namespace {
 __device__ __forceinline__ float actr(float v, int f16) {
   return f16 ? __half2float(__float2half_rn(v)) : __bfloat162float(__float2bfloat16_rn(v));
 }
-// GEMM operand: the activation rounded to the activation dtype, its 16-bit pattern stored in the
-// tiled layout (tiled_act_offset)
+// GEMM operand: the activation rounded to the activation dtype (the contract), stored as fp16 in
+// the tiled layout (tiled_act_offset): exact for bf16 values in fp16's normal range; a value past
+// 65504 would not be, so it raises the overflow flag the host checks after the prefill.
+__device__ unsigned int g_act_overflow;
 __device__ __forceinline__ uint16_t actb(float v, int f16) {
-  if (f16) {
-    const __half h = __float2half_rn(v);
-    return *reinterpret_cast<const uint16_t*>(&h);
-  }
-  const __nv_bfloat16 b = __float2bfloat16_rn(v);
-  return *reinterpret_cast<const uint16_t*>(&b);
+  const float r = actr(v, f16);
+  if (fabsf(r) > 65504.f) atomicOr(&g_act_overflow, 1u);
+  const __half h = __float2half_rn(r);
+  return *reinterpret_cast<const uint16_t*>(&h);
 }
 
 __global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32_t* __restrict__ tokens, int64_t d,
@@ -127,6 +127,17 @@ __global__ void swiglu_rows_kernel(const float* __restrict__ g, const float* __r
 int elem_grid(const fq_ctx* ctx, int64_t n) { return static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, (n + 255) / 256)); }
 
 }  // namespace
+
+bool prefill_overflow_take(fq_ctx* ctx) {
+  unsigned int h = 0;
+  FQ_CUDA(cudaMemcpyFromSymbolAsync(&h, g_act_overflow, sizeof(h), 0, cudaMemcpyDeviceToHost, ctx->stream));
+  FQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h) {
+    const unsigned int zero = 0;
+    FQ_CUDA(cudaMemcpyToSymbolAsync(g_act_overflow, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return h != 0;
+}
 
 void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev, int T, int64_t d, float* x) {
   embed_rows_kernel<<<T, 256, 0, ctx->stream>>>(tok_emb, tokens_dev, d, x);

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     txt = open(os.path.join(ROOT, "include", "fq_cuda.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:fq_status|const char\*|int32_t)\s+(fq_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:fq_status|const char\*|int32_t|int64_t)\s+(fq_\w+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -33,14 +33,17 @@ for K, N in shapes:
         for T in [int(t) for t in a.T.split(",")]:
             x = torch.randn(T, K, device="cuda").to(torch.bfloat16)
             y = torch.empty(T, N, device="cuda")
+            # the prefill's own operand format: activations pre-tiled once (fq_tile_activations)
+            xt = torch.zeros(ctx.tiled_activation_bytes(T, K), dtype=torch.uint8, device="cuda")
             with torch.cuda.stream(stream):
+                ctx.tile_activations(x, capi.DT_BF16, T, K, capi.DT_F16, xt)
                 for _ in range(2):
-                    ctx.gemm(L, rung, T, x, y)
+                    ctx.gemm_tiled(L, rung, T, xt, capi.DT_F16, y)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 for _ in range(a.iters):
-                    ctx.gemm(L, rung, T, x, y)
+                    ctx.gemm_tiled(L, rung, T, xt, capi.DT_F16, y)
                 e1.record(stream)
                 e1.synchronize()
             ms = e0.elapsed_time(e1) / a.iters
