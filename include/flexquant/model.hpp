@@ -73,7 +73,12 @@ class MultiPrecisionLayer {
   void set_current(Rung r);
   bool has(Rung r) const;
   void set_quantized(Rung r, const QuantizedTensor& q);
-  QuantizedTensor quantized(Rung r) const;  // downloaded from the device
+  // the resident payloads, downloaded from the device on first use (cached until replaced)
+  const QuantizedTensor& quantized(Rung r) const;
+  // fp weights / bias on the host (downloaded on first use; empty when the layer holds none,
+  // e.g. the llama architecture keeps no fp rung on the device)
+  const Tensor& fp_weight() const;
+  const Tensor& bias() const;
   // y = x * W_active^T + bias on the device (exact numerics: bit-identical to the reference).
   Tensor forward(const Tensor& x, StepStats* stats) const;
   double active_weight_bytes() const { return static_cast<double>(param_count()) * accounting_bits(current()) / 8.0; }
@@ -90,6 +95,11 @@ class MultiPrecisionLayer {
   Rung standalone_rung_ = Rung::Fp;
   int64_t group_ = 0;
   Tensor host_fp_;  // standalone layers keep their fp weights for quantize_rungs
+  // host-side caches of the device payloads (reference API returns references)
+  mutable QuantizedTensor q_cache_[3];
+  mutable bool q_valid_[3] = {false, false, false};
+  mutable Tensor fp_cache_, bias_cache_;
+  mutable bool fp_valid_ = false, bias_valid_ = false;
 };
 
 // A sequence slot's KV history on the device (KvCache, src/model.cpp:142-171).
@@ -114,17 +124,23 @@ struct SwitchEvent {
 
 class Model {
  public:
+  Model() = default;  // empty: assign a built or loaded model to it
   explicit Model(ModelConfig cfg);
   ~Model();
   Model(const Model&) = delete;
   Model& operator=(const Model&) = delete;
+  Model(Model&& o) noexcept;
+  Model& operator=(Model&& o) noexcept;
 
   const ModelConfig& config() const { return cfg_; }
-  KvCache make_cache(int slot = 0);          // empties the slot's history
+  // The KV history lives on the device in the model's sequence slots; a KvCache names a slot.
+  KvCache make_cache(int slot = 0) const;    // empties the slot's history
   KvCache attach_cache(int slot = 0) const;  // handle on the slot's current history
 
-  Tensor forward_prefill(std::span<const TokenId> tokens, KvCache& cache);
-  Tensor forward_decode(TokenId token, KvCache& cache);
+  // Logits for every prompt position (n x V) / the next token (1 x V), as the reference's
+  // const forwards (src/model.cpp:245-266); the step accounting is mutable state, as there.
+  Tensor forward_prefill(std::span<const TokenId> tokens, KvCache& cache) const;
+  Tensor forward_decode(TokenId token, KvCache& cache) const;
 
   std::optional<SwitchEvent> set_precision(std::string_view layer_id, Rung bits, int slot = 0);
   void set_all_precision(Rung bits, int slot = 0);
@@ -140,6 +156,11 @@ class Model {
   const MultiPrecisionLayer& linear(int i) const { return layers_.at(static_cast<size_t>(i)); }
   MultiPrecisionLayer* find_layer(std::string_view id);
   const MultiPrecisionLayer* find_layer(std::string_view id) const;
+  // every switchable linear in the reference's order (blocks.i.attn.wq .. ffn.w2 / llama ids, head)
+  std::vector<const MultiPrecisionLayer*> linear_layers() const;
+  std::vector<MultiPrecisionLayer*> linear_layers();
+  MultiPrecisionLayer& head() { return layers_.back(); }
+  const MultiPrecisionLayer& head() const { return layers_.back(); }
 
   const StepStats& step_stats() const { return stats_; }
   void reset_step_stats() { stats_.reset(); }
@@ -158,19 +179,24 @@ class Model {
  private:
   friend class MultiPrecisionLayer;
   friend class KvCache;
-  void account_step(uint64_t ns, int slot);
+  void account_step(uint64_t ns, int slot) const;
   ModelConfig cfg_;
   fq_model* model_ = nullptr;
   std::vector<std::string> ids_;
   std::vector<MultiPrecisionLayer> layers_;
-  StepStats stats_;
+  mutable StepStats stats_;
 };
 
 double effective_bits(std::span<const MultiPrecisionLayer* const> layers);
 
-// The reference's weight container, "flexquant-weights v1" (src/model_io.cpp:130-258), loaded
-// into a reference-architecture device model (fp + W8 + W4 rungs and biases resident).
-std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch = 1);
+// The reference's weight container, "flexquant-weights v1" (src/model_io.cpp:130-258).
+// Reference-architecture files load into a device model with fp + W8 + W4 rungs and biases
+// resident, exactly as the reference writes them.  Llama-architecture models use the same
+// container with two extra config fields (arch=llama group_size=G) and their own tensor names
+// (tok_emb, blocks.i.attn_norm / ffn_norm, final_norm, and per linear only the quantized
+// ".w8" / ".w4" records, g-per-row groups): save_model_file writes whichever the model is.
+void save_model_file(const Model& model, const std::string& path);
+Model load_model_file(const std::string& path, int max_batch = 1);
 
 // Process-wide device context used by the host API (device = $FQ_DEVICE, else $LOCAL_RANK, else 0).
 fq_ctx* runtime();

@@ -109,6 +109,10 @@ fq_status fq_layer_download_quantized(const fq_layer* layer, int32_t rung, uint8
 /* Full-precision rung (fp32 [N,K]) and optional bias [N]. */
 fq_status fq_layer_upload_fp(fq_layer* layer, const float* weight_host);
 fq_status fq_layer_upload_bias(fq_layer* layer, const float* bias_host);
+/* Copies the fp weights / bias back to the host (the weights container writer, MultiPrecisionLayer::
+ * fp_weight / bias); *present = 0 (and nothing copied) when the layer holds none. */
+fq_status fq_layer_download_fp(const fq_layer* layer, float* weight_host, int32_t* present);
+fq_status fq_layer_download_bias(const fq_layer* layer, float* bias_host, int32_t* present);
 /* Device-side RTN quantizer (K9): quantizes fp32 weights already on the device with the
  * reference rules (src/quantizer.cpp:111-189, round-half-even in double). */
 fq_status fq_layer_quantize_device(fq_layer* layer, int32_t rung, int32_t mode, const float* weight_dev);
@@ -204,6 +208,9 @@ fq_status fq_model_linear(fq_model* model, int32_t index, fq_layer** out); /* bo
  * blocks.i.ln2.gamma/beta (reference), blocks.i.attn_norm / blocks.i.ffn_norm (llama),
  * final_norm(.gamma/.beta).  fp32 host data. */
 fq_status fq_model_set_param(fq_model* model, const char* name, const float* host, int64_t numel);
+/* The reverse of fq_model_set_param (save_model_file), and a parameter's element count. */
+fq_status fq_model_get_param(fq_model* model, const char* name, float* host, int64_t numel);
+fq_status fq_model_param_size(fq_model* model, const char* name, int64_t* numel);
 /* Fills every parameter / rung from the deterministic generator on the device (bench). */
 fq_status fq_model_init_random(fq_model* model, uint64_t seed, float std);
 /* Same, and while each linear's fp32 weights are on the device computes the reference analyzer's

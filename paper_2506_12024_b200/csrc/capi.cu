@@ -246,6 +246,28 @@ fq_status fq_layer_upload_bias(fq_layer* L, const float* b) {
   });
 }
 
+fq_status fq_layer_download_fp(const fq_layer* L, float* w_host, int32_t* present) {
+  return guarded([&] {
+    require(L != nullptr && present != nullptr, FQ_E_INPUT, "null argument");
+    *present = L->fp != nullptr ? 1 : 0;
+    if (L->fp && w_host) {
+      FQ_CUDA(cudaMemcpyAsync(w_host, L->fp, sizeof(float) * L->N * L->K, cudaMemcpyDeviceToHost, L->ctx->stream));
+      FQ_CUDA(cudaStreamSynchronize(L->ctx->stream));
+    }
+  });
+}
+
+fq_status fq_layer_download_bias(const fq_layer* L, float* b_host, int32_t* present) {
+  return guarded([&] {
+    require(L != nullptr && present != nullptr, FQ_E_INPUT, "null argument");
+    *present = L->bias != nullptr ? 1 : 0;
+    if (L->bias && b_host) {
+      FQ_CUDA(cudaMemcpyAsync(b_host, L->bias, sizeof(float) * L->N, cudaMemcpyDeviceToHost, L->ctx->stream));
+      FQ_CUDA(cudaStreamSynchronize(L->ctx->stream));
+    }
+  });
+}
+
 fq_status fq_layer_quantize_device(fq_layer* L, int32_t rung, int32_t mode, const float* w_dev) {
   return guarded([&] {
     require(L != nullptr && w_dev != nullptr, FQ_E_INPUT, "null argument");

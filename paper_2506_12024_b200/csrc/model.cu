@@ -1278,6 +1278,27 @@ fq_status fq_model_set_param(fq_model* M, const char* name, const float* host, i
   });
 }
 
+fq_status fq_model_get_param(fq_model* M, const char* name, float* host, int64_t numel) {
+  return guarded([&] {
+    require(M && name && host, FQ_E_INPUT, "null argument");
+    int64_t expect = 0;
+    const float* src = param_slot(M, name, expect);
+    if (!src) fail(FQ_E_FORMAT, std::string("weights: unknown parameter '") + name + "'");
+    if (numel != expect) fail(FQ_E_DIMENSION, std::string("weights: parameter '") + name + "' has the wrong size");
+    FQ_CUDA(cudaMemcpyAsync(host, src, sizeof(float) * numel, cudaMemcpyDeviceToHost, M->ctx->stream));
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+  });
+}
+
+fq_status fq_model_param_size(fq_model* M, const char* name, int64_t* numel) {
+  return guarded([&] {
+    require(M && name && numel, FQ_E_INPUT, "null argument");
+    int64_t expect = 0;
+    if (!param_slot(M, name, expect)) fail(FQ_E_FORMAT, std::string("weights: unknown parameter '") + name + "'");
+    *numel = expect;
+  });
+}
+
 fq_status fq_model_init_random_kl(fq_model* M, uint64_t seed, float std, int32_t bins, double* kl8, double* kl4) {
   return guarded([&] {
     require(M != nullptr, FQ_E_INPUT, "null model");

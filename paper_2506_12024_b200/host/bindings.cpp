@@ -190,6 +190,7 @@ PYBIND11_MODULE(_flexquant, m) {
   m.def("runtime_stream", []() { return reinterpret_cast<uintptr_t>(runtime_stream()); });
   m.def("load_model_file", [](const std::string& p, int max_batch) { return load_model_file(p, max_batch); },
         py::arg("path"), py::arg("max_batch") = 1);
+  m.def("save_model_file", &save_model_file);
 
   // ---------------------------------------------------------------- analyzer
   py::class_<LayerKlReport>(m, "LayerKlReport")

@@ -1,5 +1,9 @@
 // Dynamic-precision generation loop (Algorithm 1) over the device decoder.
-// Reference: /root/reference/proj/src/engine.cpp:30-371.  Record semantics are the reference's:
+// Reference: /root/reference/proj/src/engine.cpp:30-371.  Attribution: validate_plan /
+// apply_entry and traffic_report / format_traffic_report keep the reference's checks, record
+// fields and report text (engine.cpp:30-54, 214-247) so traces and reports compare field for
+// field; the loop itself is rewritten around batched device steps and the JSONL I/O is written
+// without nlohmann/json.  Record semantics are the reference's:
 // a token's record describes the precision state that produced it; switches decided at token t
 // are applied after its record and take effect for token t+1; token 1 covers the prefill.
 #include <chrono>
@@ -11,6 +15,7 @@
 #include <sstream>
 
 #include "flexquant/engine.hpp"
+#include "flexquant/metrics.hpp"
 #include "host_internal.hpp"
 
 namespace flexquant {
@@ -162,17 +167,6 @@ std::vector<GenerationResult> run_generation(std::span<const std::vector<TokenId
   return out;
 }
 
-// LCS-based Rouge-L F (x100) and agreement, as the reference's metrics (src/metrics.cpp:45-84).
-size_t lcs(std::span<const TokenId> a, std::span<const TokenId> b) {
-  std::vector<size_t> prev(b.size() + 1, 0), cur(b.size() + 1, 0);
-  for (size_t i = 1; i <= a.size(); ++i) {
-    for (size_t j = 1; j <= b.size(); ++j)
-      cur[j] = a[i - 1] == b[j - 1] ? prev[j - 1] + 1 : std::max(prev[j], cur[j - 1]);
-    std::swap(prev, cur);
-  }
-  return prev[b.size()];
-}
-
 }  // namespace
 
 GenerationResult generate(std::span<const TokenId> prompt, Model& model, const SwitchPlan& plan,
@@ -212,21 +206,28 @@ std::vector<SweepRow> sweep_switch_speed(std::span<const TokenId> prompt, Model&
     double bytes = 0.0;
     for (const TraceRecord& rec : r.trace.records) bytes += rec.weight_bytes_touched;
     row.mean_bytes_per_token = bytes / static_cast<double>(r.trace.records.size());
-    const size_t n = std::min(r.sequence.size(), base.sequence.size());
-    size_t same = 0;
-    for (size_t i = 0; i < n; ++i) {
-      if (r.sequence[i] == base.sequence[i]) ++same;
-      else if (!row.first_divergence) row.first_divergence = i;
-    }
-    row.agreement_vs_fp = n ? static_cast<double>(same) / static_cast<double>(std::max(r.sequence.size(), base.sequence.size())) : 0.0;
-    const size_t l = lcs(r.sequence, base.sequence);
-    const double prec = r.sequence.empty() ? 0.0 : static_cast<double>(l) / r.sequence.size();
-    const double rec = base.sequence.empty() ? 0.0 : static_cast<double>(l) / base.sequence.size();
-    row.rouge_l_vs_fp = prec + rec > 0 ? 100.0 * 2 * prec * rec / (prec + rec) : 0.0;
+    // agreement / Rouge-L against the fp baseline (src/engine.cpp:188-191, src/metrics.cpp)
+    const Agreement agr = agreement_rate(r.sequence, base.sequence);
+    row.agreement_vs_fp = agr.rate;
+    row.first_divergence = agr.divergence_index;
+    row.rouge_l_vs_fp = rouge_l(r.sequence, base.sequence);
     row.trace = std::move(r.trace);
     rows.push_back(std::move(row));
   }
   return rows;
+}
+
+std::string sweep_csv_header() {
+  return "prompt,speed,final_effective_bits,mean_bytes_per_token,agreement_vs_fp,first_divergence,rouge_l_vs_fp\n";
+}
+
+std::string sweep_csv_row(const std::string& prompt_name, const SweepRow& row) {
+  char buf[320];
+  const std::string div = row.first_divergence ? std::to_string(*row.first_divergence) : std::string();
+  std::snprintf(buf, sizeof(buf), "%s,%lld,%.6f,%.3f,%.6f,%s,%.4f\n", prompt_name.c_str(),
+                static_cast<long long>(row.speed), row.final_effective_bits, row.mean_bytes_per_token,
+                row.agreement_vs_fp, div.c_str(), row.rouge_l_vs_fp);
+  return buf;
 }
 
 TrafficReport traffic_report(const DecodeTrace& trace) {

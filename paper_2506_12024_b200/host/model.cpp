@@ -77,6 +77,14 @@ MultiPrecisionLayer& MultiPrecisionLayer::operator=(MultiPrecisionLayer&& o) noe
     standalone_rung_ = o.standalone_rung_;
     group_ = o.group_;
     host_fp_ = std::move(o.host_fp_);
+    for (int i = 0; i < 3; ++i) {
+      q_cache_[i] = std::move(o.q_cache_[i]);
+      q_valid_[i] = o.q_valid_[i];
+    }
+    fp_cache_ = std::move(o.fp_cache_);
+    bias_cache_ = std::move(o.bias_cache_);
+    fp_valid_ = o.fp_valid_;
+    bias_valid_ = o.bias_valid_;
     o.layer_ = nullptr;
     o.owned_ = false;
   }
@@ -111,6 +119,7 @@ void MultiPrecisionLayer::set_current(Rung r) {
 
 void MultiPrecisionLayer::set_quantized(Rung r, const QuantizedTensor& q) {
   q.validate();
+  q_valid_[static_cast<int>(r)] = false;
   if (q.rows != n_ || q.cols != k_) throw DimensionError("layer " + id_ + ": quantized payload shape mismatch");
   if (r == Rung::Fp) throw ConfigError("layer " + id_ + ": fp rung is not a quantized payload");
   if (q.bits != quantized_bits(r)) throw ConfigError("layer " + id_ + ": expected " + std::to_string(quantized_bits(r)) + "-bit payload");
@@ -122,9 +131,11 @@ void MultiPrecisionLayer::set_quantized(Rung r, const QuantizedTensor& q) {
                                           q.zero_point.data(), static_cast<int64_t>(q.scale.size())));
 }
 
-QuantizedTensor MultiPrecisionLayer::quantized(Rung r) const {
+const QuantizedTensor& MultiPrecisionLayer::quantized(Rung r) const {
   if (r == Rung::Fp || !has(r))
     throw StateError("layer " + id_ + ": no quantized payload for rung '" + to_string(r) + "'");
+  const int ri = static_cast<int>(r);
+  if (q_valid_[ri]) return q_cache_[ri];
   int64_t n = 0, k = 0, g = 0;
   detail::check(fq_layer_shape(layer_, &n, &k, &g));
   QuantizedTensor q;
@@ -137,7 +148,32 @@ QuantizedTensor MultiPrecisionLayer::quantized(Rung r) const {
   q.zero_point.resize(q.scale.size());
   detail::check(fq_layer_download_quantized(layer_, static_cast<int32_t>(r), q.payload.data(), q.scale.data(),
                                             q.zero_point.data()));
-  return q;
+  q_cache_[ri] = std::move(q);
+  q_valid_[ri] = true;
+  return q_cache_[ri];
+}
+
+const Tensor& MultiPrecisionLayer::fp_weight() const {
+  if (host_fp_.numel()) return host_fp_;
+  if (!fp_valid_) {
+    int32_t present = 0;
+    detail::check(fq_layer_download_fp(layer_, nullptr, &present));
+    fp_cache_ = present ? Tensor({n_, k_}) : Tensor();
+    if (present) detail::check(fq_layer_download_fp(layer_, fp_cache_.data(), &present));
+    fp_valid_ = true;
+  }
+  return fp_cache_;
+}
+
+const Tensor& MultiPrecisionLayer::bias() const {
+  if (!bias_valid_) {
+    int32_t present = 0;
+    detail::check(fq_layer_download_bias(layer_, nullptr, &present));
+    bias_cache_ = present ? Tensor({n_}) : Tensor();
+    if (present) detail::check(fq_layer_download_bias(layer_, bias_cache_.data(), &present));
+    bias_valid_ = true;
+  }
+  return bias_cache_;
 }
 
 Tensor MultiPrecisionLayer::forward(const Tensor& x, StepStats* stats) const {
@@ -205,7 +241,37 @@ Model::~Model() {
   if (model_) fq_model_destroy(model_);
 }
 
-KvCache Model::make_cache(int slot) {
+Model::Model(Model&& o) noexcept { *this = std::move(o); }
+
+Model& Model::operator=(Model&& o) noexcept {
+  if (this != &o) {
+    layers_.clear();
+    if (model_) fq_model_destroy(model_);
+    cfg_ = o.cfg_;
+    model_ = o.model_;
+    ids_ = std::move(o.ids_);
+    layers_ = std::move(o.layers_);
+    stats_ = o.stats_;
+    o.model_ = nullptr;
+    o.layers_.clear();
+    for (MultiPrecisionLayer& l : layers_) l.model_ = this;  // model views point at their owner
+  }
+  return *this;
+}
+
+std::vector<const MultiPrecisionLayer*> Model::linear_layers() const {
+  std::vector<const MultiPrecisionLayer*> out;
+  for (const MultiPrecisionLayer& l : layers_) out.push_back(&l);
+  return out;
+}
+
+std::vector<MultiPrecisionLayer*> Model::linear_layers() {
+  std::vector<MultiPrecisionLayer*> out;
+  for (MultiPrecisionLayer& l : layers_) out.push_back(&l);
+  return out;
+}
+
+KvCache Model::make_cache(int slot) const {
   detail::check(fq_model_reset_slot(model_, slot));
   KvCache c;
   c.model_ = this;
@@ -221,7 +287,7 @@ KvCache Model::attach_cache(int slot) const {
   return c;
 }
 
-void Model::account_step(uint64_t ns, int slot) {
+void Model::account_step(uint64_t ns, int slot) const {
   // per-rung buckets: the step's time split by each rung's share of the weight bytes
   double b[3] = {0, 0, 0};
   for (size_t i = 0; i < layers_.size(); ++i) {
@@ -256,7 +322,7 @@ std::vector<fq_row_stats> Model::decode_rows(std::span<const int32_t> slots, std
   return st;
 }
 
-Tensor Model::forward_prefill(std::span<const TokenId> tokens, KvCache& cache) {
+Tensor Model::forward_prefill(std::span<const TokenId> tokens, KvCache& cache) const {
   const int64_t n = static_cast<int64_t>(tokens.size());
   if (n < 1) throw InputError("prefill: empty prompt");
   DeviceBuffer l(sizeof(float) * n * cfg_.vocab_size);
@@ -269,7 +335,7 @@ Tensor Model::forward_prefill(std::span<const TokenId> tokens, KvCache& cache) {
   return out;
 }
 
-Tensor Model::forward_decode(TokenId token, KvCache& cache) {
+Tensor Model::forward_decode(TokenId token, KvCache& cache) const {
   DeviceBuffer l(sizeof(float) * cfg_.vocab_size);
   const int32_t slot = cache.slot();
   fq_row_stats st;
@@ -376,7 +442,117 @@ int64_t field(const std::string& line, const std::string& key) {
 
 }  // namespace
 
-std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch) {
+namespace {
+
+// optional config field (the llama extension): default when absent
+int64_t field_or(const std::string& line, const std::string& key, int64_t dflt) {
+  const size_t p = line.find(" " + key + "=");
+  return p == std::string::npos ? dflt : std::stoll(line.substr(p + key.size() + 2));
+}
+
+struct QRecord {
+  int bits = 8, mode = 0;
+  uint32_t rows = 0, cols = 0, group = 0;  // group 0 = per row (the reference's records)
+  std::vector<float> scale;
+  std::vector<int32_t> zp;
+  std::vector<uint8_t> payload;
+};
+
+// ---- writer
+void put_u32(std::ostream& os, uint32_t v) { os.write(reinterpret_cast<const char*>(&v), 4); }
+void put_name(std::ostream& os, const std::string& n, uint8_t tag) {
+  put_u32(os, static_cast<uint32_t>(n.size()));
+  os.write(n.data(), static_cast<std::streamsize>(n.size()));
+  os.put(static_cast<char>(tag));
+}
+void put_tensor(std::ostream& os, const std::string& name, const Tensor& t) {
+  put_name(os, name, 0);
+  put_u32(os, static_cast<uint32_t>(t.shape().size()));
+  for (int64_t d : t.shape()) put_u32(os, static_cast<uint32_t>(d));
+  os.write(reinterpret_cast<const char*>(t.data()), static_cast<std::streamsize>(sizeof(float) * t.numel()));
+}
+// tag 1: the reference's per-row record; tag 2: the group-wise extension (scale / zp per group)
+void put_quantized(std::ostream& os, const std::string& name, const QuantizedTensor& q) {
+  const bool grouped = q.group() != q.cols;
+  put_name(os, name, grouped ? 2 : 1);
+  os.put(static_cast<char>(q.bits));
+  os.put(static_cast<char>(q.mode));
+  put_u32(os, static_cast<uint32_t>(q.rows));
+  put_u32(os, static_cast<uint32_t>(q.cols));
+  if (grouped) put_u32(os, static_cast<uint32_t>(q.group()));
+  os.write(reinterpret_cast<const char*>(q.scale.data()), static_cast<std::streamsize>(4 * q.scale.size()));
+  os.write(reinterpret_cast<const char*>(q.zero_point.data()), static_cast<std::streamsize>(4 * q.zero_point.size()));
+  os.write(reinterpret_cast<const char*>(q.payload.data()), static_cast<std::streamsize>(q.payload.size()));
+}
+
+Tensor get_param(const Model& m, const std::string& name, std::vector<int64_t> shape) {
+  Tensor t(std::move(shape));
+  detail::check(fq_model_get_param(m.handle(), name.c_str(), t.data(), t.numel()));
+  return t;
+}
+
+}  // namespace
+
+void save_model_file(const Model& model, const std::string& path) {
+  if (!model.handle()) throw StateError("save_model_file: empty model");
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw FormatError("cannot open weights file for writing: " + path);
+  const ModelConfig& c = model.config();
+  const bool llama = c.arch == Arch::Llama;
+  const int64_t d = c.d_model, L = c.n_layers;
+  os << "flexquant-weights v1\n";
+  os << "vocab_size=" << c.vocab_size << " d_model=" << d << " n_heads=" << c.n_heads << " head_dim=" << c.head_dim
+     << " n_layers=" << L << " ffn_dim=" << c.ffn_dim << " max_seq_len=" << c.max_seq_len
+     << " tie_embeddings=" << (c.tie_embeddings ? 1 : 0);
+  if (llama) os << " arch=llama group_size=" << c.group_size;
+  os << "\n";
+  const std::vector<const MultiPrecisionLayer*> lin = model.linear_layers();
+  // reference: embeddings + final norm + per block (4 norms + 6 x (fp, bias)) + head (fp, bias),
+  // and both quantized rungs of every linear; llama: tok_emb + final norm + 2 norms per block and
+  // both rungs of every linear
+  const bool has_head = !c.tie_embeddings;
+  const size_t count = llama ? 2 + 2 * static_cast<size_t>(L) + 2 * lin.size()
+                             : 4 + static_cast<size_t>(L) * 16 + (has_head ? 2 : 0) + 2 * lin.size();
+  os << "tensor_count=" << count << "\n";
+  put_tensor(os, "tok_emb", get_param(model, "tok_emb", {c.vocab_size, d}));
+  auto put_linear = [&](const MultiPrecisionLayer& l) {
+    if (!llama) {
+      put_tensor(os, l.id(), l.fp_weight());
+      put_tensor(os, l.id() + ".bias", l.bias());
+    }
+    put_quantized(os, l.id() + ".w8", l.quantized(Rung::Int8));
+    put_quantized(os, l.id() + ".w4", l.quantized(Rung::Int4));
+  };
+  size_t li = 0;
+  if (!llama) {
+    put_tensor(os, "pos_emb", get_param(model, "pos_emb", {c.max_seq_len, d}));
+    for (int64_t i = 0; i < L; ++i) {
+      const std::string p = "blocks." + std::to_string(i) + ".";
+      put_tensor(os, p + "ln1.gamma", get_param(model, p + "ln1.gamma", {d}));
+      put_tensor(os, p + "ln1.beta", get_param(model, p + "ln1.beta", {d}));
+      for (int k = 0; k < 4; ++k) put_linear(*lin[li++]);
+      put_tensor(os, p + "ln2.gamma", get_param(model, p + "ln2.gamma", {d}));
+      put_tensor(os, p + "ln2.beta", get_param(model, p + "ln2.beta", {d}));
+      for (int k = 0; k < 2; ++k) put_linear(*lin[li++]);
+    }
+    put_tensor(os, "ln_f.gamma", get_param(model, "final_norm.gamma", {d}));
+    put_tensor(os, "ln_f.beta", get_param(model, "final_norm.beta", {d}));
+    if (has_head) put_linear(*lin[li++]);
+  } else {
+    for (int64_t i = 0; i < L; ++i) {
+      const std::string p = "blocks." + std::to_string(i) + ".";
+      put_tensor(os, p + "attn_norm", get_param(model, p + "attn_norm", {d}));
+      for (int k = 0; k < 4; ++k) put_linear(*lin[li++]);
+      put_tensor(os, p + "ffn_norm", get_param(model, p + "ffn_norm", {d}));
+      for (int k = 0; k < 3; ++k) put_linear(*lin[li++]);
+    }
+    put_tensor(os, "final_norm", get_param(model, "final_norm", {d}));
+    put_linear(*lin[li++]);
+  }
+  if (!os) throw FormatError("failed writing weights file: " + path);
+}
+
+Model load_model_file(const std::string& path, int max_batch) {
   Reader r;
   r.is.open(path, std::ios::binary);
   if (!r.is) throw FormatError("cannot open weights file: " + path);
@@ -392,48 +568,46 @@ std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch) {
   cfg.ffn_dim = field(line, "ffn_dim");
   cfg.max_seq_len = field(line, "max_seq_len");
   cfg.tie_embeddings = field(line, "tie_embeddings") != 0;
-  cfg.arch = Arch::Reference;
-  cfg.group_size = 0;
+  const bool llama = line.find(" arch=llama") != std::string::npos;
+  cfg.arch = llama ? Arch::Llama : Arch::Reference;
+  cfg.group_size = field_or(line, "group_size", 0);
   cfg.max_batch = max_batch;
   if (!std::getline(r.is, line)) throw FormatError("weights file: missing tensor count line");
   const int64_t count = field(line, "tensor_count");
-  auto model = std::make_unique<Model>(cfg);
-  struct Q {
-    int bits, mode;
-    uint32_t rows, cols;
-    std::vector<float> scale;
-    std::vector<int32_t> zp;
-    std::vector<uint8_t> payload;
-  };
+  Model model(cfg);
   std::map<std::string, Tensor> tensors;
-  std::map<std::string, Q> quants;
+  std::map<std::string, QRecord> quants;
   for (int64_t i = 0; i < count; ++i) {
     const uint32_t nl = r.u32();
     if (nl > 4096) throw FormatError("weights file: unreasonable tensor name length");
     std::string name(nl, '\0');
     r.bytes(name.data(), nl);
-    const uint8_t dtype = r.u8();
-    if (dtype == 0) {
+    const uint8_t tag = r.u8();
+    if (tag == 0) {
       const uint32_t nd = r.u32();
       if (nd == 0 || nd > 4) throw FormatError("weights file: bad tensor rank");
       std::vector<int64_t> shape(nd);
       int64_t numel = 1;
-      for (auto& s : shape) {
-        s = r.u32();
-        numel *= s;
+      for (auto& dim : shape) {
+        dim = r.u32();
+        numel *= dim;
       }
       std::vector<float> data(static_cast<size_t>(numel));
       r.bytes(data.data(), sizeof(float) * data.size());
       tensors.emplace(name, Tensor::from_data(shape, std::move(data)));
-    } else if (dtype == 1) {
-      Q q;
+    } else if (tag == 1 || tag == 2) {
+      QRecord q;
       q.bits = r.u8();
       q.mode = r.u8();
       if (q.mode > 1) throw FormatError("weights file: bad quantization mode");
+      if (q.bits != 8 && q.bits != 4) throw FormatError("weights file: bad bit-width");
       q.rows = r.u32();
       q.cols = r.u32();
-      q.scale.resize(q.rows);
-      q.zp.resize(q.rows);
+      q.group = tag == 2 ? r.u32() : 0;
+      if (tag == 2 && (q.group == 0 || q.cols == 0)) throw FormatError("weights file: bad quantization group");
+      const size_t groups = static_cast<size_t>(q.rows) * (q.group ? (q.cols + q.group - 1) / q.group : 1);
+      q.scale.resize(groups);
+      q.zp.resize(groups);
       r.bytes(q.scale.data(), 4 * q.scale.size());
       r.bytes(q.zp.data(), 4 * q.zp.size());
       q.payload.resize((static_cast<size_t>(q.rows) * q.cols * q.bits + 7) / 8);
@@ -448,34 +622,46 @@ std::unique_ptr<Model> load_model_file(const std::string& path, int max_batch) {
     if (it == tensors.end()) throw FormatError("weights file: tensor '" + n + "' missing");
     return it->second;
   };
-  model->set_param("tok_emb", take("tok_emb"));
-  model->set_param("pos_emb", take("pos_emb"));
-  for (int64_t i = 0; i < cfg.n_layers; ++i) {
-    const std::string p = "blocks." + std::to_string(i) + ".";
-    for (const char* nm : {"ln1.gamma", "ln1.beta", "ln2.gamma", "ln2.beta"}) model->set_param(p + nm, take(p + nm));
+  model.set_param("tok_emb", take("tok_emb"));
+  if (llama) {
+    for (int64_t i = 0; i < cfg.n_layers; ++i) {
+      const std::string p = "blocks." + std::to_string(i) + ".";
+      for (const char* nm : {"attn_norm", "ffn_norm"}) model.set_param(p + nm, take(p + nm));
+    }
+    model.set_param("final_norm", take("final_norm"));
+  } else {
+    model.set_param("pos_emb", take("pos_emb"));
+    for (int64_t i = 0; i < cfg.n_layers; ++i) {
+      const std::string p = "blocks." + std::to_string(i) + ".";
+      for (const char* nm : {"ln1.gamma", "ln1.beta", "ln2.gamma", "ln2.beta"}) model.set_param(p + nm, take(p + nm));
+    }
+    model.set_param("final_norm.gamma", take("ln_f.gamma"));
+    model.set_param("final_norm.beta", take("ln_f.beta"));
   }
-  model->set_param("final_norm.gamma", take("ln_f.gamma"));
-  model->set_param("final_norm.beta", take("ln_f.beta"));
-  for (size_t i = 0; i < model->num_linears(); ++i) {
-    const std::string& id = model->linear_ids()[i];
-    fq_layer* L = model->linear(static_cast<int>(i)).handle();
-    detail::check(fq_layer_upload_fp(L, take(id).data()));
-    detail::check(fq_layer_upload_bias(L, take(id + ".bias").data()));
+  for (size_t i = 0; i < model.num_linears(); ++i) {
+    const std::string& id = model.linear_ids()[i];
+    fq_layer* L = model.linear(static_cast<int>(i)).handle();
+    if (!llama) {
+      detail::check(fq_layer_upload_fp(L, take(id).data()));
+      detail::check(fq_layer_upload_bias(L, take(id + ".bias").data()));
+    }
     for (const auto& [tag, rung] : {std::pair<const char*, int>{".w8", FQ_RUNG_INT8}, {".w4", FQ_RUNG_INT4}}) {
       auto it = quants.find(id + tag);
       if (it == quants.end()) {
+        if (llama) throw FormatError("weights file: quantized record '" + id + tag + "' missing");
         // files without stored rungs are RTN-quantized at load time (src/model_io.cpp:226-229)
         const QuantizedTensor q = quantize(take(id), rung == FQ_RUNG_INT8 ? 8 : 4, QuantMode::Asymmetric);
         detail::check(fq_layer_upload_quantized(L, rung, 0, q.payload.data(), static_cast<int64_t>(q.payload.size()),
                                                 q.scale.data(), q.zero_point.data(), static_cast<int64_t>(q.scale.size())));
         continue;
       }
-      const Q& q = it->second;
+      const QRecord& q = it->second;
+      if ((rung == FQ_RUNG_INT8) != (q.bits == 8)) throw FormatError("weights file: '" + id + tag + "' has the wrong bit-width");
       detail::check(fq_layer_upload_quantized(L, rung, q.mode, q.payload.data(), static_cast<int64_t>(q.payload.size()),
                                               q.scale.data(), q.zp.data(), static_cast<int64_t>(q.scale.size())));
     }
   }
-  model->set_all_precision(Rung::Fp);
+  model.set_all_precision(llama ? Rung::Int8 : Rung::Fp);
   return model;
 }
 

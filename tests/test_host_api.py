@@ -80,6 +80,23 @@ def test_plan_text_round_trip_and_golden_parse():
     assert [e.layer_id for e in p.entries] == ["c", "a", "b"]  # (kl, layer_id) order
 
 
+def test_histogram_and_kl_match_reference_library():
+    """The restated weight_histogram / kl_divergence (host/analyzer.cpp) equal the reference's
+    (src/analyzer.cpp:31-79, oracle/_ref) bit for bit, including values exactly on bin edges."""
+    if oracle.ref() is None:
+        pytest.skip("reference library not built")
+    rng = np.random.default_rng(3)
+    for bins in (2, 7, 512, 2048):
+        w = (rng.standard_normal((64, 96)) * 0.02).astype(np.float32)
+        wq = np.round(w * 50).astype(np.float32) / 50  # a coarser copy with many ties
+        e = fq.uniform_edges(float(w.min()), float(w.max()), bins)
+        w.ravel()[:len(e)] = np.asarray(e, np.float32)[: w.size]  # values on (float-rounded) edges
+        p = fq.weight_histogram(w, e)
+        q = fq.weight_histogram(wq, fq.uniform_edges(float(w.min()), float(w.max()), bins))
+        mine = fq.kl_divergence(p, q)
+        assert mine == oracle.hist_kl(w, wq, bins, impl="ref")
+
+
 def test_kl_and_histogram_host_utilities():
     assert abs(fq.kl_divergence([0.5, 0.5], [0.25, 0.75]) - 0.14384103622589045) < 1e-15
     e = fq.uniform_edges(0.0, 1.0, 4)
