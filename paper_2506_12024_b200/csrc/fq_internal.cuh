@@ -194,8 +194,11 @@ void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride,
 // tiled bf16 (x_dtype FQ_DT_BF16) or fp16 (FQ_DT_F16) activations above; the tensor cores multiply the exact integer codes (q - z) and the
 // per-group fp32 scale is applied per 128-code k-block in the epilogue (no weight rounding);
 // accumulate: y += instead (the residual add of the O / down projections)
+// row_rung (device, optional): rung of each row at stride rr_stride; only rows at `rung` are
+// written (a batch whose rows decode at different precisions runs one launch per copy)
 void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
-                    int64_t y_stride, bool accumulate = false);
+                    int64_t y_stride, bool accumulate = false, const uint8_t* row_rung = nullptr,
+                    int64_t rr_stride = 0);
 
 // row-parallel prefill kernels (prefill.cu; llama arch; GEMM operands bf16, stored tiled)
 // true (and cleared) when a prefill GEMM operand exceeded fp16's range since the last call
@@ -207,6 +210,14 @@ void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v
 void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
                        void* out16, int act_dtype);
 void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, int64_t f, void* out16, int act_dtype);
+
+// batched decode on the tensor-core path (batched.cu): per-row positions / slots
+void batched_rope_append(fq_ctx* ctx, const float* q, const float* k, const float* v, int B, int H, int hd,
+                         const float2* cs, const int32_t* pos, const int32_t* slots, __half* kv, int64_t slot_stride,
+                         int64_t layer_off, int64_t max_seq, float* qr, int act_dtype);
+void batched_attention(fq_ctx* ctx, const float* qr, const __half* kv, int B, int H, int hd, const int32_t* pos,
+                       const int32_t* slots, int64_t slot_stride, int64_t layer_off, int64_t max_seq, void* out16,
+                       int act_dtype);
 
 // statistics
 void launch_softmax_stats(fq_ctx* ctx, const float* logits, int64_t rows, int64_t vocab,

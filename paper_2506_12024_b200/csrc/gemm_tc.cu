@@ -30,7 +30,7 @@ namespace fqc {
 namespace {
 
 constexpr int kTM = 128;                      // weight rows per CTA (UMMA M)
-constexpr int kTN = 128;                      // tokens per CTA (UMMA N)
+constexpr int kTN = 128;                      // tokens per activation tile (the tiled layout's row block)
 constexpr int kTK = 128;                      // codes per k-block (one tiled block / group)
 constexpr int kTileBytes = kTM * kTK * 2;     // bf16 128 x 128 tile: 32 KB (A and B alike)
 constexpr int kInStages = 3;                  // activation + raw-weight ring
@@ -38,7 +38,10 @@ constexpr int kAStages = 2;                   // dequantised A ring
 constexpr int kGemmThreads = 384;             // 12 warps (3 per SM sub-partition: 168 registers each)
 constexpr int kDequantThreads = 192;          // warps 6..11
 constexpr int kRawBytes = 8 * kBlockBytes8;   // 8 raw 16x128 blocks (W8 size; W4 uses half)
-constexpr int kSmemGemm = kInStages * (kTileBytes + kRawBytes) + kAStages * kTileBytes + 1024;
+// tokens per CTA (UMMA N): 128, or 32 for decode-sized batches (the first 32 rows of a 128-row
+// tile are its first 8 KB in the canonical layout, so the same tiled activations serve both)
+template <int TN>
+constexpr int smem_gemm() { return kInStages * (TN * 256 + kRawBytes) + kAStages * kTileBytes + 1024; }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -58,10 +61,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
 }
 
 // kind::f16 instruction descriptor: D f32, A/B bf16 (F16 = 0) or fp16 (F16 = 1), both K-major,
-// N = kTN, M = kTM
-template <int F16>
+// N = TN, M = kTM
+template <int F16, int TN>
 constexpr uint32_t idesc() {
-  return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
+  return (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((TN >> 3) << 17) | ((kTM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -178,11 +181,13 @@ __device__ __forceinline__ void dequant_stage(const uint8_t* raw, int32_t zbase,
   }
 }
 
-template <int W>
+template <int W, int TN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_ws_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb, int32_t zbase, int64_t N,
                    const uint8_t* __restrict__ xt, int T, float* __restrict__ y, int64_t y_stride, int accumulate,
-                   int splits, int64_t split_stride) {
+                   int splits, int64_t split_stride, const uint8_t* __restrict__ row_rung, int64_t rr_stride,
+                   int want_rung) {
+  constexpr int kBBytes = TN * 256;  // activation bytes per k-block
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
   extern __shared__ __align__(1024) uint8_t gsm[];
@@ -191,11 +196,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __shared__ uint32_t tmem_base_s;
   uint8_t* base = gsm + ((1024u - (smem_addr(gsm) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer
   uint8_t* b_ring = base;                                        // kInStages x 32 KB activations
-  uint8_t* raw_ring = b_ring + kInStages * kTileBytes;           // kInStages x 8 raw blocks
+  uint8_t* raw_ring = b_ring + kInStages * kBBytes;              // kInStages x 8 raw blocks
   uint8_t* a_ring = raw_ring + kInStages * kRawBytes;            // kAStages x 32 KB bf16 (q - z)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
-  const int tt = blockIdx.y;  // token tile
+  const int tt = blockIdx.y;  // token tile of TN rows
+  const int64_t b_src = static_cast<int64_t>(tt * TN / kTN) * nkb * kTileBytes + (tt * TN % kTN) * 256;
   const int kb0 = static_cast<int>(static_cast<int64_t>(nkb) * blockIdx.z / splits);
   const int kb1 = static_cast<int>(static_cast<int64_t>(nkb) * (blockIdx.z + 1) / splits);
   const int nk = kb1 - kb0;
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_s)),
-                 "r"(2 * kTN));
+                 "r"(2 * TN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -231,8 +237,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int i = 0; i < nk; ++i) {
         const int s = i % kInStages, kb = kb0 + i;
         if (i >= kInStages) mbar_wait(&in_empty[s], ((i / kInStages) - 1) & 1, 0);
-        mbar_expect_tx(&in_full[s], kTileBytes + 8 * bb);
-        bulk_g2s(b_ring + s * kTileBytes, xt + (static_cast<int64_t>(tt) * nkb + kb) * kTileBytes, kTileBytes, &in_full[s]);
+        mbar_expect_tx(&in_full[s], kBBytes + 8 * bb);
+        bulk_g2s(b_ring + s * kBBytes, xt + b_src + static_cast<int64_t>(kb) * kTileBytes, kBBytes, &in_full[s]);
 #pragma unroll 1
         for (int r = 0; r < 8; ++r) {
           const int64_t tile = min(tile0 + r, static_cast<int64_t>(n_tiles) - 1);  // rows past N masked at store
@@ -249,8 +255,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&a_full[a], (i / kAStages) & 1, 1);
         if (i >= 2) mbar_wait(&d_empty[dbuf], ((i >> 1) - 1) & 1, 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_addr(a_ring + a * kTileBytes), b0 = smem_addr(b_ring + s * kTileBytes);
-        const uint32_t dt = tmem + static_cast<uint32_t>(dbuf * kTN);
+        const uint32_t a0 = smem_addr(a_ring + a * kTileBytes), b0 = smem_addr(b_ring + s * kBBytes);
+        const uint32_t dt = tmem + static_cast<uint32_t>(dbuf * TN);
 #pragma unroll
         for (int j = 0; j < kTK / 16; ++j) {
           const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               "{\n\t.reg .pred p;\n\t"
               "setp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
-              "l"(da), "l"(db), "r"(idesc<1>()), "r"(acc));
+              "l"(da), "l"(db), "r"(idesc<1, TN>()), "r"(acc));
         }
         tc_commit(&d_full[dbuf]);
         tc_commit(&a_empty[a]);
@@ -289,9 +295,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int64_t tile = min(tile0 + row / kTileRows, static_cast<int64_t>(n_tiles) - 1);
     const float* sc = reinterpret_cast<const float*>(tiles + tile * nkb * bb + cbytes) + (row % kTileRows);
     const int64_t sstride = bb / 4;  // floats between the scales of consecutive k-blocks
-    float acc[kTN];
+    float acc[TN];
 #pragma unroll
-    for (int c = 0; c < kTN; ++c) acc[c] = 0.f;
+    for (int c = 0; c < TN; ++c) acc[c] = 0.f;
     float s_next = nk > 0 ? sc[kb0 * sstride] : 0.f;
     for (int i = 0; i < nk; ++i) {
       const int dbuf = i & 1;
@@ -299,9 +305,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (i + 1 < nk) s_next = sc[(kb0 + i + 1) * sstride];
       mbar_wait(&d_full[dbuf], (i >> 1) & 1, 3);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(dbuf * kTN);
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(dbuf * TN);
 #pragma unroll
-      for (int c0 = 0; c0 < kTN; c0 += 16) {
+      for (int c0 = 0; c0 < TN; c0 += 16) {
         uint32_t v[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -318,11 +324,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) mbar_arrive(&d_empty[dbuf]);
     }
     if (n < N) {
-      const int t0 = tt * kTN;
+      const int t0 = tt * TN;
 #pragma unroll
-      for (int c = 0; c < kTN; ++c) {
+      for (int c = 0; c < TN; ++c) {
         const int t = t0 + c;
-        if (t < T) {
+        // row_rung: this launch covers only the rows decoding at want_rung (grouped batches)
+        if (t < T && (row_rung == nullptr || row_rung[t * rr_stride] == want_rung)) {
           float* yp = y + static_cast<int64_t>(t) * y_stride + n;
           *yp = accumulate ? *yp + acc[c] : acc[c];
         }
@@ -331,16 +338,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TN));
 }
 
 // y[t][n] (+)= sum over the splits in order of ws[z][t][n] (deterministic split-K reduction)
 __global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, int64_t T, int64_t N, float* __restrict__ y,
-                                    int64_t y_stride, int accumulate) {
+                                    int64_t y_stride, int accumulate, const uint8_t* __restrict__ row_rung,
+                                    int64_t rr_stride, int want_rung) {
   const int64_t total = T * N;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t t = i / N, n = i - t * N;
+    if (row_rung != nullptr && row_rung[t * rr_stride] != want_rung) continue;
     float v = ws[i];
     for (int z = 1; z < splits; ++z) v += ws[z * total + i];
     float* yp = y + t * y_stride + n;
@@ -371,11 +380,11 @@ __global__ void tile_acts_kernel(const void* __restrict__ x, int dtype, int64_t 
   }
 }
 
-template <int W>
+template <int W, int TN>
 void configure_gemm() {
   static bool done = false;
   if (!done) {
-    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemGemm));
+    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<W, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_gemm<TN>()));
     done = true;
   }
 }
@@ -398,7 +407,7 @@ void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride,
 }
 
 void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
-                    int64_t y_stride, bool accumulate) {
+                    int64_t y_stride, bool accumulate, const uint8_t* row_rung, int64_t rr_stride) {
   if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
   if (x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: the tiled activations are fp16 (bf16 values stored exactly)");
   const fq_rung_store& st = L->store(rung);
@@ -406,7 +415,8 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
   if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
   if ((reinterpret_cast<uintptr_t>(xt) & 15) != 0) fail(FQ_E_CONFIG, "gemm: tiled activations must be 16-byte aligned");
   const int n_tiles = ceil_div_i(L->N, kTileRows), nkb = ceil_div_i(L->K, kBlockK);
-  const int gx = ceil_div_i(L->N, kTM), gy = ceil_div_i(T, kTN);
+  const int tn = T <= 32 ? 32 : kTN;  // decode-sized batches: 32-token MMAs, a quarter of the activation traffic
+  const int gx = ceil_div_i(L->N, kTM), gy = ceil_div_i(T, tn);
   // split K when the output tiles alone leave SMs idle: the fewest splits with the lowest
   // (waves x work per split), at least 4 k-blocks per split
   int splits = 1;
@@ -437,23 +447,28 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
   const int acc = splits > 1 ? 0 : (accumulate ? 1 : 0);
   const auto* xb = static_cast<const uint8_t*>(xt);
+#define FQ_GEMM_LAUNCH(Wv, TNv)                                                                              \
+  do {                                                                                                      \
+    configure_gemm<Wv, TNv>();                                                                              \
+    gemm_ws_kernel<Wv, TNv><<<grid, kGemmThreads, smem_gemm<TNv>(), ctx->stream>>>(                          \
+        st.tiles, n_tiles, nkb, st.zp_base, L->N, xb, static_cast<int>(T), out, out_stride, acc, splits, split_stride, \
+        splits > 1 ? nullptr : row_rung, rr_stride, rung);                                                  \
+  } while (0)
   if (rung == FQ_RUNG_INT8) {
-    configure_gemm<0>();
-    gemm_ws_kernel<0><<<grid, kGemmThreads, kSmemGemm, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,
-                                                                     static_cast<int>(T), out, out_stride, acc, splits,
-                                                                     split_stride);
+    if (tn == 32) FQ_GEMM_LAUNCH(0, 32);
+    else FQ_GEMM_LAUNCH(0, 128);
   } else {
-    configure_gemm<1>();
-    gemm_ws_kernel<1><<<grid, kGemmThreads, kSmemGemm, ctx->stream>>>(st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,
-                                                                     static_cast<int>(T), out, out_stride, acc, splits,
-                                                                     split_stride);
+    if (tn == 32) FQ_GEMM_LAUNCH(1, 32);
+    else FQ_GEMM_LAUNCH(1, 128);
   }
+#undef FQ_GEMM_LAUNCH
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
   if (splits > 1) {
     const int64_t total = T * L->N;
     const int blocks = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
-    split_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->gemm_ws, splits, T, L->N, y, y_stride, accumulate ? 1 : 0);
+    split_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->gemm_ws, splits, T, L->N, y, y_stride, accumulate ? 1 : 0,
+                                                         row_rung, rr_stride, rung);
     FQ_CUDA(cudaGetLastError());
     ctx->launches += 1;
   }

@@ -808,6 +808,86 @@ void stage_rows(fq_model* M, int B, const int32_t* slots, const int32_t* tokens)
   }
 }
 
+void ensure_prefill_ws(fq_model* M, int64_t T);
+
+// ---------------------------------------------------------------- batched decode (tensor cores)
+// B >= batch_gemm_min() rows of a llama model (BASELINE C5): the step runs as row-parallel kernels
+// and one tcgen05 GEMM per (linear, precision copy present in the batch) -- every resident copy is
+// streamed at most once per step, however the rows' precision tables mix (batched.cu).
+int batch_gemm_min() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("FQ_BATCH_GEMM_MIN");
+    v = e ? std::max(1, std::atoi(e)) : 16;
+  }
+  return v;
+}
+
+bool batched_gemm_usable(const fq_model* M, int B) {
+  if (!M->llama || B < batch_gemm_min()) return false;
+  const fq_model_config& c = M->cfg;
+  if (c.head_dim != 64 && c.head_dim != 128) return false;
+  if (c.d_model % 8 != 0 || c.ffn_dim % 8 != 0) return false;
+  return true;
+}
+
+// Enqueues one batched step for the B rows staged in meta_dev (tokens / pos / slots / rung table);
+// `present[i]` = bit r set when some row runs linear i at rung r.
+void batched_step_enqueue(fq_model* M, int B, const std::vector<uint8_t>& present) {
+  fq_ctx* ctx = M->ctx;
+  const fq_model_config& c = M->cfg;
+  auto& w = M->pw;
+  const int64_t d = c.d_model, f = c.ffn_dim, V = c.vocab_size;
+  const int H = static_cast<int>(c.n_heads), hd = static_cast<int>(c.head_dim);
+  const int ad = c.act_dtype;
+  const StepMeta mt = M->meta(B);
+  const uint8_t* table = M->table_dev();
+  const int64_t nl = M->n_lin;
+  // one GEMM per copy present among the rows of linear i, each writing only its rows
+  auto linear = [&](int i, const void* xt, float* y, int64_t ys, bool acc) {
+    for (int r = FQ_RUNG_INT8; r <= FQ_RUNG_INT4; ++r)
+      if (present[static_cast<size_t>(i)] & (1u << r))
+        launch_gemm_dq(ctx, M->lin[i], r, B, xt, FQ_DT_F16, y, ys, acc, table + i, nl);
+  };
+  prefill_embed(ctx, M->tok_emb, mt.tokens, B, d, w.x);
+  for (int l = 0; l < c.n_layers; ++l) {
+    const int b0 = M->lin_index(l, 0);
+    const int64_t lo = static_cast<int64_t>(l) * M->layer_stride;
+    prefill_rmsnorm(ctx, w.x, B, d, M->n1g[l], c.norm_eps, w.h, ad);
+    linear(b0 + 0, w.h, w.q, d, false);
+    linear(b0 + 1, w.h, w.k, d, false);
+    linear(b0 + 2, w.h, w.v, d, false);
+    batched_rope_append(ctx, w.q, w.k, w.v, B, H, hd, M->rope_cs, mt.pos, mt.slots, static_cast<__half*>(M->kv),
+                        M->slot_stride, lo, c.max_seq_len, w.qr, ad);
+    batched_attention(ctx, w.qr, static_cast<const __half*>(M->kv), B, H, hd, mt.pos, mt.slots, M->slot_stride, lo,
+                      c.max_seq_len, w.a, ad);
+    linear(b0 + 3, w.a, w.x, d, true);  // x += attn . Wo^T
+    prefill_rmsnorm(ctx, w.x, B, d, M->n2g[l], c.norm_eps, w.h, ad);
+    linear(b0 + 4, w.h, w.g, f, false);
+    linear(b0 + 5, w.h, w.u, f, false);
+    prefill_swiglu(ctx, w.g, w.u, static_cast<int64_t>(B) * f, f, w.m, ad);
+    linear(b0 + 6, w.m, w.x, d, true);  // x += mid . Wdown^T
+  }
+  prefill_rmsnorm(ctx, w.x, B, d, M->fng, c.norm_eps, w.h, ad);
+  linear(M->head_index(), w.h, M->logits, V, false);
+  launch_softmax_stats(ctx, M->logits, B, V, V, M->stats_dev);
+}
+
+void batched_step(fq_model* M, int B) {
+  fq_ctx* ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  ensure_prefill_ws(M, B);
+  std::vector<uint8_t> present(static_cast<size_t>(M->n_lin), 0);
+  const uint8_t* tab = M->table_host();
+  for (int b = 0; b < B; ++b)
+    for (int i = 0; i < M->n_lin; ++i) present[static_cast<size_t>(i)] |= static_cast<uint8_t>(1u << tab[b * M->n_lin + i]);
+  FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+  batched_step_enqueue(M, B, present);
+  FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * B, cudaMemcpyDeviceToHost, st));
+  FQ_CUDA(cudaStreamSynchronize(st));
+  if (prefill_overflow_take(ctx)) fail(FQ_E_INPUT, "decode: an activation exceeds fp16's range (GEMM operand format)");
+}
+
 void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens, float* logits_dev,
                 fq_row_stats* stats_host) {
   require(B >= 1 && B <= M->cfg.max_batch, FQ_E_INPUT, "decode: batch out of range");
@@ -820,7 +900,8 @@ void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens,
     }
   }
   stage_rows(M, B, slots, tokens);
-  run_step(M, B);
+  if (batched_gemm_usable(M, B)) batched_step(M, B);
+  else run_step(M, B);
   for (int b = 0; b < B; ++b) M->slot_len[slots[b]] += 1;
   if (stats_host) std::memcpy(stats_host, M->stats_host, sizeof(fq_row_stats) * B);
   if (logits_dev)
