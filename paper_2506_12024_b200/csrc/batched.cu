@@ -99,12 +99,33 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
     l = l * fa + ps;
 #pragma unroll
     for (int e = 0; e < DPL; ++e) o[e] *= fa;
+    // P.V: the lanes own DPL dimensions; the round's V rows load 8 at a time, all in flight
+    // together (p_j of keys past the history is 0, their rows are not read)
     const int cnt = min(32, n - j0);
-    for (int jj = 0; jj < cnt; ++jj) {
-      const float pj = __shfl_sync(0xffffffffu, p, jj);
-      const __half* vr = vc + static_cast<int64_t>(j0 + jj) * hd + DPL * lane;
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) o[e] = fmaf(pj, __half2float(vr[e]), o[e]);
+    for (int jb = 0; jb < 32; jb += 8) {
+      if (jb >= cnt) break;
+      float vv[8][DPL];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int jj = min(jb + u, cnt - 1);
+        const __half* vr = vc + static_cast<int64_t>(j0 + jj) * hd + DPL * lane;
+        if constexpr (DPL == 4) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+          const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+          vv[u][0] = a.x; vv[u][1] = a.y; vv[u][2] = c.x; vv[u][3] = c.y;
+        } else {
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(vr));
+          vv[u][0] = a.x; vv[u][1] = a.y;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float pj = __shfl_sync(0xffffffffu, p, jb + u);  // 0 for keys past the history
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) o[e] = fmaf(pj, vv[u][e], o[e]);
+      }
     }
     m = mn;
   }

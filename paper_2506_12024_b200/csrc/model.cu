@@ -22,28 +22,16 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <string>
 
 namespace fqc {
 namespace {
 
 constexpr int kPartStride = 1024;
-constexpr int kPrefillRows = 8;  // prompt positions per prefill step (llama): the GEMV's MMA n  // columns of the sum-of-squares partial buffer per batch row
+constexpr int kPrefillRows = 8;  // prompt positions per prefill step (llama): the GEMV's MMA n
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
-
-__device__ __forceinline__ float act_load(const void* p, int dtype, int64_t i) {
-  if (dtype == FQ_DT_F32) return static_cast<const float*>(p)[i];
-  if (dtype == FQ_DT_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
-  return __half2float(static_cast<const __half*>(p)[i]);
-}
-__device__ __forceinline__ void act_store(void* p, int dtype, int64_t i, float v) {
-  if (dtype == FQ_DT_F32) static_cast<float*>(p)[i] = v;
-  else if (dtype == FQ_DT_BF16) static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
-  else static_cast<__half*>(p)[i] = __float2half_rn(v);
-}
-
 // Step metadata staged by the host each step: tokens[B], pos[B], slots[B], then the per-row
 // precision table [B][n_lin] (bytes).
 struct StepMeta {
@@ -331,6 +319,9 @@ struct fq_model {
   unsigned int* grid_barrier = nullptr;
   bool use_graphs = true;
   uint64_t built_epoch = 0;  // ctx->weight_epoch the cached programs / graphs were built at
+  // batched tensor-core steps: captured graphs per (copies per linear, B) signature
+  std::map<std::string, std::pair<cudaGraphExec_t, int64_t>> batch_graphs;
+  std::set<std::string> batch_seen;
   // device time of the step program kernels (events around the launch, captured into the graph)
   cudaEvent_t ev_prog[2] = {nullptr, nullptr};
   double prog_ms = 0.0;
@@ -400,9 +391,12 @@ void sync_weight_epoch(fq_model* M) {
     FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
     for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
+    for (auto& kv : M->batch_graphs) cudaGraphExecDestroy(kv.second.first);
     M->graphs.clear();
     M->graph_kernels.clear();
     M->programs.clear();
+    M->batch_graphs.clear();
+    M->batch_seen.clear();
   }
   M->built_epoch = M->ctx->weight_epoch;
 }
@@ -873,17 +867,54 @@ void batched_step_enqueue(fq_model* M, int B, const std::vector<uint8_t>& presen
   launch_softmax_stats(ctx, M->logits, B, V, V, M->stats_dev);
 }
 
+// One batched step.  The launch sequence depends only on B and on which copies each linear needs
+// (it changes at switch events), so it is captured once per such signature into a CUDA graph and
+// replayed; the first step of a signature runs uncaptured (it sizes the workspaces).
 void batched_step(fq_model* M, int B) {
   fq_ctx* ctx = M->ctx;
   cudaStream_t st = ctx->stream;
+  sync_weight_epoch(M);
   ensure_prefill_ws(M, B);
-  std::vector<uint8_t> present(static_cast<size_t>(M->n_lin), 0);
+  std::string sig(static_cast<size_t>(M->n_lin), '\0');
   const uint8_t* tab = M->table_host();
   for (int b = 0; b < B; ++b)
-    for (int i = 0; i < M->n_lin; ++i) present[static_cast<size_t>(i)] |= static_cast<uint8_t>(1u << tab[b * M->n_lin + i]);
-  FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
-  batched_step_enqueue(M, B, present);
-  FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * B, cudaMemcpyDeviceToHost, st));
+    for (int i = 0; i < M->n_lin; ++i) sig[static_cast<size_t>(i)] |= static_cast<char>(1u << tab[b * M->n_lin + i]);
+  const std::vector<uint8_t> present(sig.begin(), sig.end());
+  sig += "|" + std::to_string(B);
+  auto enqueue = [&] {
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    batched_step_enqueue(M, B, present);
+    FQ_CUDA(cudaMemcpyAsync(M->stats_host, M->stats_dev, sizeof(fq_row_stats) * B, cudaMemcpyDeviceToHost, st));
+  };
+  auto it = M->batch_graphs.find(sig);
+  if (!M->use_graphs || (it == M->batch_graphs.end() && !M->batch_seen.count(sig))) {
+    M->batch_seen.insert(sig);
+    enqueue();
+  } else {
+    if (it == M->batch_graphs.end()) {
+      if (M->batch_graphs.size() >= 8) {  // a few live signatures at a time
+        cudaGraphExecDestroy(M->batch_graphs.begin()->second.first);
+        M->batch_graphs.erase(M->batch_graphs.begin());
+      }
+      cudaGraph_t graph;
+      const int64_t l0 = ctx->launches;
+      FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue();
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        throw;
+      }
+      FQ_CUDA(cudaStreamEndCapture(st, &graph));
+      cudaGraphExec_t exec;
+      FQ_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      FQ_CUDA(cudaGraphDestroy(graph));
+      it = M->batch_graphs.emplace(sig, std::make_pair(exec, ctx->launches - l0)).first;
+      ctx->launches = l0;
+    }
+    FQ_CUDA(cudaGraphLaunch(it->second.first, st));
+    ctx->launches += it->second.second;
+  }
   FQ_CUDA(cudaStreamSynchronize(st));
   if (prefill_overflow_take(ctx)) fail(FQ_E_INPUT, "decode: an activation exceeds fp16's range (GEMM operand format)");
 }
@@ -1266,6 +1297,7 @@ fq_status fq_model_destroy(fq_model* M) {
     cudaStreamSynchronize(M->ctx->stream);
     for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
+    for (auto& kv : M->batch_graphs) cudaGraphExecDestroy(kv.second.first);
     dfree(M->grid_barrier);
     free_prefill_ws(M);
     for (cudaEvent_t e : M->ev_prog)
