@@ -8,6 +8,8 @@
 
 #include "flexquant/analyzer.hpp"
 #include "flexquant/engine.hpp"
+#include "flexquant/fixture.hpp"
+#include "flexquant/metrics.hpp"
 #include "flexquant/model.hpp"
 #include "flexquant/quantizer.hpp"
 #include "flexquant/scheduler.hpp"
@@ -275,6 +277,36 @@ PYBIND11_MODULE(_flexquant, m) {
     return generate_batch(ps, md, plan, c);
   });
   m.def("traffic_report", [](const DecodeTrace& t) { return format_traffic_report(traffic_report(t)); });
+  py::class_<TrafficReport>(m, "TrafficReport")
+      .def_readonly("total_weight_bytes", &TrafficReport::total_weight_bytes)
+      .def_readonly("mean_bytes_per_token", &TrafficReport::mean_bytes_per_token)
+      .def_readonly("bucket_sum_over_total", &TrafficReport::bucket_sum_over_total)
+      .def_readonly("ppl_share", &TrafficReport::ppl_share);
+  m.def("traffic_report_struct", [](const DecodeTrace& t) { return traffic_report(t); });
+  py::class_<SweepRow>(m, "SweepRow")
+      .def_readonly("speed", &SweepRow::speed)
+      .def_readonly("final_effective_bits", &SweepRow::final_effective_bits)
+      .def_readonly("mean_bytes_per_token", &SweepRow::mean_bytes_per_token)
+      .def_readonly("agreement_vs_fp", &SweepRow::agreement_vs_fp)
+      .def_readonly("first_divergence", &SweepRow::first_divergence)
+      .def_readonly("rouge_l_vs_fp", &SweepRow::rouge_l_vs_fp);
+  m.def("sweep_switch_speed", [](py::array_t<int32_t> p, Model& md, const SwitchPlan& plan, std::vector<int64_t> speeds,
+                                 const GenerationConfig& c) {
+    const std::vector<TokenId> t = to_tokens(p);
+    py::gil_scoped_release nogil;
+    return sweep_switch_speed(t, md, plan, speeds, c);
+  });
+  m.def("sweep_csv_header", &sweep_csv_header);
+  m.def("sweep_csv_row", &sweep_csv_row);
+  // fixtures and metrics (include/flexquant/fixture.hpp, metrics.hpp)
+  m.def("tiny_config", &tiny_config);
+  m.def("micro_config", &micro_config);
+  m.def("make_fixture_model", [](const ModelConfig& c, uint64_t seed) { return make_fixture_model(c, seed); });
+  m.def("agreement_rate", [](std::vector<int32_t> a, std::vector<int32_t> b) {
+    const Agreement g = agreement_rate(a, b);
+    return py::make_tuple(g.rate, g.divergence_index ? py::cast(*g.divergence_index) : py::none());
+  });
+  m.def("rouge_l", [](std::vector<int32_t> a, std::vector<int32_t> b) { return rouge_l(a, b); });
   m.def("load_trace_file", &load_trace_file);
   m.def("save_trace_file", &save_trace_file);
   m.def("trace_to_csv", &trace_to_csv);

@@ -258,3 +258,37 @@ def test_weights_container_round_trip_reference_and_llama(tmp_path):
     rb = b.prefill_rows(0, toks)
     assert [r["argmax"] for r in ra] == [r["argmax"] for r in rb]
     assert all(x["ppl_entropy"] == y["ppl_entropy"] for x, y in zip(ra, rb))
+
+
+@pytest.mark.gpu
+def test_sweep_reproduces_golden_csv_rows():
+    """Acceptance c9 (proj/tests/acceptance.cpp:410-434): the speed sweep of the tiny fixture
+    (seed 1) under its 2048-bin ladder plan, 200 tokens, speeds 1 and 20, on prompt p01, writes
+    the reference's golden CSV rows (tests/golden/sweep.csv) character for character."""
+    m = fq.make_fixture_model(fq.tiny_config(), 1)
+    plan = fq.build_ladder_plan(m, [fq.Rung.Int8, fq.Rung.Int4], 2048)
+    prompt = np.frombuffer(open(os.path.join(GOLD, "p01.txt"), "rb").read(), np.uint8).astype(np.int32)
+    cfg = fq.GenerationConfig()
+    cfg.max_new_tokens = 200
+    rows = fq.sweep_switch_speed(prompt, m, plan, [1, 20], cfg)
+    got = fq.sweep_csv_header() + "".join(fq.sweep_csv_row("p01", r) for r in rows)
+    want = "".join(open(os.path.join(GOLD, "sweep.csv")).readlines()[:3])
+    assert got == want, (got, want)
+
+
+@pytest.mark.gpu
+def test_latency_breakdown_c11_analogue():
+    """Acceptance c11 (proj/tests/acceptance.cpp:494-501): the trace's per-rung time buckets sum
+    to the step time within 5% and the PPLE computation stays under 2% of it."""
+    m = fq.make_fixture_model(fq.tiny_config(), 1)
+    plan = fq.build_ladder_plan(m, [fq.Rung.Int8, fq.Rung.Int4], 2048)
+    prompt = np.frombuffer(open(os.path.join(GOLD, "p01.txt"), "rb").read(), np.uint8).astype(np.int32)
+    cfg = fq.GenerationConfig()
+    cfg.max_new_tokens = 120
+    cfg.scheduler.threshold_mode = fq.ThresholdMode.Absolute
+    cfg.scheduler.theta = float("inf")
+    r = fq.generate(prompt, m, plan, cfg)
+    rep = fq.traffic_report_struct(r.trace)
+    print(fq.traffic_report(r.trace))
+    assert abs(rep.bucket_sum_over_total - 1.0) <= 0.05
+    assert rep.ppl_share < 0.02

@@ -67,3 +67,22 @@ def test_two_rank_gloo_sharding_timing_and_gather():
         assert t == 2.0  # max over ranks
         assert merged == [(i, parallel.prompt_seed(5, i)) for i in range(n)]
         assert thr == pytest.approx(2 * len(parallel.shard(n, rank, 2)) / 2.0)
+
+
+def test_bench_gpus_flag_launches_the_ranks():
+    """bench.py --gpus N without a launcher starts N ranks itself (torchrun, loopback rendezvous)
+    and rank 0 prints one JSON line with n_gpus = N (here the reference arm over gloo: no GPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["REF_BLOCKS"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "c1", "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference" and line["value"] > 0
