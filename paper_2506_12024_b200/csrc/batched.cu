@@ -52,7 +52,7 @@ template <int DPL>
 __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __half* __restrict__ kv, int B, int H,
                                         const int32_t* __restrict__ pos, const int32_t* __restrict__ slots,
                                         int64_t slot_stride, int64_t layer_off, int64_t max_seq,
-                                        uint16_t* __restrict__ out, int nkb, int f16) {
+                                        uint16_t* __restrict__ out, int nkb, int f16, int slot0) {
   constexpr int hd = DPL * 32;
   __shared__ float qs[8][hd];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -62,9 +62,11 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
   const int d = H * hd;
   for (int e = lane; e < hd; e += 32) qs[wib][e] = qr[static_cast<int64_t>(b) * d + h * hd + e];
   __syncwarp();
-  const __half* kc = kv + static_cast<int64_t>(slots[b]) * slot_stride + layer_off + static_cast<int64_t>(h) * max_seq * hd;
+  // pos / slots null: the rows of one prompt (row b at position b of slot slot0)
+  const int64_t slot = slots ? slots[b] : slot0;
+  const __half* kc = kv + slot * slot_stride + layer_off + static_cast<int64_t>(h) * max_seq * hd;
   const __half* vc = kc + static_cast<int64_t>(H) * max_seq * hd;
-  const int n = pos[b] + 1;
+  const int n = (pos ? pos[b] : b) + 1;
   float m = -INFINITY, l = 0.f, o[DPL];
 #pragma unroll
   for (int e = 0; e < DPL; ++e) o[e] = 0.f;
@@ -150,16 +152,18 @@ void batched_rope_append(fq_ctx* ctx, const float* q, const float* k, const floa
 
 void batched_attention(fq_ctx* ctx, const float* qr, const __half* kv, int B, int H, int hd, const int32_t* pos,
                        const int32_t* slots, int64_t slot_stride, int64_t layer_off, int64_t max_seq, void* out16,
-                       int act_dtype) {
+                       int act_dtype, int slot0) {
   const int items = B * H, per = 8;
   const int blocks = (items + per - 1) / per;
   const int nkb = ceil_div_i(static_cast<int64_t>(H) * hd, 128), f16 = act_dtype == FQ_DT_F16 ? 1 : 0;
   if (hd == 128)
     attn_decode_rows_kernel<4><<<blocks, per * 32, 0, ctx->stream>>>(qr, kv, B, H, pos, slots, slot_stride, layer_off,
-                                                                     max_seq, static_cast<uint16_t*>(out16), nkb, f16);
+                                                                     max_seq, static_cast<uint16_t*>(out16), nkb, f16,
+                                                                     slot0);
   else if (hd == 64)
     attn_decode_rows_kernel<2><<<blocks, per * 32, 0, ctx->stream>>>(qr, kv, B, H, pos, slots, slot_stride, layer_off,
-                                                                     max_seq, static_cast<uint16_t*>(out16), nkb, f16);
+                                                                     max_seq, static_cast<uint16_t*>(out16), nkb, f16,
+                                                                     slot0);
   else
     fail(FQ_E_CONFIG, "batched decode: head_dim must be 64 or 128");
   FQ_CUDA(cudaGetLastError());

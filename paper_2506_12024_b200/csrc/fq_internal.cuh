@@ -207,17 +207,16 @@ void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev,
 void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16, int act_dtype);
 void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,
                      const float2* cs, float* qr, __half* kv_layer, int64_t max_seq, int act_dtype);
-void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
-                       void* out16, int act_dtype);
 void prefill_swiglu(fq_ctx* ctx, const float* g, const float* u, int64_t n, int64_t f, void* out16, int act_dtype);
 
 // batched decode on the tensor-core path (batched.cu): per-row positions / slots
 void batched_rope_append(fq_ctx* ctx, const float* q, const float* k, const float* v, int B, int H, int hd,
                          const float2* cs, const int32_t* pos, const int32_t* slots, __half* kv, int64_t slot_stride,
                          int64_t layer_off, int64_t max_seq, float* qr, int act_dtype);
+// pos / slots null: the T rows of one prompt in slot slot0 (row t attends keys 0..t)
 void batched_attention(fq_ctx* ctx, const float* qr, const __half* kv, int B, int H, int hd, const int32_t* pos,
                        const int32_t* slots, int64_t slot_stride, int64_t layer_off, int64_t max_seq, void* out16,
-                       int act_dtype);
+                       int act_dtype, int slot0 = 0);
 
 // statistics
 void launch_softmax_stats(fq_ctx* ctx, const float* logits, int64_t rows, int64_t vocab,

@@ -419,8 +419,10 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
   const int gx = ceil_div_i(L->N, kTM), gy = ceil_div_i(T, tn);
   // split K when the output tiles alone leave SMs idle: the fewest splits with the lowest
   // (waves x work per split), at least 4 k-blocks per split
+  // the split-K reduction is a separate pass over splits x T x N floats: split only grids that
+  // leave more than half the SMs idle (decode-sized batches), not to even out waves
   int splits = 1;
-  {
+  if (static_cast<int64_t>(gx) * gy * 2 <= ctx->num_sms) {
     const int64_t cta = gx * static_cast<int64_t>(gy);
     double best = static_cast<double>((cta + ctx->num_sms - 1) / ctx->num_sms);
     for (int sp = 2; sp <= 8 && nkb / sp >= 4; ++sp) {

@@ -1064,7 +1064,9 @@ void prefill_gemm_enqueue(fq_model* M, int slot, const int32_t* tokens_host, int
     launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, FQ_DT_F16, w.k, d);
     launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, FQ_DT_F16, w.v, d);
     prefill_rope_kv(ctx, w.q, w.k, w.v, Ti, H, hd, M->rope_cs, w.qr, kvl, c.max_seq_len, ad);
-    prefill_attention(ctx, w.qr, kvl, H, hd, c.max_seq_len, Ti, w.a, ad);
+    // causal attention of the prompt rows: 32 keys per warp round (batched.cu)
+    batched_attention(ctx, w.qr, static_cast<const __half*>(M->kv), Ti, H, hd, nullptr, nullptr, M->slot_stride,
+                      static_cast<int64_t>(l) * M->layer_stride, c.max_seq_len, w.a, ad, slot);
     launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, FQ_DT_F16, w.x, d, true);  // x += attn . Wo^T
     prefill_rmsnorm(ctx, w.x, Ti, d, M->n2g[l], c.norm_eps, w.h, ad);
     launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, FQ_DT_F16, w.g, f);

@@ -78,41 +78,6 @@ __global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __
   }
 }
 
-// Causal attention of query row t, head h on one warp (lanes own hd/32 dims), online softmax over
-// the keys 0..t of the fp16 cache; output bf16.
-template <int DPL>
-__global__ void attn_rows_kernel(const float* __restrict__ qr, const __half* __restrict__ kv_layer, int H, int64_t max_seq,
-                                 int T, uint16_t* __restrict__ out, int nkb, int f16) {
-  constexpr int hd = DPL * 32;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= T * H) return;
-  const int t = warp / H, h = warp - t * H;
-  const int d = H * hd;
-  float q[DPL];
-#pragma unroll
-  for (int e = 0; e < DPL; ++e) q[e] = qr[static_cast<int64_t>(t) * d + h * hd + DPL * lane + e];
-  const __half* kc = kv_layer + static_cast<int64_t>(h) * max_seq * hd;
-  const __half* vc = kc + static_cast<int64_t>(H) * max_seq * hd;
-  float m = -INFINITY, l = 0.f, o[DPL];
-#pragma unroll
-  for (int e = 0; e < DPL; ++e) o[e] = 0.f;
-  for (int j = 0; j <= t; ++j) {
-    float s = 0.f;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) s += q[e] * __half2float(kc[static_cast<int64_t>(j) * hd + DPL * lane + e]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    const float mn = fmaxf(m, s);
-    const float fa = m == -INFINITY ? 0.f : expf(m - mn), p = expf(s - mn);
-    l = l * fa + p;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) o[e] = o[e] * fa + p * __half2float(vc[static_cast<int64_t>(j) * hd + DPL * lane + e]);
-    m = mn;
-  }
-#pragma unroll
-  for (int e = 0; e < DPL; ++e) out[tiled_act_offset(t, h * hd + DPL * lane + e, nkb)] = actb(o[e] / l, f16);
-}
-
 __global__ void swiglu_rows_kernel(const float* __restrict__ g, const float* __restrict__ u, int64_t n, int64_t f,
                                    uint16_t* __restrict__ out, int nkb, int f16) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -155,21 +120,6 @@ void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float*
 void prefill_rope_kv(fq_ctx* ctx, const float* q, const float* k, const float* v, int T, int H, int hd,
                      const float2* cs, float* qr, __half* kv_layer, int64_t max_seq, int act_dtype) {
   rope_kv_rows_kernel<<<T, 256, 0, ctx->stream>>>(q, k, v, H, hd, cs, qr, kv_layer, max_seq, act_dtype == FQ_DT_F16 ? 1 : 0);
-  FQ_CUDA(cudaGetLastError());
-  ctx->launches += 1;
-}
-
-void prefill_attention(fq_ctx* ctx, const float* qr, const __half* kv_layer, int H, int hd, int64_t max_seq, int T,
-                       void* out16, int act_dtype) {
-  const int f16 = act_dtype == FQ_DT_F16 ? 1 : 0;
-  const int warps = T * H;
-  const int blocks = (warps * 32 + 255) / 256;
-  if (hd == 128)
-    attn_rows_kernel<4><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<uint16_t*>(out16),
-                                                        ceil_div_i(static_cast<int64_t>(H) * hd, 128), f16);
-  else
-    attn_rows_kernel<2><<<blocks, 256, 0, ctx->stream>>>(qr, kv_layer, H, max_seq, T, static_cast<uint16_t*>(out16),
-                                                        ceil_div_i(static_cast<int64_t>(H) * hd, 128), f16);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
 }
