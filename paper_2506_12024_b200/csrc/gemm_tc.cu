@@ -145,15 +145,31 @@ __device__ __forceinline__ void dequant_stage(const uint8_t* raw, int32_t zbase,
   constexpr int cbytes = W == 0 ? 2048 : 1024;
   constexpr int words = W == 0 ? 4 : 2;  // 16-byte code words per lane per block
   constexpr int units = 8 * words * 32;  // (block, word, lane) units of the stage
-#pragma unroll 2
-  for (int u = d; u < units; u += kDequantThreads) {
+  constexpr int per = (units + kDequantThreads - 1) / kDequantThreads;
+  // every load of the thread's units first (independent, all in flight), then the conversions
+  uint4 wv[per];
+  uint32_t z0v[per], z1v[per];
+#pragma unroll
+  for (int j = 0; j < per; ++j) {
+    const int u = d + j * kDequantThreads;
+    if (u < units) {
+      const int rt = u / (words * 32), rem = u - rt * (words * 32);
+      const int i = rem >> 5, t = rem & 31, r = t >> 2;
+      const uint8_t* blk = raw + rt * bb;
+      wv[j] = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
+      z0v[j] = zpair(blk + cbytes + 64, r, zbase);
+      z1v[j] = zpair(blk + cbytes + 64, r + 8, zbase);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < per; ++j) {
+    const int u = d + j * kDequantThreads;
+    if (u >= units) break;
     const int rt = u / (words * 32), rem = u - rt * (words * 32);
     const int i = rem >> 5, t = rem & 31;
     const int r = t >> 2, c2 = 2 * (t & 3);
-    const uint8_t* blk = raw + rt * bb;
-    const uint4 w = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
-    const uint32_t z0 = zpair(blk + cbytes + 64, r, zbase), z1 = zpair(blk + cbytes + 64, r + 8, zbase);
-    const uint32_t q4[4] = {w.x, w.y, w.z, w.w};
+    const uint32_t q4[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+    const uint32_t z0 = z0v[j], z1 = z1v[j];
     const int row = rt * 16 + r;
     if constexpr (W == 0) {
 #pragma unroll
