@@ -34,6 +34,7 @@ CONFIGS = {
                name="tiny-4L-d512"),
 }
 METRIC = "decode tokens/s (7B-shape, entropy-switched W8/W4)"
+CAL_SEQS, CAL_LEN = 4, 128  # logit-KL calibration sample that orders the switch plan
 
 
 def peaks():
@@ -128,36 +129,35 @@ class Scheduler:
         return avg, first, cnt
 
 
-def cpu_baseline_sample(cfg, threads: int, budget_calls: int = 1):
-    """Times the reference's quantized linear (dequantize + linear, src/model.cpp:77-98) on the
-    box's host cores with the reference library built from its own sources (oracle/_ref), one
-    7B-shape layer per call; returns seconds per parameter at W8 and W4."""
-    import oracle  # noqa: E402  (cpu_baseline leg only)
-    R = oracle.ref()
-    kind = "reference"
+def cpu_decode_sample(cfg, blocks: int = 1, steps: int = 2):
+    """The reference's decode on ONE host core (oracle/_ref, built from its sources): a
+    reference-architecture model at the 7B block dimensions with `blocks` blocks and the full
+    head, a 16-token prompt, then `steps` real forward_decode + statistics + argmax tokens;
+    tokens/s scaled to a full 7B-shape token by linear parameter count."""
+    import ctypes as C
+    R = _ref_decoder_lib()
     if R is None:
         return None
-    K, N = 4096, 4096
-    rng = np.random.default_rng(0)
-    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float32)
-    x = rng.standard_normal((1, K)).astype(np.float32)
-    import ctypes as C
-    out = {}
-    for bits in (8, 4):
-        res = [0.0] * threads
-
-        def work(i):
-            s = C.c_double()
-            R.ref_time_quant_linear(w, N, K, 128, bits, x, 1, budget_calls, C.byref(s))
-            res[i] = s.value
-
-        ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-        out[bits] = statistics.mean(res) / (N * K)
-    return out, kind
+    prompt = np.random.default_rng(7).integers(0, cfg["vocab_size"], 16).astype(np.int32)
+    t0 = time.perf_counter()
+    h = R.ref_decoder_create(cfg["vocab_size"], cfg["d_model"], cfg["n_heads"], cfg["head_dim"], blocks, cfg["ffn_dim"],
+                             16 + steps + 1, 7, prompt, 16, 0.5)
+    if not h:
+        return None
+    build_s = time.perf_counter() - t0
+    secs = []
+    for _ in range(steps):
+        s_, p_ = C.c_double(), C.c_double()
+        R.ref_decoder_step(h, C.byref(s_), C.byref(p_))
+        secs.append(s_.value)
+    scale = params_per_token(cfg) / R.ref_decoder_params(h)
+    R.ref_decoder_destroy(h)
+    per_tok = statistics.mean(secs) * scale
+    return {"value": 1.0 / per_tok, "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "sample": f"{steps} real decode tokens (forward_decode + ppl_entropy + fault_tolerance + argmax, 50/50 "
+                      f"W8/W4) of a {blocks}-block reference model at the 7B block dimensions after a 16-token "
+                      f"prompt, one core, scaled x{scale:.2f} by parameters to a 7B-shape token "
+                      f"({build_s:.0f} s to build the model, not timed)"}
 
 
 def params_per_token(cfg):
@@ -338,9 +338,21 @@ def main():
                        max_seq_len=max_seq, norm_eps=1e-5, rope_theta=10000.0,
                        **{k: cfg[k] for k in ("vocab_size", "d_model", "n_heads", "head_dim", "n_layers", "ffn_dim")})
     t_init = time.perf_counter()
-    kl8, kl4 = model.init_random(seed=1234, std=0.02, kl_bins=2048)
+    model.init_random(seed=1234, std=0.02)
     t_init = time.perf_counter() - t_init
-    plan = build_plan(model.ids, kl4)
+    # the switch plan from the logit-KL calibration (BASELINE config 4: KL(softmax(l_w4-block) ||
+    # softmax(l_w8)) per block on teacher-forced random tokens, tcgen05 prefill path) on a small
+    # sample: blocks ascending by KL, a block's linears by id, build_switch_plan order
+    # (src/analyzer.cpp:124-139); the head, which the block calibration does not flip, ranks last
+    t_cal = time.perf_counter()
+    cal_rng = np.random.default_rng(4)
+    cal_toks = cal_rng.integers(0, cfg["vocab_size"], (CAL_SEQS, CAL_LEN)).astype(np.int32)
+    kl_blk, _ = model.calibrate_logit_kl(cal_toks, capi.RUNG_INT8, capi.RUNG_INT4)
+    t_cal = time.perf_counter() - t_cal
+    per_block = len(model.ids) // cfg["n_layers"]
+    kl_lin = [float(kl_blk[i // per_block]) if i < cfg["n_layers"] * per_block else float("inf")
+              for i in range(len(model.ids))]
+    plan = build_plan(model.ids, kl_lin)
     model.set_all_rungs(0, capi.RUNG_INT8)
 
     from paper_2506_12024_b200 import parallel  # noqa: E402
@@ -417,49 +429,56 @@ def main():
     prog_achieved = step_bytes / (prog_launch_ms / 1000.0) / 1e9 if prog_n else None
     gemv_achieved = gemv_bytes / gemv_per_step / (ms_gemv / 1000.0) / 1e9
 
-    # ---- e2e through the public API with host buffers: a fresh generate over the whole
-    #      config (prompt H2D, per-token statistics D2H, host scheduler), wall clock = events
+    # ---- e2e through the reference-facing C++ API (flexquant::generate, libflexquant_b200.so)
+    #      with host buffers: prompt H2D, the 256-token prefill on the tcgen05 path, then the
+    #      decode loop with the C++ SchedulerState and the plan above; device events around it
+    from paper_2506_12024_b200 import _flexquant as fq  # noqa: E402
     e2e_tokens = min(cfg["decode"], max_seq - cfg["prompt"])
-    model.reset_slot(0)
-    model.set_all_rungs(0, capi.RUNG_INT8)
+    fc = fq.ModelConfig()
+    fc.arch = fq.Arch.Llama
+    for k in ("vocab_size", "d_model", "n_heads", "head_dim", "n_layers", "ffn_dim"):
+        setattr(fc, k, cfg[k])
+    fc.max_seq_len, fc.group_size, fc.max_batch = max_seq, 128, 1
+    fmodel = fq.Model(fc)
+    fmodel.init_random(1234, 0.02)  # the same device generator and seed: identical weights
+    fplan = fq.SwitchPlan()
+    ents = []
+    for lid, _ in plan:
+        e = fq.SwitchEntry()
+        e.layer_id, e.from_, e.to, e.kl = lid, fq.Rung.Int8, fq.Rung.Int4, 0.0
+        ents.append(e)
+    fplan.entries = ents
+    gcfg = fq.GenerationConfig()
+    gcfg.max_new_tokens = e2e_tokens
+    gcfg.start_rung = fq.Rung.Int8
+    gcfg.scheduler.threshold_mode = fq.ThresholdMode.Prefill
+    gcfg.scheduler.theta = args.theta
+    gcfg.scheduler.window_len = W
+    gcfg.scheduler.layers_per_switch = args.layers_per_switch
+    fstream = torch.cuda.ExternalStream(fq.runtime_stream())
+    prompt_host = prompt.copy()  # host buffer: copied to the device by the engine each call
+    fq.generate(prompt_host[:32], fmodel, fplan, gcfg)  # warm-up (program build, graph capture)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    prompt_host = prompt.copy()  # host buffer: copied to the device by the engine each call
-    st = model.prefill(0, prompt_host)
-    sched = Scheduler(W, args.theta * (sum(float(v) for v in st["ppl_entropy"][-k:]) / k), len(plan),
-                      args.layers_per_switch)
-    row = st[-1]
-    generated = []
-    for _ in range(e2e_tokens):
-        generated.append(int(row["argmax"]))
-        _, first, cnt = sched.observe(float(row["ppl_entropy"]))
-        for i in range(cnt):
-            model.set_rung(0, plan[first + i][1], capi.RUNG_INT4)
-        if len(generated) < e2e_tokens:
-            row = model.decode([0], [generated[-1]])[0]
-    f1.record(stream)
+    f0.record(fstream)
+    res = fq.generate(prompt_host, fmodel, fplan, gcfg)
+    f1.record(fstream)
     torch.cuda.synchronize()
     e2e_ms = parallel.max_over_ranks(f0.elapsed_time(f1), device="cuda")
-    e2e_value = parallel.aggregate_throughput(e2e_tokens, world, e2e_ms / 1000.0)
+    e2e_value = parallel.aggregate_throughput(len(res.sequence), world, e2e_ms / 1000.0)
+    e2e_switches = sum(len(r.switch_events) for r in res.trace.records)
     row_bytes = capi.ROW_STATS_DTYPE.itemsize
     h2d = (cfg["prompt"] * 4 + (e2e_tokens - 1) * 4) / e2e_tokens
     d2h = (cfg["prompt"] + e2e_tokens - 1) * row_bytes / e2e_tokens
+    del fmodel
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            res = cpu_baseline_sample(cfg, 1)
-            if res is not None:
-                spp, kind = res
-                w4_share = sum(1 for r in range(model.n_linears) if model.get_rung(0, r) == capi.RUNG_INT4) / model.n_linears
-                s_tok = params_per_token(cfg) * ((1 - w4_share) * spp[8] + w4_share * spp[4])
-                cpu = {"value": 1.0 / s_tok, "unit": "tokens/s", "cores": 1, "kind": kind,
-                       "sample": "one dequantize+linear call (4096x4096, g128, W8 and W4) of the reference library "
-                                 "built from source, extrapolated by parameter count to one 7B token"}
+            cpu = cpu_decode_sample(cfg)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -480,7 +499,8 @@ def main():
             "config": {
                 "workload": f"{cfg['name']} (BASELINE config {3 if args.config == 'c3' else 1}): B=1 per GPU, {cfg['prompt']}-token random prompt, "
                             f"decode positions {cfg['prompt']}..{cfg['prompt'] + args.warmup + args.steps}, "
-                            "W8 start, 8->4 plan ordered by weight-histogram KL (2048 bins)",
+                            f"W8 start, 8->4 plan ordered by the logit-KL calibration (BASELINE config 4 on "
+                            f"{CAL_SEQS}x{CAL_LEN} tokens, {t_cal:.1f} s)",
                 "model": cfg["name"], "global_batch": world, "seq_len": cfg["prompt"] + args.warmup + args.steps,
                 "parallelism": f"dp{world}", "group_size": 128, "kv_cache": "fp16",
                 "scheduler": {"mode": "prefill", "theta": args.theta, "threshold": thre, "window": W,
@@ -504,7 +524,9 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "note": "prefill + decode of the full config through fq_model_prefill/decode with host buffers"},
+                    "note": f"flexquant::generate (C++ API, libflexquant_b200.so) of the full config with host "
+                            f"buffers: {cfg['prompt']}-token prefill on the tcgen05 path + {e2e_tokens} decode tokens "
+                            f"with the C++ SchedulerState, {e2e_switches} switch events"},
             "gpu_launches": launches_timed,
             "clocks": clocks.summary(),
         }
