@@ -9,22 +9,6 @@
 
 namespace fqc {
 
-// Split attention with the O projection's staging merging the partials (measured slower than
-// one CTA per (row, head) at the 7B shape; compiled out by default: its code costs i-cache)
-// Per-head QKV tile flags instead of the QKV -> attention grid barrier (opt-in at run time with
-// FQ_HEAD_FLAGS=1 when compiled in; measured +0.3 % per step, and +0.5 % of code cost when merely
-// compiled in, so off by default)
-#ifndef FQ_HEAD_FLAGS_DEV
-#define FQ_HEAD_FLAGS_DEV 0
-#endif
-// Tagged (half2, tag) activation hand-off before the O / down projections (run-time opt-in
-// FQ_TAGS=1 when compiled in; measured +18 % per step, so compiled out by default)
-#ifndef FQ_TAGS_DEV
-#define FQ_TAGS_DEV 0
-#endif
-#ifndef FQ_ATTN_MERGE
-#define FQ_ATTN_MERGE 0
-#endif
 constexpr int kMaxB = 8;          // batch rows per GEMV phase (the MMA's n = 8 columns)
 constexpr int kMaxMat = 3;        // matrices sharing one input (QKV)
 constexpr int kMaxStages = 8;

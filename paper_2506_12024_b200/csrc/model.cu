@@ -441,24 +441,12 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       // the O and down projections read their inputs pre-staged in B-fragment order (written by the
       // attention / SwiGLU epilogues); FQ_NO_FRAG=1 stages them from the plain activations
       const bool use_frag = std::getenv("FQ_NO_FRAG") == nullptr && B <= kMaxB;
-      // ... optionally polled as (half2, tag) words instead of a grid barrier (FQ_TAGS=1; one GEMV
-      // phase per projection, i.e. B <= kMaxB).  Measured +18% per step at the 7B shape: the
-      // consumers see the words ~6 us after the attention CTAs finish vs ~3.5 us for barrier +
-      // staging, so the barriers stay the default.
-      const bool tagged = FQ_TAGS_DEV && use_frag && std::getenv("FQ_TAGS") != nullptr;
-      // QKV -> attention through per-tile flags instead of a grid barrier (decode, one QKV phase,
-      // unsplit attention over whole 16-row tiles per head)
-      const bool head_flags = FQ_HEAD_FLAGS_DEV && std::getenv("FQ_HEAD_FLAGS") != nullptr && mode == STEP_DECODE && B <= kMaxB &&
-                              c.head_dim % 16 == 0 && M->tile_flags != nullptr;
+      // (measured alternatives to the grid barriers -- tagged activation words, per-head QKV tile
+      // flags, attention split over CTAs with the O staging merging the partials -- were all
+      // slower at the 7B shape and are not built: DESIGN.md §4)
+      const bool tagged = false, head_flags = false;
       const int frag_nkb_d = static_cast<int>((d + kBlockK - 1) / kBlockK);
-      // attention work items: (row, head, split); with few rows the keys of a head are split over
-      // up to kMaxAttnSplit CTAs and the O projection's staging merges the partials
-      // (measured: the merge costs the O projection's staging more than the split saves; off by
-      // default, FQ_ATTN_SPLITS=n to experiment)
-      const char* se = std::getenv("FQ_ATTN_SPLITS");
-      const int kMaxAttnSplit = se ? std::max(1, std::min(4, std::atoi(se))) : 1;  // needs FQ_ATTN_MERGE device code
-      const int attn_splits = gemv_only ? 1
-          : std::max(1, std::min(std::min(kMaxAttnSplit, M->n_chunks), G / std::max(1, B * static_cast<int>(c.n_heads))));
+      const int attn_splits = 1;
       for (int64_t l = 0; l < c.n_layers; ++l) {
         GemvLaunch g;
         g.nmat = 3;

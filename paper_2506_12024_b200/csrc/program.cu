@@ -21,15 +21,6 @@
 #else
 #define FQ_ONCE __device__ __noinline__
 #endif
-#ifndef FQ_W4_LO
-// W4 unpack with one shift per word: the k%16 < 8 halves of each 16-column chunk as 1024 + q
-// (bits 0-3), the k%16 >= 8 halves as 64 + q (bits 4-7); the block fold subtracts
-// 1024 X_lo + 64 X_hi (dx.y) instead of 64 X
-#define FQ_W4_LO 0  // opt-in: -5% W4 step, but 15-25x the W4 cancellation error (tools/w4_error_probe.py)
-#endif
-#ifndef FQ_SPLIT_ACC
-#define FQ_SPLIT_ACC 0  // two MMA accumulator chains per block (A/B experiment)
-#endif
 #ifndef FQ_GEMV_HOOKS
 #define FQ_GEMV_HOOKS 1  // per-phase GEMV detail stamps (tools/phase_profile.py); 0 compiles them out
 #endif
@@ -136,11 +127,6 @@ __device__ __forceinline__ float2 ld_volatile_f2(const float2* p) {
   asm volatile("ld.volatile.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
@@ -151,12 +137,6 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 // (v & 0x00F000F0) | 0x54005400 in one LOP3: the two nibbles at bits 4-7 / 20-23 as fp16 64 + q.
 // Written as PTX with both constants immediate so ptxas keeps one in a register instead of
 // splitting the AND and the OR (the W4 unpack is ALU-bound).
-// (v & 0x000F000F) | 0x64006400: the nibbles at bits 0-3 / 16-19 as fp16 1024 + q (no shift).
-__device__ __forceinline__ uint32_t nib_lo_f16(uint32_t v) {
-  uint32_t r;
-  asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(r) : "r"(v));
-  return r;
-}
 __device__ __forceinline__ uint32_t nib_f16(uint32_t v) {
   uint32_t r;
   asm("lop3.b32 %0, %1, 0x00F000F0, 0x54005400, 0xEA;" : "=r"(r) : "r"(v));
@@ -192,19 +172,6 @@ __device__ __forceinline__ void frag_store(__half* frag, int nkb, int b, int64_t
   frag[((static_cast<int64_t>(b) * nkb + kb) * 16 + p * 4 + tig) * 8 + comp * 2 + (r16 & 1)] = __float2half_rn(v);
 }
 
-// Tagged variant: the pair (k, k+1), k even, as one 8-byte word {half2, tag} at word index
-// uint4_index * 4 + comp of the fragment layout (single-copy atomic: the consumer polls the tag).
-__device__ __forceinline__ void frag_store_pair(__half* frag, int nkb, int b, int64_t k, float v0, float v1,
-                                                unsigned int tag) {
-  const int kb = static_cast<int>(k >> 7), r = static_cast<int>(k & 127), j16 = r >> 4, r16 = r & 15;
-  const int p = j16 >> 1, hh = j16 & 1, tig = (r16 & 7) >> 1, comp = 2 * hh + (r16 >> 3);
-  const __half2 h = __floats2half2_rn(v0, v1);
-  const unsigned long long w = static_cast<unsigned long long>(*reinterpret_cast<const uint32_t*>(&h)) |
-                               (static_cast<unsigned long long>(tag) << 32);
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(frag) +
-                            ((static_cast<int64_t>(b) * nkb + kb) * 16 + p * 4 + tig) * 4 + comp;
-  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
-}
 
 // ---------------------------------------------------------------- the block sequence
 // A GEMV phase is a sequence of 16x128 blocks: tile-major, and inside a tile one segment of nkb
@@ -511,14 +478,9 @@ __device__ __forceinline__ void stage_vec(const Phase& P, const GemvSmem& G, uns
         for (int i = 0; i < 4; ++i) dst[4 * i] = hp[i];
       }
       // the 16 vectors of a block sit on 16 consecutive lanes (v is 16-aligned per half-warp)
-      float slo = (c & 1) ? 0.f : sum;  // k % 16 < 8 (the W4 1024-offset halves)
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (FQ_W4_LO) slo += __shfl_xor_sync(0xffffffffu, slo, o);
-      }
-      if (v < nvec && c == 0)
-        G.dx[kb * B + b] = make_float4(1024.f * sum, FQ_W4_LO ? 1024.f * slo + 64.f * (sum - slo) : 64.f * sum, sum, 0.f);
+      for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (v < nvec && c == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
     }
     if (base + NT * VB >= nvec) break;
   }
@@ -539,127 +501,20 @@ __device__ __forceinline__ void frag_block_sums(const Phase& P, const GemvSmem& 
     const uint2 h4 = reinterpret_cast<const uint2*>(G.xs + static_cast<size_t>(blk) * 16)[lane];
     const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h4.x));
     const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h4.y));
-    float lo = a.x + a.y, hi = c.x + c.y;  // h4.x: k % 16 < 8, h4.y: k % 16 >= 8
     float sum = (a.x + a.y) + (c.x + c.y);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (FQ_W4_LO) {
-        lo += __shfl_xor_sync(0xffffffffu, lo, o);
-        hi += __shfl_xor_sync(0xffffffffu, hi, o);
-      }
-    }
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     const int b = blk / nkb, kb = blk - b * nkb;
-    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, FQ_W4_LO ? 1024.f * lo + 64.f * hi : 64.f * sum, sum, 0.f);
+    if (lane == 0) G.dx[kb * B + b] = make_float4(1024.f * sum, 64.f * sum, sum, 0.f);
   }
   named_sync(1, kNCW * 32);
 }
 
-#if FQ_ATTN_MERGE
-// Staging of the O projection's input when the attention phase ran split (attn_splits > 1): each
-// split wrote its unnormalised partial (O[hd] fp32, m, l); this thread's fragment slots load the
-// (k, k+1) pairs of every split (float2 loads, all in flight with the (m, l) loads of the merge
-// weights), then x = sum_s O_s w_s with w_s = e^(m_s - M) / sum_t l_t e^(m_t - M), rounded to the
-// activation dtype as the unsplit attention rounds its output, then fp16 into fragment order.
-constexpr int kMaxAttnSplits = 4;
-constexpr int kMergeSlots = 2;  // uint4 fragment slots per thread per round (K = 4096 at B = 1: 512)
-__device__ __forceinline__ void stage_attn_merge(const Phase& P, const GemvSmem& G, unsigned long long* gp) {
-  const int B = P.B, nkb = P.nkb;
-  const int tid = threadIdx.x;
-  constexpr int NT = kNCW * 32;
-  const int H = P.n_heads, hd = P.head_dim, ns = P.attn_splits;
-  const int64_t pst = hd + 4;
-  const float* parts = P.attn_ws;
-  float* wsm = G.red;  // [b * H + h][ns] merge weights (the reduction window is free while staging)
-  uint32_t* xs32 = reinterpret_cast<uint32_t*>(G.xs);
-  const int n = B * nkb * 16;
-  const int64_t K = P.K;
-  const int adt = P.act_dtype;
-  for (int base = 0; base < n || base == 0; base += NT * kMergeSlots) {
-    float2 o[kMergeSlots][4][kMaxAttnSplits];
-#pragma unroll
-    for (int i = 0; i < kMergeSlots; ++i) {
-      const int u = base + i * NT + tid;
-      const int b = u / (nkb * 16), r = u - b * nkb * 16, kb = r >> 4, p = (r >> 2) & 3, tg = r & 3;
-#pragma unroll
-      for (int comp = 0; comp < 4; ++comp) {
-        const int64_t k = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + (comp >> 1)) + 2 * tg + 8 * (comp & 1);
-        const bool on = u < n && k < K;
-        const int h = on ? static_cast<int>(k / hd) : 0, j = on ? static_cast<int>(k - static_cast<int64_t>(h) * hd) : 0;
-        const float* src = parts + (static_cast<int64_t>(on ? b : 0) * H + h) * ns * pst + j;
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-          o[i][comp][sp] = (on && sp < ns) ? *reinterpret_cast<const float2*>(src + sp * pst) : make_float2(0.f, 0.f);
-      }
-    }
-    if (base == 0) {
-      for (int bh = tid; bh < B * H; bh += NT) {
-        const float* src = parts + static_cast<int64_t>(bh) * ns * pst + hd;
-        float2 ml[kMaxAttnSplits];
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-          ml[sp] = sp < ns ? *reinterpret_cast<const float2*>(src + sp * pst) : make_float2(-INFINITY, 0.f);
-        float M = -INFINITY;
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp) M = fmaxf(M, ml[sp].x);
-        float Lt = 0.f, f[kMaxAttnSplits];
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp) {
-          f[sp] = ml[sp].x == -INFINITY ? 0.f : expf(ml[sp].x - M);
-          Lt += ml[sp].y * f[sp];
-        }
-#pragma unroll
-        for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-          if (sp < ns) wsm[bh * ns + sp] = f[sp] / Lt;
-      }
-      if (gp) gp[1] = gtimer();
-      named_sync(1, NT);
-      if (gp) gp[2] = gtimer();
-    }
-#pragma unroll
-    for (int i = 0; i < kMergeSlots; ++i) {
-      const int u = base + i * NT + tid;
-      if (u >= n) continue;
-      const int b = u / (nkb * 16), r = u - b * nkb * 16, kb = r >> 4, p = (r >> 2) & 3, tg = r & 3;
-#pragma unroll
-      for (int comp = 0; comp < 4; ++comp) {
-        const int64_t k = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + (comp >> 1)) + 2 * tg + 8 * (comp & 1);
-        float v0 = 0.f, v1 = 0.f;
-        if (k < K) {
-          const float* w = wsm + (b * H + static_cast<int>(k / hd)) * ns;
-#pragma unroll
-          for (int sp = 0; sp < kMaxAttnSplits; ++sp)
-            if (sp < ns) {
-              v0 = fmaf(o[i][comp][sp].x, w[sp], v0);
-              v1 = fmaf(o[i][comp][sp].y, w[sp], v1);
-            }
-          v0 = round_act(v0, adt);
-          v1 = round_act(v1, adt);
-        }
-        const __half2 h2 = __floats2half2_rn(v0, v1);
-        xs32[u * 4 + comp] = *reinterpret_cast<const uint32_t*>(&h2);
-      }
-    }
-    if (base + NT * kMergeSlots >= n) break;
-  }
-  named_sync(1, NT);
-  frag_block_sums(P, G);
-}
-#endif  // FQ_ATTN_MERGE
 
 // Staging of an input the producing phase already wrote in fragment order: a straight copy (all
 // loads of the phase in flight together), then the per-block sums dx from shared memory (one warp
 // per 128-block: four halves per lane, shuffle tree).
 constexpr int kCopyVec = 6;  // uint4s per thread per round (K = 11008 at B = 1: 1376 -> one round)
-constexpr int kTagWords = 16;
-#ifndef FQ_POLL_NS
-#define FQ_POLL_NS 256
-#endif  // tagged words per thread per round (K = 11008 at B = 1: 5504 -> one round)
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 #ifndef FQ_COPY_INLINE
 #define FQ_COPY_INLINE 1  // measured -1.8% per step vs an out-of-line call
 #endif
@@ -670,62 +525,10 @@ __device__ __noinline__
 #endif
 void stage_frag_copy(const Phase& P, const GemvSmem& G, unsigned long long* gp, unsigned int tag) {
   const int B = P.B, nkb = P.nkb;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   constexpr int NT = kNCW * 32;
   const int n = B * nkb * 16;
-  if (FQ_TAGS_DEV && P.xfrag_tagged) {
-    // no grid barrier before this phase: every word is polled until it carries the producing
-    // phase's tag (words past K are the zero padding and never written)
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(P.xfrag);
-    uint32_t* xs32 = reinterpret_cast<uint32_t*>(G.xs);
-    const int nw = n * 4;
-    const int64_t K = P.K;
-    // one poller per warp first (lane 0, on the warp's last word, backing off), so the grid does not
-    // flood the L2 slices holding the activations while their producers are still writing them
-    if (lane == 0) {
-      const int wl = min(nw - 1, (warp + 1) * 32 - 1 + (((nw - 1) / NT) * NT));
-      const int u = wl >> 2, comp = wl & 3, r = u % (nkb * 16);
-      const int64_t k = static_cast<int64_t>(r >> 4) * kBlockK + 16 * (2 * ((r >> 2) & 3) + (comp >> 1)) + 2 * (r & 3) + 8 * (comp & 1);
-      if (k < K) {
-        const unsigned long long t0 = gtimer_now();
-        while (static_cast<unsigned int>(ld_relaxed_u64(src + wl) >> 32) != tag) {
-          __nanosleep(FQ_POLL_NS);
-          if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("tagged activation (warp poll)", wl, static_cast<int>(tag));
-        }
-      }
-    }
-    __syncwarp();
-    for (int base = 0; base < nw; base += NT * kTagWords) {
-      unsigned long long v[kTagWords];
-#pragma unroll
-      for (int s = 0; s < kTagWords; ++s) {
-        const int w = base + s * NT + tid;
-        v[s] = w < nw ? ld_relaxed_u64(src + w) : 0ull;
-      }
-#pragma unroll
-      for (int s = 0; s < kTagWords; ++s) {
-        const int w = base + s * NT + tid;
-        if (w >= nw) continue;
-        const int u = w >> 2, comp = w & 3, r = u % (nkb * 16);
-        const int kb = r >> 4, p = (r >> 2) & 3, tg = r & 3;
-        const int64_t k = static_cast<int64_t>(kb) * kBlockK + 16 * (2 * p + (comp >> 1)) + 2 * tg + 8 * (comp & 1);
-        if (k >= K) {
-          xs32[w] = 0u;
-          continue;
-        }
-        if (static_cast<unsigned int>(v[s] >> 32) != tag) {
-          const unsigned long long t0 = gtimer_now();
-          do {
-            __nanosleep(FQ_POLL_NS);
-            v[s] = ld_relaxed_u64(src + w);
-            if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("tagged activation", w, static_cast<int>(tag));
-          } while (static_cast<unsigned int>(v[s] >> 32) != tag);
-        }
-        xs32[w] = static_cast<uint32_t>(v[s]);
-      }
-    }
-  }
-  for (int base = 0; !(FQ_TAGS_DEV && P.xfrag_tagged) && base < n; base += NT * kCopyVec) {
+  for (int base = 0; base < n; base += NT * kCopyVec) {
     uint4 v[kCopyVec];
 #pragma unroll
     for (int s = 0; s < kCopyVec; ++s) {
@@ -767,14 +570,7 @@ __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long
     stage_vec<4, true, true>(P, G, gp, pv);
     return;
   }
-  if (P.attn_splits > 1) {
-#if FQ_ATTN_MERGE
-    stage_attn_merge(P, G, gp);
-    return;
-#else
-    __trap();  // the builder only splits attention when the merge is compiled in
-#endif
-  }
+  if (P.attn_splits > 1) __trap();  // the builder never splits attention (measured slower)
   const bool vnorm = P.norm_gain != nullptr;
   if (FQ_VEC_STAGE && stage_vec_ok(P) && vnorm == (P.x_dtype == FQ_DT_F32)) {
     const bool norm = vnorm;
@@ -898,7 +694,7 @@ __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long
         hi += __shfl_xor_sync(0xffffffffu, hi, o);
       }
       if (active && (rem & 15) == 0)
-        G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), FQ_W4_LO ? 1024.f * lo + 64.f * hi : 64.f * (lo + hi), lo + hi, 0.f);
+        G.dx[kb * B + b] = make_float4(1024.f * (lo + hi), 64.f * (lo + hi), lo + hi, 0.f);
     }
     if (base + NT * kStageItems >= items) break;
   }
@@ -922,17 +718,6 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
   for (int n = 0; n < NBLK; ++n)
 #pragma unroll
     for (int e = 0; e < 4; ++e) c[n][e] = 0.f;
-#if FQ_SPLIT_ACC
-  // second accumulator set: each block's 8 dependent MMAs become two chains of 4
-  float c2[NBLK][4];
-#pragma unroll
-  for (int n = 0; n < NBLK; ++n)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) c2[n][e] = 0.f;
-#define FQ_ACC2 c2
-#else
-#define FQ_ACC2 c
-#endif
   if constexpr (W == 0) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -942,7 +727,7 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
         const uint4 xv = xl[n * kXBlk + p * 4];
         mma16816(c[n], prmt(wv.x, 0x64646464u, 0x4140u), prmt(wv.x, 0x64646464u, 0x4342u),
                  prmt(wv.y, 0x64646464u, 0x4140u), prmt(wv.y, 0x64646464u, 0x4342u), xv.x, xv.y);
-        mma16816(FQ_ACC2[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
+        mma16816(c[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
                  prmt(wv.w, 0x64646464u, 0x4140u), prmt(wv.w, 0x64646464u, 0x4342u), xv.z, xv.w);
       }
     }
@@ -960,24 +745,13 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
           // every nibble pair is moved to bits 4-7 / 20-23 of the halves: fp16 0x5400 | q<<4 = 64 + q
           const uint32_t q = qs[u];
           const uint4 xv = u < 2 ? x0 : x1;
-          float (&acc)[4] = (u & 1) ? FQ_ACC2[n] : c[n];
-          if (FQ_W4_LO)
-            mma16816(acc, nib_lo_f16(q), nib_lo_f16(q >> 8), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
-                     (u & 1) ? xv.w : xv.y);
-          else
-          mma16816(acc, nib_f16(q << 4), nib_f16(q >> 4), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
+          mma16816(c[n], nib_f16(q << 4), nib_f16(q >> 4), nib_f16(q), nib_f16(q >> 8), (u & 1) ? xv.z : xv.x,
                    (u & 1) ? xv.w : xv.y);
         }
       }
     }
   }
-#if FQ_SPLIT_ACC
-#pragma unroll
-  for (int n = 0; n < NBLK; ++n)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) c[n][e] += c2[n][e];
-#endif
-#undef FQ_ACC2
+
   constexpr int cbytes = W == 0 ? 2048 : 1024;
 #pragma unroll
   for (int n = 0; n < NBLK; ++n) {
@@ -1195,27 +969,6 @@ __device__ void reduce_window(const Phase& P, const PhaseCtl& C, const GemvSmem&
     } else {
       gemv_epilogue(P, C.tile0 + l, i / B, i % B, v, sqb, st);
     }
-    if (FQ_TAGS_DEV && P.epi == EPI_SWIGLU && P.yfrag != nullptr && P.yfrag_nkb < 0 && ((i / B) & 1) == 0) {
-      // tagged fragment output: the even row of each pair also sums the odd row's partials (same
-      // tile, item i + B) and writes both as one (half2, tag) word
-      const int64_t row = (C.tile0 + l) * static_cast<int64_t>(kTileRows) + i / B;
-      if (row < P.N) {
-        float o2 = 0.f;
-        if (row + 1 < P.N) {
-          float g2 = 0.f, u2 = 0.f;
-          const float* r0 = G.red + (static_cast<size_t>(((l - lo) * nmat) * kNCW)) * per + i + B;
-#pragma unroll
-          for (int w = 0; w < kNCW; ++w) {
-            g2 += r0[w * per];
-            u2 += r0[(kNCW + w) * per];
-          }
-          o2 = round_act(g2 / (1.0f + expf(-g2)) * u2, P.act_dtype);
-        }
-        const float gt = v[0];
-        const float o1 = round_act(gt / (1.0f + expf(-gt)) * v[1], P.act_dtype);
-        frag_store_pair(P.yfrag, -P.yfrag_nkb, i % B, row, o1, o2, C.tag);
-      }
-    }
   }
   named_sync(1, kNCW * 32);  // the window's slots are rewritten next
 }
@@ -1352,25 +1105,6 @@ struct AheadWalk {
   }
 };
 
-// The KV rows the next attention phase reads on this CTA (decode: one (row, head) item per CTA)
-// are prefetched into L2 when the producer starts the GEMV phase before it, so the attention's
-// loads hit L2 instead of HBM (the cache region of a head is contiguous: rows 0..pos).
-#ifndef FQ_KV_PREFETCH
-#define FQ_KV_PREFETCH 0  // measured: attention -20 us but GEMV phases +30 us per step
-#endif
-__device__ __forceinline__ void prefetch_attn_kv(const Phase& A) {
-  if (A.type != PH_ATTN || A.appended || A.attn_splits > 1) return;
-  const int H = A.n_heads, hd = A.head_dim;
-  for (int item = blockIdx.x; item < A.B * H; item += gridDim.x) {
-    const int b = item / H, h = item - b * H;
-    const int pos = A.pos[b];
-    const __half* kc = A.kv + A.slots[b] * A.slot_stride + A.layer_off + static_cast<int64_t>(h) * A.max_seq * hd;
-    const uint32_t bytes = static_cast<uint32_t>(pos + 1) * hd * 2;  // a multiple of 16
-    prefetch_l2(kc, bytes);
-    prefetch_l2(kc + static_cast<int64_t>(H) * A.max_seq * hd, bytes);
-  }
-}
-
 __device__ void produce_table(const Phase* phases, int nphases, const CtlEntry* ctab, const Ring R,
                               unsigned long long* tr, const uint8_t** s_base, bool noload, int prefetch,
                               const uint8_t** s_base2) {
@@ -1391,7 +1125,6 @@ __device__ void produce_table(const Phase* phases, int nphases, const CtlEntry* 
   while (ph < nphases) {
     const int phn = next_gemv_phase(ctab, ph + 1, nphases);
     if (phn < nphases) prod_load(phases[phn], nxt);  // in flight while this phase streams
-    if (FQ_KV_PREFETCH && ph + 1 < nphases) prefetch_attn_kv(phases[ph + 1]);
     const CtlEntry& E = ctab[ph];
     const int nseg = E.nseg, nkb = cur.nkb;
 #pragma unroll
@@ -1610,10 +1343,7 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
 #endif
       const uint8_t* slot = R.base + static_cast<size_t>(slot_i) * kStageBytes;
       const float4* dxa = G.dx + static_cast<size_t>(kb) * B + 2 * tig;
-#ifndef FQ_SKIP_MMA
-#define FQ_SKIP_MMA 0  // profiling A/B only: consumers release stages without computing
-#endif
-      for (int j = warp; j < (FQ_SKIP_MMA ? 0 : nb); j += 2 * kNCW) {
+      for (int j = warp; j < nb; j += 2 * kNCW) {
         const uint8_t* bk = slot + j * bsz;
         const uint4* xj = xl + (kb + j) * 16;
         const float4* dj = dxa + j * B;
@@ -1701,12 +1431,6 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     }
   }
   named_sync(1, kNCW * 32);  // staging / reduction buffers and C are reused by the next phase
-  if (FQ_HEAD_FLAGS_DEV && P.tile_flags != nullptr && threadIdx.x == 0 && C.ntiles > 0) {
-    // every epilogue store of this CTA's tiles is ordered before the stamps (bar.sync + fence)
-    __threadfence();
-    for (int l = 0; l < C.ntiles; ++l)
-      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(P.tile_flags + C.tile0 + l), "r"(tag) : "memory");
-  }
   if (gp) gp[6] = gtimer();
 }
 
@@ -1921,21 +1645,6 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
   const int nch = (pos + kAttnChunk) / kAttnChunk;
   const int c0 = (nch * sp) / ns, c1 = (nch * (sp + 1)) / ns;
   const int64_t qoff = static_cast<int64_t>(b) * H * hd + h * hd + DPL * lane;
-  if (FQ_HEAD_FLAGS_DEV && P.tile_flags != nullptr) {
-    // no grid barrier after the QKV phase: wait for the head's hd / 16 tiles of q / k / v only
-    const int fph = hd / 16;
-    const unsigned int want = tag - 1;  // the QKV phase precedes this one
-    const unsigned long long t0 = gtimer_now();
-    for (;;) {
-      unsigned int f = want;
-      if (lane < fph)
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.tile_flags + h * fph + lane) : "memory");
-      if (__all_sync(0xffffffffu, f == want)) break;
-      __nanosleep(32);
-      if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("head tile flags", h, static_cast<int>(want));
-    }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  }
   float q[DPL];
   float M = -INFINITY, L = 0.f, O[DPL];
 #pragma unroll
@@ -2004,12 +1713,6 @@ __device__ void attn_head(const Phase& P, int b, int h, int sp, int ns, int lane
         const float o = round_act(Ot[e] / Lt, P.act_dtype);
         store_out(P.attn_out, P.act_dtype, qoff + e, o);
         if (P.yfrag && P.yfrag_nkb > 0) frag_store(P.yfrag, P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e, o);
-      }
-      if (FQ_TAGS_DEV && P.yfrag && P.yfrag_nkb < 0) {
-#pragma unroll
-        for (int e = 0; e < DPL; e += 2)
-          frag_store_pair(P.yfrag, -P.yfrag_nkb, b, static_cast<int64_t>(h) * hd + DPL * lane + e,
-                          round_act(Ot[e] / Lt, P.act_dtype), round_act(Ot[e + 1] / Lt, P.act_dtype), tag);
       }
     } else {
       float* part = P.attn_ws + ((static_cast<int64_t>(b) * H + h) * ns + sp) * (hd + 4);
@@ -2110,9 +1813,6 @@ FQ_ONCE void run_stats(const Phase& P) {
 // Grid barrier (consumer threads): arrival counter in global memory, reset before every launch.
 // Arrival is one release reduction (no returned value to wait for); the poll is relaxed (an
 // acquire load per iteration would invalidate L1 each time) and one acquire fence follows it.
-#ifndef FQ_OLD_BARRIER
-#define FQ_OLD_BARRIER 0
-#endif
 __device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -2123,20 +1823,11 @@ __device__ void grid_barrier(unsigned int* counter, unsigned int& epoch) {
   if (threadIdx.x == 0) {
     const unsigned int target = (++epoch) * gridDim.x;
     const unsigned long long t0 = gtimer_now();
-    if (FQ_OLD_BARRIER) {
-      __threadfence();
-      atomicAdd(counter, 1u);
-      while (ld_acquire(counter) < target) {
-        if (gtimer_now() - t0 > kWatchdogNs) watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_acquire(counter)));
-      }
-      __threadfence();
-    } else {
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
-      for (uint32_t spins = 0; ld_relaxed(counter) < target; ++spins)
-        if ((spins & 255u) == 255u && gtimer_now() - t0 > kWatchdogNs)
-          watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_relaxed(counter)));
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+    for (uint32_t spins = 0; ld_relaxed(counter) < target; ++spins)
+      if ((spins & 255u) == 255u && gtimer_now() - t0 > kWatchdogNs)
+        watchdog_fire("grid barrier", static_cast<int>(target), static_cast<int>(ld_relaxed(counter)));
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   } else {
     ++epoch;
   }
