@@ -174,6 +174,10 @@ class Model {
   // Lower-level batched step used by the engine: one decode step for `slots`, per-row
   // statistics only (no logits copy).  Returns the rows' statistics.
   std::vector<fq_row_stats> decode_rows(std::span<const int32_t> slots, std::span<const TokenId> tokens);
+  // Single-row llama decode steps with the device phase clock on: step_stats() then carries the
+  // per-precision linear time and the step's device time measured on the device
+  // (fq_model_decode_timed) instead of the step time split by bytes.
+  void set_device_timed_buckets(bool on) { timed_buckets_ = on; }
   std::vector<fq_row_stats> prefill_rows(int slot, std::span<const TokenId> tokens);
 
  private:
@@ -185,6 +189,7 @@ class Model {
   std::vector<std::string> ids_;
   std::vector<MultiPrecisionLayer> layers_;
   mutable StepStats stats_;
+  bool timed_buckets_ = false;
 };
 
 double effective_bits(std::span<const MultiPrecisionLayer* const> layers);

@@ -235,6 +235,12 @@ fq_status fq_model_prefill(fq_model* model, int32_t slot, const int32_t* tokens_
  * replayed from a captured CUDA graph. logits_dev optional [batch, V] copy-out. */
 fq_status fq_model_decode(fq_model* model, int32_t batch, const int32_t* slots_host,
                           const int32_t* tokens_host, float* logits_dev, fq_row_stats* stats_host);
+/* fq_model_decode for one slot with the device phase clock on: also returns the step's device
+ * time split by precision (ns_by_rung[FQ_RUNG_*]: each GEMV phase's time shared among its
+ * linears by bytes) and the whole step (*ns_step); the remainder is embedding, attention over the
+ * cache and the statistics.  The trace's latency breakdown (src/engine.cpp:214-233) in device time. */
+fq_status fq_model_decode_timed(fq_model* model, int32_t slot, int32_t token, float* logits_dev,
+                                fq_row_stats* stats_host, uint64_t* ns_by_rung, uint64_t* ns_step);
 /* Device time of the decode-step program kernels (CUDA events recorded around the launch inside
  * the step graph): total ms and number of steps since the last reset (reset != 0 clears after
  * reading).  bench.py's roofline divides the step's algorithmic bytes by this per-launch time. */

@@ -322,6 +322,10 @@ struct fq_model {
   // batched tensor-core steps: captured graphs per (copies per linear, B) signature
   std::map<std::string, std::pair<cudaGraphExec_t, int64_t>> batch_graphs;
   std::set<std::string> batch_seen;
+  // device-timed latency buckets (fq_model_decode_timed): phase clock buffer and phase -> linears
+  unsigned long long* timed_ticks = nullptr;
+  int64_t timed_ticks_n = 0;
+  std::vector<std::vector<int>> timed_roles;
   // device time of the step program kernels (events around the launch, captured into the graph)
   cudaEvent_t ev_prog[2] = {nullptr, nullptr};
   double prog_ms = 0.0;
@@ -397,6 +401,7 @@ void sync_weight_epoch(fq_model* M) {
     M->programs.clear();
     M->batch_graphs.clear();
     M->batch_seen.clear();
+    M->timed_roles.clear();
   }
   M->built_epoch = M->ctx->weight_epoch;
 }
@@ -1289,6 +1294,7 @@ fq_status fq_model_destroy(fq_model* M) {
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
     for (auto& kv : M->batch_graphs) cudaGraphExecDestroy(kv.second.first);
     dfree(M->grid_barrier);
+    dfree(M->timed_ticks);
     free_prefill_ws(M);
     for (cudaEvent_t e : M->ev_prog)
       if (e) cudaEventDestroy(e);
@@ -1630,6 +1636,94 @@ fq_status fq_model_profile_step(fq_model* M, int32_t slot, int32_t token, uint64
         for (int i = 0; i < run.nphases; ++i) ph[i] = run.inl.phases[i];
       for (int i = 0; i < run.nphases; ++i) phase_types_host[i] = ph[i].type;
     }
+    M->slot_len[slot] += 1;
+  });
+}
+
+// One B = 1 decode step with the per-phase device clock on (the program's phase hooks): the step's
+// device time split into the linears' precision buckets -- each GEMV phase's duration (barrier
+// release to barrier release, max over CTAs) shared among its linears by their bytes at the
+// slot's rungs -- and the rest (embedding, attention over the cache, statistics).  The trace's
+// latency breakdown in device time instead of a byte-proportional split (src/engine.cpp:214-233).
+fq_status fq_model_decode_timed(fq_model* M, int32_t slot, int32_t token, float* logits_dev, fq_row_stats* stats_host,
+                                uint64_t* ns_by_rung, uint64_t* ns_step) {
+  return guarded([&] {
+    require(M && stats_host && ns_by_rung && ns_step, FQ_E_INPUT, "null argument");
+    require(M->llama, FQ_E_CONFIG, "decode_timed: llama arch only");
+    fq_ctx* ctx = M->ctx;
+    cudaStream_t st = ctx->stream;
+    sync_weight_epoch(M);
+    if (M->programs.find(std::make_pair(1, 0)) == M->programs.end()) {
+      // first use builds the program: run this step unprofiled, then account it byte-proportionally
+      model_step(M, 1, &slot, &token, logits_dev, stats_host);
+      ns_by_rung[0] = ns_by_rung[1] = ns_by_rung[2] = 0;
+      *ns_step = 0;
+      return;
+    }
+    stage_rows(M, 1, &slot, &token);
+    const ProgramRun& run = M->programs.at(std::make_pair(1, 0));
+    const int64_t n = (static_cast<int64_t>(run.nphases) * 2 + 1) * run.grid;
+    if (M->timed_ticks_n < n) {
+      dfree(M->timed_ticks);
+      M->timed_ticks = static_cast<unsigned long long*>(dmalloc(sizeof(uint64_t) * n));
+      M->timed_ticks_n = n;
+    }
+    if (M->timed_roles.size() != static_cast<size_t>(run.nphases)) {
+      // per phase: the linears of a GEMV phase (matched by their W8 tile pointers), or none
+      std::vector<Phase> ph(run.nphases);
+      if (run.dev_phases)
+        FQ_CUDA(cudaMemcpy(ph.data(), run.dev_phases, sizeof(Phase) * run.nphases, cudaMemcpyDeviceToHost));
+      else
+        for (int i = 0; i < run.nphases; ++i) ph[i] = run.inl.phases[i];
+      M->timed_roles.assign(run.nphases, {});
+      for (int i = 0; i < run.nphases; ++i) {
+        if (ph[i].type != PH_GEMV) continue;
+        for (int m = 0; m < ph[i].nmat; ++m)
+          for (int li = 0; li < M->n_lin; ++li)
+            if (M->lin[li]->r8.tiles != nullptr && M->lin[li]->r8.tiles == ph[i].mat[m].tiles[0])
+              M->timed_roles[i].push_back(li);
+      }
+    }
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    FQ_CUDA(cudaMemsetAsync(M->timed_ticks, 0, sizeof(uint64_t) * n, st));
+    FQ_CUDA(cudaStreamSynchronize(st));
+    set_phase_profile(M->timed_ticks);
+    try {
+      enqueue_step(M, 1);
+      FQ_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      set_phase_profile(nullptr);
+      throw;
+    }
+    set_phase_profile(nullptr);
+    std::vector<uint64_t> t(static_cast<size_t>(n));
+    FQ_CUDA(cudaMemcpy(t.data(), M->timed_ticks, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+    FQ_CUDA(cudaMemcpy(stats_host, M->stats_dev, sizeof(fq_row_stats), cudaMemcpyDeviceToHost));
+    if (logits_dev)
+      FQ_CUDA(cudaMemcpy(logits_dev, M->logits, sizeof(float) * M->cfg.vocab_size, cudaMemcpyDeviceToDevice));
+    const int G = run.grid;
+    uint64_t prev = ~0ull;
+    for (int c = 0; c < G; ++c) prev = std::min<uint64_t>(prev, t[static_cast<size_t>(run.nphases) * G * 2 + c]);
+    const uint64_t t0 = prev;
+    double acc[3] = {0, 0, 0}, other = 0;
+    const uint8_t* rung = &M->rungs[static_cast<size_t>(slot) * M->n_lin];
+    for (int i = 0; i < run.nphases; ++i) {
+      uint64_t rel = 0;
+      for (int c = 0; c < G; ++c) rel = std::max<uint64_t>(rel, t[(static_cast<size_t>(i) * G + c) * 2 + 1]);
+      const double dur = rel > prev ? static_cast<double>(rel - prev) : 0.0;
+      prev = std::max(prev, rel);
+      const std::vector<int>& ls = M->timed_roles[static_cast<size_t>(i)];
+      if (ls.empty()) {
+        other += dur;
+        continue;
+      }
+      double tot = 0;
+      for (int li : ls) tot += static_cast<double>(M->lin[li]->N * M->lin[li]->K) * (rung[li] == FQ_RUNG_INT4 ? 4 : 8);
+      for (int li : ls)
+        acc[rung[li]] += dur * static_cast<double>(M->lin[li]->N * M->lin[li]->K) * (rung[li] == FQ_RUNG_INT4 ? 4 : 8) / tot;
+    }
+    for (int r = 0; r < 3; ++r) ns_by_rung[r] = static_cast<uint64_t>(acc[r]);
+    *ns_step = prev > t0 ? prev - t0 : 0;
     M->slot_len[slot] += 1;
   });
 }

@@ -240,7 +240,14 @@ PYBIND11_MODULE(_flexquant, m) {
       .def_readwrite("eos_token", &GenerationConfig::eos_token)
       .def_readwrite("scheduler", &GenerationConfig::scheduler)
       .def_readwrite("start_rung", &GenerationConfig::start_rung)
-      .def_readwrite("trace_path", &GenerationConfig::trace_path);
+      .def_readwrite("trace_path", &GenerationConfig::trace_path)
+      .def_readwrite("device_timed_buckets", &GenerationConfig::device_timed_buckets);
+  py::class_<StepStats>(m, "StepStats")
+      .def_readonly("weight_bytes", &StepStats::weight_bytes)
+      .def_readonly("ns_fp", &StepStats::ns_fp)
+      .def_readonly("ns_int8", &StepStats::ns_int8)
+      .def_readonly("ns_int4", &StepStats::ns_int4)
+      .def_readonly("ns_forward", &StepStats::ns_forward);
   py::class_<TraceRecord>(m, "TraceRecord")
       .def_readonly("token_index", &TraceRecord::token_index)
       .def_readonly("token_id", &TraceRecord::token_id)
@@ -250,7 +257,8 @@ PYBIND11_MODULE(_flexquant, m) {
       .def_readonly("effective_bits", &TraceRecord::effective_bits)
       .def_readonly("weight_bytes_touched", &TraceRecord::weight_bytes_touched)
       .def_readonly("elapsed_ns", &TraceRecord::elapsed_ns)
-      .def_readonly("switch_events", &TraceRecord::switch_events);
+      .def_readonly("switch_events", &TraceRecord::switch_events)
+      .def_readonly("buckets", &TraceRecord::buckets);
   py::class_<DecodeTrace>(m, "DecodeTrace")
       .def_readonly("records", &DecodeTrace::records)
       .def("to_jsonl", [](const DecodeTrace& t) {

@@ -76,6 +76,11 @@ std::vector<GenerationResult> run_generation(std::span<const std::vector<TokenId
     if (static_cast<int64_t>(p.size()) > mc.max_seq_len) throw CapacityError("generate: prompt longer than max sequence length");
   }
   validate_plan(plan, model, cfg.start_rung);
+  model.set_device_timed_buckets(cfg.device_timed_buckets);
+  struct TimedOff {
+    Model& m;
+    ~TimedOff() { m.set_device_timed_buckets(false); }
+  } timed_off{model};
   std::vector<Seq> seqs;
   seqs.reserve(prompts.size());
   for (size_t i = 0; i < prompts.size(); ++i) {

@@ -292,3 +292,34 @@ def test_latency_breakdown_c11_analogue():
     print(fq.traffic_report(r.trace))
     assert abs(rep.bucket_sum_over_total - 1.0) <= 0.05
     assert rep.ppl_share < 0.02
+
+
+@pytest.mark.gpu
+def test_latency_breakdown_device_timed_llama():
+    """The c11 analogue with device-timed buckets on the llama engine: each decode step's linear
+    time comes from the program's phase clock, split by precision (fq_model_decode_timed); the
+    buckets still sum to the step time within 5% and the W4 bucket grows as layers switch."""
+    m = _llama(max_batch=1)
+    ids = m.linear_ids()
+    plan = fq.SwitchPlan()
+    ents = []
+    for lid in ids:
+        e = fq.SwitchEntry()
+        e.layer_id, e.from_, e.to, e.kl = lid, fq.Rung.Int8, fq.Rung.Int4, 0.0
+        ents.append(e)
+    plan.entries = ents
+    cfg = fq.GenerationConfig()
+    cfg.max_new_tokens = 60
+    cfg.start_rung = fq.Rung.Int8
+    cfg.scheduler.threshold_mode = fq.ThresholdMode.Absolute
+    cfg.scheduler.theta = float("inf")
+    cfg.scheduler.window_len = 4
+    cfg.scheduler.layers_per_switch = 4
+    cfg.device_timed_buckets = True
+    r = fq.generate(oracle.random_tokens(12, 8192, 3), m, plan, cfg)
+    rep = fq.traffic_report_struct(r.trace)
+    print(fq.traffic_report(r.trace))
+    assert abs(rep.bucket_sum_over_total - 1.0) <= 0.05
+    assert rep.ppl_share < 0.02
+    late = r.trace.records[-1].buckets
+    assert late.ns_int4 > 0 and late.ns_int8 == 0  # every linear switched to W4 by then
