@@ -705,13 +705,10 @@ __device__ void stage_acts(const Phase& P, const GemvSmem& G, unsigned long long
 // the unpacked codes, then the per-row group fold y += s * (acc - (D + z*X)) for the columns
 // (batch rows) that use this copy.  xl: this lane's B-fragment base for the first block (null
 // when its column is past the batch); blocks are kbs apart in the block sequence.
-#ifndef FQ_XPRED
-#define FQ_XPRED 0  // lanes of batch columns past B skip their activation loads (A/B)
-#endif
 template <int W, int NBLK>
 __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, const uint4* __restrict__ xl,
                                             const float4* __restrict__ dxa, int dxstep, int lane,
-                                            bool ca, bool cb_, float zmagic, float (&y)[4], bool xok = true) {
+                                            bool ca, bool cb_, float zmagic, float (&y)[4]) {
   const int g = lane >> 2;
   // blocks j and j + kNCW of a stage: codes kNCW blocks apart, activations kNCW * 16 uint4s apart
   constexpr int bstride = (W == 0 ? kBlockBytes8 : kBlockBytes4) * kNCW;
@@ -727,8 +724,7 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
 #pragma unroll
       for (int n = 0; n < NBLK; ++n) {
         const uint4 wv = reinterpret_cast<const uint4*>(blk + n * bstride)[p * 32 + lane];
-        uint4 xv = make_uint4(0u, 0u, 0u, 0u);
-        if (!FQ_XPRED || xok) xv = xl[n * kXBlk + p * 4];
+        const uint4 xv = xl[n * kXBlk + p * 4];
         mma16816(c[n], prmt(wv.x, 0x64646464u, 0x4140u), prmt(wv.x, 0x64646464u, 0x4342u),
                  prmt(wv.y, 0x64646464u, 0x4140u), prmt(wv.y, 0x64646464u, 0x4342u), xv.x, xv.y);
         mma16816(c[n], prmt(wv.z, 0x64646464u, 0x4140u), prmt(wv.z, 0x64646464u, 0x4342u),
@@ -741,11 +737,8 @@ __device__ __forceinline__ void gemv_blocks(const uint8_t* __restrict__ blk, con
 #pragma unroll
       for (int n = 0; n < NBLK; ++n) {
         const uint4 wv = reinterpret_cast<const uint4*>(blk + n * bstride)[i * 32 + lane];
-        uint4 x0 = make_uint4(0u, 0u, 0u, 0u), x1 = x0;
-        if (!FQ_XPRED || xok) {
-          x0 = xl[n * kXBlk + (2 * i) * 4];
-          x1 = xl[n * kXBlk + (2 * i + 1) * 4];
-        }
+        const uint4 x0 = xl[n * kXBlk + (2 * i) * 4];
+        const uint4 x1 = xl[n * kXBlk + (2 * i + 1) * 4];
         const uint32_t qs[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1307,7 +1300,6 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
     const int g = lane >> 2, tig = lane & 3;
     // lanes of batch columns past B read column B-1 (valid data; those MMA columns are ignored)
     const uint4* xl = G.xs + static_cast<size_t>(min(g, B - 1)) * P.nkb * 16 + tig;
-    const bool xok = g < B;  // FQ_XPRED: only the lanes of present batch columns load activations
     const bool ca0 = 2 * tig < B, cb0 = 2 * tig + 1 < B;
     float y[kMaxMat][4], yc[4];
 #pragma unroll
@@ -1356,11 +1348,11 @@ __device__ void run_gemv_phase(const Phase& P, const Ring R, const GemvSmem& G, 
         const uint4* xj = xl + (kb + j) * 16;
         const float4* dj = dxa + j * B;
         if (j + kNCW < nb) {
-          if (w == 0) gemv_blocks<0, 2>(bk, xj, dj, kNCW * B, lane, ca, cb, zm, yc, xok);
-          else gemv_blocks<1, 2>(bk, xj, dj, kNCW * B, lane, ca, cb, zm, yc, xok);
+          if (w == 0) gemv_blocks<0, 2>(bk, xj, dj, kNCW * B, lane, ca, cb, zm, yc);
+          else gemv_blocks<1, 2>(bk, xj, dj, kNCW * B, lane, ca, cb, zm, yc);
         } else {
-          if (w == 0) gemv_blocks<0, 1>(bk, xj, dj, 0, lane, ca, cb, zm, yc, xok);
-          else gemv_blocks<1, 1>(bk, xj, dj, 0, lane, ca, cb, zm, yc, xok);
+          if (w == 0) gemv_blocks<0, 1>(bk, xj, dj, 0, lane, ca, cb, zm, yc);
+          else gemv_blocks<1, 1>(bk, xj, dj, 0, lane, ca, cb, zm, yc);
         }
       }
       __syncwarp();
