@@ -3,8 +3,6 @@
 #include <vector>
 #include "fq_internal.cuh"
 
-#include <cstdlib>
-
 #include <cstring>
 #include <string>
 
@@ -316,11 +314,6 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t batch, c
     const bool fast = numerics == FQ_NUMERICS_FAST && gemv_fast_supported(L, rung) && L->bias == nullptr;
     if (!fast) {
       launch_gemv_exact(ctx, L, rung, batch, x_dev, x_dtype, y_dev, y_dtype);
-      return;
-    }
-    if (gemv_direct_rows(L->K) >= 1 && std::getenv("FQ_GEMV_PROGRAM") == nullptr) {
-      // one ordinary launch (gemv_direct.cu): no persistent-program start-up for a single call
-      launch_gemv_direct(ctx, L, rung, batch, x_dev, x_dtype, L->K, y_dev, y_dtype, L->N);
       return;
     }
     GemvLaunch g;

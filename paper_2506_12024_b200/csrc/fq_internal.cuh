@@ -175,10 +175,6 @@ int gemv_fast_grid(const fq_ctx* ctx, int64_t N);
 // out_n_partials must be >= #SM x 4).
 int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);
 double time_gemv_chain(fq_ctx* ctx, const GemvLaunch* gs, int n, int reps);
-// stand-alone fq_gemv (FAST numerics): one ordinary launch per <= gemv_direct_rows(K) batch rows
-int gemv_direct_rows(int64_t K);
-void launch_gemv_direct(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x, int x_dtype,
-                        int64_t x_stride, void* y, int y_dtype, int64_t y_stride);
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
                        int x_dtype, void* y, int y_dtype);
 
