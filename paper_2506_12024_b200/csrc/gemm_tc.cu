@@ -250,16 +250,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % kInStages, kb = kb0 + i;
-        if (i >= kInStages) mbar_wait(&in_empty[s], ((i / kInStages) - 1) & 1, 0);
-        mbar_expect_tx(&in_full[s], kBBytes + 8 * bb);
-        bulk_g2s(b_ring + s * kBBytes, xt + b_src + static_cast<int64_t>(kb) * kTileBytes, kBBytes, &in_full[s]);
+      auto weights = [&](int s, int kb) {
 #pragma unroll 1
         for (int r = 0; r < 8; ++r) {
           const int64_t tile = min(tile0 + r, static_cast<int64_t>(n_tiles) - 1);  // rows past N masked at store
           bulk_g2s(raw_ring + s * kRawBytes + r * bb, tiles + (tile * nkb + kb) * bb, bb, &in_full[s]);
         }
+      };
+      // the weights do not depend on the previous kernel: the first stages' blocks go out before
+      // the programmatic-dependency wait (the launch overlaps the previous kernel's tail), the
+      // activation tiles only after it
+      const int pre = min(nk, kInStages);
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&in_full[i], kBBytes + 8 * bb);
+        weights(i, kb0 + i);
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int i = 0; i < pre; ++i)
+        bulk_g2s(b_ring + i * kBBytes, xt + b_src + static_cast<int64_t>(kb0 + i) * kTileBytes, kBBytes, &in_full[i]);
+      for (int i = pre; i < nk; ++i) {
+        const int s = i % kInStages, kb = kb0 + i;
+        mbar_wait(&in_empty[s], ((i / kInStages) - 1) & 1, 0);
+        mbar_expect_tx(&in_full[s], kBBytes + 8 * bb);
+        bulk_g2s(b_ring + s * kBBytes, xt + b_src + static_cast<int64_t>(kb) * kTileBytes, kBBytes, &in_full[s]);
+        weights(s, kb);
       }
     }
   } else if (warp == 1) {
@@ -287,6 +301,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_commit(&a_empty[a]);
         tc_commit(&in_empty[s]);
       }
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
   } else if (warp >= 6) {
     // ---------------- dequantisers
@@ -339,6 +354,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&d_empty[dbuf]);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // y / row table may come from the previous kernel
     if (n < N) {
       const int t0 = tt * TN;
 #pragma unroll
@@ -361,6 +377,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 __global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, int64_t T, int64_t N, float* __restrict__ y,
                                     int64_t y_stride, int accumulate, const uint8_t* __restrict__ row_rung,
                                     int64_t rr_stride, int want_rung) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int64_t total = T * N;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -376,6 +393,7 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, in
 // row-major [T, K] (bf16 / fp16 / f32, row stride x_stride) -> tiled bf16 (tiled_act_offset)
 __global__ void tile_acts_kernel(const void* __restrict__ x, int dtype, int64_t x_stride, int T, int64_t K, int nkb,
                                  int out_f16, uint16_t* __restrict__ xt) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int64_t total = static_cast<int64_t>(T) * K;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -468,16 +486,37 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
 #define FQ_GEMM_LAUNCH(Wv, TNv)                                                                              \
   do {                                                                                                      \
     configure_gemm<Wv, TNv>();                                                                              \
-    gemm_ws_kernel<Wv, TNv><<<grid, kGemmThreads, smem_gemm<TNv>(), ctx->stream>>>(                          \
-        st.tiles, n_tiles, nkb, st.zp_base, L->N, xb, static_cast<int>(T), out, out_stride, acc, splits, split_stride, \
-        splits > 1 ? nullptr : row_rung, rr_stride, rung);                                                  \
+    FQ_CUDA(cudaLaunchKernelEx(&lc, gemm_ws_kernel<Wv, TNv>, st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,     \
+                               static_cast<int>(T), out, out_stride, acc, splits, split_stride,                \
+                               splits > 1 ? nullptr : row_rung, rr_stride, rung));                          \
   } while (0)
+  // programmatic dependent launch: the kernel may start while the previous one drains (its
+  // producer prefetches weights, then waits on the dependency before reading activations)
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(kGemmThreads);
+  lc.stream = ctx->stream;
+  lc.attrs = pdl;
+  lc.numAttrs = 1;
   if (rung == FQ_RUNG_INT8) {
-    if (tn == 32) FQ_GEMM_LAUNCH(0, 32);
-    else FQ_GEMM_LAUNCH(0, 128);
+    if (tn == 32) {
+      lc.dynamicSmemBytes = smem_gemm<32>();
+      FQ_GEMM_LAUNCH(0, 32);
+    } else {
+      lc.dynamicSmemBytes = smem_gemm<128>();
+      FQ_GEMM_LAUNCH(0, 128);
+    }
   } else {
-    if (tn == 32) FQ_GEMM_LAUNCH(1, 32);
-    else FQ_GEMM_LAUNCH(1, 128);
+    if (tn == 32) {
+      lc.dynamicSmemBytes = smem_gemm<32>();
+      FQ_GEMM_LAUNCH(1, 32);
+    } else {
+      lc.dynamicSmemBytes = smem_gemm<128>();
+      FQ_GEMM_LAUNCH(1, 128);
+    }
   }
 #undef FQ_GEMM_LAUNCH
   FQ_CUDA(cudaGetLastError());
