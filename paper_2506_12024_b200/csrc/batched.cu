@@ -22,7 +22,6 @@ __global__ void rope_append_rows_kernel(const float* __restrict__ q, const float
                                         const int32_t* __restrict__ pos, const int32_t* __restrict__ slots,
                                         __half* __restrict__ kv, int64_t slot_stride, int64_t layer_off,
                                         int64_t max_seq, float* __restrict__ qr, int f16) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int b = blockIdx.x;
   const int d = H * hd, half = hd / 2;
   const int p = pos[b];
@@ -54,7 +53,6 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
                                         const int32_t* __restrict__ pos, const int32_t* __restrict__ slots,
                                         int64_t slot_stride, int64_t layer_off, int64_t max_seq,
                                         uint16_t* __restrict__ out, int nkb, int f16, int slot0) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   constexpr int hd = DPL * 32;
   __shared__ float qs[8][hd];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -11,20 +11,27 @@
 // accumulated alone in fp32 in tensor memory, and the group's fp32 scale is applied in the
 // epilogue: y = sum_kb s[n, kb] * (sum_{k in kb} (q - z) x).  No weight is ever rounded.
 //
-// One CTA = 128 weight rows (UMMA M) x 128 tokens (UMMA N), warp-specialised, 12 warps:
-//   warp 0     producer: per k-block one 1-D bulk copy (cp.async.bulk) of the 32 KB activation
-//              tile (X is stored pre-tiled in the UMMA canonical K-major layout, see
-//              tiled_act_offset) and eight bulk copies of the CTA's raw 16x128 weight blocks
-//              into a 3-deep ring, completion by mbarrier transaction bytes;
-//   warps 6-11 dequantisers: raw codes -> fp16 (q - z) into a 2-deep A-operand ring (canonical
-//              K-major, no swizzle), fence.proxy.async, one arrival per k-block;
-//   warp 1     MMA issuer (one thread): 8 x tcgen05.mma (M128 N128 K16) per k-block into one of
-//              two TMEM accumulators, tcgen05.commit releases the A / input slots and hands the
-//              accumulator to the epilogue;
-//   warps 2-5  epilogue: tcgen05.ld of the k-block's accumulator (lane quarter = warp % 4), then
-//              y[128 tokens] += s[row, kb] * D in registers; the accumulator slot is returned as
-//              soon as it is read, so the MMAs of k-block kb+1 overlap the scaling of kb.
+// One CTA = 128 weight rows (UMMA M) x TN tokens (UMMA N = 128, or 32 for decode-sized
+// batches), warp-specialised; every hand-off is an mbarrier:
+//   producer   (warp 0) per k-block: lane 0 arms the stage's barrier with the byte count, lanes 0-7
+//              bulk-copy (cp.async.bulk) the CTA's eight raw 16x128 weight blocks and lane 8 the
+//              activation tile (X is stored pre-tiled in the UMMA canonical K-major layout, see
+//              tiled_act_offset) into the input ring;
+//   dequantisers (groups of 8 warps, one raw block per warp): raw codes -> exact fp16 (q - z)
+//              into the A-operand ring (canonical K-major, no swizzle) and the block's row scales
+//              into a scale ring; fence.proxy.async, named barrier, one arrival on a_full;
+//   MMA issuers (one thread each): 8 x tcgen05.mma (K16) per k-block into one of the TMEM
+//              accumulator buffers, then ONE tcgen05.commit on mma_done[k-block], which is at once
+//              the epilogue's "accumulator full", the dequantisers' "A slot free" and the
+//              producer's "stage free";
+//   epilogue   (4 or 8 warps): tcgen05.ld of the k-block's accumulator (lane quarter = warp % 4),
+//              y += s[row, kb] * D in registers, d_empty arrival.
+// Measured (clock64 traces of one CTA, tools/gemm_bench.py): an mbarrier wait costs 150-450 cycles
+// even when the phase is already complete, a bulk-copy issue ~150, a tcgen05.mma issue ~65, so the
+// loop is shaped to put as few of them as possible on any one thread per k-block; at TN = 32 two
+// dequantiser groups and two MMA issuers take alternating k-blocks.
 #include "gemv_program.cuh"
+
 
 namespace fqc {
 namespace {
@@ -33,24 +40,45 @@ constexpr int kTM = 128;                      // weight rows per CTA (UMMA M)
 constexpr int kTN = 128;                      // tokens per activation tile (the tiled layout's row block)
 constexpr int kTK = 128;                      // codes per k-block (one tiled block / group)
 constexpr int kTileBytes = kTM * kTK * 2;     // bf16 128 x 128 tile: 32 KB (A and B alike)
-constexpr int kInStages = 3;                  // activation + raw-weight ring
-constexpr int kAStages = 2;                   // dequantised A ring
-constexpr int kGemmThreads = 384;             // 12 warps (3 per SM sub-partition: 168 registers each)
-constexpr int kDequantThreads = 192;          // warps 6..11
+// ring depths (shared memory: 227 KB per CTA): input stages of raw blocks + activation tile (49 KB
+// at TN = 128, 25 KB at TN = 32), dequantised A slots (32 KB), TMEM accumulator buffers (the
+// epilogue scales every k-block's D by its own per-row scale, so MMA k-block i waits for the
+// epilogue of i - d_bufs)
+template <int TN>
+constexpr int in_stages() { return TN == 32 ? 5 : 3; }
+constexpr int kMaxInStages = 6;
+template <int TN>
+constexpr int a_stages() { return TN == 32 ? 3 : 2; }
+constexpr int kMaxAStages = 4;
+template <int TN>
+constexpr int d_bufs() { return TN == 32 ? 8 : 4; }
+constexpr int kMaxDBufs = 16;
+// warps: 0 producer, then MI MMA issuers, E epilogue warps, and G groups of 8 dequantisers (one
+// raw block per warp).  Every mbarrier hand-off costs a few hundred cycles of wake-up, so at
+// TN = 32 (where a k-block's MMAs are short) two dequantiser groups and two MMA issuers work on
+// alternating k-blocks: 1 + 2 + 4 + 16 = 23 warps (<= 88 registers; 32 fp32 sums per epilogue
+// thread).  At TN = 128 the MMAs themselves pace the loop: 1 + 1 + 8 + 8 = 18 warps (<= 112), two
+// epilogue warps per TMEM lane quarter with 64 columns each.
+template <int TN>
+constexpr int mma_issuers() { return TN == 32 ? 2 : 1; }
+template <int TN>
+constexpr int epi_warps() { return TN == 128 ? 8 : 4; }
+template <int TN>
+constexpr int dq_groups() { return TN == 32 ? 2 : 1; }
+template <int TN>
+constexpr int gemm_threads() { return 32 * (1 + mma_issuers<TN>() + epi_warps<TN>() + 8 * dq_groups<TN>()); }
+constexpr int kDequantThreads = 256;  // per group
 constexpr int kRawBytes = 8 * kBlockBytes8;   // 8 raw 16x128 blocks (W8 size; W4 uses half)
 // tokens per CTA (UMMA N): 128, or 32 for decode-sized batches (the first 32 rows of a 128-row
 // tile are its first 8 KB in the canonical layout, so the same tiled activations serve both)
 template <int TN>
-constexpr int smem_gemm() { return kInStages * (TN * 256 + kRawBytes) + kAStages * kTileBytes + 1024; }
+constexpr int smem_gemm() { return in_stages<TN>() * (TN * 256 + kRawBytes) + a_stages<TN>() * kTileBytes + 1024; }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
-// canonical K-major no-swizzle byte offset of element (row, k) inside a 128x128 16-bit tile:
-// 8x16-byte core matrices, LBO = 128 B (K-adjacent core matrices), SBO = 2 KB (8-row groups)
-__device__ __forceinline__ uint32_t kmajor_off(int row, int k) {
-  return static_cast<uint32_t>((row >> 3) * 2048 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
-}
-
+// canonical K-major no-swizzle layout of a 128x128 16-bit tile: element (row, k) at byte
+// (row >> 3) * 2048 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2 -- 8x16-byte core matrices,
+// LBO = 128 B (K-adjacent core matrices), SBO = 2 KB (8-row groups)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);  // start address
@@ -139,76 +167,73 @@ __device__ __forceinline__ uint32_t zpair(const uint8_t* zp8, int r, int32_t zba
   return u | (u << 16);
 }
 
+// One dequantiser warp per raw 16x128 block of the stage (rt = 0..7): lane (r, c2) = (lane >> 2,
+// 2 (lane & 3)) holds, in every 16-byte code word of the block, codes of rows r and r + 8 only, so
+// its two zero-point pairs are loaded once per k-block and every store lands at a compile-time
+// offset from one per-thread base (row 16 rt + r, k & 7 = c2 of the canonical K-major tile).
 template <int W>
-__device__ __forceinline__ void dequant_stage(const uint8_t* raw, int32_t zbase, uint8_t* a_tile, int d) {
+__device__ __forceinline__ void dequant_block(const uint8_t* raw, int32_t zbase, uint8_t* a_tile, int rt, int lane) {
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
-  constexpr int words = W == 0 ? 4 : 2;  // 16-byte code words per lane per block
-  constexpr int units = 8 * words * 32;  // (block, word, lane) units of the stage
-  constexpr int per = (units + kDequantThreads - 1) / kDequantThreads;
-  // every load of the thread's units first (independent, all in flight), then the conversions
-  uint4 wv[per];
-  uint32_t z0v[per], z1v[per];
+  constexpr int words = W == 0 ? 4 : 2;  // 16-byte code words per lane
+  const uint8_t* blk = raw + rt * bb;
+  const int r = lane >> 2, c2 = 2 * (lane & 3);
+  uint4 wv[words];
 #pragma unroll
-  for (int j = 0; j < per; ++j) {
-    const int u = d + j * kDequantThreads;
-    if (u < units) {
-      const int rt = u / (words * 32), rem = u - rt * (words * 32);
-      const int i = rem >> 5, t = rem & 31, r = t >> 2;
-      const uint8_t* blk = raw + rt * bb;
-      wv[j] = reinterpret_cast<const uint4*>(blk)[i * 32 + t];
-      z0v[j] = zpair(blk + cbytes + 64, r, zbase);
-      z1v[j] = zpair(blk + cbytes + 64, r + 8, zbase);
-    }
-  }
+  for (int i = 0; i < words; ++i) wv[i] = reinterpret_cast<const uint4*>(blk)[i * 32 + lane];
+  const uint32_t z0 = zpair(blk + cbytes + 64, r, zbase), z1 = zpair(blk + cbytes + 64, r + 8, zbase);
+  uint8_t* base = a_tile + rt * 4096 + r * 16 + c2 * 2;  // + (k >> 3) * 128, + 2048 for row + 8
 #pragma unroll
-  for (int j = 0; j < per; ++j) {
-    const int u = d + j * kDequantThreads;
-    if (u >= units) break;
-    const int rt = u / (words * 32), rem = u - rt * (words * 32);
-    const int i = rem >> 5, t = rem & 31;
-    const int r = t >> 2, c2 = 2 * (t & 3);
-    const uint32_t q4[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
-    const uint32_t z0 = z0v[j], z1 = z1v[j];
-    const int row = rt * 16 + r;
+  for (int i = 0; i < words; ++i) {
+    const uint32_t q4[4] = {wv[i].x, wv[i].y, wv[i].z, wv[i].w};
     if constexpr (W == 0) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {  // bytes (r, k0), (r, k0+1), (r+8, k0), (r+8, k0+1)
-          const int k0 = 16 * (2 * i + h) + c2 + 8 * e;
-          const uint32_t q = q4[2 * h + e];
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = hsub2(prmt(q, 0x64646464u, 0x4140u), z0);
-          *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = hsub2(prmt(q, 0x64646464u, 0x4342u), z1);
-        }
+      for (int j = 0; j < 4; ++j) {  // word j = (h, e): bytes (r, k0), (r, k0+1), (r+8, k0), (r+8, k0+1)
+        const int col = 4 * i + j;   // k0 = 16 (2i + h) + c2 + 8e  ->  k0 >> 3 = 4i + 2h + e
+        *reinterpret_cast<uint32_t*>(base + col * 128) = hsub2(prmt(q4[j], 0x64646464u, 0x4140u), z0);
+        *reinterpret_cast<uint32_t*>(base + 2048 + col * 128) = hsub2(prmt(q4[j], 0x64646464u, 0x4342u), z1);
       }
     } else {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9)
-        const int k0 = 16 * (4 * i + v) + c2;
+        // nibbles (low to high): (r,k0) (r,k0+8) (r+8,k0) (r+8,k0+8) (r,k0+1) (r,k0+9) (r+8,k0+1) (r+8,k0+9),
+        // k0 = 16 (4i + v) + c2
+        const int col = 2 * (4 * i + v);
         const uint32_t q = q4[v];
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0)) = hsub2(nib_pair(q), z0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row, k0 + 8)) = hsub2(nib_pair(q >> 4), z0);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0)) = hsub2(nib_pair(q >> 8), z1);
-        *reinterpret_cast<uint32_t*>(a_tile + kmajor_off(row + 8, k0 + 8)) = hsub2(nib_pair(q >> 12), z1);
+        *reinterpret_cast<uint32_t*>(base + col * 128) = hsub2(nib_pair(q), z0);
+        *reinterpret_cast<uint32_t*>(base + (col + 1) * 128) = hsub2(nib_pair(q >> 4), z0);
+        *reinterpret_cast<uint32_t*>(base + 2048 + col * 128) = hsub2(nib_pair(q >> 8), z1);
+        *reinterpret_cast<uint32_t*>(base + 2048 + (col + 1) * 128) = hsub2(nib_pair(q >> 12), z1);
       }
     }
   }
 }
 
 template <int W, int TN>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<TN>(), 1)
     gemm_ws_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb, int32_t zbase, int64_t N,
                    const uint8_t* __restrict__ xt, int T, float* __restrict__ y, int64_t y_stride, int accumulate,
                    int splits, int64_t split_stride, const uint8_t* __restrict__ row_rung, int64_t rr_stride,
                    int want_rung) {
   constexpr int kBBytes = TN * 256;  // activation bytes per k-block
+  constexpr int kInStages = in_stages<TN>();
+  constexpr int kAStages = a_stages<TN>();
   constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int cbytes = W == 0 ? 2048 : 1024;
   extern __shared__ __align__(1024) uint8_t gsm[];
-  __shared__ uint64_t in_full[kInStages], in_empty[kInStages], a_full[kAStages], a_empty[kAStages];
-  __shared__ uint64_t d_full[2], d_empty[2];
+  constexpr int kDBufs = d_bufs<TN>();
+  // mma_done[i % kR] completes (one tcgen05.commit) when k-block i's MMAs are done: it is the
+  // epilogue's "accumulator full", the dequantisers' "A slot free" (lag kAStages) and the
+  // producer's "stage free" (lag kInStages; the MMAs ran after the dequant of the raw blocks).  A
+  // waiter must never fall a whole phase behind: MMA i + kR needs the epilogue of i + kR - kDBufs
+  // and the bytes of k-block i + kR - kAStages (loaded in order, at most kInStages ahead of the
+  // slowest dequant), so kR >= max(kDBufs, kAStages + kInStages) suffices; twice that is used.
+  constexpr int kR0 = kDBufs > kAStages + kInStages ? kDBufs : kAStages + kInStages;
+  constexpr int kR = 2 * kR0 > kMaxDBufs ? kMaxDBufs : 2 * kR0;
+  static_assert(kR >= kR0, "mma_done ring too short");
+  __shared__ uint64_t in_full[kMaxInStages], a_full[kMaxAStages], mma_done[kMaxDBufs], d_empty[kMaxDBufs];
+  constexpr int kScSlots = kAStages + kDBufs;
+  __shared__ float sc_ring[kScSlots * kTM];
   __shared__ uint32_t tmem_base_s;
   uint8_t* base = gsm + ((1024u - (smem_addr(gsm) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer
   uint8_t* b_ring = base;                                        // kInStages x 32 KB activations
@@ -223,122 +248,120 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nk = kb1 - kb0;
   y += blockIdx.z * split_stride;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kInStages; ++s) {
-      mbar_init(&in_full[s], 1);
-      mbar_init(&in_empty[s], 2);  // dequantisers done with the raw blocks + MMAs done with B
-    }
-    for (int s = 0; s < kAStages; ++s) {
-      mbar_init(&a_full[s], 1);
-      mbar_init(&a_empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&d_full[s], 1);
-      mbar_init(&d_empty[s], 4);  // one arrival per epilogue warp
-    }
+    for (int s = 0; s < kInStages; ++s) mbar_init(&in_full[s], 1);
+    for (int s = 0; s < kAStages; ++s) mbar_init(&a_full[s], 1);
+    for (int s = 0; s < kR; ++s) mbar_init(&mma_done[s], 1);
+    for (int s = 0; s < kDBufs; ++s) mbar_init(&d_empty[s], epi_warps<TN>());  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_s)),
-                 "r"(2 * TN));
+                 "r"(kDBufs * TN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
+#ifdef FQ_GEMM_TRACE
+  __shared__ long long trc[9][24];
+  const bool trace_cta = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#define TRC(k, i) do { if (trace_cta && (i) < 24) trc[k][i] = clock64(); } while (0)
+  TRC(6, 0);
+#else
+#define TRC(k, i) do {} while (0)
+#endif
 
   if (warp == 0) {
-    // ---------------- producer
-    if (lane == 0) {
-      auto weights = [&](int s, int kb) {
-#pragma unroll 1
-        for (int r = 0; r < 8; ++r) {
-          const int64_t tile = min(tile0 + r, static_cast<int64_t>(n_tiles) - 1);  // rows past N masked at store
-          bulk_g2s(raw_ring + s * kRawBytes + r * bb, tiles + (tile * nkb + kb) * bb, bb, &in_full[s]);
-        }
-      };
-      // the weights do not depend on the previous kernel: the first stages' blocks go out before
-      // the programmatic-dependency wait (the launch overlaps the previous kernel's tail), the
-      // activation tiles only after it
-      const int pre = min(nk, kInStages);
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(&in_full[i], kBBytes + 8 * bb);
-        weights(i, kb0 + i);
-      }
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      for (int i = 0; i < pre; ++i)
-        bulk_g2s(b_ring + i * kBBytes, xt + b_src + static_cast<int64_t>(kb0 + i) * kTileBytes, kBBytes, &in_full[i]);
-      for (int i = pre; i < nk; ++i) {
-        const int s = i % kInStages, kb = kb0 + i;
-        mbar_wait(&in_empty[s], ((i / kInStages) - 1) & 1, 0);
-        mbar_expect_tx(&in_full[s], kBBytes + 8 * bb);
+    // ---------------- producer: lane 0 arms the stage barrier, then lanes 0-7 issue the eight
+    // raw-block copies and lane 8 the activation tile in parallel (bulk copies issued back to back
+    // by one thread cost ~150 cycles each: nine of them took longer than the k-block)
+    auto issue = [&](int s, int kb) {
+      if (lane < 8) {
+        const int64_t tile = min(tile0 + lane, static_cast<int64_t>(n_tiles) - 1);
+        bulk_g2s(raw_ring + s * kRawBytes + lane * bb, tiles + (tile * nkb + kb) * bb, bb, &in_full[s]);
+      } else if (lane == 8) {
         bulk_g2s(b_ring + s * kBBytes, xt + b_src + static_cast<int64_t>(kb) * kTileBytes, kBBytes, &in_full[s]);
-        weights(s, kb);
       }
+    };
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % kInStages;
+      if (lane == 0) {
+        if (i >= kInStages) mbar_wait(&mma_done[(i - kInStages) % kR], ((i - kInStages) / kR) & 1, 0);
+        mbar_expect_tx(&in_full[s], kBBytes + 8 * bb);
+      }
+      __syncwarp();
+      issue(s, kb0 + i);
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer
+  } else if (warp <= mma_issuers<TN>()) {
+    // ---------------- MMA issuers: issuer m = warp - 1 takes k-blocks i = m (mod MI); each
+    // tcgen05.commit tracks only its own thread's MMAs
     if (lane == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % kInStages, a = i % kAStages, dbuf = i & 1;
-        mbar_wait(&in_full[s], (i / kInStages) & 1, 1);
+      for (int i = warp - 1; i < nk; i += mma_issuers<TN>()) {
+        const int s = i % kInStages, a = i % kAStages, dbuf = i % kDBufs;
+        // a_full(i) implies in_full(i): the dequantisers waited for the stage's bytes before
+        // converting them
         mbar_wait(&a_full[a], (i / kAStages) & 1, 1);
-        if (i >= 2) mbar_wait(&d_empty[dbuf], ((i >> 1) - 1) & 1, 1);
+        if (i >= kDBufs) mbar_wait(&d_empty[dbuf], ((i / kDBufs) - 1) & 1, 1);
+        TRC(3, i);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_addr(a_ring + a * kTileBytes), b0 = smem_addr(b_ring + s * kBBytes);
+        const uint64_t da = umma_desc(smem_addr(a_ring + a * kTileBytes)), db = umma_desc(smem_addr(b_ring + s * kBBytes));
         const uint32_t dt = tmem + static_cast<uint32_t>(dbuf * TN);
 #pragma unroll
-        for (int j = 0; j < kTK / 16; ++j) {
-          const uint64_t da = umma_desc(a0 + j * 256), db = umma_desc(b0 + j * 256);
-          const uint32_t acc = j > 0 ? 1u : 0u;
+        for (int j = 0; j < kTK / 16; ++j) {  // K step of 16 = 256 B = +16 in the descriptors' address field
           asm volatile(
               "{\n\t.reg .pred p;\n\t"
               "setp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
-              "l"(da), "l"(db), "r"(idesc<1, TN>()), "r"(acc));
+              "l"(da + 16u * j), "l"(db + 16u * j), "r"(idesc<1, TN>()), "r"(j > 0 ? 1u : 0u));
         }
-        tc_commit(&d_full[dbuf]);
-        tc_commit(&a_empty[a]);
-        tc_commit(&in_empty[s]);
+        TRC(7, i);
+        tc_commit(&mma_done[i % kR]);
+        TRC(8, i);
       }
-      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
-  } else if (warp >= 6) {
-    // ---------------- dequantisers
-    const int d = threadIdx.x - 6 * 32;
-    for (int i = 0; i < nk; ++i) {
+  } else if (warp >= 1 + mma_issuers<TN>() + epi_warps<TN>()) {
+    // ---------------- dequantisers: group g takes k-blocks i = g (mod G); its warp rt converts
+    // raw block rt of the stage
+    const int dw = warp - 1 - mma_issuers<TN>() - epi_warps<TN>();
+    const int g = dw >> 3, rt = dw & 7;
+    for (int i = g; i < nk; i += dq_groups<TN>()) {
       const int s = i % kInStages, a = i % kAStages;
       mbar_wait(&in_full[s], (i / kInStages) & 1, 2);
-      if (i >= kAStages) mbar_wait(&a_empty[a], ((i / kAStages) - 1) & 1, 2);
-      dequant_stage<W>(raw_ring + s * kRawBytes, zbase, a_ring + a * kTileBytes, d);
+      if (i >= kAStages) mbar_wait(&mma_done[(i - kAStages) % kR], ((i - kAStages) / kR) & 1, 2);
+      if (g == 0 && rt == 0 && lane == 0) TRC(1, i);
+      const uint8_t* raw = raw_ring + s * kRawBytes;
+      dequant_block<W>(raw, zbase, a_ring + a * kTileBytes, rt, lane);
+      // the block's 16 row scales into the scale ring the epilogue reads: the slot is rewritten by
+      // the dequant of k-block i + kScSlots, which waits for MMA i + kDBufs, which
+      // waited (d_empty) for this k-block's epilogue
+      if (lane < 16) sc_ring[(i % kScSlots) * kTM + rt * 16 + lane] = reinterpret_cast<const float*>(raw + rt * bb + cbytes)[lane];
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-      asm volatile("bar.sync 1, %0;" ::"n"(kDequantThreads) : "memory");
-      if (d == 0) {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kDequantThreads) : "memory");
+      if (rt == 0 && lane == 0) {
+        if (g == 0) TRC(2, i);
         mbar_arrive(&a_full[a]);
-        mbar_arrive(&in_empty[s]);
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5): TMEM lane quarter q = warp % 4 = weight rows 32q..
-    const int q = warp & 3;
+    // ---------------- epilogue: TMEM lane quarter q = warp % 4 = weight rows 32q.., columns
+    // [half * EC, half * EC + EC) of the k-block's accumulator
+    constexpr int EC = TN * 4 / epi_warps<TN>();
+    const int q = warp & 3, half = (warp - 1 - mma_issuers<TN>()) >> 2;
     const int row = q * 32 + lane;
     const int64_t n = static_cast<int64_t>(blockIdx.x) * kTM + row;
-    const int64_t tile = min(tile0 + row / kTileRows, static_cast<int64_t>(n_tiles) - 1);
-    const float* sc = reinterpret_cast<const float*>(tiles + tile * nkb * bb + cbytes) + (row % kTileRows);
-    const int64_t sstride = bb / 4;  // floats between the scales of consecutive k-blocks
-    float acc[TN];
+    float acc[EC];
 #pragma unroll
-    for (int c = 0; c < TN; ++c) acc[c] = 0.f;
-    float s_next = nk > 0 ? sc[kb0 * sstride] : 0.f;
+    for (int c = 0; c < EC; ++c) acc[c] = 0.f;
     for (int i = 0; i < nk; ++i) {
-      const int dbuf = i & 1;
-      const float s_kb = s_next;
-      if (i + 1 < nk) s_next = sc[(kb0 + i + 1) * sstride];
-      mbar_wait(&d_full[dbuf], (i >> 1) & 1, 3);
+      const int dbuf = i % kDBufs;
+      mbar_wait(&mma_done[i % kR], (i / kR) & 1, 3);
+      if (q == 0 && lane == 0) TRC(4, i);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(dbuf * TN);
+      const float s_kb = sc_ring[(i % kScSlots) * kTM + row];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(dbuf * TN + half * EC);
 #pragma unroll
-      for (int c0 = 0; c0 < TN; c0 += 16) {
+      for (int c0 = 0; c0 < EC; c0 += 16) {
         uint32_t v[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -353,12 +376,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&d_empty[dbuf]);
+      if (q == 0 && lane == 0) TRC(5, i);
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // y / row table may come from the previous kernel
     if (n < N) {
-      const int t0 = tt * TN;
+      const int t0 = tt * TN + half * EC;
 #pragma unroll
-      for (int c = 0; c < TN; ++c) {
+      for (int c = 0; c < EC; ++c) {
         const int t = t0 + c;
         // row_rung: this launch covers only the rows decoding at want_rung (grouped batches)
         if (t < T && (row_rung == nullptr || row_rung[t * rr_stride] == want_rung)) {
@@ -370,14 +393,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TN));
+#ifdef FQ_GEMM_TRACE
+  if (trace_cta && threadIdx.x == 0) {
+    printf("TRACE nk=%d start=%lld\n", nk, trc[6][0]);
+    for (int i = 0; i < min(nk, 24); ++i) {
+      printf("TRACE %d P %lld D0 %lld D1 %lld M %lld Mi %lld Mc %lld E0 %lld E1 %lld\n", i, trc[0][i] - trc[6][0], trc[1][i] - trc[6][0],
+             trc[2][i] - trc[6][0], trc[3][i] - trc[6][0], trc[7][i] - trc[6][0], trc[8][i] - trc[6][0], trc[4][i] - trc[6][0], trc[5][i] - trc[6][0]);
+    }
+  }
+#endif
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kDBufs * TN));
 }
 
 // y[t][n] (+)= sum over the splits in order of ws[z][t][n] (deterministic split-K reduction)
 __global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, int64_t T, int64_t N, float* __restrict__ y,
                                     int64_t y_stride, int accumulate, const uint8_t* __restrict__ row_rung,
                                     int64_t rr_stride, int want_rung) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int64_t total = T * N;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -393,7 +424,6 @@ __global__ void split_reduce_kernel(const float* __restrict__ ws, int splits, in
 // row-major [T, K] (bf16 / fp16 / f32, row stride x_stride) -> tiled bf16 (tiled_act_offset)
 __global__ void tile_acts_kernel(const void* __restrict__ x, int dtype, int64_t x_stride, int T, int64_t K, int nkb,
                                  int out_f16, uint16_t* __restrict__ xt) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int64_t total = static_cast<int64_t>(T) * K;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -486,21 +516,14 @@ void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const v
 #define FQ_GEMM_LAUNCH(Wv, TNv)                                                                              \
   do {                                                                                                      \
     configure_gemm<Wv, TNv>();                                                                              \
-    FQ_CUDA(cudaLaunchKernelEx(&lc, gemm_ws_kernel<Wv, TNv>, st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,     \
+    FQ_CUDA(cudaLaunchKernelEx(&lc, gemm_ws_kernel<Wv, TNv>, st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,                 \
                                static_cast<int>(T), out, out_stride, acc, splits, split_stride,                \
                                splits > 1 ? nullptr : row_rung, rr_stride, rung));                          \
   } while (0)
-  // programmatic dependent launch: the kernel may start while the previous one drains (its
-  // producer prefetches weights, then waits on the dependency before reading activations)
-  cudaLaunchAttribute pdl[1];
-  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = grid;
-  lc.blockDim = dim3(kGemmThreads);
+  lc.blockDim = dim3(tn == 32 ? gemm_threads<32>() : gemm_threads<128>());
   lc.stream = ctx->stream;
-  lc.attrs = pdl;
-  lc.numAttrs = 1;
   if (rung == FQ_RUNG_INT8) {
     if (tn == 32) {
       lc.dynamicSmemBytes = smem_gemm<32>();

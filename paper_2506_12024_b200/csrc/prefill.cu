@@ -25,7 +25,6 @@ __device__ __forceinline__ uint16_t actb(float v, int f16) {
 
 __global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32_t* __restrict__ tokens, int64_t d,
                                   float* __restrict__ x) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int t = blockIdx.x;
   const float* e = tok_emb + static_cast<int64_t>(tokens[t]) * d;
   for (int64_t i = threadIdx.x; i < d; i += blockDim.x) x[t * d + i] = e[i];
@@ -34,7 +33,6 @@ __global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32
 // h[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * g)
 __global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g, float eps,
                                     uint16_t* __restrict__ h, int nkb, int f16) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int t = blockIdx.x;
   const float* xr = x + t * d;
   float s = 0.f;
@@ -60,7 +58,6 @@ __global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, cons
 __global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
                                     int H, int hd, const float2* __restrict__ cs, float* __restrict__ qr,
                                     __half* __restrict__ kv_layer, int64_t max_seq, int f16) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   const int t = blockIdx.x;
   const int d = H * hd, half = hd / 2;
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
@@ -83,7 +80,6 @@ __global__ void rope_kv_rows_kernel(const float* __restrict__ q, const float* __
 
 __global__ void swiglu_rows_kernel(const float* __restrict__ g, const float* __restrict__ u, int64_t n, int64_t f,
                                    uint16_t* __restrict__ out, int nkb, int f16) {
-  asm volatile("griddepcontrol.launch_dependents;");  // the next GEMM may start prefetching weights
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float gv = g[i];  // unrounded GEMM sums, as the decode step's SwiGLU epilogue reads them

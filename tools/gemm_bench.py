@@ -17,6 +17,7 @@ ap.add_argument("--T", default="512,2048")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--bits", default="8,4")
 ap.add_argument("--shapes", default="all")
+ap.add_argument("--graph", action="store_true", help="time a CUDA graph of the launches (no host launch gaps)")
 a = ap.parse_args()
 peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
 ctx = capi.Context(0)
@@ -41,10 +42,20 @@ for K, N in shapes:
                     ctx.gemm_tiled(L, rung, T, xt, capi.DT_F16, y)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(a.iters):
-                    ctx.gemm_tiled(L, rung, T, xt, capi.DT_F16, y)
-                e1.record(stream)
+                if a.graph:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        for _ in range(a.iters):
+                            ctx.gemm_tiled(L, rung, T, xt, capi.DT_F16, y)
+                    g.replay()
+                    e0.record(stream)
+                    g.replay()
+                    e1.record(stream)
+                else:
+                    e0.record(stream)
+                    for _ in range(a.iters):
+                        ctx.gemm_tiled(L, rung, T, xt, capi.DT_F16, y)
+                    e1.record(stream)
                 e1.synchronize()
             ms = e0.elapsed_time(e1) / a.iters
             tf = 2.0 * T * N * K / (ms * 1e-3) / 1e12
