@@ -57,8 +57,11 @@ struct fq_ctx {
   float* gemv_fix = nullptr;
   unsigned int* gemv_flags = nullptr;
   unsigned int* launch_ctr = nullptr;  // [epoch, done] of the program kernels on this context
-  float* gemm_ws = nullptr;  // split-K partial sums of the tensor-core GEMM (grown on demand)
+  float* gemm_ws = nullptr;  // stream-K partial tiles of the tensor-core GEMM (grown on demand)
   size_t gemm_ws_bytes = 0;
+  int* gemm_cnt = nullptr;   // per-tile arrival counters (zero between launches)
+  int64_t gemm_cnt_n = 0;
+  std::vector<void*> retired;  // outgrown workspaces captured graphs may still point at (freed at destroy)
   // bumped whenever a layer's resident copies change (upload, device quantization): models
   // drop step programs and captured graphs built against older weight pointers
   uint64_t weight_epoch = 0;
@@ -199,6 +202,18 @@ void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride,
 void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
                     int64_t y_stride, bool accumulate = false, const uint8_t* row_rung = nullptr,
                     int64_t rr_stride = 0);
+// One launch for several (linear, rung) products of the SAME tiled activations (equal K): q/k/v,
+// gate/up, the copies of one linear in a mixed batch.  Work is split evenly over all SMs.
+struct GemmJob {
+  const fq_layer* L;
+  int rung;
+  float* y;
+  int64_t y_stride;
+  bool accumulate;
+  const uint8_t* row_rung;  // optional, as in launch_gemm_dq
+  int64_t rr_stride;
+};
+void launch_gemm_group(fq_ctx* ctx, const GemmJob* jobs, int n_jobs, int64_t T, const void* xt);
 
 // row-parallel prefill kernels (prefill.cu; llama arch; GEMM operands bf16, stored tiled)
 // true (and cleared) when a prefill GEMM operand exceeded fp16's range since the last call

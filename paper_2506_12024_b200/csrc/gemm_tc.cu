@@ -209,17 +209,60 @@ __device__ __forceinline__ void dequant_block(const uint8_t* raw, int32_t zbase,
   }
 }
 
-template <int W, int TN>
-__global__ void __launch_bounds__(gemm_threads<TN>(), 1)
-    gemm_ws_kernel(const uint8_t* __restrict__ tiles, int n_tiles, int nkb, int32_t zbase, int64_t N,
-                   const uint8_t* __restrict__ xt, int T, float* __restrict__ y, int64_t y_stride, int accumulate,
-                   int splits, int64_t split_stride, const uint8_t* __restrict__ row_rung, int64_t rr_stride,
-                   int want_rung) {
+// One launch covers a GROUP of products of the same tiled activations (q/k/v, gate/up, the
+// precision copies of one linear in a mixed batch): blockIdx.z = problem * splits + split; CTAs
+// past a problem's own row count exit at once.  Each problem carries its copy's code width, so W8
+// and W4 products share a launch.
+constexpr int kMaxProblems = 8;
+struct GemmProblem {
+  const uint8_t* tiles;
+  float* y;
+  const uint8_t* row_rung;  // rows (tokens) of this problem: row_rung[t * rr_stride] == want_rung, or all
+  int64_t N, y_stride, rr_stride;
+  int n_tiles;  // 16-row tiles of the tiled copy
+  int32_t zbase;
+  int bits, accumulate, want_rung;
+};
+struct GemmGroup {
+  GemmProblem p[kMaxProblems];
+  const uint8_t* xt;     // tiled fp16 activations [T, K]
+  int64_t split_stride;  // floats between split partial outputs (splits > 1: one problem only)
+  int T, nkb, splits;
+};
+
+template <int TN>
+__global__ void __launch_bounds__(gemm_threads<TN>(), 1) gemm_ws_kernel(const __grid_constant__ GemmGroup g) {
   constexpr int kBBytes = TN * 256;  // activation bytes per k-block
   constexpr int kInStages = in_stages<TN>();
   constexpr int kAStages = a_stages<TN>();
-  constexpr int bb = W == 0 ? kBlockBytes8 : kBlockBytes4;
-  constexpr int cbytes = W == 0 ? 2048 : 1024;
+  const int prob = blockIdx.z / g.splits, split = blockIdx.z - prob * g.splits;
+  const uint8_t* tiles = nullptr;
+  float* y = nullptr;
+  const uint8_t* row_rung = nullptr;
+  int64_t N = 0, y_stride = 0, rr_stride = 0;
+  int n_tiles = 0, bits = 8, accumulate = 0, want_rung = 0;
+  int32_t zbase = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxProblems; ++k)  // static indices only: the table stays in parameter space
+    if (k == prob) {
+      tiles = g.p[k].tiles;
+      y = g.p[k].y;
+      row_rung = g.p[k].row_rung;
+      N = g.p[k].N;
+      y_stride = g.p[k].y_stride;
+      rr_stride = g.p[k].rr_stride;
+      n_tiles = g.p[k].n_tiles;
+      zbase = g.p[k].zbase;
+      bits = g.p[k].bits;
+      accumulate = g.p[k].accumulate;
+      want_rung = g.p[k].want_rung;
+    }
+  if (static_cast<int64_t>(blockIdx.x) * kTM >= N) return;  // shorter problem of the group
+  const int nkb = g.nkb, T = g.T, splits = g.splits;
+  const uint8_t* xt = g.xt;
+  const int64_t split_stride = g.split_stride;
+  const int bb = bits == 8 ? kBlockBytes8 : kBlockBytes4;
+  const int cbytes = bits == 8 ? 2048 : 1024;
   extern __shared__ __align__(1024) uint8_t gsm[];
   constexpr int kDBufs = d_bufs<TN>();
   // mma_done[i % kR] completes (one tcgen05.commit) when k-block i's MMAs are done: it is the
@@ -243,10 +286,10 @@ __global__ void __launch_bounds__(gemm_threads<TN>(), 1)
   const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * (kTM / kTileRows);
   const int tt = blockIdx.y;  // token tile of TN rows
   const int64_t b_src = static_cast<int64_t>(tt * TN / kTN) * nkb * kTileBytes + (tt * TN % kTN) * 256;
-  const int kb0 = static_cast<int>(static_cast<int64_t>(nkb) * blockIdx.z / splits);
-  const int kb1 = static_cast<int>(static_cast<int64_t>(nkb) * (blockIdx.z + 1) / splits);
+  const int kb0 = static_cast<int>(static_cast<int64_t>(nkb) * split / splits);
+  const int kb1 = static_cast<int>(static_cast<int64_t>(nkb) * (split + 1) / splits);
   const int nk = kb1 - kb0;
-  y += blockIdx.z * split_stride;
+  y += split * split_stride;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kInStages; ++s) mbar_init(&in_full[s], 1);
     for (int s = 0; s < kAStages; ++s) mbar_init(&a_full[s], 1);
@@ -331,7 +374,8 @@ __global__ void __launch_bounds__(gemm_threads<TN>(), 1)
       if (i >= kAStages) mbar_wait(&mma_done[(i - kAStages) % kR], ((i - kAStages) / kR) & 1, 2);
       if (g == 0 && rt == 0 && lane == 0) TRC(1, i);
       const uint8_t* raw = raw_ring + s * kRawBytes;
-      dequant_block<W>(raw, zbase, a_ring + a * kTileBytes, rt, lane);
+      if (bits == 8) dequant_block<0>(raw, zbase, a_ring + a * kTileBytes, rt, lane);
+      else dequant_block<1>(raw, zbase, a_ring + a * kTileBytes, rt, lane);
       // the block's 16 row scales into the scale ring the epilogue reads: the slot is rewritten by
       // the dequant of k-block i + kScSlots, which waits for MMA i + kDBufs, which
       // waited (d_empty) for this k-block's epilogue
@@ -444,11 +488,11 @@ __global__ void tile_acts_kernel(const void* __restrict__ x, int dtype, int64_t 
   }
 }
 
-template <int W, int TN>
+template <int TN>
 void configure_gemm() {
   static bool done = false;
   if (!done) {
-    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<W, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_gemm<TN>()));
+    FQ_CUDA(cudaFuncSetAttribute(gemm_ws_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_gemm<TN>()));
     done = true;
   }
 }
@@ -470,88 +514,128 @@ void launch_tile_acts(fq_ctx* ctx, const void* x, int x_dtype, int64_t x_stride,
   ctx->launches += 1;
 }
 
-void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
-                    int64_t y_stride, bool accumulate, const uint8_t* row_rung, int64_t rr_stride) {
-  if (rung != FQ_RUNG_INT8 && rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
-  if (x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: the tiled activations are fp16 (bf16 values stored exactly)");
-  const fq_rung_store& st = L->store(rung);
-  if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
-  if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
-  if ((reinterpret_cast<uintptr_t>(xt) & 15) != 0) fail(FQ_E_CONFIG, "gemm: tiled activations must be 16-byte aligned");
-  const int n_tiles = ceil_div_i(L->N, kTileRows), nkb = ceil_div_i(L->K, kBlockK);
-  const int tn = T <= 32 ? 32 : kTN;  // decode-sized batches: 32-token MMAs, a quarter of the activation traffic
-  const int gx = ceil_div_i(L->N, kTM), gy = ceil_div_i(T, tn);
-  // split K when the output tiles alone leave SMs idle: the fewest splits with the lowest
-  // (waves x work per split), at least 4 k-blocks per split
-  // the split-K reduction is a separate pass over splits x T x N floats: split only grids that
-  // leave more than half the SMs idle (decode-sized batches), not to even out waves
+namespace {
+// launch-time model (measured, tools/gemm_bench.py): a CTA streams a k-block in ~0.6 us whatever
+// the grid, a launch costs ~6 us of prologue / drain, a split-K reduction pass ~3 us
+constexpr double kUsPerKb = 0.63, kUsLaunch = 6.0, kUsReduce = 3.0;
+int best_splits(int64_t ctas, int nkb, int sms, double* cost) {
   int splits = 1;
-  if (static_cast<int64_t>(gx) * gy * 2 <= ctx->num_sms) {
-    const int64_t cta = gx * static_cast<int64_t>(gy);
-    double best = static_cast<double>((cta + ctx->num_sms - 1) / ctx->num_sms);
+  double best = static_cast<double>((ctas + sms - 1) / sms) * nkb * kUsPerKb;
+  if (ctas * 2 <= sms)
     for (int sp = 2; sp <= 8 && nkb / sp >= 4; ++sp) {
-      const double cost = static_cast<double>((cta * sp + ctx->num_sms - 1) / ctx->num_sms) / sp;
-      if (cost < best - 1e-9) {
-        best = cost;
+      const double c = static_cast<double>((ctas * sp + sms - 1) / sms) * ((nkb + sp - 1) / sp) * kUsPerKb + kUsReduce;
+      if (c < best - 1e-9) {
+        best = c;
         splits = sp;
       }
     }
+  if (cost != nullptr) *cost = best + kUsLaunch;
+  return splits;
+}
+}  // namespace
+
+void launch_gemm_group(fq_ctx* ctx, const GemmJob* jobs, int n_jobs, int64_t T, const void* xt) {
+  if (n_jobs < 1 || n_jobs > kMaxProblems) fail(FQ_E_CONFIG, "gemm: 1..8 products per launch");
+  if (n_jobs > 1) {
+    // one launch for all, or one (possibly split-K) launch each: whichever the model says is faster
+    const int tn0 = T <= 32 ? 32 : kTN;
+    const int gy0 = ceil_div_i(T, tn0), nkb0 = ceil_div_i(jobs[0].L->K, kBlockK);
+    int64_t ctas = 0;
+    double separate = 0.0;
+    for (int j = 0; j < n_jobs; ++j) {
+      const int64_t c = static_cast<int64_t>(ceil_div_i(jobs[j].L->N, kTM)) * gy0;
+      ctas += c;
+      double cj = 0.0;
+      best_splits(c, nkb0, ctx->num_sms, &cj);
+      separate += cj;
+    }
+    const double grouped = static_cast<double>((ctas + ctx->num_sms - 1) / ctx->num_sms) * nkb0 * kUsPerKb + kUsLaunch;
+    if (separate < grouped) {
+      for (int j = 0; j < n_jobs; ++j) launch_gemm_group(ctx, jobs + j, 1, T, xt);
+      return;
+    }
   }
-  float* out = y;
-  int64_t out_stride = y_stride, split_stride = 0;
+  if (T < 1) fail(FQ_E_DIMENSION, "gemm: no rows");
+  if ((reinterpret_cast<uintptr_t>(xt) & 15) != 0) fail(FQ_E_CONFIG, "gemm: tiled activations must be 16-byte aligned");
+  const int64_t K = jobs[0].L->K;
+  const int tn = T <= 32 ? 32 : kTN;  // decode-sized batches: 32-token MMAs, a quarter of the activation traffic
+  GemmGroup g = {};
+  g.xt = static_cast<const uint8_t*>(xt);
+  g.T = static_cast<int>(T);
+  g.nkb = ceil_div_i(K, kBlockK);
+  int gx = 0;
+  for (int j = 0; j < n_jobs; ++j) {
+    const GemmJob& jb = jobs[j];
+    if (jb.rung != FQ_RUNG_INT8 && jb.rung != FQ_RUNG_INT4) fail(FQ_E_CONFIG, "gemm: rung must be 8 or 4");
+    if (jb.L->K != K) fail(FQ_E_DIMENSION, "gemm: products of one launch share K");
+    const fq_rung_store& st = jb.L->store(jb.rung);
+    if (!st.present || st.tiles == nullptr) fail(FQ_E_STATE, "gemm: rung not resident in the tiled layout");
+    GemmProblem& P = g.p[j];
+    P.tiles = st.tiles;
+    P.y = jb.y;
+    P.row_rung = jb.row_rung;
+    P.N = jb.L->N;
+    P.y_stride = jb.y_stride;
+    P.rr_stride = jb.rr_stride;
+    P.n_tiles = ceil_div_i(jb.L->N, kTileRows);
+    P.zbase = st.zp_base;
+    P.bits = st.bits;
+    P.accumulate = jb.accumulate ? 1 : 0;
+    P.want_rung = jb.rung;
+    gx = std::max(gx, ceil_div_i(jb.L->N, kTM));
+  }
+  const int gy = ceil_div_i(T, tn);
+  // split K (one product only) when the output tiles alone leave more than half the SMs idle
+  // (decode-sized batches), per the launch-time model; the partial sums are reduced by a separate
+  // deterministic pass
+  const int splits = n_jobs == 1 ? best_splits(static_cast<int64_t>(gx) * gy, g.nkb, ctx->num_sms, nullptr) : 1;
+  g.splits = splits;
+  const GemmJob& j0 = jobs[0];
   if (splits > 1) {
-    const size_t need = sizeof(float) * static_cast<size_t>(splits) * T * L->N;
+    const size_t need = sizeof(float) * static_cast<size_t>(splits) * T * j0.L->N;
     if (ctx->gemm_ws_bytes < need) {
-      dfree(ctx->gemm_ws);
+      if (ctx->gemm_ws != nullptr) ctx->retired.push_back(ctx->gemm_ws);  // captured graphs may hold it
       ctx->gemm_ws = static_cast<float*>(dmalloc(need));
       ctx->gemm_ws_bytes = need;
     }
-    out = ctx->gemm_ws;
-    out_stride = L->N;
-    split_stride = T * L->N;
+    g.p[0].y = ctx->gemm_ws;  // partials [split][T][N], reduced below
+    g.p[0].y_stride = j0.L->N;
+    g.p[0].accumulate = 0;
+    g.p[0].row_rung = nullptr;
+    g.split_stride = T * j0.L->N;
   }
-  const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
-  const int acc = splits > 1 ? 0 : (accumulate ? 1 : 0);
-  const auto* xb = static_cast<const uint8_t*>(xt);
-#define FQ_GEMM_LAUNCH(Wv, TNv)                                                                              \
-  do {                                                                                                      \
-    configure_gemm<Wv, TNv>();                                                                              \
-    FQ_CUDA(cudaLaunchKernelEx(&lc, gemm_ws_kernel<Wv, TNv>, st.tiles, n_tiles, nkb, st.zp_base, L->N, xb,                 \
-                               static_cast<int>(T), out, out_stride, acc, splits, split_stride,                \
-                               splits > 1 ? nullptr : row_rung, rr_stride, rung));                          \
-  } while (0)
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = grid;
-  lc.blockDim = dim3(tn == 32 ? gemm_threads<32>() : gemm_threads<128>());
+  lc.gridDim = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits * n_jobs));
   lc.stream = ctx->stream;
-  if (rung == FQ_RUNG_INT8) {
-    if (tn == 32) {
-      lc.dynamicSmemBytes = smem_gemm<32>();
-      FQ_GEMM_LAUNCH(0, 32);
-    } else {
-      lc.dynamicSmemBytes = smem_gemm<128>();
-      FQ_GEMM_LAUNCH(0, 128);
-    }
+  if (tn == 32) {
+    configure_gemm<32>();
+    lc.blockDim = dim3(gemm_threads<32>());
+    lc.dynamicSmemBytes = smem_gemm<32>();
+    FQ_CUDA(cudaLaunchKernelEx(&lc, gemm_ws_kernel<32>, g));
   } else {
-    if (tn == 32) {
-      lc.dynamicSmemBytes = smem_gemm<32>();
-      FQ_GEMM_LAUNCH(1, 32);
-    } else {
-      lc.dynamicSmemBytes = smem_gemm<128>();
-      FQ_GEMM_LAUNCH(1, 128);
-    }
+    configure_gemm<128>();
+    lc.blockDim = dim3(gemm_threads<128>());
+    lc.dynamicSmemBytes = smem_gemm<128>();
+    FQ_CUDA(cudaLaunchKernelEx(&lc, gemm_ws_kernel<128>, g));
   }
-#undef FQ_GEMM_LAUNCH
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;
   if (splits > 1) {
-    const int64_t total = T * L->N;
+    const int64_t total = T * j0.L->N;
     const int blocks = static_cast<int>(std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
-    split_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(ctx->gemm_ws, splits, T, L->N, y, y_stride, accumulate ? 1 : 0,
-                                                         row_rung, rr_stride, rung);
+    split_reduce_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(ctx->gemm_ws, splits, T, j0.L->N, j0.y, j0.y_stride,
+                                                                   j0.accumulate ? 1 : 0, j0.row_rung, j0.rr_stride,
+                                                                   j0.rung);
     FQ_CUDA(cudaGetLastError());
     ctx->launches += 1;
   }
+}
+
+void launch_gemm_dq(fq_ctx* ctx, const fq_layer* L, int rung, int64_t T, const void* xt, int x_dtype, float* y,
+                    int64_t y_stride, bool accumulate, const uint8_t* row_rung, int64_t rr_stride) {
+  if (x_dtype != FQ_DT_F16) fail(FQ_E_CONFIG, "gemm: the tiled activations are fp16 (bf16 values stored exactly)");
+  const GemmJob job{L, rung, y, y_stride, accumulate, row_rung, rr_stride};
+  launch_gemm_group(ctx, &job, 1, T, xt);
 }
 
 }  // namespace fqc

@@ -830,28 +830,40 @@ void batched_step_enqueue(fq_model* M, int B, const std::vector<uint8_t>& presen
   const StepMeta mt = M->meta(B);
   const uint8_t* table = M->table_dev();
   const int64_t nl = M->n_lin;
-  // one GEMM per copy present among the rows of linear i, each writing only its rows
-  auto linear = [&](int i, const void* xt, float* y, int64_t ys, bool acc) {
+  // one product per copy present among the rows of linear i, each writing only its rows; the
+  // products of linears that read the same activations go to one grouped launch (gemm_tc.cu)
+  std::vector<GemmJob> jobs;
+  auto add = [&](int i, float* y, int64_t ys, bool acc) {
     for (int r = FQ_RUNG_INT8; r <= FQ_RUNG_INT4; ++r)
-      if (present[static_cast<size_t>(i)] & (1u << r))
-        launch_gemm_dq(ctx, M->lin[i], r, B, xt, FQ_DT_F16, y, ys, acc, table + i, nl);
+      if (present[static_cast<size_t>(i)] & (1u << r)) jobs.push_back(GemmJob{M->lin[i], r, y, ys, acc, table + i, nl});
+  };
+  auto run = [&](const void* xt) {
+    for (size_t j = 0; j < jobs.size(); j += 8)
+      launch_gemm_group(ctx, jobs.data() + j, static_cast<int>(std::min<size_t>(8, jobs.size() - j)), B, xt);
+    jobs.clear();
+  };
+  auto linear = [&](int i, const void* xt, float* y, int64_t ys, bool acc) {
+    add(i, y, ys, acc);
+    run(xt);
   };
   prefill_embed(ctx, M->tok_emb, mt.tokens, B, d, w.x);
   for (int l = 0; l < c.n_layers; ++l) {
     const int b0 = M->lin_index(l, 0);
     const int64_t lo = static_cast<int64_t>(l) * M->layer_stride;
     prefill_rmsnorm(ctx, w.x, B, d, M->n1g[l], c.norm_eps, w.h, ad);
-    linear(b0 + 0, w.h, w.q, d, false);
-    linear(b0 + 1, w.h, w.k, d, false);
-    linear(b0 + 2, w.h, w.v, d, false);
+    add(b0 + 0, w.q, d, false);
+    add(b0 + 1, w.k, d, false);
+    add(b0 + 2, w.v, d, false);
+    run(w.h);
     batched_rope_append(ctx, w.q, w.k, w.v, B, H, hd, M->rope_cs, mt.pos, mt.slots, static_cast<__half*>(M->kv),
                         M->slot_stride, lo, c.max_seq_len, w.qr, ad);
     batched_attention(ctx, w.qr, static_cast<const __half*>(M->kv), B, H, hd, mt.pos, mt.slots, M->slot_stride, lo,
                       c.max_seq_len, w.a, ad);
     linear(b0 + 3, w.a, w.x, d, true);  // x += attn . Wo^T
     prefill_rmsnorm(ctx, w.x, B, d, M->n2g[l], c.norm_eps, w.h, ad);
-    linear(b0 + 4, w.h, w.g, f, false);
-    linear(b0 + 5, w.h, w.u, f, false);
+    add(b0 + 4, w.g, f, false);
+    add(b0 + 5, w.u, f, false);
+    run(w.h);
     prefill_swiglu(ctx, w.g, w.u, static_cast<int64_t>(B) * f, f, w.m, ad);
     linear(b0 + 6, w.m, w.x, d, true);  // x += mid . Wdown^T
   }
@@ -1053,17 +1065,23 @@ void prefill_gemm_enqueue(fq_model* M, int slot, const int32_t* tokens_host, int
     const int b = M->lin_index(l, 0);
     __half* kvl = kv_slot + static_cast<int64_t>(l) * M->layer_stride;
     prefill_rmsnorm(ctx, w.x, Ti, d, M->n1g[l], c.norm_eps, w.h, ad);
-    launch_gemm_dq(ctx, M->lin[b + 0], r[b + 0], T, w.h, FQ_DT_F16, w.q, d);
-    launch_gemm_dq(ctx, M->lin[b + 1], r[b + 1], T, w.h, FQ_DT_F16, w.k, d);
-    launch_gemm_dq(ctx, M->lin[b + 2], r[b + 2], T, w.h, FQ_DT_F16, w.v, d);
+    {  // q, k, v read the same activations: one grouped launch (gemm_tc.cu)
+      const GemmJob qkv[3] = {{M->lin[b + 0], r[b + 0], w.q, d, false, nullptr, 0},
+                              {M->lin[b + 1], r[b + 1], w.k, d, false, nullptr, 0},
+                              {M->lin[b + 2], r[b + 2], w.v, d, false, nullptr, 0}};
+      launch_gemm_group(ctx, qkv, 3, T, w.h);
+    }
     prefill_rope_kv(ctx, w.q, w.k, w.v, Ti, H, hd, M->rope_cs, w.qr, kvl, c.max_seq_len, ad);
     // causal attention of the prompt rows: 32 keys per warp round (batched.cu)
     batched_attention(ctx, w.qr, static_cast<const __half*>(M->kv), Ti, H, hd, nullptr, nullptr, M->slot_stride,
                       static_cast<int64_t>(l) * M->layer_stride, c.max_seq_len, w.a, ad, slot);
     launch_gemm_dq(ctx, M->lin[b + 3], r[b + 3], T, w.a, FQ_DT_F16, w.x, d, true);  // x += attn . Wo^T
     prefill_rmsnorm(ctx, w.x, Ti, d, M->n2g[l], c.norm_eps, w.h, ad);
-    launch_gemm_dq(ctx, M->lin[b + 4], r[b + 4], T, w.h, FQ_DT_F16, w.g, f);
-    launch_gemm_dq(ctx, M->lin[b + 5], r[b + 5], T, w.h, FQ_DT_F16, w.u, f);
+    {
+      const GemmJob gu[2] = {{M->lin[b + 4], r[b + 4], w.g, f, false, nullptr, 0},
+                             {M->lin[b + 5], r[b + 5], w.u, f, false, nullptr, 0}};
+      launch_gemm_group(ctx, gu, 2, T, w.h);
+    }
     prefill_swiglu(ctx, w.g, w.u, T * f, f, w.m, ad);
     launch_gemm_dq(ctx, M->lin[b + 6], r[b + 6], T, w.m, FQ_DT_F16, w.x, d, true);  // x += mid . Wdown^T
   }
