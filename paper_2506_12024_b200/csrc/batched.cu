@@ -22,13 +22,12 @@ __global__ void rope_append_rows_kernel(const float* __restrict__ q, const float
                                         const int32_t* __restrict__ pos, const int32_t* __restrict__ slots,
                                         __half* __restrict__ kv, int64_t slot_stride, int64_t layer_off,
                                         int64_t max_seq, float* __restrict__ qr, int f16) {
-  const int b = blockIdx.x;
+  const int b = blockIdx.x, h = blockIdx.y;  // one block per (row, head): B x H blocks of hd / 2 threads
   const int d = H * hd, half = hd / 2;
   const int p = pos[b];
   const float scale = 1.0f / sqrtf(static_cast<float>(hd));
   __half* kvl = kv + static_cast<int64_t>(slots[b]) * slot_stride + layer_off;
-  for (int idx = threadIdx.x; idx < H * half; idx += blockDim.x) {
-    const int h = idx / half, i = idx - h * half;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
     const int64_t o0 = static_cast<int64_t>(b) * d + h * hd + i, o1 = o0 + half;
     const float2 c = cs[static_cast<int64_t>(p) * half + i];
     const float q0 = actr(q[o0], f16), q1 = actr(q[o1], f16);
@@ -75,10 +74,14 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
     float s = -INFINITY;
     if (j < n) {
       const uint4* kr = reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(j) * hd);
+      // the lane's whole K row in flight at once (one memory latency per round, not hd / 32)
+      uint4 kw[hd / 8];
+#pragma unroll
+      for (int c = 0; c < hd / 8; ++c) kw[c] = kr[c];
       float acc = 0.f;
-#pragma unroll 4
+#pragma unroll
       for (int c = 0; c < hd / 8; ++c) {
-        const uint4 w = kr[c];
+        const uint4 w = kw[c];
         const __half2* h2 = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -101,15 +104,15 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
     l = l * fa + ps;
 #pragma unroll
     for (int e = 0; e < DPL; ++e) o[e] *= fa;
-    // P.V: the lanes own DPL dimensions; the round's V rows load 8 at a time, all in flight
+    // P.V: the lanes own DPL dimensions; the round's V rows load 16 at a time, all in flight
     // together (p_j of keys past the history is 0, their rows are not read)
     const int cnt = min(32, n - j0);
 #pragma unroll
-    for (int jb = 0; jb < 32; jb += 8) {
+    for (int jb = 0; jb < 32; jb += 16) {
       if (jb >= cnt) break;
-      float vv[8][DPL];
+      float vv[16][DPL];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const int jj = min(jb + u, cnt - 1);
         const __half* vr = vc + static_cast<int64_t>(j0 + jj) * hd + DPL * lane;
         if constexpr (DPL == 4) {
@@ -123,7 +126,7 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const float pj = __shfl_sync(0xffffffffu, p, jb + u);  // 0 for keys past the history
 #pragma unroll
         for (int e = 0; e < DPL; ++e) o[e] = fmaf(pj, vv[u][e], o[e]);
@@ -144,7 +147,7 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
 void batched_rope_append(fq_ctx* ctx, const float* q, const float* k, const float* v, int B, int H, int hd,
                          const float2* cs, const int32_t* pos, const int32_t* slots, __half* kv, int64_t slot_stride,
                          int64_t layer_off, int64_t max_seq, float* qr, int act_dtype) {
-  rope_append_rows_kernel<<<B, 256, 0, ctx->stream>>>(q, k, v, H, hd, cs, pos, slots, kv, slot_stride, layer_off, max_seq,
+  rope_append_rows_kernel<<<dim3(B, H), hd / 2, 0, ctx->stream>>>(q, k, v, H, hd, cs, pos, slots, kv, slot_stride, layer_off, max_seq,
                                                       qr, act_dtype == FQ_DT_F16 ? 1 : 0);
   FQ_CUDA(cudaGetLastError());
   ctx->launches += 1;

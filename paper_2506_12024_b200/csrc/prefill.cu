@@ -33,10 +33,16 @@ __global__ void embed_rows_kernel(const float* __restrict__ tok_emb, const int32
 // h[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * g)
 __global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, const float* __restrict__ g, float eps,
                                     uint16_t* __restrict__ h, int nkb, int f16) {
+  // one row per block; d % 4 == 0 (the caller checks): float4 loads, 4 consecutive k -> one 8-byte
+  // store in the tiled layout (k & 7 groups of 8 are contiguous)
   const int t = blockIdx.x;
-  const float* xr = x + t * d;
+  const float4* xr = reinterpret_cast<const float4*>(x + t * d);
+  const int64_t d4 = d / 4;
   float s = 0.f;
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s += xr[i] * xr[i];
+  for (int64_t i = threadIdx.x; i < d4; i += blockDim.x) {
+    const float4 v = xr[i];
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
   __shared__ float red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -50,7 +56,13 @@ __global__ void rmsnorm_rows_kernel(const float* __restrict__ x, int64_t d, cons
   }
   __syncthreads();
   const float rstd = 1.0f / sqrtf(red[0] / static_cast<float>(d) + eps);
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) h[tiled_act_offset(t, i, nkb)] = actb(xr[i] * rstd * g[i], f16);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t i = threadIdx.x; i < d4; i += blockDim.x) {
+    const float4 v = xr[i], w = g4[i];
+    const uint32_t lo = actb(v.x * rstd * w.x, f16) | (static_cast<uint32_t>(actb(v.y * rstd * w.y, f16)) << 16);
+    const uint32_t hi = actb(v.z * rstd * w.z, f16) | (static_cast<uint32_t>(actb(v.w * rstd * w.w, f16)) << 16);
+    *reinterpret_cast<uint2*>(h + tiled_act_offset(t, 4 * i, nkb)) = make_uint2(lo, hi);
+  }
 }
 
 // q/k/v rows (fp32 GEMM outputs, rounded to bf16 as the decode step stores them) -> RoPE'd and
@@ -111,6 +123,7 @@ void prefill_embed(fq_ctx* ctx, const float* tok_emb, const int32_t* tokens_dev,
 }
 
 void prefill_rmsnorm(fq_ctx* ctx, const float* x, int T, int64_t d, const float* g, float eps, void* h16, int act_dtype) {
+  if (d % 4 != 0 || (reinterpret_cast<uintptr_t>(g) & 15) != 0) fail(FQ_E_DIMENSION, "rmsnorm rows: d must be a multiple of 4");
   rmsnorm_rows_kernel<<<T, 256, 0, ctx->stream>>>(x, d, g, eps, static_cast<uint16_t*>(h16), ceil_div_i(d, 128),
                                                   act_dtype == FQ_DT_F16 ? 1 : 0);
   FQ_CUDA(cudaGetLastError());
