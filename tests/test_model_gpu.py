@@ -337,4 +337,28 @@ def test_llama_logit_kl_calibration_tensor_core(ctx):
     want = tot / 40
     print("logit KL (tcgen05 path)", kl[0], want)
     assert abs(kl[0] - want) <= 1e-4, (kl[0], want)  # north_star: KL within 1e-4 absolute
+
+
+def test_llama_calibration_block_reuse_is_exact(ctx, monkeypatch):
+    """The tensor-core calibration starts the forward with block fl flipped at block fl, from the
+    base forward's residual-stream snapshot (the blocks below are identical): every block's KL and
+    entropy equal the full-forward run bit for bit (FQ_CALIB_FULL), and each block's KL follows the
+    teacher-forced oracle with that block flipped."""
+    m, orc = _llama(ctx, max_batch=1, cfg=dict(LLAMA_TINY, max_seq_len=32))
+    toks = oracle.random_tokens(2 * 20, 8192, 7).reshape(2, 20)
+    kl, ent = m.calibrate_logit_kl(toks, capi.RUNG_INT8, capi.RUNG_INT4)
+    monkeypatch.setenv("FQ_CALIB_FULL", "1")
+    kl_full, ent_full = m.calibrate_logit_kl(toks, capi.RUNG_INT8, capi.RUNG_INT4)
+    assert np.array_equal(kl, kl_full) and np.array_equal(ent, ent_full), (kl, kl_full)
+    per = 7  # linears per block
+    for fl in range(len(kl)):
+        tot = 0.0
+        for s in range(2):
+            c8, c4 = orc.new_cache(), orc.new_cache()
+            r4 = [4 if fl * per <= i < (fl + 1) * per else 8 for i in range(len(orc.ids))]
+            for t in toks[s]:
+                a = orc.step(int(t), c8, [8] * len(orc.ids))
+                b = orc.step(int(t), c4, r4)
+                tot += oracle.kl_logits(b, a)[0]
+        assert abs(kl[fl] - tot / 40) <= 1e-4, (fl, kl[fl], tot / 40)
     assert m.slot_length(0) == 0

@@ -27,7 +27,11 @@ def main():
     ap.add_argument("--seqs", type=int, default=64)
     ap.add_argument("--len", type=int, default=512)
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--full", action="store_true", help="every flipped forward from the embedding (FQ_CALIB_FULL)")
+    ap.add_argument("--dump", default="", help="write the per-block KL / entropy arrays (.npy pair prefix)")
     a = ap.parse_args()
+    if a.full:
+        os.environ["FQ_CALIB_FULL"] = "1"
     ctx = capi.Context(0)
     m = capi.Model(ctx, arch=capi.ARCH_LLAMA, act_dtype=capi.DT_BF16, max_batch=1, group_size=128,
                    max_seq_len=a.len + 8, vocab_size=32000, d_model=4096, n_heads=32, head_dim=128,
@@ -39,11 +43,20 @@ def main():
     kl, ent = m.calibrate_logit_kl(toks, capi.RUNG_INT8, capi.RUNG_INT4)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    params = a.layers * (4 * 4096 * 4096 + 3 * 4096 * 11008) + 32000 * 4096
-    flops = 2.0 * params * a.seqs * a.len * (a.layers + 1)
+    if a.dump:
+        np.save(a.dump + "_kl.npy", np.asarray(kl))
+        np.save(a.dump + "_ent.npy", np.asarray(ent))
+    lp, hp = 4 * 4096 * 4096 + 3 * 4096 * 11008, 32000 * 4096
+    full_flops = 2.0 * (a.layers * lp + hp) * a.seqs * a.len * (a.layers + 1)  # 33 full forwards
+    # executed: the base forward, then forward fl runs blocks fl.. only (the blocks below are the
+    # base forward's, reused from its residual-stream snapshots) unless --full
+    run_layers = a.layers + sum(a.layers if a.full else a.layers - fl for fl in range(a.layers))
+    exec_flops = 2.0 * (run_layers * lp + (a.layers + 1) * hp) * a.seqs * a.len
     order = sorted(range(a.layers), key=lambda i: (kl[i], i))
     print(json.dumps({"config": "C4", "seqs": a.seqs, "len": a.len, "blocks": a.layers, "forwards": a.layers + 1,
-                      "seconds": round(dt, 2), "tflops": round(flops / dt / 1e12, 1),
+                      "block_reuse": not a.full, "seconds": round(dt, 2),
+                      "tflops_executed": round(exec_flops / dt / 1e12, 1),
+                      "full_forward_equivalent_tflops": round(full_flops / dt / 1e12, 1),
                       "kl_min": float(np.min(kl)), "kl_max": float(np.max(kl)),
                       "entropy_mean": float(np.mean(ent)), "switch_order_blocks": order}), flush=True)
 
