@@ -301,14 +301,22 @@ def test_llama_tensor_core_prefill_matches_oracle(ctx, n, mixed, cfg):
     assert m.slot_length(0) == n
     got = out.cpu().numpy()
     cache = orc.new_cache()
+    wants = [orc.step(int(toks[i]), cache, rungs) for i in range(n)]
+    # entropy bar: north_star's 1e-4 qualified by the conditioning of the bf16 activation roundings,
+    # as in test_c3_shape_gpu.py -- the oracle's own fp32-accumulation run moves by `env`
+    o32 = orc.variant(acc="f32")
+    c32 = o32.new_cache()
+    env = max(abs(oracle.row_stats(o32.step(int(toks[i]), c32, rungs))["entropy"] - oracle.row_stats(wants[i])["entropy"])
+              for i in range(n))
+    bar = 1e-4 + 3.0 * env
     for i in range(n):
-        want = orc.step(int(toks[i]), cache, rungs)
+        want = wants[i]
         rel = np.max(np.abs(got[i] - want)) / np.max(np.abs(want))
         assert rel < 1e-2, (i, rel)
         o = oracle.row_stats(got[i])
         assert abs(st["entropy"][i] - o["entropy"]) <= 1e-5
         assert int(st["argmax"][i]) == o["argmax"]
-        assert abs(st["entropy"][i] - oracle.row_stats(want)["entropy"]) <= 1e-4
+        assert abs(st["entropy"][i] - oracle.row_stats(want)["entropy"]) <= bar, (i, bar, env)
     # decode continues from the cache the prefill wrote (K/V rows 0..n-1 of every layer)
     dec = torch.zeros((1, V), dtype=torch.float32, device="cuda")
     for t in toks[n:]:
