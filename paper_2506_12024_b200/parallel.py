@@ -78,3 +78,23 @@ def merge_shards(per_rank: Sequence[Sequence[Any]], n_items: int) -> List[Any]:
         for i, v in zip(rng, items):
             out[i] = v
     return out
+
+
+def allreduce_block_kl(kl_mean, ent_mean, rows: int, device=None):
+    """C4 calibration sharded by sequence: each rank calibrates its shard of the
+    sequences (per-block mean KL / entropy over its `rows` tokens); one all-reduce (sum) of the
+    per-block partial sums, 2 x n_blocks + 1 doubles, gives the means over every token.  Returns
+    (kl_mean, ent_mean, total_rows) as float64 numpy arrays."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    kl = np.asarray(kl_mean, dtype=np.float64)
+    ent = np.asarray(ent_mean, dtype=np.float64)
+    part = np.concatenate([kl * rows, ent * rows, [float(rows)]])
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        t = torch.tensor(part, dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        part = t.cpu().numpy()
+    n = kl.size
+    total = part[-1]
+    return part[:n] / total, part[n:2 * n] / total, int(total)

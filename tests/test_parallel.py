@@ -86,3 +86,43 @@ def test_bench_gpus_flag_launches_the_ranks():
     assert len(lines) == 1, r.stdout
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["impl"] == "reference" and line["value"] > 0
+
+
+def _calib_worker(rank, world, port, q):
+    import numpy as np
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # per-token KL / entropy of 5 sequences x 4 tokens for 3 blocks, sharded by sequence
+        rng = np.random.default_rng(11)
+        kl_tok = rng.random((5, 4, 3))
+        ent_tok = rng.random((5, 4, 3)) + 5.0
+        mine = parallel.shard(5, rank, world)
+        kl_loc = kl_tok[mine.start:mine.stop].reshape(-1, 3).mean(axis=0)
+        ent_loc = ent_tok[mine.start:mine.stop].reshape(-1, 3).mean(axis=0)
+        kl, ent, rows = parallel.allreduce_block_kl(kl_loc, ent_loc, len(mine) * 4)
+        q.put((rank, kl.tolist(), ent.tolist(), rows,
+               kl_tok.reshape(-1, 3).mean(axis=0).tolist(), ent_tok.reshape(-1, 3).mean(axis=0).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_c4_calibration_merge():
+    """C4 sharded by sequence: one all-reduce of the per-block partial sums reproduces the
+    per-block means over every token (tools/calibrate_c4.py under torchrun)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_calib_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, kl, ent, rows, kl_want, ent_want in outs:
+        assert rows == 20
+        assert kl == pytest.approx(kl_want, rel=1e-12, abs=1e-15)
+        assert ent == pytest.approx(ent_want, rel=1e-12)
