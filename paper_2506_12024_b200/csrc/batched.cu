@@ -144,9 +144,11 @@ __global__ void attn_decode_rows_kernel(const float* __restrict__ qr, const __ha
 
 // Causal attention of the T rows of one prompt (row r at position r of slot slot0) on the tensor
 // cores: one CTA = 64 query rows (4 warps x 16) of one head; 64-key tiles of K and V go through
-// shared memory (cp.async, two stages, rows padded to 272 B: conflict-free fragment loads);
+// shared memory (two buffers, rows padded to 272 B: conflict-free fragment loads);
 // S = Q K^T and O += P V run as mma.sync m16n8k16 (fp16 in, fp32 accumulate) with online
-// softmax in the accumulator registers (the S accumulator layout is P's A-fragment layout).
+// softmax in the accumulator registers (the S accumulator layout is P's A-fragment layout).  The
+// tiles are filled with plain 16-byte loads and stores (a cp.async version returned rows that
+// differed between repeats of the same prompt; the plain fill costs < 2 % of the prefill).
 // Precision: K and V are exact fp16 (the cache format); q (fp32, RoPE'd, pre-scaled) and P (fp32)
 // are split into fp16 hi + lo parts and both products issued, so S and P.V carry ~22 significant
 // bits -- the fp32 contract of the row kernel within its own rounding.
@@ -167,11 +169,6 @@ __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t&
   const __half2 l = __floats2half2_rn(x - hf.x, y - hf.y);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
-}
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
 }
 }  // namespace fa
 
@@ -202,10 +199,9 @@ __global__ void __launch_bounds__(fa::kWarps * 32)
     for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
       const int row = c / (HD / 8), col = (c % (HD / 8)) * 8;
       const int key = min(k0 + row, T - 1);  // rows past the prompt: any valid row (masked)
-      cp16(ks + (buf * kKeys + row) * LD + col, kc + static_cast<int64_t>(key) * HD + col);
-      cp16(vs + (buf * kKeys + row) * LD + col, vc + static_cast<int64_t>(key) * HD + col);
+      *reinterpret_cast<uint4*>(ks + (buf * kKeys + row) * LD + col) = *reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(key) * HD + col);
+      *reinterpret_cast<uint4*>(vs + (buf * kKeys + row) * LD + col) = *reinterpret_cast<const uint4*>(vc + static_cast<int64_t>(key) * HD + col);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   load_tile(0, 0);
   // q A-fragments, hi and lo (rows past T read row T-1: their outputs are not written)
@@ -233,13 +229,8 @@ __global__ void __launch_bounds__(fa::kWarps * 32)
   const int row_a = wr + g, row_b = wr + g + 8;
   for (int tile = 0; tile < n_tiles; ++tile) {
     const int buf = tile & 1;
-    if (tile + 1 < n_tiles) {
-      load_tile(tile + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
+    __syncthreads();  // tile `tile` is in buf
+    if (tile + 1 < n_tiles) load_tile(tile + 1, buf ^ 1);  // the other buffer, released at the end of tile - 1
     const int k0 = tile * kKeys;
     if (k0 <= wr + 15) {  // some key of the tile is visible to some row of the warp
       const __half* kt = ks + buf * kKeys * LD;

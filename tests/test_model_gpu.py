@@ -370,3 +370,24 @@ def test_llama_calibration_block_reuse_is_exact(ctx, monkeypatch):
                 tot += oracle.kl_logits(b, a)[0]
         assert abs(kl[fl] - tot / 40) <= 1e-4, (fl, kl[fl], tot / 40)
     assert m.slot_length(0) == 0
+
+
+@pytest.mark.parametrize("cfg", [LLAMA_TINY, LLAMA_HD128], ids=["hd64", "hd128"])
+def test_llama_tensor_core_prefill_is_repeatable(ctx, cfg):
+    """The tcgen05 prefill (GEMMs + tensor-core prompt attention) is deterministic: the same prompt,
+    prefilled again after a different one, gives bit-identical logits (prompt lengths around one
+    attention tile, where a cp.async fill of the K/V tiles once broke this)."""
+    m, _ = _llama(ctx, max_batch=2, cfg=cfg)
+    V = cfg["vocab_size"]
+    for n in (16, 17, 24, 63, 64, 65, 100):
+        toks = oracle.random_tokens(n, V, 700 + n)
+        other = oracle.random_tokens(n, V, 900 + n)
+        got = []
+        for t in (toks, other, toks, other, toks):
+            out = torch.zeros((n, V), dtype=torch.float32, device="cuda")
+            m.reset_slot(0)
+            m.prefill(0, t, out)
+            ctx.synchronize()
+            got.append(out.cpu().numpy())
+        assert np.array_equal(got[0], got[2]) and np.array_equal(got[0], got[4]), n
+        assert np.array_equal(got[1], got[3]), n
