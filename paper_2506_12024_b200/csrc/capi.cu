@@ -95,7 +95,6 @@ fq_status fq_ctx_destroy(fq_ctx* ctx) {
     dfree(ctx->gemv_flags);
     dfree(ctx->launch_ctr);
     dfree(ctx->gemm_ws);
-    dfree(ctx->gemm_cnt);
     for (void* r : ctx->retired) dfree(r);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;

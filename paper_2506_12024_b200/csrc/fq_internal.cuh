@@ -57,10 +57,8 @@ struct fq_ctx {
   float* gemv_fix = nullptr;
   unsigned int* gemv_flags = nullptr;
   unsigned int* launch_ctr = nullptr;  // [epoch, done] of the program kernels on this context
-  float* gemm_ws = nullptr;  // stream-K partial tiles of the tensor-core GEMM (grown on demand)
+  float* gemm_ws = nullptr;  // split-K partial sums of the tensor-core GEMM (grown on demand)
   size_t gemm_ws_bytes = 0;
-  int* gemm_cnt = nullptr;   // per-tile arrival counters (zero between launches)
-  int64_t gemm_cnt_n = 0;
   std::vector<void*> retired;  // outgrown workspaces captured graphs may still point at (freed at destroy)
   // bumped whenever a layer's resident copies change (upload, device quantization): models
   // drop step programs and captured graphs built against older weight pointers

@@ -317,7 +317,7 @@ struct fq_model {
   std::map<int, int64_t> graph_kernels;  // kernels inside each captured step graph
   std::map<std::pair<int, int>, ProgramRun> programs;  // (batch, StepMode) -> uploaded program
   unsigned int* grid_barrier = nullptr;
-  bool use_graphs = true;
+  bool use_graphs = std::getenv("FQ_NO_GRAPHS") == nullptr;  // FQ_NO_GRAPHS: plain launches (the tests' control)
   uint64_t built_epoch = 0;  // ctx->weight_epoch the cached programs / graphs were built at
   // batched tensor-core steps: captured graphs per (copies per linear, B) signature
   std::map<std::string, std::pair<cudaGraphExec_t, int64_t>> batch_graphs;
@@ -1016,6 +1016,13 @@ void free_prefill_ws(fq_model* M) {
 void ensure_prefill_ws(fq_model* M, int64_t T) {
   auto& w = M->pw;
   if (T <= w.cap) return;
+  // the batched decode step's captured graphs run on these buffers: drop them with the buffers
+  if (!M->batch_graphs.empty()) {
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    for (auto& kv : M->batch_graphs) cudaGraphExecDestroy(kv.second.first);
+    M->batch_graphs.clear();
+    M->batch_seen.clear();
+  }
   free_prefill_ws(M);
   const fq_model_config& c = M->cfg;
   const int64_t cap = std::min<int64_t>(c.max_seq_len, (T + 63) / 64 * 64);

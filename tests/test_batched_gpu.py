@@ -89,3 +89,39 @@ def test_batched_path_agrees_with_step_program(ctx):
             assert abs(r1["entropy"] - rows[t]["entropy"][s]) <= 5e-4
     m.close()
     m1.close()
+
+
+def test_batched_graphs_survive_a_larger_prefill(ctx, monkeypatch):
+    """The batched step's CUDA graphs run on the prefill workspace; a longer prompt reallocates that
+    workspace, so the graphs must be rebuilt (replaying them read freed buffers before).  Steps
+    after the regrow equal the same steps of a model that never captured a graph."""
+    cfg = dict(TINY, max_seq_len=128)
+    B = 16
+    outs = []
+    for graphs in (True, False):
+        if not graphs:
+            monkeypatch.setenv("FQ_NO_GRAPHS", "1")  # read when the model is created
+        m = capi.Model(ctx, arch=capi.ARCH_LLAMA, act_dtype=capi.DT_BF16, max_batch=B, group_size=128, **cfg)
+        orc = oracle.llama.LlamaOracle(dict(cfg, group_size=128), seed=4)
+        orc.upload(m, capi)
+        V = cfg["vocab_size"]
+        rng = np.random.default_rng(9)
+        for s in range(B):
+            m.reset_slot(s)
+            m.prefill(s, oracle.random_tokens(16, V, 50 + s))
+        toks = [int(t) for t in rng.integers(0, V, B)]
+        out = torch.zeros((B, V), dtype=torch.float32, device="cuda")
+        got = []
+        for step in range(6):
+            if step == 3:  # a 100-token prompt regrows the prefill workspace under live graphs
+                m.reset_slot(B - 1)
+                m.prefill(B - 1, oracle.random_tokens(100, V, 77))
+            st = m.decode(list(range(B)), toks, out)
+            ctx.synchronize()
+            got.append(out.cpu().numpy().copy())
+            toks = [int(r["argmax"]) for r in st]
+        outs.append(got)
+        m.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.all(np.isfinite(a))
+        assert np.array_equal(a, b)
