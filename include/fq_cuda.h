@@ -277,6 +277,57 @@ fq_status fq_model_calibrate_logit_kl(fq_model* model, const int32_t* tokens_hos
                                       int64_t len, int32_t base_rung, int32_t flip_rung,
                                       double* kl_host, double* entropy_host);
 
+/* ------------------------------------------- tensor-parallel variant (north_star)
+ * The reference has no distribution (its block is src/model.cpp:201-233 on one core); this is
+ * the variant north_star names: column-split q/k/v/gate/up, row-split o/down and a vocab-split
+ * head, with one all-reduce (sum) of an fp32 [batch, d_model] partial after each row-split
+ * projection and one all-gather of the head's softmax partials.  The collectives are the
+ * caller's (NCCL over NVLink through torch.distributed in paper_2506_12024_b200/tp.py). */
+typedef struct fq_tp_shard {
+  int32_t rank, size;
+  int64_t head0, heads;  /* attention heads [head0, head0 + heads) */
+  int64_t ffn0, ffn;     /* SwiGLU columns [ffn0, ffn0 + ffn), whole quantization groups */
+  int64_t vocab0, vocab; /* head rows [vocab0, vocab0 + vocab) */
+  int32_t n_segments;    /* 2 * n_layers + 1 */
+} fq_tp_shard;
+/* Mergeable softmax partial of one logits row (max m, S = sum e^(l-m), T = sum e^(l-m)(l-m) in
+ * double, the two largest logits, the lowest index of the largest); 32 bytes. */
+typedef struct fq_stat_part {
+  double S, T;
+  float m, v1, v2;
+  int32_t arg;
+} fq_stat_part;
+/* Host only: the shard of rank `rank` of `size` (heads split evenly -- n_heads % size == 0 and
+ * each rank's heads * head_dim a multiple of group_size; ffn split in whole groups, the ragged
+ * tail group on the last rank; vocab rows split evenly). */
+fq_status fq_tp_shard_spec(const fq_model_config* cfg, int32_t rank, int32_t size, fq_tp_shard* out);
+/* Host only: the quantized sub-matrix rows [row0, row1) x columns [col0, col1) of a g-grouped
+ * QuantizedTensor of an [N, K] weight (quantizer.hpp:24-44 in the g128 view: codes row-major,
+ * one scale / zero point per (row, group)); col0 a multiple of `group`, col1 a multiple of
+ * `group` or K.  Bit-identical to quantizing the sliced fp32 weights (groups are independent). */
+fq_status fq_shard_quantized(int32_t bits, int64_t N, int64_t K, int64_t group, const uint8_t* payload,
+                             const float* scale, const int32_t* zp, int64_t row0, int64_t row1, int64_t col0,
+                             int64_t col1, uint8_t* payload_out, float* scale_out, int32_t* zp_out);
+/* Host only: merges the ranks' head partials parts[rank * batch + b] (argmax indices local to the
+ * rank's vocab slice, offset by vocab0[rank]) into the row statistics of softmax_double /
+ * ppl_entropy / fault_tolerance / argmax_token (src/scheduler.cpp:13-49, src/engine.cpp:144-155). */
+fq_status fq_tp_merge_stats(const fq_stat_part* parts, int32_t nranks, int32_t batch, const int64_t* vocab0,
+                            fq_row_stats* out);
+/* A TP rank of the llama config `cfg` (the FULL model's config): its linears have the shard's
+ * shapes (upload the fq_shard_quantized slices), the embedding and norms are full. */
+fq_status fq_model_create_tp(fq_ctx* ctx, const fq_model_config* cfg, int32_t tp_rank, int32_t tp_size,
+                             fq_model** out);
+fq_status fq_model_tp_shard(const fq_model* model, fq_tp_shard* out);
+/* Starts one TP decode step for `batch` slots (stages tokens, positions and precision rows). */
+fq_status fq_model_tp_begin(fq_model* model, int32_t batch, const int32_t* slots_host,
+                            const int32_t* tokens_host);
+/* Enqueues segment `seg` (0 .. n_segments-1, in order) on the context stream.  reduced_dev: the
+ * sum over ranks of the previous segment's partials (fp32 [batch, d_model]; NULL for seg 0).
+ * out_dev: seg < n_segments-1 -> this rank's fp32 [batch, d_model] partial of the O / down
+ * projection; the last segment -> fq_stat_part [batch] of the rank's vocab slice (its logits
+ * stay in fq_model_logits, [batch, shard.vocab]).  The last segment completes the step. */
+fq_status fq_model_tp_segment(fq_model* model, int32_t seg, const float* reduced_dev, void* out_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,17 @@ ROW_STATS_DTYPE = np.dtype([("ppl_entropy", np.float64), ("entropy", np.float64)
 assert ROW_STATS_DTYPE.itemsize == C.sizeof(RowStats)
 
 
+class TpShard(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("size", C.c_int32), ("head0", C.c_int64), ("heads", C.c_int64),
+                ("ffn0", C.c_int64), ("ffn", C.c_int64), ("vocab0", C.c_int64), ("vocab", C.c_int64),
+                ("n_segments", C.c_int32)]
+
+
+STAT_PART_DTYPE = np.dtype([("S", np.float64), ("T", np.float64), ("m", np.float32), ("v1", np.float32),
+                            ("v2", np.float32), ("arg", np.int32)])
+assert STAT_PART_DTYPE.itemsize == 32
+
+
 class ModelConfig(C.Structure):
     _fields_ = [("arch", C.c_int32), ("act_dtype", C.c_int32), ("vocab_size", C.c_int64), ("d_model", C.c_int64),
                 ("n_heads", C.c_int64), ("head_dim", C.c_int64), ("n_layers", C.c_int64), ("ffn_dim", C.c_int64),
@@ -139,6 +150,7 @@ def load(path: str = LIB_PATH):
         "fq_model_linear_index": [v, C.c_char_p, C.POINTER(i32)],
         "fq_model_linear": [v, i32, C.POINTER(v)],
         "fq_model_set_param": [v, C.c_char_p, v, i64],
+        "fq_model_get_param": [v, C.c_char_p, v, i64],
         "fq_model_init_random": [v, u64, C.c_float],
         "fq_model_init_random_kl": [v, u64, C.c_float, i32, v, v],
         "fq_model_set_rung": [v, i32, i32, i32],
@@ -155,6 +167,13 @@ def load(path: str = LIB_PATH):
         "fq_model_profile_gemvs": [v, i32, i32, C.POINTER(C.c_double), C.POINTER(i64), C.POINTER(i64)],
         "fq_model_profile_step": [v, i32, i32, v, i64, C.POINTER(i32), C.POINTER(i32), v],
         "fq_gemm": [v, v, i32, i64, v, i64, v, i64],
+        "fq_tp_shard_spec": [C.POINTER(ModelConfig), i32, i32, C.POINTER(TpShard)],
+        "fq_shard_quantized": [i32, i64, i64, i64, v, v, v, i64, i64, i64, i64, v, v, v],
+        "fq_tp_merge_stats": [v, i32, i32, v, v],
+        "fq_model_create_tp": [v, C.POINTER(ModelConfig), i32, i32, C.POINTER(v)],
+        "fq_model_tp_shard": [v, C.POINTER(TpShard)],
+        "fq_model_tp_begin": [v, i32, v, v],
+        "fq_model_tp_segment": [v, i32, v, v],
         "fq_tile_activations": [v, v, i32, i64, i64, i64, i32, v],
         "fq_gemm_tiled": [v, v, i32, i64, v, i32, v, i64, i32],
     }
@@ -357,15 +376,52 @@ def model_config(**kw) -> ModelConfig:
     return c
 
 
-class Model:
-    """fq_model: the device-resident decoder (precision table, KV caches, decode step)."""
+def tp_shard_spec(cfg: ModelConfig, rank: int, size: int) -> TpShard:
+    """The shard of TP rank `rank` of `size` (host only, no GPU needed)."""
+    sh = TpShard()
+    check(load().fq_tp_shard_spec(C.byref(cfg), rank, size, C.byref(sh)))
+    return sh
 
-    def __init__(self, ctx: Context, **cfg):
+
+def shard_quantized(bits: int, N: int, K: int, group: int, payload, scale, zp, rows, cols):
+    """Rows [r0, r1) x columns [c0, c1) of a g-grouped quantized [N, K] weight (host only)."""
+    (r0, r1), (c0, c1) = rows, cols
+    ng_out = (c1 - c0 + group - 1) // group
+    n = r1 - r0
+    pl = np.zeros(n * (c1 - c0) * bits // 8, np.uint8)
+    sc = np.zeros(n * ng_out, np.float32)
+    z = np.zeros(n * ng_out, np.int32)
+    payload = np.ascontiguousarray(payload, np.uint8)
+    scale = np.ascontiguousarray(scale, np.float32)
+    zp = np.ascontiguousarray(zp, np.int32)
+    check(load().fq_shard_quantized(bits, N, K, group, _ptr(payload), _ptr(scale), _ptr(zp), r0, r1, c0, c1,
+                                    _ptr(pl), _ptr(sc), _ptr(z)))
+    return pl, sc, z
+
+
+def tp_merge_stats(parts: np.ndarray, vocab0) -> np.ndarray:
+    """parts: STAT_PART_DTYPE [nranks, batch] -> ROW_STATS_DTYPE [batch] (host only)."""
+    parts = np.ascontiguousarray(parts, STAT_PART_DTYPE)
+    nr, b = parts.shape
+    v0 = np.ascontiguousarray(vocab0, np.int64)
+    out = np.zeros(b, ROW_STATS_DTYPE)
+    check(load().fq_tp_merge_stats(_ptr(parts), nr, b, _ptr(v0), _ptr(out)))
+    return out
+
+
+class Model:
+    """fq_model: the device-resident decoder (precision table, KV caches, decode step).
+    tp=(rank, size): a tensor-parallel rank of the full config (see tp.py)."""
+
+    def __init__(self, ctx: Context, tp=None, **cfg):
         self.ctx = ctx
         self.L = ctx.L
         self.cfg = model_config(**cfg)
         h = C.c_void_p()
-        check(self.L.fq_model_create(ctx.h, C.byref(self.cfg), C.byref(h)))
+        if tp is None:
+            check(self.L.fq_model_create(ctx.h, C.byref(self.cfg), C.byref(h)))
+        else:
+            check(self.L.fq_model_create_tp(ctx.h, C.byref(self.cfg), int(tp[0]), int(tp[1]), C.byref(h)))
         self.h = h
         n = C.c_int32()
         check(self.L.fq_model_num_linears(h, C.byref(n)))
@@ -390,6 +446,11 @@ class Model:
     def set_param(self, name: str, arr: np.ndarray) -> None:
         a = np.ascontiguousarray(arr, np.float32)
         check(self.L.fq_model_set_param(self.h, name.encode(), _ptr(a), a.size))
+
+    def get_param(self, name: str, numel: int) -> np.ndarray:
+        a = np.zeros(numel, np.float32)
+        check(self.L.fq_model_get_param(self.h, name.encode(), _ptr(a), a.size))
+        return a
 
     def init_random(self, seed: int, std: float = 0.02, kl_bins: int = 0):
         """Device-side random init; with kl_bins > 0 also returns the weight-histogram KL of the
@@ -482,6 +543,20 @@ class Model:
         check(self.L.fq_model_calibrate_logit_kl(self.h, _ptr(t), n_seqs, length, base_rung, flip_rung, _ptr(kl),
                                                  _ptr(ent)))
         return kl, ent
+
+    # ---------------------------------------------------------------- tensor-parallel rank
+    def tp_shard(self) -> TpShard:
+        sh = TpShard()
+        check(self.L.fq_model_tp_shard(self.h, C.byref(sh)))
+        return sh
+
+    def tp_begin(self, slots, tokens) -> None:
+        self._tp_s = np.ascontiguousarray(slots, np.int32)
+        t = np.ascontiguousarray(tokens, np.int32)
+        check(self.L.fq_model_tp_begin(self.h, self._tp_s.size, _ptr(self._tp_s), _ptr(t)))
+
+    def tp_segment(self, seg: int, reduced_dev, out_dev) -> None:
+        check(self.L.fq_model_tp_segment(self.h, seg, _ptr(reduced_dev), _ptr(out_dev)))
 
     def close(self) -> None:
         if self.h:

@@ -142,6 +142,8 @@ struct ProgramRun {
   const int32_t* pos = nullptr;   // decode step: per-row positions / cache slots, copied into shared
   const int32_t* slots = nullptr; // memory at kernel start (the attention phases read them there)
   int nrows = 0;
+  const void* tp_in = nullptr;    // tensor-parallel segment: the exchange buffers baked in
+  const void* tp_out = nullptr;
   float* fix = nullptr;           // owned stream-K scratch (device programs)
   unsigned int* flags = nullptr;
 };

@@ -340,6 +340,15 @@ struct fq_model {
     int32_t* tok = nullptr;
   } pw;
   int rows = 1;  // activation rows: max(max_batch, prefill chunk) (llama); max_batch (reference)
+  // tensor-parallel rank (fq_model_create_tp): this model holds heads [sh.head0, +heads), ffn
+  // columns [sh.ffn0, +ffn) and vocab rows [sh.vocab0, +vocab) of the full config `cfg`; without
+  // TP the shard is the whole model.  q_dim = local attention width (heads * head_dim).
+  fq_tp_shard sh{};
+  int64_t q_dim = 0;
+  int tp_batch = 0;     // rows of the step begun by fq_model_tp_begin (0: none)
+  int tp_next_seg = 0;  // next segment the step expects
+  std::vector<int32_t> tp_slots_step = std::vector<int32_t>(256);
+  bool tp() const { return sh.size > 1; }
 
   int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
   int head_index() const { return static_cast<int>(cfg.n_layers) * (llama ? 7 : 6); }
@@ -927,6 +936,7 @@ void batched_step(fq_model* M, int B) {
 void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens, float* logits_dev,
                 fq_row_stats* stats_host) {
   require(B >= 1 && B <= M->cfg.max_batch, FQ_E_INPUT, "decode: batch out of range");
+  require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: decode through fq_model_tp_begin / fq_model_tp_segment");
   if (M->llama) {
     for (int i = 0; i < M->n_lin; ++i) {
       require(gemv_fast_supported(M->lin[i], FQ_RUNG_INT8) || !M->lin[i]->has(FQ_RUNG_INT8), FQ_E_STATE,
@@ -1121,6 +1131,175 @@ void prefill_gemm(fq_model* M, int slot, const int32_t* tokens, int64_t T, float
   M->slot_len[slot] = T;
 }
 
+// ---------------------------------------------------------------- tensor-parallel step (variant)
+// A TP rank's decode step is 2L + 1 segments, each one step-program launch; between segments the
+// caller sums the ranks' fp32 partials (NCCL all-reduce over NVLink) and hands the sum to the next
+// segment, which adds it to the replicated residual:
+//   segment 2l     : [embed | resid += sum] -> RMSNorm + q/k/v of the rank's heads -> RoPE +
+//                    KV append + attention of those heads -> O projection (its input columns) ->
+//                    fp32 partial [B, d]
+//   segment 2l + 1 : resid += sum -> RMSNorm + gate/up of the rank's ffn columns -> SwiGLU -> down
+//                    projection (its input columns) -> fp32 partial [B, d]
+//   segment 2L     : resid += sum -> final RMSNorm + head rows of the rank's vocab slice -> fused
+//                    softmax partials merged over the grid -> fq_stat_part [B] (the host merges the
+//                    ranks' partials: fq_tp_merge_stats)
+// The unsplit block is src/model.cpp:201-233; the statistics src/scheduler.cpp:13-49.
+void add_resid_phase(ProgramBuilder& pb, fq_model* M, int B, const float* reduced, const StepMeta& meta) {
+  Phase e{};
+  e.type = PH_EMBED;
+  e.barrier_after = 1;
+  e.B = B;
+  e.tok_emb = reduced ? nullptr : M->tok_emb;
+  e.x = reduced;
+  e.tokens = meta.tokens;
+  e.d = M->cfg.d_model;
+  e.resid = M->resid;
+  e.resid_stride = M->cfg.d_model;
+  e.out_partials = M->partials[0];
+  e.out_partials_stride = kPartStride;
+  pb.add(e);
+}
+
+ProgramRun& tp_program(fq_model* M, int B, int seg, const float* reduced, void* out) {
+  // programs bake the exchange buffers in: cached per (batch, segment, buffers)
+  const int key_mode = 1000 + seg;
+  auto key = std::make_pair(B, key_mode);
+  auto it = M->programs.find(key);
+  if (it != M->programs.end() && it->second.tp_in == reduced && it->second.tp_out == out) return it->second;
+  if (it != M->programs.end()) {
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    dfree(it->second.dev_phases);
+    M->programs.erase(it);
+  }
+  fq_ctx* ctx = M->ctx;
+  const fq_model_config& c = M->cfg;
+  const int64_t d = c.d_model, L = c.n_layers;
+  const StepMeta meta = M->meta(B);
+  const uint8_t* table = M->table_dev();
+  ProgramBuilder pb;
+  pb.grid = ctx->num_sms;
+  const int G = pb.grid;
+  add_resid_phase(pb, M, B, seg == 0 ? nullptr : reduced, meta);
+  const int frag_nkb_q = static_cast<int>((M->q_dim + kBlockK - 1) / kBlockK);
+  auto norm_in = [&](GemvLaunch& g, const float* gain) {
+    g.x = M->resid;
+    g.x_dtype = FQ_DT_F32;
+    g.x_stride = d;
+    g.norm_gain = gain;
+    g.norm_partials = M->partials[0];
+    g.n_partials = G;
+    g.partials_stride = kPartStride;
+    g.norm_eps = c.norm_eps;
+    g.act_dtype = c.act_dtype;
+  };
+  auto lin = [&](GemvLaunch& g, int m, int index) {
+    g.mat[m].layer = M->lin[index];
+    g.mat[m].rung_table = table + index;
+    g.mat[m].rung_stride = M->n_lin;
+  };
+  if (seg < 2 * L && seg % 2 == 0) {
+    const int l = seg / 2;
+    GemvLaunch g;
+    g.nmat = 3;
+    for (int j = 0; j < 3; ++j) lin(g, j, M->lin_index(l, j));
+    g.mat[0].y = M->q;
+    g.mat[1].y = M->k;
+    g.mat[2].y = M->v;
+    norm_in(g, M->n1g[l]);
+    g.epi = EPI_SPLIT3;
+    g.y_dtype = c.act_dtype;
+    g.y_stride = M->q_dim;
+    add_chunked(pb, g, B);
+    Phase a{};
+    a.type = PH_ATTN;
+    a.barrier_after = 1;
+    a.B = B;
+    a.q = M->q;
+    a.k = M->k;
+    a.v = M->v;
+    a.act_dtype = c.act_dtype;
+    a.pos = meta.pos;
+    a.slots = meta.slots;
+    a.kv = static_cast<__half*>(M->kv);
+    a.slot_stride = M->slot_stride;
+    a.layer_off = l * M->layer_stride;
+    a.max_seq = c.max_seq_len;
+    a.n_heads = static_cast<int>(M->sh.heads);
+    a.head_dim = static_cast<int>(c.head_dim);
+    a.rope_cs = M->rope_cs;
+    a.attn_ws = M->attn_ws;
+    a.attn_out = M->attn;
+    a.attn_splits = 1;
+    if (B <= kMaxB) {
+      a.yfrag = static_cast<__half*>(M->attn_frag);
+      a.yfrag_nkb = frag_nkb_q;
+    }
+    pb.add(a);
+    GemvLaunch o;
+    o.nmat = 1;
+    lin(o, 0, M->lin_index(l, 3));
+    o.x = M->attn;
+    if (B <= kMaxB) o.xfrag = M->attn_frag;
+    o.x_dtype = c.act_dtype;
+    o.x_stride = M->q_dim;
+    o.epi = EPI_STORE;
+    o.y = out;
+    o.y_dtype = FQ_DT_F32;
+    o.y_stride = d;
+    add_chunked(pb, o, B);
+  } else if (seg < 2 * L) {
+    const int l = seg / 2;
+    GemvLaunch gu;
+    gu.nmat = 2;
+    for (int j = 0; j < 2; ++j) lin(gu, j, M->lin_index(l, 4 + j));
+    norm_in(gu, M->n2g[l]);
+    gu.epi = EPI_SWIGLU;
+    gu.y = M->mid;
+    if (B <= kMaxB) gu.yfrag = M->mid_frag;
+    gu.y_dtype = c.act_dtype;
+    gu.y_stride = M->sh.ffn;
+    add_chunked(pb, gu, B);
+    GemvLaunch dn;
+    dn.nmat = 1;
+    lin(dn, 0, M->lin_index(l, 6));
+    dn.x = M->mid;
+    if (B <= kMaxB) dn.xfrag = M->mid_frag;
+    dn.x_dtype = c.act_dtype;
+    dn.x_stride = M->sh.ffn;
+    dn.epi = EPI_STORE;
+    dn.y = out;
+    dn.y_dtype = FQ_DT_F32;
+    dn.y_stride = d;
+    add_chunked(pb, dn, B);
+  } else {
+    GemvLaunch hd;
+    hd.nmat = 1;
+    lin(hd, 0, M->head_index());
+    norm_in(hd, M->fng);
+    hd.epi = EPI_STORE;
+    hd.y = M->logits;
+    hd.y_dtype = FQ_DT_F32;
+    hd.y_stride = M->sh.vocab;
+    hd.stat_part = M->stat_part;
+    add_chunked(pb, hd, B);
+    Phase sp{};
+    sp.type = PH_STATS;
+    sp.B = B;
+    sp.stats = M->stats_dev;
+    sp.stat_part = M->stat_part;
+    sp.y = out;  // merged partial per row (fq_stat_part), not the final statistics
+    pb.add(sp);
+  }
+  pb.phases.back().barrier_after = 0;
+  ProgramRun run = upload_program(ctx, pb, false);
+  run.pos = meta.pos;
+  run.slots = meta.slots;
+  run.nrows = B;
+  run.tp_in = reduced;
+  run.tp_out = out;
+  return M->programs.emplace(key, run).first->second;
+}
+
 float* param_slot(fq_model* M, const std::string& name, int64_t& expect) {
   const fq_model_config& c = M->cfg;
   const int64_t d = c.d_model;
@@ -1162,6 +1341,10 @@ using namespace fqc::mdl;
 extern "C" {
 
 fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** out) {
+  return fq_model_create_tp(ctx, cfg, 0, 1, out);
+}
+
+fq_status fq_model_create_tp(fq_ctx* ctx, const fq_model_config* cfg, int32_t tp_rank, int32_t tp_size, fq_model** out) {
   return guarded([&] {
     require(ctx && cfg && out, FQ_E_INPUT, "null argument");
     const fq_model_config& c = *cfg;
@@ -1169,6 +1352,9 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
         c.max_seq_len < 1)
       fail(FQ_E_CONFIG, "model config: all dimensions must be >= 1");
     if (c.d_model != c.n_heads * c.head_dim) fail(FQ_E_CONFIG, "model config: d_model must equal n_heads * head_dim");
+    fq_tp_shard sh{};
+    if (fq_tp_shard_spec(cfg, tp_rank, tp_size, &sh) != FQ_OK) fail(FQ_E_CONFIG, fq_last_error());
+    require(tp_size == 1 || c.arch == FQ_ARCH_LLAMA, FQ_E_CONFIG, "tensor parallel: llama arch only");
     require(c.arch == FQ_ARCH_LLAMA || c.arch == FQ_ARCH_REFERENCE, FQ_E_CONFIG, "model config: unknown arch");
     require(c.max_batch >= 1 && c.max_batch <= 256, FQ_E_CONFIG, "model config: max_batch must be in [1, 256]");
     if (c.arch == FQ_ARCH_LLAMA) {
@@ -1182,19 +1368,24 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->ctx = ctx;
     M->cfg = c;
     M->llama = c.arch == FQ_ARCH_LLAMA;
+    M->sh = sh;
+    M->q_dim = sh.heads * c.head_dim;
     const int64_t d = c.d_model, ffn = c.ffn_dim, V = c.vocab_size, L = c.n_layers;
+    const int64_t qd = M->q_dim, fl = sh.ffn, vl = sh.vocab;  // this rank's shard (== full without TP)
     const int per = M->llama ? 7 : 6;
     for (int64_t i = 0; i < L; ++i) {
       const std::string p = "blocks." + std::to_string(i) + ".";
       std::vector<std::pair<std::string, std::pair<int64_t, int64_t>>> specs;
-      specs.push_back({p + "attn.wq", {d, d}});
-      specs.push_back({p + "attn.wk", {d, d}});
-      specs.push_back({p + "attn.wv", {d, d}});
-      specs.push_back({p + "attn.wo", {d, d}});
+      // column split: q/k/v/gate/up keep their rows of the rank's heads / ffn columns; row split:
+      // o/down keep the matching input columns (model.cpp:201-233 is the unsplit block)
+      specs.push_back({p + "attn.wq", {qd, d}});
+      specs.push_back({p + "attn.wk", {qd, d}});
+      specs.push_back({p + "attn.wv", {qd, d}});
+      specs.push_back({p + "attn.wo", {d, qd}});
       if (M->llama) {
-        specs.push_back({p + "ffn.w_gate", {ffn, d}});
-        specs.push_back({p + "ffn.w_up", {ffn, d}});
-        specs.push_back({p + "ffn.w_down", {d, ffn}});
+        specs.push_back({p + "ffn.w_gate", {fl, d}});
+        specs.push_back({p + "ffn.w_up", {fl, d}});
+        specs.push_back({p + "ffn.w_down", {d, fl}});
       } else {
         specs.push_back({p + "ffn.w1", {ffn, d}});
         specs.push_back({p + "ffn.w2", {d, ffn}});
@@ -1212,7 +1403,7 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     (void)per;
     if (!(c.arch == FQ_ARCH_REFERENCE && c.tie_embeddings)) {
       fq_layer* lay = nullptr;
-      if (fq_layer_create(ctx, V, d, c.group_size, &lay) != FQ_OK) fail(FQ_E_CONFIG, fq_last_error());
+      if (fq_layer_create(ctx, vl, d, c.group_size, &lay) != FQ_OK) fail(FQ_E_CONFIG, fq_last_error());
       lay->borrowed = true;
       M->ids.push_back("head");
       M->lin.push_back(lay);
@@ -1255,7 +1446,7 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     M->rungs.assign(static_cast<size_t>(B) * M->n_lin, static_cast<uint8_t>(M->llama ? FQ_RUNG_INT8 : FQ_RUNG_FP));
     // KV cache
     const size_t kv_elem = M->llama ? 2 : 4;
-    M->layer_stride = 2 * c.max_seq_len * d;
+    M->layer_stride = 2 * c.max_seq_len * qd;
     M->slot_stride = L * M->layer_stride;
     M->kv = dmalloc(kv_elem * M->slot_stride * B);
     FQ_CUDA(cudaMemsetAsync(M->kv, 0, kv_elem * M->slot_stride * B, st));
@@ -1318,6 +1509,52 @@ fq_status fq_model_create(fq_ctx* ctx, const fq_model_config* cfg, fq_model** ou
     }
     FQ_CUDA(cudaStreamSynchronize(st));
     *out = M;
+  });
+}
+
+fq_status fq_model_tp_shard(const fq_model* M, fq_tp_shard* out) {
+  return guarded([&] {
+    require(M && out, FQ_E_INPUT, "null argument");
+    *out = M->sh;
+  });
+}
+
+fq_status fq_model_tp_begin(fq_model* M, int32_t batch, const int32_t* slots, const int32_t* tokens) {
+  return guarded([&] {
+    require(M && slots && tokens, FQ_E_INPUT, "null argument");
+    require(M->llama, FQ_E_CONFIG, "tensor parallel: llama arch only");
+    require(batch >= 1 && batch <= M->cfg.max_batch, FQ_E_INPUT, "tp step: batch out of range");
+    require(M->tp_batch == 0, FQ_E_STATE, "tp step: previous step not finished (segments pending)");
+    sync_weight_epoch(M);
+    for (int i = 0; i < M->n_lin; ++i)
+      for (int r : {FQ_RUNG_INT8, FQ_RUNG_INT4})
+        require(gemv_fast_supported(M->lin[i], r) || !M->lin[i]->has(r), FQ_E_STATE,
+                "layer " + M->ids[i] + ": copy not usable by the fast kernel");
+    // the pinned staging buffer may still feed the previous step's copy
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    stage_rows(M, batch, slots, tokens);
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, M->ctx->stream));
+    M->tp_batch = batch;
+    M->tp_next_seg = 0;
+    for (int b = 0; b < batch; ++b) M->tp_slots_step[b] = slots[b];
+  });
+}
+
+fq_status fq_model_tp_segment(fq_model* M, int32_t seg, const float* reduced_dev, void* out_dev) {
+  return guarded([&] {
+    require(M && out_dev, FQ_E_INPUT, "null argument");
+    require(M->tp_batch > 0, FQ_E_STATE, "tp step: fq_model_tp_begin first");
+    require(seg == M->tp_next_seg, FQ_E_STATE, "tp step: segments must run in order");
+    require(seg == 0 || reduced_dev, FQ_E_INPUT, "tp step: segment > 0 needs the reduced partial");
+    const int B = M->tp_batch;
+    ProgramRun& run = tp_program(M, B, seg, seg == 0 ? nullptr : reduced_dev, out_dev);
+    FQ_CUDA(cudaMemsetAsync(M->grid_barrier, 0, sizeof(unsigned int), M->ctx->stream));
+    launch_program(M->ctx, run, M->grid_barrier, false);
+    M->tp_next_seg = seg + 1;
+    if (seg == 2 * M->cfg.n_layers) {
+      for (int b = 0; b < B; ++b) M->slot_len[M->tp_slots_step[b]] += 1;
+      M->tp_batch = 0;
+    }
   });
 }
 
@@ -1536,6 +1773,7 @@ fq_status fq_model_prefill(fq_model* M, int32_t slot, const int32_t* tokens, int
                            fq_row_stats* stats_host) {
   return guarded([&] {
     require(M && tokens, FQ_E_INPUT, "null argument");
+    require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     if (n < 1) fail(FQ_E_INPUT, "prefill: empty prompt");
     require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
     if (M->slot_len[slot] != 0) fail(FQ_E_STATE, "prefill: cache already populated");
@@ -1624,6 +1862,7 @@ fq_status fq_model_profile_step(fq_model* M, int32_t slot, int32_t token, uint64
                                 int32_t* nphases_out, int32_t* grid_out, int32_t* phase_types_host) {
   return guarded([&] {
     require(M && ticks_host && nphases_out && grid_out, FQ_E_INPUT, "null argument");
+    require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(M->llama, FQ_E_CONFIG, "profile_step: llama arch only");
     fq_ctx* ctx = M->ctx;
     cudaStream_t st = ctx->stream;
@@ -1684,6 +1923,7 @@ fq_status fq_model_decode_timed(fq_model* M, int32_t slot, int32_t token, float*
                                 uint64_t* ns_by_rung, uint64_t* ns_step) {
   return guarded([&] {
     require(M && stats_host && ns_by_rung && ns_step, FQ_E_INPUT, "null argument");
+    require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(M->llama, FQ_E_CONFIG, "decode_timed: llama arch only");
     fq_ctx* ctx = M->ctx;
     cudaStream_t st = ctx->stream;
@@ -1767,6 +2007,7 @@ fq_status fq_model_profile_gemvs(fq_model* M, int32_t slot, int32_t reps, double
                                  int64_t* launches_per_pass, int64_t* bytes_per_pass) {
   return guarded([&] {
     require(M && ms_per_launch, FQ_E_INPUT, "null argument");
+    require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(M->llama, FQ_E_CONFIG, "profile_gemvs: llama arch only");
     require(reps >= 1, FQ_E_INPUT, "profile_gemvs: reps must be >= 1");
     const int32_t tok = 0;
@@ -1820,6 +2061,7 @@ fq_status fq_model_calibrate_logit_kl(fq_model* M, const int32_t* tokens, int64_
                                       int32_t base_rung, int32_t flip_rung, double* kl_host, double* entropy_host) {
   return guarded([&] {
     require(M && tokens && kl_host, FQ_E_INPUT, "null argument");
+    require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(n_seqs >= 1 && len >= 1, FQ_E_INPUT, "calibrate: empty token set");
     require(len <= M->cfg.max_seq_len, FQ_E_CAPACITY, "calibrate: sequence longer than max_seq_len");
     const fq_model_config& c = M->cfg;

@@ -1445,12 +1445,15 @@ FQ_ONCE void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
   int64_t c0;
   int cnt;
   cta_rows(P.d, c0, cnt);
+  // tok_emb null: residual add of an exchanged partial (tensor-parallel step, resid += x[b])
+  const bool add = P.tok_emb == nullptr;
   for (int b = 0; b < P.B; ++b) {
-    const float* e = P.tok_emb + static_cast<int64_t>(P.tokens[b]) * P.d;
+    const float* e = add ? static_cast<const float*>(P.x) + b * P.d : P.tok_emb + static_cast<int64_t>(P.tokens[b]) * P.d;
     float sq = 0.f;
     for (int i = threadIdx.x; i < cnt; i += kNCW * 32) {
-      const float v = e[c0 + i];
-      P.resid[b * P.resid_stride + c0 + i] = v;
+      float* rp = P.resid + b * P.resid_stride + c0 + i;
+      const float v = add ? *rp + e[c0 + i] : e[c0 + i];
+      *rp = v;
       sq += v * v;
     }
 #pragma unroll
@@ -1794,7 +1797,11 @@ FQ_ONCE void run_stats(const Phase& P) {
       const StatPart o2 = stat_shfl(a, o);
       a = (lane & o) ? stat_merge(o2, a) : stat_merge(a, o2);
     }
-    if (lane == 0) {
+    if (lane == 0 && P.y) {
+      // tensor-parallel head (vocab slice): the mergeable partial itself, merged across ranks
+      // by the host (fq_tp_merge_stats)
+      static_cast<StatPart*>(P.y)[b] = a;
+    } else if (lane == 0) {
       fq_row_stats r;
       const double H = log(a.S) - a.T / a.S;
       r.entropy = H;
