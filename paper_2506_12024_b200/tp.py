@@ -134,8 +134,12 @@ class TpDecoder:
         # and writes its new partial in its last, so the in-place all-reduce needs no second buffer
         self.part = [torch.zeros(max_batch, cfg.d_model, dtype=torch.float32, device=dev) for _ in self.models]
         self.stat = [torch.zeros(max_batch * 32, dtype=torch.uint8, device=dev) for _ in self.models]
-        for m in self.models:
-            m.ctx.set_stream(torch.cuda.current_stream())
+        # the exchange (torch / NCCL) is ordered on the engine's own stream; the local ranks share
+        # one context (one stream)
+        handles = {m.ctx.stream_handle() for m in self.models}
+        if len(handles) != 1:
+            raise capi.ConfigError("tp decode: the local rank models must share one context")
+        self.stream = torch.cuda.ExternalStream(handles.pop())
         self.max_batch = max_batch
 
     def begin(self, slots, tokens) -> None:
@@ -160,24 +164,24 @@ class TpDecoder:
         if B > self.max_batch:
             raise capi.InputError("tp decode: batch larger than the exchange buffers")
         self.begin(slots, tokens)
-        self.segments()
-        return self.finish(B)
+        with self.torch.cuda.stream(self.stream):
+            self.segments()
+            return self.finish(B)
 
     def logits(self, B: int) -> np.ndarray:
         """Full-vocabulary logits [B, V] of the last step, gathered from the local ranks (LocalExchange)."""
-        torch = self.torch
-        torch.cuda.current_stream().synchronize()
+        self.stream.synchronize()
         cols = [_device_view(m.logits_ptr(), B * v).view(B, v).cpu().numpy() for m, v in zip(self.models, self.vocab)]
         return np.concatenate(cols, axis=1)
 
 
 def _device_view(ptr: int, n: int):
-    """A torch float32 tensor over n floats of foreign device memory (read-only use)."""
+    """A torch float32 tensor over n floats of foreign device memory (the caller only reads it)."""
     import torch
 
     class _Holder:
         def __init__(self, p, n):
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (p, True), "version": 2,
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (p, False), "version": 2,
                                              "strides": None}
 
     return torch.as_tensor(_Holder(ptr, n), device="cuda")

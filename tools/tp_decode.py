@@ -87,7 +87,7 @@ def main():
     tok = int(toks[0])
     for i in range(a.prompt):  # the prompt through the same segments
         dec.step([0], [int(toks[i])])
-    st = torch.cuda.current_stream()
+    st = dec.stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if not a.local:
         dist.barrier()
