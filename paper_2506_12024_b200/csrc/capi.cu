@@ -95,6 +95,8 @@ fq_status fq_ctx_destroy(fq_ctx* ctx) {
     dfree(ctx->gemv_flags);
     dfree(ctx->launch_ctr);
     dfree(ctx->gemm_ws);
+    dfree(ctx->direct_ws);
+    dfree(ctx->direct_cnt);
     for (void* r : ctx->retired) dfree(r);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -317,19 +319,27 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t batch, c
       launch_gemv_exact(ctx, L, rung, batch, x_dev, x_dtype, y_dev, y_dtype);
       return;
     }
-    GemvLaunch g;
-    g.mat[0].layer = L;
-    g.mat[0].rung = rung;
-    g.nmat = 1;
-    g.batch = batch;
-    g.x = x_dev;
-    g.x_dtype = x_dtype;
-    g.x_stride = L->K;
-    g.epi = EPI_STORE;
-    g.y = y_dev;
-    g.y_dtype = y_dtype;
-    g.y_stride = L->N;
-    launch_gemv_fast(ctx, g);
+    // kernel choice by shape (measured, profiles/r03_gemv_sweep_c2.jsonl): the direct kernel
+    // (gemv_direct.cu) starts streaming at once and keeps every batch row of a > 8-row batch in
+    // one pass; the step-program form (a one-phase persistent program) sustains more bandwidth
+    // on long layers (N >= 16384, the 32000-row head) at up to 8 rows
+    if (L->N >= 16384 && batch <= 8) {
+      GemvLaunch g;
+      g.mat[0].layer = L;
+      g.mat[0].rung = rung;
+      g.nmat = 1;
+      g.batch = batch;
+      g.x = x_dev;
+      g.x_dtype = x_dtype;
+      g.x_stride = L->K;
+      g.epi = EPI_STORE;
+      g.y = y_dev;
+      g.y_dtype = y_dtype;
+      g.y_stride = L->N;
+      launch_gemv_fast(ctx, g);
+      return;
+    }
+    launch_gemv_direct(ctx, L, rung, batch, x_dev, x_dtype, y_dev, y_dtype);
   });
 }
 

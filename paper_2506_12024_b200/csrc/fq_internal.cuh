@@ -58,6 +58,10 @@ struct fq_ctx {
   unsigned int* gemv_flags = nullptr;
   unsigned int* launch_ctr = nullptr;  // [epoch, done] of the program kernels on this context
   float* gemm_ws = nullptr;  // split-K partial sums of the tensor-core GEMM (grown on demand)
+  float* direct_ws = nullptr;     // split-K partials of the stand-alone GEMV (gemv_direct.cu)
+  size_t direct_ws_bytes = 0;
+  unsigned* direct_cnt = nullptr; // its per-tile arrival counters (self-resetting)
+  size_t direct_cnt_n = 0;
   size_t gemm_ws_bytes = 0;
   std::vector<void*> retired;  // outgrown workspaces captured graphs may still point at (freed at destroy)
   // bumped whenever a layer's resident copies change (upload, device quantization): models
@@ -175,6 +179,9 @@ int gemv_fast_grid(const fq_ctx* ctx, int64_t N);
 // Returns the grid size used (the residual epilogue writes one sum-of-squares partial per CTA;
 // out_n_partials must be >= #SM x 4).
 int launch_gemv_fast(fq_ctx* ctx, const GemvLaunch& g);
+// Stand-alone dequant-GEMV of one linear at one precision (fq_gemv FAST; gemv_direct.cu).
+void launch_gemv_direct(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x, int x_dtype, void* y,
+                        int y_dtype);
 double time_gemv_chain(fq_ctx* ctx, const GemvLaunch* gs, int n, int reps);
 void launch_gemv_exact(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch, const void* x,
                        int x_dtype, void* y, int y_dtype);

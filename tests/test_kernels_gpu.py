@@ -63,6 +63,41 @@ def test_gemv_fast_vs_oracle(ctx, N, K, bits, B):
     assert np.all(np.abs(y - yref)[big] <= 1e-2 * np.abs(yref)[big])
 
 
+@pytest.mark.parametrize("N,K", [(200, 1376), (4096, 4096)])
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("B", [9, 24, 32, 40])
+def test_gemv_fast_wide_batches_and_repeatability(ctx, N, K, bits, B):
+    """Stand-alone GEMV (gemv_direct.cu) with 2 / 4 MMA column groups and a > 32-row batch split
+    into launches; split-K partials summed in slice order by the tile's last task: two calls are
+    bit-identical."""
+    w = _w(N, K, N * 7 + K + B)
+    L, ref = _layer(ctx, w, 128, (bits,))
+    x = np.random.default_rng(K + 3 * B).standard_normal((B, K)).astype(np.float32)
+    rung = capi.RUNG_INT8 if bits == 8 else capi.RUNG_INT4
+    y, x16 = _gemv(ctx, L, rung, x, capi.DT_F16)
+    y2, _ = _gemv(ctx, L, rung, x, capi.DT_F16)
+    assert np.array_equal(y, y2)
+    p, s, z = ref[bits]
+    yref = np.zeros((B, N), np.float32)
+    oracle.lib().fqo_quant_linear(np.ascontiguousarray(x16), B, p, N, K, 128, bits, 0, s.ravel(), z.ravel(), None, yref)
+    assert _rel(y, yref) < 1e-4, _rel(y, yref)
+
+
+@pytest.mark.parametrize("y_dtype", [capi.DT_BF16, capi.DT_F16])
+def test_gemv_fast_half_outputs(ctx, y_dtype):
+    N, K, B = 4096, 4096, 4
+    w = _w(N, K, 77)
+    L, ref = _layer(ctx, w, 128, (8,))
+    x = torch.from_numpy(np.random.default_rng(5).standard_normal((B, K)).astype(np.float32)).to("cuda").half()
+    tdt = torch.bfloat16 if y_dtype == capi.DT_BF16 else torch.float16
+    y = torch.empty((B, N), dtype=tdt, device="cuda")
+    yf = torch.empty((B, N), dtype=torch.float32, device="cuda")
+    ctx.gemv(L, capi.RUNG_INT8, B, x, capi.DT_F16, y, y_dtype, capi.NUMERICS_FAST)
+    ctx.gemv(L, capi.RUNG_INT8, B, x, capi.DT_F16, yf, capi.DT_F32, capi.NUMERICS_FAST)
+    ctx.synchronize()
+    assert torch.equal(y, yf.to(tdt))  # the same fp32 sums, rounded once at the store
+
+
 _C2_CACHE = {}
 
 
