@@ -35,6 +35,8 @@ ABI_FUNCTIONS = [
     "fq_model_init_random_kl", "fq_model_profile_gemvs", "fq_model_profile_step", "fq_gemm",
     "fq_model_step_kernel_time", "fq_gemv_chain_time", "fq_tiled_activation_bytes", "fq_tile_activations",
     "fq_gemm_tiled", "fq_model_decode_timed", "fq_layer_download_fp", "fq_layer_download_bias", "fq_model_get_param", "fq_model_param_size",
+    "fq_tp_shard_spec", "fq_shard_quantized", "fq_tp_merge_stats", "fq_model_create_tp", "fq_model_tp_shard",
+    "fq_model_tp_begin", "fq_model_tp_segment",
 ]
 
 
