@@ -3,6 +3,7 @@
 #include <vector>
 #include "fq_internal.cuh"
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -323,7 +324,8 @@ fq_status fq_gemv(fq_ctx* ctx, const fq_layer* L, int32_t rung, int64_t batch, c
     // (gemv_direct.cu) starts streaming at once and keeps every batch row of a > 8-row batch in
     // one pass; the step-program form (a one-phase persistent program) sustains more bandwidth
     // on long layers (N >= 16384, the 32000-row head) at up to 8 rows
-    if (L->N >= 16384 && batch <= 8) {
+    static const bool all_direct = std::getenv("FQ_GEMV_DIRECT_ALL") != nullptr;  // A/B measurement
+    if (L->N >= 16384 && batch <= 8 && !all_direct) {
       GemvLaunch g;
       g.mat[0].layer = L;
       g.mat[0].rung = rung;

@@ -125,7 +125,7 @@ __device__ __forceinline__ bool issue(Stream& st, const DirectArgs& a, int k0, i
 // 1024 for the W8 byte-permute operands, 64 for the W4 nibble operands).
 template <int W, int NG, int U>
 __device__ __forceinline__ void compute_batch(const uint8_t* stage, int kb, int nk, const uint4* __restrict__ xs,
-                                              const float4* __restrict__ dx, int kb_per, int zp_base, int lane,
+                                              const float4* __restrict__ dx, int rs, int bmax, int zp_base, int lane,
                                               float (&y)[NG][4]);
 
 // NB blocks of a staged batch, interleaved block by block at every k-step so the NB accumulator
@@ -134,8 +134,8 @@ __device__ __forceinline__ void compute_batch(const uint8_t* stage, int kb, int 
 // byte-permute operands, 64 for the W4 nibble operands).
 template <int W, int NG, int NB>
 __device__ __forceinline__ void compute_blocks(const uint8_t* stage, int kl0, const uint4* __restrict__ xs,
-                                               const float4* __restrict__ dx, int kb_per, int zp_base, int lane,
-                                               float (&y)[NG][4]) {
+                                               const float4* __restrict__ dx, int rs, int bmax, int zp_base,
+                                               int lane, float (&y)[NG][4]) {
   constexpr int BR = 8 * NG;
   constexpr int BB = W == 0 ? kBlockBytes8 : kBlockBytes4;
   constexpr int CB = W == 0 ? 2048 : 1024;
@@ -159,7 +159,7 @@ __device__ __forceinline__ void compute_blocks(const uint8_t* stage, int kl0, co
         const uint32_t a6 = prmt(q.w, 0x64646464u, 0x4140u), a7 = prmt(q.w, 0x64646464u, 0x4342u);
 #pragma unroll
         for (int cg = 0; cg < NG; ++cg) {
-          const uint4 xv = xs[((cg * 8 + g) * kb_per + kl0 + n) * 16 + p * 4 + tig];
+          const uint4 xv = xs[min(cg * 8 + g, bmax) * rs + (kl0 + n) * 16 + p * 4 + tig];
           mma16816(c[n][cg], a0, a1, a2, a3, xv.x, xv.y);
           mma16816(c[n][cg], a4, a5, a6, a7, xv.z, xv.w);
         }
@@ -178,7 +178,7 @@ __device__ __forceinline__ void compute_blocks(const uint8_t* stage, int kl0, co
           const uint32_t a0 = nib_f16(q << 4), a1 = nib_f16(q >> 4), a2 = nib_f16(q), a3 = nib_f16(q >> 8);
 #pragma unroll
           for (int cg = 0; cg < NG; ++cg) {
-            const uint4 xv = xs[((cg * 8 + g) * kb_per + kl0 + n) * 16 + (2 * i + (uu >> 1)) * 4 + tig];
+            const uint4 xv = xs[min(cg * 8 + g, bmax) * rs + (kl0 + n) * 16 + (2 * i + (uu >> 1)) * 4 + tig];
             mma16816(c[n][cg], a0, a1, a2, a3, (uu & 1) ? xv.z : xv.x, (uu & 1) ? xv.w : xv.y);
           }
         }
@@ -208,13 +208,13 @@ __device__ __forceinline__ void compute_blocks(const uint8_t* stage, int kl0, co
 // tail batch goes block by block.
 template <int W, int NG, int U>
 __device__ __forceinline__ void compute_batch(const uint8_t* stage, int kb, int nk, const uint4* __restrict__ xs,
-                                              const float4* __restrict__ dx, int kb_per, int zp_base, int lane,
+                                              const float4* __restrict__ dx, int rs, int bmax, int zp_base, int lane,
                                               float (&y)[NG][4]) {
   constexpr int BB = W == 0 ? kBlockBytes8 : kBlockBytes4;
   if (kb + U <= nk) {
-    compute_blocks<W, NG, U>(stage, kb, xs, dx, kb_per, zp_base, lane, y);
+    compute_blocks<W, NG, U>(stage, kb, xs, dx, rs, bmax, zp_base, lane, y);
   } else {
-    for (int u = 0; kb + u < nk; ++u) compute_blocks<W, NG, 1>(stage + u * BB, kb + u, xs, dx, kb_per, zp_base, lane, y);
+    for (int u = 0; kb + u < nk; ++u) compute_blocks<W, NG, 1>(stage + u * BB, kb + u, xs, dx, rs, bmax, zp_base, lane, y);
   }
 }
 
@@ -282,7 +282,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gemv_direct_kernel(const Direc
   const int nk = k1 - k0;
   uint8_t* ring = smem + static_cast<size_t>(warp) * kRing * kStage;
   uint4* xs = reinterpret_cast<uint4*>(smem + static_cast<size_t>(kWarps) * kRing * kStage);
-  float4* dx = reinterpret_cast<float4*>(xs + static_cast<size_t>(BR) * a.kb_per * 16);
+  // activation rows padded by 16 bytes: the 8 rows x 4 lanes of a fragment load hit 8 distinct
+  // bank quads (4 wavefronts for 32 lanes); columns past the batch read the last row (broadcast)
+  const int rs = a.kb_per * 16 + 1;
+  float4* dx = reinterpret_cast<float4*>(xs + static_cast<size_t>(BR) * rs);
 
   // the weight stream depends on nothing: start it before staging the activations
   Stream st{static_cast<int>(blockIdx.y) * kWarps + warp, 0, static_cast<int>(gridDim.y) * kWarps};
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gemv_direct_kernel(const Direc
     for (int e = 0; e < 4; ++e) {
       const int r = 4 * lane + e, j16 = r >> 4, r16 = r & 15;
       const int p = j16 >> 1, hh = j16 & 1, tig = (r16 & 7) >> 1, comp = 2 * hh + (r16 >> 3);
-      xh[((static_cast<size_t>(b) * a.kb_per + kl) * 16 + p * 4 + tig) * 8 + comp * 2 + (r16 & 1)] = __float2half_rn(v[e]);
+      xh[(static_cast<size_t>(b) * rs + kl * 16 + p * 4 + tig) * 8 + comp * 2 + (r16 & 1)] = __float2half_rn(v[e]);
     }
   }
   __syncthreads();
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gemv_direct_kernel(const Direc
   uint32_t parity = 0;
   while (tile < a.n_tiles) {
     mbar_wait(&bars[warp][s], parity);
-    compute_batch<W, NG, U>(ring + s * kStage, kb, nk, xs, dx, a.kb_per, a.zp_base, lane, y);
+    compute_batch<W, NG, U>(ring + s * kStage, kb, nk, xs, dx, rs, a.B - 1, a.zp_base, lane, y);
     __syncwarp();  // every lane is done with the stage: refill it
     if (lane == 0) issue<W, U>(st, a, k0, nk, ring + s * kStage, &bars[warp][s]);
     if (++s == kRing) {
@@ -353,7 +356,7 @@ template <int W, int NG, int U>
 void launch_t(fq_ctx* ctx, const DirectArgs& a, int Y) {
   constexpr int BB = W == 0 ? kBlockBytes8 : kBlockBytes4;
   const size_t smem = static_cast<size_t>(kWarps) * kRing * U * BB +
-                      static_cast<size_t>(8 * NG) * a.kb_per * (16 * 16 + 16);
+                      static_cast<size_t>(8 * NG) * (a.kb_per * (16 * 16 + 16) + 16);
   static bool attr = false;
   if (!attr) {
     FQ_CUDA(cudaFuncSetAttribute(gemv_direct_kernel<W, NG, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -383,7 +386,7 @@ void launch_gemv_direct(fq_ctx* ctx, const fq_layer* L, int rung, int64_t batch,
     const int U = w == 0 ? (ng == 4 ? 1 : 2) : (ng == 4 ? 2 : 4);
     const int64_t ring = static_cast<int64_t>(kWarps) * kRing * U * (w == 0 ? kBlockBytes8 : kBlockBytes4);
     const int64_t per_kb = static_cast<int64_t>(8 * ng) * (16 * 16 + 16);  // fragments + dx per k-block
-    const int64_t budget = 220 * 1024 - ring;
+    const int64_t budget = 220 * 1024 - ring - 16 * 8 * ng;
     const int s_min = std::max<int>(1, static_cast<int>((nkb * per_kb + budget - 1) / budget));
     const int sms = ctx->num_sms;
     int S = s_min, Y = 1;
