@@ -325,8 +325,12 @@ fq_status fq_model_tp_begin(fq_model* model, int32_t batch, const int32_t* slots
  * sum over ranks of the previous segment's partials (fp32 [batch, d_model]; NULL for seg 0).
  * out_dev: seg < n_segments-1 -> this rank's fp32 [batch, d_model] partial of the O / down
  * projection; the last segment -> fq_stat_part [batch] of the rank's vocab slice (its logits
- * stay in fq_model_logits, [batch, shard.vocab]).  The last segment completes the step. */
+ * stay in fq_model_logits, [batch, shard.vocab]).  Segments only enqueue work, so the sequence
+ * (with the caller's collectives) can be captured into a CUDA graph and replayed. */
 fq_status fq_model_tp_segment(fq_model* model, int32_t seg, const float* reduced_dev, void* out_dev);
+/* Completes the step begun by fq_model_tp_begin after its segments were enqueued (or a captured
+ * sequence of them replayed): every slot of the step advances by one position. */
+fq_status fq_model_tp_end(fq_model* model);
 
 #ifdef __cplusplus
 }

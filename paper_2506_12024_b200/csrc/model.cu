@@ -1524,7 +1524,8 @@ fq_status fq_model_tp_begin(fq_model* M, int32_t batch, const int32_t* slots, co
     require(M && slots && tokens, FQ_E_INPUT, "null argument");
     require(M->llama, FQ_E_CONFIG, "tensor parallel: llama arch only");
     require(batch >= 1 && batch <= M->cfg.max_batch, FQ_E_INPUT, "tp step: batch out of range");
-    require(M->tp_batch == 0, FQ_E_STATE, "tp step: previous step not finished (segments pending)");
+    // a step abandoned mid-way (a failed segment) is dropped: its slots' lengths did not advance,
+    // so the next step rewrites the same cache positions
     sync_weight_epoch(M);
     for (int i = 0; i < M->n_lin; ++i)
       for (int r : {FQ_RUNG_INT8, FQ_RUNG_INT4})
@@ -1551,10 +1552,15 @@ fq_status fq_model_tp_segment(fq_model* M, int32_t seg, const float* reduced_dev
     FQ_CUDA(cudaMemsetAsync(M->grid_barrier, 0, sizeof(unsigned int), M->ctx->stream));
     launch_program(M->ctx, run, M->grid_barrier, false);
     M->tp_next_seg = seg + 1;
-    if (seg == 2 * M->cfg.n_layers) {
-      for (int b = 0; b < B; ++b) M->slot_len[M->tp_slots_step[b]] += 1;
-      M->tp_batch = 0;
-    }
+  });
+}
+
+fq_status fq_model_tp_end(fq_model* M) {
+  return guarded([&] {
+    require(M != nullptr, FQ_E_INPUT, "null model");
+    require(M->tp_batch > 0, FQ_E_STATE, "tp step: no step begun");
+    for (int b = 0; b < M->tp_batch; ++b) M->slot_len[M->tp_slots_step[b]] += 1;
+    M->tp_batch = 0;
   });
 }
 

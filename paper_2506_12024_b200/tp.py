@@ -118,7 +118,7 @@ class TpDecoder:
     """Decode steps of the local TP rank models (all ranks with LocalExchange, one with
     DistExchange).  step() returns the merged row statistics of the full vocabulary."""
 
-    def __init__(self, models: Sequence[capi.Model], exchange, max_batch: int = 1):
+    def __init__(self, models: Sequence[capi.Model], exchange, max_batch: int = 1, graphs: bool = True):
         import torch
         self.torch = torch
         self.models = list(models)
@@ -141,6 +141,12 @@ class TpDecoder:
             raise capi.ConfigError("tp decode: the local rank models must share one context")
         self.stream = torch.cuda.ExternalStream(handles.pop())
         self.max_batch = max_batch
+        # the 2L+1 segments and the exchanges between them, captured per batch size after one
+        # eager step (which builds the segment programs) and replayed: no host round trip per
+        # segment.  Rebuild the decoder after re-uploading weights (the programs bake pointers in).
+        self.use_graphs = graphs
+        self.graphs = {}
+        self.eager_steps = {}
 
     def begin(self, slots, tokens) -> None:
         for m in self.models:
@@ -160,12 +166,25 @@ class TpDecoder:
         return capi.tp_merge_stats(parts, self.vocab0)
 
     def step(self, slots, tokens) -> np.ndarray:
+        torch = self.torch
         B = len(slots)
         if B > self.max_batch:
             raise capi.InputError("tp decode: batch larger than the exchange buffers")
         self.begin(slots, tokens)
-        with self.torch.cuda.stream(self.stream):
-            self.segments()
+        with torch.cuda.stream(self.stream):
+            g = self.graphs.get(B)
+            if g is None and self.use_graphs and self.eager_steps.get(B, 0) >= 1:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self.segments()
+                self.graphs[B] = g
+            if g is not None:
+                g.replay()
+            else:
+                self.segments()
+                self.eager_steps[B] = self.eager_steps.get(B, 0) + 1
+            for m in self.models:
+                m.tp_end()
             return self.finish(B)
 
     def logits(self, B: int) -> np.ndarray:

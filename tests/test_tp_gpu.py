@@ -175,3 +175,25 @@ def test_tp_matches_single_gpu_engine(ctx, size):
         worst_h = max(worst_h, abs(st["entropy"][0] - ref_st["entropy"][0]))
     print(f"tp{size} vs single engine: worst rel {worst:.2e} entropy {worst_h:.2e}")
     assert worst <= 5e-3 and worst_h <= 1e-4
+
+
+def test_tp_graph_replay_matches_eager(ctx):
+    """The captured segment sequence (steps 3+) computes exactly what the host-enqueued one does."""
+    cfg = LLAMA_HD128
+    orc = oracle.llama.LlamaOracle(dict(cfg, group_size=128), seed=0)
+    toks = oracle.random_tokens(10, cfg["vocab_size"], 21)
+    outs = []
+    for graphs in (False, True):
+        models = _ranks(ctx, orc, cfg, 2)
+        dec = tp.TpDecoder(models, tp.LocalExchange(2), graphs=graphs)
+        rows = []
+        for t in toks:
+            st = dec.step([0], [int(t)])
+            rows.append((dec.logits(1)[0].copy(), float(st["entropy"][0]), int(st["argmax"][0])))
+        assert (len(dec.graphs) == 1) == graphs
+        assert all(m.slot_length(0) == len(toks) for m in models)
+        outs.append(rows)
+        while _OPEN:
+            _OPEN.pop().close()
+    for (la, ha, aa), (lb, hb, ab) in zip(*outs):
+        assert np.array_equal(la, lb) and ha == hb and aa == ab

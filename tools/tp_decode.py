@@ -56,6 +56,7 @@ def main():
     ap.add_argument("--steps", type=int, default=32)
     ap.add_argument("--local", type=int, default=0, help="run this many ranks in one process (functional)")
     ap.add_argument("--w4-frac", type=float, default=0.5)
+    ap.add_argument("--no-graphs", action="store_true", help="enqueue the segments from the host every step")
     a = ap.parse_args()
     cfg = dict(SHAPES[a.shape], max_seq_len=a.prompt + a.steps + 8)
     if a.layers:
@@ -82,7 +83,7 @@ def main():
     for m in models:
         for i, r in enumerate(table):
             m.set_rung(0, i, r)
-    dec = tp.TpDecoder(models, ex)
+    dec = tp.TpDecoder(models, ex, graphs=not a.no_graphs)
     toks = np.random.default_rng(7).integers(0, cfg["vocab_size"], a.prompt + a.steps)
     tok = int(toks[0])
     for i in range(a.prompt):  # the prompt through the same segments
@@ -113,7 +114,7 @@ def main():
             "ms_per_token": ms / a.steps, "tokens_per_s": 1000.0 * a.steps / ms,
             "segments_per_token": sh.n_segments, "allreduces_per_token": sh.n_segments - 1,
             "exchange": "local (one process, sum on device)" if a.local else f"nccl x{world}",
-            "w4_frac": a.w4_frac, "build_s": build_s, "argmax_tail": argmaxes[-4:],
+            "w4_frac": a.w4_frac, "graphs": not a.no_graphs, "build_s": build_s, "argmax_tail": argmaxes[-4:],
             "note": "timing includes the host-side segment loop and the host merge of the head statistics",
         }))
     for m in models:
