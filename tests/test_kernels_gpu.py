@@ -83,6 +83,30 @@ def test_gemv_fast_wide_batches_and_repeatability(ctx, N, K, bits, B):
     assert _rel(y, yref) < 1e-4, _rel(y, yref)
 
 
+@pytest.mark.parametrize("N,K", [(5, 256), (17, 130), (33, 1376)])
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("B", [1, 3, 17])
+@pytest.mark.parametrize("x_dtype", [capi.DT_F32, capi.DT_BF16])
+def test_gemv_fast_tiny_and_ragged(ctx, N, K, bits, B, x_dtype):
+    """Layers smaller than one 16-row tile, a 2-code ragged last group, fp32 / bf16 inputs (the
+    direct kernel rounds them to the fp16 MMA operand; the oracle sees the same fp16 values)."""
+    w = _w(N, K, 900 + N + K)
+    L, ref = _layer(ctx, w, 128, (bits,))
+    x = np.random.default_rng(N + K + B).standard_normal((B, K)).astype(np.float32)
+    rung = capi.RUNG_INT8 if bits == 8 else capi.RUNG_INT4
+    y, xin = _gemv(ctx, L, rung, x, x_dtype)
+    p, s, z = ref[bits]
+    rels = []
+    # the fast kernels take fp16 operands; a layer whose zero points span more than a byte (the
+    # 2-code group of K = 130 quantizes to an extreme z) has no tiled copy and runs the exact
+    # fp32 path on the unrounded input -- each matches the oracle on its own operands
+    for xo in (xin.astype(np.float16).astype(np.float32), xin):
+        yref = np.zeros((B, N), np.float32)
+        oracle.lib().fqo_quant_linear(np.ascontiguousarray(xo), B, p, N, K, 128, bits, 0, s.ravel(), z.ravel(), None, yref)
+        rels.append(_rel(y, yref))
+    assert min(rels) < 1e-4, rels
+
+
 @pytest.mark.parametrize("y_dtype", [capi.DT_BF16, capi.DT_F16])
 def test_gemv_fast_half_outputs(ctx, y_dtype):
     N, K, B = 4096, 4096, 4
