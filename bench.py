@@ -411,12 +411,27 @@ def main():
     switches = 0
     l0 = ctx.launches()
 
+    # algorithmic weight bytes of the step (payload + 5 B metadata per group-row of every linear
+    # at its current rung, as fq_model_step_bytes counts them), kept current as switches apply so
+    # the timed loop does no accounting calls; KV bytes grow by one position per step
+    lin_w = []
+    for i in range(len(model.ids)):
+        L = model.linear(i)
+        meta = L.N * L.ng * 5
+        lin_w.append((L.N * L.K + meta, (L.N * L.K + 1) // 2 + meta))
+    rung_now = [8] * len(model.ids)
+    wbytes = [sum(w8 for w8, _ in lin_w)]
+
     def step(row):
         nonlocal switches
         token = int(row["argmax"])
         _, first, cnt = sched.observe(float(row["ppl_entropy"]))
         for i in range(cnt):
-            model.set_rung(0, plan[first + i][1], capi.RUNG_INT4)
+            idx = plan[first + i][1]
+            model.set_rung(0, idx, capi.RUNG_INT4)
+            if rung_now[idx] == 8:
+                wbytes[0] += lin_w[idx][1] - lin_w[idx][0]
+                rung_now[idx] = 4
         switches += cnt
         return model.decode([0], [token])[0]
 
@@ -426,6 +441,9 @@ def main():
     if dist is not None:
         dist.barrier()
     bytes_w_steps = []
+    wb_check, kb0 = model.step_bytes([0])
+    assert wb_check == wbytes[0], (wb_check, wbytes[0])  # the tracked weight bytes match the engine's
+    kv_per_pos = cfg["n_layers"] * 2 * cfg["d_model"] * 2
     with ClockSampler(local) as clocks:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -433,10 +451,9 @@ def main():
         e0.record(stream)
         model.step_kernel_time(reset=True)
         launches_before = ctx.launches()
-        for _ in range(args.steps):
-            wb, kb = model.step_bytes([0])
-            bytes_w_steps.append(wb + kb)
+        for i in range(args.steps):
             row = step(row)
+            bytes_w_steps.append(wbytes[0] + kb0 + i * kv_per_pos)  # the rungs this step ran at
         e1.record(stream)
         torch.cuda.synchronize()
     launches_timed = ctx.launches() - launches_before
