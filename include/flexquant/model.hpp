@@ -184,6 +184,7 @@ class Model {
   friend class MultiPrecisionLayer;
   friend class KvCache;
   void account_step(uint64_t ns, int slot) const;
+  std::vector<int32_t> precision_row(int slot) const;  // every linear's rung, one C-ABI call
   ModelConfig cfg_;
   fq_model* model_ = nullptr;
   std::vector<std::string> ids_;

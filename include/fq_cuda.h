@@ -223,6 +223,9 @@ fq_status fq_model_init_random_kl(fq_model* model, uint64_t seed, float std, int
 fq_status fq_model_set_rung(fq_model* model, int32_t slot, int32_t linear_index, int32_t rung);
 fq_status fq_model_get_rung(const fq_model* model, int32_t slot, int32_t linear_index, int32_t* out);
 fq_status fq_model_set_all_rungs(fq_model* model, int32_t slot, int32_t rung);
+/* The whole precision row of a slot (n = number of linears) in one call (host bookkeeping:
+ * effective bits, bytes per pass, latency buckets per token). */
+fq_status fq_model_get_rungs(const fq_model* model, int32_t slot, int32_t* out, int32_t n);
 /* KV cache of a slot (KvCache, src/model.cpp:142-171). */
 fq_status fq_model_reset_slot(fq_model* model, int32_t slot);
 fq_status fq_model_slot_length(const fq_model* model, int32_t slot, int64_t* out);

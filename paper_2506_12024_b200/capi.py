@@ -36,7 +36,7 @@ ABI_FUNCTIONS = [
     "fq_model_step_kernel_time", "fq_gemv_chain_time", "fq_tiled_activation_bytes", "fq_tile_activations",
     "fq_gemm_tiled", "fq_model_decode_timed", "fq_layer_download_fp", "fq_layer_download_bias", "fq_model_get_param", "fq_model_param_size",
     "fq_tp_shard_spec", "fq_shard_quantized", "fq_tp_merge_stats", "fq_model_create_tp", "fq_model_tp_shard",
-    "fq_model_tp_begin", "fq_model_tp_segment", "fq_model_tp_end",
+    "fq_model_tp_begin", "fq_model_tp_segment", "fq_model_tp_end", "fq_model_get_rungs",
 ]
 
 
@@ -177,6 +177,7 @@ def load(path: str = LIB_PATH):
         "fq_model_tp_begin": [v, i32, v, v],
         "fq_model_tp_segment": [v, i32, v, v],
         "fq_model_tp_end": [v],
+        "fq_model_get_rungs": [v, i32, v, i32],
         "fq_tile_activations": [v, v, i32, i64, i64, i64, i32, v],
         "fq_gemm_tiled": [v, v, i32, i64, v, i32, v, i64, i32],
     }

@@ -1751,6 +1751,16 @@ fq_status fq_model_get_rung(const fq_model* M, int32_t slot, int32_t li, int32_t
   });
 }
 
+fq_status fq_model_get_rungs(const fq_model* M, int32_t slot, int32_t* out, int32_t n) {
+  return guarded([&] {
+    require(M != nullptr && out != nullptr, FQ_E_INPUT, "null argument");
+    require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
+    require(n == M->n_lin, FQ_E_DIMENSION, "get_rungs: n must equal the number of linears");
+    const uint8_t* row = &M->rungs[static_cast<size_t>(slot) * M->n_lin];
+    for (int i = 0; i < n; ++i) out[i] = row[i];
+  });
+}
+
 fq_status fq_model_set_all_rungs(fq_model* M, int32_t slot, int32_t rung) {
   return guarded([&] {
     require(M != nullptr, FQ_E_INPUT, "null model");

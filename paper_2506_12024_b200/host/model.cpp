@@ -287,11 +287,18 @@ KvCache Model::attach_cache(int slot) const {
   return c;
 }
 
+std::vector<int32_t> Model::precision_row(int slot) const {
+  std::vector<int32_t> r(layers_.size());
+  detail::check(fq_model_get_rungs(model_, slot, r.data(), static_cast<int32_t>(r.size())));
+  return r;
+}
+
 void Model::account_step(uint64_t ns, int slot) const {
   // per-rung buckets: the step's time split by each rung's share of the weight bytes
   double b[3] = {0, 0, 0};
+  const std::vector<int32_t> row = precision_row(slot);
   for (size_t i = 0; i < layers_.size(); ++i) {
-    const Rung r = precision(static_cast<int>(i), slot);
+    const Rung r = static_cast<Rung>(row[i]);
     b[static_cast<int>(r)] += static_cast<double>(layers_[i].param_count()) * accounting_bits(r) / 8.0;
   }
   const double tot = b[0] + b[1] + b[2];
@@ -400,8 +407,9 @@ void Model::set_all_precision(Rung bits, int slot) {
 
 double Model::effective_bits(int slot) const {
   double num = 0.0, den = 0.0;
+  const std::vector<int32_t> row = precision_row(slot);
   for (size_t i = 0; i < layers_.size(); ++i) {
-    num += static_cast<double>(layers_[i].param_count()) * accounting_bits(precision(static_cast<int>(i), slot));
+    num += static_cast<double>(layers_[i].param_count()) * accounting_bits(static_cast<Rung>(row[i]));
     den += static_cast<double>(layers_[i].param_count());
   }
   return den > 0.0 ? num / den : 0.0;
@@ -409,8 +417,9 @@ double Model::effective_bits(int slot) const {
 
 double Model::weight_bytes_per_pass(int slot) const {
   double b = 0.0;
+  const std::vector<int32_t> row = precision_row(slot);
   for (size_t i = 0; i < layers_.size(); ++i)
-    b += static_cast<double>(layers_[i].param_count()) * accounting_bits(precision(static_cast<int>(i), slot)) / 8.0;
+    b += static_cast<double>(layers_[i].param_count()) * accounting_bits(static_cast<Rung>(row[i])) / 8.0;
   return b;
 }
 
