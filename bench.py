@@ -514,7 +514,16 @@ def main():
     gcfg.scheduler.layers_per_switch = args.layers_per_switch
     fstream = torch.cuda.ExternalStream(fq.runtime_stream())
     prompt_host = prompt.copy()  # host buffer: copied to the device by the engine each call
-    fq.generate(prompt_host[:32], fmodel, fplan, gcfg)  # warm-up (program build, graph capture)
+    # warm-up at the timed run's sizes (full prompt: the prefill workspace, step programs and
+    # graphs are built here, not inside the timed region)
+    wcfg = fq.GenerationConfig()
+    wcfg.max_new_tokens = 16
+    wcfg.start_rung = fq.Rung.Int8
+    wcfg.scheduler.threshold_mode = fq.ThresholdMode.Prefill
+    wcfg.scheduler.theta = args.theta
+    wcfg.scheduler.window_len = W
+    wcfg.scheduler.layers_per_switch = args.layers_per_switch
+    fq.generate(prompt_host.copy(), fmodel, fplan, wcfg)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -527,6 +536,12 @@ def main():
     e2e_ms = parallel.max_over_ranks(f0.elapsed_time(f1), device="cuda")
     e2e_value = parallel.aggregate_throughput(len(res.sequence), world, e2e_ms / 1000.0)
     e2e_switches = sum(len(r.switch_events) for r in res.trace.records)
+    # the trace's own per-token wall times (TraceRecord::elapsed_ns; token 1 covers the prefill)
+    tok_ns = sorted(int(r.elapsed_ns) for r in res.trace.records[1:])
+    e2e_detail = {"prefill_ms": round(int(res.trace.records[0].elapsed_ns) / 1e6, 3),
+                  "decode_ms_median": round(tok_ns[len(tok_ns) // 2] / 1e6, 4) if tok_ns else None,
+                  "decode_ms_max": round(tok_ns[-1] / 1e6, 3) if tok_ns else None,
+                  "decode_ms_sum": round(sum(tok_ns) / 1e6, 2)}
     row_bytes = capi.ROW_STATS_DTYPE.itemsize
     h2d = (cfg["prompt"] * 4 + (e2e_tokens - 1) * 4) / e2e_tokens
     d2h = (cfg["prompt"] + e2e_tokens - 1) * row_bytes / e2e_tokens
@@ -581,6 +596,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "trace": e2e_detail,
                     "note": f"flexquant::generate (C++ API, libflexquant_b200.so) of the full config with host "
                             f"buffers: {cfg['prompt']}-token prefill on the tcgen05 path + {e2e_tokens} decode tokens "
                             f"with the C++ SchedulerState, {e2e_switches} switch events"},
