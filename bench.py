@@ -433,7 +433,7 @@ def main():
                 wbytes[0] += lin_w[idx][1] - lin_w[idx][0]
                 rung_now[idx] = 4
         switches += cnt
-        return model.decode([0], [token])[0]
+        return model.decode_one(0, token)
 
     for _ in range(args.warmup):
         row = step(row)

@@ -499,6 +499,18 @@ class Model:
         check(self.L.fq_model_decode(self.h, s.size, _ptr(s), _ptr(t), _ptr(logits_dev), _ptr(st)))
         return st
 
+    def decode_one(self, slot: int, token: int):
+        """decode() for one slot with preallocated argument / result buffers (the per-token call
+        of a decode loop); returns the row's stats record (valid until the next call)."""
+        if not hasattr(self, "_d1"):
+            self._d1 = (np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1, ROW_STATS_DTYPE))
+            self._d1p = tuple(a.ctypes.data for a in self._d1)
+        s, t, st = self._d1
+        s[0] = slot
+        t[0] = token
+        check(self.L.fq_model_decode(self.h, 1, self._d1p[0], self._d1p[1], None, self._d1p[2]))
+        return st[0]
+
     def step_kernel_time(self, reset: bool = True) -> tuple:
         """(total ms, steps) of the decode-step program kernels since the last reset (device events)."""
         ms, n = C.c_double(), C.c_int64()
