@@ -17,6 +17,8 @@
 // Numerics are those of the step program's GEMV (fp16 activations, exact products, fp32
 // accumulation per 128-code group, fp32 group scale): src/quantizer.cpp:205-219 dequantize +
 // src/tensor.cpp:83-101 linear within the FAST tolerance.
+#include <atomic>
+
 #include "fq_internal.cuh"
 
 namespace fqc {
@@ -357,10 +359,12 @@ void launch_t(fq_ctx* ctx, const DirectArgs& a, int Y) {
   constexpr int BB = W == 0 ? kBlockBytes8 : kBlockBytes4;
   const size_t smem = static_cast<size_t>(kWarps) * kRing * U * BB +
                       static_cast<size_t>(8 * NG) * (a.kb_per * (16 * 16 + 16) + 16);
-  static bool attr = false;
-  if (!attr) {
+  // the shared-memory opt-in is a per-device attribute: set once per device this process uses
+  static std::atomic<uint64_t> set_on{0};
+  const uint64_t bit = 1ull << (ctx->device & 63);
+  if (!(set_on.load() & bit)) {
     FQ_CUDA(cudaFuncSetAttribute(gemv_direct_kernel<W, NG, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
+    set_on.fetch_or(bit);
   }
   if (smem > 220 * 1024) fail(FQ_E_CONFIG, "gemv: activation slice does not fit shared memory");
   gemv_direct_kernel<W, NG, U><<<dim3(a.S, Y), kWarps * 32, smem, ctx->stream>>>(a);
