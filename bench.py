@@ -168,6 +168,14 @@ class Scheduler:
         self.cool = self.W
         return avg, first, cnt
 
+    def safe_observes(self):
+        """How many of the next observe() calls cannot fire whatever the values: observe j (from
+        1) can fire only once the window is full (len + j >= W) and the cooldown has run out
+        (cool - j <= 0), or never once the plan is exhausted."""
+        if self.cursor >= self.plan_len:
+            return 1 << 30
+        return max(self.W - len(self.win), self.cool, 1) - 1
+
 
 def cpu_decode_sample(cfg, blocks: int = 1, steps: int = 2):
     """The reference's decode on ONE host core (oracle/_ref, built from its sources): a
@@ -327,6 +335,8 @@ def main():
     ap.add_argument("--window", type=int, default=20)
     ap.add_argument("--layers-per-switch", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="every token through the host loop (no device-chained blocks while the scheduler cannot switch)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -441,6 +451,7 @@ def main():
     if dist is not None:
         dist.barrier()
     bytes_w_steps = []
+    chained = 0
     wb_check, kb0 = model.step_bytes([0])
     assert wb_check == wbytes[0], (wb_check, wbytes[0])  # the tracked weight bytes match the engine's
     kv_per_pos = cfg["n_layers"] * 2 * cfg["d_model"] * 2
@@ -451,9 +462,25 @@ def main():
         e0.record(stream)
         model.step_kernel_time(reset=True)
         launches_before = ctx.launches()
-        for i in range(args.steps):
-            row = step(row)
-            bytes_w_steps.append(wbytes[0] + kb0 + i * kv_per_pos)  # the rungs this step ran at
+        i = 0
+        while i < args.steps:
+            # tokens whose scheduler decision cannot switch anything run as one device-chained
+            # block (fq_model_decode_chain: the token fed back from the previous argmax on the
+            # device, no host round trip); the observes are replayed afterwards and must not fire
+            n = min(sched.safe_observes(), args.steps - i, 64) if not args.no_chain else 0
+            if n >= 1:
+                rows = model.decode_chain(0, n)
+                for r in [row] + [rows[k] for k in range(n - 1)]:
+                    _, _, cnt = sched.observe(float(r["ppl_entropy"]))
+                    assert cnt == 0, "chained step switched"
+                row = rows[n - 1]
+                chained += n
+            else:
+                row = step(row)
+                n = 1
+            for k in range(n):
+                bytes_w_steps.append(wbytes[0] + kb0 + (i + k) * kv_per_pos)  # the rungs each step ran at
+            i += n
         e1.record(stream)
         torch.cuda.synchronize()
     launches_timed = ctx.launches() - launches_before
@@ -576,7 +603,8 @@ def main():
                 "model": cfg["name"], "global_batch": world, "seq_len": cfg["prompt"] + args.warmup + args.steps,
                 "parallelism": f"dp{world}", "group_size": 128, "kv_cache": "fp16",
                 "scheduler": {"mode": "prefill", "theta": args.theta, "threshold": thre, "window": W,
-                              "layers_per_switch": args.layers_per_switch, "switches_applied": switches},
+                              "layers_per_switch": args.layers_per_switch, "switches_applied": switches,
+                              "device_chained_steps": chained},
                 "l2": "no flush needed: >6.5 GB of weights streamed per step (126 MB L2)",
                 "weights_init_s": round(t_init, 2),
             },

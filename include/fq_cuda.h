@@ -238,6 +238,13 @@ fq_status fq_model_prefill(fq_model* model, int32_t slot, const int32_t* tokens_
  * replayed from a captured CUDA graph. logits_dev optional [batch, V] copy-out. */
 fq_status fq_model_decode(fq_model* model, int32_t batch, const int32_t* slots_host,
                           const int32_t* tokens_host, float* logits_dev, fq_row_stats* stats_host);
+/* n (<= 64) further decode steps of `slot`, each fed on the device with the previous step's
+ * argmax (argmax_token, src/engine.cpp:144-155) and run at the slot's current precision row, with
+ * no host round trip between them; stats_host receives the n rows.  For a decode loop whose
+ * scheduler provably cannot switch during those tokens (SchedulerState::observe, src/scheduler.cpp:
+ * 85-104: window still filling or cooldown running); the slot's previous operation must be a
+ * single-row fq_model_decode (or chain) step. */
+fq_status fq_model_decode_chain(fq_model* model, int32_t slot, int32_t n, fq_row_stats* stats_host);
 /* fq_model_decode for one slot with the device phase clock on: also returns the step's device
  * time split by precision (ns_by_rung[FQ_RUNG_*]: each GEMV phase's time shared among its
  * linears by bytes) and the whole step (*ns_step); the remainder is embedding, attention over the

@@ -36,7 +36,7 @@ ABI_FUNCTIONS = [
     "fq_model_step_kernel_time", "fq_gemv_chain_time", "fq_tiled_activation_bytes", "fq_tile_activations",
     "fq_gemm_tiled", "fq_model_decode_timed", "fq_layer_download_fp", "fq_layer_download_bias", "fq_model_get_param", "fq_model_param_size",
     "fq_tp_shard_spec", "fq_shard_quantized", "fq_tp_merge_stats", "fq_model_create_tp", "fq_model_tp_shard",
-    "fq_model_tp_begin", "fq_model_tp_segment", "fq_model_tp_end", "fq_model_get_rungs",
+    "fq_model_tp_begin", "fq_model_tp_segment", "fq_model_tp_end", "fq_model_get_rungs", "fq_model_decode_chain",
 ]
 
 
@@ -178,6 +178,7 @@ def load(path: str = LIB_PATH):
         "fq_model_tp_segment": [v, i32, v, v],
         "fq_model_tp_end": [v],
         "fq_model_get_rungs": [v, i32, v, i32],
+        "fq_model_decode_chain": [v, i32, i32, v],
         "fq_tile_activations": [v, v, i32, i64, i64, i64, i32, v],
         "fq_gemm_tiled": [v, v, i32, i64, v, i32, v, i64, i32],
     }
@@ -510,6 +511,12 @@ class Model:
         t[0] = token
         check(self.L.fq_model_decode(self.h, 1, self._d1p[0], self._d1p[1], None, self._d1p[2]))
         return st[0]
+
+    def decode_chain(self, slot: int, n: int) -> np.ndarray:
+        """n device-chained decode steps of `slot` (token = the previous step's argmax)."""
+        st = np.zeros(n, ROW_STATS_DTYPE)
+        check(self.L.fq_model_decode_chain(self.h, slot, n, _ptr(st)))
+        return st
 
     def step_kernel_time(self, reset: bool = True) -> tuple:
         """(total ms, steps) of the decode-step program kernels since the last reset (device events)."""

@@ -98,6 +98,8 @@ struct alignas(16) Phase {
     int appended;         // ATTN: the rows' keys / values are already in the cache (prefill)
     int xfrag_tagged;     // GEMV: xfrag holds (half2, tag) 8-byte words written by the previous
                           // phase (no grid barrier before this phase: staging polls the tags)
+    int token_stride;     // EMBED: row b's token is tokens[b * token_stride] (0 = 1); a chained
+                          // decode step points tokens at the previous step's fq_row_stats argmax
   };
   int attn_splits;        // ATTN: CTAs per (row, head), each over a contiguous chunk range; > 1:
                           // unnormalised partials (O[hd], m, l) in attn_ws, merged by the next

@@ -29,6 +29,7 @@ namespace fqc {
 namespace {
 
 constexpr int kPartStride = 1024;
+constexpr int kMaxChain = 64;  // decode steps per fq_model_decode_chain call
 constexpr int kPrefillRows = 8;  // prompt positions per prefill step (llama): the GEMV's MMA n
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -349,6 +350,11 @@ struct fq_model {
   int tp_next_seg = 0;  // next segment the step expects
   std::vector<int32_t> tp_slots_step = std::vector<int32_t>(256);
   bool tp() const { return sh.size > 1; }
+  // chained decode (fq_model_decode_chain): the slot whose single-row decode step ran last (its
+  // argmax is stats_dev[0]), -1 when another step / prefill ran since; pinned stats ring, events
+  int chain_slot = -1;
+  fq_row_stats* chain_ring = nullptr;
+  std::vector<cudaEvent_t> chain_ev;
 
   int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
   int head_index() const { return static_cast<int>(cfg.n_layers) * (llama ? 7 : 6); }
@@ -391,7 +397,9 @@ bool capturing(cudaStream_t st) {
 
 // Enqueues one decode step for B rows (metadata already staged in meta_dev).  gemv_only keeps
 // just the GEMV launches (kernel-level profiling; activations are whatever the buffers hold).
-enum StepMode : int { STEP_DECODE = 0, STEP_GEMV_ONLY = 1, STEP_PREFILL = 2 };
+// STEP_CHAIN: a decode step whose token is the previous step's argmax, read on the device
+// (fq_model_decode_chain)
+enum StepMode : int { STEP_DECODE = 0, STEP_GEMV_ONLY = 1, STEP_PREFILL = 2, STEP_CHAIN = 3 };
 
 // Prefill steps (STEP_PREFILL) take B consecutive positions of one sequence as their rows: an
 // append phase writes every row's RoPE'd key / value to the cache before the attention phase, so
@@ -444,6 +452,10 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         e.B = B;
         e.tok_emb = M->tok_emb;
         e.tokens = meta.tokens;
+        if (mode == STEP_CHAIN) {
+          e.tokens = &M->stats_dev[0].argmax;
+          e.token_stride = static_cast<int>(sizeof(fq_row_stats) / sizeof(int32_t));
+        }
         e.d = d;
         e.resid = M->resid;
         e.resid_stride = d;
@@ -946,9 +958,11 @@ void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens,
     }
   }
   stage_rows(M, B, slots, tokens);
+  M->chain_slot = -1;
   if (batched_gemm_usable(M, B)) batched_step(M, B);
   else run_step(M, B);
   for (int b = 0; b < B; ++b) M->slot_len[slots[b]] += 1;
+  if (B == 1 && M->llama) M->chain_slot = slots[0];
   if (stats_host) std::memcpy(stats_host, M->stats_host, sizeof(fq_row_stats) * B);
   if (logits_dev)
     FQ_CUDA(cudaMemcpyAsync(logits_dev, M->logits, sizeof(float) * B * M->cfg.vocab_size, cudaMemcpyDeviceToDevice,
@@ -959,6 +973,7 @@ void model_step(fq_model* M, int B, const int32_t* slots, const int32_t* tokens,
 // program (append phase, then causal attention over the cache).
 void prefill_step(fq_model* M, int slot, const int32_t* tokens, int R, float* logits_dev, fq_row_stats* stats_host) {
   const fq_model_config& c = M->cfg;
+  M->chain_slot = -1;
   int32_t* tok = reinterpret_cast<int32_t*>(M->meta_host);
   int32_t* pos = tok + M->rows;
   int32_t* sl = pos + M->rows;
@@ -1300,6 +1315,8 @@ ProgramRun& tp_program(fq_model* M, int B, int seg, const float* reduced, void* 
   return M->programs.emplace(key, run).first->second;
 }
 
+__global__ void advance_pos_kernel(int32_t* pos) { pos[0] += 1; }
+
 float* param_slot(fq_model* M, const std::string& name, int64_t& expect) {
   const fq_model_config& c = M->cfg;
   const int64_t d = c.d_model;
@@ -1512,6 +1529,58 @@ fq_status fq_model_create_tp(fq_ctx* ctx, const fq_model_config* cfg, int32_t tp
   });
 }
 
+fq_status fq_model_decode_chain(fq_model* M, int32_t slot, int32_t n, fq_row_stats* stats_host) {
+  return guarded([&] {
+    require(M && stats_host, FQ_E_INPUT, "null argument");
+    require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
+    require(M->llama, FQ_E_CONFIG, "decode chain: llama arch only");
+    require(n >= 1 && n <= kMaxChain, FQ_E_INPUT, "decode chain: 1..64 steps");
+    require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
+    require(M->chain_slot == slot, FQ_E_STATE,
+            "decode chain: the slot's previous operation must be a single-row decode step (its argmax feeds the chain)");
+    if (M->slot_len[slot] + n > M->cfg.max_seq_len) fail(FQ_E_CAPACITY, "decode: cache is full");
+    fq_ctx* ctx = M->ctx;
+    cudaStream_t st = ctx->stream;
+    sync_weight_epoch(M);
+    if (M->chain_ring == nullptr) {
+      FQ_CUDA(cudaMallocHost(&M->chain_ring, sizeof(fq_row_stats) * kMaxChain));
+      M->chain_ev.resize(2 * kMaxChain);
+      for (auto& e : M->chain_ev) FQ_CUDA(cudaEventCreate(&e));
+    }
+    // the step's rows: this slot at its next position with its current precision row; the token
+    // slot of the staging is unused (the embedding reads the previous step's argmax on the device)
+    const int32_t tok0 = M->stats_host[0].argmax;
+    stage_rows(M, 1, &slot, &tok0);
+    FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    int32_t* pos_dev = reinterpret_cast<int32_t*>(M->meta_dev) + M->rows;
+    for (int i = 0; i < n; ++i) {
+      if (i > 0) {
+        advance_pos_kernel<<<1, 1, 0, st>>>(pos_dev);
+        launch_dev(M);
+      }
+      FQ_CUDA(cudaEventRecord(M->chain_ev[2 * i], st));
+      enqueue_step(M, 1, STEP_CHAIN);
+      FQ_CUDA(cudaEventRecord(M->chain_ev[2 * i + 1], st));
+      launch_dev(M);
+      FQ_CUDA(cudaMemcpyAsync(M->chain_ring + i, M->stats_dev, sizeof(fq_row_stats), cudaMemcpyDeviceToHost, st));
+    }
+    FQ_CUDA(cudaStreamSynchronize(st));
+    FQ_CUDA(cudaGetLastError());
+    for (int i = 0; i < n; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, M->chain_ev[2 * i], M->chain_ev[2 * i + 1]) == cudaSuccess) {
+        M->prog_ms += ms;
+        M->prog_steps += 1;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    std::memcpy(stats_host, M->chain_ring, sizeof(fq_row_stats) * n);
+    std::memcpy(M->stats_host, M->chain_ring + (n - 1), sizeof(fq_row_stats));
+    M->slot_len[slot] += n;
+  });
+}
+
 fq_status fq_model_tp_shard(const fq_model* M, fq_tp_shard* out) {
   return guarded([&] {
     require(M && out, FQ_E_INPUT, "null argument");
@@ -1568,6 +1637,8 @@ fq_status fq_model_destroy(fq_model* M) {
   return guarded([&] {
     if (!M) return;
     cudaStreamSynchronize(M->ctx->stream);
+    if (M->chain_ring) cudaFreeHost(M->chain_ring);
+    for (auto& e : M->chain_ev) cudaEventDestroy(e);
     for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
     for (auto& kv : M->batch_graphs) cudaGraphExecDestroy(kv.second.first);
@@ -1771,6 +1842,7 @@ fq_status fq_model_set_all_rungs(fq_model* M, int32_t slot, int32_t rung) {
 
 fq_status fq_model_reset_slot(fq_model* M, int32_t slot) {
   return guarded([&] {
+    if (M && M->chain_slot == slot) M->chain_slot = -1;
     require(M != nullptr, FQ_E_INPUT, "null model");
     require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
     M->slot_len[slot] = 0;
@@ -1789,6 +1861,7 @@ fq_status fq_model_prefill(fq_model* M, int32_t slot, const int32_t* tokens, int
                            fq_row_stats* stats_host) {
   return guarded([&] {
     require(M && tokens, FQ_E_INPUT, "null argument");
+    M->chain_slot = -1;  // stats_dev no longer holds a single decode row
     require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     if (n < 1) fail(FQ_E_INPUT, "prefill: empty prompt");
     require(slot >= 0 && slot < M->cfg.max_batch, FQ_E_INPUT, "slot out of range");
@@ -1878,6 +1951,7 @@ fq_status fq_model_profile_step(fq_model* M, int32_t slot, int32_t token, uint64
                                 int32_t* nphases_out, int32_t* grid_out, int32_t* phase_types_host) {
   return guarded([&] {
     require(M && ticks_host && nphases_out && grid_out, FQ_E_INPUT, "null argument");
+    M->chain_slot = -1;  // stats_dev no longer holds a single decode row
     require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(M->llama, FQ_E_CONFIG, "profile_step: llama arch only");
     fq_ctx* ctx = M->ctx;
@@ -1939,6 +2013,7 @@ fq_status fq_model_decode_timed(fq_model* M, int32_t slot, int32_t token, float*
                                 uint64_t* ns_by_rung, uint64_t* ns_step) {
   return guarded([&] {
     require(M && stats_host && ns_by_rung && ns_step, FQ_E_INPUT, "null argument");
+    M->chain_slot = -1;  // stats_dev no longer holds a single decode row
     require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(M->llama, FQ_E_CONFIG, "decode_timed: llama arch only");
     fq_ctx* ctx = M->ctx;
@@ -2023,6 +2098,7 @@ fq_status fq_model_profile_gemvs(fq_model* M, int32_t slot, int32_t reps, double
                                  int64_t* launches_per_pass, int64_t* bytes_per_pass) {
   return guarded([&] {
     require(M && ms_per_launch, FQ_E_INPUT, "null argument");
+    M->chain_slot = -1;  // stats_dev no longer holds a single decode row
     require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(M->llama, FQ_E_CONFIG, "profile_gemvs: llama arch only");
     require(reps >= 1, FQ_E_INPUT, "profile_gemvs: reps must be >= 1");
@@ -2077,6 +2153,7 @@ fq_status fq_model_calibrate_logit_kl(fq_model* M, const int32_t* tokens, int64_
                                       int32_t base_rung, int32_t flip_rung, double* kl_host, double* entropy_host) {
   return guarded([&] {
     require(M && tokens && kl_host, FQ_E_INPUT, "null argument");
+    M->chain_slot = -1;  // stats_dev no longer holds a single decode row
     require(!M->tp(), FQ_E_STATE, "tensor-parallel rank: only fq_model_tp_begin / fq_model_tp_segment run it");
     require(n_seqs >= 1 && len >= 1, FQ_E_INPUT, "calibrate: empty token set");
     require(len <= M->cfg.max_seq_len, FQ_E_CAPACITY, "calibrate: sequence longer than max_seq_len");

@@ -1448,7 +1448,8 @@ FQ_ONCE void run_embed(const Phase& P, float (*sq_red)[kNCW]) {
   // tok_emb null: residual add of an exchanged partial (tensor-parallel step, resid += x[b])
   const bool add = P.tok_emb == nullptr;
   for (int b = 0; b < P.B; ++b) {
-    const float* e = add ? static_cast<const float*>(P.x) + b * P.d : P.tok_emb + static_cast<int64_t>(P.tokens[b]) * P.d;
+    const float* e = add ? static_cast<const float*>(P.x) + b * P.d
+                         : P.tok_emb + static_cast<int64_t>(P.tokens[b * max(1, P.token_stride)]) * P.d;
     float sq = 0.f;
     for (int i = threadIdx.x; i < cnt; i += kNCW * 32) {
       float* rp = P.resid + b * P.resid_stride + c0 + i;

@@ -391,3 +391,34 @@ def test_llama_tensor_core_prefill_is_repeatable(ctx, cfg):
             got.append(out.cpu().numpy())
         assert np.array_equal(got[0], got[2]) and np.array_equal(got[0], got[4]), n
         assert np.array_equal(got[1], got[3]), n
+
+
+@pytest.mark.parametrize("cfg", [LLAMA_TINY, LLAMA_HD128], ids=["hd64", "hd128"])
+def test_llama_decode_chain_matches_host_loop(ctx, cfg):
+    """fq_model_decode_chain (the token fed back on the device from the previous step's argmax)
+    is the host loop decode(argmax) step for step: identical statistics, cache and positions."""
+    a, orc = _llama(ctx, cfg=cfg)
+    b, _ = _llama(ctx, cfg=cfg)
+    rungs = [4 if i % 3 == 1 else 8 for i in range(len(orc.ids))]
+    for m in (a, b):
+        for i, r in enumerate(rungs):
+            m.set_rung(0, i, capi.RUNG_INT8 if r == 8 else capi.RUNG_INT4)
+    prompt = oracle.random_tokens(9, cfg["vocab_size"], 31)
+    ra, rb = a.prefill(0, prompt)[-1], b.prefill(0, prompt)[-1]
+    with pytest.raises(capi.StateError):
+        b.decode_chain(0, 4)  # a prefill row is not a decode row
+    host = []
+    for _ in range(14):
+        ra = a.decode([0], [int(ra["argmax"])])[0]
+        host.append(ra)
+    rb = b.decode([0], [int(rb["argmax"])])[0]
+    chained = [rb] + list(b.decode_chain(0, 6)) + list(b.decode_chain(0, 7))
+    assert a.slot_length(0) == b.slot_length(0) == len(prompt) + 14
+    for x, y in zip(host, chained):
+        assert x["argmax"] == y["argmax"] and x["entropy"] == y["entropy"] and x["p1"] == y["p1"]
+    # the chain continues seamlessly into host-fed steps
+    ra = a.decode([0], [int(host[-1]["argmax"])])[0]
+    rb = b.decode([0], [int(chained[-1]["argmax"])])[0]
+    assert ra["entropy"] == rb["entropy"]
+    a.close()
+    b.close()
