@@ -353,8 +353,10 @@ struct fq_model {
   // chained decode (fq_model_decode_chain): the slot whose single-row decode step ran last (its
   // argmax is stats_dev[0]), -1 when another step / prefill ran since; pinned stats ring, events
   int chain_slot = -1;
-  fq_row_stats* chain_ring = nullptr;
-  std::vector<cudaEvent_t> chain_ev;
+  fq_row_stats* chain_ring = nullptr;      // pinned [kMaxChain]
+  fq_row_stats* chain_ring_dev = nullptr;  // [kMaxChain], filled by the chained steps in order
+  unsigned int* chain_count = nullptr;     // device write index into chain_ring_dev
+  cudaGraphExec_t chain_graph = nullptr;   // one chained step: advance pos | step program | collect
 
   int lin_index(int layer, int j) const { return layer * (llama ? 7 : 6) + j; }
   int head_index() const { return static_cast<int>(cfg.n_layers) * (llama ? 7 : 6); }
@@ -419,6 +421,11 @@ void sync_weight_epoch(fq_model* M) {
     M->batch_graphs.clear();
     M->batch_seen.clear();
     M->timed_roles.clear();
+  }
+  if (M->chain_graph) {
+    FQ_CUDA(cudaStreamSynchronize(M->ctx->stream));
+    cudaGraphExecDestroy(M->chain_graph);
+    M->chain_graph = nullptr;
   }
   M->built_epoch = M->ctx->weight_epoch;
 }
@@ -1316,6 +1323,10 @@ ProgramRun& tp_program(fq_model* M, int B, int seg, const float* reduced, void* 
 }
 
 __global__ void advance_pos_kernel(int32_t* pos) { pos[0] += 1; }
+__global__ void collect_stats_kernel(const fq_row_stats* stats, fq_row_stats* ring, unsigned int* count) {
+  ring[*count] = stats[0];
+  *count += 1;
+}
 
 float* param_slot(fq_model* M, const std::string& name, int64_t& expect) {
   const fq_model_config& c = M->cfg;
@@ -1544,37 +1555,56 @@ fq_status fq_model_decode_chain(fq_model* M, int32_t slot, int32_t n, fq_row_sta
     sync_weight_epoch(M);
     if (M->chain_ring == nullptr) {
       FQ_CUDA(cudaMallocHost(&M->chain_ring, sizeof(fq_row_stats) * kMaxChain));
-      M->chain_ev.resize(2 * kMaxChain);
-      for (auto& e : M->chain_ev) FQ_CUDA(cudaEventCreate(&e));
+      M->chain_ring_dev = static_cast<fq_row_stats*>(dmalloc(sizeof(fq_row_stats) * kMaxChain));
+      M->chain_count = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int)));
     }
-    // the step's rows: this slot at its next position with its current precision row; the token
-    // slot of the staging is unused (the embedding reads the previous step's argmax on the device)
+    // rows of the step: this slot with its current precision row, staged one position back --
+    // every chained step first advances the position on the device; the token slot of the
+    // staging is unused (the embedding reads the previous step's argmax on the device)
     const int32_t tok0 = M->stats_host[0].argmax;
     stage_rows(M, 1, &slot, &tok0);
+    reinterpret_cast<int32_t*>(M->meta_host)[M->rows] -= 1;
     FQ_CUDA(cudaMemcpyAsync(M->meta_dev, M->meta_host, M->meta_bytes, cudaMemcpyHostToDevice, st));
+    FQ_CUDA(cudaMemsetAsync(M->chain_count, 0, sizeof(unsigned int), st));
     int32_t* pos_dev = reinterpret_cast<int32_t*>(M->meta_dev) + M->rows;
-    for (int i = 0; i < n; ++i) {
-      if (i > 0) {
-        advance_pos_kernel<<<1, 1, 0, st>>>(pos_dev);
-        launch_dev(M);
-      }
-      FQ_CUDA(cudaEventRecord(M->chain_ev[2 * i], st));
+    auto one_step = [&]() {
+      advance_pos_kernel<<<1, 1, 0, st>>>(pos_dev);
       enqueue_step(M, 1, STEP_CHAIN);
-      FQ_CUDA(cudaEventRecord(M->chain_ev[2 * i + 1], st));
-      launch_dev(M);
-      FQ_CUDA(cudaMemcpyAsync(M->chain_ring + i, M->stats_dev, sizeof(fq_row_stats), cudaMemcpyDeviceToHost, st));
+      collect_stats_kernel<<<1, 1, 0, st>>>(M->stats_dev, M->chain_ring_dev, M->chain_count);
+      ctx->launches += 2;
+    };
+    int i = 0;
+    if (M->chain_graph == nullptr) {
+      one_step();  // builds the chained-step program on first use, then captures one step
+      FQ_CUDA(cudaGetLastError());
+      ++i;
+      if (M->use_graphs) {
+        cudaGraph_t graph;
+        const int64_t l0 = ctx->launches;
+        FQ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+          one_step();
+        } catch (...) {
+          cudaStreamEndCapture(st, &graph);
+          throw;
+        }
+        FQ_CUDA(cudaStreamEndCapture(st, &graph));
+        FQ_CUDA(cudaGraphInstantiate(&M->chain_graph, graph, 0));
+        FQ_CUDA(cudaGraphDestroy(graph));
+        ctx->launches = l0;
+      }
     }
+    for (; i < n; ++i) {
+      if (M->chain_graph) {
+        FQ_CUDA(cudaGraphLaunch(M->chain_graph, st));
+        ctx->launches += 3;
+      } else {
+        one_step();
+      }
+    }
+    FQ_CUDA(cudaMemcpyAsync(M->chain_ring, M->chain_ring_dev, sizeof(fq_row_stats) * n, cudaMemcpyDeviceToHost, st));
     FQ_CUDA(cudaStreamSynchronize(st));
     FQ_CUDA(cudaGetLastError());
-    for (int i = 0; i < n; ++i) {
-      float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, M->chain_ev[2 * i], M->chain_ev[2 * i + 1]) == cudaSuccess) {
-        M->prog_ms += ms;
-        M->prog_steps += 1;
-      } else {
-        cudaGetLastError();
-      }
-    }
     std::memcpy(stats_host, M->chain_ring, sizeof(fq_row_stats) * n);
     std::memcpy(M->stats_host, M->chain_ring + (n - 1), sizeof(fq_row_stats));
     M->slot_len[slot] += n;
@@ -1638,7 +1668,9 @@ fq_status fq_model_destroy(fq_model* M) {
     if (!M) return;
     cudaStreamSynchronize(M->ctx->stream);
     if (M->chain_ring) cudaFreeHost(M->chain_ring);
-    for (auto& e : M->chain_ev) cudaEventDestroy(e);
+    dfree(M->chain_ring_dev);
+    dfree(M->chain_count);
+    if (M->chain_graph) cudaGraphExecDestroy(M->chain_graph);
     for (auto& kv : M->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : M->programs) dfree(kv.second.dev_phases);
     for (auto& kv : M->batch_graphs) cudaGraphExecDestroy(kv.second.first);
