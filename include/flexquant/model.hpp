@@ -174,6 +174,9 @@ class Model {
   // Lower-level batched step used by the engine: one decode step for `slots`, per-row
   // statistics only (no logits copy).  Returns the rows' statistics.
   std::vector<fq_row_stats> decode_rows(std::span<const int32_t> slots, std::span<const TokenId> tokens);
+  // n decode steps of `slot` fed on the device with the previous argmax (fq_model_decode_chain);
+  // step_stats() then holds ONE step's accounting (the chain's time split evenly)
+  std::vector<fq_row_stats> decode_chain_rows(int slot, int n);
   // Single-row llama decode steps with the device phase clock on: step_stats() then carries the
   // per-precision linear time and the step's device time measured on the device
   // (fq_model_decode_timed) instead of the step time split by bytes.

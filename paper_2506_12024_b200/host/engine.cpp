@@ -6,7 +6,9 @@
 // without nlohmann/json.  Record semantics are the reference's:
 // a token's record describes the precision state that produced it; switches decided at token t
 // are applied after its record and take effect for token t+1; token 1 covers the prefill.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <deque>
@@ -110,7 +112,53 @@ std::vector<GenerationResult> run_generation(std::span<const std::vector<TokenId
     s.result.threshold = thre;
     s.row = st.back();
   }
+  // one Llama sequence without eos: tokens whose scheduler decision provably cannot switch (the
+  // window still filling or the cooldown running, SchedulerState::safe_observes) are decoded as
+  // one device-chained block (Model::decode_chain_rows: the token fed back from the previous
+  // argmax on the device); their records are written afterwards from the block's rows, in the
+  // same order and with the same fields as the token-by-token loop (the block's wall time split
+  // evenly over its tokens)
+  const bool chainable = seqs.size() == 1 && mc.arch == Arch::Llama && forced_speed == 0 && !cfg.eos_token &&
+                         !cfg.device_timed_buckets && std::getenv("FQ_NO_CHAIN") == nullptr;
   for (int64_t t = 1;; ++t) {
+    if (chainable && t >= 2 && !seqs[0].done) {  // t = 1's row comes from the prefill
+      Seq& s = seqs[0];
+      int64_t len = 0;
+      detail::check(fq_model_slot_length(model.handle(), s.slot, &len));
+      const int64_t k = std::min<int64_t>({static_cast<int64_t>(std::min<size_t>(s.sched.safe_observes(), 64)),
+                                           cfg.max_new_tokens - t, mc.max_seq_len - len});
+      if (k >= 2) {
+        const uint64_t c0 = now_ns();
+        model.reset_step_stats();
+        const std::vector<fq_row_stats> rows = model.decode_chain_rows(s.slot, static_cast<int>(k));
+        const uint64_t per = (now_ns() - c0) / static_cast<uint64_t>(k);
+        const StepStats chained = model.step_stats();
+        fq_row_stats prev = s.row;
+        for (int64_t j = 0; j < k; ++j) {
+          TraceRecord rec;
+          rec.token_index = t + j;
+          rec.token_id = prev.argmax;
+          rec.fault_tolerance = prev.fault_tolerance;
+          rec.effective_bits = model.effective_bits(s.slot);
+          rec.buckets = j == 0 ? s.step_stats : chained;
+          rec.weight_bytes_touched = rec.buckets.weight_bytes;
+          rec.ppl_entropy = prev.ppl_entropy;
+          const SchedulerState::Decision d = s.sched.observe(rec.ppl_entropy);
+          if (d.count != 0) throw StateError("generate: a chained token switched precision");
+          rec.moving_average = d.window_mean;
+          rec.elapsed_ns = j == 0 ? now_ns() - s.step_start : per;
+          s.result.trace.records.push_back(std::move(rec));
+          s.result.sequence.push_back(prev.argmax);
+          prev = rows[static_cast<size_t>(j)];
+        }
+        s.row = prev;
+        s.step_start = now_ns() - per;
+        s.step_stats = chained;
+        s.step_stats.weight_bytes = model.weight_bytes_per_pass(s.slot);
+        t += k - 1;
+        continue;
+      }
+    }
     std::vector<int32_t> slots;
     std::vector<TokenId> toks;
     for (Seq& s : seqs) {

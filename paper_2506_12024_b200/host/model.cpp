@@ -344,6 +344,14 @@ std::vector<fq_row_stats> Model::decode_rows(std::span<const int32_t> slots, std
   return st;
 }
 
+std::vector<fq_row_stats> Model::decode_chain_rows(int slot, int n) {
+  std::vector<fq_row_stats> st(static_cast<size_t>(n));
+  const uint64_t t0 = now_ns();
+  detail::check(fq_model_decode_chain(model_, slot, n, st.data()));
+  account_step((now_ns() - t0) / static_cast<uint64_t>(n), slot);
+  return st;
+}
+
 Tensor Model::forward_prefill(std::span<const TokenId> tokens, KvCache& cache) const {
   const int64_t n = static_cast<int64_t>(tokens.size());
   if (n < 1) throw InputError("prefill: empty prompt");
