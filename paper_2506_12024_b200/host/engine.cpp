@@ -129,6 +129,7 @@ std::vector<GenerationResult> run_generation(std::span<const std::vector<TokenId
                                            cfg.max_new_tokens - t, mc.max_seq_len - len});
       if (k >= 2) {
         const uint64_t c0 = now_ns();
+        const uint64_t first_elapsed = c0 - s.step_start;  // token t came from the step before the block
         model.reset_step_stats();
         const std::vector<fq_row_stats> rows = model.decode_chain_rows(s.slot, static_cast<int>(k));
         const uint64_t per = (now_ns() - c0) / static_cast<uint64_t>(k);
@@ -146,7 +147,7 @@ std::vector<GenerationResult> run_generation(std::span<const std::vector<TokenId
           const SchedulerState::Decision d = s.sched.observe(rec.ppl_entropy);
           if (d.count != 0) throw StateError("generate: a chained token switched precision");
           rec.moving_average = d.window_mean;
-          rec.elapsed_ns = j == 0 ? now_ns() - s.step_start : per;
+          rec.elapsed_ns = j == 0 ? first_elapsed : per;
           s.result.trace.records.push_back(std::move(rec));
           s.result.sequence.push_back(prev.argmax);
           prev = rows[static_cast<size_t>(j)];
