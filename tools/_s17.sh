@@ -1,3 +1,4 @@
-timeout 900 python -m pytest tests/test_host_api.py tests/test_ref_suites.py tests/test_llama_schedule_gpu.py tests/test_model_gpu.py tests/test_c3_shape_gpu.py -m "gpu or not gpu" -q > gpurun_out/r03n_tests.log 2>&1; tail -3 gpurun_out/r03n_tests.log; grep -E "^FAILED|Error" gpurun_out/r03n_tests.log | head -5
-for i in 1 2; do timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/r03n_bench_$i.json 2>gpurun_out/r03n_bench_$i.err; tail -1 gpurun_out/r03n_bench_$i.err; python -c "
-import json; d=json.loads(open('gpurun_out/r03n_bench_$i.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['e2e']['trace'], d['e2e']['note'][-18:])"; done
+for i in 1 2; do timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/r03o_bench_$i.json 2>gpurun_out/r03o_bench_$i.err; tail -1 gpurun_out/r03o_bench_$i.err; python -c "
+import json; d=json.loads(open('gpurun_out/r03o_bench_$i.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['e2e']['trace'], d['e2e']['note'][-18:], d['gpu_launches'])"; done
+timeout 600 python bench.py > gpurun_out/r03o_bench200.json 2>gpurun_out/r03o_bench200.err; python -c "
+import json; d=json.loads(open('gpurun_out/r03o_bench200.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['e2e']['trace'])"
