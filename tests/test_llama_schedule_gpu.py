@@ -186,3 +186,31 @@ def test_llama_infinite_threshold_cadence():
     assert r.trace.records[-1].effective_bits == 4.0
     done = [e.layer_id for rec in r.trace.records for e in rec.switch_events]
     assert done == [e.layer_id for e in plan.entries]
+
+
+def test_generate_chained_blocks_match_token_loop(monkeypatch):
+    """flexquant::generate decodes the tokens whose scheduler decision cannot switch as device-
+    chained blocks; the trace is the token-by-token loop's (FQ_NO_CHAIN=1) field for field."""
+    orc = oracle.llama.LlamaOracle(dict(C1, group_size=128), seed=0, std=0.1, act="fp16")
+    m = _model(orc, fp16=True)
+    plan = _plan(orc)
+    cfg = fq.GenerationConfig()
+    cfg.max_new_tokens = 60
+    cfg.start_rung = fq.Rung.Int8
+    cfg.scheduler.threshold_mode = fq.ThresholdMode.Prefill
+    cfg.scheduler.theta = 1.02
+    cfg.scheduler.window_len = 8
+    cfg.scheduler.layers_per_switch = 4
+    prompt = oracle.random_tokens(PROMPT, C1["vocab_size"], 77)
+    runs = []
+    for chain in (True, False):
+        if chain:
+            monkeypatch.delenv("FQ_NO_CHAIN", raising=False)
+        else:
+            monkeypatch.setenv("FQ_NO_CHAIN", "1")
+        r = fq.generate(prompt, m, plan, cfg)
+        runs.append([(x.token_index, x.token_id, x.ppl_entropy, x.fault_tolerance, x.moving_average, x.effective_bits,
+                       x.weight_bytes_touched, [e.layer_id for e in x.switch_events]) for x in r.trace.records])
+    assert len(runs[0]) == cfg.max_new_tokens
+    assert sum(1 for x in runs[0] if x[7]) >= 2  # switches happen between the chained blocks
+    assert runs[0] == runs[1]
