@@ -296,7 +296,6 @@ struct fq_model {
   void* v = nullptr;
   void* attn = nullptr;        // [B, d]
   void* mid = nullptr;         // [B, ffn]
-  unsigned int* tile_flags = nullptr;  // [d/16] QKV tile stamps (FQ_HEAD_FLAGS)
   void* attn_frag = nullptr;   // [B][d/128][16] uint4: attention output in B-fragment order (fp16)
   void* mid_frag = nullptr;    // [B][ffn/128][16] uint4: SwiGLU output in B-fragment order
   float* tmp = nullptr;        // [B, max(d, ffn)] fp32 (reference)
@@ -477,7 +476,6 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
       // (measured alternatives to the grid barriers -- tagged activation words, per-head QKV tile
       // flags, attention split over CTAs with the O staging merging the partials -- were all
       // slower at the 7B shape and are not built: DESIGN.md §4)
-      const bool tagged = false, head_flags = false;
       const int frag_nkb_d = static_cast<int>((d + kBlockK - 1) / kBlockK);
       const int attn_splits = 1;
       for (int64_t l = 0; l < c.n_layers; ++l) {
@@ -504,10 +502,6 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         g.y_dtype = c.act_dtype;
         g.y_stride = d;
         add_chunked(pb, g, B);
-        if (head_flags) {
-          pb.phases.back().tile_flags = M->tile_flags;
-          pb.phases.back().barrier_after = 0;
-        }
         if (prefill) {
           Phase ap{};
           ap.type = PH_APPEND;
@@ -549,11 +543,9 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
           a.attn_ws = M->attn_ws;
           a.attn_out = M->attn;
           a.attn_splits = attn_splits;
-          if (head_flags) a.tile_flags = M->tile_flags;
           if (use_frag && attn_splits == 1) {
             a.yfrag = static_cast<__half*>(M->attn_frag);
-            a.yfrag_nkb = tagged ? -frag_nkb_d : frag_nkb_d;
-            if (tagged) a.barrier_after = 0;
+            a.yfrag_nkb = frag_nkb_d;
           }
           pb.add(a);
         }
@@ -573,7 +565,6 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         o.out_n_partials = kPartStride;
         const size_t o_first = pb.phases.size();
         add_chunked(pb, o, B);
-        if (tagged && attn_splits == 1 && !gemv_only) pb.phases.back().xfrag_tagged = 1;
         if (attn_splits > 1) {
           if (pb.phases.size() != o_first + 1) fail(FQ_E_STATE, "split attention needs one O-projection phase");
           Phase& op = pb.phases.back();
@@ -605,10 +596,6 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         gu.y_dtype = c.act_dtype;
         gu.y_stride = c.ffn_dim;
         add_chunked(pb, gu, B);
-        if (tagged) {
-          pb.phases.back().yfrag_nkb = -pb.phases.back().yfrag_nkb;
-          pb.phases.back().barrier_after = 0;
-        }
         GemvLaunch dn;
         dn.nmat = 1;
         dn.mat[0].layer = M->lin[M->lin_index(static_cast<int>(l), 6)];
@@ -624,7 +611,6 @@ void enqueue_step(fq_model* M, int B, int mode = STEP_DECODE) {
         dn.out_partials = M->partials[cur ^ 1];
         dn.out_n_partials = kPartStride;
         add_chunked(pb, dn, B);
-        if (tagged) pb.phases.back().xfrag_tagged = 1;
         cur ^= 1;
       }
       GemvLaunch hd;
@@ -1491,9 +1477,6 @@ fq_status fq_model_create_tp(fq_ctx* ctx, const fq_model_config* cfg, int32_t tp
     M->mid = dmalloc(as * B * ffn);
     {
       const int64_t fd = (d + kBlockK - 1) / kBlockK * kBlockK, ff = (ffn + kBlockK - 1) / kBlockK * kBlockK;
-      // room for the tagged form: one 8-byte (half2, tag) word per activation pair
-      M->tile_flags = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * ((d + 15) / 16)));
-      FQ_CUDA(cudaMemsetAsync(M->tile_flags, 0, sizeof(unsigned int) * ((d + 15) / 16), st));
       M->attn_frag = dmalloc(4 * B * fd);
       M->mid_frag = dmalloc(4 * B * ff);
       FQ_CUDA(cudaMemsetAsync(M->attn_frag, 0, 4 * B * fd, st));  // padding past K stays zero
@@ -1699,7 +1682,6 @@ fq_status fq_model_destroy(fq_model* M) {
     dfree(M->v);
     dfree(M->attn);
     dfree(M->mid);
-    dfree(M->tile_flags);
     dfree(M->attn_frag);
     dfree(M->mid_frag);
     dfree(M->tmp);
